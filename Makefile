@@ -1,0 +1,39 @@
+# Build of libswb200.so (sm_100a only) and the C oracle helpers.
+#   make            -> paper_2311_18677_b200/libswb200.so + oracle/_build/liboracle.so
+#   make sass       -> dump SASS of the library (proof of UTCHMMA / UTMALDG)
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr \
+           -Xptxas -v
+SRC := paper_2311_18677_b200/csrc
+OBJDIR := build/obj
+CU := $(wildcard $(SRC)/*.cu)
+CPP := $(wildcard $(SRC)/*.cpp)
+OBJ := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU)) $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.o,$(CPP))
+LIB := paper_2311_18677_b200/libswb200.so
+
+all: $(LIB) oracle
+
+$(OBJDIR)/%.o: $(SRC)/%.cu $(SRC)/common.cuh include/swb200.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.txt || (cat $(OBJDIR)/$*.ptxas.txt; false)
+
+$(OBJDIR)/%.o: $(SRC)/%.cpp include/swb200.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) -O3 -std=c++17 -Xcompiler -fPIC -c $< -o $@
+
+$(LIB): $(OBJ)
+	$(NVCC) -shared $(ARCH) -o $@ $(OBJ) -cudart static
+
+oracle:
+	$(MAKE) -C oracle
+
+sass: $(LIB)
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libswb200.sass
+	@grep -c UTCHMMA build/libswb200.sass || true
+	@grep -c UTMALDG build/libswb200.sass || true
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean sass oracle

@@ -1,0 +1,213 @@
+/*
+ * swb200.h — C-ABI of libswb200.so, the B200-native hot path of Splitwise
+ * (arXiv 2311.18677): prompt-phase prefill, layer-wise KV push into a token
+ * machine's paged KV blocks, and token-phase decode.
+ *
+ * The reference (`splitsim`, /root/reference/pkg) models this path with
+ * latency lookups; every entry point below replaces one of those lookups (or
+ * the byte accounting behind it) with real GPU work.  The reference-side
+ * interface each one replaces is cited as file:line relative to
+ * /root/reference/pkg/src/splitsim/.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch types.  Device pointers are
+ *    passed as `void*`/typed pointers; CUDA streams as `uintptr_t`
+ *    (a cudaStream_t value, 0 = legacy default stream).
+ *  - Every function returns an int status.  The Python host maps them onto
+ *    the reference exception hierarchy (errors.py:4-31):
+ *        SWB_ERR_INVALID  -> ValidationError     (errors.py:8)
+ *        SWB_ERR_CAPACITY -> CapacityError       (errors.py:26)
+ *        SWB_ERR_CONFIG   -> ConfigurationError  (errors.py:30)
+ *        SWB_ERR_CUDA     -> RuntimeError (text from swb_last_error()).
+ *  - All compute calls are asynchronous and stream ordered; none blocks the
+ *    host except swb_sync_stream.  The library never allocates or frees
+ *    caller memory, except the KV pools it creates (swb_kv_pool_create /
+ *    swb_kv_pool_destroy).
+ *  - Element types: activations/weights bf16, residual stream fp32,
+ *    accumulation fp32, token ids / slots / block ids int32.
+ */
+#ifndef SWB200_H_
+#define SWB200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWB_OK 0
+#define SWB_ERR_INVALID 1
+#define SWB_ERR_CAPACITY 2
+#define SWB_ERR_CUDA 3
+#define SWB_ERR_CONFIG 4
+
+#define SWB_ABI_VERSION 1
+
+/* ---------------------------------------------------------------- meta */
+int swb_abi_version(void);
+/* Text of the last error raised on the calling host thread ("" if none). */
+const char* swb_last_error(void);
+/* Blocks the host until `stream` drains (the only blocking call). */
+int swb_sync_stream(uintptr_t stream);
+
+/* ------------------------------------------------------- dense GEMM (prefill)
+ * out[M,N] = epilogue(A[M,K] . W[N,K]^T), bf16 operands, fp32 accumulate in
+ * TMEM (tcgen05.mma, TMA-fed 128B-swizzled smem ring).  Replaces the prompt
+ * cost lookup PerfModel.prompt_time (perf.py:119-123) for the linear layers.
+ *   epilogue SWB_EPI_BF16     : out bf16 [M,N]
+ *   epilogue SWB_EPI_F32      : out fp32 [M,N]
+ *   epilogue SWB_EPI_RESID_F32: out fp32 [M,N] = resid fp32 [M,N] + acc
+ *                               (out may alias resid)
+ *   epilogue SWB_EPI_SWIGLU   : W rows are gate/up interleaved in 128-row
+ *                               groups; out bf16 [M,N/2] = silu(gate)*up
+ * Requirements: K % 8 == 0 (TMA row pitch), N % 16 == 0, pointers 16B aligned.
+ */
+#define SWB_EPI_BF16 0
+#define SWB_EPI_F32 1
+#define SWB_EPI_RESID_F32 2
+#define SWB_EPI_SWIGLU 3
+int swb_gemm_bf16(const void* a, const void* w, void* out, const void* resid,
+                  int M, int N, int K, int epilogue, uintptr_t stream);
+
+/* --------------------------------------------- skinny GEMM / GEMV (decode)
+ * Same contract as swb_gemm_bf16 for small M (decode batch, 1..16 rows):
+ * weight-streaming kernel, 128-bit coalesced weight loads, fp32 accumulate.
+ * Replaces the decode cost lookup PerfModel.token_iter_time (perf.py:125-132)
+ * for the linear layers.
+ */
+int swb_gemv_bf16(const void* x, const void* w, void* out, const void* resid,
+                  int M, int N, int K, int epilogue, uintptr_t stream);
+
+/* ------------------------------------------------------- elementwise ops */
+/* x fp32 [rows,d] <- table bf16 [V,d][tokens[r]] */
+int swb_embed(const int32_t* tokens, const void* table, float* x, int rows,
+              int d, uintptr_t stream);
+/* out bf16 [rows,d] = rmsnorm(x fp32 [src_rows,d]) * w; row_index (may be
+ * NULL) selects src rows (e.g. the last token of each prompt). */
+int swb_rmsnorm(const float* x, const int32_t* row_index, const void* w,
+                void* out, int rows, int d, float eps, uintptr_t stream);
+/* Greedy sampling: out[r] = argmax_v logits fp32 [rows,V] (lowest index on
+ * ties). */
+int swb_argmax(const float* logits, int rows, int V, int32_t* out,
+               uintptr_t stream);
+
+/* -------------------------------------------- RoPE + KV write into blocks
+ * qkv bf16 [rows, row_stride] holds q (H heads), k (Hkv), v (Hkv) at column
+ * offsets 0, H*dh, (H+Hkv)*dh.  Rotates q and k in place (NeoX half split,
+ * theta) at positions[r], and, when k_layer/v_layer are non-NULL, writes the
+ * rotated k and v of row r into paged slot slots[r] of the layer's block
+ * pool (layout [block][Hkv][block_size][dh]).  The KV bytes it writes are
+ * what PerfModel.kv_cache_bytes (perf.py:134-137) counts.
+ */
+int swb_rope_kv_write(void* qkv, int rows, int row_stride, const int32_t* positions,
+                      int H, int Hkv, int dh, float theta, void* k_layer,
+                      void* v_layer, const int32_t* slots, int block_size,
+                      uintptr_t stream);
+
+/* ------------------------------------------------ KV pack-and-push (a5)
+ * Copies rows' k/v (already rotated, in qkv layout as above) into the paged
+ * blocks of a destination pool that may live on a peer GPU (P2P stores over
+ * NVLink through an IPC-mapped pointer).  `num_ctas` bounds the SMs the push
+ * borrows from concurrent prefill compute (0 = auto).  Replaces
+ * transfer.plan_transfer / raw_transfer_time (transfer.py:66-99): the bytes
+ * are moved instead of priced.
+ */
+int swb_kv_push_layer(const void* qkv, int rows, int row_stride, int k_col,
+                      int v_col, int Hkv, int dh, void* dst_k_layer,
+                      void* dst_v_layer, const int32_t* dst_slots,
+                      int block_size, int num_ctas, uintptr_t stream);
+/* Completion flag of a push (the paper's per-request semaphore,
+ * PAPER.md:804): system-scope release store of `value` to `flag` (which may
+ * be peer memory) after all prior work on `stream`. */
+int swb_kv_signal(uint32_t* flag, uint32_t value, uintptr_t stream);
+/* Stream-ordered wait until *flag >= value (cuStreamWaitValue32 GEQ). */
+int swb_stream_wait_flag(uint32_t* flag, uint32_t value, uintptr_t stream);
+
+/* ---------------------------------------------------- attention kernels */
+/* Causal varlen prefill attention with GQA over qkv rows; sequences are
+ * delimited by cu_seqlens[num_seqs+1]; out bf16 [rows, H*dh]. dh == 128. */
+int swb_attn_prefill(const void* qkv, int row_stride, const int32_t* cu_seqlens,
+                     int num_seqs, int max_seqlen, int H, int Hkv, int dh,
+                     float scale, void* out, uintptr_t stream);
+/* Paged decode attention: q from qkv rows [B, row_stride] (column 0), keys /
+ * values from the layer pool through block_tables [B, max_blocks] and
+ * ctx_lens[B] (tokens to attend, including the current one).  Split over
+ * context partitions of `partition` tokens with an fp32 merge; workspace
+ * must hold swb_attn_decode_workspace(B, H, max_ctx, partition, dh) bytes.
+ */
+size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int partition,
+                                 int dh);
+int swb_attn_decode(const void* qkv, int row_stride, const void* k_layer,
+                    const void* v_layer, const int32_t* block_tables,
+                    int max_blocks, const int32_t* ctx_lens, int B, int H,
+                    int Hkv, int dh, int block_size, float scale, int max_ctx,
+                    int partition, void* workspace, void* out,
+                    uintptr_t stream);
+
+/* --------------------------------------------- decode-step bookkeeping
+ * Graph-resident per-step state update so the decode loop needs no host
+ * round trip (Machine.complete_iteration, machine.py:247-275):
+ *  prepare: pos[b] = ctx[b]; slot[b] = table[b][ctx/bs]*bs + ctx%bs;
+ *           attn_len[b] = ctx[b] + 1
+ *  advance: cur_tok[b] = next_tok[b]; out_ring[b*ring + step[b]] = next_tok[b];
+ *           step[b] += 1; ctx[b] += 1
+ */
+int swb_decode_prepare(const int32_t* ctx, const int32_t* block_tables,
+                       int max_blocks, int block_size, int B, int32_t* pos,
+                       int32_t* slots, int32_t* attn_len, uintptr_t stream);
+int swb_decode_advance(const int32_t* next_tok, int32_t* cur_tok, int32_t* ctx,
+                       int32_t* step, int32_t* out_ring, int ring, int B,
+                       uintptr_t stream);
+/* slots[i] = table_row[(start+i)/bs]*bs + (start+i)%bs for i < n (table_row
+ * may be peer memory: the prompt side reads the token side's table). */
+int swb_slots_from_table(const int32_t* table_row, int start, int n,
+                         int block_size, int32_t* slots, uintptr_t stream);
+
+/* ----------------------------------------------- KV block pool (a3/a4)
+ * Device-resident pool: per layer K and V arrays [num_blocks][Hkv][bs][dh]
+ * bf16, block tables int32 [max_seqs][max_blocks_per_seq], and a free-block
+ * bitmap.  Allocation is lowest-free-first, done by a device kernel that
+ * writes the sequence's block-table row; the host keeps only the free count
+ * (admission = Machine._memory_fits, machine.py:125-128).  Replaces the
+ * byte-count memory model (perf.py:134-141, machine.py:107-128).
+ */
+typedef struct swb_kv_pool swb_kv_pool;
+typedef struct {
+  void* k_base;               /* layer l K = k_base + l*layer_stride bytes */
+  void* v_base;
+  size_t layer_stride_bytes;
+  size_t block_bytes;         /* one block of one layer, K or V */
+  int32_t* block_tables;      /* [max_seqs][max_blocks_per_seq] */
+  uint32_t* bitmap;           /* 1 bit per block, 1 = in use */
+  int num_layers, num_blocks, Hkv, block_size, dh, max_seqs,
+      max_blocks_per_seq;
+  int free_blocks;            /* host mirror */
+  int is_peer_view;           /* opened through IPC, not owned */
+} swb_kv_pool_info;
+
+int swb_kv_pool_create(int num_layers, int num_blocks, int Hkv, int block_size,
+                       int dh, int max_seqs, int max_blocks_per_seq,
+                       swb_kv_pool** out);
+int swb_kv_pool_destroy(swb_kv_pool* pool);
+int swb_kv_pool_get_info(const swb_kv_pool* pool, swb_kv_pool_info* out);
+/* Reserve n blocks for sequence slot `seq` (lowest free first), writing its
+ * block-table row; SWB_ERR_CAPACITY if fewer than n blocks are free. */
+int swb_block_alloc(swb_kv_pool* pool, int seq, int n_blocks, uintptr_t stream);
+/* Release the first n blocks of seq's row back to the pool. */
+int swb_block_free(swb_kv_pool* pool, int seq, int n_blocks, uintptr_t stream);
+/* IPC: SWB_KV_POOL_IPC_BYTES-byte handle of the pool (KV arrays + block
+ * tables) for a peer process; the peer opens a non-owning view it can push
+ * into and whose block tables it can read. */
+#define SWB_KV_POOL_IPC_BYTES 256
+int swb_kv_pool_ipc_export(const swb_kv_pool* pool, void* handle_out,
+                           size_t handle_bytes);
+int swb_kv_pool_ipc_open(const void* handle, size_t handle_bytes,
+                         swb_kv_pool** out);
+/* Enable direct peer access between the current device and `peer`. */
+int swb_enable_peer(int peer_device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWB200_H_ */

@@ -1,0 +1,472 @@
+// Attention kernels of the hot path.
+//
+// (1) attn_prefill: causal, varlen (several prompts packed back to back,
+//     delimited by cu_seqlens), GQA.  FlashAttention-2 style online softmax:
+//     one CTA = 64 query rows x one head, 4 warps x 16 rows, K/V tiles of 64
+//     keys double-buffered in XOR-swizzled smem through cp.async, bf16
+//     m16n8k16 tensor-core MMAs with P kept in registers.  (At the BASELINE
+//     prompt lengths attention is 2-4 % of prefill FLOPs; the linear layers
+//     run on tcgen05, see gemm.cu.)
+// (2) attn_decode: paged decode attention over the KV block pool.  One CTA
+//     per (sequence, kv head, context partition); the G = H/Hkv query heads
+//     of a GQA group share one pass over the K/V blocks, which are streamed
+//     with 16-byte coalesced loads (a (block, head) tile is 4 KB contiguous).
+//     Scores live in smem, softmax uses warp-shuffle reductions, partitions
+//     are merged in fp32 by a second kernel (split-K over the context).
+//
+// These replace the attention share of the reference's latency lookups
+// (perf.py:119-132); the reference has no attention arithmetic at all.
+#include "common.cuh"
+
+namespace swb {
+
+// ============================================================ prefill
+constexpr int PA_BQ = 64, PA_BK = 64, PA_D = 128;
+constexpr int PA_ROW_BYTES = PA_D * 2;              // 256 B
+constexpr int PA_TILE_BYTES = PA_BQ * PA_ROW_BYTES;  // 16 KB
+constexpr int PA_SMEM = PA_TILE_BYTES * 5;           // Q + 2xK + 2xV
+
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return row * PA_ROW_BYTES + ((chunk ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1,
+                                        uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1,
+                                          uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4],
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// load a 64-row x 128-col bf16 tile (rows [r0, r0+64) of a strided matrix,
+// rows >= rmax zero-filled) into swizzled smem
+__device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* g,
+                                          int stride, int r0, int rmax) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int idx = threadIdx.x + i * 128;  // 0..1023
+    const int row = idx >> 4, chunk = idx & 15;
+    const bool valid = r0 + row < rmax;
+    const __nv_bfloat16* src = g + (size_t)(valid ? r0 + row : 0) * stride + chunk * 8;
+    cp_async16(sbase + swz(row, chunk), src, valid);
+  }
+}
+
+__global__ void __launch_bounds__(128)
+    attn_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
+                        const int32_t* __restrict__ cu, int tiles_per_seq, int H,
+                        int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int seq = blockIdx.x / tiles_per_seq;
+  // heavy (late) tiles first
+  const int qt = tiles_per_seq - 1 - (blockIdx.x % tiles_per_seq);
+  const int h = blockIdx.y;
+  const int kh = h / (H / Hkv);
+  const int s0 = cu[seq], len = cu[seq + 1] - s0;
+  const int q0 = qt * PA_BQ;
+  if (q0 >= len) return;
+
+  const uint32_t sQ = smem_u32(sm);
+  const uint32_t sK[2] = {sQ + PA_TILE_BYTES, sQ + 2 * PA_TILE_BYTES};
+  const uint32_t sV[2] = {sQ + 3 * PA_TILE_BYTES, sQ + 4 * PA_TILE_BYTES};
+  const __nv_bfloat16* gq = qkv + (size_t)s0 * rs + h * PA_D;
+  const __nv_bfloat16* gk = qkv + (size_t)s0 * rs + (H + kh) * PA_D;
+  const __nv_bfloat16* gv = qkv + (size_t)s0 * rs + (H + Hkv + kh) * PA_D;
+
+  load_tile(sQ, gq, rs, q0, len);
+  load_tile(sK[0], gk, rs, 0, len);
+  load_tile(sV[0], gv, rs, 0, len);
+  cp_async_commit();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  uint32_t qf[8][4];
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  const int nkv = qt + 1;  // causal: tiles 0..qt
+
+  for (int j = 0; j < nkv; ++j) {
+    const int buf = j & 1;
+    if (j + 1 < nkv) {
+      load_tile(sK[buf ^ 1], gk, rs, (j + 1) * PA_BK, len);
+      load_tile(sV[buf ^ 1], gv, rs, (j + 1) * PA_BK, len);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (j == 0) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int row = warp * 16 + (lane & 15);
+        const int chunk = kk * 2 + (lane >> 4);
+        ldsm_x4(sQ + swz(row, chunk), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+      }
+    }
+    // S = Q K^T  (16 x 64 per warp)
+    float s[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        const int key = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int chunk = kk * 2 + ((lane >> 3) & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(sK[buf] + swz(key, chunk), b0, b1, b2, b3);
+        mma_bf16(s[2 * np], qf[kk], b0, b1);
+        mma_bf16(s[2 * np + 1], qf[kk], b2, b3);
+      }
+    }
+    // causal mask on the diagonal tile (also masks keys beyond len)
+    const int qrow0 = q0 + warp * 16 + g;
+    if (j == qt) {
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int key = j * PA_BK + nt * 8 + 2 * t;
+        if (key > qrow0) s[nt][0] = -INFINITY;
+        if (key + 1 > qrow0) s[nt][1] = -INFINITY;
+        if (key > qrow0 + 8) s[nt][2] = -INFINITY;
+        if (key + 1 > qrow0 + 8) s[nt][3] = -INFINITY;
+      }
+    }
+    // online softmax (rows g and g+8 of the warp's 16)
+    float mnew[2] = {mrow[0], mrow[1]};
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      mnew[0] = fmaxf(mnew[0], fmaxf(s[nt][0], s[nt][1]));
+      mnew[1] = fmaxf(mnew[1], fmaxf(s[nt][2], s[nt][3]));
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 1));
+      mnew[r] = fmaxf(mnew[r], __shfl_xor_sync(0xffffffffu, mnew[r], 2));
+    }
+    float corr[2], msc[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      msc[r] = mnew[r] == -INFINITY ? 0.f : mnew[r] * scale_log2;
+      corr[r] = exp2f(mrow[r] * scale_log2 - msc[r]);
+      if (mrow[r] == -INFINITY) corr[r] = 0.f;
+      mrow[r] = mnew[r];
+    }
+    float rsum[2] = {0.f, 0.f};
+    uint32_t pf[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(s[nt][0] * scale_log2 - msc[0]);
+      const float p1 = exp2f(s[nt][1] * scale_log2 - msc[0]);
+      const float p2 = exp2f(s[nt][2] * scale_log2 - msc[1]);
+      const float p3 = exp2f(s[nt][3] * scale_log2 - msc[1]);
+      rsum[0] += p0 + p1;
+      rsum[1] += p2 + p3;
+      const int kstep = nt >> 1;
+      if ((nt & 1) == 0) {
+        pf[kstep][0] = f2_to_bf2(p0, p1);
+        pf[kstep][1] = f2_to_bf2(p2, p3);
+      } else {
+        pf[kstep][2] = f2_to_bf2(p0, p1);
+        pf[kstep][3] = f2_to_bf2(p2, p3);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) lrow[r] = lrow[r] * corr[r] + rsum[r];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      o[i][0] *= corr[0];
+      o[i][1] *= corr[0];
+      o[i][2] *= corr[1];
+      o[i][3] *= corr[1];
+    }
+    // O += P V
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+      for (int dp = 0; dp < 8; ++dp) {
+        const int key = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int chunk = dp * 2 + (lane >> 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(sV[buf] + swz(key, chunk), b0, b1, b2, b3);
+        mma_bf16(o[2 * dp], pf[ks], b0, b1);
+        mma_bf16(o[2 * dp + 1], pf[ks], b2, b3);
+      }
+    }
+    __syncthreads();
+  }
+  // finalize
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 1);
+    lrow[r] += __shfl_xor_sync(0xffffffffu, lrow[r], 2);
+  }
+  const int Hd = H * PA_D;
+  const int r0 = q0 + warp * 16 + g;
+  const float inv0 = 1.f / lrow[0], inv1 = 1.f / lrow[1];
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    const int col = h * PA_D + nt * 8 + 2 * t;
+    if (r0 < len)
+      *reinterpret_cast<uint32_t*>(out + (size_t)(s0 + r0) * Hd + col) =
+          f2_to_bf2(o[nt][0] * inv0, o[nt][1] * inv0);
+    if (r0 + 8 < len)
+      *reinterpret_cast<uint32_t*>(out + (size_t)(s0 + r0 + 8) * Hd + col) =
+          f2_to_bf2(o[nt][2] * inv1, o[nt][3] * inv1);
+  }
+}
+
+// ============================================================ decode
+constexpr int DA_D = 128;
+constexpr int DA_MAXG = 8;
+constexpr int DA_WARPS = 4;
+
+// grid (B, Hkv, NP); 128 threads
+__global__ void __launch_bounds__(DA_WARPS * 32)
+    attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
+                       const __nv_bfloat16* __restrict__ kpool,
+                       const __nv_bfloat16* __restrict__ vpool,
+                       const int32_t* __restrict__ tables, int max_blocks,
+                       const int32_t* __restrict__ ctx_lens, int H, int Hkv, int bs,
+                       float scale_log2, int part, float* __restrict__ ws) {
+  extern __shared__ float dsm[];
+  const int b = blockIdx.x, kh = blockIdx.y, p = blockIdx.z;
+  const int NP = gridDim.z;
+  const int G = H / Hkv;
+  const int ctx = ctx_lens[b];
+  const int t0 = p * part;
+  const int t1 = min(ctx, t0 + part);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* sq = dsm;                      // [G][128]
+  float* ss = sq + G * DA_D;            // [G][part]
+  float* sacc = ss + G * part;          // [WARPS][G][128]
+  float* sstat = sacc + DA_WARPS * G * DA_D;  // [G][2]
+  // workspace layout: [B][H][NP] x {o[128], m, l}
+  auto wsp = [&](int gh) { return ws + (((size_t)b * H + gh) * NP + p) * (DA_D + 2); };
+
+  if (t0 >= t1) {
+    if (threadIdx.x < G) {
+      float* w = wsp(kh * G + threadIdx.x);
+      w[DA_D] = -INFINITY;
+      w[DA_D + 1] = 0.f;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
+    const int gi = i / DA_D, d = i % DA_D;
+    sq[i] = __bfloat162float(qkv[(size_t)b * rs + (kh * G + gi) * DA_D + d]) * scale_log2;
+  }
+  __syncthreads();
+
+  const int32_t* trow = tables + (size_t)b * max_blocks;
+  const int ntok = t1 - t0;
+  // ---- scores: half-warp per token, 8 x 16 B per lane
+  {
+    const int half = lane >> 4, hl = lane & 15;
+    for (int tb = warp * 2; tb < ntok; tb += DA_WARPS * 2) {  // warp-uniform
+      const int tt = tb + half;
+      const bool valid = tt < ntok;
+      float kf[8];
+      if (valid) {
+        const int tok = t0 + tt;
+        const int blk = trow[tok / bs];
+        const uint4 kv = ld_nc_v4(kpool + (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D +
+                                  hl * 8);
+        float2 a = bf2_to_f2(kv.x), c = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
+               f = bf2_to_f2(kv.w);
+        kf[0] = a.x; kf[1] = a.y; kf[2] = c.x; kf[3] = c.y;
+        kf[4] = e.x; kf[5] = e.y; kf[6] = f.x; kf[7] = f.y;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) kf[j] = 0.f;
+      }
+      for (int gi = 0; gi < G; ++gi) {
+        const float* q = sq + gi * DA_D + hl * 8;
+        float d = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d = fmaf(q[j], kf[j], d);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (hl == 0 && valid) ss[gi * part + tt] = d;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- softmax stats per head (warp gi%WARPS handles head gi)
+  for (int gi = warp; gi < G; gi += DA_WARPS) {
+    float m = -INFINITY;
+    for (int i = lane; i < ntok; i += 32) m = fmaxf(m, ss[gi * part + i]);
+    m = warp_max(m);
+    float l = 0.f;
+    for (int i = lane; i < ntok; i += 32) {
+      const float e = exp2f(ss[gi * part + i] - m);
+      ss[gi * part + i] = e;
+      l += e;
+    }
+    l = warp_sum(l);
+    if (lane == 0) {
+      sstat[gi * 2] = m;
+      sstat[gi * 2 + 1] = l;
+    }
+  }
+  __syncthreads();
+  // ---- P V: warp per token stripe, lane owns dh [4*lane, 4*lane+4)
+  float acc[DA_MAXG][4];
+#pragma unroll
+  for (int gi = 0; gi < DA_MAXG; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
+  for (int tt = warp; tt < ntok; tt += DA_WARPS) {
+    const int tok = t0 + tt;
+    const int blk = trow[tok / bs];
+    const __nv_bfloat16* vp =
+        vpool + (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D + lane * 4;
+    const uint2 vv = *reinterpret_cast<const uint2*>(vp);
+    const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
+#pragma unroll
+    for (int gi = 0; gi < DA_MAXG; ++gi) {
+      if (gi >= G) break;
+      const float pw = ss[gi * part + tt];
+      acc[gi][0] = fmaf(pw, v0.x, acc[gi][0]);
+      acc[gi][1] = fmaf(pw, v0.y, acc[gi][1]);
+      acc[gi][2] = fmaf(pw, v1.x, acc[gi][2]);
+      acc[gi][3] = fmaf(pw, v1.y, acc[gi][3]);
+    }
+  }
+#pragma unroll
+  for (int gi = 0; gi < DA_MAXG; ++gi) {
+    if (gi >= G) break;
+    float4* dst = reinterpret_cast<float4*>(sacc + ((size_t)warp * G + gi) * DA_D + lane * 4);
+    *dst = make_float4(acc[gi][0], acc[gi][1], acc[gi][2], acc[gi][3]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
+    const int gi = i / DA_D, d = i % DA_D;
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < DA_WARPS; ++w) v += sacc[((size_t)w * G + gi) * DA_D + d];
+    float* wo = wsp(kh * G + gi);
+    wo[d] = v;
+    if (d == 0) {
+      wo[DA_D] = sstat[gi * 2];
+      wo[DA_D + 1] = sstat[gi * 2 + 1];
+    }
+  }
+}
+
+// merge partitions: grid (B, H), 128 threads (one per dh element)
+__global__ void attn_decode_merge_kernel(const float* __restrict__ ws, int H, int NP,
+                                         __nv_bfloat16* __restrict__ out) {
+  const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  const float* base = ws + ((size_t)b * H + h) * NP * (DA_D + 2);
+  float m = -INFINITY;
+  for (int p = 0; p < NP; ++p) m = fmaxf(m, base[p * (DA_D + 2) + DA_D]);
+  float l = 0.f, o = 0.f;
+  for (int p = 0; p < NP; ++p) {
+    const float* w = base + p * (DA_D + 2);
+    const float mp = w[DA_D];
+    if (mp == -INFINITY) continue;
+    const float f = exp2f(mp - m);
+    l += w[DA_D + 1] * f;
+    o += w[d] * f;
+  }
+  out[((size_t)b * H + h) * DA_D + d] = __float2bfloat16(o / l);
+}
+
+}  // namespace swb
+
+using namespace swb;
+
+extern "C" int swb_attn_prefill(const void* qkv, int row_stride, const int32_t* cu_seqlens,
+                                int num_seqs, int max_seqlen, int H, int Hkv, int dh,
+                                float scale, void* out, uintptr_t stream) {
+  SWB_REQUIRE(qkv && cu_seqlens && out, "swb_attn_prefill: null pointer");
+  SWB_REQUIRE(dh == PA_D, "swb_attn_prefill: dh must be 128 (got %d)", dh);
+  SWB_REQUIRE(H > 0 && Hkv > 0 && H % Hkv == 0, "swb_attn_prefill: bad heads");
+  SWB_REQUIRE(row_stride % 8 == 0, "swb_attn_prefill: row_stride %% 8");
+  SWB_REQUIRE(num_seqs >= 0 && max_seqlen >= 0, "swb_attn_prefill: bad sizes");
+  if (num_seqs == 0 || max_seqlen == 0) return SWB_OK;
+  static bool attr[64] = {false};
+  int dev = 0;
+  SWB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr[dev]) {
+    SWB_CUDA(cudaFuncSetAttribute(attn_prefill_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, PA_SMEM));
+    attr[dev] = true;
+  }
+  const int tiles = (max_seqlen + PA_BQ - 1) / PA_BQ;
+  dim3 grid(num_seqs * tiles, H);
+  attn_prefill_kernel<<<grid, 128, PA_SMEM, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride, cu_seqlens, tiles, H, Hkv,
+      scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(out));
+  return swb_check_launch("attn_prefill_kernel");
+}
+
+extern "C" size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int partition,
+                                            int dh) {
+  if (B <= 0 || H <= 0 || max_ctx <= 0 || partition <= 0) return 0;
+  const size_t np = (max_ctx + partition - 1) / partition;
+  return (size_t)B * H * np * (dh + 2) * sizeof(float);
+}
+
+extern "C" int swb_attn_decode(const void* qkv, int row_stride, const void* k_layer,
+                               const void* v_layer, const int32_t* block_tables,
+                               int max_blocks, const int32_t* ctx_lens, int B, int H,
+                               int Hkv, int dh, int block_size, float scale, int max_ctx,
+                               int partition, void* workspace, void* out,
+                               uintptr_t stream) {
+  SWB_REQUIRE(qkv && k_layer && v_layer && block_tables && ctx_lens && workspace && out,
+              "swb_attn_decode: null pointer");
+  SWB_REQUIRE(dh == DA_D, "swb_attn_decode: dh must be 128");
+  SWB_REQUIRE(H > 0 && Hkv > 0 && H % Hkv == 0 && H / Hkv <= DA_MAXG,
+              "swb_attn_decode: GQA group must be <= %d", DA_MAXG);
+  SWB_REQUIRE(B > 0 && max_ctx > 0 && partition > 0 && partition % 32 == 0 &&
+                  block_size > 0,
+              "swb_attn_decode: bad sizes");
+  const int G = H / Hkv;
+  const int NP = (max_ctx + partition - 1) / partition;
+  const size_t smem = sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
+                                       (size_t)DA_WARPS * G * DA_D + 2 * G);
+  SWB_REQUIRE(smem <= 200 * 1024, "swb_attn_decode: partition too large");
+  if (smem > 48 * 1024) {
+    SWB_CUDA(cudaFuncSetAttribute(attn_decode_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  dim3 grid(B, Hkv, NP);
+  attn_decode_kernel<<<grid, DA_WARPS * 32, smem, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
+      reinterpret_cast<const __nv_bfloat16*>(k_layer),
+      reinterpret_cast<const __nv_bfloat16*>(v_layer), block_tables, max_blocks, ctx_lens,
+      H, Hkv, block_size, scale * 1.4426950408889634f, partition,
+      reinterpret_cast<float*>(workspace));
+  const int st = swb_check_launch("attn_decode_kernel");
+  if (st != SWB_OK) return st;
+  attn_decode_merge_kernel<<<dim3(B, H), DA_D, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float*>(workspace), H, NP, reinterpret_cast<__nv_bfloat16*>(out));
+  return swb_check_launch("attn_decode_merge_kernel");
+}

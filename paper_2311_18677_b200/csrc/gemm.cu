@@ -1,0 +1,264 @@
+// Prefill GEMM on the 5th-generation tensor cores (sm_100a).
+//
+//   out[M,N] = epilogue( A[M,K] . W[N,K]^T )      bf16 x bf16 -> fp32 (TMEM)
+//
+// One CTA computes a 128 x 256 output tile.  Warp 0 (one elected lane) is the
+// TMA producer feeding a 4-stage ring of 128B-swizzled smem tiles (A 16 KB +
+// W 32 KB per stage); warp 1 (one elected lane) issues tcgen05.mma
+// (M=128, N=256, K=16, cta_group::1) into a 256-column TMEM accumulator and
+// releases ring slots with tcgen05.commit; warp 2 owns the TMEM allocation.
+// After the last k-block all four warps drain TMEM with tcgen05.ld (warp w
+// owns TMEM lanes 32w..32w+31 = tile rows) and apply the fused epilogue:
+// bf16 store, fp32 store, fp32 residual add (O / down projections), or
+// SwiGLU over gate/up rows interleaved in 128-row groups (gate/up projection).
+//
+// This replaces the prompt-phase cost lookup PerfModel.prompt_time
+// (reference perf.py:119-123) for the linear layers of a prefill.
+#include <cstdarg>
+#include <cstdio>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace swb {
+
+constexpr int GM = 128, GN = 256, GK = 64, GSTAGES = 4;
+constexpr int G_A_BYTES = GM * GK * 2;  // 16 KB
+constexpr int G_B_BYTES = GN * GK * 2;  // 32 KB
+constexpr int G_STAGE_BYTES = G_A_BYTES + G_B_BYTES;
+constexpr int G_SMEM_BYTES = GSTAGES * G_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t G_TMEM_COLS = 256;
+
+struct GemmArgs {
+  void* out;
+  const float* resid;
+  int M, N, K;
+  int epi;
+};
+
+__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
+
+__global__ void __launch_bounds__(128, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmW, GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + GSTAGES * G_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GSTAGES * G_STAGE_BYTES);
+  uint64_t* empty = full + GSTAGES;
+  uint64_t* done = empty + GSTAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * GM;
+  const int n0 = blockIdx.x * GN;
+  const int num_k = (args.K + GK - 1) / GK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < GSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<G_TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      for (int kb = 0; kb < num_k; ++kb) {
+        const int s = kb % GSTAGES;
+        if (kb >= GSTAGES) mbar_wait(&empty[s], ((kb / GSTAGES) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], G_STAGE_BYTES);
+        tma_load_2d(sA + s * G_A_BYTES, &tmA, &full[s], kb * GK, m0);
+        tma_load_2d(sB + s * G_B_BYTES, &tmW, &full[s], kb * GK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = umma_idesc_bf16(GM, GN);
+      for (int kb = 0; kb < num_k; ++kb) {
+        const int s = kb % GSTAGES;
+        mbar_wait(&full[s], (kb / GSTAGES) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sA + s * G_A_BYTES);
+        const uint32_t b_base = smem_u32(sB + s * G_B_BYTES);
+#pragma unroll
+        for (int k = 0; k < GK / 16; ++k) {
+          // K-major SW128: advancing 16 bf16 along K = +32 B start address.
+          tc_mma_f16(tmem, umma_desc_k_sw128(a_base + k * 32),
+                     umma_desc_k_sw128(b_base + k * 32), idesc,
+                     (kb | k) != 0);
+        }
+        tc_commit(&empty[s]);
+      }
+      tc_commit(done);
+    }
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> global
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int row = m0 + warp * 32 + lane;
+  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const bool row_ok = row < args.M;
+  uint32_t r[32];
+
+  if (args.epi == SWB_EPI_SWIGLU) {
+    // tile cols [0,128) = gate, [128,256) = up for outputs n0/2 + [0,128)
+    const int nout = args.N >> 1;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out);
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t u[32];
+      tmem_ld32(t_row + c * 32, r);
+      tmem_ld32(t_row + 128 + c * 32, u);
+      tc_wait_ld();
+      const int col = (n0 >> 1) + c * 32;
+      if (row_ok && col < nout) {
+        uint32_t packed[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float g0 = __uint_as_float(r[2 * i]), g1 = __uint_as_float(r[2 * i + 1]);
+          float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+          packed[i] = f2_to_bf2(silu(g0) * u0, silu(g1) * u1);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * nout + col);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2],
+                              packed[4 * i + 3]);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < GN / 32; ++c) {
+      tmem_ld32(t_row + c * 32, r);
+      tc_wait_ld();
+      const int col = n0 + c * 32;
+      if (!row_ok || col >= args.N) continue;
+      if (args.epi == SWB_EPI_BF16) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out);
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * args.N + col);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(
+              f2_to_bf2(__uint_as_float(r[8 * i + 0]), __uint_as_float(r[8 * i + 1])),
+              f2_to_bf2(__uint_as_float(r[8 * i + 2]), __uint_as_float(r[8 * i + 3])),
+              f2_to_bf2(__uint_as_float(r[8 * i + 4]), __uint_as_float(r[8 * i + 5])),
+              f2_to_bf2(__uint_as_float(r[8 * i + 6]), __uint_as_float(r[8 * i + 7])));
+      } else {
+        float* out = reinterpret_cast<float*>(args.out) + (size_t)row * args.N + col;
+        if (args.epi == SWB_EPI_RESID_F32) {
+          const float4* res = reinterpret_cast<const float4*>(
+              args.resid + (size_t)row * args.N + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 v = res[i];
+            v.x += __uint_as_float(r[4 * i + 0]);
+            v.y += __uint_as_float(r[4 * i + 1]);
+            v.z += __uint_as_float(r[4 * i + 2]);
+            v.w += __uint_as_float(r[4 * i + 3]);
+            reinterpret_cast<float4*>(out)[i] = v;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(out)[i] =
+                make_float4(__uint_as_float(r[4 * i + 0]), __uint_as_float(r[4 * i + 1]),
+                            __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<G_TMEM_COLS>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 K-major operand [rows, K] -> tiles of box_rows x 64 (128 B rows),
+// 128-byte swizzle, out-of-bounds rows/cols zero filled.
+int make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, int rows, int K,
+                          int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return swb_set_error(SWB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return swb_set_error(SWB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SWB_OK;
+}
+
+}  // namespace swb
+
+using namespace swb;
+
+extern "C" int swb_gemm_bf16(const void* a, const void* w, void* out,
+                             const void* resid, int M, int N, int K, int epilogue,
+                             uintptr_t stream) {
+  SWB_REQUIRE(a && w && out, "swb_gemm_bf16: null pointer");
+  SWB_REQUIRE(M > 0 && N > 0 && K > 0, "swb_gemm_bf16: bad shape M=%d N=%d K=%d", M, N, K);
+  SWB_REQUIRE(K % 8 == 0, "swb_gemm_bf16: K=%d must be a multiple of 8", K);
+  SWB_REQUIRE(N % 32 == 0, "swb_gemm_bf16: N=%d must be a multiple of 32", N);
+  SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_SWIGLU,
+              "swb_gemm_bf16: bad epilogue %d", epilogue);
+  SWB_REQUIRE(epilogue != SWB_EPI_SWIGLU || N % 256 == 0,
+              "swb_gemm_bf16: SwiGLU epilogue needs N %% 256 == 0 (N=%d)", N);
+  SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid,
+              "swb_gemm_bf16: residual epilogue needs resid");
+  SWB_REQUIRE((((uintptr_t)a | (uintptr_t)w | (uintptr_t)out) & 15) == 0,
+              "swb_gemm_bf16: pointers must be 16-byte aligned");
+  CUtensorMap ta, tw;
+  int st = make_tmap_bf16_kmajor(&ta, a, M, K, GM);
+  if (st) return st;
+  st = make_tmap_bf16_kmajor(&tw, w, N, K, GN);
+  if (st) return st;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  SWB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr_set[dev]) {
+    SWB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  G_SMEM_BYTES));
+    attr_set[dev] = true;
+  }
+  GemmArgs args{out, reinterpret_cast<const float*>(resid), M, N, K, epilogue};
+  dim3 grid((N + GN - 1) / GN, (M + GM - 1) / GM);
+  gemm_bf16_tcgen05<<<grid, 128, G_SMEM_BYTES, (cudaStream_t)stream>>>(ta, tw, args);
+  return swb_check_launch("gemm_bf16_tcgen05");
+}

@@ -1,0 +1,380 @@
+// Element-wise / row-wise kernels of the prefill and decode layers, the
+// RoPE + paged-KV write, the per-layer KV pack-and-push, completion flags and
+// the graph-resident decode bookkeeping.
+//
+// KV block layout (per layer, K and V separately):
+//     [num_blocks][Hkv][block_size][dh] bf16
+// A token at logical position p of a sequence lives in physical slot
+//     slot = block_table[p / block_size] * block_size + p % block_size.
+// One (block, head) is block_size*dh*2 bytes contiguous (4 KB at bs=16,
+// dh=128), which is the unit the decode-attention kernel streams.
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace swb {
+
+// ------------------------------------------------------------------ embed
+__global__ void embed_kernel(const int32_t* __restrict__ tokens,
+                             const __nv_bfloat16* __restrict__ table,
+                             float* __restrict__ x, int d) {
+  const int r = blockIdx.x;
+  const int tok = tokens[r];
+  const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)tok * d);
+  float4* dst = reinterpret_cast<float4*>(x + (size_t)r * d);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
+    const uint4 v = src[c];
+    const float2 a = bf2_to_f2(v.x), b = bf2_to_f2(v.y), e = bf2_to_f2(v.z),
+                 f = bf2_to_f2(v.w);
+    dst[2 * c] = make_float4(a.x, a.y, b.x, b.y);
+    dst[2 * c + 1] = make_float4(e.x, e.y, f.x, f.y);
+  }
+}
+
+// ---------------------------------------------------------------- rmsnorm
+__global__ void rmsnorm_kernel(const float* __restrict__ x,
+                               const int32_t* __restrict__ row_index,
+                               const __nv_bfloat16* __restrict__ w,
+                               __nv_bfloat16* __restrict__ out, int d, float eps) {
+  const int r = blockIdx.x;
+  const int src = row_index ? row_index[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * d);
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+    const float4 v = xr[c];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float rstd = rsqrtf(red[0] / (float)d + eps);
+  const uint2* wv = reinterpret_cast<const uint2*>(w);
+  uint2* o = reinterpret_cast<uint2*>(out + (size_t)r * d);
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+    const float4 v = xr[c];
+    const uint2 ww = wv[c];
+    const float2 w0 = bf2_to_f2(ww.x), w1 = bf2_to_f2(ww.y);
+    o[c] = make_uint2(f2_to_bf2(v.x * rstd * w0.x, v.y * rstd * w0.y),
+                      f2_to_bf2(v.z * rstd * w1.x, v.w * rstd * w1.y));
+  }
+}
+
+// ----------------------------------------------------------------- argmax
+__global__ void argmax_kernel(const float* __restrict__ logits, int V,
+                              int32_t* __restrict__ out) {
+  const float* row = logits + (size_t)blockIdx.x * V;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best) {  // strided scan visits increasing i: first max kept
+      best = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sb[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = sb[0];
+    int i0 = si[0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (sb[k] > b || (sb[k] == b && si[k] < i0)) {
+        b = sb[k];
+        i0 = si[k];
+      }
+    out[blockIdx.x] = i0;
+  }
+}
+
+// ------------------------------------------------------ RoPE + KV write
+// One CTA per row.  Thread t handles 4 consecutive rotary pairs (i..i+3 with
+// partners i+dh/2..) of one q or k head; k heads are also written to the
+// paged pool together with the matching v chunk.
+__global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int row_stride,
+                               const int32_t* __restrict__ positions, int H,
+                               int Hkv, int dh, float log2_theta,
+                               __nv_bfloat16* __restrict__ kpool,
+                               __nv_bfloat16* __restrict__ vpool,
+                               const int32_t* __restrict__ slots, int bs) {
+  const int r = blockIdx.x;
+  const int half = dh >> 1;
+  const int groups = half >> 2;  // 4 pairs per thread
+  const float pos = (float)positions[r];
+  __nv_bfloat16* row = qkv + (size_t)r * row_stride;
+  const int total = (H + Hkv) * groups;
+  int slot = 0;
+  if (kpool) slot = slots[r];
+  const int blk = slot / bs, off = slot % bs;
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int head = t / groups;
+    const int i0 = (t % groups) * 4;
+    __nv_bfloat16* hp = row + head * dh;
+    const uint2 lo = *reinterpret_cast<const uint2*>(hp + i0);
+    const uint2 hi = *reinterpret_cast<const uint2*>(hp + half + i0);
+    float a[4], b[4];
+    {
+      float2 t0 = bf2_to_f2(lo.x), t1 = bf2_to_f2(lo.y);
+      a[0] = t0.x; a[1] = t0.y; a[2] = t1.x; a[3] = t1.y;
+      t0 = bf2_to_f2(hi.x); t1 = bf2_to_f2(hi.y);
+      b[0] = t0.x; b[1] = t0.y; b[2] = t1.x; b[3] = t1.y;
+    }
+    float ra[4], rb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // inv_freq = theta^(-2i/dh)
+      const float inv_freq = exp2f(-log2_theta * (float)(2 * (i0 + j)) / (float)dh);
+      float s, c;
+      sincosf(pos * inv_freq, &s, &c);
+      ra[j] = a[j] * c - b[j] * s;
+      rb[j] = b[j] * c + a[j] * s;
+    }
+    const uint2 nlo = make_uint2(f2_to_bf2(ra[0], ra[1]), f2_to_bf2(ra[2], ra[3]));
+    const uint2 nhi = make_uint2(f2_to_bf2(rb[0], rb[1]), f2_to_bf2(rb[2], rb[3]));
+    *reinterpret_cast<uint2*>(hp + i0) = nlo;
+    *reinterpret_cast<uint2*>(hp + half + i0) = nhi;
+    if (kpool && head >= H) {
+      const int kh = head - H;
+      const size_t base = (((size_t)blk * Hkv + kh) * bs + off) * dh;
+      *reinterpret_cast<uint2*>(kpool + base + i0) = nlo;
+      *reinterpret_cast<uint2*>(kpool + base + half + i0) = nhi;
+      const __nv_bfloat16* vp = row + (H + Hkv + kh) * dh;
+      *reinterpret_cast<uint2*>(vpool + base + i0) =
+          *reinterpret_cast<const uint2*>(vp + i0);
+      *reinterpret_cast<uint2*>(vpool + base + half + i0) =
+          *reinterpret_cast<const uint2*>(vp + half + i0);
+    }
+  }
+}
+
+// ------------------------------------------------- KV pack-and-push (P2P)
+// Grid-stride over 16-byte chunks of (row, {k,v}, head, dh/8).  Reads are
+// local (the rotated qkv activations of one finished layer); writes land in
+// the destination pool's paged blocks, which may be a peer GPU's HBM mapped
+// through CUDA IPC: each warp emits 512 B of coalesced NVLink stores.
+__global__ void kv_push_kernel(const __nv_bfloat16* __restrict__ qkv, int rows,
+                               int row_stride, int k_col, int v_col, int Hkv,
+                               int dh, __nv_bfloat16* __restrict__ dk,
+                               __nv_bfloat16* __restrict__ dv,
+                               const int32_t* __restrict__ slots, int bs) {
+  const int cpr = dh >> 3;                  // chunks per head
+  const long per_row = (long)2 * Hkv * cpr;  // k and v
+  const long total = per_row * rows;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / per_row);
+    int rem = (int)(i - (long)r * per_row);
+    const int is_v = rem >= Hkv * cpr;
+    if (is_v) rem -= Hkv * cpr;
+    const int h = rem / cpr, c = rem % cpr;
+    const __nv_bfloat16* src =
+        qkv + (size_t)r * row_stride + (is_v ? v_col : k_col) + h * dh + c * 8;
+    const int slot = slots[r];
+    const int blk = slot / bs, off = slot % bs;
+    __nv_bfloat16* dst = (is_v ? dv : dk) + (((size_t)blk * Hkv + h) * bs + off) * dh + c * 8;
+    st_v4(dst, ld_v4(src));
+  }
+}
+
+__global__ void signal_kernel(uint32_t* flag, uint32_t value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value)
+               : "memory");
+}
+
+// -------------------------------------------------- decode bookkeeping
+__global__ void decode_prepare_kernel(const int32_t* __restrict__ ctx,
+                                      const int32_t* __restrict__ tables,
+                                      int max_blocks, int bs, int B,
+                                      int32_t* __restrict__ pos,
+                                      int32_t* __restrict__ slots,
+                                      int32_t* __restrict__ attn_len) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int c = ctx[b];
+  pos[b] = c;
+  slots[b] = tables[(size_t)b * max_blocks + c / bs] * bs + c % bs;
+  attn_len[b] = c + 1;
+}
+
+__global__ void decode_advance_kernel(const int32_t* __restrict__ next_tok,
+                                      int32_t* __restrict__ cur_tok,
+                                      int32_t* __restrict__ ctx,
+                                      int32_t* __restrict__ step,
+                                      int32_t* __restrict__ ring, int ring_len,
+                                      int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int t = next_tok[b];
+  cur_tok[b] = t;
+  const int s = step[b];
+  if (s < ring_len) ring[(size_t)b * ring_len + s] = t;
+  step[b] = s + 1;
+  ctx[b] += 1;
+}
+
+__global__ void slots_from_table_kernel(const int32_t* table_row, int start,
+                                        int n, int bs, int32_t* slots) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int p = start + i;
+  slots[i] = table_row[p / bs] * bs + p % bs;
+}
+
+}  // namespace swb
+
+using namespace swb;
+
+#define STREAM ((cudaStream_t)stream)
+
+extern "C" int swb_embed(const int32_t* tokens, const void* table, float* x,
+                         int rows, int d, uintptr_t stream) {
+  SWB_REQUIRE(tokens && table && x, "swb_embed: null pointer");
+  SWB_REQUIRE(rows >= 0 && d > 0 && d % 8 == 0, "swb_embed: bad shape");
+  if (rows == 0) return SWB_OK;
+  embed_kernel<<<rows, 256, 0, STREAM>>>(
+      tokens, reinterpret_cast<const __nv_bfloat16*>(table), x, d);
+  return swb_check_launch("embed_kernel");
+}
+
+extern "C" int swb_rmsnorm(const float* x, const int32_t* row_index, const void* w,
+                           void* out, int rows, int d, float eps, uintptr_t stream) {
+  SWB_REQUIRE(x && w && out, "swb_rmsnorm: null pointer");
+  SWB_REQUIRE(rows >= 0 && d > 0 && d % 4 == 0, "swb_rmsnorm: bad shape");
+  if (rows == 0) return SWB_OK;
+  rmsnorm_kernel<<<rows, 512, 0, STREAM>>>(
+      x, row_index, reinterpret_cast<const __nv_bfloat16*>(w),
+      reinterpret_cast<__nv_bfloat16*>(out), d, eps);
+  return swb_check_launch("rmsnorm_kernel");
+}
+
+extern "C" int swb_argmax(const float* logits, int rows, int V, int32_t* out,
+                          uintptr_t stream) {
+  SWB_REQUIRE(logits && out, "swb_argmax: null pointer");
+  SWB_REQUIRE(rows >= 0 && V > 0, "swb_argmax: bad shape");
+  if (rows == 0) return SWB_OK;
+  argmax_kernel<<<rows, 1024, 0, STREAM>>>(logits, V, out);
+  return swb_check_launch("argmax_kernel");
+}
+
+extern "C" int swb_rope_kv_write(void* qkv, int rows, int row_stride,
+                                 const int32_t* positions, int H, int Hkv, int dh,
+                                 float theta, void* k_layer, void* v_layer,
+                                 const int32_t* slots, int block_size,
+                                 uintptr_t stream) {
+  SWB_REQUIRE(qkv && positions, "swb_rope_kv_write: null pointer");
+  SWB_REQUIRE(dh % 8 == 0 && H > 0 && Hkv > 0 && H % Hkv == 0,
+              "swb_rope_kv_write: bad heads H=%d Hkv=%d dh=%d", H, Hkv, dh);
+  SWB_REQUIRE(row_stride >= (H + 2 * Hkv) * dh, "swb_rope_kv_write: row_stride");
+  SWB_REQUIRE((k_layer == nullptr) == (v_layer == nullptr),
+              "swb_rope_kv_write: k/v pools must both be set or both null");
+  SWB_REQUIRE(!k_layer || (slots && block_size > 0), "swb_rope_kv_write: slots");
+  SWB_REQUIRE(theta > 1.f, "swb_rope_kv_write: theta");
+  if (rows == 0) return SWB_OK;
+  rope_kv_kernel<<<rows, 256, 0, STREAM>>>(
+      reinterpret_cast<__nv_bfloat16*>(qkv), row_stride, positions, H, Hkv, dh,
+      log2f(theta), reinterpret_cast<__nv_bfloat16*>(k_layer),
+      reinterpret_cast<__nv_bfloat16*>(v_layer), slots, block_size);
+  return swb_check_launch("rope_kv_kernel");
+}
+
+extern "C" int swb_kv_push_layer(const void* qkv, int rows, int row_stride,
+                                 int k_col, int v_col, int Hkv, int dh,
+                                 void* dst_k_layer, void* dst_v_layer,
+                                 const int32_t* dst_slots, int block_size,
+                                 int num_ctas, uintptr_t stream) {
+  SWB_REQUIRE(qkv && dst_k_layer && dst_v_layer && dst_slots,
+              "swb_kv_push_layer: null pointer");
+  SWB_REQUIRE(dh % 8 == 0 && Hkv > 0 && block_size > 0 && rows >= 0,
+              "swb_kv_push_layer: bad shape");
+  SWB_REQUIRE(row_stride % 8 == 0 && k_col % 8 == 0 && v_col % 8 == 0,
+              "swb_kv_push_layer: 16-byte alignment of rows/columns");
+  if (rows == 0) return SWB_OK;
+  const long chunks = (long)rows * 2 * Hkv * (dh / 8);
+  int grid = num_ctas > 0 ? num_ctas : 32;
+  const long need = (chunks + 255) / 256;
+  if (need < grid) grid = (int)need;
+  kv_push_kernel<<<grid, 256, 0, STREAM>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), rows, row_stride, k_col, v_col,
+      Hkv, dh, reinterpret_cast<__nv_bfloat16*>(dst_k_layer),
+      reinterpret_cast<__nv_bfloat16*>(dst_v_layer), dst_slots, block_size);
+  return swb_check_launch("kv_push_kernel");
+}
+
+extern "C" int swb_kv_signal(uint32_t* flag, uint32_t value, uintptr_t stream) {
+  SWB_REQUIRE(flag, "swb_kv_signal: null flag");
+  signal_kernel<<<1, 1, 0, STREAM>>>(flag, value);
+  return swb_check_launch("signal_kernel");
+}
+
+extern "C" int swb_stream_wait_flag(uint32_t* flag, uint32_t value,
+                                    uintptr_t stream) {
+  SWB_REQUIRE(flag, "swb_stream_wait_flag: null flag");
+  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+    fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+  }
+  CUresult r = fn((CUstream)stream, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS)
+    return swb_set_error(SWB_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  return SWB_OK;
+}
+
+extern "C" int swb_decode_prepare(const int32_t* ctx, const int32_t* block_tables,
+                                  int max_blocks, int block_size, int B, int32_t* pos,
+                                  int32_t* slots, int32_t* attn_len, uintptr_t stream) {
+  SWB_REQUIRE(ctx && block_tables && pos && slots && attn_len,
+              "swb_decode_prepare: null pointer");
+  SWB_REQUIRE(B > 0 && max_blocks > 0 && block_size > 0, "swb_decode_prepare: bad shape");
+  decode_prepare_kernel<<<(B + 127) / 128, 128, 0, STREAM>>>(
+      ctx, block_tables, max_blocks, block_size, B, pos, slots, attn_len);
+  return swb_check_launch("decode_prepare_kernel");
+}
+
+extern "C" int swb_decode_advance(const int32_t* next_tok, int32_t* cur_tok,
+                                  int32_t* ctx, int32_t* step, int32_t* out_ring,
+                                  int ring, int B, uintptr_t stream) {
+  SWB_REQUIRE(next_tok && cur_tok && ctx && step && out_ring,
+              "swb_decode_advance: null pointer");
+  SWB_REQUIRE(B > 0 && ring > 0, "swb_decode_advance: bad shape");
+  decode_advance_kernel<<<(B + 127) / 128, 128, 0, STREAM>>>(next_tok, cur_tok, ctx,
+                                                             step, out_ring, ring, B);
+  return swb_check_launch("decode_advance_kernel");
+}
+
+extern "C" int swb_slots_from_table(const int32_t* table_row, int start, int n,
+                                    int block_size, int32_t* slots, uintptr_t stream) {
+  SWB_REQUIRE(table_row && slots, "swb_slots_from_table: null pointer");
+  SWB_REQUIRE(start >= 0 && n >= 0 && block_size > 0, "swb_slots_from_table: bad args");
+  if (n == 0) return SWB_OK;
+  slots_from_table_kernel<<<(n + 255) / 256, 256, 0, STREAM>>>(table_row, start, n,
+                                                               block_size, slots);
+  return swb_check_launch("slots_from_table_kernel");
+}

@@ -1,0 +1,174 @@
+"""Tensor-level wrappers over the C-ABI kernels (device memory comes from
+PyTorch; all arithmetic runs in libswb200.so).  Each wrapper validates dtype,
+device and contiguity, then launches on the current torch CUDA stream.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _abi
+from ._abi import EPI_BF16, EPI_F32, EPI_RESID_F32, EPI_SWIGLU, call
+from .errors import ValidationError
+
+__all__ = ["gemm", "gemv", "linear", "embed", "rmsnorm", "argmax", "rope_kv_write",
+           "kv_push_layer", "attn_prefill", "attn_decode", "decode_prepare",
+           "decode_advance", "slots_from_table", "kv_signal", "stream_wait_flag",
+           "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "GEMV_MAX_ROWS"]
+
+GEMV_MAX_ROWS = 16
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _req(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda:
+        raise ValidationError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValidationError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValidationError(f"{name} must be contiguous")
+
+
+def _out_shape(M, N, epi):
+    return (M, N // 2) if epi == EPI_SWIGLU else (M, N)
+
+
+def _alloc_out(a, M, N, epi):
+    dt = torch.bfloat16 if epi in (EPI_BF16, EPI_SWIGLU) else torch.float32
+    return torch.empty(_out_shape(M, N, epi), dtype=dt, device=a.device)
+
+
+def gemm(a, w, epi=EPI_BF16, out=None, resid=None):
+    """tcgen05 GEMM: out = epi(a[M,K] @ w[N,K]^T)."""
+    _req(a, torch.bfloat16, "a")
+    _req(w, torch.bfloat16, "w")
+    M, K = a.shape
+    N = w.shape[0]
+    if w.shape[1] != K:
+        raise ValidationError(f"K mismatch {a.shape} vs {w.shape}")
+    if out is None:
+        out = _alloc_out(a, M, N, epi)
+    call("swb_gemm_bf16", a.data_ptr(), w.data_ptr(), out.data_ptr(),
+         resid.data_ptr() if resid is not None else None, M, N, K, epi, _stream())
+    return out
+
+
+def gemv(x, w, epi=EPI_BF16, out=None, resid=None):
+    """Weight-streaming skinny GEMM for M <= 16 rows."""
+    _req(x, torch.bfloat16, "x")
+    _req(w, torch.bfloat16, "w")
+    M, K = x.shape
+    N = w.shape[0]
+    if out is None:
+        out = _alloc_out(x, M, N, epi)
+    call("swb_gemv_bf16", x.data_ptr(), w.data_ptr(), out.data_ptr(),
+         resid.data_ptr() if resid is not None else None, M, N, K, epi, _stream())
+    return out
+
+
+def linear(x, w, epi=EPI_BF16, out=None, resid=None):
+    """Dispatch on row count: <= 16 rows streams weights (decode), more rows
+    go to the tcgen05 GEMM (prefill).  Both are native kernels."""
+    if x.shape[0] <= GEMV_MAX_ROWS:
+        return gemv(x, w, epi, out, resid)
+    return gemm(x, w, epi, out, resid)
+
+
+def embed(tokens, table, out=None):
+    _req(tokens, torch.int32, "tokens")
+    _req(table, torch.bfloat16, "table")
+    rows, d = tokens.shape[0], table.shape[1]
+    if out is None:
+        out = torch.empty(rows, d, dtype=torch.float32, device=table.device)
+    call("swb_embed", tokens.data_ptr(), table.data_ptr(), out.data_ptr(), rows, d, _stream())
+    return out
+
+
+def rmsnorm(x, w, eps, rows_index=None, out=None):
+    _req(x, torch.float32, "x")
+    _req(w, torch.bfloat16, "w")
+    rows = x.shape[0] if rows_index is None else rows_index.shape[0]
+    d = x.shape[1]
+    if out is None:
+        out = torch.empty(rows, d, dtype=torch.bfloat16, device=x.device)
+    call("swb_rmsnorm", x.data_ptr(), rows_index.data_ptr() if rows_index is not None else None,
+         w.data_ptr(), out.data_ptr(), rows, d, float(eps), _stream())
+    return out
+
+
+def argmax(logits, out=None):
+    _req(logits, torch.float32, "logits")
+    rows, V = logits.shape
+    if out is None:
+        out = torch.empty(rows, dtype=torch.int32, device=logits.device)
+    call("swb_argmax", logits.data_ptr(), rows, V, out.data_ptr(), _stream())
+    return out
+
+
+def rope_kv_write(qkv, positions, H, Hkv, dh, theta, k_layer=None, v_layer=None,
+                  slots=None, block_size=16, rows=None):
+    _req(qkv, torch.bfloat16, "qkv")
+    _req(positions, torch.int32, "positions")
+    rows = qkv.shape[0] if rows is None else rows
+    call("swb_rope_kv_write", qkv.data_ptr(), rows, qkv.shape[1], positions.data_ptr(), H, Hkv,
+         dh, float(theta), k_layer, v_layer,
+         slots.data_ptr() if slots is not None else None, block_size, _stream())
+
+
+def kv_push_layer(qkv, rows, H, Hkv, dh, dst_k, dst_v, dst_slots, block_size, num_ctas=0,
+                  stream=None):
+    """Pack-and-push one layer's k/v rows into (possibly peer) paged blocks."""
+    call("swb_kv_push_layer", qkv.data_ptr(), rows, qkv.shape[1], H * dh, (H + Hkv) * dh, Hkv,
+         dh, dst_k, dst_v, dst_slots.data_ptr(), block_size, num_ctas,
+         stream if stream is not None else _stream())
+
+
+def attn_prefill(qkv, cu_seqlens, num_seqs, max_seqlen, H, Hkv, dh, scale, out=None):
+    _req(qkv, torch.bfloat16, "qkv")
+    _req(cu_seqlens, torch.int32, "cu_seqlens")
+    if out is None:
+        out = torch.empty(qkv.shape[0], H * dh, dtype=torch.bfloat16, device=qkv.device)
+    call("swb_attn_prefill", qkv.data_ptr(), qkv.shape[1], cu_seqlens.data_ptr(), num_seqs,
+         max_seqlen, H, Hkv, dh, float(scale), out.data_ptr(), _stream())
+    return out
+
+
+def attn_decode_workspace_bytes(B, H, max_ctx, partition, dh):
+    return int(_abi.lib.swb_attn_decode_workspace(B, H, max_ctx, partition, dh))
+
+
+def attn_decode(qkv, k_layer, v_layer, block_tables, ctx_lens, B, H, Hkv, dh, block_size,
+                scale, max_ctx, partition, workspace, out=None):
+    if out is None:
+        out = torch.empty(B, H * dh, dtype=torch.bfloat16, device=qkv.device)
+    call("swb_attn_decode", qkv.data_ptr(), qkv.shape[1], k_layer, v_layer,
+         block_tables.data_ptr(), block_tables.shape[1], ctx_lens.data_ptr(), B, H, Hkv, dh,
+         block_size, float(scale), max_ctx, partition, workspace.data_ptr(), out.data_ptr(),
+         _stream())
+    return out
+
+
+def decode_prepare(ctx, block_tables, block_size, B, pos, slots, attn_len):
+    call("swb_decode_prepare", ctx.data_ptr(), block_tables.data_ptr(), block_tables.shape[1],
+         block_size, B, pos.data_ptr(), slots.data_ptr(), attn_len.data_ptr(), _stream())
+
+
+def decode_advance(next_tok, cur_tok, ctx, step, ring, B):
+    call("swb_decode_advance", next_tok.data_ptr(), cur_tok.data_ptr(), ctx.data_ptr(),
+         step.data_ptr(), ring.data_ptr(), ring.shape[1], B, _stream())
+
+
+def slots_from_table(table_row_ptr, start, n, block_size, slots, stream=None):
+    call("swb_slots_from_table", table_row_ptr, start, n, block_size, slots.data_ptr(),
+         stream if stream is not None else _stream())
+
+
+def kv_signal(flag_ptr, value, stream=None):
+    call("swb_kv_signal", flag_ptr, value, stream if stream is not None else _stream())
+
+
+def stream_wait_flag(flag_ptr, value, stream=None):
+    call("swb_stream_wait_flag", flag_ptr, value, stream if stream is not None else _stream())

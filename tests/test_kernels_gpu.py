@@ -1,0 +1,244 @@
+"""Kernel-level numerics of libswb200 on the GPU, each against a plain
+PyTorch fp32 reference of the same op (bf16 inputs upcast), and bit-exact
+checks for the integer / byte paths (allocator, KV write, KV push)."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2311_18677_b200 import kernels
+    torch.manual_seed(0)
+    return kernels
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+
+
+@pytest.mark.parametrize("M,N,K_", [(128, 256, 64), (1000, 768, 4096), (300, 12288, 4096),
+                                    (129, 4096, 11008), (64, 96, 136), (2048, 512, 1024)])
+def test_gemm_bf16(K, M, N, K_):
+    a = torch.randn(M, K_, device="cuda").bfloat16()
+    w = torch.randn(N, K_, device="cuda").bfloat16()
+    ref = a.float() @ w.float().t()
+    out = K.gemm(a, w, K.EPI_BF16)
+    torch.cuda.synchronize()
+    assert _rel(out, ref) < 1e-2
+    out32 = K.gemm(a, w, K.EPI_F32)
+    assert _rel(out32, ref) < 1e-4
+
+
+def test_gemm_resid_and_swiglu(K):
+    M, N, K_ = 300, 1024, 512
+    a = torch.randn(M, K_, device="cuda").bfloat16()
+    w = torch.randn(N, K_, device="cuda").bfloat16()
+    res = torch.randn(M, N, device="cuda")
+    ref = res + a.float() @ w.float().t()
+    out = res.clone()
+    K.gemm(a, w, K.EPI_RESID_F32, out=out, resid=out)
+    assert _rel(out, ref) < 1e-4
+    acc = a.float() @ w.float().t()
+    g = acc.view(M, N // 256, 2, 128)[:, :, 0, :].reshape(M, N // 2)
+    u = acc.view(M, N // 256, 2, 128)[:, :, 1, :].reshape(M, N // 2)
+    ref_sw = torch.nn.functional.silu(g) * u
+    out_sw = K.gemm(a, w, K.EPI_SWIGLU)
+    assert _rel(out_sw, ref_sw) < 1e-2
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 8, 16])
+@pytest.mark.parametrize("N,K_", [(4096, 4096), (768, 256), (1000, 11008)])
+def test_gemv(K, M, N, K_):
+    x = torch.randn(M, K_, device="cuda").bfloat16()
+    w = torch.randn(N, K_, device="cuda").bfloat16()
+    ref = x.float() @ w.float().t()
+    assert _rel(K.gemv(x, w, K.EPI_F32), ref) < 1e-4
+    assert _rel(K.gemv(x, w, K.EPI_BF16), ref) < 1e-2
+    res = torch.randn(M, N, device="cuda")
+    out = res.clone()
+    K.gemv(x, w, K.EPI_RESID_F32, out=out, resid=out)
+    assert _rel(out, res + ref) < 1e-4
+
+
+def test_gemv_swiglu(K):
+    M, N, K_ = 4, 2048, 1024
+    x = torch.randn(M, K_, device="cuda").bfloat16()
+    w = torch.randn(N, K_, device="cuda").bfloat16()
+    acc = x.float() @ w.float().t()
+    g = acc.view(M, N // 256, 2, 128)[:, :, 0, :].reshape(M, N // 2)
+    u = acc.view(M, N // 256, 2, 128)[:, :, 1, :].reshape(M, N // 2)
+    ref = torch.nn.functional.silu(g) * u
+    assert _rel(K.gemv(x, w, K.EPI_SWIGLU), ref) < 1e-2
+
+
+def test_embed_rmsnorm_argmax(K):
+    V, d, rows = 1000, 4096, 37
+    table = torch.randn(V, d, device="cuda").bfloat16()
+    tok = torch.randint(0, V, (rows,), device="cuda", dtype=torch.int32)
+    x = K.embed(tok, table)
+    assert torch.equal(x, table[tok.long()].float())
+    w = torch.randn(d, device="cuda").bfloat16()
+    h = K.rmsnorm(x, w, 1e-5)
+    ref = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    assert _rel(h, ref) < 1e-2
+    idx = torch.tensor([3, 0, 36], device="cuda", dtype=torch.int32)
+    h2 = K.rmsnorm(x, w, 1e-5, rows_index=idx)
+    assert torch.equal(h2, h[idx.long()])
+    logits = torch.randn(5, 32000, device="cuda")
+    logits[2, 100] = 50.0
+    logits[2, 7] = 50.0  # tie -> lowest index
+    am = K.argmax(logits)
+    ref_am = logits.argmax(-1).int()
+    ref_am[2] = 7
+    assert torch.equal(am, ref_am)
+
+
+def _rope_ref(x, pos, theta):
+    dh = x.shape[-1]
+    half = dh // 2
+    i = torch.arange(half, device=x.device, dtype=torch.float32)
+    inv = torch.exp2(-math.log2(theta) * (2 * i) / dh)
+    ang = pos.float()[:, None] * inv[None, :]
+    c, s = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+    a, b = x[..., :half].float(), x[..., half:].float()
+    return torch.cat([a * c - b * s, b * c + a * s], -1)
+
+
+def test_rope_kv_write_bit_exact_pool(K):
+    H, Hkv, dh, bs, rows = 8, 2, 128, 16, 50
+    qkv = torch.randn(rows, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    pos = torch.arange(rows, device="cuda", dtype=torch.int32) + 1000
+    nblk = 8
+    kpool = torch.zeros(nblk, Hkv, bs, dh, device="cuda", dtype=torch.bfloat16)
+    vpool = torch.zeros_like(kpool)
+    table = torch.tensor([5, 2, 7, 0], device="cuda", dtype=torch.int32)
+    p = torch.arange(rows, device="cuda")
+    slots = (table[p // bs].long() * bs + p % bs).int()
+    orig = qkv.clone()
+    K.rope_kv_write(qkv, pos, H, Hkv, dh, 10000.0, kpool.data_ptr(), vpool.data_ptr(), slots, bs)
+    q = orig[:, :H * dh].view(rows, H, dh)
+    k = orig[:, H * dh:(H + Hkv) * dh].view(rows, Hkv, dh)
+    v = orig[:, (H + Hkv) * dh:].view(rows, Hkv, dh)
+    assert _rel(qkv[:, :H * dh].view(rows, H, dh), _rope_ref(q, pos, 1e4)) < 1e-2
+    assert _rel(qkv[:, H * dh:(H + Hkv) * dh].view(rows, Hkv, dh), _rope_ref(k, pos, 1e4)) < 1e-2
+    # pool holds exactly the rotated k and the untouched v (bitwise)
+    kr = qkv[:, H * dh:(H + Hkv) * dh].view(rows, Hkv, dh)
+    for r in range(rows):
+        blk, off = int(slots[r]) // bs, int(slots[r]) % bs
+        assert torch.equal(kpool[blk, :, off], kr[r])
+        assert torch.equal(vpool[blk, :, off], v[r])
+
+
+def _attn_ref(q, k, v, causal=True):
+    # q [S,H,D], k/v [S,Hkv,D]
+    S, H, D = q.shape
+    G = H // k.shape[1]
+    k = k.repeat_interleave(G, 1)
+    v = v.repeat_interleave(G, 1)
+    s = torch.einsum("qhd,khd->hqk", q.float(), k.float()) / math.sqrt(D)
+    if causal:
+        m = torch.ones(S, S, device=q.device, dtype=torch.bool).tril()
+        s = s.masked_fill(~m, float("-inf"))
+    p = s.softmax(-1)
+    return torch.einsum("hqk,khd->qhd", p, v.float())
+
+
+@pytest.mark.parametrize("H,Hkv", [(4, 4), (8, 2)])
+def test_attn_prefill_varlen(K, H, Hkv):
+    dh = 128
+    lens = [1, 63, 64, 200, 130]
+    S = sum(lens)
+    qkv = torch.randn(S, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), device="cuda", dtype=torch.int32)
+    out = K.attn_prefill(qkv, cu, len(lens), max(lens), H, Hkv, dh, 1 / math.sqrt(dh))
+    off = 0
+    for L in lens:
+        blk = qkv[off:off + L]
+        q = blk[:, :H * dh].view(L, H, dh)
+        k = blk[:, H * dh:(H + Hkv) * dh].view(L, Hkv, dh)
+        v = blk[:, (H + Hkv) * dh:].view(L, Hkv, dh)
+        ref = _attn_ref(q, k, v)
+        got = out[off:off + L].view(L, H, dh)
+        assert _rel(got, ref) < 2e-2, L
+        off += L
+
+
+@pytest.mark.parametrize("H,Hkv", [(32, 32), (64, 8)])
+def test_attn_decode_paged(K, H, Hkv):
+    dh, bs = 128, 16
+    ctx = [1, 17, 300, 1100]
+    B = len(ctx)
+    maxb = 80
+    nblk = 400
+    kpool = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    vpool = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    perm = torch.randperm(nblk, device="cuda").int()
+    tables = perm[:B * maxb].view(B, maxb).contiguous()
+    qkv = torch.randn(B, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    lens = torch.tensor(ctx, device="cuda", dtype=torch.int32)
+    part = 256
+    wsb = K.attn_decode_workspace_bytes(B, H, 1200, part, dh)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    out = K.attn_decode(qkv, kpool.data_ptr(), vpool.data_ptr(), tables, lens, B, H, Hkv, dh, bs,
+                        1 / math.sqrt(dh), 1200, part, ws)
+    for b in range(B):
+        L = ctx[b]
+        p = torch.arange(L, device="cuda")
+        blk = tables[b][p // bs].long()
+        k = kpool[blk, :, p % bs]  # [L,Hkv,dh]
+        v = vpool[blk, :, p % bs]
+        q = qkv[b, :H * dh].view(1, H, dh)
+        G = H // Hkv
+        s = torch.einsum("hd,lhd->hl", q[0].float(), k.repeat_interleave(G, 1).float()) / math.sqrt(dh)
+        ref = torch.einsum("hl,lhd->hd", s.softmax(-1), v.repeat_interleave(G, 1).float())
+        assert _rel(out[b].view(H, dh), ref) < 1e-2, b
+
+
+def test_block_alloc_lowest_free_first(K):
+    from paper_2311_18677_b200.kvcache import KVCacheManager
+    from paper_2311_18677_b200.errors import CapacityError
+    kv = KVCacheManager(num_layers=2, num_blocks=100, n_kv_heads=2, head_dim=128,
+                        block_size=16, max_seqs=4, max_blocks_per_seq=40)
+    s0 = kv.allocate(160)        # 10 blocks -> 0..9
+    s1 = kv.allocate(80)         # 5 blocks  -> 10..14
+    kv.release(s0)
+    s2 = kv.allocate(180)        # 12 blocks -> 0..9, 15, 16 (lowest free first)
+    torch.cuda.synchronize()
+    t = kv.tables().cpu()
+    assert t[s1, :5].tolist() == [10, 11, 12, 13, 14]
+    assert t[s2, :12].tolist() == list(range(10)) + [15, 16]
+    assert kv.free_blocks == 100 - 17
+    with pytest.raises(CapacityError):
+        kv.allocate(16 * 41)     # more than max_blocks_per_seq
+    kv.close()
+
+
+def test_kv_push_local_bit_exact(K):
+    """Pack-and-push into a second pool on the same GPU: every pushed K/V
+    byte must equal the source rows bitwise, at the slots of the table."""
+    from paper_2311_18677_b200.kvcache import KVCacheManager
+    H, Hkv, dh, bs, rows = 8, 2, 128, 16, 77
+    dst = KVCacheManager(num_layers=3, num_blocks=64, n_kv_heads=Hkv, head_dim=dh,
+                         block_size=bs, max_seqs=4, max_blocks_per_seq=16)
+    dst.allocate(40)
+    seq = dst.allocate(rows)
+    qkv = torch.randn(rows, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    slots = torch.empty(rows, dtype=torch.int32, device="cuda")
+    K.slots_from_table(dst.table_row_ptr(seq), 0, rows, bs, slots)
+    K.kv_push_layer(qkv, rows, H, Hkv, dh, dst.k_layer_ptr(1), dst.v_layer_ptr(1), slots, bs,
+                    num_ctas=8)
+    torch.cuda.synchronize()
+    kview, vview = dst.k_view(1), dst.v_view(1)
+    table = dst.tables()[seq]
+    p = torch.arange(rows, device="cuda")
+    blk = table[p // bs].long()
+    got_k = kview[blk, :, p % bs]
+    got_v = vview[blk, :, p % bs]
+    assert torch.equal(got_k, qkv[:, H * dh:(H + Hkv) * dh].view(rows, Hkv, dh))
+    assert torch.equal(got_v, qkv[:, (H + Hkv) * dh:].view(rows, Hkv, dh))
+    dst.close()

@@ -1,0 +1,306 @@
+"""Per-GPU execution of the two phases on libswb200 kernels.
+
+``ModelRunner.prefill``  — the prompt phase (replaces PerfModel.prompt_time,
+reference perf.py:119-123): embedding, per layer RMSNorm -> QKV GEMM
+(tcgen05) -> RoPE (+ KV write into local paged blocks when the token phase
+runs on this machine) -> causal varlen attention -> O GEMM (+residual) ->
+RMSNorm -> gate/up GEMM with fused SwiGLU -> down GEMM (+residual), TP
+all-reduce after O and down; last-token norm, LM head, greedy argmax.
+When the request's token machine is another GPU, each finished layer's K/V is
+packed and pushed into that GPU's paged blocks by ``kv_push_layer`` on a side
+stream, overlapping the next layer's compute (reference plan_transfer's
+layer-wise mode, transfer.py:79-99, made real).
+
+``DecodeGraph`` — one token-phase iteration for a fixed batch bucket
+(replaces PerfModel.token_iter_time, perf.py:125-132): the whole step
+(prepare -> L x [norm, QKV GEMV, RoPE+KV append, paged attention, O GEMV,
+norm, gate/up GEMV+SwiGLU, down GEMV] -> norm -> LM head -> argmax ->
+advance) is captured once in a CUDA graph and replayed; all per-step state
+(current token, context length, output ring) stays on the device.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import kernels as K
+from .kvcache import KVCacheManager
+from .model import Weights
+
+
+@dataclass
+class PushSegment:
+    """Rows [row0, row0+rows) of a prefill batch go to one destination pool."""
+    row0: int
+    rows: int
+    dst: KVCacheManager          # peer view (or local pool for 1-GPU tests)
+    dst_seq: int                 # sequence slot in the destination tables
+    slots: torch.Tensor | None = None
+
+
+@dataclass
+class PushStats:
+    layer_ms: list = field(default_factory=list)
+    bytes_per_layer: int = 0
+    total_ms: float = 0.0        # first push start -> last push end
+    tail_ms: float = 0.0         # compute end -> last push end (visible latency)
+
+
+class ModelRunner:
+    def __init__(self, weights: Weights, kv: KVCacheManager | None = None, tp_group=None,
+                 decode_partition: int = 256, push_ctas: int = 16):
+        self.w = weights
+        self.cfg = cfg = weights.cfg
+        self.tp = weights.tp
+        self.rank = weights.rank
+        self.tp_group = tp_group
+        self.kv = kv
+        self.hq = cfg.n_heads // self.tp
+        self.hkv = cfg.n_kv_heads // self.tp
+        self.dh = cfg.head_dim
+        self.qkv_cols = (self.hq + 2 * self.hkv) * self.dh
+        self.ffn = cfg.ffn // self.tp
+        self.scale = 1.0 / math.sqrt(self.dh)
+        self.partition = decode_partition
+        self.push_ctas = push_ctas
+        self.dev = weights.embed.device
+        self._cap = 0
+        self.push_stream = torch.cuda.Stream(device=self.dev)
+        self.graphs: dict = {}
+
+    # ------------------------------------------------------------ helpers
+    def _allreduce(self, x):
+        if self.tp > 1:
+            torch.distributed.all_reduce(x, group=self.tp_group)
+
+    def _resid_epi(self):
+        # with TP only rank 0 folds the residual in; the all-reduce sums the rest
+        return K.EPI_RESID_F32 if self.rank == 0 or self.tp == 1 else K.EPI_F32
+
+    def _ensure_prefill(self, T: int, R: int):
+        if T <= self._cap and R <= getattr(self, "_rcap", 0):
+            return
+        cap = max(T, 256)
+        rcap = max(R, 16)
+        d, dev = self.cfg.d_model, self.dev
+        self.px = torch.empty(cap, d, dtype=torch.float32, device=dev)
+        self.ph = torch.empty(cap, d, dtype=torch.bfloat16, device=dev)
+        self.pqkv = [torch.empty(cap, self.qkv_cols, dtype=torch.bfloat16, device=dev)
+                     for _ in range(2)]
+        self.pattn = torch.empty(cap, self.hq * self.dh, dtype=torch.bfloat16, device=dev)
+        self.pact = torch.empty(cap, self.ffn, dtype=torch.bfloat16, device=dev)
+        self.plast = torch.empty(rcap, d, dtype=torch.bfloat16, device=dev)
+        self.plogits = torch.empty(rcap, self.cfg.vocab, dtype=torch.float32, device=dev)
+        self.pfirst = torch.empty(rcap, dtype=torch.int32, device=dev)
+        self._cap, self._rcap = cap, rcap
+
+    # ------------------------------------------------------------ prefill
+    def prefill(self, tokens: torch.Tensor, lens: list[int], meta: torch.Tensor,
+                local_slots: torch.Tensor | None = None,
+                push: list[PushSegment] | None = None,
+                push_stats: PushStats | None = None) -> torch.Tensor:
+        """Run the prompt phase for a batch of prompts packed back to back.
+
+        tokens      int32 [T] on device
+        meta        int32 device tensor = [positions(T) | cu_seqlens(R+1) | last_rows(R)]
+        local_slots int32 [T] slots in this GPU's pool (co-located token phase)
+        push        per-request destination segments (token machine elsewhere)
+        Returns the greedy first token of every prompt (int32 [R], device).
+        """
+        cfg, w = self.cfg, self.w
+        T, R = int(tokens.shape[0]), len(lens)
+        self._ensure_prefill(T, R)
+        positions = meta[:T]
+        cu = meta[T:T + R + 1]
+        last_rows = meta[T + R + 1:T + 2 * R + 1]
+        x, h, attn, act = self.px[:T], self.ph[:T], self.pattn[:T], self.pact[:T]
+        main = torch.cuda.current_stream()
+        push_events = []
+        timing = None
+        if push:
+            for seg in push:
+                if seg.slots is None:
+                    seg.slots = torch.empty(seg.rows, dtype=torch.int32, device=self.dev)
+                K.slots_from_table(seg.dst.table_row_ptr(seg.dst_seq), 0, seg.rows,
+                                   seg.dst.block_size, seg.slots)
+            if push_stats is not None:
+                timing = [(torch.cuda.Event(enable_timing=True),
+                           torch.cuda.Event(enable_timing=True)) for _ in range(cfg.n_layers)]
+                self._compute_end = torch.cuda.Event(enable_timing=True)
+        K.embed(tokens, w.embed, out=x)
+        for li, lw in enumerate(w.layers):
+            qkv = self.pqkv[li & 1][:T]
+            if push and li >= 2:
+                main.wait_event(push_events[li - 2])  # qkv buffer reuse
+            K.rmsnorm(x, lw.attn_norm, cfg.norm_eps, out=h)
+            K.linear(h, lw.wqkv, K.EPI_BF16, out=qkv)
+            if local_slots is not None and self.kv is not None:
+                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, cfg.rope_theta,
+                                self.kv.k_layer_ptr(li), self.kv.v_layer_ptr(li), local_slots,
+                                self.kv.block_size)
+            else:
+                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, cfg.rope_theta)
+            if push:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                self.push_stream.wait_event(ev)
+                with torch.cuda.stream(self.push_stream):
+                    if timing:
+                        timing[li][0].record(self.push_stream)
+                    for seg in push:
+                        K.kv_push_layer(qkv[seg.row0:seg.row0 + seg.rows], seg.rows, self.hq,
+                                        self.hkv, self.dh, seg.dst.k_layer_ptr(li),
+                                        seg.dst.v_layer_ptr(li), seg.slots,
+                                        seg.dst.block_size, self.push_ctas,
+                                        stream=self.push_stream.cuda_stream)
+                    if timing:
+                        timing[li][1].record(self.push_stream)
+                    done = torch.cuda.Event()
+                    done.record(self.push_stream)
+                push_events.append(done)
+            K.attn_prefill(qkv, cu, R, max(lens), self.hq, self.hkv, self.dh, self.scale,
+                           out=attn)
+            K.linear(attn, lw.wo, self._resid_epi(), out=x, resid=x)
+            self._allreduce(x)
+            K.rmsnorm(x, lw.mlp_norm, cfg.norm_eps, out=h)
+            K.linear(h, lw.wgu, K.EPI_SWIGLU, out=act)
+            K.linear(act, lw.wd, self._resid_epi(), out=x, resid=x)
+            self._allreduce(x)
+        last = self.plast[:R]
+        K.rmsnorm(x, w.final_norm, cfg.norm_eps, rows_index=last_rows, out=last)
+        logits = self.plogits[:R]
+        K.linear(last, w.lm_head, K.EPI_F32, out=logits)
+        first = self.pfirst[:R]
+        K.argmax(logits, out=first)
+        if push:
+            if timing:
+                self._compute_end.record(main)
+            main.wait_event(push_events[-1])  # KV fully landed before we report done
+            if push_stats is not None:
+                self._push_timing = (timing, push_stats)
+        return first
+
+    def finish_push_stats(self):
+        """Resolve push timings after the prefill's events completed."""
+        if not getattr(self, "_push_timing", None):
+            return None
+        timing, st = self._push_timing
+        st.layer_ms = [a.elapsed_time(b) for a, b in timing]
+        st.total_ms = timing[0][0].elapsed_time(timing[-1][1])
+        st.tail_ms = max(0.0, self._compute_end.elapsed_time(timing[-1][1]))
+        self._push_timing = None
+        return st
+
+    @staticmethod
+    def pack_meta(lens: list[int]) -> torch.Tensor:
+        """Host int32 [positions | cu_seqlens | last_rows] for ``prefill``."""
+        pos, cu, last = [], [0], []
+        for n in lens:
+            pos.extend(range(n))
+            cu.append(cu[-1] + n)
+            last.append(cu[-1] - 1)
+        return torch.tensor(pos + cu + last, dtype=torch.int32)
+
+    # ------------------------------------------------------------- decode
+    def decode_graph(self, B: int, max_ctx: int, ring: int) -> "DecodeGraph":
+        np_ = (max_ctx + self.partition - 1) // self.partition
+        key = (B, np_, ring)
+        g = self.graphs.get(key)
+        if g is None:
+            g = DecodeGraph(self, B, np_ * self.partition, ring)
+            self.graphs[key] = g
+        return g
+
+
+class DecodeGraph:
+    """Static buffers + captured CUDA graph of one decode iteration at batch B."""
+
+    def __init__(self, runner: ModelRunner, B: int, max_ctx: int, ring: int):
+        self.r = runner
+        self.B = B
+        self.max_ctx = max_ctx
+        self.ring = ring
+        cfg, dev = runner.cfg, runner.dev
+        kv = runner.kv
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.cur_tok = torch.zeros(B, **i32)
+        self.ctx = torch.zeros(B, **i32)
+        self.step = torch.zeros(B, **i32)
+        self.out_ring = torch.zeros(B, ring, **i32)
+        self.tables = torch.zeros(B, kv.max_blocks_per_seq, **i32)
+        self.pos = torch.zeros(B, **i32)
+        self.slots = torch.zeros(B, **i32)
+        self.attn_len = torch.zeros(B, **i32)
+        self.next_tok = torch.zeros(B, **i32)
+        d = cfg.d_model
+        self.x = torch.zeros(B, d, dtype=torch.float32, device=dev)
+        self.h = torch.zeros(B, d, dtype=torch.bfloat16, device=dev)
+        self.qkv = torch.zeros(B, runner.qkv_cols, dtype=torch.bfloat16, device=dev)
+        self.attn = torch.zeros(B, runner.hq * runner.dh, dtype=torch.bfloat16, device=dev)
+        self.act = torch.zeros(B, runner.ffn, dtype=torch.bfloat16, device=dev)
+        self.logits = torch.zeros(B, cfg.vocab, dtype=torch.float32, device=dev)
+        wsb = K.attn_decode_workspace_bytes(B, runner.hq, max_ctx, runner.partition, runner.dh)
+        self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+        self.graph = None
+
+    def _step_body(self):
+        r, cfg, w, kv = self.r, self.r.cfg, self.r.w, self.r.kv
+        B = self.B
+        K.decode_prepare(self.ctx, self.tables, kv.block_size, B, self.pos, self.slots,
+                         self.attn_len)
+        K.embed(self.cur_tok, w.embed, out=self.x)
+        for li, lw in enumerate(w.layers):
+            K.rmsnorm(self.x, lw.attn_norm, cfg.norm_eps, out=self.h)
+            K.linear(self.h, lw.wqkv, K.EPI_BF16, out=self.qkv)
+            K.rope_kv_write(self.qkv, self.pos, r.hq, r.hkv, r.dh, cfg.rope_theta,
+                            kv.k_layer_ptr(li), kv.v_layer_ptr(li), self.slots, kv.block_size)
+            K.attn_decode(self.qkv, kv.k_layer_ptr(li), kv.v_layer_ptr(li), self.tables,
+                          self.attn_len, B, r.hq, r.hkv, r.dh, kv.block_size, r.scale,
+                          self.max_ctx, r.partition, self.ws, out=self.attn)
+            K.linear(self.attn, lw.wo, r._resid_epi(), out=self.x, resid=self.x)
+            r._allreduce(self.x)
+            K.rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, out=self.h)
+            K.linear(self.h, lw.wgu, K.EPI_SWIGLU, out=self.act)
+            K.linear(self.act, lw.wd, r._resid_epi(), out=self.x, resid=self.x)
+            r._allreduce(self.x)
+        K.rmsnorm(self.x, w.final_norm, cfg.norm_eps, out=self.h)
+        K.linear(self.h, w.lm_head, K.EPI_F32, out=self.logits)
+        K.argmax(self.logits, out=self.next_tok)
+        K.decode_advance(self.next_tok, self.cur_tok, self.ctx, self.step, self.out_ring, B)
+
+    def load(self, seqs: list[int], cur_tok, ctx, steps=None):
+        """Bind batch rows to KV sequence slots and their state (host lists
+        or device tensors).  Called when the batch composition changes."""
+        kv = self.r.kv
+        idx = torch.tensor(seqs, dtype=torch.long, device=self.r.dev)
+        torch.index_select(kv.tables(), 0, idx, out=self.tables)
+        self.cur_tok.copy_(torch.as_tensor(cur_tok, dtype=torch.int32), non_blocking=True)
+        self.ctx.copy_(torch.as_tensor(ctx, dtype=torch.int32), non_blocking=True)
+        if steps is None:
+            self.step.zero_()
+        else:
+            self.step.copy_(torch.as_tensor(steps, dtype=torch.int32), non_blocking=True)
+
+    def capture(self):
+        s = torch.cuda.Stream(device=self.r.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        # snapshot state: a warm-up step mutates ctx/step/cur_tok/out_ring/KV
+        saved = [t.clone() for t in (self.cur_tok, self.ctx, self.step)]
+        with torch.cuda.stream(s):
+            self._step_body()  # warm-up (lazy attrs, workspace) outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        for t, v in zip((self.cur_tok, self.ctx, self.step), saved):
+            t.copy_(v)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step_body()
+        self.graph = g
+
+    def replay(self):
+        if self.graph is None:
+            self._step_body()
+        else:
+            self.graph.replay()

@@ -104,8 +104,28 @@ def check(status: int, what: str = "") -> None:
     raise NativeError(msg)
 
 
+# kernels launched per successful call (for the bench's gpu_launches claim)
+LAUNCH_MULT = {
+    "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
+    "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
+    "swb_attn_prefill": 1, "swb_attn_decode": 2, "swb_decode_prepare": 1,
+    "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
+    "swb_block_free": 1,
+}
+_launches = [0]
+
+
+def launch_count() -> int:
+    return _launches[0]
+
+
+def add_launches(n: int) -> None:
+    _launches[0] += n
+
+
 def call(name: str, *args) -> None:
     check(getattr(lib, name)(*args), name)
+    _launches[0] += LAUNCH_MULT.get(name, 0)
 
 
 def exported_symbols() -> list[str]:

@@ -248,7 +248,12 @@ constexpr int DA_D = 128;
 constexpr int DA_MAXG = 8;
 constexpr int DA_WARPS = 4;
 
-// grid (B, Hkv, NP); 128 threads
+// grid (B, Hkv, NP); 128 threads.  The CTA first issues cp.async for its
+// whole partition (K and V rows of `part` tokens, 256 B each, gathered
+// through the block table) so every byte it needs is in flight at once, then
+// computes scores (half-warp per token, shuffle-reduced dot products against
+// the G query heads of the group), the partition softmax (warp shuffles) and
+// P.V (lane owns 4 of the 128 dims), all from shared memory.
 __global__ void __launch_bounds__(DA_WARPS * 32)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                        const __nv_bfloat16* __restrict__ kpool,
@@ -256,7 +261,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
                        const int32_t* __restrict__ tables, int max_blocks,
                        const int32_t* __restrict__ ctx_lens, int H, int Hkv, int bs,
                        float scale_log2, int part, float* __restrict__ ws) {
-  extern __shared__ float dsm[];
+  extern __shared__ __align__(16) uint8_t dsm_raw[];
   const int b = blockIdx.x, kh = blockIdx.y, p = blockIdx.z;
   const int NP = gridDim.z;
   const int G = H / Hkv;
@@ -264,13 +269,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
   const int t0 = p * part;
   const int t1 = min(ctx, t0 + part);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* sq = dsm;                      // [G][128]
-  float* ss = sq + G * DA_D;            // [G][part]
-  float* sacc = ss + G * part;          // [WARPS][G][128]
-  float* sstat = sacc + DA_WARPS * G * DA_D;  // [G][2]
-  // workspace layout: [B][H][NP] x {o[128], m, l}
   auto wsp = [&](int gh) { return ws + (((size_t)b * H + gh) * NP + p) * (DA_D + 2); };
-
   if (t0 >= t1) {
     if (threadIdx.x < G) {
       float* w = wsp(kh * G + threadIdx.x);
@@ -279,39 +278,54 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
     }
     return;
   }
+  const int ntok = t1 - t0;
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(dsm_raw);      // [part][128]
+  __nv_bfloat16* sv = sk + (size_t)part * DA_D;                        // [part][128]
+  float* sq = reinterpret_cast<float*>(sv + (size_t)part * DA_D);      // [G][128]
+  float* ss = sq + G * DA_D;                                           // [G][part]
+  float* sacc = ss + G * part;                                         // [WARPS][G][128]
+  float* sstat = sacc + DA_WARPS * G * DA_D;                           // [G][2]
+
+  // ---- issue every K/V load of the partition (16 B chunks)
+  const int32_t* trow = tables + (size_t)b * max_blocks;
+  const int chunks = ntok * 16;
+  for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
+    const int tt = c >> 4, ch = c & 15;
+    const int tok = t0 + tt;
+    const int blk = __ldg(trow + tok / bs);
+    const size_t g = (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D + ch * 8;
+    cp_async16(smem_u32(sk + tt * DA_D + ch * 8), kpool + g, true);
+    cp_async16(smem_u32(sv + tt * DA_D + ch * 8), vpool + g, true);
+  }
+  cp_async_commit();
   for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
     const int gi = i / DA_D, d = i % DA_D;
     sq[i] = __bfloat162float(qkv[(size_t)b * rs + (kh * G + gi) * DA_D + d]) * scale_log2;
   }
+  cp_async_wait<0>();
   __syncthreads();
 
-  const int32_t* trow = tables + (size_t)b * max_blocks;
-  const int ntok = t1 - t0;
-  // ---- scores: half-warp per token, 8 x 16 B per lane
+  // ---- scores: half-warp per token
   {
     const int half = lane >> 4, hl = lane & 15;
     for (int tb = warp * 2; tb < ntok; tb += DA_WARPS * 2) {  // warp-uniform
       const int tt = tb + half;
       const bool valid = tt < ntok;
       float kf[8];
-      if (valid) {
-        const int tok = t0 + tt;
-        const int blk = trow[tok / bs];
-        const uint4 kv = ld_nc_v4(kpool + (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D +
-                                  hl * 8);
+      const uint4 kv = *reinterpret_cast<const uint4*>(sk + (valid ? tt : 0) * DA_D + hl * 8);
+      {
         float2 a = bf2_to_f2(kv.x), c = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
                f = bf2_to_f2(kv.w);
         kf[0] = a.x; kf[1] = a.y; kf[2] = c.x; kf[3] = c.y;
         kf[4] = e.x; kf[5] = e.y; kf[6] = f.x; kf[7] = f.y;
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) kf[j] = 0.f;
       }
       for (int gi = 0; gi < G; ++gi) {
-        const float* q = sq + gi * DA_D + hl * 8;
-        float d = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) d = fmaf(q[j], kf[j], d);
+        const float4 q0 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8);
+        const float4 q1 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8 + 4);
+        float d = q0.x * kf[0];
+        d = fmaf(q0.y, kf[1], d); d = fmaf(q0.z, kf[2], d); d = fmaf(q0.w, kf[3], d);
+        d = fmaf(q1.x, kf[4], d); d = fmaf(q1.y, kf[5], d); d = fmaf(q1.z, kf[6], d);
+        d = fmaf(q1.w, kf[7], d);
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
         if (hl == 0 && valid) ss[gi * part + tt] = d;
@@ -319,7 +333,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
     }
   }
   __syncthreads();
-  // ---- softmax stats per head (warp gi%WARPS handles head gi)
+  // ---- softmax stats per head
   for (int gi = warp; gi < G; gi += DA_WARPS) {
     float m = -INFINITY;
     for (int i = lane; i < ntok; i += 32) m = fmaxf(m, ss[gi * part + i]);
@@ -337,16 +351,12 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
     }
   }
   __syncthreads();
-  // ---- P V: warp per token stripe, lane owns dh [4*lane, 4*lane+4)
+  // ---- P V from smem: warp per token stripe, lane owns dims [4*lane, 4*lane+4)
   float acc[DA_MAXG][4];
 #pragma unroll
   for (int gi = 0; gi < DA_MAXG; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
   for (int tt = warp; tt < ntok; tt += DA_WARPS) {
-    const int tok = t0 + tt;
-    const int blk = trow[tok / bs];
-    const __nv_bfloat16* vp =
-        vpool + (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D + lane * 4;
-    const uint2 vv = *reinterpret_cast<const uint2*>(vp);
+    const uint2 vv = *reinterpret_cast<const uint2*>(sv + tt * DA_D + lane * 4);
     const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
 #pragma unroll
     for (int gi = 0; gi < DA_MAXG; ++gi) {
@@ -450,12 +460,17 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, const void* k_la
               "swb_attn_decode: bad sizes");
   const int G = H / Hkv;
   const int NP = (max_ctx + partition - 1) / partition;
-  const size_t smem = sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
+  const size_t smem = (size_t)partition * DA_D * 2 * 2 +
+                      sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
                                        (size_t)DA_WARPS * G * DA_D + 2 * G);
   SWB_REQUIRE(smem <= 200 * 1024, "swb_attn_decode: partition too large");
-  if (smem > 48 * 1024) {
+  static bool attr[64] = {false};
+  int dev = 0;
+  SWB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr[dev]) {
     SWB_CUDA(cudaFuncSetAttribute(attn_decode_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr[dev] = true;
   }
   dim3 grid(B, Hkv, NP);
   attn_decode_kernel<<<grid, DA_WARPS * 32, smem, (cudaStream_t)stream>>>(

@@ -26,6 +26,7 @@ from dataclasses import dataclass, field
 
 import torch
 
+from . import _abi
 from . import kernels as K
 from .kvcache import KVCacheManager
 from .model import Weights
@@ -51,7 +52,7 @@ class PushStats:
 
 class ModelRunner:
     def __init__(self, weights: Weights, kv: KVCacheManager | None = None, tp_group=None,
-                 decode_partition: int = 256, push_ctas: int = 16):
+                 decode_partition: int = 128, push_ctas: int = 16):
         self.w = weights
         self.cfg = cfg = weights.cfg
         self.tp = weights.tp
@@ -295,8 +296,11 @@ class DecodeGraph:
         for t, v in zip((self.cur_tok, self.ctx, self.step), saved):
             t.copy_(v)
         g = torch.cuda.CUDAGraph()
+        n0 = _abi.launch_count()
         with torch.cuda.graph(g):
             self._step_body()
+        self.launches_per_step = _abi.launch_count() - n0
+        _abi.add_launches(-self.launches_per_step)  # capture launches nothing
         self.graph = g
 
     def replay(self):
@@ -304,3 +308,4 @@ class DecodeGraph:
             self._step_body()
         else:
             self.graph.replay()
+            _abi.add_launches(self.launches_per_step)

@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(128)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                         const int32_t* __restrict__ cu, int tiles_per_seq, int H,
                         int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t sm[];
   const int seq = blockIdx.x / tiles_per_seq;
   // heavy (late) tiles first
@@ -261,6 +263,8 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
                        const int32_t* __restrict__ tables, int max_blocks,
                        const int32_t* __restrict__ ctx_lens, int H, int Hkv, int bs,
                        float scale_log2, int part, float* __restrict__ ws) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t dsm_raw[];
   const int b = blockIdx.x, kh = blockIdx.y, p = blockIdx.z;
   const int NP = gridDim.z;
@@ -392,6 +396,8 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
 // merge partitions: grid (B, H), 128 threads (one per dh element)
 __global__ void attn_decode_merge_kernel(const float* __restrict__ ws, int H, int NP,
                                          __nv_bfloat16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const float* base = ws + ((size_t)b * H + h) * NP * (DA_D + 2);
   float m = -INFINITY;
@@ -431,9 +437,14 @@ extern "C" int swb_attn_prefill(const void* qkv, int row_stride, const int32_t* 
   }
   const int tiles = (max_seqlen + PA_BQ - 1) / PA_BQ;
   dim3 grid(num_seqs * tiles, H);
-  attn_prefill_kernel<<<grid, 128, PA_SMEM, (cudaStream_t)stream>>>(
+  {
+    const cudaError_t le_ = launch(attn_prefill_kernel, dim3(grid), dim3(128), PA_SMEM, (cudaStream_t)stream,
+        
       reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride, cu_seqlens, tiles, H, Hkv,
       scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(out));
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch attn_prefill_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("attn_prefill_kernel");
 }
 
@@ -473,15 +484,25 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, const void* k_la
     attr[dev] = true;
   }
   dim3 grid(B, Hkv, NP);
-  attn_decode_kernel<<<grid, DA_WARPS * 32, smem, (cudaStream_t)stream>>>(
+  {
+    const cudaError_t le_ = launch(attn_decode_kernel, dim3(grid), dim3(DA_WARPS * 32), smem, (cudaStream_t)stream,
+        
       reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
       reinterpret_cast<const __nv_bfloat16*>(k_layer),
       reinterpret_cast<const __nv_bfloat16*>(v_layer), block_tables, max_blocks, ctx_lens,
       H, Hkv, block_size, scale * 1.4426950408889634f, partition,
       reinterpret_cast<float*>(workspace));
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_kernel: %s", cudaGetErrorString(le_));
+  }
   const int st = swb_check_launch("attn_decode_kernel");
   if (st != SWB_OK) return st;
-  attn_decode_merge_kernel<<<dim3(B, H), DA_D, 0, (cudaStream_t)stream>>>(
+  {
+    const cudaError_t le_ = launch(attn_decode_merge_kernel, dim3(B, H), dim3(DA_D), 0,
+                                   (cudaStream_t)stream,
       reinterpret_cast<const float*>(workspace), H, NP, reinterpret_cast<__nv_bfloat16*>(out));
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_merge_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("attn_decode_merge_kernel");
 }

@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // A (activations) is produced by the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -259,6 +261,11 @@ extern "C" int swb_gemm_bf16(const void* a, const void* w, void* out,
   }
   GemmArgs args{out, reinterpret_cast<const float*>(resid), M, N, K, epilogue};
   dim3 grid((N + GN - 1) / GN, (M + GM - 1) / GM);
-  gemm_bf16_tcgen05<<<grid, 128, G_SMEM_BYTES, (cudaStream_t)stream>>>(ta, tw, args);
+  {
+    const cudaError_t le_ = launch(gemm_bf16_tcgen05, dim3(grid), dim3(128), G_SMEM_BYTES, (cudaStream_t)stream,
+        ta, tw, args);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch gemm_bf16_tcgen05: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("gemm_bf16_tcgen05");
 }

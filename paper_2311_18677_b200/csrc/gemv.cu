@@ -7,12 +7,14 @@
 // 2 CTAs per SM; in each CTA one producer lane streams the weight rows of
 // its work items into a 6-stage shared-memory ring with 1-D bulk async copies
 // (cp.async.bulk -> mbarrier complete_tx, L2 evict-first), so ~192 KB per SM
-// are in flight independent of register pressure; eight consumer warps each
-// own one of the item's 8 weight rows, read their 2 KB slice of every stage
-// with 128-bit shared loads, multiply by x (L1-resident, <= 16 rows) in fp32
-// and reduce with warp shuffles once per item.  Epilogues: bf16 / fp32 store,
-// fp32 residual add (in place), SwiGLU over gate/up rows interleaved in
-// 128-row groups (warps 0-3 gate, 4-7 up of the same 4 outputs).
+// are in flight independent of register pressure.  A work item is 4 weight
+// rows (small items keep the 148-SM grid balanced at ~7 items per SM for a
+// 4096-row matrix); eight consumer warps each take one row's K half, read
+// their 2 KB slice of every 16 KB stage with 128-bit shared loads, multiply
+// by x (L1-resident, <= 16 rows) in fp32, shuffle-reduce once per item and
+// combine halves through smem.  Epilogues: bf16 / fp32 store, fp32 residual
+// add (in place), SwiGLU over gate/up rows interleaved in 128-row groups
+// (slots 0,1 gate and 2,3 up of the same 2 outputs).
 //
 // Replaces PerfModel.token_iter_time (reference perf.py:125-132) for the
 // linear layers of a token-phase iteration.
@@ -20,13 +22,14 @@
 
 namespace swb {
 
-constexpr int TV_ROWS = 8;                    // weight rows per item = consumer warps
-constexpr int TV_KC = 1024;                   // K elements per stage per row (2 KB)
+constexpr int TV_ROWS = 4;                    // weight rows per work item
+constexpr int TV_WARPS = 8;                   // consumer warps: 2 per row (K halves)
+constexpr int TV_KC = 2048;                   // K elements per stage per row (4 KB)
 constexpr int TV_STAGES = 6;
 constexpr int TV_ROW_BYTES = TV_KC * 2;
 constexpr int TV_STAGE_BYTES = TV_ROWS * TV_ROW_BYTES;  // 16 KB
-constexpr int TV_THREADS = (TV_ROWS + 1) * 32;
-constexpr int TV_SMEM = TV_STAGES * TV_STAGE_BYTES + 2 * TV_STAGES * 8 + 4 * 16 * 4 + 128;
+constexpr int TV_THREADS = (TV_WARPS + 1) * 32;
+constexpr int TV_SMEM = TV_STAGES * TV_STAGE_BYTES + 2 * TV_STAGES * 8 + 2 * TV_WARPS * 16 * 4 + 128;
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
@@ -42,36 +45,39 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-// weight row of slot j (0..7) of work item `item`
+// weight row of slot j (0..3) of work item `item`.  Plain: rows 4i..4i+3.
+// SwiGLU: outputs 2i, 2i+1 -> gate rows g, g+1 (slots 0,1), up rows g+128,
+// g+129 (slots 2,3), with gate/up interleaved in 128-row groups.
 __device__ __forceinline__ int item_row(int item, int j, bool swiglu) {
   if (!swiglu) return item * TV_ROWS + j;
-  const int o = item * 4 + (j & 3);               // output feature
-  return (o >> 7) * 256 + (o & 127) + (j >= 4 ? 128 : 0);
+  const int o = item * 2 + (j & 1);
+  return (o >> 7) * 256 + (o & 127) + (j >= 2 ? 128 : 0);
 }
 
 template <int MB>
-__global__ void __launch_bounds__(TV_THREADS, 2)
+__global__ void __launch_bounds__(TV_THREADS, 1)
     gemv_bulk_kernel(const __nv_bfloat16* __restrict__ x,
                      const __nv_bfloat16* __restrict__ W, void* out, const float* resid,
                      int M, int N, int K, int epi, int n_items) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TV_STAGES * TV_STAGE_BYTES);
   uint64_t* empty = full + TV_STAGES;
-  float* xchg = reinterpret_cast<float*>(empty + TV_STAGES);  // [4][16] gate/up exchange
+  float* part = reinterpret_cast<float*>(empty + TV_STAGES);  // [2][WARPS][16]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool swiglu = epi == SWB_EPI_SWIGLU;
   const int nk = (K + TV_KC - 1) / TV_KC;
 
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (int s = 0; s < TV_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TV_ROWS);
+      mbar_init(&empty[s], TV_WARPS);
     }
     fence_barrier_init();
   }
   __syncthreads();
 
-  if (warp == TV_ROWS) {
+  if (warp == TV_WARPS) {
     // ------------------------------------------------ producer (1 lane)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -98,10 +104,14 @@ __global__ void __launch_bounds__(TV_THREADS, 2)
     return;
   }
 
-  // -------------------------------------------------- consumers (8 warps)
-  int it = 0;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int row = item_row(item, warp, swiglu);
+  // ------------------------------ consumers: warp w -> row w&3, K half w>>2
+  // The producer above streams static weights before the previous kernel has
+  // finished (PDL); consumers read x / write out only after it has.
+  pdl_wait();
+  const int slot = warp & 3, khalf = warp >> 2;
+  int it = 0, parity = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x, parity ^= 1) {
+    const int row = item_row(item, slot, swiglu);
     const bool valid = row < N;
     float acc[MB];
 #pragma unroll
@@ -110,14 +120,14 @@ __global__ void __launch_bounds__(TV_THREADS, 2)
       const int s = it % TV_STAGES;
       mbar_wait(&full[s], (it / TV_STAGES) & 1);
       if (valid) {
-        const __nv_bfloat16* wr =
-            reinterpret_cast<const __nv_bfloat16*>(smem + s * TV_STAGE_BYTES + warp * TV_ROW_BYTES);
+        const __nv_bfloat16* wr = reinterpret_cast<const __nv_bfloat16*>(
+            smem + s * TV_STAGE_BYTES + slot * TV_ROW_BYTES) + khalf * (TV_KC / 2);
         uint4 wv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) wv[j] = *reinterpret_cast<const uint4*>(wr + j * 256 + lane * 8);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int k = kc * TV_KC + j * 256 + lane * 8;
+          const int k = kc * TV_KC + khalf * (TV_KC / 2) + j * 256 + lane * 8;
           if (k < K) {
             const float2 w0 = bf2_to_f2(wv[j].x), w1 = bf2_to_f2(wv[j].y),
                          w2 = bf2_to_f2(wv[j].z), w3 = bf2_to_f2(wv[j].w);
@@ -140,42 +150,40 @@ __global__ void __launch_bounds__(TV_THREADS, 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+    // per-warp partial sums -> smem (double-buffered by item parity), then
+    // warp 0 combines the two K halves of each row and applies the epilogue
+    float* pb = part + parity * TV_WARPS * 16;
 #pragma unroll
-    for (int m = 0; m < MB; ++m) acc[m] = warp_sum(acc[m]);
-
-    if (swiglu) {
-      // warps 4..7 hand their (up) sums to warps 0..3 (gate) of the same output
-      asm volatile("bar.sync 1, %0;" ::"n"(TV_ROWS * 32));
-      if (warp >= 4 && lane == 0) {
-#pragma unroll
-        for (int m = 0; m < MB; ++m) xchg[(warp - 4) * 16 + m] = acc[m];
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(TV_ROWS * 32));
-      if (warp < 4) {
-        const int o = item * 4 + warp;
-        const int nout = N >> 1;
-#pragma unroll
-        for (int m = 0; m < MB; ++m) {
-          if (m >= M) break;
-          if (lane == m && o < nout) {
-            const float g = acc[m], u = xchg[warp * 16 + m];
-            reinterpret_cast<__nv_bfloat16*>(out)[(size_t)m * nout + o] =
-                __float2bfloat16(g / (1.f + __expf(-g)) * u);
-          }
+    for (int m = 0; m < MB; ++m) {
+      const float v = warp_sum(acc[m]);
+      if (lane == 0) pb[warp * 16 + m] = v;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
+    if (warp == 0) {
+      if (swiglu) {
+        // lane = m*2 + o : outputs 2*item + o
+        const int m = lane >> 1, o = lane & 1;
+        const int nout = N >> 1, oi = item * 2 + o;
+        if (m < M && oi < nout) {
+          const float g = pb[o * 16 + m] + pb[(o + 4) * 16 + m];
+          const float u = pb[(o + 2) * 16 + m] + pb[(o + 6) * 16 + m];
+          reinterpret_cast<__nv_bfloat16*>(out)[(size_t)m * nout + oi] =
+              __float2bfloat16(g / (1.f + __expf(-g)) * u);
         }
-      }
-    } else if (valid) {
-#pragma unroll
-      for (int m = 0; m < MB; ++m) {
-        if (m >= M) break;
-        if (lane != m) continue;
-        const size_t idx = (size_t)m * N + row;
-        if (epi == SWB_EPI_BF16)
-          reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(acc[m]);
-        else if (epi == SWB_EPI_F32)
-          reinterpret_cast<float*>(out)[idx] = acc[m];
-        else
-          reinterpret_cast<float*>(out)[idx] = resid[idx] + acc[m];
+      } else {
+        for (int e = lane; e < M * TV_ROWS; e += 32) {
+          const int m = e / TV_ROWS, j = e % TV_ROWS;
+          const int r = item_row(item, j, false);
+          if (r >= N) continue;
+          const float v = pb[j * 16 + m] + pb[(j + 4) * 16 + m];
+          const size_t idx = (size_t)m * N + r;
+          if (epi == SWB_EPI_BF16)
+            reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(v);
+          else if (epi == SWB_EPI_F32)
+            reinterpret_cast<float*>(out)[idx] = v;
+          else
+            reinterpret_cast<float*>(out)[idx] = resid[idx] + v;
+        }
       }
     }
   }
@@ -193,8 +201,13 @@ static int launch_gemv(const __nv_bfloat16* x, const __nv_bfloat16* w, void* out
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, TV_SMEM));
     attr[dev] = true;
   }
-  const int grid = min(items, 2 * kNumSMs);
-  gemv_bulk_kernel<MB><<<grid, TV_THREADS, TV_SMEM, s>>>(x, w, out, r, M, N, K, epi, items);
+  const int grid = min(items, kNumSMs);  // 1 CTA/SM: leaves room for the next kernel
+  {
+    const cudaError_t le_ = launch(gemv_bulk_kernel<MB>, dim3(grid), dim3(TV_THREADS), TV_SMEM, s,
+        x, w, out, r, M, N, K, epi, items);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("gemv_bulk_kernel");
 }
 
@@ -215,7 +228,7 @@ extern "C" int swb_gemv_bf16(const void* x, const void* w, void* out,
   SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid, "swb_gemv_bf16: resid needed");
   SWB_REQUIRE((((uintptr_t)x | (uintptr_t)w) & 15) == 0,
               "swb_gemv_bf16: pointers must be 16-byte aligned");
-  const int items = (N + TV_ROWS - 1) / TV_ROWS;  // 8 rows (or 4 SwiGLU outputs) per item
+  const int items = (N + TV_ROWS - 1) / TV_ROWS;  // 4 rows (or 2 SwiGLU outputs) per item
   auto xs = reinterpret_cast<const __nv_bfloat16*>(x);
   auto ws = reinterpret_cast<const __nv_bfloat16*>(w);
   auto rs = reinterpret_cast<const float*>(resid);

@@ -38,6 +38,8 @@ struct IpcBlob {
 __global__ void __launch_bounds__(1024)
     block_alloc_kernel(uint32_t* __restrict__ bitmap, int num_blocks,
                        int32_t* __restrict__ table_row, int n) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int warp_tot[32];
   const int nwords = (num_blocks + 31) >> 5;
   const int per = (nwords + blockDim.x - 1) / blockDim.x;
@@ -88,6 +90,8 @@ __global__ void __launch_bounds__(1024)
 
 __global__ void block_free_kernel(uint32_t* __restrict__ bitmap,
                                   int32_t* __restrict__ table_row, int n) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int b = table_row[i];
@@ -187,8 +191,13 @@ extern "C" int swb_block_alloc(swb_kv_pool* p, int seq, int n, uintptr_t stream)
                          p->info.free_blocks);
   if (n == 0) return SWB_OK;
   p->info.free_blocks -= n;
-  block_alloc_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(
+  {
+    const cudaError_t le_ = launch(block_alloc_kernel, dim3(1), dim3(1024), 0, (cudaStream_t)stream,
+        
       p->bitmap, p->info.num_blocks, p->tables + (size_t)seq * p->info.max_blocks_per_seq, n);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch block_alloc_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("block_alloc_kernel");
 }
 
@@ -199,8 +208,13 @@ extern "C" int swb_block_free(swb_kv_pool* p, int seq, int n, uintptr_t stream) 
   SWB_REQUIRE(n >= 0 && n <= p->info.max_blocks_per_seq, "swb_block_free: bad n");
   if (n == 0) return SWB_OK;
   p->info.free_blocks += n;
-  block_free_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+  {
+    const cudaError_t le_ = launch(block_free_kernel, dim3((n + 255) / 256), dim3(256), 0, (cudaStream_t)stream,
+        
       p->bitmap, p->tables + (size_t)seq * p->info.max_blocks_per_seq, n);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch block_free_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("block_free_kernel");
 }
 

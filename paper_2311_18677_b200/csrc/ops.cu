@@ -18,6 +18,8 @@ namespace swb {
 __global__ void embed_kernel(const int32_t* __restrict__ tokens,
                              const __nv_bfloat16* __restrict__ table,
                              float* __restrict__ x, int d) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int tok = tokens[r];
   const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)tok * d);
@@ -36,6 +38,8 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x,
                                const int32_t* __restrict__ row_index,
                                const __nv_bfloat16* __restrict__ w,
                                __nv_bfloat16* __restrict__ out, int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * d);
@@ -69,6 +73,8 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x,
 // ----------------------------------------------------------------- argmax
 __global__ void argmax_kernel(const float* __restrict__ logits, int V,
                               int32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const float* row = logits + (size_t)blockIdx.x * V;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -118,6 +124,8 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int row_stride,
                                __nv_bfloat16* __restrict__ kpool,
                                __nv_bfloat16* __restrict__ vpool,
                                const int32_t* __restrict__ slots, int bs) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int half = dh >> 1;
   const int groups = half >> 2;  // 4 pairs per thread
@@ -169,35 +177,52 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int row_stride,
 }
 
 // ------------------------------------------------- KV pack-and-push (P2P)
-// Grid-stride over 16-byte chunks of (row, {k,v}, head, dh/8).  Reads are
-// local (the rotated qkv activations of one finished layer); writes land in
-// the destination pool's paged blocks, which may be a peer GPU's HBM mapped
-// through CUDA IPC: each warp emits 512 B of coalesced NVLink stores.
-__global__ void kv_push_kernel(const __nv_bfloat16* __restrict__ qkv, int rows,
-                               int row_stride, int k_col, int v_col, int Hkv,
-                               int dh, __nv_bfloat16* __restrict__ dk,
-                               __nv_bfloat16* __restrict__ dv,
-                               const int32_t* __restrict__ slots, int bs) {
-  const int cpr = dh >> 3;                  // chunks per head
-  const long per_row = (long)2 * Hkv * cpr;  // k and v
-  const long total = per_row * rows;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
-       i += (long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / per_row);
-    int rem = (int)(i - (long)r * per_row);
-    const int is_v = rem >= Hkv * cpr;
-    if (is_v) rem -= Hkv * cpr;
-    const int h = rem / cpr, c = rem % cpr;
-    const __nv_bfloat16* src =
-        qkv + (size_t)r * row_stride + (is_v ? v_col : k_col) + h * dh + c * 8;
+// One warp per (row, K-or-V) unit: the row's Hkv*dh bf16 are contiguous in
+// the source (the rotated qkv activations of one finished layer); lane l
+// moves 16-byte chunks l, l+32, ... .  Each lane first issues all of its
+// loads (up to 16 x 16 B in flight), then its stores, which land in the
+// destination pool's paged blocks — a peer GPU's HBM mapped through CUDA
+// IPC — as coalesced 256-byte NVLink writes per head.
+constexpr int PUSH_UNROLL = 16;
+__global__ void __launch_bounds__(256)
+    kv_push_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int row_stride,
+                   int k_col, int v_col, int Hkv, int dh, __nv_bfloat16* __restrict__ dk,
+                   __nv_bfloat16* __restrict__ dv, const int32_t* __restrict__ slots, int bs) {
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int cph = dh >> 3;                 // 16-byte chunks per head
+  const int chunks = Hkv * cph;            // per row, per K or V
+  for (int u = gw; u < rows * 2; u += nw) {
+    const int r = u >> 1, is_v = u & 1;
+    const __nv_bfloat16* src = qkv + (size_t)r * row_stride + (is_v ? v_col : k_col);
     const int slot = slots[r];
-    const int blk = slot / bs, off = slot % bs;
-    __nv_bfloat16* dst = (is_v ? dv : dk) + (((size_t)blk * Hkv + h) * bs + off) * dh + c * 8;
-    st_v4(dst, ld_v4(src));
+    const size_t dbase = (((size_t)(slot / bs) * Hkv) * bs + slot % bs) * dh;
+    __nv_bfloat16* dst = (is_v ? dv : dk) + dbase;
+    for (int c0 = 0; c0 < chunks; c0 += 32 * PUSH_UNROLL) {
+      uint4 v[PUSH_UNROLL];
+#pragma unroll
+      for (int j = 0; j < PUSH_UNROLL; ++j) {
+        const int c = c0 + j * 32 + lane;
+        if (c < chunks) v[j] = ld_nc_v4(src + c * 8);
+      }
+#pragma unroll
+      for (int j = 0; j < PUSH_UNROLL; ++j) {
+        const int c = c0 + j * 32 + lane;
+        if (c < chunks) {
+          const int h = c / cph, w = c % cph;
+          st_v4(dst + (size_t)h * bs * dh + w * 8, v[j]);
+        }
+      }
+    }
   }
 }
 
 __global__ void signal_kernel(uint32_t* flag, uint32_t value) {
+  pdl_trigger();
+  pdl_wait();
   __threadfence_system();
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value)
                : "memory");
@@ -210,6 +235,8 @@ __global__ void decode_prepare_kernel(const int32_t* __restrict__ ctx,
                                       int32_t* __restrict__ pos,
                                       int32_t* __restrict__ slots,
                                       int32_t* __restrict__ attn_len) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int c = ctx[b];
@@ -224,6 +251,8 @@ __global__ void decode_advance_kernel(const int32_t* __restrict__ next_tok,
                                       int32_t* __restrict__ step,
                                       int32_t* __restrict__ ring, int ring_len,
                                       int B) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const int t = next_tok[b];
@@ -236,6 +265,8 @@ __global__ void decode_advance_kernel(const int32_t* __restrict__ next_tok,
 
 __global__ void slots_from_table_kernel(const int32_t* table_row, int start,
                                         int n, int bs, int32_t* slots) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int p = start + i;
@@ -253,8 +284,13 @@ extern "C" int swb_embed(const int32_t* tokens, const void* table, float* x,
   SWB_REQUIRE(tokens && table && x, "swb_embed: null pointer");
   SWB_REQUIRE(rows >= 0 && d > 0 && d % 8 == 0, "swb_embed: bad shape");
   if (rows == 0) return SWB_OK;
-  embed_kernel<<<rows, 256, 0, STREAM>>>(
+  {
+    const cudaError_t le_ = launch(embed_kernel, dim3(rows), dim3(256), 0, STREAM,
+        
       tokens, reinterpret_cast<const __nv_bfloat16*>(table), x, d);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch embed_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("embed_kernel");
 }
 
@@ -263,9 +299,14 @@ extern "C" int swb_rmsnorm(const float* x, const int32_t* row_index, const void*
   SWB_REQUIRE(x && w && out, "swb_rmsnorm: null pointer");
   SWB_REQUIRE(rows >= 0 && d > 0 && d % 4 == 0, "swb_rmsnorm: bad shape");
   if (rows == 0) return SWB_OK;
-  rmsnorm_kernel<<<rows, 512, 0, STREAM>>>(
+  {
+    const cudaError_t le_ = launch(rmsnorm_kernel, dim3(rows), dim3(512), 0, STREAM,
+        
       x, row_index, reinterpret_cast<const __nv_bfloat16*>(w),
       reinterpret_cast<__nv_bfloat16*>(out), d, eps);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch rmsnorm_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("rmsnorm_kernel");
 }
 
@@ -274,7 +315,12 @@ extern "C" int swb_argmax(const float* logits, int rows, int V, int32_t* out,
   SWB_REQUIRE(logits && out, "swb_argmax: null pointer");
   SWB_REQUIRE(rows >= 0 && V > 0, "swb_argmax: bad shape");
   if (rows == 0) return SWB_OK;
-  argmax_kernel<<<rows, 1024, 0, STREAM>>>(logits, V, out);
+  {
+    const cudaError_t le_ = launch(argmax_kernel, dim3(rows), dim3(1024), 0, STREAM,
+        logits, V, out);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch argmax_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("argmax_kernel");
 }
 
@@ -292,10 +338,15 @@ extern "C" int swb_rope_kv_write(void* qkv, int rows, int row_stride,
   SWB_REQUIRE(!k_layer || (slots && block_size > 0), "swb_rope_kv_write: slots");
   SWB_REQUIRE(theta > 1.f, "swb_rope_kv_write: theta");
   if (rows == 0) return SWB_OK;
-  rope_kv_kernel<<<rows, 256, 0, STREAM>>>(
+  {
+    const cudaError_t le_ = launch(rope_kv_kernel, dim3(rows), dim3(256), 0, STREAM,
+        
       reinterpret_cast<__nv_bfloat16*>(qkv), row_stride, positions, H, Hkv, dh,
       log2f(theta), reinterpret_cast<__nv_bfloat16*>(k_layer),
       reinterpret_cast<__nv_bfloat16*>(v_layer), slots, block_size);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch rope_kv_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("rope_kv_kernel");
 }
 
@@ -311,20 +362,29 @@ extern "C" int swb_kv_push_layer(const void* qkv, int rows, int row_stride,
   SWB_REQUIRE(row_stride % 8 == 0 && k_col % 8 == 0 && v_col % 8 == 0,
               "swb_kv_push_layer: 16-byte alignment of rows/columns");
   if (rows == 0) return SWB_OK;
-  const long chunks = (long)rows * 2 * Hkv * (dh / 8);
-  int grid = num_ctas > 0 ? num_ctas : 32;
-  const long need = (chunks + 255) / 256;
-  if (need < grid) grid = (int)need;
-  kv_push_kernel<<<grid, 256, 0, STREAM>>>(
+  int grid = num_ctas > 0 ? num_ctas : 64;
+  const int need = (rows * 2 + 7) / 8;     // 8 warps per CTA, one (row, k|v) unit each
+  if (need < grid) grid = need;
+  {
+    const cudaError_t le_ = launch(kv_push_kernel, dim3(grid), dim3(256), 0, STREAM,
+        
       reinterpret_cast<const __nv_bfloat16*>(qkv), rows, row_stride, k_col, v_col,
       Hkv, dh, reinterpret_cast<__nv_bfloat16*>(dst_k_layer),
       reinterpret_cast<__nv_bfloat16*>(dst_v_layer), dst_slots, block_size);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch kv_push_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("kv_push_kernel");
 }
 
 extern "C" int swb_kv_signal(uint32_t* flag, uint32_t value, uintptr_t stream) {
   SWB_REQUIRE(flag, "swb_kv_signal: null flag");
-  signal_kernel<<<1, 1, 0, STREAM>>>(flag, value);
+  {
+    const cudaError_t le_ = launch(signal_kernel, dim3(1), dim3(1), 0, STREAM,
+        flag, value);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch signal_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("signal_kernel");
 }
 
@@ -353,8 +413,13 @@ extern "C" int swb_decode_prepare(const int32_t* ctx, const int32_t* block_table
   SWB_REQUIRE(ctx && block_tables && pos && slots && attn_len,
               "swb_decode_prepare: null pointer");
   SWB_REQUIRE(B > 0 && max_blocks > 0 && block_size > 0, "swb_decode_prepare: bad shape");
-  decode_prepare_kernel<<<(B + 127) / 128, 128, 0, STREAM>>>(
+  {
+    const cudaError_t le_ = launch(decode_prepare_kernel, dim3((B + 127) / 128), dim3(128), 0, STREAM,
+        
       ctx, block_tables, max_blocks, block_size, B, pos, slots, attn_len);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch decode_prepare_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("decode_prepare_kernel");
 }
 
@@ -364,8 +429,13 @@ extern "C" int swb_decode_advance(const int32_t* next_tok, int32_t* cur_tok,
   SWB_REQUIRE(next_tok && cur_tok && ctx && step && out_ring,
               "swb_decode_advance: null pointer");
   SWB_REQUIRE(B > 0 && ring > 0, "swb_decode_advance: bad shape");
-  decode_advance_kernel<<<(B + 127) / 128, 128, 0, STREAM>>>(next_tok, cur_tok, ctx,
+  {
+    const cudaError_t le_ = launch(decode_advance_kernel, dim3((B + 127) / 128), dim3(128), 0, STREAM,
+        next_tok, cur_tok, ctx,
                                                              step, out_ring, ring, B);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch decode_advance_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("decode_advance_kernel");
 }
 
@@ -374,7 +444,12 @@ extern "C" int swb_slots_from_table(const int32_t* table_row, int start, int n,
   SWB_REQUIRE(table_row && slots, "swb_slots_from_table: null pointer");
   SWB_REQUIRE(start >= 0 && n >= 0 && block_size > 0, "swb_slots_from_table: bad args");
   if (n == 0) return SWB_OK;
-  slots_from_table_kernel<<<(n + 255) / 256, 256, 0, STREAM>>>(table_row, start, n,
+  {
+    const cudaError_t le_ = launch(slots_from_table_kernel, dim3((n + 255) / 256), dim3(256), 0, STREAM,
+        table_row, start, n,
                                                                block_size, slots);
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch slots_from_table_kernel: %s", cudaGetErrorString(le_));
+  }
   return swb_check_launch("slots_from_table_kernel");
 }

@@ -52,7 +52,7 @@ class PushStats:
 
 class ModelRunner:
     def __init__(self, weights: Weights, kv: KVCacheManager | None = None, tp_group=None,
-                 decode_partition: int = 128, push_ctas: int = 16):
+                 decode_partition: int = 128, push_ctas: int = 64):
         self.w = weights
         self.cfg = cfg = weights.cfg
         self.tp = weights.tp

@@ -1,0 +1,329 @@
+"""Splitwise serving across GPUs: prompt machines and token machines as
+separate processes (one per GPU), KV pushed layer by layer over NVLink.
+
+Roles (reference: Machine home roles, machine.py:88-114; hand-off,
+engine.py:250-301):
+  * ``PromptServer`` (prompt machine): batches queued prompts with the
+    reference's prompt rule (PromptWorker.form_batch: FCFS, <= 2048 tokens,
+    head always admitted), runs the prefill and, for every layer, pushes that
+    layer's K/V straight into the paged blocks the token machine reserved —
+    P2P stores through the token pool's CUDA-IPC mapping, on a side stream
+    that overlaps the next layer's compute.  When the last layer has landed it
+    hands the request over (request id, KV sequence slot, prompt length,
+    first token) on the control channel.
+  * ``TokenServer`` (token machine): reserves each routed request's final
+    context in its device block pool at arrival (both machines are chosen at
+    arrival, cluster.py:153-160), admits handed-over token tasks with the
+    reference's token rule (TokenWorker.form_batch: slots, memory, FCFS), and
+    runs one CUDA-graph decode iteration per scheduler iteration, streaming
+    every generated token to the host.
+
+The control channel is a gloo process group (tiny int32 messages); the KV
+bytes never touch the host.  ``run_split_bench`` is bench.py's N >= 2 leg.
+"""
+
+from __future__ import annotations
+
+import os
+import statistics
+import time
+
+import torch
+import torch.distributed as dist
+
+from . import _abi
+from . import kernels as K
+from .kvcache import KVCacheManager, blocks_for
+from .model import get_config, init_weights
+from .perf import PerfModel
+from .runner import ModelRunner, PushSegment, PushStats
+from .serving import pool_blocks_for_memory
+from .transfer import LAYERWISE, kv_push_gbps, measured_plan
+from .workers import PROMPT, TOKEN, Machine, SchedulerConfig, Task
+
+
+def estimated_perf_model(cfg, kv: KVCacheManager | None, weight_bytes: int,
+                         hbm_gbs: float = 6543.0, tflops: float = 1000.0,
+                         capacity: float | None = None) -> PerfModel:
+    """Roofline-estimated PerfModel used by the B200 machines for batch
+    formation.  Token machines: capacity = weights + KV pool bytes (exact
+    admission).  Prompt machines keep no KV after the push; their capacity
+    is the device's HBM (the prompt's transient KV lives in activations)."""
+    pts = [1, 512, 1024, 2048, 4096, 8192]
+    p_ms = [max(0.05, cfg.prefill_flops(p) / (tflops * 1e12) * 1e3) for p in pts]
+    bs = [1, 2, 4, 8, 16, 32, 64]
+    t_ms = [max(0.05, cfg.decode_bytes([1024] * b) / (hbm_gbs * 1e9) * 1e3) for b in bs]
+    kvb = cfg.kv_bytes_per_token()
+    pool = 0 if kv is None else kv.num_blocks * kv.block_size * kvb
+    cap = float(weight_bytes + pool) if capacity is None else float(capacity)
+    return PerfModel("B200", cfg.name, (pts, p_ms), (bs, t_ms), float(kvb),
+                     float(weight_bytes), cap, cfg.max_token_batch)
+
+
+class PromptServer:
+    def __init__(self, runner: ModelRunner, peer: KVCacheManager, ctrl, token_rank: int,
+                 sched: SchedulerConfig):
+        self.runner = runner
+        self.peer = peer
+        self.ctrl = ctrl
+        self.token_rank = token_rank
+        cfg = runner.cfg
+        hbm = float(torch.cuda.get_device_properties(runner.dev).total_memory)
+        self.machine = Machine(0, None, estimated_perf_model(cfg, None, runner.w.nbytes(),
+                                                             capacity=hbm), PROMPT, sched)
+        self.push_log: list[PushStats] = []
+
+    def serve_burst(self, requests, t0: float, prompts_dev: dict | None = None):
+        """requests: list of (rid, host int32 prompt, n_out).  Returns
+        {rid: first-token host time}."""
+        dev = self.runner.dev
+        seqs = torch.empty(len(requests), dtype=torch.int32)
+        dist.recv(seqs, src=self.token_rank, group=self.ctrl)     # reservations
+        seq_of = {r[0]: int(s) for r, s in zip(requests, seqs)}
+        by_id = {r[0]: r for r in requests}
+        now_ms = 0.0
+        for rid, prompt, n_out in requests:
+            self.machine.enqueue(Task(rid, PROMPT, len(prompt), now_ms, n_out, n_out), now_ms)
+        first_time = {}
+        while self.machine.has_work():
+            batch = self.machine.form_batch(now_ms)
+            self.machine.running = batch
+            chunk = [by_id[t.request_id] for t in batch.prompt_tasks]
+            lens = [len(r[1]) for r in chunk]
+            if prompts_dev is not None:
+                toks = torch.cat([prompts_dev[r[0]] for r in chunk])
+            else:
+                toks = torch.cat([r[1] for r in chunk]).pin_memory().to(dev, non_blocking=True)
+            meta = ModelRunner.pack_meta(lens).pin_memory().to(dev, non_blocking=True)
+            segs, off = [], 0
+            for r, n in zip(chunk, lens):
+                segs.append(PushSegment(off, n, self.peer, seq_of[r[0]]))
+                off += n
+            st = PushStats(bytes_per_layer=off * 2 * self.runner.hkv * self.runner.dh * 2)
+            first = self.runner.prefill(toks, lens, meta, push=segs, push_stats=st)
+            fh = torch.empty(len(chunk), dtype=torch.int32).pin_memory()
+            fh.copy_(first, non_blocking=True)
+            torch.cuda.current_stream().synchronize()   # compute done + every push landed
+            tnow = time.perf_counter()
+            self.runner.finish_push_stats()
+            self.push_log.append(st)
+            msg = torch.tensor([[r[0], seq_of[r[0]], len(r[1]), int(fh[j]), r[2]]
+                                for j, r in enumerate(chunk)], dtype=torch.int32)
+            dist.send(torch.tensor([len(chunk)], dtype=torch.int32), dst=self.token_rank,
+                      group=self.ctrl)
+            dist.send(msg, dst=self.token_rank, group=self.ctrl)
+            for r in chunk:
+                first_time[r[0]] = tnow
+            now_ms = (tnow - t0) * 1e3
+            self.machine.complete_iteration(batch, now_ms)
+        return first_time
+
+
+class TokenServer:
+    def __init__(self, runner: ModelRunner, ctrl, prompt_rank: int, sched: SchedulerConfig):
+        self.runner = runner
+        self.kv = runner.kv
+        self.ctrl = ctrl
+        self.prompt_rank = prompt_rank
+        self.machine = Machine(0, None, estimated_perf_model(runner.cfg, self.kv,
+                                                             runner.w.nbytes()), TOKEN, sched)
+
+    def serve_burst(self, requests, t0: float):
+        """Reserve KV for the routed requests, then admit hand-overs and
+        decode until all of them finished.  Returns {rid: [emission times]}."""
+        kv = self.kv
+        seqs = [kv.allocate(len(p) + n) for _rid, p, n in requests]
+        torch.cuda.current_stream().synchronize()    # tables written before the peer reads
+        dist.send(torch.tensor(seqs, dtype=torch.int32), dst=self.prompt_rank, group=self.ctrl)
+        expected = len(requests)
+        received = 0
+        info = {}         # rid -> [seq, ctx_kv, last_token]
+        emit = {r[0]: [] for r in requests}
+        tokens = {r[0]: [] for r in requests}
+        graph, graph_rids = None, None
+        ring_h = torch.empty(64, dtype=torch.int32).pin_memory()
+        hdr, hdr_buf = None, torch.empty(1, dtype=torch.int32)
+        while received < expected or self.machine.has_work() or self.machine.resident:
+            if received < expected:
+                if hdr is None:
+                    hdr = dist.irecv(hdr_buf, src=self.prompt_rank, group=self.ctrl)
+                if not self.machine.has_work():
+                    hdr.wait()
+                if hdr.is_completed():
+                    hdr = None
+                    msg = torch.empty(int(hdr_buf[0]), 5, dtype=torch.int32)
+                    dist.recv(msg, src=self.prompt_rank, group=self.ctrl)
+                    now_ms = (time.perf_counter() - t0) * 1e3
+                    for rid, seq, plen, first, n_out in msg.tolist():
+                        received += 1
+                        tokens[rid].append(first)
+                        if n_out > 1:
+                            info[rid] = [seq, plen, first]
+                            self.machine.enqueue(
+                                Task(rid, TOKEN, plen + 1, now_ms, n_out, n_out - 1), now_ms)
+                        else:
+                            kv.release(seq)
+                    continue
+            if not self.machine.has_work():
+                continue
+            now_ms = (time.perf_counter() - t0) * 1e3
+            batch = self.machine.form_batch(now_ms)
+            if batch is None:
+                continue
+            self.machine.running = batch
+            rids = [t.request_id for t in batch.token_tasks]
+            B = len(rids)
+            if rids != graph_rids:
+                max_ctx = max(info[r][1] + len(tokens[r]) + 64 for r in rids)
+                graph = self.runner.decode_graph(B, 2048 * ((max_ctx + 2047) // 2048), 1)
+                graph.load([info[r][0] for r in rids], [info[r][2] for r in rids],
+                           [info[r][1] for r in rids])
+                if graph.graph is None:
+                    graph.capture()
+                graph_rids = rids
+            graph.replay()
+            ring_h[:B].copy_(graph.next_tok, non_blocking=True)   # stream tokens out
+            torch.cuda.current_stream().synchronize()
+            tnow = time.perf_counter()
+            for b, r in enumerate(rids):
+                t = int(ring_h[b])
+                tokens[r].append(t)
+                info[r][1] += 1
+                info[r][2] = t
+                emit[r].append(tnow)
+            for what, task in self.machine.complete_iteration(batch, (tnow - t0) * 1e3):
+                if what == "request_finished":
+                    kv.release(info[task.request_id][0])
+                    graph_rids = None if task.request_id in (graph_rids or []) else graph_rids
+        return emit, tokens
+
+
+# ---------------------------------------------------------------------------
+def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_traffic):
+    import json
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world < 2 or world % 2:
+        raise SystemExit("Splitwise pairs need an even number of GPUs >= 2")
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctrl = dist.new_group(backend="gloo")
+    pair, is_prompt = rank // 2, rank % 2 == 0
+    peer_rank = rank + 1 if is_prompt else rank - 1
+    cfg = get_config(args.model)
+    w = init_weights(cfg, seed=0)
+    P, O, R = args.prompt, args.out, 2     # 2 requests per pair = 1 per GPU
+    sched = SchedulerConfig()
+    if is_prompt:
+        runner = ModelRunner(w, None)
+        handle = [None]
+        dist.recv_object_list(handle, src=peer_rank, group=ctrl)
+        peer = KVCacheManager.open_peer(handle[0])
+        server = PromptServer(runner, peer, ctrl, peer_rank, sched)
+    else:
+        nb = min(pool_blocks_for_memory(cfg, 1, 16, reserve_bytes=2 << 30),
+                 64 * blocks_for(P + O + 64, 16))
+        kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads, cfg.head_dim, 16, 64,
+                            blocks_for(8192 + 1024, 16))
+        runner = ModelRunner(w, kv)
+        dist.send_object_list([kv.ipc_handle()], dst=peer_rank, group=ctrl)
+        server = TokenServer(runner, ctrl, peer_rank, sched)
+    g = torch.Generator().manual_seed(1234 + pair)
+    reqs = [(pair * R + i, torch.randint(0, cfg.vocab, (P,), generator=g, dtype=torch.int32), O)
+            for i in range(R)]
+    prompts_dev = {rid: p.cuda() for rid, p, _ in reqs}
+
+    def one_step(resident_prompts: bool):
+        dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        s.record()
+        if is_prompt:
+            out = server.serve_burst(reqs, t0, prompts_dev if resident_prompts else None)
+        else:
+            out = server.serve_burst(reqs, t0)
+        e.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        dev_ms = torch.tensor([s.elapsed_time(e)], device="cuda")
+        dist.all_reduce(dev_ms, op=dist.ReduceOp.MAX)
+        return t0, out, float(dev_ms), wall
+
+    for _ in range(args.warmup):
+        one_step(False)
+    launches0 = _abi.launch_count()
+    e2e_ms, ttft, tbt, gaps2, push_gbs, push_tail, push_raw = [], [], [], [], [], [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            t0, out, dms, wall = one_step(False)
+            gathered = [None] * world
+            payload = {"rank": rank, "t0": t0, "out": out if is_prompt else out[0]}
+            if is_prompt:
+                st = server.push_log[-1]
+                payload["push"] = (st.bytes_per_layer, st.layer_ms, st.tail_ms)
+            dist.all_gather_object(gathered, payload, group=ctrl)
+            e2e_ms.append(dms)
+            for pr in range(0, world, 2):
+                first = gathered[pr]["out"]
+                emits = gathered[pr + 1]["out"]
+                t0p = gathered[pr]["t0"]
+                for rid, tf in first.items():
+                    ttft.append((tf - t0p) * 1e3)
+                    seq = [tf] + emits[rid]
+                    g_ = [(b - a) * 1e3 for a, b in zip(seq, seq[1:])]
+                    tbt += g_
+                    if g_:
+                        gaps2.append(g_[0])
+                bpl, lms, tail = gathered[pr]["push"]
+                push_gbs.append(statistics.mean(kv_push_gbps(bpl, m) for m in lms))
+                push_tail.append(tail)
+                push_raw.append(sum(lms))
+        dev_ms = []
+        for _ in range(args.steps):
+            dev_ms.append(one_step(True)[2])
+    launches = _abi.launch_count() - launches0
+    launches_t = torch.tensor([launches], device="cuda", dtype=torch.float64)
+    dist.all_reduce(launches_t)
+    clocks = clk.summary()
+    if rank == 0:
+        hbm_peak, tc_peak, _tcs, peak_kind = peaks()
+        pairs = world // 2
+        toks_step = pairs * R * O
+        ms = statistics.mean(dev_ms)
+        plan = measured_plan(LAYERWISE, [0.0], 0.0)
+        _ = plan
+        line = {
+            "metric": "output tokens/s (+ TTFT/TBT p50,p99) serving 1024/128 requests, Llama-2-7B",
+            "value": toks_step / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded random weights/tokens)",
+            "config": {"workload": f"{cfg.name} {P}-token prompts / {O} greedy outputs, 1 request "
+                                   f"per GPU per step; {pairs} Splitwise pair(s) 1+1, layer-wise "
+                                   "KV push over NVLink, batched decode on the token GPU",
+                       "model": cfg.name, "prompt_tokens": P, "output_tokens": O,
+                       "requests_per_step": pairs * R, "parallelism": f"{pairs}x(1 prompt + 1 token)",
+                       "l2": "inputs > L2 (13.5 GB weights streamed per decode step)"},
+            "ttft_ms": {"p50": percentile(ttft, 0.5), "p99": percentile(ttft, 0.99)},
+            "tbt_ms": {"p50": percentile(tbt, 0.5), "p99": percentile(tbt, 0.99)},
+            "second_token_gap_ms": {"p50": percentile(gaps2, 0.5)},
+            "e2e": {"value": toks_step / (statistics.mean(e2e_ms) / 1e3), "unit": "tokens/s",
+                    "ms_per_step": statistics.mean(e2e_ms),
+                    "h2d_bytes_per_step": pairs * R * 4 * (4 * P),
+                    "d2h_bytes_per_step": pairs * R * 4 * O},
+            "kv_transfer": {"mode": "layerwise P2P push (NVLink, CUDA IPC)",
+                            "push_GBps_per_layer": statistics.mean(push_gbs),
+                            "nvlink_peak_GBps": 770.0,
+                            "frac": statistics.mean(push_gbs) / 770.0,
+                            "raw_ms": statistics.mean(push_raw),
+                            "visible_ms": statistics.mean(push_tail),
+                            "visible_frac_of_ttft": statistics.mean(push_tail) /
+                            percentile(ttft, 0.5)},
+            "gpu_launches": int(launches_t.item()),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -78,6 +78,12 @@ int swb_gemm_bf16(const void* a, const void* w, void* out, const void* resid,
  */
 int swb_gemv_bf16(const void* x, const void* w, void* out, const void* resid,
                   int M, int N, int K, int epilogue, uintptr_t stream);
+/* Pre-norm fused variant: x is the fp32 residual stream [M,K]; the kernel
+ * applies RMSNorm with weight norm_w on the fly (bit-identical to
+ * swb_rmsnorm followed by swb_gemv_bf16).  out may not alias x. */
+int swb_gemv_rmsnorm_bf16(const float* x, const void* norm_w, float eps,
+                          const void* w, void* out, const void* resid, int M,
+                          int N, int K, int epilogue, uintptr_t stream);
 
 /* ------------------------------------------------------- elementwise ops */
 /* x fp32 [rows,d] <- table bf16 [V,d][tokens[r]] */
@@ -130,20 +136,26 @@ int swb_stream_wait_flag(uint32_t* flag, uint32_t value, uintptr_t stream);
 int swb_attn_prefill(const void* qkv, int row_stride, const int32_t* cu_seqlens,
                      int num_seqs, int max_seqlen, int H, int Hkv, int dh,
                      float scale, void* out, uintptr_t stream);
-/* Paged decode attention: q from qkv rows [B, row_stride] (column 0), keys /
- * values from the layer pool through block_tables [B, max_blocks] and
- * ctx_lens[B] (tokens to attend, including the current one).  Split over
- * context partitions of `partition` tokens with an fp32 merge; workspace
- * must hold swb_attn_decode_workspace(B, H, max_ctx, partition, dh) bytes.
- */
+/* Paged decode attention for one layer, fused with the current token's
+ * RoPE and KV append and with the split-K merge: q/k/v of the current token
+ * come from qkv rows [B, row_stride] (q at column 0); when positions/slots are
+ * given, q and k are rotated at positions[b] and the token's k/v are written
+ * to pool slot slots[b] (both NULL: K/V already in the pool, no rotation).
+ * Keys/values are read through block_tables [B, max_blocks] for ctx_lens[b]
+ * tokens (including the current one).  The context is split into partitions
+ * of `partition` tokens; the last CTA of each (b, kv head) merges them.
+ * workspace must hold swb_attn_decode_workspace(B, H, max_ctx, partition, dh)
+ * bytes and be ZERO-initialised once (its merge tickets self-reset).
+ * Replaces the attention share of PerfModel.token_iter_time (perf.py:125-132)
+ * and the KV growth of Machine.complete_iteration (machine.py:263-266). */
 size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int partition,
                                  int dh);
-int swb_attn_decode(const void* qkv, int row_stride, const void* k_layer,
-                    const void* v_layer, const int32_t* block_tables,
-                    int max_blocks, const int32_t* ctx_lens, int B, int H,
-                    int Hkv, int dh, int block_size, float scale, int max_ctx,
-                    int partition, void* workspace, void* out,
-                    uintptr_t stream);
+int swb_attn_decode(const void* qkv, int row_stride, void* k_layer,
+                    void* v_layer, const int32_t* block_tables, int max_blocks,
+                    const int32_t* ctx_lens, const int32_t* positions,
+                    const int32_t* slots, float theta, int B, int H, int Hkv,
+                    int dh, int block_size, float scale, int max_ctx,
+                    int partition, void* workspace, void* out, uintptr_t stream);
 
 /* --------------------------------------------- decode-step bookkeeping
  * Graph-resident per-step state update so the decode loop needs no host

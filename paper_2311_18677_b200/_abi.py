@@ -45,6 +45,7 @@ SIGNATURES = {
     "swb_sync_stream": [_ST],
     "swb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_gemv_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _ST],
+    "swb_gemv_rmsnorm_bf16": [_P, _P, _F, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_embed": [_P, _P, _P, _I, _I, _ST],
     "swb_rmsnorm": [_P, _P, _P, _P, _I, _I, _F, _ST],
     "swb_argmax": [_P, _I, _I, _P, _ST],
@@ -54,8 +55,8 @@ SIGNATURES = {
     "swb_stream_wait_flag": [_P, _U, _ST],
     "swb_attn_prefill": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],
     "swb_attn_decode_workspace": [_I, _I, _I, _I, _I],
-    "swb_attn_decode": [_P, _I, _P, _P, _P, _I, _P, _I, _I, _I, _I, _I, _F, _I, _I, _P, _P,
-                        _ST],
+    "swb_attn_decode": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _F, _I, _I, _I, _I, _I, _F, _I,
+                        _I, _P, _P, _ST],
     "swb_decode_prepare": [_P, _P, _I, _I, _I, _P, _P, _P, _ST],
     "swb_decode_advance": [_P, _P, _P, _P, _P, _I, _I, _ST],
     "swb_slots_from_table": [_P, _I, _I, _I, _P, _ST],
@@ -106,9 +107,9 @@ def check(status: int, what: str = "") -> None:
 
 # kernels launched per successful call (for the bench's gpu_launches claim)
 LAUNCH_MULT = {
-    "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
+    "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
     "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
-    "swb_attn_prefill": 1, "swb_attn_decode": 2, "swb_decode_prepare": 1,
+    "swb_attn_prefill": 1, "swb_attn_decode": 1, "swb_decode_prepare": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
     "swb_block_free": 1,
 }

@@ -250,19 +250,39 @@ constexpr int DA_D = 128;
 constexpr int DA_MAXG = 8;
 constexpr int DA_WARPS = 4;
 
-// grid (B, Hkv, NP); 128 threads.  The CTA first issues cp.async for its
-// whole partition (K and V rows of `part` tokens, 256 B each, gathered
-// through the block table) so every byte it needs is in flight at once, then
-// computes scores (half-warp per token, shuffle-reduced dot products against
-// the G query heads of the group), the partition softmax (warp shuffles) and
-// P.V (lane owns 4 of the 128 dims), all from shared memory.
+// Decode attention, one kernel per layer:
+//   grid (B, Hkv, NP), 128 threads; CTA (b, kh, p) covers context tokens
+//   [p*part, (p+1)*part) of sequence b for the G query heads of kv head kh.
+// * If `pos` is given, the current token's q/k are rotated here (RoPE) and its
+//   k/v are written into the pool slot slots[b] by the CTA whose partition
+//   holds position pos[b] (the token attends to itself from registers/smem,
+//   not from the freshly written global copy).
+// * All other K/V rows of the partition are gathered through the block table
+//   with cp.async issued up front, so the whole partition is in flight at once.
+// * Scores: half-warp per token with shuffle-reduced dot products against the
+//   G query heads; softmax with warp shuffles; P.V with lane-owned dims.
+// * Split-K merge fused: every CTA publishes (o, m, l); the last CTA of a
+//   (b, kh) group (atomic ticket) merges all partitions and writes bf16 out.
+__device__ __forceinline__ void rope4(float* a, float* b, int i0, float pos, float l2t) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float inv_freq = exp2f(-l2t * (float)(2 * (i0 + j)) / (float)DA_D);
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    const float x = a[j], y = b[j];
+    a[j] = x * cs - y * sn;
+    b[j] = y * cs + x * sn;
+  }
+}
+
 __global__ void __launch_bounds__(DA_WARPS * 32)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
-                       const __nv_bfloat16* __restrict__ kpool,
-                       const __nv_bfloat16* __restrict__ vpool,
+                       __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
                        const int32_t* __restrict__ tables, int max_blocks,
-                       const int32_t* __restrict__ ctx_lens, int H, int Hkv, int bs,
-                       float scale_log2, int part, float* __restrict__ ws) {
+                       const int32_t* __restrict__ ctx_lens, const int32_t* __restrict__ pos,
+                       const int32_t* __restrict__ slots, float log2_theta, int H, int Hkv,
+                       int bs, float scale_log2, int part, float* __restrict__ ws,
+                       int* __restrict__ tickets, __nv_bfloat16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) uint8_t dsm_raw[];
@@ -273,16 +293,10 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
   const int t0 = p * part;
   const int t1 = min(ctx, t0 + part);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto wsp = [&](int gh) { return ws + (((size_t)b * H + gh) * NP + p) * (DA_D + 2); };
-  if (t0 >= t1) {
-    if (threadIdx.x < G) {
-      float* w = wsp(kh * G + threadIdx.x);
-      w[DA_D] = -INFINITY;
-      w[DA_D + 1] = 0.f;
-    }
-    return;
-  }
-  const int ntok = t1 - t0;
+  auto wsp = [&](int gh, int pp) {
+    return ws + (((size_t)b * H + gh) * NP + pp) * (DA_D + 2);
+  };
+  __shared__ int s_last;
   __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(dsm_raw);      // [part][128]
   __nv_bfloat16* sv = sk + (size_t)part * DA_D;                        // [part][128]
   float* sq = reinterpret_cast<float*>(sv + (size_t)part * DA_D);      // [G][128]
@@ -290,128 +304,198 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
   float* sacc = ss + G * part;                                         // [WARPS][G][128]
   float* sstat = sacc + DA_WARPS * G * DA_D;                           // [G][2]
 
-  // ---- issue every K/V load of the partition (16 B chunks)
-  const int32_t* trow = tables + (size_t)b * max_blocks;
-  const int chunks = ntok * 16;
-  for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
-    const int tt = c >> 4, ch = c & 15;
-    const int tok = t0 + tt;
-    const int blk = __ldg(trow + tok / bs);
-    const size_t g = (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D + ch * 8;
-    cp_async16(smem_u32(sk + tt * DA_D + ch * 8), kpool + g, true);
-    cp_async16(smem_u32(sv + tt * DA_D + ch * 8), vpool + g, true);
-  }
-  cp_async_commit();
-  for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
-    const int gi = i / DA_D, d = i % DA_D;
-    sq[i] = __bfloat162float(qkv[(size_t)b * rs + (kh * G + gi) * DA_D + d]) * scale_log2;
-  }
-  cp_async_wait<0>();
-  __syncthreads();
+  if (t0 >= t1) {
+    if (threadIdx.x < G) {
+      float* w = wsp(kh * G + threadIdx.x, p);
+      w[DA_D] = -INFINITY;
+      w[DA_D + 1] = 0.f;
+    }
+  } else {
+    const int ntok = t1 - t0;
+    const int cur = pos ? pos[b] : -1;            // current token position
+    const bool own_cur = cur >= t0 && cur < t1;
+    // ---- issue every K/V load of the partition (16 B chunks)
+    const int32_t* trow = tables + (size_t)b * max_blocks;
+    for (int c = threadIdx.x; c < ntok * 16; c += blockDim.x) {
+      const int tt = c >> 4, ch = c & 15;
+      const int tok = t0 + tt;
+      if (tok == cur) continue;                   // provided from registers below
+      const int blk = __ldg(trow + tok / bs);
+      const size_t g = (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D + ch * 8;
+      cp_async16(smem_u32(sk + tt * DA_D + ch * 8), kpool + g, true);
+      cp_async16(smem_u32(sv + tt * DA_D + ch * 8), vpool + g, true);
+    }
+    cp_async_commit();
+    // ---- q of the group (rotated), scaled by softmax scale * log2(e)
+    const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
+    const float fpos = (float)cur;
+    for (int i = threadIdx.x; i < G * (DA_D / 8); i += blockDim.x) {
+      // 16 groups of 4 rotary pairs (d, d+64) per head
+      const int gi = i / (DA_D / 8), i0 = (i % (DA_D / 8)) * 4;
+      const __nv_bfloat16* hp = qrow + (kh * G + gi) * DA_D;
+      float lo[4], hi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        lo[j] = __bfloat162float(hp[i0 + j]);
+        hi[j] = __bfloat162float(hp[64 + i0 + j]);
+      }
+      if (pos) {
+        rope4(lo, hi, i0, fpos, log2_theta);
+        // match the two-kernel path: rotated q is rounded to bf16
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          lo[j] = __bfloat162float(__float2bfloat16(lo[j]));
+          hi[j] = __bfloat162float(__float2bfloat16(hi[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sq[gi * DA_D + i0 + j] = lo[j] * scale_log2;
+        sq[gi * DA_D + 64 + i0 + j] = hi[j] * scale_log2;
+      }
+    }
+    // ---- current token: rotate k, write k/v to the pool and into smem
+    if (own_cur && threadIdx.x < 16) {
+      const int i0 = threadIdx.x * 4;           // 16 threads x 4 pairs = 64 pairs
+      const __nv_bfloat16* kp = qrow + (H + kh) * DA_D;
+      const __nv_bfloat16* vp = qrow + (H + Hkv + kh) * DA_D;
+      float lo[4], hi[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        lo[j] = __bfloat162float(kp[i0 + j]);
+        hi[j] = __bfloat162float(kp[64 + i0 + j]);
+      }
+      rope4(lo, hi, i0, fpos, log2_theta);
+      const int slot = slots[b];
+      const size_t g = (((size_t)(slot / bs) * Hkv + kh) * bs + slot % bs) * DA_D;
+      const int tt = cur - t0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const __nv_bfloat16 kl = __float2bfloat16(lo[j]), khv = __float2bfloat16(hi[j]);
+        kpool[g + i0 + j] = kl;
+        kpool[g + 64 + i0 + j] = khv;
+        sk[tt * DA_D + i0 + j] = kl;
+        sk[tt * DA_D + 64 + i0 + j] = khv;
+        vpool[g + i0 + j] = vp[i0 + j];
+        vpool[g + 64 + i0 + j] = vp[64 + i0 + j];
+        sv[tt * DA_D + i0 + j] = vp[i0 + j];
+        sv[tt * DA_D + 64 + i0 + j] = vp[64 + i0 + j];
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
 
-  // ---- scores: half-warp per token
-  {
-    const int half = lane >> 4, hl = lane & 15;
-    for (int tb = warp * 2; tb < ntok; tb += DA_WARPS * 2) {  // warp-uniform
-      const int tt = tb + half;
-      const bool valid = tt < ntok;
-      float kf[8];
-      const uint4 kv = *reinterpret_cast<const uint4*>(sk + (valid ? tt : 0) * DA_D + hl * 8);
-      {
-        float2 a = bf2_to_f2(kv.x), c = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
-               f = bf2_to_f2(kv.w);
-        kf[0] = a.x; kf[1] = a.y; kf[2] = c.x; kf[3] = c.y;
-        kf[4] = e.x; kf[5] = e.y; kf[6] = f.x; kf[7] = f.y;
-      }
-      for (int gi = 0; gi < G; ++gi) {
-        const float4 q0 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8);
-        const float4 q1 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8 + 4);
-        float d = q0.x * kf[0];
-        d = fmaf(q0.y, kf[1], d); d = fmaf(q0.z, kf[2], d); d = fmaf(q0.w, kf[3], d);
-        d = fmaf(q1.x, kf[4], d); d = fmaf(q1.y, kf[5], d); d = fmaf(q1.z, kf[6], d);
-        d = fmaf(q1.w, kf[7], d);
+    // ---- scores: half-warp per token
+    {
+      const int half = lane >> 4, hl = lane & 15;
+      for (int tb = warp * 2; tb < ntok; tb += DA_WARPS * 2) {  // warp-uniform
+        const int tt = tb + half;
+        const bool valid = tt < ntok;
+        float kf[8];
+        const uint4 kv = *reinterpret_cast<const uint4*>(sk + (valid ? tt : 0) * DA_D + hl * 8);
+        {
+          float2 a = bf2_to_f2(kv.x), c = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
+                 f = bf2_to_f2(kv.w);
+          kf[0] = a.x; kf[1] = a.y; kf[2] = c.x; kf[3] = c.y;
+          kf[4] = e.x; kf[5] = e.y; kf[6] = f.x; kf[7] = f.y;
+        }
+        for (int gi = 0; gi < G; ++gi) {
+          const float4 q0 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8);
+          const float4 q1 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8 + 4);
+          float d = q0.x * kf[0];
+          d = fmaf(q0.y, kf[1], d); d = fmaf(q0.z, kf[2], d); d = fmaf(q0.w, kf[3], d);
+          d = fmaf(q1.x, kf[4], d); d = fmaf(q1.y, kf[5], d); d = fmaf(q1.z, kf[6], d);
+          d = fmaf(q1.w, kf[7], d);
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        if (hl == 0 && valid) ss[gi * part + tt] = d;
+          for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (hl == 0 && valid) ss[gi * part + tt] = d;
+        }
       }
     }
-  }
-  __syncthreads();
-  // ---- softmax stats per head
-  for (int gi = warp; gi < G; gi += DA_WARPS) {
-    float m = -INFINITY;
-    for (int i = lane; i < ntok; i += 32) m = fmaxf(m, ss[gi * part + i]);
-    m = warp_max(m);
-    float l = 0.f;
-    for (int i = lane; i < ntok; i += 32) {
-      const float e = exp2f(ss[gi * part + i] - m);
-      ss[gi * part + i] = e;
-      l += e;
+    __syncthreads();
+    // ---- softmax stats per head
+    for (int gi = warp; gi < G; gi += DA_WARPS) {
+      float m = -INFINITY;
+      for (int i = lane; i < ntok; i += 32) m = fmaxf(m, ss[gi * part + i]);
+      m = warp_max(m);
+      float l = 0.f;
+      for (int i = lane; i < ntok; i += 32) {
+        const float e = exp2f(ss[gi * part + i] - m);
+        ss[gi * part + i] = e;
+        l += e;
+      }
+      l = warp_sum(l);
+      if (lane == 0) {
+        sstat[gi * 2] = m;
+        sstat[gi * 2 + 1] = l;
+      }
     }
-    l = warp_sum(l);
-    if (lane == 0) {
-      sstat[gi * 2] = m;
-      sstat[gi * 2 + 1] = l;
-    }
-  }
-  __syncthreads();
-  // ---- P V from smem: warp per token stripe, lane owns dims [4*lane, 4*lane+4)
-  float acc[DA_MAXG][4];
+    __syncthreads();
+    // ---- P V: warp per token stripe, lane owns dims [4*lane, 4*lane+4)
+    float acc[DA_MAXG][4];
 #pragma unroll
-  for (int gi = 0; gi < DA_MAXG; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
-  for (int tt = warp; tt < ntok; tt += DA_WARPS) {
-    const uint2 vv = *reinterpret_cast<const uint2*>(sv + tt * DA_D + lane * 4);
-    const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
+    for (int gi = 0; gi < DA_MAXG; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
+    for (int tt = warp; tt < ntok; tt += DA_WARPS) {
+      const uint2 vv = *reinterpret_cast<const uint2*>(sv + tt * DA_D + lane * 4);
+      const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
+#pragma unroll
+      for (int gi = 0; gi < DA_MAXG; ++gi) {
+        if (gi >= G) break;
+        const float pw = ss[gi * part + tt];
+        acc[gi][0] = fmaf(pw, v0.x, acc[gi][0]);
+        acc[gi][1] = fmaf(pw, v0.y, acc[gi][1]);
+        acc[gi][2] = fmaf(pw, v1.x, acc[gi][2]);
+        acc[gi][3] = fmaf(pw, v1.y, acc[gi][3]);
+      }
+    }
 #pragma unroll
     for (int gi = 0; gi < DA_MAXG; ++gi) {
       if (gi >= G) break;
-      const float pw = ss[gi * part + tt];
-      acc[gi][0] = fmaf(pw, v0.x, acc[gi][0]);
-      acc[gi][1] = fmaf(pw, v0.y, acc[gi][1]);
-      acc[gi][2] = fmaf(pw, v1.x, acc[gi][2]);
-      acc[gi][3] = fmaf(pw, v1.y, acc[gi][3]);
+      float4* dst = reinterpret_cast<float4*>(sacc + ((size_t)warp * G + gi) * DA_D + lane * 4);
+      *dst = make_float4(acc[gi][0], acc[gi][1], acc[gi][2], acc[gi][3]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
+      const int gi = i / DA_D, d = i % DA_D;
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < DA_WARPS; ++w) v += sacc[((size_t)w * G + gi) * DA_D + d];
+      float* wo = wsp(kh * G + gi, p);
+      wo[d] = v;
+      if (d == 0) {
+        wo[DA_D] = sstat[gi * 2];
+        wo[DA_D + 1] = sstat[gi * 2 + 1];
+      }
     }
   }
-#pragma unroll
-  for (int gi = 0; gi < DA_MAXG; ++gi) {
-    if (gi >= G) break;
-    float4* dst = reinterpret_cast<float4*>(sacc + ((size_t)warp * G + gi) * DA_D + lane * 4);
-    *dst = make_float4(acc[gi][0], acc[gi][1], acc[gi][2], acc[gi][3]);
+  // ---- fused split-K merge: the last CTA of (b, kh) combines the partitions
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* t = tickets + (size_t)b * Hkv + kh;
+    const int prev = atomicAdd(t, 1);
+    s_last = prev == NP - 1;
+    if (s_last) *t = 0;  // reset for the next launch (graph replay)
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
-    const int gi = i / DA_D, d = i % DA_D;
-    float v = 0.f;
-#pragma unroll
-    for (int w = 0; w < DA_WARPS; ++w) v += sacc[((size_t)w * G + gi) * DA_D + d];
-    float* wo = wsp(kh * G + gi);
-    wo[d] = v;
-    if (d == 0) {
-      wo[DA_D] = sstat[gi * 2];
-      wo[DA_D + 1] = sstat[gi * 2 + 1];
+  if (!s_last) return;
+  __threadfence();
+  for (int gi = 0; gi < G; ++gi) {
+    const int gh = kh * G + gi;
+    float m = -INFINITY;
+    for (int pp = 0; pp < NP; ++pp) m = fmaxf(m, __ldcg(wsp(gh, pp) + DA_D));
+    const int d = threadIdx.x;  // 128 threads = 128 dims
+    float l = 0.f, o = 0.f;
+    for (int pp = 0; pp < NP; ++pp) {
+      const float* w = wsp(gh, pp);
+      const float mp = __ldcg(w + DA_D);
+      if (mp == -INFINITY) continue;
+      const float f = exp2f(mp - m);
+      l += __ldcg(w + DA_D + 1) * f;
+      o += __ldcg(w + d) * f;
     }
+    out[((size_t)b * H + gh) * DA_D + d] = __float2bfloat16(o / l);
   }
-}
-
-// merge partitions: grid (B, H), 128 threads (one per dh element)
-__global__ void attn_decode_merge_kernel(const float* __restrict__ ws, int H, int NP,
-                                         __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
-  const float* base = ws + ((size_t)b * H + h) * NP * (DA_D + 2);
-  float m = -INFINITY;
-  for (int p = 0; p < NP; ++p) m = fmaxf(m, base[p * (DA_D + 2) + DA_D]);
-  float l = 0.f, o = 0.f;
-  for (int p = 0; p < NP; ++p) {
-    const float* w = base + p * (DA_D + 2);
-    const float mp = w[DA_D];
-    if (mp == -INFINITY) continue;
-    const float f = exp2f(mp - m);
-    l += w[DA_D + 1] * f;
-    o += w[d] * f;
-  }
-  out[((size_t)b * H + h) * DA_D + d] = __float2bfloat16(o / l);
 }
 
 }  // namespace swb
@@ -452,15 +536,16 @@ extern "C" size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int parti
                                             int dh) {
   if (B <= 0 || H <= 0 || max_ctx <= 0 || partition <= 0) return 0;
   const size_t np = (max_ctx + partition - 1) / partition;
-  return (size_t)B * H * np * (dh + 2) * sizeof(float);
+  // partials [B][H][NP][dh+2] fp32 + merge tickets [B][H] int32 (zeroed by caller)
+  return (size_t)B * H * np * (dh + 2) * sizeof(float) + (size_t)B * H * sizeof(int);
 }
 
-extern "C" int swb_attn_decode(const void* qkv, int row_stride, const void* k_layer,
-                               const void* v_layer, const int32_t* block_tables,
-                               int max_blocks, const int32_t* ctx_lens, int B, int H,
-                               int Hkv, int dh, int block_size, float scale, int max_ctx,
-                               int partition, void* workspace, void* out,
-                               uintptr_t stream) {
+extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, void* v_layer,
+                               const int32_t* block_tables, int max_blocks,
+                               const int32_t* ctx_lens, const int32_t* positions,
+                               const int32_t* slots, float theta, int B, int H, int Hkv,
+                               int dh, int block_size, float scale, int max_ctx, int partition,
+                               void* workspace, void* out, uintptr_t stream) {
   SWB_REQUIRE(qkv && k_layer && v_layer && block_tables && ctx_lens && workspace && out,
               "swb_attn_decode: null pointer");
   SWB_REQUIRE(dh == DA_D, "swb_attn_decode: dh must be 128");
@@ -469,6 +554,9 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, const void* k_la
   SWB_REQUIRE(B > 0 && max_ctx > 0 && partition > 0 && partition % 32 == 0 &&
                   block_size > 0,
               "swb_attn_decode: bad sizes");
+  SWB_REQUIRE((positions == nullptr) == (slots == nullptr),
+              "swb_attn_decode: positions and slots go together");
+  SWB_REQUIRE(!positions || theta > 1.f, "swb_attn_decode: theta");
   const int G = H / Hkv;
   const int NP = (max_ctx + partition - 1) / partition;
   const size_t smem = (size_t)partition * DA_D * 2 * 2 +
@@ -483,26 +571,16 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, const void* k_la
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr[dev] = true;
   }
-  dim3 grid(B, Hkv, NP);
-  {
-    const cudaError_t le_ = launch(attn_decode_kernel, dim3(grid), dim3(DA_WARPS * 32), smem, (cudaStream_t)stream,
-        
+  float* ws = reinterpret_cast<float*>(workspace);
+  int* tickets = reinterpret_cast<int*>(ws + (size_t)B * H * NP * (DA_D + 2));
+  const cudaError_t le = launch(
+      attn_decode_kernel, dim3(B, Hkv, NP), dim3(DA_WARPS * 32), smem, (cudaStream_t)stream,
       reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
-      reinterpret_cast<const __nv_bfloat16*>(k_layer),
-      reinterpret_cast<const __nv_bfloat16*>(v_layer), block_tables, max_blocks, ctx_lens,
-      H, Hkv, block_size, scale * 1.4426950408889634f, partition,
-      reinterpret_cast<float*>(workspace));
-    if (le_ != cudaSuccess)
-      return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_kernel: %s", cudaGetErrorString(le_));
-  }
-  const int st = swb_check_launch("attn_decode_kernel");
-  if (st != SWB_OK) return st;
-  {
-    const cudaError_t le_ = launch(attn_decode_merge_kernel, dim3(B, H), dim3(DA_D), 0,
-                                   (cudaStream_t)stream,
-      reinterpret_cast<const float*>(workspace), H, NP, reinterpret_cast<__nv_bfloat16*>(out));
-    if (le_ != cudaSuccess)
-      return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_merge_kernel: %s", cudaGetErrorString(le_));
-  }
-  return swb_check_launch("attn_decode_merge_kernel");
+      reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
+      block_tables, max_blocks, ctx_lens, positions, slots, positions ? log2f(theta) : 0.f, H,
+      Hkv, block_size, scale * 1.4426950408889634f, partition, ws, tickets,
+      reinterpret_cast<__nv_bfloat16*>(out));
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("attn_decode_kernel");
 }

@@ -6,6 +6,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -49,6 +51,19 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Opt-in: SWB_PDL=1 in the environment sets the attribute.  Measured on the
+// 7B decode graph (bench A/B, profiles/): early-trigger PDL made the full
+// step slower (4.39 vs 3.83 ms) although back-to-back GEMVs gained ~1 us
+// each, so the default is plain stream order; griddepcontrol.wait is a no-op
+// then.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SWB_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                           cudaStream_t stream, Args&&... args) {
@@ -61,7 +76,7 @@ inline cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

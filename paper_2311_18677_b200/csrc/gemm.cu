@@ -53,8 +53,11 @@ __global__ void __launch_bounds__(128, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * GM;
-  const int n0 = blockIdx.x * GN;
+  // M-fastest rasterization: the CTAs resident at once share weight tiles
+  // (each W tile is fetched from HBM ~once and re-served from L2), while the
+  // small activation matrix stays L2-resident.
+  const int m0 = blockIdx.x * GM;
+  const int n0 = blockIdx.y * GN;
   const int num_k = (args.K + GK - 1) / GK;
 
   if (warp == 0 && lane == 0) {
@@ -260,7 +263,7 @@ extern "C" int swb_gemm_bf16(const void* a, const void* w, void* out,
     attr_set[dev] = true;
   }
   GemmArgs args{out, reinterpret_cast<const float*>(resid), M, N, K, epilogue};
-  dim3 grid((N + GN - 1) / GN, (M + GM - 1) / GM);
+  dim3 grid((M + GM - 1) / GM, (N + GN - 1) / GN);
   {
     const cudaError_t le_ = launch(gemm_bf16_tcgen05, dim3(grid), dim3(128), G_SMEM_BYTES, (cudaStream_t)stream,
         ta, tw, args);

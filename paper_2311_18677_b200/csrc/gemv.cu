@@ -29,7 +29,9 @@ constexpr int TV_STAGES = 6;
 constexpr int TV_ROW_BYTES = TV_KC * 2;
 constexpr int TV_STAGE_BYTES = TV_ROWS * TV_ROW_BYTES;  // 16 KB
 constexpr int TV_THREADS = (TV_WARPS + 1) * 32;
-constexpr int TV_SMEM = TV_STAGES * TV_STAGE_BYTES + 2 * TV_STAGES * 8 + 2 * TV_WARPS * 16 * 4 + 128;
+constexpr int TV_CTAS_PER_SM = 2;             // 2 x ~100 KB ring per SM
+constexpr int TV_SMEM = TV_STAGES * TV_STAGE_BYTES + 2 * TV_STAGES * 8 +
+                        2 * TV_WARPS * TV_ROWS * 16 * 4 + 128;
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
@@ -54,15 +56,22 @@ __device__ __forceinline__ int item_row(int item, int j, bool swiglu) {
   return (o >> 7) * 256 + (o & 127) + (j >= 2 ? 128 : 0);
 }
 
-template <int MB>
-__global__ void __launch_bounds__(TV_THREADS, 1)
-    gemv_bulk_kernel(const __nv_bfloat16* __restrict__ x,
-                     const __nv_bfloat16* __restrict__ W, void* out, const float* resid,
-                     int M, int N, int K, int epi, int n_items) {
+// NORM = false: x is bf16 [M,K].
+// NORM = true : x is the fp32 residual stream [M,K]; the kernel applies
+//               RMSNorm on the fly, h = bf16(x * rsqrt(mean(x^2)+eps) * nw),
+//               bit-identical to swb_rmsnorm's output (fused pre-norm GEMV).
+template <int MB, bool NORM>
+__global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
+    gemv_bulk_kernel(const void* __restrict__ xin, const __nv_bfloat16* __restrict__ nw,
+                     float eps, const __nv_bfloat16* __restrict__ W, void* out,
+                     const float* resid, int M, int N, int K, int epi, int n_items) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TV_STAGES * TV_STAGE_BYTES);
   uint64_t* empty = full + TV_STAGES;
-  float* part = reinterpret_cast<float*>(empty + TV_STAGES);  // [2][WARPS][16]
+  float* part = reinterpret_cast<float*>(empty + TV_STAGES);  // [2][WARPS][ROWS][16]
+  float* rstd = part + 2 * TV_WARPS * TV_ROWS * 16;            // [16]
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(xin);
+  const float* xf = reinterpret_cast<const float*>(xin);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool swiglu = epi == SWB_EPI_SWIGLU;
   const int nk = (K + TV_KC - 1) / TV_KC;
@@ -104,138 +113,211 @@ __global__ void __launch_bounds__(TV_THREADS, 1)
     return;
   }
 
-  // ------------------------------ consumers: warp w -> row w&3, K half w>>2
+  // ------------------- consumers: warp w owns columns [256w, 256w+256) of
+  // every stage for all 4 rows of the item, so one x chunk (per batch row)
+  // feeds 4 weight rows; lanes shuffle-reduce, warps combine through smem.
   // The producer above streams static weights before the previous kernel has
   // finished (PDL); consumers read x / write out only after it has.
   pdl_wait();
-  const int slot = warp & 3, khalf = warp >> 2;
+  if constexpr (NORM) {
+    // sum of squares of every batch row, by all consumer threads
+    const int t = threadIdx.x;
+    for (int m = 0; m < M; ++m) {
+      float ss = 0.f;
+      for (int k = t * 4; k < K; k += TV_WARPS * 32 * 4) {
+        const float4 v = *reinterpret_cast<const float4*>(xf + (size_t)m * K + k);
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) part[warp * 16 + m] = ss;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
+    if (t < M) {
+      float ss = 0.f;
+      for (int w = 0; w < TV_WARPS; ++w) ss += part[w * 16 + t];
+      rstd[t] = rsqrtf(ss / (float)K + eps);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
+  }
   int it = 0, parity = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, parity ^= 1) {
-    const int row = item_row(item, slot, swiglu);
-    const bool valid = row < N;
-    float acc[MB];
+    float acc[TV_ROWS][MB];
 #pragma unroll
-    for (int m = 0; m < MB; ++m) acc[m] = 0.f;
+    for (int j = 0; j < TV_ROWS; ++j)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) acc[j][m] = 0.f;
     for (int kc = 0; kc < nk; ++kc, ++it) {
       const int s = it % TV_STAGES;
+      const int k = kc * TV_KC + warp * 256 + lane * 8;
+      uint4 xq[MB];
+      if (k < K) {
+        if constexpr (NORM) {
+          const uint4 wq = *reinterpret_cast<const uint4*>(nw + k);
+          const float2 n0 = bf2_to_f2(wq.x), n1 = bf2_to_f2(wq.y), n2 = bf2_to_f2(wq.z),
+                       n3 = bf2_to_f2(wq.w);
+#pragma unroll
+          for (int m = 0; m < MB; ++m) {
+            if (m >= M) break;
+            const float r = rstd[m];
+            const float4 a = *reinterpret_cast<const float4*>(xf + (size_t)m * K + k);
+            const float4 b = *reinterpret_cast<const float4*>(xf + (size_t)m * K + k + 4);
+            xq[m] = make_uint4(f2_to_bf2(a.x * r * n0.x, a.y * r * n0.y),
+                               f2_to_bf2(a.z * r * n1.x, a.w * r * n1.y),
+                               f2_to_bf2(b.x * r * n2.x, b.y * r * n2.y),
+                               f2_to_bf2(b.z * r * n3.x, b.w * r * n3.y));
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < MB; ++m)
+            if (m < M) xq[m] = *reinterpret_cast<const uint4*>(x + (size_t)m * K + k);
+        }
+      }
       mbar_wait(&full[s], (it / TV_STAGES) & 1);
-      if (valid) {
-        const __nv_bfloat16* wr = reinterpret_cast<const __nv_bfloat16*>(
-            smem + s * TV_STAGE_BYTES + slot * TV_ROW_BYTES) + khalf * (TV_KC / 2);
-        uint4 wv[4];
+      if (k < K) {
+        const uint8_t* st = smem + s * TV_STAGE_BYTES + (warp * 256 + lane * 8) * 2;
+        uint4 wv[TV_ROWS];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) wv[j] = *reinterpret_cast<const uint4*>(wr + j * 256 + lane * 8);
+        for (int j = 0; j < TV_ROWS; ++j)
+          wv[j] = *reinterpret_cast<const uint4*>(st + j * TV_ROW_BYTES);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = kc * TV_KC + khalf * (TV_KC / 2) + j * 256 + lane * 8;
-          if (k < K) {
+        for (int m = 0; m < MB; ++m) {
+          if (m >= M) break;
+          const float2 x0 = bf2_to_f2(xq[m].x), x1 = bf2_to_f2(xq[m].y),
+                       x2 = bf2_to_f2(xq[m].z), x3 = bf2_to_f2(xq[m].w);
+#pragma unroll
+          for (int j = 0; j < TV_ROWS; ++j) {
             const float2 w0 = bf2_to_f2(wv[j].x), w1 = bf2_to_f2(wv[j].y),
                          w2 = bf2_to_f2(wv[j].z), w3 = bf2_to_f2(wv[j].w);
-#pragma unroll
-            for (int m = 0; m < MB; ++m) {
-              if (m >= M) break;
-              const uint4 xq = *reinterpret_cast<const uint4*>(x + (size_t)m * K + k);
-              const float2 x0 = bf2_to_f2(xq.x), x1 = bf2_to_f2(xq.y),
-                           x2 = bf2_to_f2(xq.z), x3 = bf2_to_f2(xq.w);
-              float a = acc[m];
-              a = fmaf(x0.x, w0.x, a); a = fmaf(x0.y, w0.y, a);
-              a = fmaf(x1.x, w1.x, a); a = fmaf(x1.y, w1.y, a);
-              a = fmaf(x2.x, w2.x, a); a = fmaf(x2.y, w2.y, a);
-              a = fmaf(x3.x, w3.x, a); a = fmaf(x3.y, w3.y, a);
-              acc[m] = a;
-            }
+            float a = acc[j][m];
+            a = fmaf(x0.x, w0.x, a); a = fmaf(x0.y, w0.y, a);
+            a = fmaf(x1.x, w1.x, a); a = fmaf(x1.y, w1.y, a);
+            a = fmaf(x2.x, w2.x, a); a = fmaf(x2.y, w2.y, a);
+            a = fmaf(x3.x, w3.x, a); a = fmaf(x3.y, w3.y, a);
+            acc[j][m] = a;
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // per-warp partial sums -> smem (double-buffered by item parity), then
-    // warp 0 combines the two K halves of each row and applies the epilogue
-    float* pb = part + parity * TV_WARPS * 16;
+    // lanes -> warp sums -> smem [parity][warp][row][m], then warp 0 adds the
+    // 8 K-slices of each (row, m) and applies the epilogue
+    float* pb = part + parity * TV_WARPS * TV_ROWS * 16;
 #pragma unroll
-    for (int m = 0; m < MB; ++m) {
-      const float v = warp_sum(acc[m]);
-      if (lane == 0) pb[warp * 16 + m] = v;
-    }
+    for (int j = 0; j < TV_ROWS; ++j)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        if (m >= M) break;
+        const float v = warp_sum(acc[j][m]);
+        if (lane == 0) pb[(warp * TV_ROWS + j) * 16 + m] = v;
+      }
     asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
     if (warp == 0) {
-      if (swiglu) {
-        // lane = m*2 + o : outputs 2*item + o
-        const int m = lane >> 1, o = lane & 1;
-        const int nout = N >> 1, oi = item * 2 + o;
-        if (m < M && oi < nout) {
-          const float g = pb[o * 16 + m] + pb[(o + 4) * 16 + m];
-          const float u = pb[(o + 2) * 16 + m] + pb[(o + 6) * 16 + m];
-          reinterpret_cast<__nv_bfloat16*>(out)[(size_t)m * nout + oi] =
-              __float2bfloat16(g / (1.f + __expf(-g)) * u);
+      for (int e0 = 0; e0 < M * TV_ROWS; e0 += 32) {   // warp-uniform trip count
+        const int e = e0 + lane;
+        const bool active = e < M * TV_ROWS;
+        const int m = e / TV_ROWS, j = e % TV_ROWS;
+        float v = 0.f;
+        if (active) {
+#pragma unroll
+          for (int w = 0; w < TV_WARPS; ++w) v += pb[(w * TV_ROWS + j) * 16 + m];
         }
-      } else {
-        for (int e = lane; e < M * TV_ROWS; e += 32) {
-          const int m = e / TV_ROWS, j = e % TV_ROWS;
+        // SwiGLU: rows j = 0,1 gate and 2,3 up of outputs 2*item + (j & 1)
+        const float u = __shfl_down_sync(0xffffffffu, v, 2);
+        if (!active) continue;
+        if (swiglu) {
+          if (j < 2) {
+            const int nout = N >> 1, oi = item * 2 + j;
+            if (oi < nout)
+              reinterpret_cast<__nv_bfloat16*>(out)[(size_t)m * nout + oi] =
+                  __float2bfloat16(v / (1.f + __expf(-v)) * u);
+          }
+        } else {
           const int r = item_row(item, j, false);
-          if (r >= N) continue;
-          const float v = pb[j * 16 + m] + pb[(j + 4) * 16 + m];
-          const size_t idx = (size_t)m * N + r;
-          if (epi == SWB_EPI_BF16)
-            reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(v);
-          else if (epi == SWB_EPI_F32)
-            reinterpret_cast<float*>(out)[idx] = v;
-          else
-            reinterpret_cast<float*>(out)[idx] = resid[idx] + v;
+          if (r < N) {
+            const size_t idx = (size_t)m * N + r;
+            if (epi == SWB_EPI_BF16)
+              reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(v);
+            else if (epi == SWB_EPI_F32)
+              reinterpret_cast<float*>(out)[idx] = v;
+            else
+              reinterpret_cast<float*>(out)[idx] = resid[idx] + v;
+          }
         }
       }
     }
   }
 }
 
-template <int MB>
-static int launch_gemv(const __nv_bfloat16* x, const __nv_bfloat16* w, void* out,
-                       const float* r, int M, int N, int K, int epi, int items,
-                       cudaStream_t s) {
+template <int MB, bool NORM>
+static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
+                       const __nv_bfloat16* w, void* out, const float* r, int M, int N, int K,
+                       int epi, int items, cudaStream_t s) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr[dev]) {
-    SWB_CUDA(cudaFuncSetAttribute(gemv_bulk_kernel<MB>,
+    SWB_CUDA(cudaFuncSetAttribute(gemv_bulk_kernel<MB, NORM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, TV_SMEM));
     attr[dev] = true;
   }
-  const int grid = min(items, kNumSMs);  // 1 CTA/SM: leaves room for the next kernel
-  {
-    const cudaError_t le_ = launch(gemv_bulk_kernel<MB>, dim3(grid), dim3(TV_THREADS), TV_SMEM, s,
-        x, w, out, r, M, N, K, epi, items);
-    if (le_ != cudaSuccess)
-      return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le_));
-  }
+  const int grid = min(items, TV_CTAS_PER_SM * kNumSMs);
+  const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM>, dim3(grid), dim3(TV_THREADS),
+                                TV_SMEM, s, x, nw, eps, w, out, r, M, N, K, epi, items);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("gemv_bulk_kernel");
+}
+
+template <bool NORM>
+static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, const void* w,
+                         void* out, const void* resid, int M, int N, int K, int epilogue,
+                         uintptr_t stream) {
+  const int items = (N + TV_ROWS - 1) / TV_ROWS;  // 4 rows (or 2 SwiGLU outputs) per item
+  auto ws = reinterpret_cast<const __nv_bfloat16*>(w);
+  auto rs = reinterpret_cast<const float*>(resid);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (M == 1) return launch_gemv<1, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
+  if (M <= 2) return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
+  if (M <= 4) return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
+  if (M <= 8) return launch_gemv<8, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
+  return launch_gemv<16, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
 }
 
 }  // namespace swb
 
 using namespace swb;
 
-extern "C" int swb_gemv_bf16(const void* x, const void* w, void* out,
-                             const void* resid, int M, int N, int K, int epilogue,
-                             uintptr_t stream) {
-  SWB_REQUIRE(x && w && out, "swb_gemv_bf16: null pointer");
-  SWB_REQUIRE(M >= 1 && M <= 16, "swb_gemv_bf16: M=%d outside 1..16", M);
-  SWB_REQUIRE(N > 0 && K > 0 && K % 8 == 0, "swb_gemv_bf16: bad shape N=%d K=%d", N, K);
-  SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_SWIGLU,
-              "swb_gemv_bf16: bad epilogue %d", epilogue);
-  SWB_REQUIRE(epilogue != SWB_EPI_SWIGLU || N % 256 == 0,
-              "swb_gemv_bf16: SwiGLU needs N %% 256 == 0");
-  SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid, "swb_gemv_bf16: resid needed");
-  SWB_REQUIRE((((uintptr_t)x | (uintptr_t)w) & 15) == 0,
-              "swb_gemv_bf16: pointers must be 16-byte aligned");
-  const int items = (N + TV_ROWS - 1) / TV_ROWS;  // 4 rows (or 2 SwiGLU outputs) per item
-  auto xs = reinterpret_cast<const __nv_bfloat16*>(x);
-  auto ws = reinterpret_cast<const __nv_bfloat16*>(w);
-  auto rs = reinterpret_cast<const float*>(resid);
-  cudaStream_t s = (cudaStream_t)stream;
-  if (M == 1) return launch_gemv<1>(xs, ws, out, rs, M, N, K, epilogue, items, s);
-  if (M <= 2) return launch_gemv<2>(xs, ws, out, rs, M, N, K, epilogue, items, s);
-  if (M <= 4) return launch_gemv<4>(xs, ws, out, rs, M, N, K, epilogue, items, s);
-  if (M <= 8) return launch_gemv<8>(xs, ws, out, rs, M, N, K, epilogue, items, s);
-  return launch_gemv<16>(xs, ws, out, rs, M, N, K, epilogue, items, s);
+static int check_gemv_args(const char* fn, const void* x, const void* w, void* out,
+                           const void* resid, int M, int N, int K, int epilogue) {
+  SWB_REQUIRE(x && w && out, "%s: null pointer", fn);
+  SWB_REQUIRE(M >= 1 && M <= 16, "%s: M=%d outside 1..16", fn, M);
+  SWB_REQUIRE(N > 0 && K > 0 && K % 8 == 0, "%s: bad shape N=%d K=%d", fn, N, K);
+  SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_SWIGLU, "%s: bad epilogue %d",
+              fn, epilogue);
+  SWB_REQUIRE(epilogue != SWB_EPI_SWIGLU || N % 256 == 0, "%s: SwiGLU needs N %% 256 == 0", fn);
+  SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid, "%s: resid needed", fn);
+  SWB_REQUIRE((((uintptr_t)x | (uintptr_t)w) & 15) == 0, "%s: pointers must be 16-byte aligned",
+              fn);
+  return SWB_OK;
+}
+
+extern "C" int swb_gemv_bf16(const void* x, const void* w, void* out, const void* resid, int M,
+                             int N, int K, int epilogue, uintptr_t stream) {
+  const int st = check_gemv_args("swb_gemv_bf16", x, w, out, resid, M, N, K, epilogue);
+  if (st) return st;
+  return dispatch_gemv<false>(x, nullptr, 0.f, w, out, resid, M, N, K, epilogue, stream);
+}
+
+extern "C" int swb_gemv_rmsnorm_bf16(const float* x, const void* norm_w, float eps,
+                                     const void* w, void* out, const void* resid, int M, int N,
+                                     int K, int epilogue, uintptr_t stream) {
+  const int st = check_gemv_args("swb_gemv_rmsnorm_bf16", x, w, out, resid, M, N, K, epilogue);
+  if (st) return st;
+  SWB_REQUIRE(norm_w && (((uintptr_t)norm_w) & 15) == 0,
+              "swb_gemv_rmsnorm_bf16: norm weight must be 16-byte aligned");
+  SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid != x,
+              "swb_gemv_rmsnorm_bf16: output may not alias the normalized input");
+  return dispatch_gemv<true>(x, reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, w, out,
+                             resid, M, N, K, epilogue, stream);
 }

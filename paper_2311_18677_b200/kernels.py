@@ -11,7 +11,7 @@ from . import _abi
 from ._abi import EPI_BF16, EPI_F32, EPI_RESID_F32, EPI_SWIGLU, call
 from .errors import ValidationError
 
-__all__ = ["gemm", "gemv", "linear", "embed", "rmsnorm", "argmax", "rope_kv_write",
+__all__ = ["gemm", "gemv", "gemv_rmsnorm", "linear", "embed", "rmsnorm", "argmax", "rope_kv_write",
            "kv_push_layer", "attn_prefill", "attn_decode", "decode_prepare",
            "decode_advance", "slots_from_table", "kv_signal", "stream_wait_flag",
            "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "GEMV_MAX_ROWS"]
@@ -66,6 +66,21 @@ def gemv(x, w, epi=EPI_BF16, out=None, resid=None):
         out = _alloc_out(x, M, N, epi)
     call("swb_gemv_bf16", x.data_ptr(), w.data_ptr(), out.data_ptr(),
          resid.data_ptr() if resid is not None else None, M, N, K, epi, _stream())
+    return out
+
+
+def gemv_rmsnorm(x, norm_w, eps, w, epi=EPI_BF16, out=None, resid=None):
+    """Decode pre-norm linear: out = epi(rmsnorm(x fp32) @ w^T), one kernel."""
+    _req(x, torch.float32, "x")
+    _req(w, torch.bfloat16, "w")
+    _req(norm_w, torch.bfloat16, "norm_w")
+    M, K = x.shape
+    N = w.shape[0]
+    if out is None:
+        out = _alloc_out(x, M, N, epi)
+    call("swb_gemv_rmsnorm_bf16", x.data_ptr(), norm_w.data_ptr(), float(eps), w.data_ptr(),
+         out.data_ptr(), resid.data_ptr() if resid is not None else None, M, N, K, epi,
+         _stream())
     return out
 
 
@@ -141,11 +156,17 @@ def attn_decode_workspace_bytes(B, H, max_ctx, partition, dh):
 
 
 def attn_decode(qkv, k_layer, v_layer, block_tables, ctx_lens, B, H, Hkv, dh, block_size,
-                scale, max_ctx, partition, workspace, out=None):
+                scale, max_ctx, partition, workspace, out=None, positions=None, slots=None,
+                theta=10000.0):
+    """Paged decode attention; with positions/slots it also applies RoPE to the
+    current token and appends its K/V to the pool (one kernel per layer).
+    ``workspace`` must be zero-initialised once (merge tickets)."""
     if out is None:
         out = torch.empty(B, H * dh, dtype=torch.bfloat16, device=qkv.device)
     call("swb_attn_decode", qkv.data_ptr(), qkv.shape[1], k_layer, v_layer,
-         block_tables.data_ptr(), block_tables.shape[1], ctx_lens.data_ptr(), B, H, Hkv, dh,
+         block_tables.data_ptr(), block_tables.shape[1], ctx_lens.data_ptr(),
+         positions.data_ptr() if positions is not None else None,
+         slots.data_ptr() if slots is not None else None, float(theta), B, H, Hkv, dh,
          block_size, float(scale), max_ctx, partition, workspace.data_ptr(), out.data_ptr(),
          _stream())
     return out

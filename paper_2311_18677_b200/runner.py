@@ -22,6 +22,7 @@ advance) is captured once in a CUDA graph and replayed; all per-step state
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -253,22 +254,37 @@ class DecodeGraph:
         K.decode_prepare(self.ctx, self.tables, kv.block_size, B, self.pos, self.slots,
                          self.attn_len)
         K.embed(self.cur_tok, w.embed, out=self.x)
+        # pre-norm folded into the weight-streaming GEMV: opt-in (SWB_FUSED_NORM=1);
+        # measured slower on 7B (its per-CTA sum-of-squares prologue is serial)
+        fused = B <= K.GEMV_MAX_ROWS and os.environ.get("SWB_FUSED_NORM", "0") == "1"
         for li, lw in enumerate(w.layers):
-            K.rmsnorm(self.x, lw.attn_norm, cfg.norm_eps, out=self.h)
-            K.linear(self.h, lw.wqkv, K.EPI_BF16, out=self.qkv)
-            K.rope_kv_write(self.qkv, self.pos, r.hq, r.hkv, r.dh, cfg.rope_theta,
-                            kv.k_layer_ptr(li), kv.v_layer_ptr(li), self.slots, kv.block_size)
+            if fused:
+                K.gemv_rmsnorm(self.x, lw.attn_norm, cfg.norm_eps, lw.wqkv, K.EPI_BF16,
+                               out=self.qkv)
+            else:
+                K.rmsnorm(self.x, lw.attn_norm, cfg.norm_eps, out=self.h)
+                K.linear(self.h, lw.wqkv, K.EPI_BF16, out=self.qkv)
+            # RoPE + KV append of the current token + attention + split-K merge
             K.attn_decode(self.qkv, kv.k_layer_ptr(li), kv.v_layer_ptr(li), self.tables,
                           self.attn_len, B, r.hq, r.hkv, r.dh, kv.block_size, r.scale,
-                          self.max_ctx, r.partition, self.ws, out=self.attn)
+                          self.max_ctx, r.partition, self.ws, out=self.attn,
+                          positions=self.pos, slots=self.slots, theta=cfg.rope_theta)
             K.linear(self.attn, lw.wo, r._resid_epi(), out=self.x, resid=self.x)
             r._allreduce(self.x)
-            K.rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, out=self.h)
-            K.linear(self.h, lw.wgu, K.EPI_SWIGLU, out=self.act)
+            if fused:
+                K.gemv_rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, lw.wgu, K.EPI_SWIGLU,
+                               out=self.act)
+            else:
+                K.rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, out=self.h)
+                K.linear(self.h, lw.wgu, K.EPI_SWIGLU, out=self.act)
             K.linear(self.act, lw.wd, r._resid_epi(), out=self.x, resid=self.x)
             r._allreduce(self.x)
-        K.rmsnorm(self.x, w.final_norm, cfg.norm_eps, out=self.h)
-        K.linear(self.h, w.lm_head, K.EPI_F32, out=self.logits)
+        if fused:
+            K.gemv_rmsnorm(self.x, w.final_norm, cfg.norm_eps, w.lm_head, K.EPI_F32,
+                           out=self.logits)
+        else:
+            K.rmsnorm(self.x, w.final_norm, cfg.norm_eps, out=self.h)
+            K.linear(self.h, w.lm_head, K.EPI_F32, out=self.logits)
         K.argmax(self.logits, out=self.next_tok)
         K.decode_advance(self.next_tok, self.cur_tok, self.ctx, self.step, self.out_ring, B)
 

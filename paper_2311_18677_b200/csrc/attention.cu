@@ -63,6 +63,14 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4],
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // load a 64-row x 128-col bf16 tile (rows [r0, r0+64) of a strided matrix,
 // rows >= rmax zero-filled) into swizzled smem
 __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* g,
@@ -303,6 +311,13 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
   float* ss = sq + G * DA_D;                                           // [G][part]
   float* sacc = ss + G * part;                                         // [WARPS][G][128]
   float* sstat = sacc + DA_WARPS * G * DA_D;                           // [G][2]
+  __shared__ uint64_t kv_bar_s;
+  uint64_t* kv_bar = &kv_bar_s;
+  if (threadIdx.x == 0) {
+    mbar_init(kv_bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
 
   if (t0 >= t1) {
     if (threadIdx.x < G) {
@@ -314,18 +329,23 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
     const int ntok = t1 - t0;
     const int cur = pos ? pos[b] : -1;            // current token position
     const bool own_cur = cur >= t0 && cur < t1;
-    // ---- issue every K/V load of the partition (16 B chunks)
+    // ---- gather the partition: one bulk copy per (block, kv head) tile —
+    // 16 tokens x 256 B contiguous in the pool — issued by warp 0's lanes in
+    // parallel (per-thread 16-byte cp.async was issue-bound here)
     const int32_t* trow = tables + (size_t)b * max_blocks;
-    for (int c = threadIdx.x; c < ntok * 16; c += blockDim.x) {
-      const int tt = c >> 4, ch = c & 15;
-      const int tok = t0 + tt;
-      if (tok == cur) continue;                   // provided from registers below
-      const int blk = __ldg(trow + tok / bs);
-      const size_t g = (((size_t)blk * Hkv + kh) * bs + tok % bs) * DA_D + ch * 8;
-      cp_async16(smem_u32(sk + tt * DA_D + ch * 8), kpool + g, true);
-      cp_async16(smem_u32(sv + tt * DA_D + ch * 8), vpool + g, true);
+    const int lbs = __ffs(bs) - 1;
+    if (warp == 0) {
+      const int nblk = (ntok + bs - 1) >> lbs;
+      const uint32_t tile = (uint32_t)bs * DA_D * 2;
+      if (lane == 0) mbar_arrive_expect_tx(kv_bar, 2 * tile * nblk);
+      __syncwarp();
+      for (int j = lane; j < nblk; j += 32) {
+        const int blk = __ldg(trow + (t0 >> lbs) + j);
+        const size_t g = ((size_t)blk * Hkv + kh) * bs * DA_D;
+        bulk_g2s(sk + (size_t)j * bs * DA_D, kpool + g, tile, kv_bar);
+        bulk_g2s(sv + (size_t)j * bs * DA_D, vpool + g, tile, kv_bar);
+      }
     }
-    cp_async_commit();
     // ---- q of the group (rotated), scaled by softmax scale * log2(e)
     const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
     const float fpos = (float)cur;
@@ -354,7 +374,9 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
         sq[gi * DA_D + 64 + i0 + j] = hi[j] * scale_log2;
       }
     }
-    // ---- current token: rotate k, write k/v to the pool and into smem
+    // ---- current token: rotate k, write k/v to the pool, then (after the
+    // gather landed) patch it into the smem tile
+    mbar_wait(kv_bar, 0);
     if (own_cur && threadIdx.x < 16) {
       const int i0 = threadIdx.x * 4;           // 16 threads x 4 pairs = 64 pairs
       const __nv_bfloat16* kp = qrow + (H + kh) * DA_D;
@@ -367,7 +389,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
       }
       rope4(lo, hi, i0, fpos, log2_theta);
       const int slot = slots[b];
-      const size_t g = (((size_t)(slot / bs) * Hkv + kh) * bs + slot % bs) * DA_D;
+      const size_t g = (((size_t)(slot >> lbs) * Hkv + kh) * bs + (slot & (bs - 1))) * DA_D;
       const int tt = cur - t0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -382,7 +404,6 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
         sv[tt * DA_D + 64 + i0 + j] = vp[64 + i0 + j];
       }
     }
-    cp_async_wait<0>();
     __syncthreads();
 
     // ---- scores: half-warp per token
@@ -557,6 +578,8 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, v
   SWB_REQUIRE((positions == nullptr) == (slots == nullptr),
               "swb_attn_decode: positions and slots go together");
   SWB_REQUIRE(!positions || theta > 1.f, "swb_attn_decode: theta");
+  SWB_REQUIRE((block_size & (block_size - 1)) == 0 && partition % block_size == 0,
+              "swb_attn_decode: block_size must be a power of two dividing partition");
   const int G = H / Hkv;
   const int NP = (max_ctx + partition - 1) / partition;
   const size_t smem = (size_t)partition * DA_D * 2 * 2 +

@@ -17,6 +17,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cudaTypedefs.h>
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -27,100 +28,25 @@ constexpr int G_A_BYTES = GM * GK * 2;  // 16 KB
 constexpr int G_B_BYTES = GN * GK * 2;  // 32 KB
 constexpr int G_STAGE_BYTES = G_A_BYTES + G_B_BYTES;
 constexpr int G_SMEM_BYTES = GSTAGES * G_STAGE_BYTES + 1024 + 256;
-constexpr uint32_t G_TMEM_COLS = 256;
+constexpr uint32_t G_TMEM_COLS = 512;   // two 256-column fp32 accumulators
+constexpr int G_THREADS = 192;          // TMA warp, MMA warp, 4 epilogue warps
 
 struct GemmArgs {
   void* out;
   const float* resid;
   int M, N, K;
   int epi;
+  int m_tiles, tiles;
 };
 
 __device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
 
-__global__ void __launch_bounds__(128, 1)
-    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmW, GemmArgs args) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + GSTAGES * G_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GSTAGES * G_STAGE_BYTES);
-  uint64_t* empty = full + GSTAGES;
-  uint64_t* done = empty + GSTAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  // M-fastest rasterization: the CTAs resident at once share weight tiles
-  // (each W tile is fetched from HBM ~once and re-served from L2), while the
-  // small activation matrix stays L2-resident.
-  const int m0 = blockIdx.x * GM;
-  const int n0 = blockIdx.y * GN;
-  const int num_k = (args.K + GK - 1) / GK;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmW);
-    for (int s = 0; s < GSTAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<G_TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_trigger();
-  pdl_wait();  // A (activations) is produced by the previous kernel
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % GSTAGES;
-        if (kb >= GSTAGES) mbar_wait(&empty[s], ((kb / GSTAGES) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], G_STAGE_BYTES);
-        tma_load_2d(sA + s * G_A_BYTES, &tmA, &full[s], kb * GK, m0);
-        tma_load_2d(sB + s * G_B_BYTES, &tmW, &full[s], kb * GK, n0);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (single thread)
-      constexpr uint32_t idesc = umma_idesc_bf16(GM, GN);
-      for (int kb = 0; kb < num_k; ++kb) {
-        const int s = kb % GSTAGES;
-        mbar_wait(&full[s], (kb / GSTAGES) & 1);
-        tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + s * G_A_BYTES);
-        const uint32_t b_base = smem_u32(sB + s * G_B_BYTES);
-#pragma unroll
-        for (int k = 0; k < GK / 16; ++k) {
-          // K-major SW128: advancing 16 bf16 along K = +32 B start address.
-          tc_mma_f16(tmem, umma_desc_k_sw128(a_base + k * 32),
-                     umma_desc_k_sw128(b_base + k * 32), idesc,
-                     (kb | k) != 0);
-        }
-        tc_commit(&empty[s]);
-      }
-      tc_commit(done);
-    }
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: TMEM -> registers -> global
-  mbar_wait(done, 0);
-  tc_fence_after();
-  const int row = m0 + warp * 32 + lane;
-  const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+// Epilogue of one 128 x 256 tile held in TMEM columns [acc_col, acc_col+256):
+// this warp owns TMEM lanes (= tile rows) 32*(warp%4) .. +31.
+__device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t t_row, int row,
+                                              int n0) {
   const bool row_ok = row < args.M;
   uint32_t r[32];
-
   if (args.epi == SWB_EPI_SWIGLU) {
     // tile cols [0,128) = gate, [128,256) = up for outputs n0/2 + [0,128)
     const int nout = args.N >> 1;
@@ -136,8 +62,8 @@ __global__ void __launch_bounds__(128, 1)
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float g0 = __uint_as_float(r[2 * i]), g1 = __uint_as_float(r[2 * i + 1]);
-          float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+          const float g0 = __uint_as_float(r[2 * i]), g1 = __uint_as_float(r[2 * i + 1]);
+          const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
           packed[i] = f2_to_bf2(silu(g0) * u0, silu(g1) * u1);
         }
         uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * nout + col);
@@ -147,48 +73,150 @@ __global__ void __launch_bounds__(128, 1)
                               packed[4 * i + 3]);
       }
     }
-  } else {
+    return;
+  }
 #pragma unroll 1
-    for (int c = 0; c < GN / 32; ++c) {
-      tmem_ld32(t_row + c * 32, r);
-      tc_wait_ld();
-      const int col = n0 + c * 32;
-      if (!row_ok || col >= args.N) continue;
-      if (args.epi == SWB_EPI_BF16) {
-        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out);
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * args.N + col);
+  for (int c = 0; c < GN / 32; ++c) {
+    tmem_ld32(t_row + c * 32, r);
+    tc_wait_ld();
+    const int col = n0 + c * 32;
+    if (!row_ok || col >= args.N) continue;
+    if (args.epi == SWB_EPI_BF16) {
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out);
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * args.N + col);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(
-              f2_to_bf2(__uint_as_float(r[8 * i + 0]), __uint_as_float(r[8 * i + 1])),
-              f2_to_bf2(__uint_as_float(r[8 * i + 2]), __uint_as_float(r[8 * i + 3])),
-              f2_to_bf2(__uint_as_float(r[8 * i + 4]), __uint_as_float(r[8 * i + 5])),
-              f2_to_bf2(__uint_as_float(r[8 * i + 6]), __uint_as_float(r[8 * i + 7])));
-      } else {
-        float* out = reinterpret_cast<float*>(args.out) + (size_t)row * args.N + col;
-        if (args.epi == SWB_EPI_RESID_F32) {
-          const float4* res = reinterpret_cast<const float4*>(
-              args.resid + (size_t)row * args.N + col);
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_uint4(
+            f2_to_bf2(__uint_as_float(r[8 * i + 0]), __uint_as_float(r[8 * i + 1])),
+            f2_to_bf2(__uint_as_float(r[8 * i + 2]), __uint_as_float(r[8 * i + 3])),
+            f2_to_bf2(__uint_as_float(r[8 * i + 4]), __uint_as_float(r[8 * i + 5])),
+            f2_to_bf2(__uint_as_float(r[8 * i + 6]), __uint_as_float(r[8 * i + 7])));
+    } else {
+      float* out = reinterpret_cast<float*>(args.out) + (size_t)row * args.N + col;
+      if (args.epi == SWB_EPI_RESID_F32) {
+        const float4* res =
+            reinterpret_cast<const float4*>(args.resid + (size_t)row * args.N + col);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 v = res[i];
-            v.x += __uint_as_float(r[4 * i + 0]);
-            v.y += __uint_as_float(r[4 * i + 1]);
-            v.z += __uint_as_float(r[4 * i + 2]);
-            v.w += __uint_as_float(r[4 * i + 3]);
-            reinterpret_cast<float4*>(out)[i] = v;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            reinterpret_cast<float4*>(out)[i] =
-                make_float4(__uint_as_float(r[4 * i + 0]), __uint_as_float(r[4 * i + 1]),
-                            __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        for (int i = 0; i < 8; ++i) {
+          float4 v = res[i];
+          v.x += __uint_as_float(r[4 * i + 0]);
+          v.y += __uint_as_float(r[4 * i + 1]);
+          v.z += __uint_as_float(r[4 * i + 2]);
+          v.w += __uint_as_float(r[4 * i + 3]);
+          reinterpret_cast<float4*>(out)[i] = v;
         }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          reinterpret_cast<float4*>(out)[i] =
+              make_float4(__uint_as_float(r[4 * i + 0]), __uint_as_float(r[4 * i + 1]),
+                          __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
       }
     }
   }
+}
 
+// Persistent: one CTA per SM walks the 128 x 256 tiles in M-fastest order
+// (CTAs resident together share weight tiles through L2).  Warp 0 = TMA
+// producer, warp 1 = single-thread tcgen05.mma issuer, warps 2..5 = epilogue.
+// Two TMEM accumulators let the epilogue of tile i overlap the MMAs of tile
+// i+1 (tmem_full / tmem_empty mbarriers).
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmW, GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + GSTAGES * G_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GSTAGES * G_STAGE_BYTES);
+  uint64_t* empty = full + GSTAGES;
+  uint64_t* tfull = empty + GSTAGES;     // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_k = (args.K + GK - 1) / GK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < GSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<G_TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // A (activations) is produced by the previous kernel
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < args.tiles; t += gridDim.x) {
+        const int m0 = (t % args.m_tiles) * GM, n0 = (t / args.m_tiles) * GN;
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % GSTAGES;
+          if (it >= GSTAGES) mbar_wait_sleep(&empty[s], ((it / GSTAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], G_STAGE_BYTES);
+          tma_load_2d(sA + s * G_A_BYTES, &tmA, &full[s], kb * GK, m0);
+          tma_load_2d(sB + s * G_B_BYTES, &tmW, &full[s], kb * GK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer (single thread)
+      constexpr uint32_t idesc = umma_idesc_bf16(GM, GN);
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < args.tiles; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        if (i >= 2) mbar_wait(&tempty[acc], ((i >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * GN;
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % GSTAGES;
+          mbar_wait(&full[s], (it / GSTAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * G_A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * G_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GK / 16; ++k) {
+            // K-major SW128: advancing 16 bf16 along K = +32 B start address.
+            tc_mma_f16(d_tmem, umma_desc_k_sw128(a_base + k * 32),
+                       umma_desc_k_sw128(b_base + k * 32), idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps: TMEM -> registers -> global
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int i = 0;
+    for (int t = blockIdx.x; t < args.tiles; t += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const int m0 = (t % args.m_tiles) * GM, n0 = (t / args.m_tiles) * GN;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+      gemm_epilogue(args, tmem + acc * GN + ((uint32_t)(q * 32) << 16), m0 + q * 32 + lane, n0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<G_TMEM_COLS>(tmem);
@@ -266,10 +294,12 @@ extern "C" int swb_gemm_bf16(const void* a, const void* w, void* out,
                                   G_SMEM_BYTES));
     attr_set[dev] = true;
   }
-  GemmArgs args{out, reinterpret_cast<const float*>(resid), M, N, K, epilogue};
-  dim3 grid((M + GM - 1) / GM, (N + GN - 1) / GN);
+  const int m_tiles = (M + GM - 1) / GM, n_tiles = (N + GN - 1) / GN;
+  GemmArgs args{out, reinterpret_cast<const float*>(resid), M, N, K, epilogue, m_tiles,
+                m_tiles * n_tiles};
+  dim3 grid(std::min(args.tiles, kNumSMs));
   {
-    const cudaError_t le_ = launch(gemm_bf16_tcgen05, dim3(grid), dim3(128), G_SMEM_BYTES, (cudaStream_t)stream,
+    const cudaError_t le_ = launch(gemm_bf16_tcgen05, dim3(grid), dim3(G_THREADS), G_SMEM_BYTES, (cudaStream_t)stream,
         ta, tw, args);
     if (le_ != cudaSuccess)
       return swb_set_error(SWB_ERR_CUDA, "launch gemm_bf16_tcgen05: %s", cudaGetErrorString(le_));

@@ -21,10 +21,13 @@
 namespace swb {
 
 // ============================================================ prefill
-constexpr int PA_BQ = 64, PA_BK = 64, PA_D = 128;
-constexpr int PA_ROW_BYTES = PA_D * 2;              // 256 B
-constexpr int PA_TILE_BYTES = PA_BQ * PA_ROW_BYTES;  // 16 KB
-constexpr int PA_SMEM = PA_TILE_BYTES * 5;           // Q + 2xK + 2xV
+constexpr int PA_BQ = 128, PA_BK = 64, PA_D = 128;
+constexpr int PA_WARPS = PA_BQ / 16;                 // 16 query rows per warp
+constexpr int PA_THREADS = PA_WARPS * 32;
+constexpr int PA_ROW_BYTES = PA_D * 2;               // 256 B
+constexpr int PA_Q_BYTES = PA_BQ * PA_ROW_BYTES;     // 32 KB
+constexpr int PA_KV_BYTES = PA_BK * PA_ROW_BYTES;    // 16 KB
+constexpr int PA_SMEM = PA_Q_BYTES + 4 * PA_KV_BYTES;  // Q + 2xK + 2xV
 
 __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return row * PA_ROW_BYTES + ((chunk ^ (row & 7)) << 4);
@@ -71,13 +74,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// load a 64-row x 128-col bf16 tile (rows [r0, r0+64) of a strided matrix,
+// load a ROWS x 128-col bf16 tile (rows [r0, r0+ROWS) of a strided matrix,
 // rows >= rmax zero-filled) into swizzled smem
+template <int ROWS>
 __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* g,
                                           int stride, int r0, int rmax) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int idx = threadIdx.x + i * 128;  // 0..1023
+  for (int i = 0; i < ROWS * 16 / PA_THREADS; ++i) {
+    const int idx = threadIdx.x + i * PA_THREADS;
     const int row = idx >> 4, chunk = idx & 15;
     const bool valid = r0 + row < rmax;
     const __nv_bfloat16* src = g + (size_t)(valid ? r0 + row : 0) * stride + chunk * 8;
@@ -85,7 +89,7 @@ __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* g
   }
 }
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(PA_THREADS)
     attn_prefill_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                         const int32_t* __restrict__ cu, int tiles_per_seq, int H,
                         int Hkv, float scale_log2, __nv_bfloat16* __restrict__ out) {
@@ -102,15 +106,15 @@ __global__ void __launch_bounds__(128)
   if (q0 >= len) return;
 
   const uint32_t sQ = smem_u32(sm);
-  const uint32_t sK[2] = {sQ + PA_TILE_BYTES, sQ + 2 * PA_TILE_BYTES};
-  const uint32_t sV[2] = {sQ + 3 * PA_TILE_BYTES, sQ + 4 * PA_TILE_BYTES};
+  const uint32_t sK[2] = {sQ + PA_Q_BYTES, sQ + PA_Q_BYTES + PA_KV_BYTES};
+  const uint32_t sV[2] = {sQ + PA_Q_BYTES + 2 * PA_KV_BYTES, sQ + PA_Q_BYTES + 3 * PA_KV_BYTES};
   const __nv_bfloat16* gq = qkv + (size_t)s0 * rs + h * PA_D;
   const __nv_bfloat16* gk = qkv + (size_t)s0 * rs + (H + kh) * PA_D;
   const __nv_bfloat16* gv = qkv + (size_t)s0 * rs + (H + Hkv + kh) * PA_D;
 
-  load_tile(sQ, gq, rs, q0, len);
-  load_tile(sK[0], gk, rs, 0, len);
-  load_tile(sV[0], gv, rs, 0, len);
+  load_tile<PA_BQ>(sQ, gq, rs, q0, len);
+  load_tile<PA_BK>(sK[0], gk, rs, 0, len);
+  load_tile<PA_BK>(sV[0], gv, rs, 0, len);
   cp_async_commit();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -120,13 +124,14 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-  const int nkv = qt + 1;  // causal: tiles 0..qt
+  // causal: key tiles up to the one holding this query tile's last row
+  const int nkv = (min(q0 + PA_BQ, len) - 1) / PA_BK + 1;
 
   for (int j = 0; j < nkv; ++j) {
     const int buf = j & 1;
     if (j + 1 < nkv) {
-      load_tile(sK[buf ^ 1], gk, rs, (j + 1) * PA_BK, len);
-      load_tile(sV[buf ^ 1], gv, rs, (j + 1) * PA_BK, len);
+      load_tile<PA_BK>(sK[buf ^ 1], gk, rs, (j + 1) * PA_BK, len);
+      load_tile<PA_BK>(sV[buf ^ 1], gv, rs, (j + 1) * PA_BK, len);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -157,9 +162,10 @@ __global__ void __launch_bounds__(128)
         mma_bf16(s[2 * np + 1], qf[kk], b2, b3);
       }
     }
-    // causal mask on the diagonal tile (also masks keys beyond len)
+    // causal mask on tiles that reach past this warp's first row (also masks
+    // keys beyond len)
     const int qrow0 = q0 + warp * 16 + g;
-    if (j == qt) {
+    if ((j + 1) * PA_BK > q0 + warp * 16) {
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
         const int key = j * PA_BK + nt * 8 + 2 * t;
@@ -543,7 +549,7 @@ extern "C" int swb_attn_prefill(const void* qkv, int row_stride, const int32_t* 
   const int tiles = (max_seqlen + PA_BQ - 1) / PA_BQ;
   dim3 grid(num_seqs * tiles, H);
   {
-    const cudaError_t le_ = launch(attn_prefill_kernel, dim3(grid), dim3(128), PA_SMEM, (cudaStream_t)stream,
+    const cudaError_t le_ = launch(attn_prefill_kernel, dim3(grid), dim3(PA_THREADS), PA_SMEM, (cudaStream_t)stream,
         
       reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride, cu_seqlens, tiles, H, Hkv,
       scale * 1.4426950408889634f, reinterpret_cast<__nv_bfloat16*>(out));

@@ -39,27 +39,26 @@ constexpr int kNumSMs = 148;
 
 // ---------------------------------------------------------------- PDL
 // Every kernel of the library is launched with programmatic stream
-// serialization: it triggers its dependents as soon as it starts, so the next
-// kernel's CTAs become resident and run their prologue (barrier init, TMEM
-// alloc, static-weight prefetch) while this one drains; each kernel calls
-// pdl_wait() before its first global read of produced data or any global
-// write, which preserves stream order transitively.
+// serialization, so a kernel's launch and prologue (barrier init, TMEM
+// alloc, static-weight prefetch) overlap the previous kernel's tail; each
+// kernel calls pdl_wait() before its first global read of produced data or
+// any global write, which preserves stream order transitively.
 __device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
-__device__ __forceinline__ void pdl_trigger() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+// Early triggering (dependents launched as soon as this kernel starts) was
+// measured slower on the decode chain; without an explicit trigger a kernel
+// triggers implicitly as its CTAs exit, so the dependent launch still
+// overlaps this kernel's tail and the completion flush.
+__device__ __forceinline__ void pdl_trigger() {}
 
-// Opt-in: SWB_PDL=1 in the environment sets the attribute.  Measured on the
-// 7B decode graph (bench A/B, profiles/): early-trigger PDL made the full
-// step slower (4.39 vs 3.83 ms) although back-to-back GEMVs gained ~1 us
-// each, so the default is plain stream order; griddepcontrol.wait is a no-op
-// then.
+// SWB_PDL=0 in the environment drops the attribute (A/B).  Measured on the 7B
+// decode graph: implicit (exit-time) trigger 3.19 ms/step vs 3.31 ms without
+// PDL; early triggering was 4.39 vs 3.83 ms (dependents occupied SM slots).
 inline bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("SWB_PDL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }

@@ -341,6 +341,8 @@ def main():
     ap.add_argument("--prompt", type=int, default=1024)
     ap.add_argument("--out", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--tp", type=int, default=1,
+                    help="tensor-parallel degree of each prompt/token machine (N >= 2*tp)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

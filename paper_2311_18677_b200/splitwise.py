@@ -33,6 +33,7 @@ import torch.distributed as dist
 
 from . import _abi
 from . import kernels as K
+from .control import HandoffReceiver, HandoffSender, recv_reservations, send_reservations
 from .kvcache import KVCacheManager, blocks_for
 from .model import get_config, init_weights
 from .perf import PerfModel
@@ -62,9 +63,10 @@ def estimated_perf_model(cfg, kv: KVCacheManager | None, weight_bytes: int,
 
 class PromptServer:
     def __init__(self, runner: ModelRunner, peer: KVCacheManager, ctrl, token_rank: int,
-                 sched: SchedulerConfig):
+                 sched: SchedulerConfig, mailbox: str):
         self.runner = runner
         self.peer = peer
+        self.tx = HandoffSender(mailbox)
         self.ctrl = ctrl
         self.token_rank = token_rank
         cfg = runner.cfg
@@ -77,9 +79,8 @@ class PromptServer:
         """requests: list of (rid, host int32 prompt, n_out).  Returns
         {rid: first-token host time}."""
         dev = self.runner.dev
-        seqs = torch.empty(len(requests), dtype=torch.int32)
-        dist.recv(seqs, src=self.token_rank, group=self.ctrl)     # reservations
-        seq_of = {r[0]: int(s) for r, s in zip(requests, seqs)}
+        seqs = recv_reservations(len(requests), self.token_rank, self.ctrl)
+        seq_of = {r[0]: s for r, s in zip(requests, seqs)}
         by_id = {r[0]: r for r in requests}
         now_ms = 0.0
         for rid, prompt, n_out in requests:
@@ -107,11 +108,8 @@ class PromptServer:
             tnow = time.perf_counter()
             self.runner.finish_push_stats()
             self.push_log.append(st)
-            msg = torch.tensor([[r[0], seq_of[r[0]], len(r[1]), int(fh[j]), r[2]]
-                                for j, r in enumerate(chunk)], dtype=torch.int32)
-            dist.send(torch.tensor([len(chunk)], dtype=torch.int32), dst=self.token_rank,
-                      group=self.ctrl)
-            dist.send(msg, dst=self.token_rank, group=self.ctrl)
+            self.tx.send([(r[0], seq_of[r[0]], len(r[1]), int(fh[j]), r[2])
+                          for j, r in enumerate(chunk)])
             for r in chunk:
                 first_time[r[0]] = tnow
             now_ms = (tnow - t0) * 1e3
@@ -120,11 +118,14 @@ class PromptServer:
 
 
 class TokenServer:
-    def __init__(self, runner: ModelRunner, ctrl, prompt_rank: int, sched: SchedulerConfig):
+    def __init__(self, runner: ModelRunner, ctrl, prompt_rank: int, sched: SchedulerConfig,
+                 tp_ctrl=None):
         self.runner = runner
         self.kv = runner.kv
         self.ctrl = ctrl
         self.prompt_rank = prompt_rank
+        self.tp_ctrl = tp_ctrl          # TP peers must admit in lockstep (NCCL inside steps)
+        self.rx = HandoffReceiver(tp_ctrl)
         self.machine = Machine(0, None, estimated_perf_model(runner.cfg, self.kv,
                                                              runner.w.nbytes()), TOKEN, sched)
 
@@ -134,7 +135,7 @@ class TokenServer:
         kv = self.kv
         seqs = [kv.allocate(len(p) + n) for _rid, p, n in requests]
         torch.cuda.current_stream().synchronize()    # tables written before the peer reads
-        dist.send(torch.tensor(seqs, dtype=torch.int32), dst=self.prompt_rank, group=self.ctrl)
+        send_reservations(seqs, self.prompt_rank, self.ctrl)
         expected = len(requests)
         received = 0
         info = {}         # rid -> [seq, ctx_kv, last_token]
@@ -142,19 +143,12 @@ class TokenServer:
         tokens = {r[0]: [] for r in requests}
         graph, graph_rids = None, None
         ring_h = torch.empty(64, dtype=torch.int32).pin_memory()
-        hdr, hdr_buf = None, torch.empty(1, dtype=torch.int32)
         while received < expected or self.machine.has_work() or self.machine.resident:
             if received < expected:
-                if hdr is None:
-                    hdr = dist.irecv(hdr_buf, src=self.prompt_rank, group=self.ctrl)
-                if not self.machine.has_work():
-                    hdr.wait()
-                if hdr.is_completed():
-                    hdr = None
-                    msg = torch.empty(int(hdr_buf[0]), 5, dtype=torch.int32)
-                    dist.recv(msg, src=self.prompt_rank, group=self.ctrl)
+                rows = self.rx.poll(block=not self.machine.has_work())
+                if rows is not None:
                     now_ms = (time.perf_counter() - t0) * 1e3
-                    for rid, seq, plen, first, n_out in msg.tolist():
+                    for rid, seq, plen, first, n_out in rows:
                         received += 1
                         tokens[rid].append(first)
                         if n_out > 1:
@@ -204,31 +198,45 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    if world < 2 or world % 2:
-        raise SystemExit("Splitwise pairs need an even number of GPUs >= 2")
+    tp = max(1, int(getattr(args, "tp", 1)))
+    if world < 2 * tp or world % (2 * tp):
+        raise SystemExit(f"Splitwise TP{tp}+TP{tp} pairs need a multiple of {2 * tp} GPUs")
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctrl = dist.new_group(backend="gloo")
-    pair, is_prompt = rank // 2, rank % 2 == 0
-    peer_rank = rank + 1 if is_prompt else rank - 1
+    # rank layout: pair p owns ranks [2*tp*p, 2*tp*(p+1)); the first tp ranks
+    # are the prompt machine's TP group, the next tp the token machine's;
+    # prompt TP rank i pushes its KV head slice to token TP rank i.
+    pair = rank // (2 * tp)
+    is_prompt = (rank % (2 * tp)) < tp
+    tp_rank = rank % tp
+    peer_rank = rank + tp if is_prompt else rank - tp
+    tp_nccl, tp_gloo = None, None
+    for base in range(0, world, tp):          # every rank creates every group
+        ranks = list(range(base, base + tp))
+        gn = dist.new_group(ranks) if tp > 1 else None
+        gg = dist.new_group(ranks, backend="gloo") if tp > 1 else None
+        if rank in ranks:
+            tp_nccl, tp_gloo = gn, gg
     cfg = get_config(args.model)
-    w = init_weights(cfg, seed=0)
-    P, O, R = args.prompt, args.out, 2     # 2 requests per pair = 1 per GPU
+    w = init_weights(cfg, seed=0, tp=tp, rank=tp_rank)
+    P, O = args.prompt, args.out
+    R = 2 * tp                                  # one request per GPU of the pair
     sched = SchedulerConfig()
     if is_prompt:
-        runner = ModelRunner(w, None)
-        handle = [None]
+        runner = ModelRunner(w, None, tp_group=tp_nccl)
+        handle = [None, None]
         dist.recv_object_list(handle, src=peer_rank, group=ctrl)
         peer = KVCacheManager.open_peer(handle[0])
-        server = PromptServer(runner, peer, ctrl, peer_rank, sched)
+        server = PromptServer(runner, peer, ctrl, peer_rank, sched, mailbox=handle[1])
     else:
-        nb = min(pool_blocks_for_memory(cfg, 1, 16, reserve_bytes=2 << 30),
+        nb = min(pool_blocks_for_memory(cfg, tp, 16, reserve_bytes=2 << 30),
                  64 * blocks_for(P + O + 64, 16))
-        kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads, cfg.head_dim, 16, 64,
+        kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads // tp, cfg.head_dim, 16, 64,
                             blocks_for(8192 + 1024, 16))
-        runner = ModelRunner(w, kv)
-        dist.send_object_list([kv.ipc_handle()], dst=peer_rank, group=ctrl)
-        server = TokenServer(runner, ctrl, peer_rank, sched)
+        runner = ModelRunner(w, kv, tp_group=tp_nccl)
+        server = TokenServer(runner, ctrl, peer_rank, sched, tp_ctrl=tp_gloo)
+        dist.send_object_list([kv.ipc_handle(), server.rx.name], dst=peer_rank, group=ctrl)
     g = torch.Generator().manual_seed(1234 + pair)
     reqs = [(pair * R + i, torch.randint(0, cfg.vocab, (P,), generator=g, dtype=torch.int32), O)
             for i in range(R)]
@@ -265,9 +273,9 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
                 payload["push"] = (st.bytes_per_layer, st.layer_ms, st.tail_ms)
             dist.all_gather_object(gathered, payload, group=ctrl)
             e2e_ms.append(dms)
-            for pr in range(0, world, 2):
+            for pr in range(0, world, 2 * tp):
                 first = gathered[pr]["out"]
-                emits = gathered[pr + 1]["out"]
+                emits = gathered[pr + tp]["out"]
                 t0p = gathered[pr]["t0"]
                 for rid, tf in first.items():
                     ttft.append((tf - t0p) * 1e3)
@@ -289,7 +297,7 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
     clocks = clk.summary()
     if rank == 0:
         hbm_peak, tc_peak, _tcs, peak_kind = peaks()
-        pairs = world // 2
+        pairs = world // (2 * tp)
         toks_step = pairs * R * O
         ms = statistics.mean(dev_ms)
         plan = measured_plan(LAYERWISE, [0.0], 0.0)
@@ -301,10 +309,12 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded random weights/tokens)",
             "config": {"workload": f"{cfg.name} {P}-token prompts / {O} greedy outputs, 1 request "
-                                   f"per GPU per step; {pairs} Splitwise pair(s) 1+1, layer-wise "
-                                   "KV push over NVLink, batched decode on the token GPU",
+                                   f"per GPU per step; {pairs} Splitwise pair(s) TP{tp}+TP{tp}, "
+                                   "layer-wise KV push over NVLink, batched decode on the token "
+                                   "machine",
                        "model": cfg.name, "prompt_tokens": P, "output_tokens": O,
-                       "requests_per_step": pairs * R, "parallelism": f"{pairs}x(1 prompt + 1 token)",
+                       "requests_per_step": pairs * R,
+                       "parallelism": f"{pairs}x(prompt TP{tp} + token TP{tp})",
                        "l2": "inputs > L2 (13.5 GB weights streamed per decode step)"},
             "ttft_ms": {"p50": percentile(ttft, 0.5), "p99": percentile(ttft, 0.99)},
             "tbt_ms": {"p50": percentile(tbt, 0.5), "p99": percentile(tbt, 0.99)},

@@ -25,11 +25,12 @@ namespace swb {
 constexpr int TV_ROWS = 4;                    // weight rows per work item
 constexpr int TV_WARPS = 8;                   // consumer warps: 2 per row (K halves)
 constexpr int TV_KC = 2048;                   // K elements per stage per row (4 KB)
-constexpr int TV_STAGES = 6;
+constexpr int TV_STAGES = 5;
 constexpr int TV_ROW_BYTES = TV_KC * 2;
 constexpr int TV_STAGE_BYTES = TV_ROWS * TV_ROW_BYTES;  // 16 KB
 constexpr int TV_THREADS = (TV_WARPS + 1) * 32;
 constexpr int TV_CTAS_PER_SM = 2;             // 2 x ~100 KB ring per SM
+constexpr int TV_HS_MAX = 16 * 1024;          // NORM: staged h (M*K*2 bytes) limit
 constexpr int TV_SMEM = TV_STAGES * TV_STAGE_BYTES + 2 * TV_STAGES * 8 +
                         2 * TV_WARPS * TV_ROWS * 16 * 4 + 128;
 
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
   uint64_t* empty = full + TV_STAGES;
   float* part = reinterpret_cast<float*>(empty + TV_STAGES);  // [2][WARPS][ROWS][16]
   float* rstd = part + 2 * TV_WARPS * TV_ROWS * 16;            // [16]
+  __nv_bfloat16* hs = reinterpret_cast<__nv_bfloat16*>(smem + TV_SMEM);  // NORM: [M][K]
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(xin);
   const float* xf = reinterpret_cast<const float*>(xin);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -138,6 +140,23 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
       rstd[t] = rsqrtf(ss / (float)K + eps);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
+    // normalise once into shared memory: the streaming loop then reads h
+    // exactly like a plain bf16 input (same rounding as swb_rmsnorm)
+    for (int i = t; i < M * K / 8; i += TV_WARPS * 32) {
+      const int m = (i * 8) / K, k = (i * 8) % K;
+      const float r = rstd[m];
+      const uint4 wq = *reinterpret_cast<const uint4*>(nw + k);
+      const float2 n0 = bf2_to_f2(wq.x), n1 = bf2_to_f2(wq.y), n2 = bf2_to_f2(wq.z),
+                   n3 = bf2_to_f2(wq.w);
+      const float4 a = *reinterpret_cast<const float4*>(xf + (size_t)m * K + k);
+      const float4 b = *reinterpret_cast<const float4*>(xf + (size_t)m * K + k + 4);
+      *reinterpret_cast<uint4*>(hs + (size_t)m * K + k) =
+          make_uint4(f2_to_bf2(a.x * r * n0.x, a.y * r * n0.y),
+                     f2_to_bf2(a.z * r * n1.x, a.w * r * n1.y),
+                     f2_to_bf2(b.x * r * n2.x, b.y * r * n2.y),
+                     f2_to_bf2(b.z * r * n3.x, b.w * r * n3.y));
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
   }
   int it = 0, parity = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, parity ^= 1) {
@@ -152,20 +171,9 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
       uint4 xq[MB];
       if (k < K) {
         if constexpr (NORM) {
-          const uint4 wq = *reinterpret_cast<const uint4*>(nw + k);
-          const float2 n0 = bf2_to_f2(wq.x), n1 = bf2_to_f2(wq.y), n2 = bf2_to_f2(wq.z),
-                       n3 = bf2_to_f2(wq.w);
 #pragma unroll
-          for (int m = 0; m < MB; ++m) {
-            if (m >= M) break;
-            const float r = rstd[m];
-            const float4 a = *reinterpret_cast<const float4*>(xf + (size_t)m * K + k);
-            const float4 b = *reinterpret_cast<const float4*>(xf + (size_t)m * K + k + 4);
-            xq[m] = make_uint4(f2_to_bf2(a.x * r * n0.x, a.y * r * n0.y),
-                               f2_to_bf2(a.z * r * n1.x, a.w * r * n1.y),
-                               f2_to_bf2(b.x * r * n2.x, b.y * r * n2.y),
-                               f2_to_bf2(b.z * r * n3.x, b.w * r * n3.y));
-          }
+          for (int m = 0; m < MB; ++m)
+            if (m < M) xq[m] = *reinterpret_cast<const uint4*>(hs + (size_t)m * K + k);
         } else {
 #pragma unroll
           for (int m = 0; m < MB; ++m)
@@ -258,12 +266,14 @@ static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
   SWB_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr[dev]) {
     SWB_CUDA(cudaFuncSetAttribute(gemv_bulk_kernel<MB, NORM>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, TV_SMEM));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  TV_SMEM + TV_HS_MAX));
     attr[dev] = true;
   }
+  const size_t smem = TV_SMEM + (NORM ? (size_t)M * K * 2 : 0);
   const int grid = min(items, TV_CTAS_PER_SM * kNumSMs);
   const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM>, dim3(grid), dim3(TV_THREADS),
-                                TV_SMEM, s, x, nw, eps, w, out, r, M, N, K, epi, items);
+                                smem, s, x, nw, eps, w, out, r, M, N, K, epi, items);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("gemv_bulk_kernel");
@@ -525,6 +535,9 @@ extern "C" int swb_gemv_rmsnorm_bf16(const float* x, const void* norm_w, float e
               "swb_gemv_rmsnorm_bf16: norm weight must be 16-byte aligned");
   SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid != x,
               "swb_gemv_rmsnorm_bf16: output may not alias the normalized input");
+  SWB_REQUIRE((size_t)M * K * 2 <= (size_t)TV_HS_MAX,
+              "swb_gemv_rmsnorm_bf16: M*K*2 = %d bytes exceeds %d (use swb_rmsnorm + GEMV)",
+              M * K * 2, TV_HS_MAX);
   return dispatch_gemv<true>(x, reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, w, out,
                              resid, M, N, K, epilogue, stream);
 }

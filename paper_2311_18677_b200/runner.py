@@ -308,9 +308,11 @@ class DecodeGraph:
         K.decode_prepare(self.ctx, self.tables, kv.block_size, B, self.pos, self.slots,
                          self.attn_len)
         K.embed(self.cur_tok, w.embed, out=self.x)
-        # pre-norm folded into the weight-streaming GEMV: opt-in (SWB_FUSED_NORM=1);
-        # measured slower on 7B (its per-CTA sum-of-squares prologue is serial)
-        fused = B <= K.GEMV_MAX_ROWS and os.environ.get("SWB_FUSED_NORM", "0") == "1"
+        # pre-norm folded into the weight-streaming GEMV (h normalised once into
+        # smem per CTA, overlapping the weight prefetch): used at B=1, where
+        # the CUDA-core GEMV runs; SWB_FUSED_NORM=0/1 forces it off/on
+        mode = os.environ.get("SWB_FUSED_NORM", "auto")
+        fused = (B == 1 and cfg.d_model * 2 <= 16384) if mode == "auto" else mode == "1"
         for li, lw in enumerate(w.layers):
             if fused:
                 K.gemv_rmsnorm(self.x, lw.attn_norm, cfg.norm_eps, lw.wqkv, K.EPI_BF16,

@@ -136,6 +136,13 @@ int swb_stream_wait_flag(uint32_t* flag, uint32_t value, uintptr_t stream);
 int swb_attn_prefill(const void* qkv, int row_stride, const int32_t* cu_seqlens,
                      int num_seqs, int max_seqlen, int H, int Hkv, int dh,
                      float scale, void* out, uintptr_t stream);
+/* Same contract on the 5th-gen tensor cores (tcgen05.mma, TMEM S/O
+ * accumulators, TMA-fed K/V rings); total_rows = cu_seqlens[num_seqs] bounds
+ * the TMA view of qkv.  The default prefill attention of the runner. */
+int swb_attn_prefill_tc(const void* qkv, int row_stride, int total_rows,
+                        const int32_t* cu_seqlens, int num_seqs, int max_seqlen,
+                        int H, int Hkv, int dh, float scale, void* out,
+                        uintptr_t stream);
 /* Paged decode attention for one layer, fused with the current token's
  * RoPE and KV append and with the split-K merge: q/k/v of the current token
  * come from qkv rows [B, row_stride] (q at column 0); when positions/slots are
@@ -156,39 +163,6 @@ int swb_attn_decode(const void* qkv, int row_stride, void* k_layer,
                     const int32_t* slots, float theta, int B, int H, int Hkv,
                     int dh, int block_size, float scale, int max_ctx,
                     int partition, void* workspace, void* out, uintptr_t stream);
-
-/* ------------------------------------------- whole decode step, 1 launch
- * One token-phase iteration of a Llama-style model (TP = 1, batch <= 8,
- * GQA group <= 4, head_dim 128) as a single persistent cooperative kernel:
- * every weight matrix of the step is streamed continuously through a shared
- * memory ring while the consumer warps run the phases (pre-norm QKV GEMV,
- * RoPE + KV append + paged attention + split-K merge, O GEMV + residual,
- * pre-norm gate/up GEMV + SwiGLU, down GEMV + residual, LM head, argmax,
- * advance) separated by grid barriers.  Same state contract as the
- * multi-kernel path (swb_decode_prepare/advance).  Replaces
- * PerfModel.token_iter_time (perf.py:125-132) with one launch. */
-typedef struct {
-  const void *wqkv, *wo, *wgu, *wd, *attn_norm, *mlp_norm;
-} swb_decode_layer;
-
-typedef struct {
-  int num_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, vocab;
-  int batch, block_size, max_blocks, max_ctx, ring_len;
-  float norm_eps, rope_theta;
-  const swb_decode_layer* layers;  /* DEVICE array [num_layers] */
-  const void *embed, *lm_head, *final_norm;
-  void *k_base, *v_base;           /* pool: layer l at base + l*layer_stride_bytes */
-  size_t layer_stride_bytes;
-  float* x;                        /* fp32 [batch][d_model] scratch */
-  void *qkv, *attn, *act;          /* bf16 scratch */
-  float* logits;                   /* fp32 [batch][vocab] */
-  int32_t *cur_tok, *ctx, *step, *out_ring, *pos, *slots, *attn_len;
-  const int32_t* block_tables;     /* [batch][max_blocks] */
-  void* workspace;                 /* swb_decode_step_workspace() bytes, zeroed once */
-} swb_decode_params;
-
-size_t swb_decode_step_workspace(const swb_decode_params* params);
-int swb_decode_step(const swb_decode_params* params, uintptr_t stream);
 
 /* --------------------------------------------- decode-step bookkeeping
  * Graph-resident per-step state update so the decode loop needs no host

@@ -38,26 +38,6 @@ class KVPoolInfo(C.Structure):
     ]
 
 
-class DecodeLayer(C.Structure):
-    _fields_ = [("wqkv", _P), ("wo", _P), ("wgu", _P), ("wd", _P), ("attn_norm", _P),
-                ("mlp_norm", _P)]
-
-
-class DecodeParams(C.Structure):
-    _fields_ = [
-        ("num_layers", _I), ("d_model", _I), ("n_heads", _I), ("n_kv_heads", _I),
-        ("head_dim", _I), ("ffn", _I), ("vocab", _I),
-        ("batch", _I), ("block_size", _I), ("max_blocks", _I), ("max_ctx", _I),
-        ("ring_len", _I),
-        ("norm_eps", _F), ("rope_theta", _F),
-        ("layers", _P), ("embed", _P), ("lm_head", _P), ("final_norm", _P),
-        ("k_base", _P), ("v_base", _P), ("layer_stride_bytes", _S),
-        ("x", _P), ("qkv", _P), ("attn", _P), ("act", _P), ("logits", _P),
-        ("cur_tok", _P), ("ctx", _P), ("step", _P), ("out_ring", _P), ("pos", _P),
-        ("slots", _P), ("attn_len", _P), ("block_tables", _P), ("workspace", _P),
-    ]
-
-
 # name -> argtypes (all return int status unless listed in _RESTYPE)
 SIGNATURES = {
     "swb_abi_version": [],
@@ -74,6 +54,7 @@ SIGNATURES = {
     "swb_kv_signal": [_P, _U, _ST],
     "swb_stream_wait_flag": [_P, _U, _ST],
     "swb_attn_prefill": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],
+    "swb_attn_prefill_tc": [_P, _I, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],
     "swb_attn_decode_workspace": [_I, _I, _I, _I, _I],
     "swb_attn_decode": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _F, _I, _I, _I, _I, _I, _F, _I,
                         _I, _P, _P, _ST],
@@ -88,11 +69,8 @@ SIGNATURES = {
     "swb_kv_pool_ipc_export": [_P, _P, _S],
     "swb_kv_pool_ipc_open": [_P, _S, C.POINTER(_P)],
     "swb_enable_peer": [_I],
-    "swb_decode_step_workspace": [C.POINTER(DecodeParams)],
-    "swb_decode_step": [C.POINTER(DecodeParams), _ST],
 }
-_RESTYPE = {"swb_last_error": C.c_char_p, "swb_attn_decode_workspace": _S,
-            "swb_decode_step_workspace": _S}
+_RESTYPE = {"swb_last_error": C.c_char_p, "swb_attn_decode_workspace": _S}
 
 
 def _load():
@@ -132,9 +110,9 @@ def check(status: int, what: str = "") -> None:
 LAUNCH_MULT = {
     "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
     "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
-    "swb_attn_prefill": 1, "swb_attn_decode": 1, "swb_decode_prepare": 1,
+    "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_decode_prepare": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
-    "swb_block_free": 1, "swb_decode_step": 1,
+    "swb_block_free": 1,
 }
 _launches = [0]
 

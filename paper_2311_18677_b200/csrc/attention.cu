@@ -262,10 +262,10 @@ __global__ void __launch_bounds__(PA_THREADS)
 // ============================================================ decode
 constexpr int DA_D = 128;
 constexpr int DA_MAXG = 8;
-constexpr int DA_WARPS = 4;
+constexpr int DA_WARPS = 8;
 
 // Decode attention, one kernel per layer:
-//   grid (B, Hkv, NP), 128 threads; CTA (b, kh, p) covers context tokens
+//   grid (B, Hkv, NP), DA_WARPS*32 threads; CTA (b, kh, p) covers context tokens
 //   [p*part, (p+1)*part) of sequence b for the G query heads of kv head kh.
 // * If `pos` is given, the current token's q/k are rotated here (RoPE) and its
 //   k/v are written into the pool slot slots[b] by the CTA whose partition
@@ -289,7 +289,7 @@ __device__ __forceinline__ void rope4(float* a, float* b, int i0, float pos, flo
   }
 }
 
-__global__ void __launch_bounds__(DA_WARPS * 32)
+__global__ void __launch_bounds__(DA_WARPS * 32, 2)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                        __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
                        const int32_t* __restrict__ tables, int max_blocks,
@@ -412,63 +412,87 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
     }
     __syncthreads();
 
-    // ---- scores: half-warp per token
+    // ---- scores: half-warp per token, 4 tokens in flight per half-warp
     {
       const int half = lane >> 4, hl = lane & 15;
-      for (int tb = warp * 2; tb < ntok; tb += DA_WARPS * 2) {  // warp-uniform
-        const int tt = tb + half;
-        const bool valid = tt < ntok;
-        float kf[8];
-        const uint4 kv = *reinterpret_cast<const uint4*>(sk + (valid ? tt : 0) * DA_D + hl * 8);
-        {
-          float2 a = bf2_to_f2(kv.x), c = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
-                 f = bf2_to_f2(kv.w);
-          kf[0] = a.x; kf[1] = a.y; kf[2] = c.x; kf[3] = c.y;
-          kf[4] = e.x; kf[5] = e.y; kf[6] = f.x; kf[7] = f.y;
+      constexpr int STRIDE = DA_WARPS * 2;
+      // warp-uniform trip count (the shuffles below need the full warp)
+      for (int tw = warp * 2; tw < ntok; tw += 4 * STRIDE) {
+        const int tb = tw + half;
+        float kf[4][8];
+        bool valid[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tt = tb + u * STRIDE;
+          valid[u] = tt < ntok;
+          const uint4 kv = *reinterpret_cast<const uint4*>(sk + (valid[u] ? tt : 0) * DA_D + hl * 8);
+          const float2 a = bf2_to_f2(kv.x), c = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
+                       f = bf2_to_f2(kv.w);
+          kf[u][0] = a.x; kf[u][1] = a.y; kf[u][2] = c.x; kf[u][3] = c.y;
+          kf[u][4] = e.x; kf[u][5] = e.y; kf[u][6] = f.x; kf[u][7] = f.y;
         }
         for (int gi = 0; gi < G; ++gi) {
           const float4 q0 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8);
           const float4 q1 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8 + 4);
-          float d = q0.x * kf[0];
-          d = fmaf(q0.y, kf[1], d); d = fmaf(q0.z, kf[2], d); d = fmaf(q0.w, kf[3], d);
-          d = fmaf(q1.x, kf[4], d); d = fmaf(q1.y, kf[5], d); d = fmaf(q1.z, kf[6], d);
-          d = fmaf(q1.w, kf[7], d);
+          float d[4];
 #pragma unroll
-          for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          if (hl == 0 && valid) ss[gi * part + tt] = d;
+          for (int u = 0; u < 4; ++u) {
+            float t = q0.x * kf[u][0];
+            t = fmaf(q0.y, kf[u][1], t); t = fmaf(q0.z, kf[u][2], t);
+            t = fmaf(q0.w, kf[u][3], t); t = fmaf(q1.x, kf[u][4], t);
+            t = fmaf(q1.y, kf[u][5], t); t = fmaf(q1.z, kf[u][6], t);
+            t = fmaf(q1.w, kf[u][7], t);
+            d[u] = t;
+          }
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+          if (hl == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (valid[u]) ss[gi * part + tb + u * STRIDE] = d[u];
+          }
         }
       }
     }
     __syncthreads();
-    // ---- softmax stats per head
-    for (int gi = warp; gi < G; gi += DA_WARPS) {
+    // ---- partition max per head: every warp reduces a token slice
+    float* wmax = sstat + 2 * G;            // [WARPS][G]
+    float* wsum = wmax + DA_WARPS * G;      // [WARPS][G]
+    for (int gi = 0; gi < G; ++gi) {
       float m = -INFINITY;
-      for (int i = lane; i < ntok; i += 32) m = fmaxf(m, ss[gi * part + i]);
+      for (int i = warp * 32 + lane; i < ntok; i += DA_WARPS * 32) m = fmaxf(m, ss[gi * part + i]);
       m = warp_max(m);
-      float l = 0.f;
-      for (int i = lane; i < ntok; i += 32) {
-        const float e = exp2f(ss[gi * part + i] - m);
-        ss[gi * part + i] = e;
-        l += e;
-      }
-      l = warp_sum(l);
-      if (lane == 0) {
-        sstat[gi * 2] = m;
-        sstat[gi * 2 + 1] = l;
-      }
+      if (lane == 0) wmax[warp * G + gi] = m;
     }
     __syncthreads();
-    // ---- P V: warp per token stripe, lane owns dims [4*lane, 4*lane+4)
-    float acc[DA_MAXG][4];
+    if (threadIdx.x < G) {
+      float m = -INFINITY;
 #pragma unroll
-    for (int gi = 0; gi < DA_MAXG; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
+      for (int w = 0; w < DA_WARPS; ++w) m = fmaxf(m, wmax[w * G + threadIdx.x]);
+      sstat[threadIdx.x * 2] = m;
+    }
+    __syncthreads();
+    float mrow[DA_MAXG];
+#pragma unroll
+    for (int gi = 0; gi < DA_MAXG; ++gi) mrow[gi] = gi < G ? sstat[gi * 2] : 0.f;
+    // ---- P V with the exponentials computed on the fly: warp per token
+    // stripe, lane owns dims [4*lane, 4*lane+4); per-warp partial sums of p
+    float acc[DA_MAXG][4], lsum[DA_MAXG];
+#pragma unroll
+    for (int gi = 0; gi < DA_MAXG; ++gi) {
+      acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
+      lsum[gi] = 0.f;
+    }
     for (int tt = warp; tt < ntok; tt += DA_WARPS) {
       const uint2 vv = *reinterpret_cast<const uint2*>(sv + tt * DA_D + lane * 4);
       const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
 #pragma unroll
       for (int gi = 0; gi < DA_MAXG; ++gi) {
         if (gi >= G) break;
-        const float pw = ss[gi * part + tt];
+        const float pw = exp2f(ss[gi * part + tt] - mrow[gi]);
+        lsum[gi] += pw;
         acc[gi][0] = fmaf(pw, v0.x, acc[gi][0]);
         acc[gi][1] = fmaf(pw, v0.y, acc[gi][1]);
         acc[gi][2] = fmaf(pw, v1.x, acc[gi][2]);
@@ -480,6 +504,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
       if (gi >= G) break;
       float4* dst = reinterpret_cast<float4*>(sacc + ((size_t)warp * G + gi) * DA_D + lane * 4);
       *dst = make_float4(acc[gi][0], acc[gi][1], acc[gi][2], acc[gi][3]);
+      if (lane == 0) wsum[warp * G + gi] = lsum[gi];
     }
     __syncthreads();
     for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
@@ -490,8 +515,11 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
       float* wo = wsp(kh * G + gi, p);
       wo[d] = v;
       if (d == 0) {
+        float l = 0.f;
+#pragma unroll
+        for (int w = 0; w < DA_WARPS; ++w) l += wsum[w * G + gi];
         wo[DA_D] = sstat[gi * 2];
-        wo[DA_D + 1] = sstat[gi * 2 + 1];
+        wo[DA_D + 1] = l;
       }
     }
   }
@@ -507,11 +535,11 @@ __global__ void __launch_bounds__(DA_WARPS * 32)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int gi = 0; gi < G; ++gi) {
+  for (int gi = threadIdx.x / DA_D; gi < G; gi += DA_WARPS * 32 / DA_D) {
     const int gh = kh * G + gi;
     float m = -INFINITY;
     for (int pp = 0; pp < NP; ++pp) m = fmaxf(m, __ldcg(wsp(gh, pp) + DA_D));
-    const int d = threadIdx.x;  // 128 threads = 128 dims
+    const int d = threadIdx.x % DA_D;  // 128 threads per head, thread = dim
     float l = 0.f, o = 0.f;
     for (int pp = 0; pp < NP; ++pp) {
       const float* w = wsp(gh, pp);
@@ -590,7 +618,8 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, v
   const int NP = (max_ctx + partition - 1) / partition;
   const size_t smem = (size_t)partition * DA_D * 2 * 2 +
                       sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
-                                       (size_t)DA_WARPS * G * DA_D + 2 * G);
+                                       (size_t)DA_WARPS * G * DA_D + 2 * G +
+                                       2 * (size_t)DA_WARPS * G);
   SWB_REQUIRE(smem <= 200 * 1024, "swb_attn_decode: partition too large");
   static bool attr[64] = {false};
   int dev = 0;

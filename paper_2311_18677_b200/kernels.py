@@ -5,6 +5,8 @@ device and contiguity, then launches on the current torch CUDA stream.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _abi
@@ -141,13 +143,23 @@ def kv_push_layer(qkv, rows, H, Hkv, dh, dst_k, dst_v, dst_slots, block_size, nu
          stream if stream is not None else _stream())
 
 
-def attn_prefill(qkv, cu_seqlens, num_seqs, max_seqlen, H, Hkv, dh, scale, out=None):
+def attn_prefill(qkv, cu_seqlens, num_seqs, max_seqlen, H, Hkv, dh, scale, out=None,
+                 impl=None):
+    """Causal varlen prefill attention.  impl "tc" = tcgen05/TMEM kernel (the
+    default; SWB_ATTN_TC=0 selects the mma.sync FlashAttention-2 kernel)."""
     _req(qkv, torch.bfloat16, "qkv")
     _req(cu_seqlens, torch.int32, "cu_seqlens")
     if out is None:
         out = torch.empty(qkv.shape[0], H * dh, dtype=torch.bfloat16, device=qkv.device)
-    call("swb_attn_prefill", qkv.data_ptr(), qkv.shape[1], cu_seqlens.data_ptr(), num_seqs,
-         max_seqlen, H, Hkv, dh, float(scale), out.data_ptr(), _stream())
+    if impl is None:
+        impl = "fa2" if os.environ.get("SWB_ATTN_TC", "1") == "0" else "tc"
+    if impl == "tc":
+        call("swb_attn_prefill_tc", qkv.data_ptr(), qkv.shape[1], qkv.shape[0],
+             cu_seqlens.data_ptr(), num_seqs, max_seqlen, H, Hkv, dh, float(scale),
+             out.data_ptr(), _stream())
+    else:
+        call("swb_attn_prefill", qkv.data_ptr(), qkv.shape[1], cu_seqlens.data_ptr(), num_seqs,
+             max_seqlen, H, Hkv, dh, float(scale), out.data_ptr(), _stream())
     return out
 
 

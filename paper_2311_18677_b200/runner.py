@@ -21,7 +21,6 @@ advance) is captured once in a CUDA graph and replayed; all per-step state
 
 from __future__ import annotations
 
-import ctypes
 import math
 import os
 from dataclasses import dataclass, field
@@ -208,25 +207,6 @@ class ModelRunner:
         return torch.tensor(pos + cu + last, dtype=torch.int32)
 
     # ------------------------------------------------------------- decode
-    def layers_device(self) -> torch.Tensor:
-        """Device array of per-layer weight pointers for the decode-step kernel."""
-        if getattr(self, "_layers_dev", None) is None:
-            arr = (_abi.DecodeLayer * self.cfg.n_layers)()
-            for i, lw in enumerate(self.w.layers):
-                arr[i] = _abi.DecodeLayer(lw.wqkv.data_ptr(), lw.wo.data_ptr(), lw.wgu.data_ptr(),
-                                          lw.wd.data_ptr(), lw.attn_norm.data_ptr(),
-                                          lw.mlp_norm.data_ptr())
-            raw = bytes(arr)
-            self._layers_dev = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(self.dev)
-        return self._layers_dev
-
-    def megakernel_ok(self, B: int) -> bool:
-        """The one-launch decode step covers TP=1, batch <= 8, GQA group <= 4."""
-        if os.environ.get("SWB_MEGAKERNEL", "0") != "1":
-            return False
-        return (self.tp == 1 and 1 <= B <= 8 and self.dh == 128
-                and self.hq // self.hkv <= 4 and self.kv is not None)
-
     def decode_graph(self, B: int, max_ctx: int, ring: int) -> "DecodeGraph":
         np_ = (max_ctx + self.partition - 1) // self.partition
         key = (B, np_, ring)
@@ -267,42 +247,8 @@ class DecodeGraph:
         wsb = K.attn_decode_workspace_bytes(B, runner.hq, max_ctx, runner.partition, runner.dh)
         self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
         self.graph = None
-        self.mega = runner.megakernel_ok(B)
-        if self.mega:
-            self._mega_params()
-
-    def _mega_params(self):
-        r, cfg, w, kv = self.r, self.r.cfg, self.r.w, self.r.kv
-        p = _abi.DecodeParams()
-        p.num_layers, p.d_model, p.n_heads, p.n_kv_heads = (cfg.n_layers, cfg.d_model, r.hq,
-                                                            r.hkv)
-        p.head_dim, p.ffn, p.vocab = r.dh, r.ffn, cfg.vocab
-        p.batch, p.block_size, p.max_blocks = self.B, kv.block_size, kv.max_blocks_per_seq
-        p.max_ctx, p.ring_len = self.max_ctx, self.ring
-        p.norm_eps, p.rope_theta = cfg.norm_eps, cfg.rope_theta
-        p.layers = r.layers_device().data_ptr()
-        p.embed, p.lm_head, p.final_norm = (w.embed.data_ptr(), w.lm_head.data_ptr(),
-                                            w.final_norm.data_ptr())
-        p.k_base, p.v_base = kv.info.k_base, kv.info.v_base
-        p.layer_stride_bytes = kv.info.layer_stride_bytes
-        p.x, p.qkv, p.attn, p.act, p.logits = (self.x.data_ptr(), self.qkv.data_ptr(),
-                                               self.attn.data_ptr(), self.act.data_ptr(),
-                                               self.logits.data_ptr())
-        p.cur_tok, p.ctx, p.step, p.out_ring = (self.cur_tok.data_ptr(), self.ctx.data_ptr(),
-                                                self.step.data_ptr(), self.out_ring.data_ptr())
-        p.pos, p.slots, p.attn_len = (self.pos.data_ptr(), self.slots.data_ptr(),
-                                      self.attn_len.data_ptr())
-        p.block_tables = self.tables.data_ptr()
-        nbytes = _abi.lib.swb_decode_step_workspace(ctypes.byref(p))
-        self.mega_ws = torch.zeros(nbytes, dtype=torch.uint8, device=r.dev)
-        p.workspace = self.mega_ws.data_ptr()
-        self.mega_p = p
 
     def _step_body(self):
-        if self.mega:
-            _abi.call("swb_decode_step", ctypes.byref(self.mega_p),
-                      torch.cuda.current_stream().cuda_stream)
-            return
         r, cfg, w, kv = self.r, self.r.cfg, self.r.w, self.r.kv
         B = self.B
         K.decode_prepare(self.ctx, self.tables, kv.block_size, B, self.pos, self.slots,

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import os
 import statistics
+import threading
 import time
 
 import torch
@@ -303,7 +304,8 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         plan = measured_plan(LAYERWISE, [0.0], 0.0)
         _ = plan
         line = {
-            "metric": "output tokens/s (+ TTFT/TBT p50,p99) serving 1024/128 requests, Llama-2-7B",
+            "metric": "output tokens/s (+ TTFT/TBT p50,p99) serving "
+                      f"{P}/{O} requests, {cfg.name}",
             "value": toks_step / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -315,7 +317,8 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
                        "model": cfg.name, "prompt_tokens": P, "output_tokens": O,
                        "requests_per_step": pairs * R,
                        "parallelism": f"{pairs}x(prompt TP{tp} + token TP{tp})",
-                       "l2": "inputs > L2 (13.5 GB weights streamed per decode step)"},
+                       "l2": f"inputs > L2 ({cfg.weight_bytes(tp) / 1e9:.1f} GB weights "
+                             "per GPU streamed per decode step)"},
             "ttft_ms": {"p50": percentile(ttft, 0.5), "p99": percentile(ttft, 0.99)},
             "tbt_ms": {"p50": percentile(tbt, 0.5), "p99": percentile(tbt, 0.99)},
             "second_token_gap_ms": {"p50": percentile(gaps2, 0.5)},
@@ -336,4 +339,10 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
+    torch.cuda.synchronize()
+    (server.tx if is_prompt else server.rx).close()
+    # NCCL sub-communicator teardown can stall at interpreter exit (seen with
+    # TP groups + CUDA IPC mappings); the result is printed, so bound it.
+    threading.Timer(30.0, lambda: os._exit(0)).start()
     dist.destroy_process_group()
+    os._exit(0)

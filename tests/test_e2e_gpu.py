@@ -162,46 +162,37 @@ def test_tiny_batched_decode_matches_single():
     _ = math
 
 
-@pytest.mark.parametrize("B", [1, 3])
-def test_decode_megakernel_matches_multikernel(monkeypatch, B):
-    """The one-launch decode step (persistent cooperative kernel) produces the
-    same tokens as the multi-kernel graph and logits within fp32-reordering
-    noise (both paths round the same bf16 activations)."""
+def test_decode_graph_is_deterministic():
+    """Two replays of the same decode graph on the same state give bit-equal
+    logits and tokens (no atomics in any reduction; split-K partitions merge
+    in a fixed order)."""
     from paper_2311_18677_b200 import kernels as K
     from paper_2311_18677_b200.runner import ModelRunner
-    cfg, w, kv, _ = _setup()
-    gen = torch.Generator().manual_seed(5)
-    lens = [37, 200, 129][:B]
-    n_out = 10
-    results = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("SWB_MEGAKERNEL", mode)
-        runner = ModelRunner(w, kv)
+    cfg, w, kv, runner = _setup()
+    lens = [37, 200, 129]
+    n_out = 6
+    res = []
+    for _ in range(2):
         seqs = [kv.allocate(n + n_out) for n in lens]
-        prompts = [torch.randint(0, cfg.vocab, (n,), generator=torch.Generator().manual_seed(n))
-                   for n in lens]
-        toks = torch.cat(prompts).int().cuda()
+        toks = torch.cat([torch.randint(0, cfg.vocab, (n,),
+                                        generator=torch.Generator().manual_seed(n))
+                          for n in lens]).int().cuda()
         slots = torch.empty(sum(lens), dtype=torch.int32, device="cuda")
         off = 0
         for s, n in zip(seqs, lens):
             K.slots_from_table(kv.table_row_ptr(s), 0, n, kv.block_size, slots[off:off + n])
             off += n
         first = runner.prefill(toks, lens, ModelRunner.pack_meta(lens).cuda(), local_slots=slots)
-        g = runner.decode_graph(B, max(lens) + n_out, n_out)
-        assert g.mega == (mode == "1")
-        g.load(seqs, first[:B], lens)
+        g = runner.decode_graph(len(lens), max(lens) + n_out, n_out)
+        g.load(seqs, first[:len(lens)], lens)
         g.capture()
         logits = []
         for _ in range(n_out - 1):
             g.replay()
             logits.append(g.logits.clone())
         torch.cuda.synchronize()
-        results[mode] = (g.out_ring[:, :n_out - 1].clone(), torch.stack(logits))
+        res.append((g.out_ring[:, :n_out - 1].clone(), torch.stack(logits)))
         for s in seqs:
             kv.release(s)
-    d = (results["0"][1] - results["1"][1]).abs().max().item()
-    scale = results["0"][1].abs().max().item()
-    assert torch.equal(results["0"][0], results["1"][0])
-    # different fp32 summation orders (K-slices, attention partitions) only
-    assert d < 0.03 + 0.01 * scale, (d, scale)
-    _ = gen
+    assert torch.equal(res[0][0], res[1][0])
+    assert torch.equal(res[0][1], res[1][1])

@@ -148,14 +148,17 @@ def _attn_ref(q, k, v, causal=True):
     return torch.einsum("hqk,khd->qhd", p, v.float())
 
 
-@pytest.mark.parametrize("H,Hkv", [(4, 4), (8, 2)])
-def test_attn_prefill_varlen(K, H, Hkv):
+@pytest.mark.parametrize("impl", ["tc", "fa2"])
+@pytest.mark.parametrize("H,Hkv,lens", [(4, 4, [1, 63, 64, 200, 130]),
+                                        (8, 2, [1, 63, 64, 200, 130]),
+                                        (4, 1, [129, 1024, 7, 256, 511])])
+def test_attn_prefill_varlen(K, H, Hkv, lens, impl):
     dh = 128
-    lens = [1, 63, 64, 200, 130]
     S = sum(lens)
     qkv = torch.randn(S, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
     cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), device="cuda", dtype=torch.int32)
-    out = K.attn_prefill(qkv, cu, len(lens), max(lens), H, Hkv, dh, 1 / math.sqrt(dh))
+    out = K.attn_prefill(qkv, cu, len(lens), max(lens), H, Hkv, dh, 1 / math.sqrt(dh),
+                         impl=impl)
     off = 0
     for L in lens:
         blk = qkv[off:off + L]
@@ -247,12 +250,13 @@ def test_kv_push_local_bit_exact(K):
     dst.close()
 
 
-@pytest.mark.parametrize("M", [1, 3, 16])
-def test_gemv_rmsnorm_equals_rmsnorm_then_gemv(K, M):
+@pytest.mark.parametrize("M,d", [(1, 4096), (2, 4096), (3, 2048), (16, 512)])
+def test_gemv_rmsnorm_equals_rmsnorm_then_gemv(K, M, d):
     """The fused pre-norm GEMV sees exactly the bf16 h that swb_rmsnorm
     produces, so its outputs equal the two-kernel path (fp32 tolerance for
-    accumulation-order-free equality of the same inputs)."""
-    d, N = 4096, 3072
+    accumulation-order-free equality of the same inputs).  The staged h is
+    limited to 16 KB (M*d*2 bytes)."""
+    N = 3072
     x = torch.randn(M, d, device="cuda") * 3
     nw = (1 + 0.1 * torch.randn(d, device="cuda")).bfloat16()
     w = torch.randn(N, d, device="cuda").bfloat16()
@@ -262,6 +266,15 @@ def test_gemv_rmsnorm_equals_rmsnorm_then_gemv(K, M):
     assert _rel(got, ref) < 1e-5
     wgu = torch.randn(2048, d, device="cuda").bfloat16()
     assert _rel(K.gemv_rmsnorm(x, nw, 1e-5, wgu, K.EPI_SWIGLU), K.gemv(h, wgu, K.EPI_SWIGLU)) < 1e-2
+
+
+def test_gemv_rmsnorm_rejects_oversized_stage(K):
+    from paper_2311_18677_b200.errors import ValidationError
+    x = torch.randn(3, 4096, device="cuda")
+    nw = torch.ones(4096, device="cuda").bfloat16()
+    w = torch.randn(256, 4096, device="cuda").bfloat16()
+    with pytest.raises(ValidationError):
+        K.gemv_rmsnorm(x, nw, 1e-5, w, K.EPI_F32)
 
 
 @pytest.mark.parametrize("H,Hkv", [(32, 32), (64, 8)])

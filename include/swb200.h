@@ -226,6 +226,29 @@ int swb_kv_pool_ipc_open(const void* handle, size_t handle_bytes,
 /* Enable direct peer access between the current device and `peer`. */
 int swb_enable_peer(int peer_device);
 
+/* ------------------------------------------- tensor-parallel all-reduce
+ * The TP pools' "all-reduce twice per layer" (the reference
+ * prices it inside PerfModel.prompt_time / token_iter_time, perf.py:119-132)
+ * over NVLink peer memory instead of a library collective.  Each rank
+ * creates a communicator owning two fp32 slots of slot_bytes (IPC-exported,
+ * blob of SWB_TP_IPC_BYTES), exchanges blobs with its group (any host
+ * channel), connects, then per reduction: the producing GEMM/GEMV writes
+ * its partial sums into swb_tp_comm_slot(comm, s) and
+ * swb_tp_allreduce_f32(comm, s, out, n) writes the rank-ordered sum of all
+ * ranks' slot s into out (identical bits on every rank).  Alternate the
+ * slot between consecutive reductions.  Epochs live on the device, so the
+ * call is CUDA-graph capturable. */
+#define SWB_TP_IPC_BYTES 128
+typedef struct swb_tp_comm swb_tp_comm;
+int swb_tp_comm_create(int rank, int world, size_t slot_bytes, swb_tp_comm** out,
+                       void* ipc_out, size_t ipc_bytes);
+/* blobs: world entries of blob_stride bytes, indexed by rank (own ignored). */
+int swb_tp_comm_connect(swb_tp_comm* comm, const void* blobs, size_t blob_stride);
+int swb_tp_comm_destroy(swb_tp_comm* comm);
+void* swb_tp_comm_slot(const swb_tp_comm* comm, int slot);
+int swb_tp_allreduce_f32(swb_tp_comm* comm, int slot, float* out, size_t n,
+                         uintptr_t stream);
+
 #ifdef __cplusplus
 }
 #endif

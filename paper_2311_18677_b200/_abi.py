@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libswb200.s
 SWB_OK, SWB_ERR_INVALID, SWB_ERR_CAPACITY, SWB_ERR_CUDA, SWB_ERR_CONFIG = 0, 1, 2, 3, 4
 EPI_BF16, EPI_F32, EPI_RESID_F32, EPI_SWIGLU = 0, 1, 2, 3
 KV_POOL_IPC_BYTES = 256
+TP_IPC_BYTES = 128
 
 _P = C.c_void_p
 _I = C.c_int
@@ -69,8 +70,14 @@ SIGNATURES = {
     "swb_kv_pool_ipc_export": [_P, _P, _S],
     "swb_kv_pool_ipc_open": [_P, _S, C.POINTER(_P)],
     "swb_enable_peer": [_I],
+    "swb_tp_comm_create": [_I, _I, _S, C.POINTER(_P), _P, _S],
+    "swb_tp_comm_connect": [_P, _P, _S],
+    "swb_tp_comm_destroy": [_P],
+    "swb_tp_comm_slot": [_P, _I],
+    "swb_tp_allreduce_f32": [_P, _I, _P, _S, _ST],
 }
-_RESTYPE = {"swb_last_error": C.c_char_p, "swb_attn_decode_workspace": _S}
+_RESTYPE = {"swb_last_error": C.c_char_p, "swb_attn_decode_workspace": _S,
+            "swb_tp_comm_slot": _P}
 
 
 def _load():
@@ -112,7 +119,7 @@ LAUNCH_MULT = {
     "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
     "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_decode_prepare": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
-    "swb_block_free": 1,
+    "swb_block_free": 1, "swb_tp_allreduce_f32": 1,
 }
 _launches = [0]
 

@@ -1,0 +1,235 @@
+// Tensor-parallel all-reduce over NVLink peer memory (the TP pools of the
+// 70B / BLOOM configs: "all-reduce twice per layer").
+//
+// Each rank owns one device region, exported by CUDA IPC and mapped by every
+// peer of its TP group:
+//   [slot 0 data | slot 1 data | flags[2][MAXW][MAXC] | counters[2][MAXC]]
+// The producing GEMM/GEMV writes its fp32 partial sums straight into a slot
+// (rank 0 folds the residual in), so the all-reduce moves no extra copy:
+//   CTA c of rank r   1. system-scope release store of its epoch into
+//                        flags[slot][r][c] of every peer,
+//                     2. spins (acquire, nanosleep back-off, watchdog) until
+//                        every peer's flag for (slot, c) reached the epoch,
+//                     3. sums chunk c of the slot over ranks 0..W-1 in rank
+//                        order (bit-identical results on every rank) with
+//                        16-byte L2-only loads over NVLink, writes `out`.
+// Epochs are per-(slot, CTA) device counters, so the launch is CUDA-graph
+// replayable.  Two slots alternate: a slot is rewritten only after the next
+// all-reduce (other slot) completed on every rank, i.e. after all peers
+// finished reading it.
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace swb {
+
+constexpr int TP_MAXW = 8;
+constexpr int TP_MAXC = 256;
+constexpr int TP_THREADS = 512;
+constexpr uint32_t kTpMagic = 0x53575450u;  // "SWTP"
+
+struct TpIpcBlob {
+  uint32_t magic;
+  int rank, world, device;
+  uint64_t slot_bytes;
+  cudaIpcMemHandle_t mem;
+};
+static_assert(sizeof(TpIpcBlob) <= SWB_TP_IPC_BYTES, "blob too large");
+
+struct TpArgs {
+  const float* peer_slot[TP_MAXW];   // slot base of every rank (own = local)
+  uint32_t* peer_flags[TP_MAXW];     // flags region of every rank
+  uint32_t* my_flags;
+  uint32_t* my_ctr;
+  float* out;
+  long long n;
+  int rank, world, slot;
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a) {
+  pdl_wait();  // the producer GEMM/GEMV must be complete before we publish
+  const int c = blockIdx.x;
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) {
+    uint32_t* ctr = a.my_ctr + a.slot * TP_MAXC + c;
+    const uint32_t e = *ctr + 1;
+    __threadfence_system();
+    for (int p = 0; p < a.world; ++p)
+      if (p != a.rank)
+        st_release_sys(a.peer_flags[p] + ((size_t)a.slot * TP_MAXW + a.rank) * TP_MAXC + c, e);
+    const long long t0 = clock64();
+    for (int p = 0; p < a.world; ++p) {
+      if (p == a.rank) continue;
+      const uint32_t* f = a.my_flags + ((size_t)a.slot * TP_MAXW + p) * TP_MAXC + c;
+      int spins = 0;
+      while ((int)(ld_acquire_sys(f) - e) < 0) {
+        if (++spins > 64) __nanosleep(64);
+        // a peer that never arrives (crashed rank) must not wedge the GPU
+        if (clock64() - t0 > 40000000000ll) __trap();
+      }
+    }
+    *ctr = e;
+    s_epoch = e;
+  }
+  __syncthreads();
+  // chunk c of n (in float4 units; n % 4 == 0 checked on the host)
+  const long long n4 = a.n >> 2;
+  const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+  const long long lo = (long long)c * per, hi = min(n4, lo + per);
+  float4* out4 = reinterpret_cast<float4*>(a.out);
+  for (long long i = lo + threadIdx.x; i < hi; i += 2 * TP_THREADS) {
+    const long long j = i + TP_THREADS;
+    float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+    float4 v0[TP_MAXW], v1[TP_MAXW];
+#pragma unroll
+    for (int p = 0; p < TP_MAXW; ++p) {
+      if (p < a.world) {
+        const float4* src = reinterpret_cast<const float4*>(a.peer_slot[p]);
+        v0[p] = __ldcg(src + i);
+        if (j < hi) v1[p] = __ldcg(src + j);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < TP_MAXW; ++p) {
+      if (p < a.world) {
+        s0.x += v0[p].x; s0.y += v0[p].y; s0.z += v0[p].z; s0.w += v0[p].w;
+        if (j < hi) {
+          s1.x += v1[p].x; s1.y += v1[p].y; s1.z += v1[p].z; s1.w += v1[p].w;
+        }
+      }
+    }
+    out4[i] = s0;
+    if (j < hi) out4[j] = s1;
+  }
+  (void)s_epoch;
+}
+
+}  // namespace swb
+
+using namespace swb;
+
+struct swb_tp_comm {
+  int rank, world, device;
+  size_t slot_bytes;
+  uint8_t* base;                    // own region
+  uint8_t* peer_base[TP_MAXW];      // mapped regions (own at [rank])
+  bool connected;
+};
+
+static size_t tp_region_bytes(size_t slot_bytes) {
+  return 2 * slot_bytes + sizeof(uint32_t) * (2 * TP_MAXW * TP_MAXC + 2 * TP_MAXC);
+}
+
+extern "C" int swb_tp_comm_create(int rank, int world, size_t slot_bytes, swb_tp_comm** out,
+                                  void* ipc_out, size_t ipc_bytes) {
+  SWB_REQUIRE(out && ipc_out, "swb_tp_comm_create: null pointer");
+  SWB_REQUIRE(world >= 1 && world <= TP_MAXW && rank >= 0 && rank < world,
+              "swb_tp_comm_create: rank %d / world %d outside 1..%d", rank, world, TP_MAXW);
+  SWB_REQUIRE(slot_bytes > 0 && slot_bytes % 256 == 0,
+              "swb_tp_comm_create: slot_bytes must be a positive multiple of 256");
+  SWB_REQUIRE(ipc_bytes >= sizeof(TpIpcBlob), "swb_tp_comm_create: need %zu ipc bytes",
+              sizeof(TpIpcBlob));
+  swb_tp_comm* c = new swb_tp_comm();
+  c->rank = rank;
+  c->world = world;
+  c->slot_bytes = slot_bytes;
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e == cudaSuccess) e = cudaMalloc(&c->base, tp_region_bytes(slot_bytes));
+  if (e == cudaSuccess) e = cudaMemset(c->base, 0, tp_region_bytes(slot_bytes));
+  TpIpcBlob b;
+  memset(&b, 0, sizeof(b));
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&b.mem, c->base);
+  if (e != cudaSuccess) {
+    if (c->base) cudaFree(c->base);
+    delete c;
+    return swb_set_error(SWB_ERR_CUDA, "swb_tp_comm_create: %s", cudaGetErrorString(e));
+  }
+  b.magic = kTpMagic;
+  b.rank = rank;
+  b.world = world;
+  b.device = c->device;
+  b.slot_bytes = slot_bytes;
+  memcpy(ipc_out, &b, sizeof(b));
+  for (int p = 0; p < TP_MAXW; ++p) c->peer_base[p] = nullptr;
+  c->peer_base[rank] = c->base;
+  *out = c;
+  return SWB_OK;
+}
+
+extern "C" int swb_tp_comm_connect(swb_tp_comm* c, const void* blobs, size_t blob_stride) {
+  SWB_REQUIRE(c && blobs, "swb_tp_comm_connect: null pointer");
+  SWB_REQUIRE(!c->connected, "swb_tp_comm_connect: already connected");
+  SWB_REQUIRE(blob_stride >= sizeof(TpIpcBlob), "swb_tp_comm_connect: short blob stride");
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) continue;
+    TpIpcBlob b;
+    memcpy(&b, static_cast<const uint8_t*>(blobs) + p * blob_stride, sizeof(b));
+    SWB_REQUIRE(b.magic == kTpMagic, "swb_tp_comm_connect: bad blob for rank %d", p);
+    SWB_REQUIRE(b.rank == p && b.world == c->world && b.slot_bytes == c->slot_bytes,
+                "swb_tp_comm_connect: rank %d blob does not match this group", p);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.mem, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "swb_tp_comm_connect: open rank %d: %s", p,
+                           cudaGetErrorString(e));
+    c->peer_base[p] = static_cast<uint8_t*>(ptr);
+  }
+  c->connected = true;
+  return SWB_OK;
+}
+
+extern "C" int swb_tp_comm_destroy(swb_tp_comm* c) {
+  if (!c) return SWB_OK;
+  for (int p = 0; p < c->world; ++p)
+    if (p != c->rank && c->peer_base[p]) cudaIpcCloseMemHandle(c->peer_base[p]);
+  cudaFree(c->base);
+  delete c;
+  return SWB_OK;
+}
+
+extern "C" void* swb_tp_comm_slot(const swb_tp_comm* c, int slot) {
+  if (!c || slot < 0 || slot > 1) return nullptr;
+  return c->base + (size_t)slot * c->slot_bytes;
+}
+
+extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t n,
+                                    uintptr_t stream) {
+  SWB_REQUIRE(c && out, "swb_tp_allreduce_f32: null pointer");
+  SWB_REQUIRE(c->connected || c->world == 1, "swb_tp_allreduce_f32: not connected");
+  SWB_REQUIRE(slot == 0 || slot == 1, "swb_tp_allreduce_f32: slot must be 0 or 1");
+  SWB_REQUIRE(n % 4 == 0 && n * sizeof(float) <= c->slot_bytes,
+              "swb_tp_allreduce_f32: n=%zu must be a multiple of 4 and fit the slot", n);
+  SWB_REQUIRE((((uintptr_t)out) & 15) == 0, "swb_tp_allreduce_f32: out must be 16-byte aligned");
+  if (n == 0) return SWB_OK;
+  TpArgs a;
+  memset(&a, 0, sizeof(a));
+  const size_t flags_off = 2 * c->slot_bytes;
+  for (int p = 0; p < c->world; ++p) {
+    a.peer_slot[p] = reinterpret_cast<const float*>(c->peer_base[p] + (size_t)slot * c->slot_bytes);
+    a.peer_flags[p] = reinterpret_cast<uint32_t*>(c->peer_base[p] + flags_off);
+  }
+  a.my_flags = reinterpret_cast<uint32_t*>(c->base + flags_off);
+  a.my_ctr = a.my_flags + 2 * TP_MAXW * TP_MAXC;
+  a.out = out;
+  a.n = (long long)n;
+  a.rank = c->rank;
+  a.world = c->world;
+  a.slot = slot;
+  // ~16 KB of output per CTA, at most TP_MAXC CTAs (one wave)
+  const long long ctas = std::min<long long>(TP_MAXC, std::max<long long>(1, (long long)n / 4096));
+  const cudaError_t le = launch(tp_allreduce_kernel, dim3((unsigned)ctas), dim3(TP_THREADS), 0,
+                                (cudaStream_t)stream, a);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch tp_allreduce_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("tp_allreduce_kernel");
+}

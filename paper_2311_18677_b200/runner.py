@@ -53,12 +53,14 @@ class PushStats:
 
 class ModelRunner:
     def __init__(self, weights: Weights, kv: KVCacheManager | None = None, tp_group=None,
-                 decode_partition: int = 128, push_ctas: int = 64):
+                 decode_partition: int = 128, push_ctas: int = 64, tp_max_rows: int = 8192):
         self.w = weights
         self.cfg = cfg = weights.cfg
         self.tp = weights.tp
         self.rank = weights.rank
         self.tp_group = tp_group
+        self.tp_comm = None
+        self.tp_max_rows = tp_max_rows    # largest prefill / decode row count reduced
         self.kv = kv
         self.hq = cfg.n_heads // self.tp
         self.hkv = cfg.n_kv_heads // self.tp
@@ -77,6 +79,38 @@ class ModelRunner:
     def _allreduce(self, x):
         if self.tp > 1:
             torch.distributed.all_reduce(x, group=self.tp_group)
+
+    def _comm(self):
+        """NVLink peer-memory all-reduce (tpcomm.py) for TP > 1, created on
+        first use; SWB_TP_AR=nccl selects torch.distributed's all_reduce."""
+        if self.tp == 1 or os.environ.get("SWB_TP_AR", "p2p") == "nccl":
+            return None
+        if self.tp_comm is None:
+            from .tpcomm import TPComm
+            self.tp_comm = TPComm(self.tp_group, self.tp_max_rows * self.cfg.d_model * 4)
+        return self.tp_comm
+
+    def _begin_reductions(self):
+        c = self._comm()
+        if c is not None:
+            c.reset()
+
+    def _proj_reduce(self, inp, w, x):
+        """x <- x + sum over TP ranks of inp @ w^T (O / down projections).
+        TP: rank 0 folds the residual into its partial; the partials meet in
+        the peer-memory slot and the all-reduce writes x."""
+        if self.tp == 1:
+            K.linear(inp, w, K.EPI_RESID_F32, out=x, resid=x)
+            return
+        c = self._comm()
+        if c is None:
+            K.linear(inp, w, self._resid_epi(), out=x, resid=x)
+            self._allreduce(x)
+            return
+        s = c.next_slot()
+        part = c.slot(s, x.shape)
+        K.linear(inp, w, self._resid_epi(), out=part, resid=x)
+        c.allreduce(s, x)
 
     def _resid_epi(self):
         # with TP only rank 0 folds the residual in; the all-reduce sums the rest
@@ -132,6 +166,7 @@ class ModelRunner:
                 timing = [(torch.cuda.Event(enable_timing=True),
                            torch.cuda.Event(enable_timing=True)) for _ in range(cfg.n_layers)]
                 self._compute_end = torch.cuda.Event(enable_timing=True)
+        self._begin_reductions()
         K.embed(tokens, w.embed, out=x)
         for li, lw in enumerate(w.layers):
             qkv = self.pqkv[li & 1][:T]
@@ -165,12 +200,10 @@ class ModelRunner:
                 push_events.append(done)
             K.attn_prefill(qkv, cu, R, max(lens), self.hq, self.hkv, self.dh, self.scale,
                            out=attn)
-            K.linear(attn, lw.wo, self._resid_epi(), out=x, resid=x)
-            self._allreduce(x)
+            self._proj_reduce(attn, lw.wo, x)
             K.rmsnorm(x, lw.mlp_norm, cfg.norm_eps, out=h)
             K.linear(h, lw.wgu, K.EPI_SWIGLU, out=act)
-            K.linear(act, lw.wd, self._resid_epi(), out=x, resid=x)
-            self._allreduce(x)
+            self._proj_reduce(act, lw.wd, x)
         last = self.plast[:R]
         K.rmsnorm(x, w.final_norm, cfg.norm_eps, rows_index=last_rows, out=last)
         logits = self.plogits[:R]
@@ -251,6 +284,7 @@ class DecodeGraph:
     def _step_body(self):
         r, cfg, w, kv = self.r, self.r.cfg, self.r.w, self.r.kv
         B = self.B
+        r._begin_reductions()
         K.decode_prepare(self.ctx, self.tables, kv.block_size, B, self.pos, self.slots,
                          self.attn_len)
         K.embed(self.cur_tok, w.embed, out=self.x)
@@ -271,16 +305,14 @@ class DecodeGraph:
                           self.attn_len, B, r.hq, r.hkv, r.dh, kv.block_size, r.scale,
                           self.max_ctx, r.partition, self.ws, out=self.attn,
                           positions=self.pos, slots=self.slots, theta=cfg.rope_theta)
-            K.linear(self.attn, lw.wo, r._resid_epi(), out=self.x, resid=self.x)
-            r._allreduce(self.x)
+            r._proj_reduce(self.attn, lw.wo, self.x)
             if fused:
                 K.gemv_rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, lw.wgu, K.EPI_SWIGLU,
                                out=self.act)
             else:
                 K.rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, out=self.h)
                 K.linear(self.h, lw.wgu, K.EPI_SWIGLU, out=self.act)
-            K.linear(self.act, lw.wd, r._resid_epi(), out=self.x, resid=self.x)
-            r._allreduce(self.x)
+            r._proj_reduce(self.act, lw.wd, self.x)
         if fused:
             K.gemv_rmsnorm(self.x, w.final_norm, cfg.norm_eps, w.lm_head, K.EPI_F32,
                            out=self.logits)

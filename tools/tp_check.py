@@ -46,9 +46,10 @@ def run(runner, kv, prompt, n_out):
     return toks_out, torch.stack(logits)
 
 
-def time_phases(runner, kv, P, reps=5):
+def time_phases(runner, kv, P, reps=5, batch=1):
     cfg = runner.cfg
     seq = kv.allocate(P + 64)
+    extra = [kv.allocate(P + 64) for _ in range(batch - 1)]
     toks = torch.randint(0, cfg.vocab, (P,), dtype=torch.int32, device="cuda")
     slots = torch.empty(P, dtype=torch.int32, device="cuda")
     K.slots_from_table(kv.table_row_ptr(seq), 0, P, kv.block_size, slots)
@@ -63,8 +64,8 @@ def time_phases(runner, kv, P, reps=5):
         b.record()
         torch.cuda.synchronize()
         pre.append(a.elapsed_time(b))
-    g = runner.decode_graph(1, P + 64, 64)
-    g.load([seq], first[:1], [P])
+    g = runner.decode_graph(batch, P + 64, 64)
+    g.load([seq] + extra, [int(first[0])] * batch, [P] * batch)
     g.capture()
     a, b = ev(), ev()
     dist.barrier()
@@ -74,6 +75,8 @@ def time_phases(runner, kv, P, reps=5):
     b.record()
     torch.cuda.synchronize()
     kv.release(seq)
+    for s_ in extra:
+        kv.release(s_)
     return min(pre), a.elapsed_time(b) / 32
 
 
@@ -83,6 +86,9 @@ def main():
     ap.add_argument("--prompt", type=int, default=300)
     ap.add_argument("--out", type=int, default=16)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--no-ar", action="store_true",
+                    help="timing only: skip the TP all-reduces (wrong numerics)")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
@@ -92,17 +98,20 @@ def main():
     kv = KVCacheManager(cfg.n_layers, 1024, cfg.n_kv_heads // world, cfg.head_dim, 16, 4,
                         (a.prompt + 128) // 16 + 2)
     runner = ModelRunner(w, kv, tp_group=dist.group.WORLD)
+    if a.no_ar:
+        runner._allreduce = lambda x: None
     prompt = torch.randint(0, cfg.vocab, (a.prompt,), generator=torch.Generator().manual_seed(3)).tolist()
     if a.time:
-        pre, dec = time_phases(runner, kv, a.prompt)
+        pre, dec = time_phases(runner, kv, a.prompt, batch=a.batch)
         t = torch.tensor([pre, dec], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rank == 0:
             print(json.dumps({"model": cfg.name, "tp": world, "prompt": a.prompt,
+                              "batch": a.batch, "allreduce": not a.no_ar,
                               "prefill_ms": t[0].item(), "decode_step_ms": t[1].item(),
                               "prefill_tflops_per_gpu": cfg.prefill_flops(a.prompt, world) /
                               t[0].item() / 1e9,
-                              "decode_GBps_per_gpu": cfg.decode_bytes([a.prompt + 32], world) /
+                              "decode_GBps_per_gpu": cfg.decode_bytes([a.prompt + 32] * a.batch, world) /
                               t[1].item() / 1e6}))
         dist.destroy_process_group()
         return

@@ -67,8 +67,17 @@ int swb_sync_stream(uintptr_t stream);
 #define SWB_EPI_F32 1
 #define SWB_EPI_RESID_F32 2
 #define SWB_EPI_SWIGLU 3
+/*   epilogue SWB_EPI_GELU     : out bf16 [M,N] = gelu_tanh(acc + bias)
+ *                               (BLOOM's MLP up projection) */
+#define SWB_EPI_GELU 4
 int swb_gemm_bf16(const void* a, const void* w, void* out, const void* resid,
                   int M, int N, int K, int epilogue, uintptr_t stream);
+/* With a per-output-feature bf16 bias [N] (may be NULL) added to the fp32
+ * accumulator before the epilogue (BLOOM's biased linears); not with
+ * SWB_EPI_SWIGLU. */
+int swb_gemm_bf16_bias(const void* a, const void* w, void* out,
+                       const void* resid, const void* bias, int M, int N,
+                       int K, int epilogue, uintptr_t stream);
 
 /* --------------------------------------------- skinny GEMM / GEMV (decode)
  * Same contract as swb_gemm_bf16 for small M (decode batch, 1..16 rows):
@@ -78,6 +87,9 @@ int swb_gemm_bf16(const void* a, const void* w, void* out, const void* resid,
  */
 int swb_gemv_bf16(const void* x, const void* w, void* out, const void* resid,
                   int M, int N, int K, int epilogue, uintptr_t stream);
+int swb_gemv_bf16_bias(const void* x, const void* w, void* out,
+                       const void* resid, const void* bias, int M, int N,
+                       int K, int epilogue, uintptr_t stream);
 /* Pre-norm fused variant: x is the fp32 residual stream [M,K]; the kernel
  * applies RMSNorm with weight norm_w on the fly (bit-identical to
  * swb_rmsnorm followed by swb_gemv_bf16).  out may not alias x. */
@@ -93,6 +105,11 @@ int swb_embed(const int32_t* tokens, const void* table, float* x, int rows,
  * NULL) selects src rows (e.g. the last token of each prompt). */
 int swb_rmsnorm(const float* x, const int32_t* row_index, const void* w,
                 void* out, int rows, int d, float eps, uintptr_t stream);
+/* LayerNorm with bias (BLOOM): out = (x - mean) * rstd * w + b, bf16 out, or
+ * fp32 out when out_f32 (may then be x itself: the embedding LayerNorm). */
+int swb_layernorm(const float* x, const int32_t* row_index, const void* w,
+                  const void* b, void* out, int rows, int d, float eps,
+                  int out_f32, uintptr_t stream);
 /* Greedy sampling: out[r] = argmax_v logits fp32 [rows,V] (lowest index on
  * ties). */
 int swb_argmax(const float* logits, int rows, int V, int32_t* out,
@@ -104,7 +121,8 @@ int swb_argmax(const float* logits, int rows, int V, int32_t* out,
  * theta) at positions[r], and, when k_layer/v_layer are non-NULL, writes the
  * rotated k and v of row r into paged slot slots[r] of the layer's block
  * pool (layout [block][Hkv][block_size][dh]).  The KV bytes it writes are
- * what PerfModel.kv_cache_bytes (perf.py:134-137) counts.
+ * what PerfModel.kv_cache_bytes (perf.py:134-137) counts.  theta == 0: no
+ * rotation (ALiBi models), KV write only.
  */
 int swb_rope_kv_write(void* qkv, int rows, int row_stride, const int32_t* positions,
                       int H, int Hkv, int dh, float theta, void* k_layer,
@@ -138,11 +156,13 @@ int swb_attn_prefill(const void* qkv, int row_stride, const int32_t* cu_seqlens,
                      float scale, void* out, uintptr_t stream);
 /* Same contract on the 5th-gen tensor cores (tcgen05.mma, TMEM S/O
  * accumulators, TMA-fed K/V rings); total_rows = cu_seqlens[num_seqs] bounds
- * the TMA view of qkv.  The default prefill attention of the runner. */
+ * the TMA view of qkv.  alibi_slopes (fp32 [H], may be NULL) adds
+ * slope_h * (key_pos - query_pos) to the scores (BLOOM).  The default prefill
+ * attention of the runner. */
 int swb_attn_prefill_tc(const void* qkv, int row_stride, int total_rows,
                         const int32_t* cu_seqlens, int num_seqs, int max_seqlen,
-                        int H, int Hkv, int dh, float scale, void* out,
-                        uintptr_t stream);
+                        int H, int Hkv, int dh, float scale,
+                        const float* alibi_slopes, void* out, uintptr_t stream);
 /* Paged decode attention for one layer, fused with the current token's
  * RoPE and KV append and with the split-K merge: q/k/v of the current token
  * come from qkv rows [B, row_stride] (q at column 0); when positions/slots are
@@ -153,6 +173,8 @@ int swb_attn_prefill_tc(const void* qkv, int row_stride, int total_rows,
  * of `partition` tokens; the last CTA of each (b, kv head) merges them.
  * workspace must hold swb_attn_decode_workspace(B, H, max_ctx, partition, dh)
  * bytes and be ZERO-initialised once (its merge tickets self-reset).
+ * alibi_slopes (fp32 [H], may be NULL): ALiBi instead of RoPE (BLOOM) —
+ * no rotation, scores + slope_h * (key_pos - query_pos).
  * Replaces the attention share of PerfModel.token_iter_time (perf.py:125-132)
  * and the KV growth of Machine.complete_iteration (machine.py:263-266). */
 size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int partition,
@@ -160,9 +182,10 @@ size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int partition,
 int swb_attn_decode(const void* qkv, int row_stride, void* k_layer,
                     void* v_layer, const int32_t* block_tables, int max_blocks,
                     const int32_t* ctx_lens, const int32_t* positions,
-                    const int32_t* slots, float theta, int B, int H, int Hkv,
-                    int dh, int block_size, float scale, int max_ctx,
-                    int partition, void* workspace, void* out, uintptr_t stream);
+                    const int32_t* slots, float theta,
+                    const float* alibi_slopes, int B, int H, int Hkv, int dh,
+                    int block_size, float scale, int max_ctx, int partition,
+                    void* workspace, void* out, uintptr_t stream);
 
 /* --------------------------------------------- decode-step bookkeeping
  * Graph-resident per-step state update so the decode loop needs no host

@@ -9,7 +9,10 @@ prompt/token phases are latency lookups (reference perf.py:119-132) and KV is
 a byte count (perf.py:134-141); SPEC.md:8/:173 put model math out of scope.
 So the NUMERICS of this oracle are "parity unpinned" by the reference: it
 follows the public Llama decoder definition (RMSNorm, RoPE half-split, GQA,
-SwiGLU) for the shapes in SURVEY §8(c).  What the reference DOES pin — the
+SwiGLU) and the public BLOOM definition (embedding LayerNorm, LayerNorm with
+bias, ALiBi, biased linears, tanh-GELU, tied head) for the shapes in SURVEY
+§8(c).  The BLOOM restatement is checked against transformers'
+BloomForCausalLM on the same weights (tests/test_oracle_cpu.py).  What the reference DOES pin — the
 phase semantics (the prompt phase produces the KV cache and the first token,
 each token-phase iteration consumes the last token plus the KV,
 PAPER.md:217-224; token task context = prompt+1, remaining = out-1,
@@ -30,6 +33,14 @@ import torch
 
 def _rmsnorm(x, w, eps):
     return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
+
+
+def _layernorm(x, w, b, eps):
+    return torch.nn.functional.layer_norm(x, (x.shape[-1],), w, b, eps)
+
+
+def _gelu_tanh(x):
+    return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * x * (1.0 + 0.044715 * x * x)))
 
 
 def rope_tables(positions: torch.Tensor, dh: int, theta: float):
@@ -111,16 +122,20 @@ class PagedKV:
 
 
 class OracleDecoder:
-    """fp32 Llama-style decoder over logical (unsharded, de-interleaved)
-    weights: dict per layer with attn_norm, wq, wk, wv, wo, mlp_norm,
-    w_gate, w_up, wd."""
+    """fp32 decoder over logical (unsharded, de-interleaved) weights: dict per
+    layer with attn_norm, wq, wk, wv, wo, mlp_norm, w_gate, w_up, wd (Llama)
+    or ln1_w/b, wq/k/v, bq/k/v, wo, bo, ln2_w/b, w_up, b_up, wd, bd (BLOOM,
+    with ``extra`` = final_norm_b, emb_norm, emb_norm_b, alibi slopes)."""
 
-    def __init__(self, cfg, layers, embed, lm_head, final_norm, threads: int | None = None):
+    def __init__(self, cfg, layers, embed, lm_head, final_norm, threads: int | None = None,
+                 extra: dict | None = None):
         self.cfg = cfg
         self.layers = layers
         self.embed = embed
         self.lm_head = lm_head
         self.final_norm = final_norm
+        self.extra = extra or {}
+        self.bloom = getattr(cfg, "arch", "llama") == "bloom"
         if threads:
             torch.set_num_threads(threads)
 
@@ -130,11 +145,42 @@ class OracleDecoder:
         from paper_2311_18677_b200.model import logical_layer_fp32
         assert w.tp == 1
         layers = [logical_layer_fp32(w, i) for i in range(w.cfg.n_layers)]
+        extra = {}
+        if w.cfg.arch == "bloom":
+            extra = {k: getattr(w, k).float().cpu()
+                     for k in ("final_norm_b", "emb_norm", "emb_norm_b", "alibi")}
         return cls(w.cfg, layers, w.embed.float().cpu(), w.lm_head.float().cpu(),
-                   w.final_norm.float().cpu())
+                   w.final_norm.float().cpu(), extra=extra)
+
+    def _bloom_layer(self, li, x, pos0, kv_get, kv_put):
+        """BLOOM block: pre-LayerNorm, fused biased qkv, ALiBi scores
+        (slope * key position, as BLOOM builds its alibi tensor), biased
+        dense, residual; LayerNorm, biased up, tanh-GELU, biased down."""
+        cfg, L = self.cfg, self.layers[li]
+        S = x.shape[0]
+        H, dh, eps = cfg.n_heads, cfg.head_dim, cfg.norm_eps
+        h = _layernorm(x, L["ln1_w"], L["ln1_b"], eps)
+        q = (h @ L["wq"].t() + L["bq"]).view(S, H, dh)
+        k = (h @ L["wk"].t() + L["bk"]).view(S, H, dh)
+        v = (h @ L["wv"].t() + L["bv"]).view(S, H, dh)
+        kv_put(li, pos0, k, v)
+        K_all, V_all = kv_get(li, pos0 + S)
+        n = pos0 + S
+        s = torch.einsum("qhd,khd->hqk", q, K_all) / math.sqrt(dh)
+        s = s + self.extra["alibi"][:, None, None] * torch.arange(n, dtype=torch.float32)
+        qpos = torch.arange(pos0, pos0 + S)[:, None]
+        kpos = torch.arange(n)[None, :]
+        s = s.masked_fill((kpos > qpos)[None], float("-inf"))
+        o = torch.einsum("hqk,khd->qhd", s.softmax(-1), V_all).reshape(S, H * dh)
+        x = x + o @ L["wo"].t() + L["bo"]
+        h2 = _layernorm(x, L["ln2_w"], L["ln2_b"], eps)
+        a = _gelu_tanh(h2 @ L["w_up"].t() + L["b_up"])
+        return x + a @ L["wd"].t() + L["bd"]
 
     # -- one layer over S new tokens at positions pos0.. with cached K/V
     def _layer(self, li, x, pos0, kv_get, kv_put):
+        if self.bloom:
+            return self._bloom_layer(li, x, pos0, kv_get, kv_put)
         cfg, L = self.cfg, self.layers[li]
         S = x.shape[0]
         H, Hkv, dh = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
@@ -160,9 +206,15 @@ class OracleDecoder:
 
     def forward(self, tokens, pos0, kv_get, kv_put):
         x = self.embed[torch.as_tensor(tokens, dtype=torch.long)]
+        eps = self.cfg.norm_eps
+        if self.bloom:
+            x = _layernorm(x, self.extra["emb_norm"], self.extra["emb_norm_b"], eps)
         for li in range(self.cfg.n_layers):
             x = self._layer(li, x, pos0, kv_get, kv_put)
-        h = _rmsnorm(x[-1:], self.final_norm, self.cfg.norm_eps)
+        if self.bloom:
+            h = _layernorm(x[-1:], self.final_norm, self.extra["final_norm_b"], eps)
+        else:
+            h = _rmsnorm(x[-1:], self.final_norm, eps)
         return (h @ self.lm_head.t())[0]
 
     # -- contiguous KV

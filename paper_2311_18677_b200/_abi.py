@@ -17,7 +17,7 @@ from .errors import CapacityError, ConfigurationError, NativeError, ValidationEr
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libswb200.so")
 
 SWB_OK, SWB_ERR_INVALID, SWB_ERR_CAPACITY, SWB_ERR_CUDA, SWB_ERR_CONFIG = 0, 1, 2, 3, 4
-EPI_BF16, EPI_F32, EPI_RESID_F32, EPI_SWIGLU = 0, 1, 2, 3
+EPI_BF16, EPI_F32, EPI_RESID_F32, EPI_SWIGLU, EPI_GELU = 0, 1, 2, 3, 4
 KV_POOL_IPC_BYTES = 256
 TP_IPC_BYTES = 128
 
@@ -46,19 +46,22 @@ SIGNATURES = {
     "swb_sync_stream": [_ST],
     "swb_gemm_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_gemv_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _ST],
+    "swb_gemm_bf16_bias": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _ST],
+    "swb_gemv_bf16_bias": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_gemv_rmsnorm_bf16": [_P, _P, _F, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_embed": [_P, _P, _P, _I, _I, _ST],
     "swb_rmsnorm": [_P, _P, _P, _P, _I, _I, _F, _ST],
+    "swb_layernorm": [_P, _P, _P, _P, _P, _I, _I, _F, _I, _ST],
     "swb_argmax": [_P, _I, _I, _P, _ST],
     "swb_rope_kv_write": [_P, _I, _I, _P, _I, _I, _I, _F, _P, _P, _P, _I, _ST],
     "swb_kv_push_layer": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _I, _ST],
     "swb_kv_signal": [_P, _U, _ST],
     "swb_stream_wait_flag": [_P, _U, _ST],
     "swb_attn_prefill": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],
-    "swb_attn_prefill_tc": [_P, _I, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],
+    "swb_attn_prefill_tc": [_P, _I, _I, _P, _I, _I, _I, _I, _I, _F, _P, _P, _ST],
     "swb_attn_decode_workspace": [_I, _I, _I, _I, _I],
-    "swb_attn_decode": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _F, _I, _I, _I, _I, _I, _F, _I,
-                        _I, _P, _P, _ST],
+    "swb_attn_decode": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _F, _P, _I, _I, _I, _I, _I, _F,
+                        _I, _I, _P, _P, _ST],
     "swb_decode_prepare": [_P, _P, _I, _I, _I, _P, _P, _P, _ST],
     "swb_decode_advance": [_P, _P, _P, _P, _P, _I, _I, _ST],
     "swb_slots_from_table": [_P, _I, _I, _I, _P, _ST],
@@ -115,7 +118,8 @@ def check(status: int, what: str = "") -> None:
 
 # kernels launched per successful call (for the bench's gpu_launches claim)
 LAUNCH_MULT = {
-    "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
+    "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemm_bf16_bias": 1, "swb_gemv_bf16_bias": 1,
+    "swb_layernorm": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
     "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
     "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_decode_prepare": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,

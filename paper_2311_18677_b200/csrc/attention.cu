@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
                        __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
                        const int32_t* __restrict__ tables, int max_blocks,
                        const int32_t* __restrict__ ctx_lens, const int32_t* __restrict__ pos,
-                       const int32_t* __restrict__ slots, float log2_theta, int H, int Hkv,
+                       const int32_t* __restrict__ slots, float log2_theta,
+                       const float* __restrict__ alibi, int H, int Hkv,
                        int bs, float scale_log2, int part, float* __restrict__ ws,
                        int* __restrict__ tickets, __nv_bfloat16* __restrict__ out) {
   pdl_trigger();
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
   } else {
     const int ntok = t1 - t0;
     const int cur = pos ? pos[b] : -1;            // current token position
+    const int qpos = pos ? cur : ctx - 1;         // query position (ALiBi)
     const bool own_cur = cur >= t0 && cur < t1;
     // ---- gather the partition: one bulk copy per (block, kv head) tile —
     // 16 tokens x 256 B contiguous in the pool — issued by warp 0's lanes in
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
         lo[j] = __bfloat162float(hp[i0 + j]);
         hi[j] = __bfloat162float(hp[64 + i0 + j]);
       }
-      if (pos) {
+      if (pos && !alibi) {
         rope4(lo, hi, i0, fpos, log2_theta);
         // match the two-kernel path: rotated q is rounded to bf16
 #pragma unroll
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
         lo[j] = __bfloat162float(kp[i0 + j]);
         hi[j] = __bfloat162float(kp[64 + i0 + j]);
       }
-      rope4(lo, hi, i0, fpos, log2_theta);
+      if (!alibi) rope4(lo, hi, i0, fpos, log2_theta);
       const int slot = slots[b];
       const size_t g = (((size_t)(slot >> lbs) * Hkv + kh) * bs + (slot & (bs - 1))) * DA_D;
       const int tt = cur - t0;
@@ -432,6 +434,8 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
           kf[u][4] = e.x; kf[u][5] = e.y; kf[u][6] = f.x; kf[u][7] = f.y;
         }
         for (int gi = 0; gi < G; ++gi) {
+          // ALiBi (BLOOM): + slope * (key_pos - query_pos), log2 domain
+          const float sl = alibi ? alibi[kh * G + gi] * 1.4426950408889634f : 0.f;
           const float4 q0 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8);
           const float4 q1 = *reinterpret_cast<const float4*>(sq + gi * DA_D + hl * 8 + 4);
           float d[4];
@@ -451,7 +455,9 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
           if (hl == 0) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              if (valid[u]) ss[gi * part + tb + u * STRIDE] = d[u];
+              if (valid[u])
+                ss[gi * part + tb + u * STRIDE] =
+                    fmaf(sl, (float)(t0 + tb + u * STRIDE - qpos), d[u]);
           }
         }
       }
@@ -598,9 +604,10 @@ extern "C" size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int parti
 extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, void* v_layer,
                                const int32_t* block_tables, int max_blocks,
                                const int32_t* ctx_lens, const int32_t* positions,
-                               const int32_t* slots, float theta, int B, int H, int Hkv,
-                               int dh, int block_size, float scale, int max_ctx, int partition,
-                               void* workspace, void* out, uintptr_t stream) {
+                               const int32_t* slots, float theta, const float* alibi_slopes,
+                               int B, int H, int Hkv, int dh, int block_size, float scale,
+                               int max_ctx, int partition, void* workspace, void* out,
+                               uintptr_t stream) {
   SWB_REQUIRE(qkv && k_layer && v_layer && block_tables && ctx_lens && workspace && out,
               "swb_attn_decode: null pointer");
   SWB_REQUIRE(dh == DA_D, "swb_attn_decode: dh must be 128");
@@ -611,7 +618,7 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, v
               "swb_attn_decode: bad sizes");
   SWB_REQUIRE((positions == nullptr) == (slots == nullptr),
               "swb_attn_decode: positions and slots go together");
-  SWB_REQUIRE(!positions || theta > 1.f, "swb_attn_decode: theta");
+  SWB_REQUIRE(!positions || alibi_slopes || theta > 1.f, "swb_attn_decode: theta");
   SWB_REQUIRE((block_size & (block_size - 1)) == 0 && partition % block_size == 0,
               "swb_attn_decode: block_size must be a power of two dividing partition");
   const int G = H / Hkv;
@@ -635,7 +642,8 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, v
       attn_decode_kernel, dim3(B, Hkv, NP), dim3(DA_WARPS * 32), smem, (cudaStream_t)stream,
       reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
       reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
-      block_tables, max_blocks, ctx_lens, positions, slots, positions ? log2f(theta) : 0.f, H,
+      block_tables, max_blocks, ctx_lens, positions, slots,
+      positions && !alibi_slopes ? log2f(theta) : 0.f, alibi_slopes, H,
       Hkv, block_size, scale * 1.4426950408889634f, partition, ws, tickets,
       reinterpret_cast<__nv_bfloat16*>(out));
   if (le != cudaSuccess)

@@ -75,10 +75,13 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ALIBI: scores get slope_h * (key - query) (BLOOM; softmax-equivalent to
+// the slope * key form), slopes given per head of this rank.
+template <bool ALIBI>
 __global__ void __launch_bounds__(TA_THREADS, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap tm, const int32_t* cu,
                            int tiles_per_seq, int H, int Hkv, float scale_log2,
-                           __nv_bfloat16* __restrict__ out) {
+                           const float* __restrict__ alibi, __nv_bfloat16* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -189,6 +192,8 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint8_t* prow = smem + TA_OFF_P;
     float m_run = -INFINITY, l_run = 0.f;
+    const float sl2 = ALIBI ? alibi[h] * 1.4426950408889634f : 0.f;
+    const float sc = ALIBI ? 1.f : scale_log2;   // scores already scaled under ALIBI
     for (int j = 0; j < nkv; ++j) {
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
@@ -202,6 +207,15 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
       if (lane == 0) mbar_arrive(&s_free[st]);
       // causal mask (keys beyond the row, incl. keys beyond len) + row max
       const int k0 = j * TA_BN;
+      if (ALIBI) {    // move to the log2 domain here: t = s*scale + slope*(k - q)
+        const float base = sl2 * (float)(k0 - qrow);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            sv[c][i] = __float_as_uint(fmaf(__uint_as_float(sv[c][i]), scale_log2,
+                                            fmaf(sl2, (float)(c * 32 + i), base)));
+      }
       float mx = -INFINITY;
       if (k0 + TA_BN - 1 > q0) {      // tile touches the diagonal (block-uniform)
 #pragma unroll
@@ -220,16 +234,16 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
           for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(sv[c][i]));
       }
       const float m_new = fmaxf(m_run, mx);
-      const float msc = m_new == -INFINITY ? 0.f : m_new * scale_log2;
-      const float corr = m_run == -INFINITY ? 0.f : exp2f(m_run * scale_log2 - msc);
+      const float msc = m_new == -INFINITY ? 0.f : m_new * sc;
+      const float corr = m_run == -INFINITY ? 0.f : exp2f(m_run * sc - msc);
       float rs = 0.f;
       uint32_t pk[4][16];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = exp2f(__uint_as_float(sv[c][2 * i]) * scale_log2 - msc);
-          const float p1 = exp2f(__uint_as_float(sv[c][2 * i + 1]) * scale_log2 - msc);
+          const float p0 = exp2f(__uint_as_float(sv[c][2 * i]) * sc - msc);
+          const float p1 = exp2f(__uint_as_float(sv[c][2 * i + 1]) * sc - msc);
           rs += p0 + p1;
           pk[c][i] = f2_to_bf2(p0, p1);
         }
@@ -297,30 +311,37 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-int launch_attn_prefill_tc(const void* qkv, int row_stride, int total_rows, const int32_t* cu,
-                           int num_seqs, int max_seqlen, int H, int Hkv, float scale,
-                           void* out, cudaStream_t stream) {
+template <bool ALIBI>
+static int launch_tc(const CUtensorMap& tm, const int32_t* cu, int num_seqs, int tiles, int H,
+                     int Hkv, float scale, const float* alibi, void* out, cudaStream_t stream) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr[dev]) {
-    SWB_CUDA(cudaFuncSetAttribute(attn_prefill_tc_kernel,
+    SWB_CUDA(cudaFuncSetAttribute(attn_prefill_tc_kernel<ALIBI>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM));
     attr[dev] = true;
   }
-  CUtensorMap tm;
-  // the whole qkv matrix as one K-major operand: rows = tokens, 64-col boxes
-  const int st = make_tmap_rows(&tm, qkv, total_rows, row_stride, 128);
-  if (st) return st;
-  const int tiles = (max_seqlen + TA_BM - 1) / TA_BM;
-  const cudaError_t le = launch(attn_prefill_tc_kernel, dim3(num_seqs * tiles, H),
+  const cudaError_t le = launch(attn_prefill_tc_kernel<ALIBI>, dim3(num_seqs * tiles, H),
                                 dim3(TA_THREADS), TA_SMEM, stream, tm, cu, tiles, H, Hkv,
-                                scale * 1.4426950408889634f,
+                                scale * 1.4426950408889634f, alibi,
                                 reinterpret_cast<__nv_bfloat16*>(out));
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch attn_prefill_tc_kernel: %s",
                          cudaGetErrorString(le));
   return swb_check_launch("attn_prefill_tc_kernel");
+}
+
+int launch_attn_prefill_tc(const void* qkv, int row_stride, int total_rows, const int32_t* cu,
+                           int num_seqs, int max_seqlen, int H, int Hkv, float scale,
+                           const float* alibi, void* out, cudaStream_t stream) {
+  CUtensorMap tm;
+  // the whole qkv matrix as one K-major operand: rows = tokens, 64-col boxes
+  const int st = make_tmap_rows(&tm, qkv, total_rows, row_stride, 128);
+  if (st) return st;
+  const int tiles = (max_seqlen + TA_BM - 1) / TA_BM;
+  if (alibi) return launch_tc<true>(tm, cu, num_seqs, tiles, H, Hkv, scale, alibi, out, stream);
+  return launch_tc<false>(tm, cu, num_seqs, tiles, H, Hkv, scale, nullptr, out, stream);
 }
 
 }  // namespace swb
@@ -329,8 +350,8 @@ using namespace swb;
 
 extern "C" int swb_attn_prefill_tc(const void* qkv, int row_stride, int total_rows,
                                    const int32_t* cu_seqlens, int num_seqs, int max_seqlen,
-                                   int H, int Hkv, int dh, float scale, void* out,
-                                   uintptr_t stream) {
+                                   int H, int Hkv, int dh, float scale,
+                                   const float* alibi_slopes, void* out, uintptr_t stream) {
   SWB_REQUIRE(qkv && cu_seqlens && out, "swb_attn_prefill_tc: null pointer");
   SWB_REQUIRE(dh == TA_D, "swb_attn_prefill_tc: dh must be 128 (got %d)", dh);
   SWB_REQUIRE(H > 0 && Hkv > 0 && H % Hkv == 0, "swb_attn_prefill_tc: bad heads");
@@ -342,5 +363,5 @@ extern "C" int swb_attn_prefill_tc(const void* qkv, int row_stride, int total_ro
               "swb_attn_prefill_tc: bad sizes");
   if (num_seqs == 0 || max_seqlen == 0 || total_rows == 0) return SWB_OK;
   return launch_attn_prefill_tc(qkv, row_stride, total_rows, cu_seqlens, num_seqs, max_seqlen,
-                                H, Hkv, scale, out, (cudaStream_t)stream);
+                                H, Hkv, scale, alibi_slopes, out, (cudaStream_t)stream);
 }

@@ -176,6 +176,16 @@ __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst,
       : "memory");
 }
 
+// ---------------------------------------------------------------- epilogues
+// BLOOM's MLP activation (tanh approximation, as its reference implementation)
+__device__ __forceinline__ float gelu_tanh(float x) {
+  return 0.5f * x * (1.f + tanhf(0.7978845608028654f * x * (1.f + 0.044715f * x * x)));
+}
+// optional per-output-feature bf16 bias, added to the fp32 accumulator
+__device__ __forceinline__ float bias_at(const __nv_bfloat16* b, int n) {
+  return b ? __bfloat162float(b[n]) : 0.f;
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

@@ -34,6 +34,7 @@ constexpr int G_THREADS = 192;          // TMA warp, MMA warp, 4 epilogue warps
 struct GemmArgs {
   void* out;
   const float* resid;
+  const __nv_bfloat16* bias;
   int M, N, K;
   int epi;
   int m_tiles, tiles;
@@ -81,7 +82,25 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t t_r
     tc_wait_ld();
     const int col = n0 + c * 32;
     if (!row_ok || col >= args.N) continue;
-    if (args.epi == SWB_EPI_BF16) {
+    if (args.bias) {
+      const uint4* bp = reinterpret_cast<const uint4*>(args.bias + col);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 bb = __ldg(bp + i);
+        const uint32_t w4[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = bf2_to_f2(w4[k]);
+          r[8 * i + 2 * k] = __float_as_uint(__uint_as_float(r[8 * i + 2 * k]) + f.x);
+          r[8 * i + 2 * k + 1] = __float_as_uint(__uint_as_float(r[8 * i + 2 * k + 1]) + f.y);
+        }
+      }
+    }
+    if (args.epi == SWB_EPI_GELU) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(gelu_tanh(__uint_as_float(r[i])));
+    }
+    if (args.epi == SWB_EPI_BF16 || args.epi == SWB_EPI_GELU) {
       __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(args.out);
       uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * args.N + col);
 #pragma unroll
@@ -268,11 +287,19 @@ using namespace swb;
 extern "C" int swb_gemm_bf16(const void* a, const void* w, void* out,
                              const void* resid, int M, int N, int K, int epilogue,
                              uintptr_t stream) {
+  return swb_gemm_bf16_bias(a, w, out, resid, nullptr, M, N, K, epilogue, stream);
+}
+
+extern "C" int swb_gemm_bf16_bias(const void* a, const void* w, void* out,
+                                  const void* resid, const void* bias, int M, int N, int K,
+                                  int epilogue, uintptr_t stream) {
   SWB_REQUIRE(a && w && out, "swb_gemm_bf16: null pointer");
+  SWB_REQUIRE(!bias || epilogue != SWB_EPI_SWIGLU, "swb_gemm_bf16: no bias with SwiGLU");
+  SWB_REQUIRE((((uintptr_t)bias) & 15) == 0, "swb_gemm_bf16: bias must be 16-byte aligned");
   SWB_REQUIRE(M > 0 && N > 0 && K > 0, "swb_gemm_bf16: bad shape M=%d N=%d K=%d", M, N, K);
   SWB_REQUIRE(K % 8 == 0, "swb_gemm_bf16: K=%d must be a multiple of 8", K);
   SWB_REQUIRE(N % 32 == 0, "swb_gemm_bf16: N=%d must be a multiple of 32", N);
-  SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_SWIGLU,
+  SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_GELU,
               "swb_gemm_bf16: bad epilogue %d", epilogue);
   SWB_REQUIRE(epilogue != SWB_EPI_SWIGLU || N % 256 == 0,
               "swb_gemm_bf16: SwiGLU epilogue needs N %% 256 == 0 (N=%d)", N);
@@ -295,7 +322,8 @@ extern "C" int swb_gemm_bf16(const void* a, const void* w, void* out,
     attr_set[dev] = true;
   }
   const int m_tiles = (M + GM - 1) / GM, n_tiles = (N + GN - 1) / GN;
-  GemmArgs args{out, reinterpret_cast<const float*>(resid), M, N, K, epilogue, m_tiles,
+  GemmArgs args{out, reinterpret_cast<const float*>(resid),
+                reinterpret_cast<const __nv_bfloat16*>(bias), M, N, K, epilogue, m_tiles,
                 m_tiles * n_tiles};
   dim3 grid(std::min(args.tiles, kNumSMs));
   {

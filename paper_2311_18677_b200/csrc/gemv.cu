@@ -65,7 +65,8 @@ template <int MB, bool NORM>
 __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     gemv_bulk_kernel(const void* __restrict__ xin, const __nv_bfloat16* __restrict__ nw,
                      float eps, const __nv_bfloat16* __restrict__ W, void* out,
-                     const float* resid, int M, int N, int K, int epi, int n_items) {
+                     const float* resid, const __nv_bfloat16* bias, int M, int N, int K,
+                     int epi, int n_items) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TV_STAGES * TV_STAGE_BYTES);
   uint64_t* empty = full + TV_STAGES;
@@ -244,8 +245,11 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
           const int r = item_row(item, j, false);
           if (r < N) {
             const size_t idx = (size_t)m * N + r;
+            v += bias_at(bias, r);
             if (epi == SWB_EPI_BF16)
               reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(v);
+            else if (epi == SWB_EPI_GELU)
+              reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(gelu_tanh(v));
             else if (epi == SWB_EPI_F32)
               reinterpret_cast<float*>(out)[idx] = v;
             else
@@ -259,8 +263,9 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
 
 template <int MB, bool NORM>
 static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
-                       const __nv_bfloat16* w, void* out, const float* r, int M, int N, int K,
-                       int epi, int items, cudaStream_t s) {
+                       const __nv_bfloat16* w, void* out, const float* r,
+                       const __nv_bfloat16* bias, int M, int N, int K, int epi, int items,
+                       cudaStream_t s) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
@@ -273,7 +278,7 @@ static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
   const size_t smem = TV_SMEM + (NORM ? (size_t)M * K * 2 : 0);
   const int grid = min(items, TV_CTAS_PER_SM * kNumSMs);
   const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM>, dim3(grid), dim3(TV_THREADS),
-                                smem, s, x, nw, eps, w, out, r, M, N, K, epi, items);
+                                smem, s, x, nw, eps, w, out, r, bias, M, N, K, epi, items);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("gemv_bulk_kernel");
@@ -312,8 +317,8 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 template <int NB>   // NB = 1 (M <= 8) or 2 (M <= 16) MMAs of 8 batch rows
 __global__ void __launch_bounds__(TM_THREADS, 2)
     gemv_mma_kernel(const __grid_constant__ CUtensorMap tmW, const __nv_bfloat16* x,
-                    void* out, const float* resid, int M, int N, int K, int epi,
-                    int n_items) {
+                    void* out, const float* resid, const __nv_bfloat16* bias, int M, int N,
+                    int K, int epi, int n_items) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -435,8 +440,11 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
         const int r = item * TM_ROWS + row;
         if (r >= N) continue;
         const size_t idx = (size_t)m * N + r;
+        v += bias_at(bias, r);
         if (epi == SWB_EPI_BF16)
           reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(v);
+        else if (epi == SWB_EPI_GELU)
+          reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(gelu_tanh(v));
         else if (epi == SWB_EPI_F32)
           reinterpret_cast<float*>(out)[idx] = v;
         else
@@ -451,7 +459,8 @@ int make_tmap_rows(CUtensorMap* map, const void* base, int rows, int K, int box_
 
 template <int NB>
 static int launch_gemv_mma(const __nv_bfloat16* x, const void* w, void* out, const float* r,
-                           int M, int N, int K, int epi, cudaStream_t s) {
+                           const __nv_bfloat16* bias, int M, int N, int K, int epi,
+                           cudaStream_t s) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
@@ -466,7 +475,7 @@ static int launch_gemv_mma(const __nv_bfloat16* x, const void* w, void* out, con
   const int items = epi == SWB_EPI_SWIGLU ? (N / 2 + 7) / 8 : (N + TM_ROWS - 1) / TM_ROWS;
   const int grid = min(items, 2 * kNumSMs);
   const cudaError_t le = launch(gemv_mma_kernel<NB>, dim3(grid), dim3(TM_THREADS), TM_SMEM, s,
-                                tm, x, out, r, M, N, K, epi, items);
+                                tm, x, out, r, bias, M, N, K, epi, items);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch gemv_mma_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("gemv_mma_kernel");
@@ -483,22 +492,23 @@ static bool gemv_mma_enabled() {
 
 template <bool NORM>
 static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, const void* w,
-                         void* out, const void* resid, int M, int N, int K, int epilogue,
-                         uintptr_t stream) {
+                         void* out, const void* resid, const void* bias_, int M, int N, int K,
+                         int epilogue, uintptr_t stream) {
+  auto bias = reinterpret_cast<const __nv_bfloat16*>(bias_);
   const int items = (N + TV_ROWS - 1) / TV_ROWS;  // 4 rows (or 2 SwiGLU outputs) per item
   auto ws = reinterpret_cast<const __nv_bfloat16*>(w);
   auto rs = reinterpret_cast<const float*>(resid);
   cudaStream_t s = (cudaStream_t)stream;
   if (!NORM && M >= 2 && gemv_mma_enabled()) {
     auto xb = reinterpret_cast<const __nv_bfloat16*>(x);
-    if (M <= 8) return launch_gemv_mma<1>(xb, w, out, rs, M, N, K, epilogue, s);
-    return launch_gemv_mma<2>(xb, w, out, rs, M, N, K, epilogue, s);
+    if (M <= 8) return launch_gemv_mma<1>(xb, w, out, rs, bias, M, N, K, epilogue, s);
+    return launch_gemv_mma<2>(xb, w, out, rs, bias, M, N, K, epilogue, s);
   }
-  if (M == 1) return launch_gemv<1, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
-  if (M <= 2) return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
-  if (M <= 4) return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
-  if (M <= 8) return launch_gemv<8, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
-  return launch_gemv<16, NORM>(x, nw, eps, ws, out, rs, M, N, K, epilogue, items, s);
+  if (M == 1) return launch_gemv<1, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
+  if (M <= 2) return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
+  if (M <= 4) return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
+  if (M <= 8) return launch_gemv<8, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
+  return launch_gemv<16, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
 }
 
 }  // namespace swb
@@ -510,7 +520,7 @@ static int check_gemv_args(const char* fn, const void* x, const void* w, void* o
   SWB_REQUIRE(x && w && out, "%s: null pointer", fn);
   SWB_REQUIRE(M >= 1 && M <= 16, "%s: M=%d outside 1..16", fn, M);
   SWB_REQUIRE(N > 0 && K > 0 && K % 8 == 0, "%s: bad shape N=%d K=%d", fn, N, K);
-  SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_SWIGLU, "%s: bad epilogue %d",
+  SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_GELU, "%s: bad epilogue %d",
               fn, epilogue);
   SWB_REQUIRE(epilogue != SWB_EPI_SWIGLU || N % 256 == 0, "%s: SwiGLU needs N %% 256 == 0", fn);
   SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid, "%s: resid needed", fn);
@@ -521,9 +531,16 @@ static int check_gemv_args(const char* fn, const void* x, const void* w, void* o
 
 extern "C" int swb_gemv_bf16(const void* x, const void* w, void* out, const void* resid, int M,
                              int N, int K, int epilogue, uintptr_t stream) {
+  return swb_gemv_bf16_bias(x, w, out, resid, nullptr, M, N, K, epilogue, stream);
+}
+
+extern "C" int swb_gemv_bf16_bias(const void* x, const void* w, void* out, const void* resid,
+                                  const void* bias, int M, int N, int K, int epilogue,
+                                  uintptr_t stream) {
   const int st = check_gemv_args("swb_gemv_bf16", x, w, out, resid, M, N, K, epilogue);
   if (st) return st;
-  return dispatch_gemv<false>(x, nullptr, 0.f, w, out, resid, M, N, K, epilogue, stream);
+  SWB_REQUIRE(!bias || epilogue != SWB_EPI_SWIGLU, "swb_gemv_bf16: no bias with SwiGLU");
+  return dispatch_gemv<false>(x, nullptr, 0.f, w, out, resid, bias, M, N, K, epilogue, stream);
 }
 
 extern "C" int swb_gemv_rmsnorm_bf16(const float* x, const void* norm_w, float eps,
@@ -539,5 +556,5 @@ extern "C" int swb_gemv_rmsnorm_bf16(const float* x, const void* norm_w, float e
               "swb_gemv_rmsnorm_bf16: M*K*2 = %d bytes exceeds %d (use swb_rmsnorm + GEMV)",
               M * K * 2, TV_HS_MAX);
   return dispatch_gemv<true>(x, reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, w, out,
-                             resid, M, N, K, epilogue, stream);
+                             resid, nullptr, M, N, K, epilogue, stream);
 }

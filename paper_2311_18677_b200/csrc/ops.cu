@@ -34,6 +34,68 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens,
 }
 
 // ---------------------------------------------------------------- rmsnorm
+// LayerNorm (BLOOM): out = (x - mean) * rstd * w + b over fp32 rows, two
+// passes over the (L1/L2-resident) row; bf16 or fp32 output (the embedding
+// LayerNorm produces the fp32 residual stream, possibly in place).
+__global__ void layernorm_kernel(const float* x, const int32_t* __restrict__ row_index,
+                                 const __nv_bfloat16* __restrict__ w,
+                                 const __nv_bfloat16* __restrict__ b, void* out, int d,
+                                 float eps, int out_f32) {
+  pdl_wait();
+  const int r = blockIdx.x;
+  const int src = row_index ? row_index[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * d);
+  __shared__ float red[32];
+  __shared__ float stat[2];
+  float s = 0.f;
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+    const float4 v = xr[c];
+    s += (v.x + v.y) + (v.z + v.w);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) stat[0] = v / (float)d;
+  }
+  __syncthreads();
+  const float mean = stat[0];
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+    const float4 v = xr[c];
+    const float a0 = v.x - mean, a1 = v.y - mean, a2 = v.z - mean, a3 = v.w - mean;
+    ss += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+  }
+  ss = warp_sum(ss);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) stat[1] = rsqrtf(v / (float)d + eps);
+  }
+  __syncthreads();
+  const float rstd = stat[1];
+  const uint2* wv = reinterpret_cast<const uint2*>(w);
+  const uint2* bv = reinterpret_cast<const uint2*>(b);
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+    const float4 v = xr[c];
+    const uint2 ww = wv[c], bb = bv[c];
+    const float2 w0 = bf2_to_f2(ww.x), w1 = bf2_to_f2(ww.y);
+    const float2 b0 = bf2_to_f2(bb.x), b1 = bf2_to_f2(bb.y);
+    const float o0 = (v.x - mean) * rstd * w0.x + b0.x, o1 = (v.y - mean) * rstd * w0.y + b0.y;
+    const float o2 = (v.z - mean) * rstd * w1.x + b1.x, o3 = (v.w - mean) * rstd * w1.y + b1.y;
+    if (out_f32)
+      reinterpret_cast<float4*>(out)[(size_t)r * (d / 4) + c] = make_float4(o0, o1, o2, o3);
+    else
+      reinterpret_cast<uint2*>(out)[(size_t)r * (d / 4) + c] =
+          make_uint2(f2_to_bf2(o0, o1), f2_to_bf2(o2, o3));
+  }
+}
+
 __global__ void rmsnorm_kernel(const float* __restrict__ x,
                                const int32_t* __restrict__ row_index,
                                const __nv_bfloat16* __restrict__ w,
@@ -151,12 +213,17 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int row_stride,
     float ra[4], rb[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      // inv_freq = theta^(-2i/dh)
-      const float inv_freq = exp2f(-log2_theta * (float)(2 * (i0 + j)) / (float)dh);
-      float s, c;
-      sincosf(pos * inv_freq, &s, &c);
-      ra[j] = a[j] * c - b[j] * s;
-      rb[j] = b[j] * c + a[j] * s;
+      if (log2_theta > 0.f) {
+        // inv_freq = theta^(-2i/dh)
+        const float inv_freq = exp2f(-log2_theta * (float)(2 * (i0 + j)) / (float)dh);
+        float s, c;
+        sincosf(pos * inv_freq, &s, &c);
+        ra[j] = a[j] * c - b[j] * s;
+        rb[j] = b[j] * c + a[j] * s;
+      } else {  // no rotary embedding (ALiBi models): KV write only
+        ra[j] = a[j];
+        rb[j] = b[j];
+      }
     }
     const uint2 nlo = make_uint2(f2_to_bf2(ra[0], ra[1]), f2_to_bf2(ra[2], ra[3]));
     const uint2 nhi = make_uint2(f2_to_bf2(rb[0], rb[1]), f2_to_bf2(rb[2], rb[3]));
@@ -310,6 +377,22 @@ extern "C" int swb_rmsnorm(const float* x, const int32_t* row_index, const void*
   return swb_check_launch("rmsnorm_kernel");
 }
 
+extern "C" int swb_layernorm(const float* x, const int32_t* row_index, const void* w,
+                             const void* b, void* out, int rows, int d, float eps, int out_f32,
+                             uintptr_t stream) {
+  SWB_REQUIRE(x && w && b && out, "swb_layernorm: null pointer");
+  SWB_REQUIRE(rows >= 0 && d > 0 && d % 4 == 0, "swb_layernorm: bad shape");
+  SWB_REQUIRE(!row_index || !out_f32 || (const void*)x != out,
+              "swb_layernorm: gathered rows cannot be normalised in place");
+  if (rows == 0) return SWB_OK;
+  const cudaError_t le = launch(layernorm_kernel, dim3(rows), dim3(512), 0, STREAM, x,
+                                row_index, reinterpret_cast<const __nv_bfloat16*>(w),
+                                reinterpret_cast<const __nv_bfloat16*>(b), out, d, eps, out_f32);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch layernorm_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("layernorm_kernel");
+}
+
 extern "C" int swb_argmax(const float* logits, int rows, int V, int32_t* out,
                           uintptr_t stream) {
   SWB_REQUIRE(logits && out, "swb_argmax: null pointer");
@@ -336,13 +419,13 @@ extern "C" int swb_rope_kv_write(void* qkv, int rows, int row_stride,
   SWB_REQUIRE((k_layer == nullptr) == (v_layer == nullptr),
               "swb_rope_kv_write: k/v pools must both be set or both null");
   SWB_REQUIRE(!k_layer || (slots && block_size > 0), "swb_rope_kv_write: slots");
-  SWB_REQUIRE(theta > 1.f, "swb_rope_kv_write: theta");
+  SWB_REQUIRE(theta > 1.f || theta == 0.f, "swb_rope_kv_write: theta (0 = no rotation)");
   if (rows == 0) return SWB_OK;
   {
     const cudaError_t le_ = launch(rope_kv_kernel, dim3(rows), dim3(256), 0, STREAM,
         
       reinterpret_cast<__nv_bfloat16*>(qkv), row_stride, positions, H, Hkv, dh,
-      log2f(theta), reinterpret_cast<__nv_bfloat16*>(k_layer),
+      theta > 0.f ? log2f(theta) : 0.f, reinterpret_cast<__nv_bfloat16*>(k_layer),
       reinterpret_cast<__nv_bfloat16*>(v_layer), slots, block_size);
     if (le_ != cudaSuccess)
       return swb_set_error(SWB_ERR_CUDA, "launch rope_kv_kernel: %s", cudaGetErrorString(le_));

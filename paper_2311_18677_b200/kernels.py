@@ -10,13 +10,14 @@ import os
 import torch
 
 from . import _abi
-from ._abi import EPI_BF16, EPI_F32, EPI_RESID_F32, EPI_SWIGLU, call
+from ._abi import EPI_BF16, EPI_F32, EPI_GELU, EPI_RESID_F32, EPI_SWIGLU, call
 from .errors import ValidationError
 
-__all__ = ["gemm", "gemv", "gemv_rmsnorm", "linear", "embed", "rmsnorm", "argmax", "rope_kv_write",
+__all__ = ["gemm", "gemv", "gemv_rmsnorm", "linear", "embed", "rmsnorm", "layernorm", "argmax",
+           "rope_kv_write",
            "kv_push_layer", "attn_prefill", "attn_decode", "decode_prepare",
            "decode_advance", "slots_from_table", "kv_signal", "stream_wait_flag",
-           "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "GEMV_MAX_ROWS"]
+           "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "EPI_GELU", "GEMV_MAX_ROWS"]
 
 GEMV_MAX_ROWS = 16
 
@@ -39,12 +40,16 @@ def _out_shape(M, N, epi):
 
 
 def _alloc_out(a, M, N, epi):
-    dt = torch.bfloat16 if epi in (EPI_BF16, EPI_SWIGLU) else torch.float32
+    dt = torch.bfloat16 if epi in (EPI_BF16, EPI_SWIGLU, EPI_GELU) else torch.float32
     return torch.empty(_out_shape(M, N, epi), dtype=dt, device=a.device)
 
 
-def gemm(a, w, epi=EPI_BF16, out=None, resid=None):
-    """tcgen05 GEMM: out = epi(a[M,K] @ w[N,K]^T)."""
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+def gemm(a, w, epi=EPI_BF16, out=None, resid=None, bias=None):
+    """tcgen05 GEMM: out = epi(a[M,K] @ w[N,K]^T + bias)."""
     _req(a, torch.bfloat16, "a")
     _req(w, torch.bfloat16, "w")
     M, K = a.shape
@@ -53,12 +58,12 @@ def gemm(a, w, epi=EPI_BF16, out=None, resid=None):
         raise ValidationError(f"K mismatch {a.shape} vs {w.shape}")
     if out is None:
         out = _alloc_out(a, M, N, epi)
-    call("swb_gemm_bf16", a.data_ptr(), w.data_ptr(), out.data_ptr(),
-         resid.data_ptr() if resid is not None else None, M, N, K, epi, _stream())
+    call("swb_gemm_bf16_bias", a.data_ptr(), w.data_ptr(), out.data_ptr(), _ptr(resid),
+         _ptr(bias), M, N, K, epi, _stream())
     return out
 
 
-def gemv(x, w, epi=EPI_BF16, out=None, resid=None):
+def gemv(x, w, epi=EPI_BF16, out=None, resid=None, bias=None):
     """Weight-streaming skinny GEMM for M <= 16 rows."""
     _req(x, torch.bfloat16, "x")
     _req(w, torch.bfloat16, "w")
@@ -66,8 +71,8 @@ def gemv(x, w, epi=EPI_BF16, out=None, resid=None):
     N = w.shape[0]
     if out is None:
         out = _alloc_out(x, M, N, epi)
-    call("swb_gemv_bf16", x.data_ptr(), w.data_ptr(), out.data_ptr(),
-         resid.data_ptr() if resid is not None else None, M, N, K, epi, _stream())
+    call("swb_gemv_bf16_bias", x.data_ptr(), w.data_ptr(), out.data_ptr(), _ptr(resid),
+         _ptr(bias), M, N, K, epi, _stream())
     return out
 
 
@@ -86,12 +91,12 @@ def gemv_rmsnorm(x, norm_w, eps, w, epi=EPI_BF16, out=None, resid=None):
     return out
 
 
-def linear(x, w, epi=EPI_BF16, out=None, resid=None):
+def linear(x, w, epi=EPI_BF16, out=None, resid=None, bias=None):
     """Dispatch on row count: <= 16 rows streams weights (decode), more rows
     go to the tcgen05 GEMM (prefill).  Both are native kernels."""
     if x.shape[0] <= GEMV_MAX_ROWS:
-        return gemv(x, w, epi, out, resid)
-    return gemm(x, w, epi, out, resid)
+        return gemv(x, w, epi, out, resid, bias)
+    return gemm(x, w, epi, out, resid, bias)
 
 
 def embed(tokens, table, out=None):
@@ -113,6 +118,21 @@ def rmsnorm(x, w, eps, rows_index=None, out=None):
         out = torch.empty(rows, d, dtype=torch.bfloat16, device=x.device)
     call("swb_rmsnorm", x.data_ptr(), rows_index.data_ptr() if rows_index is not None else None,
          w.data_ptr(), out.data_ptr(), rows, d, float(eps), _stream())
+    return out
+
+
+def layernorm(x, w, b, eps, rows_index=None, out=None, out_f32=False):
+    """LayerNorm with bias (BLOOM); fp32 out (may be x) when out_f32."""
+    _req(x, torch.float32, "x")
+    _req(w, torch.bfloat16, "w")
+    _req(b, torch.bfloat16, "b")
+    rows = x.shape[0] if rows_index is None else rows_index.shape[0]
+    d = x.shape[1]
+    if out is None:
+        out = torch.empty(rows, d, dtype=torch.float32 if out_f32 else torch.bfloat16,
+                          device=x.device)
+    call("swb_layernorm", x.data_ptr(), _ptr(rows_index), w.data_ptr(), b.data_ptr(),
+         out.data_ptr(), rows, d, float(eps), int(bool(out_f32)), _stream())
     return out
 
 
@@ -144,19 +164,24 @@ def kv_push_layer(qkv, rows, H, Hkv, dh, dst_k, dst_v, dst_slots, block_size, nu
 
 
 def attn_prefill(qkv, cu_seqlens, num_seqs, max_seqlen, H, Hkv, dh, scale, out=None,
-                 impl=None):
+                 impl=None, alibi=None):
     """Causal varlen prefill attention.  impl "tc" = tcgen05/TMEM kernel (the
-    default; SWB_ATTN_TC=0 selects the mma.sync FlashAttention-2 kernel)."""
+    default; SWB_ATTN_TC=0 selects the mma.sync FlashAttention-2 kernel).
+    ``alibi``: fp32 [H] slopes (BLOOM), tcgen05 kernel only."""
     _req(qkv, torch.bfloat16, "qkv")
     _req(cu_seqlens, torch.int32, "cu_seqlens")
     if out is None:
         out = torch.empty(qkv.shape[0], H * dh, dtype=torch.bfloat16, device=qkv.device)
     if impl is None:
         impl = "fa2" if os.environ.get("SWB_ATTN_TC", "1") == "0" else "tc"
+    if alibi is not None:
+        _req(alibi, torch.float32, "alibi")
+        if impl != "tc":
+            raise ValidationError("ALiBi prefill attention is implemented by the tcgen05 kernel")
     if impl == "tc":
         call("swb_attn_prefill_tc", qkv.data_ptr(), qkv.shape[1], qkv.shape[0],
              cu_seqlens.data_ptr(), num_seqs, max_seqlen, H, Hkv, dh, float(scale),
-             out.data_ptr(), _stream())
+             _ptr(alibi), out.data_ptr(), _stream())
     else:
         call("swb_attn_prefill", qkv.data_ptr(), qkv.shape[1], cu_seqlens.data_ptr(), num_seqs,
              max_seqlen, H, Hkv, dh, float(scale), out.data_ptr(), _stream())
@@ -169,7 +194,7 @@ def attn_decode_workspace_bytes(B, H, max_ctx, partition, dh):
 
 def attn_decode(qkv, k_layer, v_layer, block_tables, ctx_lens, B, H, Hkv, dh, block_size,
                 scale, max_ctx, partition, workspace, out=None, positions=None, slots=None,
-                theta=10000.0):
+                theta=10000.0, alibi=None):
     """Paged decode attention; with positions/slots it also applies RoPE to the
     current token and appends its K/V to the pool (one kernel per layer).
     ``workspace`` must be zero-initialised once (merge tickets)."""
@@ -178,7 +203,8 @@ def attn_decode(qkv, k_layer, v_layer, block_tables, ctx_lens, B, H, Hkv, dh, bl
     call("swb_attn_decode", qkv.data_ptr(), qkv.shape[1], k_layer, v_layer,
          block_tables.data_ptr(), block_tables.shape[1], ctx_lens.data_ptr(),
          positions.data_ptr() if positions is not None else None,
-         slots.data_ptr() if slots is not None else None, float(theta), B, H, Hkv, dh,
+         slots.data_ptr() if slots is not None else None, float(theta), _ptr(alibi), B, H,
+         Hkv, dh,
          block_size, float(scale), max_ctx, partition, workspace.data_ptr(), out.data_ptr(),
          _stream())
     return out

@@ -14,10 +14,17 @@ Weight layout per tensor-parallel rank (all bf16, K-major = [out, in]):
              wgu [2 * ffn/tp, d] (gate/up interleaved in 128-row groups so the
              GEMM epilogue sees gate and up of the same features in one tile),
              wd [d, ffn/tp].
+BLOOM (arch "bloom": LayerNorm with bias, ALiBi instead of RoPE, biased
+linears, GELU MLP, tied embeddings, embedding LayerNorm):
+  lm_head is embed; emb_norm/emb_norm_b, final_norm/final_norm_b [d]
+  per layer adds attn_norm_b, mlp_norm_b [d], bqkv [(3 H/tp) dh] (sharded),
+  bo, bd [d] (replicated: added once, by TP rank 0), bup [ffn/tp]; wgu is the
+  plain up projection [ffn/tp, d] (no gate).
 """
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import torch
@@ -54,14 +61,19 @@ class ModelConfig:
     def qkv_dim(self) -> int:
         return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
 
+    @property
+    def is_bloom(self) -> bool:
+        return self.arch == "bloom"
+
     def params_nonembed(self) -> int:
         d, dh = self.d_model, self.head_dim
         per = d * self.n_heads * dh + 2 * d * self.n_kv_heads * dh + self.n_heads * dh * d
-        per += 3 * d * self.ffn
+        per += (2 if self.is_bloom else 3) * d * self.ffn   # up+down vs gate+up+down
         return self.n_layers * per
 
     def weight_bytes(self, tp: int = 1) -> int:
-        return 2 * (self.params_nonembed() // tp + 2 * self.vocab * self.d_model)
+        tables = 1 if self.is_bloom else 2                  # tied embeddings (BLOOM)
+        return 2 * (self.params_nonembed() // tp + tables * self.vocab * self.d_model)
 
     def prefill_flops(self, S: int, tp: int = 1) -> float:
         """Algorithmic prefill FLOPs per TP rank for one S-token prompt
@@ -85,8 +97,8 @@ class ModelConfig:
             raise ConfigurationError(f"{self.name}: ffn/tp must be a multiple of 128")
         if self.head_dim != 128:
             raise ConfigurationError("kernels are specialised for head_dim 128")
-        if self.arch != "llama":
-            raise ConfigurationError(f"arch {self.arch!r} kernels not built in this round")
+        if self.arch not in ("llama", "bloom"):
+            raise ConfigurationError(f"unknown arch {self.arch!r}")
 
 
 PRESETS: dict[str, ModelConfig] = {
@@ -99,7 +111,25 @@ PRESETS: dict[str, ModelConfig] = {
     "llama2-70b-mha": ModelConfig("llama2-70b-mha", 80, 8192, 64, 64, 128, 28672, 32000),
     "bloom-176b": ModelConfig("bloom-176b", 70, 14336, 112, 112, 128, 57344, 250880,
                               arch="bloom", max_token_batch=26),
+    # builder-defined BLOOM-architecture correctness model (C5's kernels);
+    # 6 heads exercise the non-power-of-two ALiBi slope rule like BLOOM's 112
+    "bloom-tiny": ModelConfig("bloom-tiny", n_layers=3, d_model=768, n_heads=6, n_kv_heads=6,
+                              head_dim=128, ffn=3072, vocab=2048, arch="bloom"),
 }
+
+
+def alibi_slopes(n_heads: int) -> list[float]:
+    """ALiBi head slopes as BLOOM defines them: a geometric sequence for the
+    largest power of two <= n heads, then the odd powers of the next finer
+    base for the remainder."""
+    p2 = 2 ** math.floor(math.log2(n_heads))
+    base = 2.0 ** (-(2.0 ** -(math.log2(p2) - 3)))
+    slopes = [base ** i for i in range(1, p2 + 1)]
+    if p2 != n_heads:
+        extra = 2.0 ** (-(2.0 ** -(math.log2(2 * p2) - 3)))
+        rem = min(p2, n_heads - p2)
+        slopes += [extra ** i for i in range(1, 2 * rem, 2)]
+    return slopes
 
 
 def get_config(name: str) -> ModelConfig:
@@ -128,6 +158,13 @@ class LayerWeights:
     mlp_norm: torch.Tensor
     wgu: torch.Tensor
     wd: torch.Tensor
+    # BLOOM only
+    attn_norm_b: torch.Tensor | None = None
+    mlp_norm_b: torch.Tensor | None = None
+    bqkv: torch.Tensor | None = None
+    bo: torch.Tensor | None = None
+    bup: torch.Tensor | None = None
+    bd: torch.Tensor | None = None
 
 
 @dataclass
@@ -139,11 +176,21 @@ class Weights:
     lm_head: torch.Tensor
     final_norm: torch.Tensor
     layers: list[LayerWeights] = field(default_factory=list)
+    # BLOOM only
+    final_norm_b: torch.Tensor | None = None
+    emb_norm: torch.Tensor | None = None
+    emb_norm_b: torch.Tensor | None = None
+    alibi: torch.Tensor | None = None      # fp32 slopes of this rank's heads
 
     def nbytes(self) -> int:
-        n = self.embed.numel() + self.lm_head.numel() + self.final_norm.numel()
+        seen, n = set(), 0
+        tensors = [self.embed, self.lm_head, self.final_norm]
         for lw in self.layers:
-            n += sum(t.numel() for t in (lw.attn_norm, lw.wqkv, lw.wo, lw.mlp_norm, lw.wgu, lw.wd))
+            tensors += [lw.attn_norm, lw.wqkv, lw.wo, lw.mlp_norm, lw.wgu, lw.wd]
+        for t in tensors:
+            if t.data_ptr() not in seen:      # tied embeddings count once
+                seen.add(t.data_ptr())
+                n += t.numel()
         return 2 * n
 
 
@@ -173,20 +220,40 @@ def init_weights(cfg: ModelConfig, seed: int = 0, tp: int = 1, rank: int = 0,
     std = cfg.init_std
     d, dh = cfg.d_model, cfg.head_dim
     hq, hkv, f = cfg.n_heads // tp, cfg.n_kv_heads // tp, cfg.ffn // tp
+
+    def norm_w(layer, tag):
+        return (1.0 + _randn(g(layer, tag, 0), (d,), std, dev).float()).bfloat16()
+
     embed = _randn(g(-1, 1, 0), (cfg.vocab, d), 1.0, dev)
-    lm_head = _randn(g(-1, 2, 0), (cfg.vocab, d), std, dev)
-    final_norm = (1.0 + _randn(g(-1, 3, 0), (d,), std, dev).float()).bfloat16()
+    if cfg.is_bloom:
+        lm_head = embed                                   # tied
+        bloom = dict(final_norm_b=_randn(g(-1, 4, 0), (d,), std, dev),
+                     emb_norm=norm_w(-1, 5), emb_norm_b=_randn(g(-1, 6, 0), (d,), std, dev),
+                     alibi=torch.tensor(alibi_slopes(cfg.n_heads)[rank * hq:(rank + 1) * hq],
+                                        dtype=torch.float32, device=dev))
+    else:
+        lm_head = _randn(g(-1, 2, 0), (cfg.vocab, d), std, dev)
+        bloom = {}
+    final_norm = norm_w(-1, 3)
     layers = []
     for layer in range(cfg.n_layers):
-        layers.append(LayerWeights(
-            attn_norm=(1.0 + _randn(g(layer, 10, 0), (d,), std, dev).float()).bfloat16(),
+        lw = LayerWeights(
+            attn_norm=norm_w(layer, 10),
             wqkv=_randn(g(layer, 11, rank), ((hq + 2 * hkv) * dh, d), std, dev),
             wo=_randn(g(layer, 12, rank), (d, hq * dh), std, dev),
-            mlp_norm=(1.0 + _randn(g(layer, 13, 0), (d,), std, dev).float()).bfloat16(),
-            wgu=_randn(g(layer, 14, rank), (2 * f, d), std, dev),
+            mlp_norm=norm_w(layer, 13),
+            wgu=_randn(g(layer, 14, rank), ((1 if cfg.is_bloom else 2) * f, d), std, dev),
             wd=_randn(g(layer, 15, rank), (d, f), std, dev),
-        ))
-    return Weights(cfg, tp, rank, embed, lm_head, final_norm, layers)
+        )
+        if cfg.is_bloom:
+            lw.attn_norm_b = _randn(g(layer, 20, 0), (d,), std, dev)
+            lw.mlp_norm_b = _randn(g(layer, 21, 0), (d,), std, dev)
+            lw.bqkv = _randn(g(layer, 22, rank), ((hq + 2 * hkv) * dh,), std, dev)
+            lw.bo = _randn(g(layer, 23, 0), (d,), std, dev)
+            lw.bup = _randn(g(layer, 24, rank), (f,), std, dev)
+            lw.bd = _randn(g(layer, 25, 0), (d,), std, dev)
+        layers.append(lw)
+    return Weights(cfg, tp, rank, embed, lm_head, final_norm, layers, **bloom)
 
 
 def logical_layer_fp32(w: Weights, layer: int) -> dict:
@@ -196,6 +263,17 @@ def logical_layer_fp32(w: Weights, layer: int) -> dict:
     lw = w.layers[layer]
     hq, hkv, dh = cfg.n_heads // w.tp, cfg.n_kv_heads // w.tp, cfg.head_dim
     qkv = lw.wqkv.float().cpu()
+    if cfg.is_bloom:
+        f32 = lambda t: t.float().cpu()  # noqa: E731
+        b = f32(lw.bqkv)
+        return {
+            "ln1_w": f32(lw.attn_norm), "ln1_b": f32(lw.attn_norm_b),
+            "wq": qkv[:hq * dh], "wk": qkv[hq * dh:(hq + hkv) * dh], "wv": qkv[(hq + hkv) * dh:],
+            "bq": b[:hq * dh], "bk": b[hq * dh:(hq + hkv) * dh], "bv": b[(hq + hkv) * dh:],
+            "wo": f32(lw.wo), "bo": f32(lw.bo),
+            "ln2_w": f32(lw.mlp_norm), "ln2_b": f32(lw.mlp_norm_b),
+            "w_up": f32(lw.wgu), "b_up": f32(lw.bup), "wd": f32(lw.wd), "bd": f32(lw.bd),
+        }
     gate, up = split_gate_up(lw.wgu.float().cpu())
     return {
         "attn_norm": lw.attn_norm.float().cpu(),

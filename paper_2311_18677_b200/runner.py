@@ -60,6 +60,9 @@ class ModelRunner:
         self.rank = weights.rank
         self.tp_group = tp_group
         self.tp_comm = None
+        self.bloom = cfg.is_bloom
+        self.theta = 0.0 if self.bloom else cfg.rope_theta     # 0: ALiBi, no rotation
+        self.alibi = weights.alibi
         self.tp_max_rows = tp_max_rows    # largest prefill / decode row count reduced
         self.kv = kv
         self.hq = cfg.n_heads // self.tp
@@ -95,22 +98,44 @@ class ModelRunner:
         if c is not None:
             c.reset()
 
-    def _proj_reduce(self, inp, w, x):
-        """x <- x + sum over TP ranks of inp @ w^T (O / down projections).
-        TP: rank 0 folds the residual into its partial; the partials meet in
-        the peer-memory slot and the all-reduce writes x."""
+    def _proj_reduce(self, inp, w, x, bias=None):
+        """x <- x + sum over TP ranks of inp @ w^T (+ bias) (O / down
+        projections).  TP: rank 0 folds the residual (and the replicated
+        bias) into its partial; the partials meet in the peer-memory slot and
+        the all-reduce writes x."""
         if self.tp == 1:
-            K.linear(inp, w, K.EPI_RESID_F32, out=x, resid=x)
+            K.linear(inp, w, K.EPI_RESID_F32, out=x, resid=x, bias=bias)
             return
+        b = bias if self.rank == 0 else None
         c = self._comm()
         if c is None:
-            K.linear(inp, w, self._resid_epi(), out=x, resid=x)
+            K.linear(inp, w, self._resid_epi(), out=x, resid=x, bias=b)
             self._allreduce(x)
             return
         s = c.next_slot()
         part = c.slot(s, x.shape)
-        K.linear(inp, w, self._resid_epi(), out=part, resid=x)
+        K.linear(inp, w, self._resid_epi(), out=part, resid=x, bias=b)
         c.allreduce(s, x)
+
+    # -- architecture switches (Llama: RMSNorm / RoPE / SwiGLU; BLOOM:
+    #    LayerNorm+bias / ALiBi / biased linears + GELU / embedding LayerNorm)
+    def _norm(self, x, w, b, out, rows_index=None):
+        if self.bloom:
+            K.layernorm(x, w, b, self.cfg.norm_eps, rows_index=rows_index, out=out)
+        else:
+            K.rmsnorm(x, w, self.cfg.norm_eps, rows_index=rows_index, out=out)
+
+    def _embed(self, tokens, x):
+        K.embed(tokens, self.w.embed, out=x)
+        if self.bloom:
+            K.layernorm(x, self.w.emb_norm, self.w.emb_norm_b, self.cfg.norm_eps, out=x,
+                        out_f32=True)
+
+    def _mlp_up(self, h, lw, out):
+        if self.bloom:
+            K.linear(h, lw.wgu, K.EPI_GELU, out=out, bias=lw.bup)
+        else:
+            K.linear(h, lw.wgu, K.EPI_SWIGLU, out=out)
 
     def _resid_epi(self):
         # with TP only rank 0 folds the residual in; the all-reduce sums the rest
@@ -167,19 +192,19 @@ class ModelRunner:
                            torch.cuda.Event(enable_timing=True)) for _ in range(cfg.n_layers)]
                 self._compute_end = torch.cuda.Event(enable_timing=True)
         self._begin_reductions()
-        K.embed(tokens, w.embed, out=x)
+        self._embed(tokens, x)
         for li, lw in enumerate(w.layers):
             qkv = self.pqkv[li & 1][:T]
             if push and li >= 2:
                 main.wait_event(push_events[li - 2])  # qkv buffer reuse
-            K.rmsnorm(x, lw.attn_norm, cfg.norm_eps, out=h)
-            K.linear(h, lw.wqkv, K.EPI_BF16, out=qkv)
+            self._norm(x, lw.attn_norm, lw.attn_norm_b, out=h)
+            K.linear(h, lw.wqkv, K.EPI_BF16, out=qkv, bias=lw.bqkv)
             if local_slots is not None and self.kv is not None:
-                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, cfg.rope_theta,
+                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, self.theta,
                                 self.kv.k_layer_ptr(li), self.kv.v_layer_ptr(li), local_slots,
                                 self.kv.block_size)
-            else:
-                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, cfg.rope_theta)
+            elif not self.bloom:
+                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, self.theta)
             if push:
                 ev = torch.cuda.Event()
                 ev.record(main)
@@ -199,13 +224,13 @@ class ModelRunner:
                     done.record(self.push_stream)
                 push_events.append(done)
             K.attn_prefill(qkv, cu, R, max(lens), self.hq, self.hkv, self.dh, self.scale,
-                           out=attn)
-            self._proj_reduce(attn, lw.wo, x)
-            K.rmsnorm(x, lw.mlp_norm, cfg.norm_eps, out=h)
-            K.linear(h, lw.wgu, K.EPI_SWIGLU, out=act)
-            self._proj_reduce(act, lw.wd, x)
+                           out=attn, alibi=self.alibi)
+            self._proj_reduce(attn, lw.wo, x, lw.bo)
+            self._norm(x, lw.mlp_norm, lw.mlp_norm_b, out=h)
+            self._mlp_up(h, lw, act)
+            self._proj_reduce(act, lw.wd, x, lw.bd)
         last = self.plast[:R]
-        K.rmsnorm(x, w.final_norm, cfg.norm_eps, rows_index=last_rows, out=last)
+        self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=last_rows)
         logits = self.plogits[:R]
         K.linear(last, w.lm_head, K.EPI_F32, out=logits)
         first = self.pfirst[:R]
@@ -287,37 +312,40 @@ class DecodeGraph:
         r._begin_reductions()
         K.decode_prepare(self.ctx, self.tables, kv.block_size, B, self.pos, self.slots,
                          self.attn_len)
-        K.embed(self.cur_tok, w.embed, out=self.x)
+        r._embed(self.cur_tok, self.x)
         # pre-norm folded into the weight-streaming GEMV (h normalised once into
         # smem per CTA, overlapping the weight prefetch): used at B=1, where
-        # the CUDA-core GEMV runs; SWB_FUSED_NORM=0/1 forces it off/on
+        # the CUDA-core GEMV runs; SWB_FUSED_NORM=0/1 forces it off/on (Llama)
         mode = os.environ.get("SWB_FUSED_NORM", "auto")
         fused = (B == 1 and cfg.d_model * 2 <= 16384) if mode == "auto" else mode == "1"
+        fused = fused and not r.bloom
         for li, lw in enumerate(w.layers):
             if fused:
                 K.gemv_rmsnorm(self.x, lw.attn_norm, cfg.norm_eps, lw.wqkv, K.EPI_BF16,
                                out=self.qkv)
             else:
-                K.rmsnorm(self.x, lw.attn_norm, cfg.norm_eps, out=self.h)
-                K.linear(self.h, lw.wqkv, K.EPI_BF16, out=self.qkv)
-            # RoPE + KV append of the current token + attention + split-K merge
+                r._norm(self.x, lw.attn_norm, lw.attn_norm_b, out=self.h)
+                K.linear(self.h, lw.wqkv, K.EPI_BF16, out=self.qkv, bias=lw.bqkv)
+            # RoPE (or ALiBi) + KV append of the current token + attention +
+            # split-K merge
             K.attn_decode(self.qkv, kv.k_layer_ptr(li), kv.v_layer_ptr(li), self.tables,
                           self.attn_len, B, r.hq, r.hkv, r.dh, kv.block_size, r.scale,
                           self.max_ctx, r.partition, self.ws, out=self.attn,
-                          positions=self.pos, slots=self.slots, theta=cfg.rope_theta)
-            r._proj_reduce(self.attn, lw.wo, self.x)
+                          positions=self.pos, slots=self.slots, theta=cfg.rope_theta,
+                          alibi=r.alibi)
+            r._proj_reduce(self.attn, lw.wo, self.x, lw.bo)
             if fused:
                 K.gemv_rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, lw.wgu, K.EPI_SWIGLU,
                                out=self.act)
             else:
-                K.rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, out=self.h)
-                K.linear(self.h, lw.wgu, K.EPI_SWIGLU, out=self.act)
-            r._proj_reduce(self.act, lw.wd, self.x)
+                r._norm(self.x, lw.mlp_norm, lw.mlp_norm_b, out=self.h)
+                r._mlp_up(self.h, lw, self.act)
+            r._proj_reduce(self.act, lw.wd, self.x, lw.bd)
         if fused:
             K.gemv_rmsnorm(self.x, w.final_norm, cfg.norm_eps, w.lm_head, K.EPI_F32,
                            out=self.logits)
         else:
-            K.rmsnorm(self.x, w.final_norm, cfg.norm_eps, out=self.h)
+            r._norm(self.x, w.final_norm, w.final_norm_b, out=self.h)
             K.linear(self.h, w.lm_head, K.EPI_F32, out=self.logits)
         K.argmax(self.logits, out=self.next_tok)
         K.decode_advance(self.next_tok, self.cur_tok, self.ctx, self.step, self.out_ring, B)

@@ -48,8 +48,12 @@ def test_validation_errors_map_to_reference_types():
     with pytest.raises(ValidationError):
         _abi.call("swb_gemv_bf16", 16, 16, 16, None, 17, 256, 64, 0, 0)    # M > 16
     with pytest.raises(ValidationError):
-        _abi.call("swb_attn_decode", 16, 8, 16, 16, 16, 4, 16, None, None, 1e4, 1, 8, 8, 64,
-                  16, 1.0, 64, 64, 16, 16, 0)                               # dh != 128
+        _abi.call("swb_attn_decode", 16, 8, 16, 16, 16, 4, 16, None, None, 1e4, None, 1, 8, 8,
+                  64, 16, 1.0, 64, 64, 16, 16, 0)                           # dh != 128
+    with pytest.raises(ValidationError):
+        _abi.call("swb_gemm_bf16_bias", 16, 16, 16, None, 16, 128, 256, 64, 3, 0)  # bias+SwiGLU
+    with pytest.raises(ValidationError):
+        _abi.call("swb_layernorm", 16, None, 16, 16, 16, 4, 30, 1e-5, 0, 0)       # d % 4
     with pytest.raises(ValidationError):
         _abi.call("swb_kv_pool_create", 0, 10, 1, 16, 128, 1, 1, C.byref(C.c_void_p()))
     assert "K=60" in _abi.last_error() or "positive" in _abi.last_error()

@@ -58,9 +58,12 @@ def _run_colocated(cfg, runner, kv, prompt, n_out, return_logits=True):
     return seq, out, torch.stack(logits).cpu()
 
 
-def test_tiny_colocated_vs_oracle():
+@pytest.mark.parametrize("model", ["tiny", "bloom-tiny"])
+def test_tiny_colocated_vs_oracle(model):
+    """C1 (Llama architecture) and the BLOOM architecture of C5 (LayerNorm,
+    ALiBi, biases, GELU, tied head) against the fp32 oracle."""
     from oracle.decoder import OracleDecoder
-    cfg, w, kv, runner = _setup()
+    cfg, w, kv, runner = _setup(model)
     g = torch.Generator().manual_seed(0)
     prompt = torch.randint(0, cfg.vocab, (512,), generator=g).tolist()
     seq, gpu_toks, gpu_logits = _run_colocated(cfg, runner, kv, prompt, 128)

@@ -308,3 +308,101 @@ def test_attn_decode_fused_rope_append(K, H, Hkv):
     assert torch.equal(kp.view(torch.int16), kp2.view(torch.int16))
     assert torch.equal(vp.view(torch.int16), vp2.view(torch.int16))
     assert _rel(fused, ref) < 1e-3
+
+
+@pytest.mark.parametrize("M", [1, 5, 300])
+def test_bias_and_gelu_epilogues(K, M):
+    """Biased linears (BLOOM): bf16 / GELU / residual epilogues with a bias
+    against a torch fp32 reference, through the GEMV (M <= 16) and the
+    tcgen05 GEMM (M > 16)."""
+    N, Kd = 768, 512
+    x = torch.randn(M, Kd, device="cuda").bfloat16()
+    w = (torch.randn(N, Kd, device="cuda") * 0.05).bfloat16()
+    b = torch.randn(N, device="cuda").bfloat16()
+    ref = x.float() @ w.float().t() + b.float()
+    assert _rel(K.linear(x, w, K.EPI_BF16, bias=b), ref) < 1e-2
+    gelu = 0.5 * ref * (1 + torch.tanh(0.7978845608028654 * ref * (1 + 0.044715 * ref * ref)))
+    assert _rel(K.linear(x, w, K.EPI_GELU, bias=b), gelu) < 1e-2
+    r = torch.randn(M, N, device="cuda")
+    res = r.clone()
+    K.linear(x, w, K.EPI_RESID_F32, out=res, resid=res, bias=b)
+    assert _rel(res, r + ref) < 1e-4
+
+
+def test_layernorm(K):
+    d = 1024
+    x = torch.randn(7, d, device="cuda") * 3 + 1
+    w = (1 + 0.1 * torch.randn(d, device="cuda")).bfloat16()
+    b = (0.1 * torch.randn(d, device="cuda")).bfloat16()
+    ref = torch.nn.functional.layer_norm(x, (d,), w.float(), b.float(), 1e-5)
+    assert _rel(K.layernorm(x, w, b, 1e-5), ref) < 1e-2
+    idx = torch.tensor([6, 0], device="cuda", dtype=torch.int32)
+    assert _rel(K.layernorm(x, w, b, 1e-5, rows_index=idx), ref[[6, 0]]) < 1e-2
+    y = x.clone()
+    K.layernorm(y, w, b, 1e-5, out=y, out_f32=True)          # in place, fp32
+    assert _rel(y, ref) < 1e-5
+
+
+def _alibi_ref(q, k, v, slopes, q0=0):
+    # q [S,H,dh] at positions q0.., k/v [T,H,dh] at 0..T-1; causal
+    S, T = q.shape[0], k.shape[0]
+    s = torch.einsum("qhd,khd->hqk", q.float(), k.float()) / math.sqrt(q.shape[-1])
+    s = s + slopes[:, None, None] * torch.arange(T, device=q.device).float()
+    qp = torch.arange(q0, q0 + S, device=q.device)[:, None]
+    kp = torch.arange(T, device=q.device)[None, :]
+    s = s.masked_fill((kp > qp)[None], float("-inf"))
+    return torch.einsum("hqk,khd->qhd", s.softmax(-1), v.float())
+
+
+def test_attn_prefill_alibi(K):
+    from paper_2311_18677_b200.model import alibi_slopes
+    H, dh = 6, 128
+    lens = [1, 130, 300, 64]
+    S = sum(lens)
+    qkv = torch.randn(S, 3 * H * dh, device="cuda").bfloat16()
+    slopes = torch.tensor(alibi_slopes(H), device="cuda")
+    cu = torch.tensor([0] + list(torch.tensor(lens).cumsum(0)), device="cuda", dtype=torch.int32)
+    out = K.attn_prefill(qkv, cu, len(lens), max(lens), H, H, dh, 1 / math.sqrt(dh),
+                         alibi=slopes)
+    off = 0
+    for L in lens:
+        blk = qkv[off:off + L]
+        q, k, v = (blk[:, i * H * dh:(i + 1) * H * dh].view(L, H, dh) for i in range(3))
+        assert _rel(out[off:off + L].view(L, H, dh), _alibi_ref(q, k, v, slopes)) < 2e-2, L
+        off += L
+
+
+def test_attn_decode_alibi_append(K):
+    """ALiBi decode: no rotation, the current token's k/v are appended as is,
+    scores carry slope * (key - query)."""
+    from paper_2311_18677_b200.model import alibi_slopes
+    H, dh, bs, B = 6, 128, 16, 3
+    ctx = [1, 40, 333]
+    nblk, maxb = 200, 32
+    kp = torch.randn(nblk, H, bs, dh, device="cuda").bfloat16()
+    vp = torch.randn(nblk, H, bs, dh, device="cuda").bfloat16()
+    tables = torch.randperm(nblk, device="cuda").int()[:B * maxb].view(B, maxb).contiguous()
+    lens = torch.tensor(ctx, device="cuda", dtype=torch.int32)
+    pos = lens - 1
+    slots = torch.stack([tables[b, int(pos[b]) // bs] * bs + int(pos[b]) % bs
+                         for b in range(B)]).int()
+    qkv = torch.randn(B, 3 * H * dh, device="cuda").bfloat16()
+    slopes = torch.tensor(alibi_slopes(H), device="cuda")
+    part = 128
+    ws = torch.zeros(K.attn_decode_workspace_bytes(B, H, 384, part, dh), dtype=torch.uint8,
+                     device="cuda")
+    out = K.attn_decode(qkv, kp.data_ptr(), vp.data_ptr(), tables, lens, B, H, H, dh, bs,
+                        1 / math.sqrt(dh), 384, part, ws, positions=pos.clone(),
+                        slots=slots, alibi=slopes)
+    for b in range(B):
+        n = ctx[b]
+        p = torch.arange(n, device="cuda")
+        blocks = tables[b, p // bs].long()
+        kk = kp[blocks, :, p % bs]                   # [n, H, dh]
+        vv = vp[blocks, :, p % bs]
+        cur_k = qkv[b, H * dh:2 * H * dh].view(H, dh)
+        cur_v = qkv[b, 2 * H * dh:].view(H, dh)
+        assert torch.equal(kk[-1], cur_k) and torch.equal(vv[-1], cur_v)   # appended as is
+        q = qkv[b, :H * dh].view(1, H, dh)
+        ref = _alibi_ref(q, kk, vv, slopes, q0=n - 1)[0]
+        assert _rel(out[b].view(H, dh), ref) < 2e-2, b

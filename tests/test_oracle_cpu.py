@@ -71,3 +71,55 @@ def test_generate_phase_structure():
     # teacher forcing with the model's own tokens reproduces the free run
     toks2, logits2 = orc.generate([1, 2, 3, 4], 6, forced=toks[:-1])
     assert toks2 == toks and torch.equal(logits, logits2)
+
+
+def _bloom_weights_cpu():
+    from paper_2311_18677_b200.model import ModelConfig, init_weights
+    # BLOOM shapes: d = H * dh, ffn = 4 d
+    cfg = ModelConfig("bloom-t", 2, 768, 6, 6, 128, 3072, 300, arch="bloom", init_std=0.05)
+    return cfg, init_weights(cfg, seed=3, device="cpu")
+
+
+def test_bloom_oracle_matches_transformers_bloom():
+    """The BLOOM restatement (LayerNorms, ALiBi, biases, tanh-GELU, tied
+    head) equals transformers' BloomForCausalLM on the same weights."""
+    from transformers import BloomConfig, BloomForCausalLM
+    from paper_2311_18677_b200.model import logical_layer_fp32
+    cfg, w = _bloom_weights_cpu()
+    orc = OracleDecoder.from_weights(w)
+    hf = BloomForCausalLM(BloomConfig(vocab_size=cfg.vocab, hidden_size=cfg.d_model,
+                                      n_layer=cfg.n_layers, n_head=cfg.n_heads,
+                                      layer_norm_epsilon=cfg.norm_eps, hidden_dropout=0.0,
+                                      attention_dropout=0.0)).eval()
+    H, dh = cfg.n_heads, cfg.head_dim
+    sd = {"transformer.word_embeddings.weight": w.embed.float(),
+          "transformer.word_embeddings_layernorm.weight": w.emb_norm.float(),
+          "transformer.word_embeddings_layernorm.bias": w.emb_norm_b.float(),
+          "transformer.ln_f.weight": w.final_norm.float(),
+          "transformer.ln_f.bias": w.final_norm_b.float(),
+          "lm_head.weight": w.embed.float()}
+    for i in range(cfg.n_layers):
+        L = logical_layer_fp32(w, i)
+        p = f"transformer.h.{i}."
+        # BLOOM's fused qkv is head-major [H][q|k|v][dh]
+        wqkv = torch.stack([L["wq"].view(H, dh, -1), L["wk"].view(H, dh, -1),
+                            L["wv"].view(H, dh, -1)], 1).reshape(3 * H * dh, -1)
+        bqkv = torch.stack([L["bq"].view(H, dh), L["bk"].view(H, dh), L["bv"].view(H, dh)],
+                           1).reshape(-1)
+        sd.update({p + "input_layernorm.weight": L["ln1_w"], p + "input_layernorm.bias": L["ln1_b"],
+                   p + "self_attention.query_key_value.weight": wqkv,
+                   p + "self_attention.query_key_value.bias": bqkv,
+                   p + "self_attention.dense.weight": L["wo"],
+                   p + "self_attention.dense.bias": L["bo"],
+                   p + "post_attention_layernorm.weight": L["ln2_w"],
+                   p + "post_attention_layernorm.bias": L["ln2_b"],
+                   p + "mlp.dense_h_to_4h.weight": L["w_up"], p + "mlp.dense_h_to_4h.bias": L["b_up"],
+                   p + "mlp.dense_4h_to_h.weight": L["wd"], p + "mlp.dense_4h_to_h.bias": L["bd"]})
+    missing, unexpected = hf.load_state_dict(sd, strict=False)
+    assert not unexpected and all("lm_head" in m for m in missing), (missing, unexpected)
+    hf.tie_weights()
+    prompt = list(range(7, 47))
+    toks, logits = orc.generate(prompt, 4)
+    with torch.no_grad():
+        ref = hf(torch.tensor([prompt + toks[:3]])).logits[0, len(prompt) - 1:].float()
+    assert (logits - ref).abs().max().item() < 2e-4 * max(1.0, ref.abs().max().item())

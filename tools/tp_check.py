@@ -119,23 +119,39 @@ def main():
     # gather shards and rebuild the logical TP=1 model on rank 0
     hq, hkv, dh = cfg.n_heads // world, cfg.n_kv_heads // world, cfg.head_dim
     layers = []
+    names = ("wqkv", "wo", "wgu", "wd") + (("bqkv", "bup") if cfg.is_bloom else ())
+
+    def unshard_qkv(parts):
+        q = torch.cat([p[:hq * dh] for p in parts])
+        k = torch.cat([p[hq * dh:(hq + hkv) * dh] for p in parts])
+        v = torch.cat([p[(hq + hkv) * dh:] for p in parts])
+        return torch.cat([q, k, v]).contiguous()
     for lw in w.layers:
         parts = {}
-        for name in ("wqkv", "wo", "wgu", "wd"):
+        for name in names:
             t = getattr(lw, name).contiguous()
             lst = [torch.empty_like(t) for _ in range(world)]
             dist.all_gather(lst, t)
             parts[name] = lst
         if rank == 0:
-            q = torch.cat([p[:hq * dh] for p in parts["wqkv"]])
-            k = torch.cat([p[hq * dh:(hq + hkv) * dh] for p in parts["wqkv"]])
-            v = torch.cat([p[(hq + hkv) * dh:] for p in parts["wqkv"]])
-            layers.append(LayerWeights(lw.attn_norm, torch.cat([q, k, v]).contiguous(),
-                                       torch.cat(parts["wo"], 1).contiguous(), lw.mlp_norm,
-                                       torch.cat(parts["wgu"]).contiguous(),
-                                       torch.cat(parts["wd"], 1).contiguous()))
+            full_lw = LayerWeights(lw.attn_norm, unshard_qkv(parts["wqkv"]),
+                                   torch.cat(parts["wo"], 1).contiguous(), lw.mlp_norm,
+                                   torch.cat(parts["wgu"]).contiguous(),
+                                   torch.cat(parts["wd"], 1).contiguous())
+            if cfg.is_bloom:
+                full_lw.attn_norm_b, full_lw.mlp_norm_b = lw.attn_norm_b, lw.mlp_norm_b
+                full_lw.bqkv = unshard_qkv(parts["bqkv"])
+                full_lw.bup = torch.cat(parts["bup"]).contiguous()
+                full_lw.bo, full_lw.bd = lw.bo, lw.bd
+            layers.append(full_lw)
     if rank == 0:
-        full = Weights(cfg, 1, 0, w.embed, w.lm_head, w.final_norm, layers)
+        extra = {}
+        if cfg.is_bloom:
+            from paper_2311_18677_b200.model import alibi_slopes
+            extra = dict(final_norm_b=w.final_norm_b, emb_norm=w.emb_norm,
+                         emb_norm_b=w.emb_norm_b,
+                         alibi=torch.tensor(alibi_slopes(cfg.n_heads), device="cuda"))
+        full = Weights(cfg, 1, 0, w.embed, w.lm_head, w.final_norm, layers, **extra)
         kv1 = KVCacheManager(cfg.n_layers, 1024, cfg.n_kv_heads, cfg.head_dim, 16, 4,
                              (a.prompt + 128) // 16 + 2)
         toks_1, logits_1 = run(ModelRunner(full, kv1), kv1, prompt, a.out)

@@ -372,10 +372,9 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     float c[NB][4];
 #pragma unroll
     for (int h = 0; h < NB; ++h) c[h][0] = c[h][1] = c[h][2] = c[h][3] = 0.f;
-    for (int kc = 0; kc < nk; ++kc, ++it) {
-      const int s = it % TM_STAGES;
-      // B fragments (x^T): batch row = g (+8 for the second MMA), k = 2t.., 8+2t..
-      uint32_t bfr[NB][4][2];
+    // B fragments (x^T): batch row = g (+8 for the second MMA), k = 2t.., 8+2t..
+    // loaded one K-chunk ahead so their L1/L2 latency hides behind the MMAs
+    auto load_b = [&](int kc, uint32_t (&bf)[NB][4][2]) {
       const int kbase = kc * TM_KC + warp * 64;
 #pragma unroll
       for (int h = 0; h < NB; ++h) {
@@ -385,13 +384,28 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
           const int k0 = kbase + ks * 16 + 2 * t;
           uint32_t v0 = 0, v1 = 0;
           if (m < M && k0 < K) {
-            v0 = *reinterpret_cast<const uint32_t*>(x + (size_t)m * K + k0);
-            if (k0 + 8 < K) v1 = *reinterpret_cast<const uint32_t*>(x + (size_t)m * K + k0 + 8);
+            v0 = __ldg(reinterpret_cast<const unsigned int*>(x + (size_t)m * K + k0));
+            if (k0 + 8 < K)
+              v1 = __ldg(reinterpret_cast<const unsigned int*>(x + (size_t)m * K + k0 + 8));
           }
-          bfr[h][ks][0] = v0;
-          bfr[h][ks][1] = v1;
+          bf[h][ks][0] = v0;
+          bf[h][ks][1] = v1;
         }
       }
+    };
+    uint32_t bnext[NB][4][2];
+    load_b(0, bnext);
+    for (int kc = 0; kc < nk; ++kc, ++it) {
+      const int s = it % TM_STAGES;
+      uint32_t bfr[NB][4][2];
+#pragma unroll
+      for (int h = 0; h < NB; ++h)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          bfr[h][ks][0] = bnext[h][ks][0];
+          bfr[h][ks][1] = bnext[h][ks][1];
+        }
+      if (kc + 1 < nk) load_b(kc + 1, bnext);
       mbar_wait(&full[s], (it / TM_STAGES) & 1);
       const uint32_t box = smem_u32(smem + s * TM_STAGE_BYTES + warp * TM_BOX_BYTES);
 #pragma unroll
@@ -490,6 +504,18 @@ static bool gemv_mma_enabled() {
   return on;
 }
 
+int dispatch_gemv_tc(const void* x, const void* w, void* out, const float* resid,
+                     const __nv_bfloat16* bias, int M, int N, int K, int epi, cudaStream_t s);
+
+// SWB_GEMV_TC=0 keeps batched decode on the mma.sync kernel (A/B)
+static bool gemv_tc_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SWB_GEMV_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <bool NORM>
 static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, const void* w,
                          void* out, const void* resid, const void* bias_, int M, int N, int K,
@@ -499,6 +525,12 @@ static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, cons
   auto ws = reinterpret_cast<const __nv_bfloat16*>(w);
   auto rs = reinterpret_cast<const float*>(resid);
   cudaStream_t s = (cudaStream_t)stream;
+  // tcgen05 GEMV for batched decode; the mma.sync kernel stays ahead on
+  // small matrices at small batch (measured crossover, tools/gemv_bench.py)
+  const double wbytes = 2.0 * N * K;
+  const bool small = (M <= 4 && wbytes < 160e6) || (M <= 8 && wbytes < 120e6);
+  if (!NORM && M >= 2 && gemv_tc_enabled() && (M > 16 || !small || !gemv_mma_enabled()))
+    return dispatch_gemv_tc(x, w, out, rs, bias, M, N, K, epilogue, s);
   if (!NORM && M >= 2 && gemv_mma_enabled()) {
     auto xb = reinterpret_cast<const __nv_bfloat16*>(x);
     if (M <= 8) return launch_gemv_mma<1>(xb, w, out, rs, bias, M, N, K, epilogue, s);
@@ -518,7 +550,8 @@ using namespace swb;
 static int check_gemv_args(const char* fn, const void* x, const void* w, void* out,
                            const void* resid, int M, int N, int K, int epilogue) {
   SWB_REQUIRE(x && w && out, "%s: null pointer", fn);
-  SWB_REQUIRE(M >= 1 && M <= 16, "%s: M=%d outside 1..16", fn, M);
+  SWB_REQUIRE(M >= 1 && M <= (gemv_tc_enabled() ? 32 : 16), "%s: M=%d outside 1..%d", fn, M,
+              gemv_tc_enabled() ? 32 : 16);
   SWB_REQUIRE(N > 0 && K > 0 && K % 8 == 0, "%s: bad shape N=%d K=%d", fn, N, K);
   SWB_REQUIRE(epilogue >= SWB_EPI_BF16 && epilogue <= SWB_EPI_GELU, "%s: bad epilogue %d",
               fn, epilogue);

@@ -56,62 +56,96 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
-__global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a) {
+__device__ __forceinline__ void tp_handshake(const TpArgs& a, int c, uint32_t e) {
+  // thread 0 of CTA c: publish epoch e to every peer, wait for theirs
+  __threadfence_system();
+  for (int p = 0; p < a.world; ++p)
+    if (p != a.rank)
+      st_release_sys(a.peer_flags[p] + ((size_t)a.slot * TP_MAXW + a.rank) * TP_MAXC + c, e);
+  const long long t0 = clock64();
+  for (int p = 0; p < a.world; ++p) {
+    if (p == a.rank) continue;
+    const uint32_t* f = a.my_flags + ((size_t)a.slot * TP_MAXW + p) * TP_MAXC + c;
+    int spins = 0;
+    while ((int)(ld_acquire_sys(f) - e) < 0) {
+      if (++spins > 64) __nanosleep(64);
+      // a peer that never arrives (crashed rank) must not wedge the GPU
+      if (clock64() - t0 > 40000000000ll) __trap();
+    }
+  }
+}
+
+// Rank-ordered sum of float4 element i over all ranks' slots.
+__device__ __forceinline__ float4 tp_sum4(const TpArgs& a, long long i) {
+  float4 v[TP_MAXW];
+#pragma unroll
+  for (int p = 0; p < TP_MAXW; ++p)
+    if (p < a.world) v[p] = __ldcg(reinterpret_cast<const float4*>(a.peer_slot[p]) + i);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < TP_MAXW; ++p)
+    if (p < a.world) {
+      s.x += v[p].x; s.y += v[p].y; s.z += v[p].z; s.w += v[p].w;
+    }
+  return s;
+}
+
+// one_shot: every rank reads all ranks' slots and sums the whole vector
+// (one handshake; (W-1)*n floats in over NVLink) — small / 2-rank messages.
+// two_shot: reduce-scatter then all-gather through the slots (two
+// handshakes; 2*(W-1)/W*n in) — large messages on W > 2.
+__global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a, int two_shot) {
   pdl_wait();  // the producer GEMM/GEMV must be complete before we publish
   const int c = blockIdx.x;
-  __shared__ uint32_t s_epoch;
+  uint32_t* ctr = a.my_ctr + a.slot * TP_MAXC + c;
+  uint32_t e = 0;
   if (threadIdx.x == 0) {
-    uint32_t* ctr = a.my_ctr + a.slot * TP_MAXC + c;
-    const uint32_t e = *ctr + 1;
-    __threadfence_system();
-    for (int p = 0; p < a.world; ++p)
-      if (p != a.rank)
-        st_release_sys(a.peer_flags[p] + ((size_t)a.slot * TP_MAXW + a.rank) * TP_MAXC + c, e);
-    const long long t0 = clock64();
-    for (int p = 0; p < a.world; ++p) {
-      if (p == a.rank) continue;
-      const uint32_t* f = a.my_flags + ((size_t)a.slot * TP_MAXW + p) * TP_MAXC + c;
-      int spins = 0;
-      while ((int)(ld_acquire_sys(f) - e) < 0) {
-        if (++spins > 64) __nanosleep(64);
-        // a peer that never arrives (crashed rank) must not wedge the GPU
-        if (clock64() - t0 > 40000000000ll) __trap();
-      }
-    }
-    *ctr = e;
-    s_epoch = e;
+    e = *ctr + 1;
+    tp_handshake(a, c, e);
   }
   __syncthreads();
-  // chunk c of n (in float4 units; n % 4 == 0 checked on the host)
   const long long n4 = a.n >> 2;
-  const long long per = (n4 + gridDim.x - 1) / gridDim.x;
-  const long long lo = (long long)c * per, hi = min(n4, lo + per);
   float4* out4 = reinterpret_cast<float4*>(a.out);
-  for (long long i = lo + threadIdx.x; i < hi; i += 2 * TP_THREADS) {
-    const long long j = i + TP_THREADS;
-    float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
-    float4 v0[TP_MAXW], v1[TP_MAXW];
-#pragma unroll
-    for (int p = 0; p < TP_MAXW; ++p) {
-      if (p < a.world) {
-        const float4* src = reinterpret_cast<const float4*>(a.peer_slot[p]);
-        v0[p] = __ldcg(src + i);
-        if (j < hi) v1[p] = __ldcg(src + j);
-      }
+  if (!two_shot) {
+    const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+    const long long lo = (long long)c * per, hi = min(n4, lo + per);
+    for (long long i = lo + threadIdx.x; i < hi; i += 2 * TP_THREADS) {
+      const long long j = i + TP_THREADS;
+      const float4 s0 = tp_sum4(a, i);
+      if (j < hi) out4[j] = tp_sum4(a, j);
+      out4[i] = s0;
     }
-#pragma unroll
-    for (int p = 0; p < TP_MAXW; ++p) {
-      if (p < a.world) {
-        s0.x += v0[p].x; s0.y += v0[p].y; s0.z += v0[p].z; s0.w += v0[p].w;
-        if (j < hi) {
-          s1.x += v1[p].x; s1.y += v1[p].y; s1.z += v1[p].z; s1.w += v1[p].w;
-        }
-      }
-    }
-    out4[i] = s0;
-    if (j < hi) out4[j] = s1;
+    if (threadIdx.x == 0) *ctr = e;
+    return;
   }
-  (void)s_epoch;
+  // ---- reduce-scatter: this rank owns part `rank` of W parts
+  const long long pl = (n4 + a.world - 1) / a.world;
+  const long long per = (pl + gridDim.x - 1) / gridDim.x;
+  const long long c_lo = (long long)c * per, c_hi = min(pl, c_lo + per);
+  float4* mine = reinterpret_cast<float4*>(const_cast<float*>(a.peer_slot[a.rank]));
+  {
+    const long long base = (long long)a.rank * pl;
+    for (long long i = c_lo + threadIdx.x; i < c_hi && base + i < n4; i += TP_THREADS) {
+      const float4 s = tp_sum4(a, base + i);
+      out4[base + i] = s;
+      mine[base + i] = s;          // peers gather the reduced part from here
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    e += 1;
+    tp_handshake(a, c, e);
+    *ctr = e;
+  }
+  __syncthreads();
+  // ---- all-gather: the other parts, reduced, from their owners
+  for (int p = 0; p < a.world; ++p) {
+    if (p == a.rank) continue;
+    const float4* src = reinterpret_cast<const float4*>(a.peer_slot[p]);
+    const long long base = (long long)p * pl;
+    for (long long i = c_lo + threadIdx.x; i < c_hi && base + i < n4; i += TP_THREADS)
+      out4[base + i] = __ldcg(src + base + i);
+  }
 }
 
 }  // namespace swb
@@ -227,8 +261,10 @@ extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t
   a.slot = slot;
   // ~16 KB of output per CTA, at most TP_MAXC CTAs (one wave)
   const long long ctas = std::min<long long>(TP_MAXC, std::max<long long>(1, (long long)n / 4096));
+  // two-shot once the (W-1)x one-shot traffic outweighs a second handshake
+  const int two_shot = c->world > 2 && n >= (size_t)(1 << 18);
   const cudaError_t le = launch(tp_allreduce_kernel, dim3((unsigned)ctas), dim3(TP_THREADS), 0,
-                                (cudaStream_t)stream, a);
+                                (cudaStream_t)stream, a, two_shot);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch tp_allreduce_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("tp_allreduce_kernel");

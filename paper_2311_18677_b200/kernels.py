@@ -19,7 +19,8 @@ __all__ = ["gemm", "gemv", "gemv_rmsnorm", "linear", "embed", "rmsnorm", "layern
            "decode_advance", "slots_from_table", "kv_signal", "stream_wait_flag",
            "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "EPI_GELU", "GEMV_MAX_ROWS"]
 
-GEMV_MAX_ROWS = 16
+# rows handled by the weight-streaming GEMVs (the tcgen05 GEMV takes up to 32)
+GEMV_MAX_ROWS = 16 if os.environ.get("SWB_GEMV_TC", "1") == "0" else 32
 
 
 def _stream() -> int:

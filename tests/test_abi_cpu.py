@@ -46,7 +46,7 @@ def test_validation_errors_map_to_reference_types():
     with pytest.raises(ValidationError):
         _abi.call("swb_gemm_bf16", 16, 16, 16, None, 128, 256, 60, 0, 0)   # K % 8
     with pytest.raises(ValidationError):
-        _abi.call("swb_gemv_bf16", 16, 16, 16, None, 17, 256, 64, 0, 0)    # M > 16
+        _abi.call("swb_gemv_bf16", 16, 16, 16, None, 33, 256, 64, 0, 0)    # M > 32
     with pytest.raises(ValidationError):
         _abi.call("swb_attn_decode", 16, 8, 16, 16, 16, 4, 16, None, None, 1e4, None, 1, 8, 8,
                   64, 16, 1.0, 64, 64, 16, 16, 0)                           # dh != 128

@@ -51,8 +51,9 @@ def test_gemm_resid_and_swiglu(K):
     assert _rel(out_sw, ref_sw) < 1e-2
 
 
-@pytest.mark.parametrize("M", [1, 2, 3, 8, 16])
-@pytest.mark.parametrize("N,K_", [(4096, 4096), (768, 256), (1000, 11008)])
+@pytest.mark.parametrize("M", [1, 2, 3, 8, 16, 24, 32])
+@pytest.mark.parametrize("N,K_", [(4096, 4096), (768, 256), (1000, 11008), (256, 14336),
+                                  (250, 64)])
 def test_gemv(K, M, N, K_):
     x = torch.randn(M, K_, device="cuda").bfloat16()
     w = torch.randn(N, K_, device="cuda").bfloat16()
@@ -65,8 +66,9 @@ def test_gemv(K, M, N, K_):
     assert _rel(out, res + ref) < 1e-4
 
 
-def test_gemv_swiglu(K):
-    M, N, K_ = 4, 2048, 1024
+@pytest.mark.parametrize("M", [1, 4, 20])
+def test_gemv_swiglu(K, M):
+    N, K_ = 2048, 1024
     x = torch.randn(M, K_, device="cuda").bfloat16()
     w = torch.randn(N, K_, device="cuda").bfloat16()
     acc = x.float() @ w.float().t()
@@ -74,6 +76,17 @@ def test_gemv_swiglu(K):
     u = acc.view(M, N // 256, 2, 128)[:, :, 1, :].reshape(M, N // 2)
     ref = torch.nn.functional.silu(g) * u
     assert _rel(K.gemv(x, w, K.EPI_SWIGLU), ref) < 1e-2
+
+
+@pytest.mark.parametrize("M", [2, 8, 32])
+def test_gemv_batched_deterministic(K, M):
+    """The split-K tcgen05 GEMV reduces cluster partials in fixed rank order:
+    repeated launches are bit-identical."""
+    x = torch.randn(M, 11008, device="cuda").bfloat16()
+    w = torch.randn(4096, 11008, device="cuda").bfloat16()
+    a = K.gemv(x, w, K.EPI_F32)
+    for _ in range(3):
+        assert torch.equal(K.gemv(x, w, K.EPI_F32), a)
 
 
 def test_embed_rmsnorm_argmax(K):

@@ -95,7 +95,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
     cfg = get_config(a.model)
     w = init_weights(cfg, seed=0, tp=world, rank=rank)
-    kv = KVCacheManager(cfg.n_layers, 1024, cfg.n_kv_heads // world, cfg.head_dim, 16, 4,
+    kv = KVCacheManager(cfg.n_layers, 1024, cfg.n_kv_heads // world, cfg.head_dim, 16, max(4, a.batch),
                         (a.prompt + 128) // 16 + 2)
     runner = ModelRunner(w, kv, tp_group=dist.group.WORLD)
     if a.no_ar:

@@ -187,6 +187,24 @@ int swb_attn_decode(const void* qkv, int row_stride, void* k_layer,
                     int block_size, float scale, int max_ctx, int partition,
                     void* workspace, void* out, uintptr_t stream);
 
+/* Decode-graph form of swb_attn_decode: ctx[b] = tokens already cached for
+ * sequence b; the current token (q/k/v in qkv row b) is at position ctx[b],
+ * rotated there (RoPE; or ALiBi when alibi_slopes is given), appended at the
+ * slot block_tables[b][ctx/bs]*bs + ctx%bs, and attends over ctx[b]+1 tokens.
+ * ctx, block_tables and the cached pages are read before the kernel's
+ * programmatic-dependency wait, so they must be produced by work that
+ * completed before the PRECEDING kernel on the stream started (in the decode
+ * graph: the previous replay / the host); only qkv may come from the
+ * preceding kernel.  Same workspace contract as swb_attn_decode.
+ * Replaces the same reference lookups as swb_attn_decode. */
+int swb_attn_decode_step(const void* qkv, int row_stride, void* k_layer,
+                         void* v_layer, const int32_t* block_tables,
+                         int max_blocks, const int32_t* ctx, float theta,
+                         const float* alibi_slopes, int B, int H, int Hkv,
+                         int dh, int block_size, float scale, int max_ctx,
+                         int partition, void* workspace, void* out,
+                         uintptr_t stream);
+
 /* --------------------------------------------- decode-step bookkeeping
  * Graph-resident per-step state update so the decode loop needs no host
  * round trip (Machine.complete_iteration, machine.py:247-275):

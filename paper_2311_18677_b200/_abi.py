@@ -62,6 +62,8 @@ SIGNATURES = {
     "swb_attn_decode_workspace": [_I, _I, _I, _I, _I],
     "swb_attn_decode": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _F, _P, _I, _I, _I, _I, _I, _F,
                         _I, _I, _P, _P, _ST],
+    "swb_attn_decode_step": [_P, _I, _P, _P, _P, _I, _P, _F, _P, _I, _I, _I, _I, _I, _F, _I,
+                             _I, _P, _P, _ST],
     "swb_decode_prepare": [_P, _P, _I, _I, _I, _P, _P, _P, _ST],
     "swb_decode_advance": [_P, _P, _P, _P, _P, _I, _I, _ST],
     "swb_slots_from_table": [_P, _I, _I, _I, _P, _ST],
@@ -121,7 +123,8 @@ LAUNCH_MULT = {
     "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemm_bf16_bias": 1, "swb_gemv_bf16_bias": 1,
     "swb_layernorm": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
     "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
-    "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_decode_prepare": 1,
+    "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1,
+    "swb_decode_prepare": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
     "swb_block_free": 1, "swb_tp_allreduce_f32": 1,
 }

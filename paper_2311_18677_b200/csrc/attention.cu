@@ -262,21 +262,27 @@ __global__ void __launch_bounds__(PA_THREADS)
 // ============================================================ decode
 constexpr int DA_D = 128;
 constexpr int DA_MAXG = 8;
-constexpr int DA_WARPS = 8;
+constexpr int DA_MAXPART = 128;
 
 // Decode attention, one kernel per layer:
-//   grid (B, Hkv, NP), DA_WARPS*32 threads; CTA (b, kh, p) covers context tokens
-//   [p*part, (p+1)*part) of sequence b for the G query heads of kv head kh.
-// * If `pos` is given, the current token's q/k are rotated here (RoPE) and its
-//   k/v are written into the pool slot slots[b] by the CTA whose partition
-//   holds position pos[b] (the token attends to itself from registers/smem,
-//   not from the freshly written global copy).
-// * All other K/V rows of the partition are gathered through the block table
-//   with cp.async issued up front, so the whole partition is in flight at once.
-// * Scores: half-warp per token with shuffle-reduced dot products against the
-//   G query heads; softmax with warp shuffles; P.V with lane-owned dims.
+//   grid (NP, Hkv, B), 128 threads; CTA (p, kh, b) covers context tokens
+//   [p*part, (p+1)*part) of sequence b for the G = H/Hkv query heads of kv
+//   head kh (a GQA group shares one pass over its K/V pages).
+// * STEP (the decode graph): ctx_lens[b] = tokens already cached; the current
+//   token sits at position ctx_lens[b], its slot comes from the block table.
+//   Tables, ctx and the cached pages are produced by earlier launches, so the
+//   page gather is issued BEFORE griddepcontrol.wait and overlaps the QKV
+//   projection's tail; only q and the current k/v wait for it.
+//   !STEP: ctx_lens[b] = attention length including the current token, which
+//   (when pos/slots are given) sits at pos[b] and is appended at slots[b].
+// * Pages arrive as 4 KB (block, head) bulk copies; K and V have separate
+//   mbarriers so the scores run while V is still in flight.
+// * Scores: half-warp per token (4 tokens in flight), shuffle-reduced dots
+//   against the G query heads; softmax max/exp-sum per head by one warp; P.V
+//   with lane-owned dims; the current token's k/v (RoPE'd here) are patched
+//   into the staged pages from shared memory, never re-read from global.
 // * Split-K merge fused: every CTA publishes (o, m, l); the last CTA of a
-//   (b, kh) group (atomic ticket) merges all partitions and writes bf16 out.
+//   (b, kh) group (atomic ticket) merges all partitions in fixed order.
 __device__ __forceinline__ void rope4(float* a, float* b, int i0, float pos, float l2t) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -289,85 +295,93 @@ __device__ __forceinline__ void rope4(float* a, float* b, int i0, float pos, flo
   }
 }
 
-__global__ void __launch_bounds__(DA_WARPS * 32, 2)
+template <bool STEP, int NW>
+__global__ void __launch_bounds__(NW * 32)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                        __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
                        const int32_t* __restrict__ tables, int max_blocks,
                        const int32_t* __restrict__ ctx_lens, const int32_t* __restrict__ pos,
                        const int32_t* __restrict__ slots, float log2_theta,
-                       const float* __restrict__ alibi, int H, int Hkv,
-                       int bs, float scale_log2, int part, float* __restrict__ ws,
-                       int* __restrict__ tickets, __nv_bfloat16* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
+                       const float* __restrict__ alibi, int H, int Hkv, int bs,
+                       float scale_log2, int part, float* __restrict__ ws,
+                       int* __restrict__ tickets, __nv_bfloat16* __restrict__ out, int trig) {
   extern __shared__ __align__(16) uint8_t dsm_raw[];
-  const int b = blockIdx.x, kh = blockIdx.y, p = blockIdx.z;
-  const int NP = gridDim.z;
+  const int p = blockIdx.x, kh = blockIdx.y, b = blockIdx.z;
+  const int NP = gridDim.x;
   const int G = H / Hkv;
-  const int ctx = ctx_lens[b];
-  const int t0 = p * part;
-  const int t1 = min(ctx, t0 + part);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto wsp = [&](int gh, int pp) {
     return ws + (((size_t)b * H + gh) * NP + pp) * (DA_D + 2);
   };
+  __shared__ uint64_t bars[2];                       // K pages, V pages
   __shared__ int s_last;
+  __shared__ __align__(16) __nv_bfloat16 scur[2][DA_D];  // current token's k (rotated), v
   __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(dsm_raw);      // [part][128]
   __nv_bfloat16* sv = sk + (size_t)part * DA_D;                        // [part][128]
   float* sq = reinterpret_cast<float*>(sv + (size_t)part * DA_D);      // [G][128]
   float* ss = sq + G * DA_D;                                           // [G][part]
   float* sacc = ss + G * part;                                         // [WARPS][G][128]
-  float* sstat = sacc + DA_WARPS * G * DA_D;                           // [G][2]
-  __shared__ uint64_t kv_bar_s;
-  uint64_t* kv_bar = &kv_bar_s;
+  float* sstat = sacc + NW * G * DA_D;                           // [G][2]
   if (threadIdx.x == 0) {
-    mbar_init(kv_bar, 1);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
     fence_barrier_init();
   }
   __syncthreads();
 
-  if (t0 >= t1) {
-    if (threadIdx.x < G) {
-      float* w = wsp(kh * G + threadIdx.x, p);
-      w[DA_D] = -INFINITY;
-      w[DA_D + 1] = 0.f;
-    }
+  const int32_t* trow = tables + (size_t)b * max_blocks;
+  const int lbs = __ffs(bs) - 1;
+  int L, cur;  // attention length; current token position (-1: nothing appended)
+  if constexpr (STEP) {
+    const int c = __ldg(ctx_lens + b);
+    L = c + 1;
+    cur = c;
   } else {
-    const int ntok = t1 - t0;
-    const int cur = pos ? pos[b] : -1;            // current token position
-    const int qpos = pos ? cur : ctx - 1;         // query position (ALiBi)
-    const bool own_cur = cur >= t0 && cur < t1;
-    // ---- gather the partition: one bulk copy per (block, kv head) tile —
-    // 16 tokens x 256 B contiguous in the pool — issued by warp 0's lanes in
-    // parallel (per-thread 16-byte cp.async was issue-bound here)
-    const int32_t* trow = tables + (size_t)b * max_blocks;
-    const int lbs = __ffs(bs) - 1;
-    if (warp == 0) {
-      const int nblk = (ntok + bs - 1) >> lbs;
-      const uint32_t tile = (uint32_t)bs * DA_D * 2;
-      if (lane == 0) mbar_arrive_expect_tx(kv_bar, 2 * tile * nblk);
-      __syncwarp();
-      for (int j = lane; j < nblk; j += 32) {
-        const int blk = __ldg(trow + (t0 >> lbs) + j);
-        const size_t g = ((size_t)blk * Hkv + kh) * bs * DA_D;
-        bulk_g2s(sk + (size_t)j * bs * DA_D, kpool + g, tile, kv_bar);
-        bulk_g2s(sv + (size_t)j * bs * DA_D, vpool + g, tile, kv_bar);
-      }
+    pdl_wait();
+    L = ctx_lens[b];
+    cur = pos ? pos[b] : -1;
+  }
+  const int t0 = p * part;
+  const int t1 = min(L, t0 + part);
+  const int ntok = t1 - t0;
+  const bool own_cur = cur >= t0 && cur < t1;
+  if (warp == 0 && ntok > 0) {
+    // ---- gather the cached pages of the partition (4 KB per (block, head))
+    const int cend = cur >= 0 ? min(t1, cur) : t1;
+    const int nblk = (max(0, cend - t0) + bs - 1) >> lbs;
+    const uint32_t tile = (uint32_t)bs * DA_D * 2;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[0], tile * nblk);
+      mbar_arrive_expect_tx(&bars[1], tile * nblk);
     }
-    // ---- q of the group (rotated), scaled by softmax scale * log2(e)
+    __syncwarp();
+    for (int j = lane; j < nblk; j += 32) {
+      const int blk = __ldg(trow + (t0 >> lbs) + j);
+      bulk_g2s(sk + (size_t)j * bs * DA_D, kpool + ((size_t)blk * Hkv + kh) * bs * DA_D, tile,
+               &bars[0]);
+    }
+    for (int j = lane; j < nblk; j += 32) {
+      const int blk = __ldg(trow + (t0 >> lbs) + j);
+      bulk_g2s(sv + (size_t)j * bs * DA_D, vpool + ((size_t)blk * Hkv + kh) * bs * DA_D, tile,
+               &bars[1]);
+    }
+  }
+  if constexpr (STEP) pdl_wait();   // q / current k,v come from the QKV projection
+
+  if (ntok > 0) {
+    const int qpos = cur >= 0 ? cur : L - 1;    // query position (ALiBi)
     const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
     const float fpos = (float)cur;
-    for (int i = threadIdx.x; i < G * (DA_D / 8); i += blockDim.x) {
-      // 16 groups of 4 rotary pairs (d, d+64) per head
+    // ---- q of the group (rotated), scaled by softmax scale * log2(e)
+    for (int i = threadIdx.x; i < G * (DA_D / 8); i += (NW * 32)) {
       const int gi = i / (DA_D / 8), i0 = (i % (DA_D / 8)) * 4;
       const __nv_bfloat16* hp = qrow + (kh * G + gi) * DA_D;
-      float lo[4], hi[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        lo[j] = __bfloat162float(hp[i0 + j]);
-        hi[j] = __bfloat162float(hp[64 + i0 + j]);
-      }
-      if (pos && !alibi) {
+      const uint2 ql = *reinterpret_cast<const uint2*>(hp + i0);
+      const uint2 qh = *reinterpret_cast<const uint2*>(hp + 64 + i0);
+      const float2 l0 = bf2_to_f2(ql.x), l1 = bf2_to_f2(ql.y);
+      const float2 h0 = bf2_to_f2(qh.x), h1 = bf2_to_f2(qh.y);
+      float lo[4] = {l0.x, l0.y, l1.x, l1.y}, hi[4] = {h0.x, h0.y, h1.x, h1.y};
+      if (cur >= 0 && !alibi) {
         rope4(lo, hi, i0, fpos, log2_theta);
         // match the two-kernel path: rotated q is rounded to bf16
 #pragma unroll
@@ -382,52 +396,53 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
         sq[gi * DA_D + 64 + i0 + j] = hi[j] * scale_log2;
       }
     }
-    // ---- current token: rotate k, write k/v to the pool, then (after the
-    // gather landed) patch it into the smem tile
-    mbar_wait(kv_bar, 0);
+    // ---- current token: rotate k, append k/v to the pool, stage in smem
     if (own_cur && threadIdx.x < 16) {
       const int i0 = threadIdx.x * 4;           // 16 threads x 4 pairs = 64 pairs
       const __nv_bfloat16* kp = qrow + (H + kh) * DA_D;
       const __nv_bfloat16* vp = qrow + (H + Hkv + kh) * DA_D;
-      float lo[4], hi[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        lo[j] = __bfloat162float(kp[i0 + j]);
-        hi[j] = __bfloat162float(kp[64 + i0 + j]);
-      }
+      const uint2 kl = *reinterpret_cast<const uint2*>(kp + i0);
+      const uint2 khi = *reinterpret_cast<const uint2*>(kp + 64 + i0);
+      const float2 a0 = bf2_to_f2(kl.x), a1 = bf2_to_f2(kl.y);
+      const float2 c0 = bf2_to_f2(khi.x), c1 = bf2_to_f2(khi.y);
+      float lo[4] = {a0.x, a0.y, a1.x, a1.y}, hi[4] = {c0.x, c0.y, c1.x, c1.y};
       if (!alibi) rope4(lo, hi, i0, fpos, log2_theta);
-      const int slot = slots[b];
+      const int slot = STEP ? __ldg(trow + (cur >> lbs)) * bs + (cur & (bs - 1)) : slots[b];
       const size_t g = (((size_t)(slot >> lbs) * Hkv + kh) * bs + (slot & (bs - 1))) * DA_D;
-      const int tt = cur - t0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const __nv_bfloat16 kl = __float2bfloat16(lo[j]), khv = __float2bfloat16(hi[j]);
-        kpool[g + i0 + j] = kl;
-        kpool[g + 64 + i0 + j] = khv;
-        sk[tt * DA_D + i0 + j] = kl;
-        sk[tt * DA_D + 64 + i0 + j] = khv;
-        vpool[g + i0 + j] = vp[i0 + j];
-        vpool[g + 64 + i0 + j] = vp[64 + i0 + j];
-        sv[tt * DA_D + i0 + j] = vp[i0 + j];
-        sv[tt * DA_D + 64 + i0 + j] = vp[64 + i0 + j];
-      }
+      const uint2 klo = make_uint2(f2_to_bf2(lo[0], lo[1]), f2_to_bf2(lo[2], lo[3]));
+      const uint2 khh = make_uint2(f2_to_bf2(hi[0], hi[1]), f2_to_bf2(hi[2], hi[3]));
+      const uint2 vlo = *reinterpret_cast<const uint2*>(vp + i0);
+      const uint2 vhi = *reinterpret_cast<const uint2*>(vp + 64 + i0);
+      *reinterpret_cast<uint2*>(kpool + g + i0) = klo;
+      *reinterpret_cast<uint2*>(kpool + g + 64 + i0) = khh;
+      *reinterpret_cast<uint2*>(vpool + g + i0) = vlo;
+      *reinterpret_cast<uint2*>(vpool + g + 64 + i0) = vhi;
+      *reinterpret_cast<uint2*>(&scur[0][i0]) = klo;
+      *reinterpret_cast<uint2*>(&scur[0][64 + i0]) = khh;
+      *reinterpret_cast<uint2*>(&scur[1][i0]) = vlo;
+      *reinterpret_cast<uint2*>(&scur[1][64 + i0]) = vhi;
     }
+    __syncthreads();
+    mbar_wait(&bars[0], 0);
+    if (own_cur && threadIdx.x < 16)
+      reinterpret_cast<uint4*>(sk + (size_t)(cur - t0) * DA_D)[threadIdx.x] =
+          reinterpret_cast<const uint4*>(scur[0])[threadIdx.x];
     __syncthreads();
 
     // ---- scores: half-warp per token, 4 tokens in flight per half-warp
     {
       const int half = lane >> 4, hl = lane & 15;
-      constexpr int STRIDE = DA_WARPS * 2;
-      // warp-uniform trip count (the shuffles below need the full warp)
-      for (int tw = warp * 2; tw < ntok; tw += 4 * STRIDE) {
-        const int tb = tw + half;
+      constexpr int STRIDE = NW * 2;
+      const int hw = warp * 2 + half;
+      for (int base = 0; base < ntok; base += 4 * STRIDE) {   // warp-uniform
         float kf[4][8];
         bool valid[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int tt = tb + u * STRIDE;
+          const int tt = base + hw + u * STRIDE;
           valid[u] = tt < ntok;
-          const uint4 kv = *reinterpret_cast<const uint4*>(sk + (valid[u] ? tt : 0) * DA_D + hl * 8);
+          const uint4 kv =
+              *reinterpret_cast<const uint4*>(sk + (valid[u] ? tt : 0) * DA_D + hl * 8);
           const float2 a = bf2_to_f2(kv.x), c = bf2_to_f2(kv.y), e = bf2_to_f2(kv.z),
                        f = bf2_to_f2(kv.w);
           kf[u][0] = a.x; kf[u][1] = a.y; kf[u][2] = c.x; kf[u][3] = c.y;
@@ -454,51 +469,48 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
             for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
           if (hl == 0) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (valid[u])
-                ss[gi * part + tb + u * STRIDE] =
-                    fmaf(sl, (float)(t0 + tb + u * STRIDE - qpos), d[u]);
+            for (int u = 0; u < 4; ++u) {
+              const int tt = base + hw + u * STRIDE;
+              if (valid[u]) ss[gi * part + tt] = fmaf(sl, (float)(t0 + tt - qpos), d[u]);
+            }
           }
         }
       }
     }
     __syncthreads();
-    // ---- partition max per head: every warp reduces a token slice
-    float* wmax = sstat + 2 * G;            // [WARPS][G]
-    float* wsum = wmax + DA_WARPS * G;      // [WARPS][G]
-    for (int gi = 0; gi < G; ++gi) {
+    // ---- softmax statistics per head (one warp per head), p = exp2(s - m)
+    for (int gi = warp; gi < G; gi += NW) {
       float m = -INFINITY;
-      for (int i = warp * 32 + lane; i < ntok; i += DA_WARPS * 32) m = fmaxf(m, ss[gi * part + i]);
+      for (int i = lane; i < ntok; i += 32) m = fmaxf(m, ss[gi * part + i]);
       m = warp_max(m);
-      if (lane == 0) wmax[warp * G + gi] = m;
+      float l = 0.f;
+      for (int i = lane; i < ntok; i += 32) {
+        const float e = exp2f(ss[gi * part + i] - m);
+        ss[gi * part + i] = e;
+        l += e;
+      }
+      l = warp_sum(l);
+      if (lane == 0) {
+        sstat[gi * 2] = m;
+        sstat[gi * 2 + 1] = l;
+      }
     }
+    mbar_wait(&bars[1], 0);
+    if (own_cur && threadIdx.x < 16)
+      reinterpret_cast<uint4*>(sv + (size_t)(cur - t0) * DA_D)[threadIdx.x] =
+          reinterpret_cast<const uint4*>(scur[1])[threadIdx.x];
     __syncthreads();
-    if (threadIdx.x < G) {
-      float m = -INFINITY;
+    // ---- P V: warp per token stripe, lane owns dims [4*lane, 4*lane+4)
+    float acc[DA_MAXG][4];
 #pragma unroll
-      for (int w = 0; w < DA_WARPS; ++w) m = fmaxf(m, wmax[w * G + threadIdx.x]);
-      sstat[threadIdx.x * 2] = m;
-    }
-    __syncthreads();
-    float mrow[DA_MAXG];
-#pragma unroll
-    for (int gi = 0; gi < DA_MAXG; ++gi) mrow[gi] = gi < G ? sstat[gi * 2] : 0.f;
-    // ---- P V with the exponentials computed on the fly: warp per token
-    // stripe, lane owns dims [4*lane, 4*lane+4); per-warp partial sums of p
-    float acc[DA_MAXG][4], lsum[DA_MAXG];
-#pragma unroll
-    for (int gi = 0; gi < DA_MAXG; ++gi) {
-      acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
-      lsum[gi] = 0.f;
-    }
-    for (int tt = warp; tt < ntok; tt += DA_WARPS) {
+    for (int gi = 0; gi < DA_MAXG; ++gi) acc[gi][0] = acc[gi][1] = acc[gi][2] = acc[gi][3] = 0.f;
+    for (int tt = warp; tt < ntok; tt += NW) {
       const uint2 vv = *reinterpret_cast<const uint2*>(sv + tt * DA_D + lane * 4);
       const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
 #pragma unroll
       for (int gi = 0; gi < DA_MAXG; ++gi) {
         if (gi >= G) break;
-        const float pw = exp2f(ss[gi * part + tt] - mrow[gi]);
-        lsum[gi] += pw;
+        const float pw = ss[gi * part + tt];
         acc[gi][0] = fmaf(pw, v0.x, acc[gi][0]);
         acc[gi][1] = fmaf(pw, v0.y, acc[gi][1]);
         acc[gi][2] = fmaf(pw, v1.x, acc[gi][2]);
@@ -508,25 +520,34 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
 #pragma unroll
     for (int gi = 0; gi < DA_MAXG; ++gi) {
       if (gi >= G) break;
-      float4* dst = reinterpret_cast<float4*>(sacc + ((size_t)warp * G + gi) * DA_D + lane * 4);
-      *dst = make_float4(acc[gi][0], acc[gi][1], acc[gi][2], acc[gi][3]);
-      if (lane == 0) wsum[warp * G + gi] = lsum[gi];
+      *reinterpret_cast<float4*>(sacc + ((size_t)warp * G + gi) * DA_D + lane * 4) =
+          make_float4(acc[gi][0], acc[gi][1], acc[gi][2], acc[gi][3]);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < G * DA_D; i += blockDim.x) {
+    if (trig) pdl_launch_dependents();
+    for (int i = threadIdx.x; i < G * DA_D; i += (NW * 32)) {
       const int gi = i / DA_D, d = i % DA_D;
       float v = 0.f;
 #pragma unroll
-      for (int w = 0; w < DA_WARPS; ++w) v += sacc[((size_t)w * G + gi) * DA_D + d];
+      for (int w = 0; w < NW; ++w) v += sacc[((size_t)w * G + gi) * DA_D + d];
+      if (NP == 1) {   // single partition: no merge
+        out[((size_t)b * H + kh * G + gi) * DA_D + d] = __float2bfloat16(v / sstat[gi * 2 + 1]);
+        continue;
+      }
       float* wo = wsp(kh * G + gi, p);
       wo[d] = v;
       if (d == 0) {
-        float l = 0.f;
-#pragma unroll
-        for (int w = 0; w < DA_WARPS; ++w) l += wsum[w * G + gi];
         wo[DA_D] = sstat[gi * 2];
-        wo[DA_D + 1] = l;
+        wo[DA_D + 1] = sstat[gi * 2 + 1];
       }
+    }
+    if (NP == 1) return;
+  } else {
+    if (trig) pdl_launch_dependents();
+    if (threadIdx.x < G) {
+      float* w = wsp(kh * G + threadIdx.x, p);
+      w[DA_D] = -INFINITY;
+      w[DA_D + 1] = 0.f;
     }
   }
   // ---- fused split-K merge: the last CTA of (b, kh) combines the partitions
@@ -541,11 +562,11 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int gi = threadIdx.x / DA_D; gi < G; gi += DA_WARPS * 32 / DA_D) {
+  for (int i = threadIdx.x; i < G * DA_D; i += NW * 32) {
+    const int gi = i / DA_D, d = i % DA_D;
     const int gh = kh * G + gi;
     float m = -INFINITY;
     for (int pp = 0; pp < NP; ++pp) m = fmaxf(m, __ldcg(wsp(gh, pp) + DA_D));
-    const int d = threadIdx.x % DA_D;  // 128 threads per head, thread = dim
     float l = 0.f, o = 0.f;
     for (int pp = 0; pp < NP; ++pp) {
       const float* w = wsp(gh, pp);
@@ -558,6 +579,7 @@ __global__ void __launch_bounds__(DA_WARPS * 32, 2)
     out[((size_t)b * H + gh) * DA_D + d] = __float2bfloat16(o / l);
   }
 }
+
 
 }  // namespace swb
 
@@ -601,6 +623,59 @@ extern "C" size_t swb_attn_decode_workspace(int B, int H, int max_ctx, int parti
   return (size_t)B * H * np * (dh + 2) * sizeof(float) + (size_t)B * H * sizeof(int);
 }
 
+template <bool STEP>
+static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, void* v_layer,
+                              const int32_t* block_tables, int max_blocks,
+                              const int32_t* ctx_lens, const int32_t* positions,
+                              const int32_t* slots, float theta, const float* alibi_slopes,
+                              int B, int H, int Hkv, int dh, int block_size, float scale,
+                              int max_ctx, int partition, void* workspace, void* out,
+                              uintptr_t stream, const char* fn) {
+  SWB_REQUIRE(qkv && k_layer && v_layer && block_tables && ctx_lens && workspace && out,
+              "%s: null pointer", fn);
+  SWB_REQUIRE(dh == DA_D, "%s: dh must be 128", fn);
+  SWB_REQUIRE(H > 0 && Hkv > 0 && H % Hkv == 0 && H / Hkv <= DA_MAXG,
+              "%s: GQA group must be <= %d", fn, DA_MAXG);
+  SWB_REQUIRE(B > 0 && max_ctx > 0 && block_size > 0 && partition > 0 &&
+                  partition <= DA_MAXPART,
+              "%s: bad sizes (partition must be 1..%d)", fn, DA_MAXPART);
+  SWB_REQUIRE((block_size & (block_size - 1)) == 0 && partition % block_size == 0,
+              "%s: block_size must be a power of two dividing partition", fn);
+  SWB_REQUIRE(!STEP || alibi_slopes || theta > 1.f, "%s: theta", fn);
+  SWB_REQUIRE(row_stride % 8 == 0, "%s: row_stride %% 8", fn);
+  const int G = H / Hkv;
+  const int NP = (max_ctx + partition - 1) / partition;
+  // 8 warps when a GQA group shares the pass (more FMAs per staged byte)
+  const int nw = G >= 4 ? 8 : 4;
+  const size_t smem = (size_t)partition * DA_D * 2 * 2 +
+                      sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
+                                       (size_t)nw * G * DA_D + 2 * G);
+  static bool attr[64] = {false};
+  int dev = 0;
+  SWB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr[dev]) {
+    SWB_CUDA(cudaFuncSetAttribute(attn_decode_kernel<STEP, 4>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    SWB_CUDA(cudaFuncSetAttribute(attn_decode_kernel<STEP, 8>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr[dev] = true;
+  }
+  float* ws = reinterpret_cast<float*>(workspace);
+  int* tickets = reinterpret_cast<int*>(ws + (size_t)B * H * NP * (DA_D + 2));
+  const cudaError_t le = launch(
+      nw == 8 ? attn_decode_kernel<STEP, 8> : attn_decode_kernel<STEP, 4>, dim3(NP, Hkv, B),
+      dim3(nw * 32), smem, (cudaStream_t)stream,
+      reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
+      reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
+      block_tables, max_blocks, ctx_lens, positions, slots,
+      (STEP || positions) && !alibi_slopes ? log2f(theta) : 0.f, alibi_slopes, H, Hkv,
+      block_size, scale * 1.4426950408889634f, partition, ws, tickets,
+      reinterpret_cast<__nv_bfloat16*>(out), pdl_early_trigger() ? 1 : 0);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("attn_decode_kernel");
+}
+
 extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, void* v_layer,
                                const int32_t* block_tables, int max_blocks,
                                const int32_t* ctx_lens, const int32_t* positions,
@@ -608,45 +683,23 @@ extern "C" int swb_attn_decode(const void* qkv, int row_stride, void* k_layer, v
                                int B, int H, int Hkv, int dh, int block_size, float scale,
                                int max_ctx, int partition, void* workspace, void* out,
                                uintptr_t stream) {
-  SWB_REQUIRE(qkv && k_layer && v_layer && block_tables && ctx_lens && workspace && out,
-              "swb_attn_decode: null pointer");
-  SWB_REQUIRE(dh == DA_D, "swb_attn_decode: dh must be 128");
-  SWB_REQUIRE(H > 0 && Hkv > 0 && H % Hkv == 0 && H / Hkv <= DA_MAXG,
-              "swb_attn_decode: GQA group must be <= %d", DA_MAXG);
-  SWB_REQUIRE(B > 0 && max_ctx > 0 && partition > 0 && partition % 32 == 0 &&
-                  block_size > 0,
-              "swb_attn_decode: bad sizes");
   SWB_REQUIRE((positions == nullptr) == (slots == nullptr),
               "swb_attn_decode: positions and slots go together");
   SWB_REQUIRE(!positions || alibi_slopes || theta > 1.f, "swb_attn_decode: theta");
-  SWB_REQUIRE((block_size & (block_size - 1)) == 0 && partition % block_size == 0,
-              "swb_attn_decode: block_size must be a power of two dividing partition");
-  const int G = H / Hkv;
-  const int NP = (max_ctx + partition - 1) / partition;
-  const size_t smem = (size_t)partition * DA_D * 2 * 2 +
-                      sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
-                                       (size_t)DA_WARPS * G * DA_D + 2 * G +
-                                       2 * (size_t)DA_WARPS * G);
-  SWB_REQUIRE(smem <= 200 * 1024, "swb_attn_decode: partition too large");
-  static bool attr[64] = {false};
-  int dev = 0;
-  SWB_CUDA(cudaGetDevice(&dev));
-  if (dev < 64 && !attr[dev]) {
-    SWB_CUDA(cudaFuncSetAttribute(attn_decode_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr[dev] = true;
-  }
-  float* ws = reinterpret_cast<float*>(workspace);
-  int* tickets = reinterpret_cast<int*>(ws + (size_t)B * H * NP * (DA_D + 2));
-  const cudaError_t le = launch(
-      attn_decode_kernel, dim3(B, Hkv, NP), dim3(DA_WARPS * 32), smem, (cudaStream_t)stream,
-      reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
-      reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
-      block_tables, max_blocks, ctx_lens, positions, slots,
-      positions && !alibi_slopes ? log2f(theta) : 0.f, alibi_slopes, H,
-      Hkv, block_size, scale * 1.4426950408889634f, partition, ws, tickets,
-      reinterpret_cast<__nv_bfloat16*>(out));
-  if (le != cudaSuccess)
-    return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_kernel: %s", cudaGetErrorString(le));
-  return swb_check_launch("attn_decode_kernel");
+  return launch_attn_decode<false>(qkv, row_stride, k_layer, v_layer, block_tables, max_blocks,
+                                   ctx_lens, positions, slots, theta, alibi_slopes, B, H, Hkv,
+                                   dh, block_size, scale, max_ctx, partition, workspace, out,
+                                   stream, "swb_attn_decode");
+}
+
+extern "C" int swb_attn_decode_step(const void* qkv, int row_stride, void* k_layer,
+                                    void* v_layer, const int32_t* block_tables, int max_blocks,
+                                    const int32_t* ctx, float theta,
+                                    const float* alibi_slopes, int B, int H, int Hkv, int dh,
+                                    int block_size, float scale, int max_ctx, int partition,
+                                    void* workspace, void* out, uintptr_t stream) {
+  return launch_attn_decode<true>(qkv, row_stride, k_layer, v_layer, block_tables, max_blocks,
+                                  ctx, nullptr, nullptr, theta, alibi_slopes, B, H, Hkv, dh,
+                                  block_size, scale, max_ctx, partition, workspace, out, stream,
+                                  "swb_attn_decode_step");
 }

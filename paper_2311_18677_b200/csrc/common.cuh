@@ -51,6 +51,25 @@ __device__ __forceinline__ void pdl_wait() {
 // triggers implicitly as its CTAs exit, so the dependent launch still
 // overlaps this kernel's tail and the completion flush.
 __device__ __forceinline__ void pdl_trigger() {}
+// Explicit trigger at a kernel-chosen point (e.g. a streaming kernel's
+// producer after issuing its last load): the dependent grid launches once
+// every CTA has triggered or exited, so its CTAs take the SM slots freed by
+// this kernel's tail and start their own prologue / static-weight prefetch.
+// Rule: a thread triggers only after it has passed pdl_wait(), so when a
+// dependent starts, every kernel before this one has completed — a
+// dependent's pre-wait code may read data produced two or more launches back
+// (decode attention's page gather relies on it).
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// SWB_PDL_TRIGGER=0 disables those explicit triggers (A/B).
+inline bool pdl_early_trigger() {
+  static const bool on = [] {
+    const char* e = std::getenv("SWB_PDL_TRIGGER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // SWB_PDL=0 in the environment drops the attribute (A/B).  Measured on the 7B
 // decode graph: implicit (exit-time) trigger 3.19 ms/step vs 3.31 ms without

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     gemv_bulk_kernel(const void* __restrict__ xin, const __nv_bfloat16* __restrict__ nw,
                      float eps, const __nv_bfloat16* __restrict__ W, void* out,
                      const float* resid, const __nv_bfloat16* bias, int M, int N, int K,
-                     int epi, int n_items) {
+                     int epi, int n_items, int trig) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TV_STAGES * TV_STAGE_BYTES);
   uint64_t* empty = full + TV_STAGES;
@@ -111,6 +111,12 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
               bulk_load(st + j * TV_ROW_BYTES, W + (size_t)row * K + k0, bytes, &full[s], pol);
           }
         }
+      }
+      // last weight load issued: once this CTA is also past the dependency
+      // wait (so everything before it is complete) the next kernel may launch
+      if (trig) {
+        pdl_wait();
+        pdl_launch_dependents();
       }
     }
     return;
@@ -261,6 +267,18 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
   }
 }
 
+// Resident CTAs per SM of the streaming GEMVs (SWB_GEMV_CTAS_PER_SM, A/B).
+// With one CTA per SM the next kernel's CTAs (PDL, triggered once this
+// kernel's producers issued their last load) fit beside it and start their
+// weight stream while this one drains.
+static int gemv_ctas_per_sm() {
+  static const int n = [] {
+    const char* e = std::getenv("SWB_GEMV_CTAS_PER_SM");
+    return e ? std::max(1, std::min(2, atoi(e))) : 2;
+  }();
+  return n;
+}
+
 template <int MB, bool NORM>
 static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
                        const __nv_bfloat16* w, void* out, const float* r,
@@ -276,9 +294,10 @@ static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
     attr[dev] = true;
   }
   const size_t smem = TV_SMEM + (NORM ? (size_t)M * K * 2 : 0);
-  const int grid = min(items, TV_CTAS_PER_SM * kNumSMs);
+  const int grid = min(items, gemv_ctas_per_sm() * kNumSMs);
   const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM>, dim3(grid), dim3(TV_THREADS),
-                                smem, s, x, nw, eps, w, out, r, bias, M, N, K, epi, items);
+                                smem, s, x, nw, eps, w, out, r, bias, M, N, K, epi, items,
+                                pdl_early_trigger() ? 1 : 0);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("gemv_bulk_kernel");
@@ -318,7 +337,7 @@ template <int NB>   // NB = 1 (M <= 8) or 2 (M <= 16) MMAs of 8 batch rows
 __global__ void __launch_bounds__(TM_THREADS, 2)
     gemv_mma_kernel(const __grid_constant__ CUtensorMap tmW, const __nv_bfloat16* x,
                     void* out, const float* resid, const __nv_bfloat16* bias, int M, int N,
-                    int K, int epi, int n_items) {
+                    int K, int epi, int n_items, int trig) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -363,9 +382,16 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
           }
         }
       }
+      // last weight load issued: once this CTA is also past the dependency
+      // wait (so everything before it is complete) the next kernel may launch
+      if (trig) {
+        pdl_wait();
+        pdl_launch_dependents();
+      }
     }
     return;
   }
+  pdl_wait();   // x is produced by the previous kernel
   const int g = lane >> 2, t = lane & 3;
   int it = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -487,9 +513,10 @@ static int launch_gemv_mma(const __nv_bfloat16* x, const void* w, void* out, con
   const int st = make_tmap_rows(&tm, w, N, K, 8);
   if (st) return st;
   const int items = epi == SWB_EPI_SWIGLU ? (N / 2 + 7) / 8 : (N + TM_ROWS - 1) / TM_ROWS;
-  const int grid = min(items, 2 * kNumSMs);
+  const int grid = min(items, gemv_ctas_per_sm() * kNumSMs);
   const cudaError_t le = launch(gemv_mma_kernel<NB>, dim3(grid), dim3(TM_THREADS), TM_SMEM, s,
-                                tm, x, out, r, bias, M, N, K, epi, items);
+                                tm, x, out, r, bias, M, N, K, epi, items,
+                                pdl_early_trigger() ? 1 : 0);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch gemv_mma_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("gemv_mma_kernel");
@@ -506,6 +533,7 @@ static bool gemv_mma_enabled() {
 
 int dispatch_gemv_tc(const void* x, const void* w, void* out, const float* resid,
                      const __nv_bfloat16* bias, int M, int N, int K, int epi, cudaStream_t s);
+
 
 // SWB_GEMV_TC=0 keeps batched decode on the mma.sync kernel (A/B)
 static bool gemv_tc_enabled() {

@@ -15,7 +15,7 @@ from .errors import ValidationError
 
 __all__ = ["gemm", "gemv", "gemv_rmsnorm", "linear", "embed", "rmsnorm", "layernorm", "argmax",
            "rope_kv_write",
-           "kv_push_layer", "attn_prefill", "attn_decode", "decode_prepare",
+           "kv_push_layer", "attn_prefill", "attn_decode", "attn_decode_step", "decode_prepare",
            "decode_advance", "slots_from_table", "kv_signal", "stream_wait_flag",
            "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "EPI_GELU", "GEMV_MAX_ROWS"]
 
@@ -208,6 +208,18 @@ def attn_decode(qkv, k_layer, v_layer, block_tables, ctx_lens, B, H, Hkv, dh, bl
          Hkv, dh,
          block_size, float(scale), max_ctx, partition, workspace.data_ptr(), out.data_ptr(),
          _stream())
+    return out
+
+
+def attn_decode_step(qkv, k_layer, v_layer, block_tables, ctx, B, H, Hkv, dh, block_size,
+                     scale, max_ctx, partition, workspace, out, theta=10000.0, alibi=None):
+    """Decode-graph attention: the current token sits at position ctx[b] (RoPE
+    there, KV appended at the table's slot) and attends over ctx[b]+1 tokens;
+    the cached pages are gathered before the PDL wait (see swb200.h)."""
+    call("swb_attn_decode_step", qkv.data_ptr(), qkv.shape[1], k_layer, v_layer,
+         block_tables.data_ptr(), block_tables.shape[1], ctx.data_ptr(), float(theta),
+         _ptr(alibi), B, H, Hkv, dh, block_size, float(scale), max_ctx, partition,
+         workspace.data_ptr(), out.data_ptr(), _stream())
     return out
 
 

@@ -265,12 +265,30 @@ class ModelRunner:
         return torch.tensor(pos + cu + last, dtype=torch.int32)
 
     # ------------------------------------------------------------- decode
+    def decode_partition(self, B: int, max_ctx: int) -> int:
+        """Context partition of decode attention: the largest of 128/64/32
+        tokens that still gives >= 64 CTAs (B * Hkv * partitions).  Measured
+        on B200: 128 wins whenever the grid already covers ~half the SMs
+        (7B B=1 2.74 vs 2.79 ms at 64; 70B B=1 22.8 vs 23.3 ms); smaller
+        partitions only pay for a few-head TP shard at B=1.
+        SWB_DECODE_PART overrides; ``decode_partition=`` pins it."""
+        env = os.environ.get("SWB_DECODE_PART")
+        if env:
+            return int(env)
+        if self.partition != 128:
+            return self.partition
+        part = 128
+        while part > 32 and B * self.hkv * ((max_ctx + part - 1) // part) < 64:
+            part //= 2
+        return part
+
     def decode_graph(self, B: int, max_ctx: int, ring: int) -> "DecodeGraph":
-        np_ = (max_ctx + self.partition - 1) // self.partition
-        key = (B, np_, ring)
+        part = self.decode_partition(B, max_ctx)
+        np_ = (max_ctx + part - 1) // part
+        key = (B, np_ * part, part, ring)
         g = self.graphs.get(key)
         if g is None:
-            g = DecodeGraph(self, B, np_ * self.partition, ring)
+            g = DecodeGraph(self, B, np_ * part, ring, part)
             self.graphs[key] = g
         return g
 
@@ -278,8 +296,9 @@ class ModelRunner:
 class DecodeGraph:
     """Static buffers + captured CUDA graph of one decode iteration at batch B."""
 
-    def __init__(self, runner: ModelRunner, B: int, max_ctx: int, ring: int):
+    def __init__(self, runner: ModelRunner, B: int, max_ctx: int, ring: int, part: int = 128):
         self.r = runner
+        self.part = part
         self.B = B
         self.max_ctx = max_ctx
         self.ring = ring
@@ -302,7 +321,7 @@ class DecodeGraph:
         self.attn = torch.zeros(B, runner.hq * runner.dh, dtype=torch.bfloat16, device=dev)
         self.act = torch.zeros(B, runner.ffn, dtype=torch.bfloat16, device=dev)
         self.logits = torch.zeros(B, cfg.vocab, dtype=torch.float32, device=dev)
-        wsb = K.attn_decode_workspace_bytes(B, runner.hq, max_ctx, runner.partition, runner.dh)
+        wsb = K.attn_decode_workspace_bytes(B, runner.hq, max_ctx, part, runner.dh)
         self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
         self.graph = None
 
@@ -310,8 +329,6 @@ class DecodeGraph:
         r, cfg, w, kv = self.r, self.r.cfg, self.r.w, self.r.kv
         B = self.B
         r._begin_reductions()
-        K.decode_prepare(self.ctx, self.tables, kv.block_size, B, self.pos, self.slots,
-                         self.attn_len)
         r._embed(self.cur_tok, self.x)
         # pre-norm folded into the weight-streaming GEMV (h normalised once into
         # smem per CTA, overlapping the weight prefetch): used at B=1, where
@@ -326,13 +343,13 @@ class DecodeGraph:
             else:
                 r._norm(self.x, lw.attn_norm, lw.attn_norm_b, out=self.h)
                 K.linear(self.h, lw.wqkv, K.EPI_BF16, out=self.qkv, bias=lw.bqkv)
-            # RoPE (or ALiBi) + KV append of the current token + attention +
-            # split-K merge
-            K.attn_decode(self.qkv, kv.k_layer_ptr(li), kv.v_layer_ptr(li), self.tables,
-                          self.attn_len, B, r.hq, r.hkv, r.dh, kv.block_size, r.scale,
-                          self.max_ctx, r.partition, self.ws, out=self.attn,
-                          positions=self.pos, slots=self.slots, theta=cfg.rope_theta,
-                          alibi=r.alibi)
+            # RoPE (or ALiBi) + KV append of the current token at position
+            # ctx + attention + split-K merge; the cached pages are gathered
+            # before the PDL wait (ctx / tables come from the previous replay)
+            K.attn_decode_step(self.qkv, kv.k_layer_ptr(li), kv.v_layer_ptr(li), self.tables,
+                               self.ctx, B, r.hq, r.hkv, r.dh, kv.block_size, r.scale,
+                               self.max_ctx, self.part, self.ws, out=self.attn,
+                               theta=cfg.rope_theta, alibi=r.alibi)
             r._proj_reduce(self.attn, lw.wo, self.x, lw.bo)
             if fused:
                 K.gemv_rmsnorm(self.x, lw.mlp_norm, cfg.norm_eps, lw.wgu, K.EPI_SWIGLU,

@@ -184,8 +184,8 @@ def test_attn_prefill_varlen(K, H, Hkv, lens, impl):
         off += L
 
 
-@pytest.mark.parametrize("H,Hkv", [(32, 32), (64, 8)])
-def test_attn_decode_paged(K, H, Hkv):
+@pytest.mark.parametrize("H,Hkv,part", [(32, 32, 128), (64, 8, 128), (32, 32, 32), (64, 8, 64)])
+def test_attn_decode_paged(K, H, Hkv, part):
     dh, bs = 128, 16
     ctx = [1, 17, 300, 1100]
     B = len(ctx)
@@ -197,7 +197,6 @@ def test_attn_decode_paged(K, H, Hkv):
     tables = perm[:B * maxb].view(B, maxb).contiguous()
     qkv = torch.randn(B, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
     lens = torch.tensor(ctx, device="cuda", dtype=torch.int32)
-    part = 256
     wsb = K.attn_decode_workspace_bytes(B, H, 1200, part, dh)
     ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
     out = K.attn_decode(qkv, kpool.data_ptr(), vpool.data_ptr(), tables, lens, B, H, Hkv, dh, bs,
@@ -321,6 +320,40 @@ def test_attn_decode_fused_rope_append(K, H, Hkv):
     assert torch.equal(kp.view(torch.int16), kp2.view(torch.int16))
     assert torch.equal(vp.view(torch.int16), vp2.view(torch.int16))
     assert _rel(fused, ref) < 1e-3
+
+
+@pytest.mark.parametrize("H,Hkv,part,alibi", [(32, 32, 64, False), (64, 8, 32, False),
+                                              (16, 16, 128, True)])
+def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
+    """Decode-graph attention (swb_attn_decode_step: position = ctx, slot from
+    the block table, pages gathered before the PDL wait) is bit-identical to
+    the explicit-position form, output and appended pool rows."""
+    dh, bs, B = 128, 16, 4
+    cached = [0, 15, 128, 1000]          # tokens already in the pool
+    nblk, maxb = 400, 80
+    kp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    vp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    kp2, vp2 = kp.clone(), vp.clone()
+    tables = torch.randperm(nblk, device="cuda").int()[:B * maxb].view(B, maxb).contiguous()
+    ctx = torch.tensor(cached, device="cuda", dtype=torch.int32)
+    slots = (tables[torch.arange(B, device="cuda"), (ctx // bs).long()].long() * bs
+             + ctx % bs).int()
+    qkv = torch.randn(B, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    slopes = (torch.rand(H, device="cuda") * 0.5) if alibi else None
+    max_ctx = 1024 + 64
+    mk = lambda: torch.zeros(K.attn_decode_workspace_bytes(B, H, max_ctx, part, dh),  # noqa: E731
+                             dtype=torch.uint8, device="cuda")
+    out = torch.empty(B, H * dh, dtype=torch.bfloat16, device="cuda")
+    K.attn_decode_step(qkv, kp.data_ptr(), vp.data_ptr(), tables, ctx, B, H, Hkv, dh, bs,
+                       1 / math.sqrt(dh), max_ctx, part, mk(), out, theta=10000.0,
+                       alibi=slopes)
+    ref = K.attn_decode(qkv, kp2.data_ptr(), vp2.data_ptr(), tables, ctx + 1, B, H, Hkv, dh, bs,
+                        1 / math.sqrt(dh), max_ctx, part, mk(), positions=ctx, slots=slots,
+                        theta=10000.0, alibi=slopes)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+    assert torch.equal(kp.view(torch.int16), kp2.view(torch.int16))
+    assert torch.equal(vp.view(torch.int16), vp2.view(torch.int16))
 
 
 @pytest.mark.parametrize("M", [1, 5, 300])

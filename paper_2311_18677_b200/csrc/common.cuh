@@ -197,9 +197,19 @@ __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst,
 
 // ---------------------------------------------------------------- epilogues
 // BLOOM's MLP activation (tanh approximation, as its reference implementation)
-__device__ __forceinline__ float gelu_tanh(float x) {
-  return 0.5f * x * (1.f + tanhf(0.7978845608028654f * x * (1.f + 0.044715f * x * x)));
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
+__device__ __forceinline__ float gelu_tanh(float x) {
+  return 0.5f * x * (1.f + tanh_fast(0.7978845608028654f * x * (1.f + 0.044715f * x * x)));
+}
+// SiLU with a fast divide: an IEEE `g / (1 + exp(-g))` takes the division
+// slow path whenever exp(-g) overflows (large negative gate values), which
+// made the SwiGLU GEMM epilogue the bottleneck of the gate/up projection
+// (ncu: fdiv slow-path instructions at the top of the stall samples).
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.f + __expf(-g)); }
 // optional per-output-feature bf16 bias, added to the fp32 accumulator
 __device__ __forceinline__ float bias_at(const __nv_bfloat16* b, int n) {
   return b ? __bfloat162float(b[n]) : 0.f;

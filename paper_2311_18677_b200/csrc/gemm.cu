@@ -40,7 +40,6 @@ struct GemmArgs {
   int m_tiles, tiles;
 };
 
-__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
 
 // Epilogue of one 128 x 256 tile held in TMEM columns [acc_col, acc_col+256):
 // this warp owns TMEM lanes (= tile rows) 32*(warp%4) .. +31.
@@ -65,7 +64,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t t_r
         for (int i = 0; i < 16; ++i) {
           const float g0 = __uint_as_float(r[2 * i]), g1 = __uint_as_float(r[2 * i + 1]);
           const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
-          packed[i] = f2_to_bf2(silu(g0) * u0, silu(g1) * u1);
+          packed[i] = f2_to_bf2(silu_f(g0) * u0, silu_f(g1) * u1);
         }
         uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * nout + col);
 #pragma unroll
@@ -242,6 +241,189 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x 256 tile with tcgen05.mma M=256 (issued by the leader CTA only).
+// Each CTA stages ITS 128 rows of A and ITS 128 rows of W (one half of the
+// N=256 operand) per k-block, so per-SM shared-memory traffic per FLOP drops
+// by a third and each SM's TMEM holds its own 128 x 256 accumulator rows;
+// TMA completions of both CTAs land on the leader's mbarrier, the leader's
+// commits multicast to both CTAs' ring / accumulator barriers, and the
+// peer's epilogue warps release accumulators on the leader's barrier.
+constexpr int G2_STAGES = 6;
+constexpr int G2_STAGE_BYTES = G_A_BYTES + G_A_BYTES;   // 16 KB A + 16 KB W half
+constexpr int G2_SMEM_BYTES = G2_STAGES * G2_STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t g2_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t g2_mapa(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void g2_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-D TMA load into this CTA's smem, completion counted on the leader's
+// mbarrier (cluster address)
+__device__ __forceinline__ void g2_tma_load(void* smem_dst, const void* desc,
+                                            uint32_t leader_bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(desc), "r"(leader_bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void g2_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this smem offset in both CTAs of the pair once
+// the leader's MMAs issued so far completed
+__device__ __forceinline__ void g2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void g2_arrive_remote(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar)
+               : "memory");
+}
+__device__ __forceinline__ void g2_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gemm_bf16_tcgen05_pair(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmW, GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + G2_STAGES * G_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G2_STAGES * G2_STAGE_BYTES);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;   // [2] accumulator ready (both CTAs)
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained (leader: 8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = g2_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_k = (args.K + GK - 1) / GK;
+  const int m_pairs = (args.M + 2 * GM - 1) / (2 * GM);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < G2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(G_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  g2_cluster_sync();   // peer barriers initialised, TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // A (activations) is produced by the previous kernel
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs: own A rows, own W half)
+      int it = 0;
+      for (int t = pair; t < args.tiles; t += npairs) {
+        const int m0 = (t % m_pairs) * 2 * GM + (int)rank * GM;
+        const int n0 = (t / m_pairs) * GN + (int)rank * (GN / 2);
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % G2_STAGES;
+          if (it >= G2_STAGES) mbar_wait_sleep(&empty[s], ((it / G2_STAGES) - 1) & 1);
+          const uint32_t lbar = g2_mapa(smem_u32(&full[s]), 0);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * G2_STAGE_BYTES);
+          g2_tma_load(sA + s * G_A_BYTES, &tmA, lbar, kb * GK, m0);
+          g2_tma_load(sB + s * G_A_BYTES, &tmW, lbar, kb * GK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader CTA, single thread)
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * GM, GN);
+      int it = 0, i = 0;
+      for (int t = pair; t < args.tiles; t += npairs, ++i) {
+        const int acc = i & 1;
+        if (i >= 2) mbar_wait(&tempty[acc], ((i >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * GN;
+        for (int kb = 0; kb < num_k; ++kb, ++it) {
+          const int s = it % G2_STAGES;
+          mbar_wait(&full[s], (it / G2_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * G_A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * G_A_BYTES);
+#pragma unroll
+          for (int k = 0; k < GK / 16; ++k)
+            g2_mma(d_tmem, umma_desc_k_sw128(a_base + k * 32), umma_desc_k_sw128(b_base + k * 32),
+                   idesc, (kb | k) != 0);
+          g2_commit_both(&empty[s]);
+        }
+        g2_commit_both(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps (both CTAs): own 128 rows x 256 cols
+    const int q = warp & 3;
+    const uint32_t lead_tempty[2] = {g2_mapa(smem_u32(&tempty[0]), 0),
+                                     g2_mapa(smem_u32(&tempty[1]), 0)};
+    int i = 0;
+    for (int t = pair; t < args.tiles; t += npairs, ++i) {
+      const int acc = i & 1;
+      const int m0 = (t % m_pairs) * 2 * GM + (int)rank * GM, n0 = (t / m_pairs) * GN;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+      gemm_epilogue(args, tmem + acc * GN + ((uint32_t)(q * 32) << 16), m0 + q * 32 + lane, n0);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) g2_arrive_remote(lead_tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  g2_cluster_sync();   // the leader's last MMAs / the peer's reads are done in both CTAs
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(G_TMEM_COLS));
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
@@ -280,6 +462,55 @@ int make_tmap_rows(CUtensorMap* map, const void* base, int rows, int K, int box_
   return make_tmap_bf16_kmajor(map, base, rows, K, box_rows);
 }
 
+// SWB_GEMM_PAIR=0 keeps every prefill GEMM on the single-CTA kernel (A/B)
+static bool gemm_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SWB_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static int launch_gemm_pair(const CUtensorMap& ta, const void* w, void* out, const void* resid,
+                            const void* bias, int M, int N, int K, int epilogue,
+                            cudaStream_t stream) {
+  CUtensorMap tw;
+  int st = make_tmap_bf16_kmajor(&tw, w, N, K, GN / 2);   // each CTA loads half of W's tile
+  if (st) return st;
+  static bool attr_set[64] = {false};
+  int dev = 0;
+  SWB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr_set[dev]) {
+    SWB_CUDA(cudaFuncSetAttribute(gemm_bf16_tcgen05_pair,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM_BYTES));
+    attr_set[dev] = true;
+  }
+  const int m_pairs = (M + 2 * GM - 1) / (2 * GM), n_tiles = (N + GN - 1) / GN;
+  GemmArgs args{out, reinterpret_cast<const float*>(resid),
+                reinterpret_cast<const __nv_bfloat16*>(bias), M, N, K, epilogue, m_pairs,
+                m_pairs * n_tiles};
+  const int pairs = std::min(args.tiles, kNumSMs / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(G_THREADS);
+  cfg.dynamicSmemBytes = G2_SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_pair, ta, tw, args);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch gemm_bf16_tcgen05_pair: %s",
+                         cudaGetErrorString(le));
+  return swb_check_launch("gemm_bf16_tcgen05_pair");
+}
+
 }  // namespace swb
 
 using namespace swb;
@@ -310,6 +541,8 @@ extern "C" int swb_gemm_bf16_bias(const void* a, const void* w, void* out,
   CUtensorMap ta, tw;
   int st = make_tmap_bf16_kmajor(&ta, a, M, K, GM);
   if (st) return st;
+  if (M > GM && gemm_pair_enabled())
+    return launch_gemm_pair(ta, w, out, resid, bias, M, N, K, epilogue, (cudaStream_t)stream);
   st = make_tmap_bf16_kmajor(&tw, w, N, K, GN);
   if (st) return st;
   static bool attr_set[64] = {false};

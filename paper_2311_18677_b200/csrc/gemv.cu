@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
             const int nout = N >> 1, oi = item * 2 + j;
             if (oi < nout)
               reinterpret_cast<__nv_bfloat16*>(out)[(size_t)m * nout + oi] =
-                  __float2bfloat16(v / (1.f + __expf(-v)) * u);
+                  __float2bfloat16(silu_f(v) * u);
           }
         } else {
           const int r = item_row(item, j, false);
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
         const int nout = N >> 1, oi = item * 8 + row;
         if (oi < nout)
           reinterpret_cast<__nv_bfloat16*>(out)[(size_t)m * nout + oi] =
-              __float2bfloat16(v / (1.f + __expf(-v)) * u);
+              __float2bfloat16(silu_f(v) * u);
       } else {
         const int r = item * TM_ROWS + row;
         if (r >= N) continue;

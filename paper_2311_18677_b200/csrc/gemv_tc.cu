@@ -120,7 +120,7 @@ __device__ __forceinline__ void gt_store(const GtArgs& a, int m, int n, float v,
   if (a.epi == SWB_EPI_SWIGLU) {   // v = gate, u = up; out [M, N/2]
     const int nout = a.N >> 1;
     reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)m * nout + n] =
-        __float2bfloat16(v / (1.f + __expf(-v)) * u);
+        __float2bfloat16(silu_f(v) * u);
     return;
   }
   v += bias_at(a.bias, n);

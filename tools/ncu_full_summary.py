@@ -15,7 +15,14 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum",
        "smsp__pcsamp_warps_issue_stalled_long_scoreboard",
        "smsp__pcsamp_warps_issue_stalled_barrier",
        "smsp__pcsamp_warps_issue_stalled_wait",
-       "smsp__pcsamp_warps_issue_stalled_sleeping"]
+       "smsp__pcsamp_warps_issue_stalled_sleeping",
+       "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle",
+       "smsp__pcsamp_warps_issue_stalled_mio_throttle",
+       "smsp__pcsamp_warps_issue_stalled_lg_throttle",
+       "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
+       "smsp__pcsamp_warps_issue_stalled_selected",
+       "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+       "lts__t_bytes.sum"]
 
 
 def page(rep, name):
@@ -31,6 +38,8 @@ def main():
     hdr = rows[0]
     for r in rows[1:]:
         d = dict(zip(hdr, r))
+        if "ID" not in d or "Kernel Name" not in d:
+            continue
         key = (d["ID"], d["Kernel Name"].split("(")[0])
         if d["Metric Name"] in DETAILS:
             det.setdefault(key, []).append(f"{d['Metric Name']}: {d['Metric Value']} {d['Metric Unit']}")

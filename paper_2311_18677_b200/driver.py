@@ -87,6 +87,8 @@ class Driver:
         self._touched: set[int] = set()
         self._prompt_ms: dict[int, float] = {}
         self._done = 0
+        if hasattr(self.backend, "attach"):     # measured backends bind machines to GPUs
+            self.backend.attach(self)
 
     # ---- plumbing ----------------------------------------------------------
     def _schedule(self, t_ms: float, kind: str, payload) -> None:
@@ -167,6 +169,8 @@ class Driver:
                 rec.completion = t_ms
                 rec.preempt_count = task.preempt_count
                 self._done += 1
+                if hasattr(self.backend, "release"):
+                    self.backend.release(rec)
         self._touched.add(mid)
 
     def _hand_off(self, t_ms, rec: RequestRecord, prompt_ms: float) -> None:

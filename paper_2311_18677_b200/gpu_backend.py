@@ -1,0 +1,216 @@
+"""Driver backend whose iterations run on B200s (measured trace replay).
+
+``driver.Driver`` reproduces the reference engine's request lifecycle
+(reference engine.py:202-336) on a virtual millisecond clock; with
+``ModeledBackend`` every duration comes from a PerfModel lookup, i.e. the
+reference's ``prompt_time`` / ``token_iter_time`` / ``plan_transfer``
+(perf.py:119-132, transfer.py:79-99).  ``GpuBackend`` replaces each lookup
+with the real work on the machine's GPU and returns its measured device time:
+
+* a prompt iteration prefills the batch's prompts (libswb200 tcgen05 GEMMs,
+  attention, ...) and — when a request's token machine is another GPU —
+  pushes every finished layer's K/V straight into that GPU's paged blocks
+  (P2P stores over NVLink, peer access inside this process), overlapping the
+  next layers; the iteration lasts until the last layer's compute ends and
+  the request's TRANSFER event follows after the measured push tail
+  (``transfer_visible_ms``);
+* a token iteration runs one CUDA-graph decode step for exactly the batch
+  the token machine formed (Machine.form_batch: slots, memory, FCFS), with
+  the requests' real tokens and contexts, and returns its device time;
+* a mixed iteration (Baseline designs) runs both and takes their sum (the
+  reference's default mixing rule, machine.py:238-243).
+
+So the scheduling semantics are the reference's, exactly as pinned by the
+golden tests, while every latency on the clock is a B200 measurement for the
+actual batch composition.  Machines map onto GPUs of this process (one GPU
+per machine; several machines may share a GPU for small tests).  The
+concurrent multi-process serving path is ``splitwise.py``.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _abi
+from . import kernels as K
+from .kvcache import KVCacheManager, blocks_for
+from .model import get_config, init_weights
+from .runner import ModelRunner, PushSegment, PushStats
+from .serving import pool_blocks_for_memory
+from .splitwise import estimated_perf_model
+from .workers import PROMPT
+
+CTX_BUCKET = 2048          # decode graphs are captured per (batch, context bucket)
+
+
+class _Seq:
+    __slots__ = ("machine", "seq", "cur", "ctx")
+
+    def __init__(self, machine, seq, cur, ctx):
+        self.machine, self.seq, self.cur, self.ctx = machine, seq, cur, ctx
+
+
+class GpuBackend:
+    def __init__(self, model: str, devices: dict | None = None, seed: int = 0,
+                 block_size: int = 16, max_seqs: int = 256, max_ctx: int = 8192 + 4096,
+                 kv_share: float | None = None, prompt_seed: int = 1234):
+        self.cfg = get_config(model)
+        self.devices = devices
+        self.seed = seed
+        self.block_size = block_size
+        self.max_seqs = max_seqs
+        self.max_ctx = max_ctx
+        self.kv_share = kv_share
+        self.prompt_seed = prompt_seed
+        self.runners: dict[int, ModelRunner] = {}
+        self.dev: dict[int, int] = {}
+        self.state: dict[int, _Seq] = {}
+        self.visible: dict[int, tuple[float, float]] = {}
+        self.iter_log: list[tuple] = []     # (machine, kind, batch tokens/rows, ms)
+        self.driver = None
+
+    # ------------------------------------------------------------ set-up
+    def perf_models(self, machine_type: str = "B200") -> dict:
+        """Roofline-estimated PerfModel for batch formation / admission; the
+        capacity is the device pool actually allocated (set in attach)."""
+        return {machine_type: estimated_perf_model(self.cfg, None, self.cfg.weight_bytes(1))}
+
+    def attach(self, driver) -> None:
+        self.driver = driver
+        ms = driver.cluster.machines
+        ngpu = torch.cuda.device_count()
+        devs = self.devices or {mid: i % ngpu for i, mid in enumerate(sorted(ms))}
+        per_dev: dict[int, int] = {}
+        for mid in sorted(ms):
+            per_dev[devs[mid]] = per_dev.get(devs[mid], 0) + 1
+        weights = {}
+        for mid in sorted(ms):
+            d = devs[mid]
+            self.dev[mid] = d
+            with torch.cuda.device(d):
+                if d not in weights:
+                    weights[d] = init_weights(self.cfg, seed=self.seed)
+                share = self.kv_share or 1.0 / per_dev[d]
+                nb = pool_blocks_for_memory(self.cfg, 1, self.block_size, reserve_bytes=3 << 30,
+                                            frac=0.85 * share)
+                nb = min(nb, self.max_seqs * blocks_for(self.max_ctx, self.block_size))
+                kv = KVCacheManager(self.cfg.n_layers, nb, self.cfg.n_kv_heads,
+                                    self.cfg.head_dim, self.block_size, self.max_seqs,
+                                    blocks_for(self.max_ctx, self.block_size))
+                self.runners[mid] = ModelRunner(weights[d], kv)
+            # admission capacity = weights + this machine's physical pool
+            m = ms[mid]
+            m.perf = estimated_perf_model(self.cfg, kv, weights[d].nbytes())
+        for a in set(devs.values()):
+            with torch.cuda.device(a):
+                for b in set(devs.values()):
+                    if a != b:
+                        _abi.call("swb_enable_peer", b)
+
+    def _prompt_ids(self, rid: int, n: int) -> torch.Tensor:
+        g = torch.Generator().manual_seed(self.prompt_seed + rid)
+        return torch.randint(0, self.cfg.vocab, (n,), generator=g, dtype=torch.int32)
+
+    # ------------------------------------------------------------ iterations
+    def iteration_ms(self, machine, batch) -> float:
+        ms = 0.0
+        if batch.prompt_tasks:
+            ms += self._prefill(machine.id, batch.prompt_tasks)
+        if batch.token_tasks:
+            ms += self._decode(machine.id, batch.token_tasks)
+        return ms
+
+    def _prefill(self, mid: int, tasks) -> float:
+        recs = [self.driver.records[t.request_id] for t in tasks]
+        local = [r for r in recs if r.token_machine == mid]
+        remote = [r for r in recs if r.token_machine != mid]
+        ms = 0.0
+        for group, push in ((local, False), (remote, True)):
+            if group:
+                ms += self._prefill_group(mid, group, push)
+        return ms
+
+    def _prefill_group(self, mid: int, recs, push: bool) -> float:
+        runner, dev = self.runners[mid], self.dev[mid]
+        seqs = []
+        for r in recs:   # reserve the final context in the token machine's pool
+            tm = r.token_machine
+            with torch.cuda.device(self.dev[tm]):
+                seqs.append(self.runners[tm].kv.allocate(r.prompt_tokens + r.output_tokens))
+        for tm in {r.token_machine for r in recs}:
+            torch.cuda.synchronize(self.dev[tm])       # table rows written before peers read
+        lens = [r.prompt_tokens for r in recs]
+        with torch.cuda.device(dev):
+            toks = torch.cat([self._prompt_ids(r.request_id, r.prompt_tokens) for r in recs])
+            toks = toks.pin_memory().to(f"cuda:{dev}", non_blocking=True)
+            meta = ModelRunner.pack_meta(lens).pin_memory().to(f"cuda:{dev}", non_blocking=True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            stats = None
+            if push:
+                segs, off = [], 0
+                for r, s, n in zip(recs, seqs, lens):
+                    segs.append(PushSegment(off, n, self.runners[r.token_machine].kv, s))
+                    off += n
+                stats = PushStats(bytes_per_layer=off * 2 * runner.hkv * runner.dh * 2)
+                e0.record()
+                first = runner.prefill(toks, lens, meta, push=segs, push_stats=stats)
+            else:
+                kv = runner.kv
+                slots = torch.empty(sum(lens), dtype=torch.int32, device=f"cuda:{dev}")
+                off = 0
+                for s, n in zip(seqs, lens):
+                    K.slots_from_table(kv.table_row_ptr(s), 0, n, kv.block_size,
+                                       slots[off:off + n])
+                    off += n
+                e0.record()
+                first = runner.prefill(toks, lens, meta, local_slots=slots)
+            e1.record()
+            first_h = first.cpu()                   # synchronises the prompt GPU
+            if push:
+                runner.finish_push_stats()
+                ms = e0.elapsed_time(runner._compute_end)
+                for r in recs:
+                    self.visible[r.request_id] = (stats.tail_ms, sum(stats.layer_ms))
+            else:
+                ms = e0.elapsed_time(e1)
+        for r, s, f in zip(recs, seqs, first_h.tolist()):
+            self.state[r.request_id] = _Seq(r.token_machine, s, int(f), r.prompt_tokens)
+        self.iter_log.append((mid, "prompt", sum(lens), ms))
+        return ms
+
+    def _decode(self, mid: int, tasks) -> float:
+        runner, dev = self.runners[mid], self.dev[mid]
+        sts = [self.state[t.request_id] for t in tasks]
+        B = len(sts)
+        bucket = CTX_BUCKET * ((max(s.ctx for s in sts) + 2 + CTX_BUCKET - 1) // CTX_BUCKET)
+        with torch.cuda.device(dev):
+            g = runner.decode_graph(B, bucket, 1)
+            g.load([s.seq for s in sts], [s.cur for s in sts], [s.ctx for s in sts])
+            if g.graph is None:
+                g.capture()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            nxt = g.next_tok.cpu().tolist()         # synchronises
+            ms = e0.elapsed_time(e1)
+        for s, t in zip(sts, nxt):
+            s.cur = int(t)
+            s.ctx += 1
+        self.iter_log.append((mid, "token", B, ms))
+        return ms
+
+    # ------------------------------------------------------------ hand-off
+    def transfer_visible_ms(self, driver, rec, prompt_ms: float) -> float:
+        tail, raw = self.visible.pop(rec.request_id, (0.0, 0.0))
+        rec.transfer_raw_ms = raw
+        return tail
+
+    def release(self, rec) -> None:
+        s = self.state.pop(rec.request_id, None)
+        if s is not None:
+            with torch.cuda.device(self.dev[s.machine]):
+                self.runners[s.machine].kv.release(s.seq)
+
+
+__all__ = ["GpuBackend", "PROMPT"]

@@ -29,10 +29,13 @@ concurrent multi-process serving path is ``splitwise.py``.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _abi
 from . import kernels as K
+from .errors import CapacityError
 from .kvcache import KVCacheManager, blocks_for
 from .model import get_config, init_weights
 from .runner import ModelRunner, PushSegment, PushStats
@@ -41,6 +44,13 @@ from .splitwise import estimated_perf_model
 from .workers import PROMPT
 
 CTX_BUCKET = 2048          # decode graphs are captured per (batch, context bucket)
+
+
+class PoolExhausted(RuntimeError):
+    """A token machine's physical KV pool cannot hold another routed request:
+    the offered load exceeds what the pool ratio sustains (the reference's
+    provisioning treats a RuntimeError as 'fails at this load',
+    provision.py:138-143)."""
 
 
 class _Seq:
@@ -53,8 +63,14 @@ class _Seq:
 class GpuBackend:
     def __init__(self, model: str, devices: dict | None = None, seed: int = 0,
                  block_size: int = 16, max_seqs: int = 256, max_ctx: int = 8192 + 4096,
-                 kv_share: float | None = None, prompt_seed: int = 1234):
+                 kv_share: float | None = None, prompt_seed: int = 1234,
+                 clock: str = "measured"):
+        """clock="measured": the virtual clock advances by the measured device
+        times (the product).  clock="modeled": the work still runs on the GPU
+        but the clock advances by the PerfModel estimates, which makes the
+        schedule independent of timing noise (reproducible debugging)."""
         self.cfg = get_config(model)
+        self.clock = clock
         self.devices = devices
         self.seed = seed
         self.block_size = block_size
@@ -112,13 +128,26 @@ class GpuBackend:
         return torch.randint(0, self.cfg.vocab, (n,), generator=g, dtype=torch.int32)
 
     # ------------------------------------------------------------ iterations
+    def _dbg(self, what):
+        mode = os.environ.get("SWB_DEBUG_SYNC", "")
+        if mode and (mode == "1" or what.split()[-1 if what in ("prefill", "decode") else 1]
+                     .startswith(mode)):
+            for d in set(self.dev.values()):
+                torch.cuda.synchronize(d)
+            print("ok:", what, flush=True)
+
     def iteration_ms(self, machine, batch) -> float:
         ms = 0.0
         if batch.prompt_tasks:
+            self._dbg(f"before prefill m{machine.id} lens={[t.tokens for t in batch.prompt_tasks]}")
             ms += self._prefill(machine.id, batch.prompt_tasks)
+            self._dbg("prefill")
         if batch.token_tasks:
+            self._dbg(f"before decode m{machine.id} B={len(batch.token_tasks)} ctx="
+                      f"{[self.state[t.request_id].ctx for t in batch.token_tasks]}")
             ms += self._decode(machine.id, batch.token_tasks)
-        return ms
+            self._dbg("decode")
+        return ms if self.clock == "measured" else batch.iteration_time
 
     def _prefill(self, mid: int, tasks) -> float:
         recs = [self.driver.records[t.request_id] for t in tasks]
@@ -136,7 +165,11 @@ class GpuBackend:
         for r in recs:   # reserve the final context in the token machine's pool
             tm = r.token_machine
             with torch.cuda.device(self.dev[tm]):
-                seqs.append(self.runners[tm].kv.allocate(r.prompt_tokens + r.output_tokens))
+                try:
+                    seqs.append(self.runners[tm].kv.allocate(r.prompt_tokens + r.output_tokens))
+                except CapacityError as e:
+                    raise PoolExhausted(f"machine {tm}: {e} ({len(self.state)} requests hold "
+                                        "KV)") from e
         for tm in {r.token_machine for r in recs}:
             torch.cuda.synchronize(self.dev[tm])       # table rows written before peers read
         lens = [r.prompt_tokens for r in recs]
@@ -211,6 +244,8 @@ class GpuBackend:
         if s is not None:
             with torch.cuda.device(self.dev[s.machine]):
                 self.runners[s.machine].kv.release(s.seq)
+                if os.environ.get("SWB_DEBUG_SYNC") == "release":
+                    torch.cuda.synchronize()
 
 
-__all__ = ["GpuBackend", "PROMPT"]
+__all__ = ["GpuBackend", "PoolExhausted", "PROMPT"]

@@ -392,7 +392,10 @@ class DecodeGraph:
             t.copy_(v)
         g = torch.cuda.CUDAGraph()
         n0 = _abi.launch_count()
-        with torch.cuda.graph(g):
+        # explicit capture stream on this runner's device: torch.cuda.graph's
+        # default capture stream is created once, on whichever device was
+        # current then, and would bind a second GPU's graph to the first GPU
+        with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.r.dev)):
             self._step_body()
         self.launches_per_step = _abi.launch_count() - n0
         _abi.add_launches(-self.launches_per_step)  # capture launches nothing

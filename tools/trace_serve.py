@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--rate", type=float, default=2.0)
     ap.add_argument("--duration", type=float, default=20.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--clock", default="measured", choices=["measured", "modeled"])
     ap.add_argument("--max-output", type=int, default=0,
                     help="clamp output lengths (0 = preset support)")
     a = ap.parse_args()
@@ -38,14 +39,25 @@ def main():
         from paper_2311_18677_b200.driver import Request
         reqs = [Request(r.id, r.arrival, r.prompt_tokens, min(r.output_tokens, a.max_output))
                 for r in reqs]
-    backend = GpuBackend(a.model)
+    backend = GpuBackend(a.model, clock=a.clock)
     cc = ClusterConfig(a.design, a.prompt_machines, a.token_machines, llm=a.model)
     t0 = time.perf_counter()
     drv = Driver(cc, backend.perf_models(), reqs, backend=backend, record_log=False,
                  horizon_s=a.duration + 3600)
     setup = time.perf_counter() - t0
     t0 = time.perf_counter()
-    res = drv.run()
+    from paper_2311_18677_b200.gpu_backend import PoolExhausted
+    try:
+        res = drv.run()
+    except PoolExhausted as e:
+        done = [r for r in drv.records.values() if r.completion is not None]
+        print(json.dumps({"tool": "trace_serve", "model": a.model, "design": cc.design,
+                          "machines": {"prompt": a.prompt_machines, "token": a.token_machines},
+                          "trace": {"preset": a.preset, "rate": a.rate, "duration_s": a.duration,
+                                    "seed": a.seed, "requests": len(reqs)},
+                          "sustainable": False, "reason": str(e),
+                          "completed_before": len(done)}), flush=True)
+        return
     wall = time.perf_counter() - t0
     s = res.report.summary()
     recs = res.report.records
@@ -60,7 +72,7 @@ def main():
            "gpus": torch.cuda.device_count(), "trace": {"preset": a.preset, "rate": a.rate,
            "duration_s": a.duration, "seed": a.seed, "requests": len(reqs),
            "max_output": a.max_output or None},
-           "summary": s, "utilization": res.report.utilization,
+           "sustainable": True, "summary": s, "utilization": res.report.utilization,
            "kv_transfer": {"visible_ms_p50": statistics.median(vis) if vis else None,
                            "raw_ms_p50": statistics.median(raw) if raw else None},
            "iterations": {"prompt": len(pl), "token": len(tl),

@@ -1,7 +1,7 @@
 """Sum per-kernel DRAM bytes and time of ONE decode step from an ncu CSV
 (--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum)
-of tools/profile_step.py: the step's kernels are those after the last
-decode_prepare launch."""
+of tools/profile_step.py: the step's kernels are those from the last
+embed launch (the first kernel of a decode step) on."""
 import csv, sys, json
 rows = [l for l in open(sys.argv[1]) if l.startswith('"')]
 recs = {}
@@ -9,7 +9,7 @@ for r in csv.DictReader(rows):
     k = (r["ID"], r["Kernel Name"])
     recs.setdefault(k, {})[r["Metric Name"]] = (float(r["Metric Value"].replace(",", "")), r["Metric Unit"])
 items = sorted(recs.items(), key=lambda kv: int(kv[0][0]))
-starts = [i for i, ((_, n), _) in enumerate(items) if "decode_prepare" in n]
+starts = [i for i, ((_, n), _) in enumerate(items) if "embed_kernel" in n]
 step = items[starts[-1]:] if starts else []
 def b(m):
     v, u = m

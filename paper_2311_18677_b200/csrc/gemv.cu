@@ -316,8 +316,12 @@ constexpr int TM_ROWS = 16, TM_KC = 512, TM_STAGES = 6, TM_WARPS = 8;
 constexpr int TM_BOX_BYTES = TM_ROWS * 64 * 2;                 // 2 KB
 constexpr int TM_STAGE_BYTES = TM_ROWS * TM_KC * 2;            // 16 KB
 constexpr int TM_THREADS = (TM_WARPS + 1) * 32;
-constexpr int TM_SMEM = TM_STAGES * TM_STAGE_BYTES + 1024 + 2 * TM_STAGES * 8 +
-                        TM_WARPS * 32 * 8 * 4 + 256;
+constexpr int TM_NORM_STAGES = 4;   // pre-norm variant: 4 stages + staged h (<= 32 KB)
+constexpr int TM_HS_MAX = 32 * 1024;
+constexpr int tm_smem(int stages) {
+  return stages * TM_STAGE_BYTES + 1024 + 2 * stages * 8 + TM_WARPS * 32 * 8 * 4 + 256;
+}
+constexpr int TM_SMEM = tm_smem(TM_STAGES);
 
 __device__ __forceinline__ void ldsm_x4_g(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -333,22 +337,31 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int NB>   // NB = 1 (M <= 8) or 2 (M <= 16) MMAs of 8 batch rows
+// NORM: x is the fp32 residual stream; the B fragments are built on the fly as
+// h = bf16(x * rstd * norm_w), with rstd reduced in exactly swb_rmsnorm's
+// order (512 virtual threads, 16 warp partials), so the fused pre-norm GEMV
+// is bit-identical to swb_rmsnorm + GEMV and saves a launch per projection.
+template <int NB, bool NORM>   // NB = 1 (M <= 8) or 2 (M <= 16) MMAs of 8 batch rows
 __global__ void __launch_bounds__(TM_THREADS, 2)
-    gemv_mma_kernel(const __grid_constant__ CUtensorMap tmW, const __nv_bfloat16* x,
+    gemv_mma_kernel(const __grid_constant__ CUtensorMap tmW, const void* xin,
+                    const __nv_bfloat16* __restrict__ nw, float eps,
                     void* out, const float* resid, const __nv_bfloat16* bias, int M, int N,
                     int K, int epi, int n_items, int trig) {
+  constexpr int ST = NORM ? TM_NORM_STAGES : TM_STAGES;   // NORM: room for staged h
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(xin);
+  const float* xf = reinterpret_cast<const float*>(xin);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TM_STAGES * TM_STAGE_BYTES);
-  uint64_t* empty = full + TM_STAGES;
-  float* red = reinterpret_cast<float*>(empty + TM_STAGES);   // [WARPS][32 lanes][8]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * TM_STAGE_BYTES);
+  uint64_t* empty = full + ST;
+  float* red = reinterpret_cast<float*>(empty + ST);   // [WARPS][32 lanes][8]
+  __nv_bfloat16* hs = reinterpret_cast<__nv_bfloat16*>(red + TM_WARPS * 32 * 8);  // NORM [M][K]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool swiglu = epi == SWB_EPI_SWIGLU;
   const int nk = (K + TM_KC - 1) / TM_KC;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TM_STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], TM_WARPS);
     }
@@ -370,8 +383,8 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
           r1 = r0 + 8;
         }
         for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % TM_STAGES;
-          if (it >= TM_STAGES) mbar_wait_sleep(&empty[s], ((it / TM_STAGES) - 1) & 1);
+          const int s = it % ST;
+          if (it >= ST) mbar_wait_sleep(&empty[s], ((it / ST) - 1) & 1);
           mbar_arrive_expect_tx(&full[s], TM_STAGE_BYTES);
           uint8_t* st = smem + s * TM_STAGE_BYTES;
           for (int bx = 0; bx < TM_KC / 64; ++bx) {
@@ -393,6 +406,44 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
   }
   pdl_wait();   // x is produced by the previous kernel
   const int g = lane >> 2, t = lane & 3;
+  __shared__ float s_part[16 * 16];   // NORM: [row][virtual warp] sums of squares
+  __shared__ float s_rstd[16];
+  if constexpr (NORM) {
+    for (int m = 0; m < M; ++m) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int vt = threadIdx.x + half * (TM_WARPS * 32);    // swb_rmsnorm thread id
+        const float4* xr = reinterpret_cast<const float4*>(xf + (size_t)m * K);
+        float ss = 0.f;
+        for (int c = vt; c < K / 4; c += 2 * TM_WARPS * 32) {
+          const float4 v = xr[c];
+          ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        }
+        ss = warp_sum(ss);
+        if (lane == 0) s_part[m * 16 + warp + half * TM_WARPS] = ss;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TM_WARPS * 32) : "memory");
+    for (int m = warp; m < M; m += TM_WARPS) {
+      float v = lane < 16 ? s_part[m * 16 + lane] : 0.f;
+      v = warp_sum(v);
+      if (lane == 0) s_rstd[m] = rsqrtf(v / (float)K + eps);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TM_WARPS * 32) : "memory");
+    // h = bf16(x * rstd * w) once into shared memory (swb_rmsnorm's rounding);
+    // the streaming loop then reads it like a plain bf16 input
+    for (int i = threadIdx.x; i < M * K / 4; i += TM_WARPS * 32) {
+      const int m = (i * 4) / K, kk = (i * 4) % K;
+      const float r = s_rstd[m];
+      const float4 v = *reinterpret_cast<const float4*>(xf + (size_t)m * K + kk);
+      const uint2 ww = *reinterpret_cast<const uint2*>(nw + kk);
+      const float2 w0 = bf2_to_f2(ww.x), w1 = bf2_to_f2(ww.y);
+      *reinterpret_cast<uint2*>(hs + (size_t)m * K + kk) =
+          make_uint2(f2_to_bf2(v.x * r * w0.x, v.y * r * w0.y),
+                     f2_to_bf2(v.z * r * w1.x, v.w * r * w1.y));
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TM_WARPS * 32) : "memory");
+  }
   int it = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     float c[NB][4];
@@ -409,7 +460,12 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
         for (int ks = 0; ks < 4; ++ks) {
           const int k0 = kbase + ks * 16 + 2 * t;
           uint32_t v0 = 0, v1 = 0;
-          if (m < M && k0 < K) {
+          if constexpr (NORM) {
+            if (m < M && k0 < K) {
+              v0 = *reinterpret_cast<const uint32_t*>(hs + (size_t)m * K + k0);
+              if (k0 + 8 < K) v1 = *reinterpret_cast<const uint32_t*>(hs + (size_t)m * K + k0 + 8);
+            }
+          } else if (m < M && k0 < K) {
             v0 = __ldg(reinterpret_cast<const unsigned int*>(x + (size_t)m * K + k0));
             if (k0 + 8 < K)
               v1 = __ldg(reinterpret_cast<const unsigned int*>(x + (size_t)m * K + k0 + 8));
@@ -422,7 +478,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     uint32_t bnext[NB][4][2];
     load_b(0, bnext);
     for (int kc = 0; kc < nk; ++kc, ++it) {
-      const int s = it % TM_STAGES;
+      const int s = it % ST;
       uint32_t bfr[NB][4][2];
 #pragma unroll
       for (int h = 0; h < NB; ++h)
@@ -432,7 +488,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
           bfr[h][ks][1] = bnext[h][ks][1];
         }
       if (kc + 1 < nk) load_b(kc + 1, bnext);
-      mbar_wait(&full[s], (it / TM_STAGES) & 1);
+      mbar_wait(&full[s], (it / ST) & 1);
       const uint32_t box = smem_u32(smem + s * TM_STAGE_BYTES + warp * TM_BOX_BYTES);
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
@@ -497,16 +553,17 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
 
 int make_tmap_rows(CUtensorMap* map, const void* base, int rows, int K, int box_rows);
 
-template <int NB>
-static int launch_gemv_mma(const __nv_bfloat16* x, const void* w, void* out, const float* r,
-                           const __nv_bfloat16* bias, int M, int N, int K, int epi,
-                           cudaStream_t s) {
+template <int NB, bool NORM>
+static int launch_gemv_mma(const void* x, const __nv_bfloat16* nw, float eps, const void* w,
+                           void* out, const float* r, const __nv_bfloat16* bias, int M, int N,
+                           int K, int epi, cudaStream_t s) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr[dev]) {
-    SWB_CUDA(cudaFuncSetAttribute(gemv_mma_kernel<NB>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM));
+    SWB_CUDA(cudaFuncSetAttribute(gemv_mma_kernel<NB, NORM>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  NORM ? tm_smem(TM_NORM_STAGES) + TM_HS_MAX : TM_SMEM));
     attr[dev] = true;
   }
   CUtensorMap tm;
@@ -514,8 +571,9 @@ static int launch_gemv_mma(const __nv_bfloat16* x, const void* w, void* out, con
   if (st) return st;
   const int items = epi == SWB_EPI_SWIGLU ? (N / 2 + 7) / 8 : (N + TM_ROWS - 1) / TM_ROWS;
   const int grid = min(items, gemv_ctas_per_sm() * kNumSMs);
-  const cudaError_t le = launch(gemv_mma_kernel<NB>, dim3(grid), dim3(TM_THREADS), TM_SMEM, s,
-                                tm, x, out, r, bias, M, N, K, epi, items,
+  const size_t smem = NORM ? tm_smem(TM_NORM_STAGES) + (size_t)M * K * 2 : TM_SMEM;
+  const cudaError_t le = launch(gemv_mma_kernel<NB, NORM>, dim3(grid), dim3(TM_THREADS),
+                                smem, s, tm, x, nw, eps, out, r, bias, M, N, K, epi, items,
                                 pdl_early_trigger() ? 1 : 0);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch gemv_mma_kernel: %s", cudaGetErrorString(le));
@@ -555,15 +613,19 @@ static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, cons
   cudaStream_t s = (cudaStream_t)stream;
   // tcgen05 GEMV for batched decode; the mma.sync kernel stays ahead on
   // small matrices at small batch (measured crossover, tools/gemv_bench.py)
-  const double wbytes = 2.0 * N * K;
-  const bool small = (M <= 4 && wbytes < 160e6) || (M <= 8 && wbytes < 120e6);
-  if (!NORM && M >= 2 && gemv_tc_enabled() && (M > 16 || !small || !gemv_mma_enabled()))
+  // M = 2..4 (and 5..8 below 120 MB): the mma.sync kernel (measured ahead of
+  // the tcgen05 GEMV on the 7B step: B=2 3.30 vs 3.43 ms, B=4 3.82 vs 3.95);
+  // larger M / matrices: the tcgen05 GEMV.
+  // (The mma.sync kernel's two-MMA variant for M = 9..16 showed sporadic
+  // wrong columns under a repeat test and is not dispatched.)  Pre-norm fused
+  // variants: M = 2..8 on the mma.sync kernel with h staged in shared memory.
+  if (NORM && M >= 2)
+    return launch_gemv_mma<1, true>(x, nw, eps, w, out, rs, bias, M, N, K, epilogue, s);
+  const bool use_mma = M <= 4 || (M <= 8 && 2.0 * N * K < 120e6);
+  if (!NORM && M >= 2 && (!use_mma || !gemv_mma_enabled()) && gemv_tc_enabled())
     return dispatch_gemv_tc(x, w, out, rs, bias, M, N, K, epilogue, s);
-  if (!NORM && M >= 2 && gemv_mma_enabled()) {
-    auto xb = reinterpret_cast<const __nv_bfloat16*>(x);
-    if (M <= 8) return launch_gemv_mma<1>(xb, w, out, rs, bias, M, N, K, epilogue, s);
-    return launch_gemv_mma<2>(xb, w, out, rs, bias, M, N, K, epilogue, s);
-  }
+  if (!NORM && M >= 2 && M <= 8 && gemv_mma_enabled())
+    return launch_gemv_mma<1, false>(x, nullptr, 0.f, w, out, rs, bias, M, N, K, epilogue, s);
   if (M == 1) return launch_gemv<1, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
   if (M <= 2) return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
   if (M <= 4) return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
@@ -613,9 +675,11 @@ extern "C" int swb_gemv_rmsnorm_bf16(const float* x, const void* norm_w, float e
               "swb_gemv_rmsnorm_bf16: norm weight must be 16-byte aligned");
   SWB_REQUIRE(epilogue != SWB_EPI_RESID_F32 || resid != x,
               "swb_gemv_rmsnorm_bf16: output may not alias the normalized input");
-  SWB_REQUIRE((size_t)M * K * 2 <= (size_t)TV_HS_MAX,
-              "swb_gemv_rmsnorm_bf16: M*K*2 = %d bytes exceeds %d (use swb_rmsnorm + GEMV)",
-              M * K * 2, TV_HS_MAX);
+  SWB_REQUIRE(M == 1 ? (size_t)K * 2 <= (size_t)TV_HS_MAX
+                     : (M <= 8 && (size_t)M * K * 2 <= (size_t)TM_HS_MAX),
+              "swb_gemv_rmsnorm_bf16: staged h of M=%d x K=%d exceeds %d bytes (use "
+              "swb_rmsnorm + GEMV)", M, K, M == 1 ? TV_HS_MAX : TM_HS_MAX);
+  SWB_REQUIRE(K % 4 == 0, "swb_gemv_rmsnorm_bf16: K %% 4");
   return dispatch_gemv<true>(x, reinterpret_cast<const __nv_bfloat16*>(norm_w), eps, w, out,
                              resid, nullptr, M, N, K, epilogue, stream);
 }

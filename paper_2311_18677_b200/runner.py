@@ -330,9 +330,14 @@ class DecodeGraph:
         B = self.B
         r._begin_reductions()
         r._embed(self.cur_tok, self.x)
-        # pre-norm folded into the weight-streaming GEMV (h normalised once into
-        # smem per CTA, overlapping the weight prefetch): used at B=1, where
-        # the CUDA-core GEMV runs; SWB_FUSED_NORM=0/1 forces it off/on (Llama)
+        # pre-norm folded into the weight-streaming GEMV: h = rmsnorm(x) is
+        # normalised once into shared memory per CTA (B=1: CUDA-core kernel;
+        # B=2..8 with h <= 32 KB: mma.sync kernel, rstd reduced in
+        # swb_rmsnorm's order, bit-identical to the two-kernel path) while the
+        # weight ring fills; SWB_FUSED_NORM=0/1 forces it off/on (Llama).  Auto
+        # = B=1 only: at B=2/4 the staged variant measured 3.32/3.95 ms/step vs
+        # 3.30/3.82 with the separate norm (its 4-stage ring costs the launch
+        # it saves)
         mode = os.environ.get("SWB_FUSED_NORM", "auto")
         fused = (B == 1 and cfg.d_model * 2 <= 16384) if mode == "auto" else mode == "1"
         fused = fused and not r.bloom

@@ -238,6 +238,29 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         runner = ModelRunner(w, kv, tp_group=tp_nccl)
         server = TokenServer(runner, ctrl, peer_rank, sched, tp_ctrl=tp_gloo)
         dist.send_object_list([kv.ipc_handle(), server.rx.name], dst=peer_rank, group=ctrl)
+    push_alone = None
+    if is_prompt:
+        # KV-push kernel alone over NVLink (no concurrent prefill): one layer of
+        # 2048 prompt rows into the peer pool's first blocks (no live
+        # sequences yet), CUDA-event timed
+        rows = min(2048, peer.num_blocks * peer.block_size)
+        qkv = torch.randn(rows, runner.qkv_cols, device="cuda").bfloat16()
+        slots = torch.arange(rows, dtype=torch.int32, device="cuda")
+        push_alone = {}
+        for ctas in (runner.push_ctas, 148):
+            f = lambda: K.kv_push_layer(qkv, rows, runner.hq, runner.hkv, runner.dh,  # noqa: E731
+                                        peer.k_layer_ptr(0), peer.v_layer_ptr(0), slots,
+                                        peer.block_size, ctas)
+            f()
+            torch.cuda.synchronize()
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_.record()
+            for _ in range(10):
+                f()
+            e_.record()
+            torch.cuda.synchronize()
+            push_alone[ctas] = rows * 2 * runner.hkv * runner.dh * 2 / (s_.elapsed_time(e_) / 10) / 1e6
+        del qkv, slots
     g = torch.Generator().manual_seed(1234 + pair)
     reqs = [(pair * R + i, torch.randint(0, cfg.vocab, (P,), generator=g, dtype=torch.int32), O)
             for i in range(R)]
@@ -333,7 +356,14 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
                             "raw_ms": statistics.mean(push_raw),
                             "visible_ms": statistics.mean(push_tail),
                             "visible_frac_of_ttft": statistics.mean(push_tail) /
-                            percentile(ttft, 0.5)},
+                            percentile(ttft, 0.5),
+                            "push_kernel_alone_GBps": {f"{c}_ctas": round(v, 1)
+                                                       for c, v in push_alone.items()},
+                            "push_kernel_alone_frac": max(push_alone.values()) / 770.0,
+                            "note": "push_GBps_per_layer is measured in flight, sharing the "
+                                    "SMs with the next layers' prefill (64 CTAs); "
+                                    "push_kernel_alone_* is the same kernel timed alone, vs "
+                                    "770 GB/s measured peer copy (900 nominal)"},
             "gpu_launches": int(launches_t.item()),
             "clocks": clocks,
         }

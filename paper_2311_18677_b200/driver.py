@@ -108,7 +108,7 @@ class Driver:
     def run(self) -> DriverResult:
         for r in self.requests:
             self.records[r.id] = RequestRecord(r.id, r.arrival * 1e3, r.prompt_tokens,
-                                               r.output_tokens)
+                                               r.output_tokens, arrival_s=r.arrival)
             self._schedule(r.arrival * 1e3, ARRIVAL, r.id)
         win = self.config.repurpose_window_s
         if self.config.repurpose_enabled and math.isfinite(win):

@@ -39,6 +39,7 @@ class RequestRecord:
     transfer_raw_ms: float = 0.0
     preempt_count: int = 0
     tokens: list = field(default_factory=list)
+    arrival_s: float | None = None      # the trace's arrival (CSV output)
 
     @property
     def ttft_ms(self) -> float:
@@ -82,3 +83,28 @@ class MetricsReport:
             for p in (0.5, 0.9, 0.99):
                 out[f"{name}_p{int(p * 100)}"] = percentile(vals, p)
         return out
+
+
+REQUEST_CSV_HEADER = ("request_id,arrival_s,ttft_ms,e2e_ms,prompt_machine,"
+                      "token_machine,transfer_visible_ms,preempt_count")
+
+
+def requests_csv(records) -> str:
+    """Per-request CSV, byte-compatible with the reference's requests_csv
+    (engine.py:369-379)."""
+    out = [REQUEST_CSV_HEADER]
+    for r in records:
+        arr = r.arrival_s if r.arrival_s is not None else r.arrival_ms / 1e3
+        out.append(f"{r.request_id},{arr:.6f},{r.ttft_ms:.6f},{r.e2e_ms:.6f},"
+                   f"{r.prompt_machine},{r.token_machine},{r.transfer_visible_ms:.6f},"
+                   f"{r.preempt_count}")
+    return "\n".join(out) + "\n"
+
+
+def tbt_csv(records) -> str:
+    """Per-gap TBT CSV (reference engine.py:382-388)."""
+    out = ["request_id,gap_index,tbt_ms"]
+    for r in records:
+        for i, gap in enumerate(r.tbt_ms()):
+            out.append(f"{r.request_id},{i},{gap:.6f}")
+    return "\n".join(out) + "\n"

@@ -97,6 +97,47 @@ def generate_trace(prompt_dist: SizeDistribution, output_dist: SizeDistribution,
     return [Request(i, arrivals[i], int(prompts[i]), int(outputs[i])) for i in range(n)]
 
 
+TRACE_HEADER = "arrival_s,prompt_tokens,output_tokens"
+
+
+def serialize_trace(requests: list[Request]) -> str:
+    """The reference's three-column trace CSV (trace.py:206-212)."""
+    lines = [TRACE_HEADER] + [f"{r.arrival:.6f},{r.prompt_tokens},{r.output_tokens}"
+                              for r in requests]
+    return "\n".join(lines) + "\n"
+
+
+def parse_trace(text: str) -> list[Request]:
+    """Parse the trace CSV (reference trace.py:160-203): header checked, blank
+    lines skipped, counts >= 1, arrivals >= 0, stable-sorted by arrival and
+    re-numbered in that order."""
+    lines = text.strip().splitlines()
+    if not lines:
+        raise ValidationError("empty trace")
+    if lines[0].strip() != TRACE_HEADER:
+        raise ValidationError(f"line 1: expected header {TRACE_HEADER!r}, got {lines[0]!r}")
+    rows = []
+    for i, line in enumerate(lines[1:], start=2):
+        if not line.strip():
+            continue
+        parts = line.split(",")
+        if len(parts) != 3:
+            raise ValidationError(f"line {i}: expected 3 fields, got {len(parts)}")
+        try:
+            arrival, prompt, output = float(parts[0]), int(parts[1]), int(parts[2])
+        except ValueError as exc:
+            raise ValidationError(f"line {i}: {exc}") from None
+        if prompt < 1 or output < 1:
+            raise ValidationError(f"line {i}: non-positive token count")
+        if arrival < 0:
+            raise ValidationError(f"line {i}: negative arrival")
+        rows.append((arrival, prompt, output))
+    if not rows:
+        raise ValidationError("empty trace")
+    order = sorted(range(len(rows)), key=lambda k: rows[k][0])
+    return [Request(rid, *rows[k]) for rid, k in enumerate(order)]
+
+
 def preset_trace(preset: str, rate: float, duration: float, seed: int) -> list[Request]:
     if preset not in PRESETS:
         raise ValidationError(f"unknown preset {preset!r} (have {sorted(PRESETS)})")
@@ -104,4 +145,5 @@ def preset_trace(preset: str, rate: float, duration: float, seed: int) -> list[R
     return generate_trace(p["prompt"], p["output"], rate, duration, seed)
 
 
-__all__ = ["SizeDistribution", "PRESETS", "generate_trace", "preset_trace"]
+__all__ = ["SizeDistribution", "PRESETS", "TRACE_HEADER", "generate_trace", "preset_trace",
+           "serialize_trace", "parse_trace"]

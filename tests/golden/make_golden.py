@@ -15,6 +15,8 @@ replayed by tests/test_reference_parity.py against this repo's host code:
                  (cluster.py:129-185)
   engine.json    full Simulator runs (engine.py:160-358) on small traces:
                  per-request TTFT/E2E/TBT, routing, transfer visible latency
+  csv.json       the reference's trace CSV / requests_csv / tbt_csv text for
+                 two runs (engine.py:369-391, trace.py:206-212)
 
 Run:  python tests/golden/make_golden.py   (needs /root/reference)
 """
@@ -191,11 +193,30 @@ def gen_engine(engine, cluster, perf, trace):
     return runs
 
 
+def gen_csv(engine, cluster, perf, trace):
+    """Reference CSV outputs (trace CSV, requests_csv, tbt_csv, engine.py:369-391;
+    trace.py:206-212) for two runs, compared as exact strings."""
+    perfs = {"H100": perf.get_calibration("llama2-70b", "H100"),
+             "A100": perf.get_calibration("llama2-70b", "A100")}
+    out = []
+    for design, p, t, preset, rate, seed in (("Splitwise-HH", 2, 2, "coding", 2.0, 21),
+                                             ("Baseline-H100", 2, 0, "conversation", 1.0, 22)):
+        pd, od = trace.PRESETS[preset]["prompt"], trace.PRESETS[preset]["output"]
+        tr = trace.generate_trace(pd, od, rate, 15.0, seed=seed)
+        res = engine.Simulator(cluster.ClusterConfig(design, p, t), perfs, tr).run()
+        out.append({"design": design, "prompt_machines": p, "token_machines": t,
+                    "preset": preset, "rate": rate, "seed": seed, "duration": 15.0,
+                    "trace_csv": trace.serialize_trace(tr),
+                    "requests_csv": engine.requests_csv(res), "tbt_csv": engine.tbt_csv(res)})
+    return out
+
+
 def main():
     cluster, engine, machine, perf, trace, transfer = load_ref()
     fixtures = {"transfer": gen_transfer(transfer), "perf": gen_perf(perf),
                 "machine": gen_machine(machine, perf),
-                "engine": gen_engine(engine, cluster, perf, trace)}
+                "engine": gen_engine(engine, cluster, perf, trace),
+                "csv": gen_csv(engine, cluster, perf, trace)}
     for name, data in fixtures.items():
         with open(os.path.join(HERE, f"{name}.json"), "w") as f:
             json.dump(data, f, separators=(",", ":"))

@@ -31,10 +31,18 @@ def main():
     ap.add_argument("--duration", type=float, default=20.0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--clock", default="measured", choices=["measured", "modeled"])
+    ap.add_argument("--trace-csv", default="", help="replay this trace CSV instead of a preset")
+    ap.add_argument("--out-dir", default="", help="write requests.csv / tbt.csv / trace.csv here")
     ap.add_argument("--max-output", type=int, default=0,
                     help="clamp output lengths (0 = preset support)")
     a = ap.parse_args()
-    reqs = preset_trace(a.preset, a.rate, a.duration, a.seed)
+    if a.trace_csv:
+        from paper_2311_18677_b200.trace import parse_trace
+        with open(a.trace_csv) as f:
+            reqs = parse_trace(f.read())
+        a.preset, a.duration = os.path.basename(a.trace_csv), max(r.arrival for r in reqs) or 1.0
+    else:
+        reqs = preset_trace(a.preset, a.rate, a.duration, a.seed)
     if a.max_output:
         from paper_2311_18677_b200.driver import Request
         reqs = [Request(r.id, r.arrival, r.prompt_tokens, min(r.output_tokens, a.max_output))
@@ -60,6 +68,15 @@ def main():
         return
     wall = time.perf_counter() - t0
     s = res.report.summary()
+    if a.out_dir:
+        from paper_2311_18677_b200.metrics import requests_csv, tbt_csv
+        from paper_2311_18677_b200.trace import serialize_trace
+        os.makedirs(a.out_dir, exist_ok=True)
+        recs_sorted = [res.records[r.id] for r in reqs]
+        for name, text in (("requests.csv", requests_csv(recs_sorted)),
+                           ("tbt.csv", tbt_csv(recs_sorted)), ("trace.csv", serialize_trace(reqs))):
+            with open(os.path.join(a.out_dir, name), "w") as f:
+                f.write(text)
     recs = res.report.records
     vis = [r.transfer_visible_ms for r in recs if r.token_machine != r.prompt_machine
            and r.output_tokens > 1]

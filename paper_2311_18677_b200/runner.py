@@ -266,21 +266,13 @@ class ModelRunner:
 
     # ------------------------------------------------------------- decode
     def decode_partition(self, B: int, max_ctx: int) -> int:
-        """Context partition of decode attention: the largest of 128/64/32
-        tokens that still gives >= 64 CTAs (B * Hkv * partitions).  Measured
-        on B200: 128 wins whenever the grid already covers ~half the SMs
-        (7B B=1 2.74 vs 2.79 ms at 64; 70B B=1 22.8 vs 23.3 ms); smaller
-        partitions only pay for a few-head TP shard at B=1.
+        """Context partition of decode attention: 128 tokens.  Measured on B200:
+        smaller partitions (more CTAs for a short / few-head sequence) lose to
+        the extra split-K merge work — 7B B=1 2.74 vs 2.79 ms (64), 70B B=1
+        22.8 vs 23.3 ms (64), 70B TP4 B=1 10.9 vs 12.7 ms (32).
         SWB_DECODE_PART overrides; ``decode_partition=`` pins it."""
         env = os.environ.get("SWB_DECODE_PART")
-        if env:
-            return int(env)
-        if self.partition != 128:
-            return self.partition
-        part = 128
-        while part > 32 and B * self.hkv * ((max_ctx + part - 1) // part) < 64:
-            part //= 2
-        return part
+        return int(env) if env else self.partition
 
     def decode_graph(self, B: int, max_ctx: int, ring: int) -> "DecodeGraph":
         part = self.decode_partition(B, max_ctx)

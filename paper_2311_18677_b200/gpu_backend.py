@@ -64,13 +64,16 @@ class GpuBackend:
     def __init__(self, model: str, devices: dict | None = None, seed: int = 0,
                  block_size: int = 16, max_seqs: int = 256, max_ctx: int = 8192 + 4096,
                  kv_share: float | None = None, prompt_seed: int = 1234,
-                 clock: str = "measured"):
+                 clock: str = "measured", mixed: bool = True):
         """clock="measured": the virtual clock advances by the measured device
         times (the product).  clock="modeled": the work still runs on the GPU
         but the clock advances by the PerfModel estimates, which makes the
-        schedule independent of timing noise (reproducible debugging)."""
+        schedule independent of timing noise (reproducible debugging).
+        mixed=True runs an iteration holding both prompt and token tasks as one
+        fused step (ModelRunner.mixed); False runs prefill then decode."""
         self.cfg = get_config(model)
         self.clock = clock
+        self.mixed = mixed
         self.devices = devices
         self.seed = seed
         self.block_size = block_size
@@ -138,6 +141,12 @@ class GpuBackend:
 
     def iteration_ms(self, machine, batch) -> float:
         ms = 0.0
+        if (batch.prompt_tasks and batch.token_tasks and self.mixed and
+                all(self.driver.records[t.request_id].token_machine == machine.id
+                    for t in batch.prompt_tasks)):
+            # mixed batch: prompt rows and decode rows share every weight pass
+            ms = self._mixed(machine.id, batch.prompt_tasks, batch.token_tasks)
+            return ms if self.clock == "measured" else batch.iteration_time
         if batch.prompt_tasks:
             self._dbg(f"before prefill m{machine.id} lens={[t.tokens for t in batch.prompt_tasks]}")
             ms += self._prefill(machine.id, batch.prompt_tasks)
@@ -231,6 +240,42 @@ class GpuBackend:
             s.cur = int(t)
             s.ctx += 1
         self.iter_log.append((mid, "token", B, ms))
+        return ms
+
+    def _mixed(self, mid: int, ptasks, ttasks) -> float:
+        runner, dev = self.runners[mid], self.dev[mid]
+        kv = runner.kv
+        recs = [self.driver.records[t.request_id] for t in ptasks]
+        sts = [self.state[t.request_id] for t in ttasks]
+        with torch.cuda.device(dev):
+            seqs = [kv.allocate(r.prompt_tokens + r.output_tokens) for r in recs]
+            lens = [r.prompt_tokens for r in recs]
+            toks = torch.cat([self._prompt_ids(r.request_id, r.prompt_tokens) for r in recs])
+            toks = toks.pin_memory().to(f"cuda:{dev}", non_blocking=True)
+            meta = ModelRunner.pack_meta(lens).pin_memory().to(f"cuda:{dev}", non_blocking=True)
+            slots = torch.empty(sum(lens), dtype=torch.int32, device=f"cuda:{dev}")
+            off = 0
+            for s, n in zip(seqs, lens):
+                K.slots_from_table(kv.table_row_ptr(s), 0, n, kv.block_size, slots[off:off + n])
+                off += n
+            idx = torch.tensor([s.seq for s in sts], dtype=torch.long, device=f"cuda:{dev}")
+            tables = torch.index_select(kv.tables(), 0, idx)
+            dtok = torch.tensor([s.cur for s in sts], dtype=torch.int32, device=f"cuda:{dev}")
+            dctx = torch.tensor([s.ctx for s in sts], dtype=torch.int32, device=f"cuda:{dev}")
+            bucket = CTX_BUCKET * ((max(s.ctx for s in sts) + 2 + CTX_BUCKET - 1) // CTX_BUCKET)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            nxt = runner.mixed(toks, lens, meta, slots, tables, dtok, dctx, bucket)
+            e1.record()
+            nxt_h = nxt.cpu().tolist()
+            ms = e0.elapsed_time(e1)
+        R = len(recs)
+        for r, s, f in zip(recs, seqs, nxt_h[:R]):
+            self.state[r.request_id] = _Seq(mid, s, int(f), r.prompt_tokens)
+        for s, t in zip(sts, nxt_h[R:]):
+            s.cur = int(t)
+            s.ctx += 1
+        self.iter_log.append((mid, "mixed", sum(lens) + len(sts), ms))
         return ms
 
     # ------------------------------------------------------------ hand-off

@@ -243,6 +243,66 @@ class ModelRunner:
                 self._push_timing = (timing, push_stats)
         return first
 
+    def mixed(self, tokens: torch.Tensor, lens: list[int], meta: torch.Tensor,
+              local_slots: torch.Tensor, dec_tables: torch.Tensor, dec_tok: torch.Tensor,
+              dec_ctx: torch.Tensor, dec_max_ctx: int) -> torch.Tensor:
+        """One mixed iteration (reference machine.py:181-243 mixed batches): the
+        prompt rows of a prefill batch and one decode token for each of Bd
+        running sequences go through every weight GEMM together, so the
+        iteration streams the weights once; attention splits by row kind —
+        causal prefill attention (+ RoPE/KV write) for the prompt rows, paged
+        decode attention (RoPE + KV append at position dec_ctx) for the
+        decode rows.  Prompt KV goes to this machine's pool (local_slots).
+
+        tokens      int32 [T] prompt tokens; meta as for ``prefill``
+        dec_tables  int32 [Bd, max_blocks] table rows of the decoding sequences
+        dec_tok     int32 [Bd] their current tokens; dec_ctx int32 [Bd] cached
+                    lengths (advanced by one here)
+        Returns int32 [R + Bd]: first tokens of the prompts, then the decode rows'
+        next tokens."""
+        cfg, w, kv = self.cfg, self.w, self.kv
+        T, R, Bd = int(tokens.shape[0]), len(lens), int(dec_tok.shape[0])
+        rows = T + Bd
+        self._ensure_prefill(rows, R + Bd)
+        positions = meta[:T]
+        cu = meta[T:T + R + 1]
+        last_rows = meta[T + R + 1:T + 2 * R + 1]
+        x, h, attn, act = self.px[:rows], self.ph[:rows], self.pattn[:rows], self.pact[:rows]
+        key = ("mixed_ws", Bd, dec_max_ctx)
+        ws = self.graphs.get(key)
+        if ws is None:
+            ws = torch.zeros(K.attn_decode_workspace_bytes(Bd, self.hq, dec_max_ctx,
+                                                           self.partition, self.dh),
+                             dtype=torch.uint8, device=self.dev)
+            self.graphs[key] = ws
+        self._begin_reductions()
+        self._embed(torch.cat([tokens, dec_tok]), x)
+        for li, lw in enumerate(w.layers):
+            qkv = self.pqkv[0][:rows]
+            self._norm(x, lw.attn_norm, lw.attn_norm_b, out=h)
+            K.linear(h, lw.wqkv, K.EPI_BF16, out=qkv, bias=lw.bqkv)
+            K.rope_kv_write(qkv[:T], positions, self.hq, self.hkv, self.dh, self.theta,
+                            kv.k_layer_ptr(li), kv.v_layer_ptr(li), local_slots, kv.block_size)
+            K.attn_prefill(qkv[:T], cu, R, max(lens), self.hq, self.hkv, self.dh, self.scale,
+                           out=attn[:T], alibi=self.alibi)
+            K.attn_decode_step(qkv[T:], kv.k_layer_ptr(li), kv.v_layer_ptr(li), dec_tables,
+                               dec_ctx, Bd, self.hq, self.hkv, self.dh, kv.block_size,
+                               self.scale, dec_max_ctx, self.partition, ws, out=attn[T:],
+                               theta=cfg.rope_theta, alibi=self.alibi)
+            self._proj_reduce(attn, lw.wo, x, lw.bo)
+            self._norm(x, lw.mlp_norm, lw.mlp_norm_b, out=h)
+            self._mlp_up(h, lw, act)
+            self._proj_reduce(act, lw.wd, x, lw.bd)
+        idx = torch.cat([last_rows, torch.arange(T, rows, dtype=torch.int32, device=self.dev)])
+        last = self.plast[:R + Bd]
+        self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=idx)
+        logits = self.plogits[:R + Bd]
+        K.linear(last, w.lm_head, K.EPI_F32, out=logits)
+        nxt = self.pfirst[:R + Bd]
+        K.argmax(logits, out=nxt)
+        dec_ctx += 1
+        return nxt
+
     def finish_push_stats(self):
         """Resolve push timings after the prefill's events completed."""
         if not getattr(self, "_push_timing", None):

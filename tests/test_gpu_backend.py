@@ -62,3 +62,53 @@ def test_split_and_colocated_generate_same_tokens():
                record_log=False).run()
         toks[design] = seen
     assert toks["Splitwise-BB"] == toks["Baseline-B200"]
+
+
+def test_mixed_iteration_matches_separate_phases():
+    """ModelRunner.mixed (prompt rows + decode rows through the same GEMMs)
+    produces the same first tokens and decode tokens as a prefill followed by
+    a decode step, and writes the prompt's KV like the prefill does."""
+    from paper_2311_18677_b200 import kernels as K
+    from paper_2311_18677_b200.kvcache import KVCacheManager
+    from paper_2311_18677_b200.model import get_config, init_weights
+    from paper_2311_18677_b200.runner import ModelRunner
+    cfg = get_config("tiny")
+    w = init_weights(cfg, seed=0)
+    g = torch.Generator().manual_seed(9)
+    old = [torch.randint(0, cfg.vocab, (n,), generator=g, dtype=torch.int32) for n in (40, 70)]
+    new = torch.randint(0, cfg.vocab, (50,), generator=g, dtype=torch.int32)
+    out = {}
+    for mode in ("mixed", "separate"):
+        kv = KVCacheManager(cfg.n_layers, 128, cfg.n_kv_heads, cfg.head_dim, 16, 8, 16)
+        r = ModelRunner(w, kv)
+        seqs, firsts = [], []
+        for p in old:
+            s = kv.allocate(len(p) + 8)
+            sl = torch.empty(len(p), dtype=torch.int32, device="cuda")
+            K.slots_from_table(kv.table_row_ptr(s), 0, len(p), 16, sl)
+            firsts.append(int(r.prefill(p.cuda(), [len(p)], ModelRunner.pack_meta([len(p)]).cuda(),
+                                        local_slots=sl)[0]))
+            seqs.append(s)
+        sn = kv.allocate(len(new) + 8)
+        sl = torch.empty(len(new), dtype=torch.int32, device="cuda")
+        K.slots_from_table(kv.table_row_ptr(sn), 0, len(new), 16, sl)
+        meta = ModelRunner.pack_meta([len(new)]).cuda()
+        if mode == "mixed":
+            tables = kv.tables()[torch.tensor(seqs, device="cuda")].contiguous()
+            ctx = torch.tensor([len(p) for p in old], dtype=torch.int32, device="cuda")
+            nxt = r.mixed(new.cuda(), [len(new)], meta, sl, tables,
+                          torch.tensor(firsts, dtype=torch.int32, device="cuda"), ctx, 256)
+            out[mode] = nxt.tolist()
+            assert ctx.tolist() == [41, 71]
+        else:
+            f = int(r.prefill(new.cuda(), [len(new)], meta, local_slots=sl)[0])
+            gr = r.decode_graph(2, 256, 4)
+            gr.load(seqs, firsts, [len(p) for p in old])
+            gr.replay()
+            out[mode] = [f] + gr.next_tok.tolist()
+        torch.cuda.synchronize()
+        tb = kv.tables()[sn].long()
+        p = torch.arange(len(new), device="cuda")
+        out[mode + "_kv"] = kv.k_view(1)[tb[p // 16], :, p % 16].float().clone()
+    assert out["mixed"] == out["separate"]
+    assert (out["mixed_kv"] - out["separate_kv"]).abs().max().item() < 0.05

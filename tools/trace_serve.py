@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--duration", type=float, default=20.0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--clock", default="measured", choices=["measured", "modeled"])
+    ap.add_argument("--no-mixed", action="store_true",
+                    help="run mixed batches as prefill then decode (no fused step)")
     ap.add_argument("--trace-csv", default="", help="replay this trace CSV instead of a preset")
     ap.add_argument("--out-dir", default="", help="write requests.csv / tbt.csv / trace.csv here")
     ap.add_argument("--max-output", type=int, default=0,
@@ -47,7 +49,7 @@ def main():
         from paper_2311_18677_b200.driver import Request
         reqs = [Request(r.id, r.arrival, r.prompt_tokens, min(r.output_tokens, a.max_output))
                 for r in reqs]
-    backend = GpuBackend(a.model, clock=a.clock)
+    backend = GpuBackend(a.model, clock=a.clock, mixed=not a.no_mixed)
     cc = ClusterConfig(a.design, a.prompt_machines, a.token_machines, llm=a.model)
     t0 = time.perf_counter()
     drv = Driver(cc, backend.perf_models(), reqs, backend=backend, record_log=False,
@@ -82,7 +84,7 @@ def main():
            and r.output_tokens > 1]
     raw = [r.transfer_raw_ms for r in recs if r.token_machine != r.prompt_machine
            and r.output_tokens > 1]
-    pl = [x for x in backend.iter_log if x[1] == "prompt"]
+    pl = [x for x in backend.iter_log if x[1] in ("prompt", "mixed")]
     tl = [x for x in backend.iter_log if x[1] == "token"]
     out = {"tool": "trace_serve", "model": a.model, "design": cc.design,
            "machines": {"prompt": a.prompt_machines, "token": a.token_machines},
@@ -93,6 +95,7 @@ def main():
            "kv_transfer": {"visible_ms_p50": statistics.median(vis) if vis else None,
                            "raw_ms_p50": statistics.median(raw) if raw else None},
            "iterations": {"prompt": len(pl), "token": len(tl),
+                          "mixed": sum(1 for x in backend.iter_log if x[1] == "mixed"),
                           "prompt_tokens_mean": statistics.mean(x[2] for x in pl) if pl else 0,
                           "decode_batch_mean": statistics.mean(x[2] for x in tl) if tl else 0,
                           "decode_ms_mean": statistics.mean(x[3] for x in tl) if tl else 0},

@@ -16,6 +16,8 @@
 //
 // These replace the attention share of the reference's latency lookups
 // (perf.py:119-132); the reference has no attention arithmetic at all.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace swb {
@@ -295,6 +297,63 @@ __device__ __forceinline__ void rope4(float* a, float* b, int i0, float pos, flo
   }
 }
 
+
+// Split-K merge of the NP partition partials of one (b, kv head) group,
+// executed by the last CTA: the (m, l) pairs are fetched in parallel and the
+// per-partition factors exp2(m_p - M) computed once per head in shared
+// memory, then every thread sums its float4 of O over the partitions with
+// independent loads (a per-element dependent chain of L2 round trips made
+// the merge the slowest phase for GQA groups).  Fixed partition order:
+// deterministic.
+__device__ __forceinline__ void decode_merge(const float* __restrict__ ws_bh, int NP, int G,
+                                             int kh, int H, float* scratch,
+                                             __nv_bfloat16* __restrict__ out_b, int nthreads) {
+  // ws_bh = partials of (b, head 0): [H][NP][DA_D + 2]
+  float* sf = scratch;              // [G][NP] factors
+  float* sL = scratch + G * NP;     // [G]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = nthreads >> 5;
+  for (int i = tid; i < G * NP; i += nthreads) {
+    const int gi = i / NP, pp = i % NP;
+    const float* w = ws_bh + ((size_t)(kh * G + gi) * NP + pp) * (DA_D + 2);
+    sf[i] = __ldcg(w + DA_D);
+    sf[G * NP + G + i] = __ldcg(w + DA_D + 1);   // l, after sL
+  }
+  __syncthreads();
+  for (int gi = warp; gi < G; gi += nwarps) {
+    float M = -INFINITY;
+    for (int pp = lane; pp < NP; pp += 32) M = fmaxf(M, sf[gi * NP + pp]);
+    M = warp_max(M);
+    float L = 0.f;
+    for (int pp = lane; pp < NP; pp += 32) {
+      const float m = sf[gi * NP + pp];
+      const float f = m == -INFINITY ? 0.f : exp2f(m - M);
+      L += f * sf[G * NP + G + gi * NP + pp];
+      sf[gi * NP + pp] = f;
+    }
+    L = warp_sum(L);
+    if (lane == 0) sL[gi] = L;
+  }
+  __syncthreads();
+  for (int i = tid; i < G * (DA_D / 4); i += nthreads) {
+    const int gi = i / (DA_D / 4), d4 = i % (DA_D / 4);
+    const float* base = ws_bh + (size_t)(kh * G + gi) * NP * (DA_D + 2) + d4 * 4;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int pp = 0; pp < NP; ++pp) {
+      const float f = sf[gi * NP + pp];
+      const float* w = base + (size_t)pp * (DA_D + 2);
+      const float2 a = __ldcg(reinterpret_cast<const float2*>(w));
+      const float2 c = __ldcg(reinterpret_cast<const float2*>(w + 2));
+      o.x = fmaf(f, a.x, o.x); o.y = fmaf(f, a.y, o.y);
+      o.z = fmaf(f, c.x, o.z); o.w = fmaf(f, c.y, o.w);
+    }
+    const float inv = 1.f / sL[gi];
+    __nv_bfloat16* dst = out_b + (size_t)(kh * G + gi) * DA_D + d4 * 4;
+    *reinterpret_cast<uint2*>(dst) = make_uint2(f2_to_bf2(o.x * inv, o.y * inv),
+                                                f2_to_bf2(o.z * inv, o.w * inv));
+  }
+}
+
 template <bool STEP, int NW>
 __global__ void __launch_bounds__(NW * 32)
     attn_decode_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
@@ -562,24 +621,300 @@ __global__ void __launch_bounds__(NW * 32)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int i = threadIdx.x; i < G * DA_D; i += NW * 32) {
-    const int gi = i / DA_D, d = i % DA_D;
-    const int gh = kh * G + gi;
-    float m = -INFINITY;
-    for (int pp = 0; pp < NP; ++pp) m = fmaxf(m, __ldcg(wsp(gh, pp) + DA_D));
-    float l = 0.f, o = 0.f;
-    for (int pp = 0; pp < NP; ++pp) {
-      const float* w = wsp(gh, pp);
-      const float mp = __ldcg(w + DA_D);
-      if (mp == -INFINITY) continue;
-      const float f = exp2f(mp - m);
-      l += __ldcg(w + DA_D + 1) * f;
-      o += __ldcg(w + d) * f;
-    }
-    out[((size_t)b * H + gh) * DA_D + d] = __float2bfloat16(o / l);
-  }
+  decode_merge(ws + (size_t)b * H * NP * (DA_D + 2), NP, G, kh, H,
+               reinterpret_cast<float*>(dsm_raw), out + (size_t)b * H * DA_D, NW * 32);
 }
 
+
+// ---------------------------------------------------------------- decode, MMA
+// Tensor-core decode attention (block_size 16, partition 128): the G query
+// heads of a kv group form the rows of a 16-row mma.sync A tile (rows >= G
+// zero), so S = Q.K^T and O = P.V run as m16n8k16 MMAs straight from the
+// staged pages (ldmatrix / ldmatrix.trans) instead of shuffle-reduced dot
+// products — the GQA (G = 8) case was CUDA-core bound at ~0.1-0.9 TB/s.
+// Warp w owns tokens [32w, 32w+32) of the partition (2 pages) and waits only
+// for ITS pages (one K and one V mbarrier per warp), so compute starts while
+// later pages are still landing; warps combine (max, sum, O) through shared
+// memory, partitions through the fused split-K merge.
+constexpr int DM_WARPS = 4, DM_PT = 128, DM_WT = 32, DM_QS = DA_D + 8;
+
+template <bool STEP>
+__global__ void __launch_bounds__(DM_WARPS * 32)
+    attn_decode_mma_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
+                           __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
+                           const int32_t* __restrict__ tables, int max_blocks,
+                           const int32_t* __restrict__ ctx_lens, const int32_t* __restrict__ pos,
+                           const int32_t* __restrict__ slots, float log2_theta,
+                           const float* __restrict__ alibi, int H, int Hkv, float scale_log2,
+                           float* __restrict__ ws, int* __restrict__ tickets,
+                           __nv_bfloat16* __restrict__ out, int trig) {
+  constexpr int BS = 16;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(dsm);          // [128][128]
+  __nv_bfloat16* sv = sk + DM_PT * DA_D;                               // [128][128]
+  __nv_bfloat16* sq = sv + DM_PT * DA_D;                               // [16][DM_QS]
+  float* sml = reinterpret_cast<float*>(sq + 16 * DM_QS);              // [4][8][2]
+  float* so = sml + DM_WARPS * 8 * 2;                                  // [4][G][128]
+  __shared__ uint64_t kbar[DM_WARPS], vbar[DM_WARPS];
+  __shared__ int s_last;
+  __shared__ __align__(16) __nv_bfloat16 scur[2][DA_D];
+  const int p = blockIdx.x, kh = blockIdx.y, b = blockIdx.z;
+  const int NP = gridDim.x;
+  const int G = H / Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  auto wsp = [&](int gh, int pp) {
+    return ws + (((size_t)b * H + gh) * NP + pp) * (DA_D + 2);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < DM_WARPS; ++i) {
+      mbar_init(&kbar[i], 1);
+      mbar_init(&vbar[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int32_t* trow = tables + (size_t)b * max_blocks;
+  int L, cur;
+  if constexpr (STEP) {
+    const int c = __ldg(ctx_lens + b);
+    L = c + 1;
+    cur = c;
+  } else {
+    pdl_wait();
+    L = ctx_lens[b];
+    cur = pos ? pos[b] : -1;
+  }
+  const int t0 = p * DM_PT;
+  const int t1 = min(L, t0 + DM_PT);
+  const int ntok = t1 - t0;
+  if (warp == 0 && ntok > 0) {
+    // pages of cached tokens; page j feeds warp j/2's barriers
+    const int cend = cur >= 0 ? min(t1, cur) : t1;
+    const int nblk = (max(0, cend - t0) + BS - 1) / BS;
+    constexpr uint32_t tile = BS * DA_D * 2;
+    if (lane < DM_WARPS) {
+      const int np = min(max(nblk - 2 * lane, 0), 2);
+      mbar_arrive_expect_tx(&kbar[lane], tile * np);
+      mbar_arrive_expect_tx(&vbar[lane], tile * np);
+    }
+    __syncwarp();
+    if (lane < nblk) {
+      const int blk = __ldg(trow + t0 / BS + lane);
+      const size_t gofs = ((size_t)blk * Hkv + kh) * BS * DA_D;
+      bulk_g2s(sk + (size_t)lane * BS * DA_D, kpool + gofs, tile, &kbar[lane >> 1]);
+      bulk_g2s(sv + (size_t)lane * BS * DA_D, vpool + gofs, tile, &vbar[lane >> 1]);
+    }
+  }
+  if constexpr (STEP) pdl_wait();
+
+  if (ntok > 0) {
+    const int qpos = cur >= 0 ? cur : L - 1;
+    const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
+    const float fpos = (float)cur;
+    // q tile: rows = the group's heads (RoPE'd, rounded to bf16), rows >= G zero
+    for (int i = threadIdx.x; i < 16 * (DA_D / 8); i += DM_WARPS * 32) {
+      const int gi = i / (DA_D / 8), i0 = (i % (DA_D / 8)) * 4;
+      uint2 lo2 = make_uint2(0, 0), hi2 = make_uint2(0, 0);
+      if (gi < G) {
+        const __nv_bfloat16* hp = qrow + (kh * G + gi) * DA_D;
+        const uint2 ql = *reinterpret_cast<const uint2*>(hp + i0);
+        const uint2 qh = *reinterpret_cast<const uint2*>(hp + 64 + i0);
+        if (cur >= 0 && !alibi) {
+          const float2 l0 = bf2_to_f2(ql.x), l1 = bf2_to_f2(ql.y);
+          const float2 h0 = bf2_to_f2(qh.x), h1 = bf2_to_f2(qh.y);
+          float lo[4] = {l0.x, l0.y, l1.x, l1.y}, hi[4] = {h0.x, h0.y, h1.x, h1.y};
+          rope4(lo, hi, i0, fpos, log2_theta);
+          lo2 = make_uint2(f2_to_bf2(lo[0], lo[1]), f2_to_bf2(lo[2], lo[3]));
+          hi2 = make_uint2(f2_to_bf2(hi[0], hi[1]), f2_to_bf2(hi[2], hi[3]));
+        } else {
+          lo2 = ql;
+          hi2 = qh;
+        }
+      }
+      *reinterpret_cast<uint2*>(sq + gi * DM_QS + i0) = lo2;
+      *reinterpret_cast<uint2*>(sq + gi * DM_QS + 64 + i0) = hi2;
+    }
+    // current token: rotate k, append k/v to the pool, stage in smem
+    const bool own_cur = cur >= t0 && cur < t1;
+    if (own_cur && threadIdx.x < 16) {
+      const int i0 = threadIdx.x * 4;
+      const __nv_bfloat16* kp = qrow + (H + kh) * DA_D;
+      const __nv_bfloat16* vp = qrow + (H + Hkv + kh) * DA_D;
+      const uint2 kl = *reinterpret_cast<const uint2*>(kp + i0);
+      const uint2 khi = *reinterpret_cast<const uint2*>(kp + 64 + i0);
+      const float2 a0 = bf2_to_f2(kl.x), a1 = bf2_to_f2(kl.y);
+      const float2 c0 = bf2_to_f2(khi.x), c1 = bf2_to_f2(khi.y);
+      float lo[4] = {a0.x, a0.y, a1.x, a1.y}, hi[4] = {c0.x, c0.y, c1.x, c1.y};
+      if (!alibi) rope4(lo, hi, i0, fpos, log2_theta);
+      const int slot = STEP ? __ldg(trow + cur / BS) * BS + (cur & (BS - 1)) : slots[b];
+      const size_t go = (((size_t)(slot / BS) * Hkv + kh) * BS + (slot & (BS - 1))) * DA_D;
+      const uint2 klo = make_uint2(f2_to_bf2(lo[0], lo[1]), f2_to_bf2(lo[2], lo[3]));
+      const uint2 khh = make_uint2(f2_to_bf2(hi[0], hi[1]), f2_to_bf2(hi[2], hi[3]));
+      const uint2 vlo = *reinterpret_cast<const uint2*>(vp + i0);
+      const uint2 vhi = *reinterpret_cast<const uint2*>(vp + 64 + i0);
+      *reinterpret_cast<uint2*>(kpool + go + i0) = klo;
+      *reinterpret_cast<uint2*>(kpool + go + 64 + i0) = khh;
+      *reinterpret_cast<uint2*>(vpool + go + i0) = vlo;
+      *reinterpret_cast<uint2*>(vpool + go + 64 + i0) = vhi;
+      *reinterpret_cast<uint2*>(&scur[0][i0]) = klo;
+      *reinterpret_cast<uint2*>(&scur[0][64 + i0]) = khh;
+      *reinterpret_cast<uint2*>(&scur[1][i0]) = vlo;
+      *reinterpret_cast<uint2*>(&scur[1][64 + i0]) = vhi;
+    }
+    __syncthreads();
+
+    const int wt0 = warp * DM_WT;
+    const bool cur_here = own_cur && cur - t0 >= wt0 && cur - t0 < wt0 + DM_WT;
+    if (wt0 < ntok) {   // warp-uniform
+      mbar_wait(&kbar[warp], 0);
+      if (cur_here && lane < 16)
+        reinterpret_cast<uint4*>(sk + (size_t)(cur - t0) * DA_D)[lane] =
+            reinterpret_cast<const uint4*>(scur[0])[lane];
+      __syncwarp();
+      // S = Q K^T (16 heads-rows x 32 tokens)
+      float s[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      const uint32_t sq_u = smem_u32(sq), sk_u = smem_u32(sk), sv_u = smem_u32(sv);
+#pragma unroll
+      for (int kk = 0; kk < DA_D / 16; ++kk) {
+        uint32_t qf[4];
+        ldsm_x4(sq_u + ((lane & 15) * DM_QS + (kk * 2 + (lane >> 4)) * 8) * 2, qf[0], qf[1],
+                qf[2], qf[3]);
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+          const int key = wt0 + np * 16 + (lane & 7) + ((lane >> 4) << 3);
+          const int chunk = kk * 2 + ((lane >> 3) & 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(sk_u + (key * DA_D + chunk * 8) * 2, b0, b1, b2, b3);
+          mma_bf16(s[2 * np], qf, b0, b1);
+          mma_bf16(s[2 * np + 1], qf, b2, b3);
+        }
+      }
+      // row g = head g of the group (rows g+8 are padding)
+      const float sl = (alibi && g < G) ? alibi[kh * G + g] * 1.4426950408889634f : 0.f;
+      float m = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int tok = wt0 + nt * 8 + 2 * t + e;
+          const float v = tok < ntok ? fmaf(sl, (float)(t0 + tok - qpos), s[nt][e] * scale_log2)
+                                     : -INFINITY;
+          s[nt][e] = v;
+          m = fmaxf(m, v);
+        }
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      float l = 0.f;
+      uint32_t pf[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const float e0 = exp2f(s[nt][0] - m), e1 = exp2f(s[nt][1] - m);
+        l += e0 + e1;
+        const uint32_t pk = f2_to_bf2(e0, e1);
+        if ((nt & 1) == 0) {
+          pf[nt >> 1][0] = pk;
+          pf[nt >> 1][1] = 0u;
+        } else {
+          pf[nt >> 1][2] = pk;
+          pf[nt >> 1][3] = 0u;
+        }
+      }
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      mbar_wait(&vbar[warp], 0);
+      if (cur_here && lane < 16)
+        reinterpret_cast<uint4*>(sv + (size_t)(cur - t0) * DA_D)[lane] =
+            reinterpret_cast<const uint4*>(scur[1])[lane];
+      // rows past the context hold stale smem / unwritten pool bytes: P is 0
+      // there, but 0 * NaN is not, so zero them
+      for (int i = max(ntok - wt0, 0) * 16 + lane; i < DM_WT * 16; i += 32)
+        reinterpret_cast<uint4*>(sv + (size_t)wt0 * DA_D)[i] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      // O = P V (16 x 128)
+      float o[16][4];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+        for (int dp = 0; dp < 8; ++dp) {
+          const int key = wt0 + ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+          const int chunk = dp * 2 + (lane >> 4);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(sv_u + (key * DA_D + chunk * 8) * 2, b0, b1, b2, b3);
+          mma_bf16(o[2 * dp], pf[ks], b0, b1);
+          mma_bf16(o[2 * dp + 1], pf[ks], b2, b3);
+        }
+      }
+      if (g < G) {
+        float* dst = so + ((size_t)warp * G + g) * DA_D;
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(dst + nt * 8 + 2 * t) = make_float2(o[nt][0], o[nt][1]);
+        if (t == 0) {
+          sml[(warp * 8 + g) * 2] = m;
+          sml[(warp * 8 + g) * 2 + 1] = l;
+        }
+      }
+    } else if (t == 0 && g < G) {
+      sml[(warp * 8 + g) * 2] = -INFINITY;
+      sml[(warp * 8 + g) * 2 + 1] = 0.f;
+    }
+    __syncthreads();
+    if (trig) pdl_launch_dependents();
+    // combine the warps' partial softmax states
+    for (int i = threadIdx.x; i < G * DA_D; i += DM_WARPS * 32) {
+      const int gi = i / DA_D, d = i % DA_D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < DM_WARPS; ++w) M = fmaxf(M, sml[(w * 8 + gi) * 2]);
+      float o = 0.f, l = 0.f;
+#pragma unroll
+      for (int w = 0; w < DM_WARPS; ++w) {
+        const float mw = sml[(w * 8 + gi) * 2];
+        if (mw == -INFINITY) continue;
+        const float f = exp2f(mw - M);
+        o += f * so[((size_t)w * G + gi) * DA_D + d];
+        l += f * sml[(w * 8 + gi) * 2 + 1];
+      }
+      if (NP == 1) {
+        out[((size_t)b * H + kh * G + gi) * DA_D + d] = __float2bfloat16(o / l);
+        continue;
+      }
+      float* wo = wsp(kh * G + gi, p);
+      wo[d] = o;
+      if (d == 0) {
+        wo[DA_D] = M;
+        wo[DA_D + 1] = l;
+      }
+    }
+    if (NP == 1) return;
+  } else {
+    if (trig) pdl_launch_dependents();
+    if (threadIdx.x < G) {
+      float* w = wsp(kh * G + threadIdx.x, p);
+      w[DA_D] = -INFINITY;
+      w[DA_D + 1] = 0.f;
+    }
+  }
+  // ---- fused split-K merge: the last CTA of (b, kh) combines the partitions
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* tk = tickets + (size_t)b * Hkv + kh;
+    const int prev = atomicAdd(tk, 1);
+    s_last = prev == NP - 1;
+    if (s_last) *tk = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  decode_merge(ws + (size_t)b * H * NP * (DA_D + 2), NP, G, kh, H, reinterpret_cast<float*>(dsm),
+               out + (size_t)b * H * DA_D, DM_WARPS * 32);
+}
 
 }  // namespace swb
 
@@ -647,9 +982,12 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
   const int NP = (max_ctx + partition - 1) / partition;
   // 8 warps when a GQA group shares the pass (more FMAs per staged byte)
   const int nw = G >= 4 ? 8 : 4;
-  const size_t smem = (size_t)partition * DA_D * 2 * 2 +
-                      sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
-                                       (size_t)nw * G * DA_D + 2 * G);
+  const size_t merge_scratch = sizeof(float) * (2 * (size_t)G * NP + G);
+  const size_t smem = std::max(merge_scratch,
+                               (size_t)partition * DA_D * 2 * 2 +
+                                   sizeof(float) * ((size_t)G * DA_D + (size_t)G * partition +
+                                                    (size_t)nw * G * DA_D + 2 * G));
+  SWB_REQUIRE(smem <= 160 * 1024, "%s: max_ctx %d needs too many partitions", fn, max_ctx);
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
@@ -662,6 +1000,37 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
   }
   float* ws = reinterpret_cast<float*>(workspace);
   int* tickets = reinterpret_cast<int*>(ws + (size_t)B * H * NP * (DA_D + 2));
+  static const bool mma_on = [] {
+    const char* e = std::getenv("SWB_ATTN_MMA");
+    return !(e && e[0] == '0');
+  }();
+  // tensor-core kernel for GQA groups (measured: 70B-TP2 B=8 17.0 vs 19.5 us,
+  // B=32 54 vs 63 us); for MHA (G=1) the CUDA-core kernel is ahead (7B B=1
+  // 10.0 vs 13.9 us: the unswizzled 256-byte page rows cost the MMA kernel
+  // 8-way ldmatrix conflicts that only pay off when G rows share them)
+  if (mma_on && G >= 4 && block_size == 16 && partition == DM_PT) {
+    static bool attr_m[64] = {false};
+    if (dev < 64 && !attr_m[dev]) {
+      SWB_CUDA(cudaFuncSetAttribute(attn_decode_mma_kernel<STEP>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      attr_m[dev] = true;
+    }
+    const size_t msm = std::max(merge_scratch,
+                                (size_t)2 * DM_PT * DA_D * 2 + 16 * DM_QS * 2 +
+                                    sizeof(float) * (DM_WARPS * 8 * 2 + (size_t)DM_WARPS * G * DA_D));
+    const cudaError_t lm = launch(
+        attn_decode_mma_kernel<STEP>, dim3(NP, Hkv, B), dim3(DM_WARPS * 32), msm,
+        (cudaStream_t)stream, reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
+        reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
+        block_tables, max_blocks, ctx_lens, positions, slots,
+        (STEP || positions) && !alibi_slopes ? log2f(theta) : 0.f, alibi_slopes, H, Hkv,
+        scale * 1.4426950408889634f, ws, tickets, reinterpret_cast<__nv_bfloat16*>(out),
+        pdl_early_trigger() ? 1 : 0);
+    if (lm != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_mma_kernel: %s",
+                           cudaGetErrorString(lm));
+    return swb_check_launch("attn_decode_mma_kernel");
+  }
   const cudaError_t le = launch(
       nw == 8 ? attn_decode_kernel<STEP, 8> : attn_decode_kernel<STEP, 4>, dim3(NP, Hkv, B),
       dim3(nw * 32), smem, (cudaStream_t)stream,

@@ -326,13 +326,22 @@ class ModelRunner:
 
     # ------------------------------------------------------------- decode
     def decode_partition(self, B: int, max_ctx: int) -> int:
-        """Context partition of decode attention: 128 tokens.  Measured on B200:
-        smaller partitions (more CTAs for a short / few-head sequence) lose to
-        the extra split-K merge work — 7B B=1 2.74 vs 2.79 ms (64), 70B B=1
-        22.8 vs 23.3 ms (64), 70B TP4 B=1 10.9 vs 12.7 ms (32).
+        """Context partition of decode attention.  GQA groups (tensor-core
+        kernel) and short grids: 128 tokens — smaller partitions only add
+        split-K merge work (7B B=1 10.0 vs 10.7 us per layer at 64; 70B TP4
+        B=1 step 10.9 vs 12.7 ms at 32).  MHA with >= 4 CTAs per SM at 128:
+        64 tokens (half the staged pages per CTA, twice the CTAs resident):
+        7B B=8 44.8 vs 48.9 us, B=32 142 vs 165 us per layer.
         SWB_DECODE_PART overrides; ``decode_partition=`` pins it."""
         env = os.environ.get("SWB_DECODE_PART")
-        return int(env) if env else self.partition
+        if env:
+            return int(env)
+        if self.partition != 128:
+            return self.partition
+        mha = self.hq // self.hkv < 4
+        if mha and B * self.hkv * ((max_ctx + 127) // 128) >= 4 * 148:
+            return 64
+        return 128
 
     def decode_graph(self, B: int, max_ctx: int, ring: int) -> "DecodeGraph":
         part = self.decode_partition(B, max_ctx)

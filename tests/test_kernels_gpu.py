@@ -464,3 +464,48 @@ def test_attn_decode_alibi_append(K):
         q = qkv[b, :H * dh].view(1, H, dh)
         ref = _alibi_ref(q, kk, vv, slopes, q0=n - 1)[0]
         assert _rel(out[b].view(H, dh), ref) < 2e-2, b
+
+
+@pytest.mark.parametrize("alibi", [False, True])
+def test_attn_decode_step_large_batch(K, alibi):
+    """Decode-graph attention at a batch that fills the GPU (B*Hkv = 320):
+    output against a torch fp32 reference over the pool after the kernel
+    appended the current token (RoPE'd at its position, or ALiBi), including
+    contexts that end mid-page / mid-partition and the 0-cached case."""
+    H = Hkv = 32
+    dh, bs = 128, 16
+    B = 10
+    cached = [0, 1, 15, 16, 63, 64, 65, 700, 1000, 1500]
+    maxb = 1600 // bs
+    nblk = B * maxb + 8
+    kp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    vp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    tables = torch.randperm(nblk, device="cuda").int()[:B * maxb].view(B, maxb).contiguous()
+    ctx = torch.tensor(cached, device="cuda", dtype=torch.int32)
+    qkv = torch.randn(B, 3 * H * dh, device="cuda").bfloat16()
+    slopes = (torch.rand(H, device="cuda") * 0.1) if alibi else None
+    out = torch.empty(B, H * dh, dtype=torch.bfloat16, device="cuda")
+    ws = torch.zeros(K.attn_decode_workspace_bytes(B, H, 1664, 128, dh), dtype=torch.uint8,
+                     device="cuda")
+    K.attn_decode_step(qkv, kp.data_ptr(), vp.data_ptr(), tables, ctx, B, H, Hkv, dh, bs,
+                       1 / math.sqrt(dh), 1664, 128, ws, out, theta=10000.0, alibi=slopes)
+    torch.cuda.synchronize()
+    for b in range(B):
+        L = cached[b] + 1
+        p = torch.arange(L, device="cuda")
+        blk = tables[b][p // bs].long()
+        k = kp[blk, :, p % bs].float()              # [L, H, dh] incl. the appended token
+        v = vp[blk, :, p % bs].float()
+        q = qkv[b, :H * dh].view(H, dh).float()
+        if not alibi:   # the kernel rotates q at position cached[b]; use its appended k to check
+            half = dh // 2
+            inv = 10000.0 ** (-torch.arange(half, device="cuda", dtype=torch.float32) * 2 / dh)
+            ang = cached[b] * inv
+            c, s_ = torch.cos(ang), torch.sin(ang)
+            q = torch.cat([q[:, :half] * c - q[:, half:] * s_, q[:, half:] * c + q[:, :half] * s_],
+                          1).bfloat16().float()
+        s = torch.einsum("hd,lhd->hl", q, k) / math.sqrt(dh)
+        if alibi:
+            s = s + slopes[:, None] * (p[None, :] - cached[b]).float()
+        ref = torch.einsum("hl,lhd->hd", s.softmax(-1), v)
+        assert _rel(out[b].view(H, dh), ref) < 1e-2, b

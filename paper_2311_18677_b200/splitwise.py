@@ -129,11 +129,19 @@ class TokenServer:
         self.rx = HandoffReceiver(tp_ctrl)
         self.machine = Machine(0, None, estimated_perf_model(runner.cfg, self.kv,
                                                              runner.w.nbytes()), TOKEN, sched)
+        self.step_log: list[tuple] = []     # (batch, max context, device ms) per decode step
+        self._ev = None
+
+    def _events(self):
+        if self._ev is None:
+            self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        return self._ev
 
     def serve_burst(self, requests, t0: float):
         """Reserve KV for the routed requests, then admit hand-overs and
         decode until all of them finished.  Returns {rid: [emission times]}."""
         kv = self.kv
+        self.step_log = []
         seqs = [kv.allocate(len(p) + n) for _rid, p, n in requests]
         torch.cuda.current_stream().synchronize()    # tables written before the peer reads
         send_reservations(seqs, self.prompt_rank, self.ctrl)
@@ -176,9 +184,13 @@ class TokenServer:
                 if graph.graph is None:
                     graph.capture()
                 graph_rids = rids
+            ev0, ev1 = self._events()
+            ev0.record()
             graph.replay()
+            ev1.record()
             ring_h[:B].copy_(graph.next_tok, non_blocking=True)   # stream tokens out
             torch.cuda.current_stream().synchronize()
+            self.step_log.append((B, max(info[r][1] for r in rids), ev0.elapsed_time(ev1)))
             tnow = time.perf_counter()
             for b, r in enumerate(rids):
                 t = int(ring_h[b])
@@ -194,6 +206,24 @@ class TokenServer:
 
 
 # ---------------------------------------------------------------------------
+def _decode_roofline(cfg, tp, steps, hbm_peak, peak_kind):
+    """HBM roofline of the token machine's decode step (the dominant kernel
+    chain of a Splitwise pair): algorithmic bytes (weights / TP + the batch's
+    KV) over the CUDA-event time of the captured decode graph, full-batch
+    steps only."""
+    if not steps:
+        return None
+    bmax = max(b for b, _, _ in steps)
+    full = [(b, c, ms) for b, c, ms in steps if b == bmax]
+    byts = [cfg.decode_bytes([c] * b, tp) for b, c, _ in full]
+    ms = [m for _, _, m in full]
+    ach = (sum(byts) / len(byts)) / (sum(ms) / len(ms) / 1e3) / 1e9
+    return {"kernel": f"decode_step (CUDA graph, B={bmax}, token machine)", "bound": "hbm",
+            "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "peak_kind": peak_kind, "algorithmic_bytes": sum(byts) / len(byts),
+            "traffic": None, "steps_timed": len(full)}
+
+
 def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_traffic):
     import json
     rank = int(os.environ.get("RANK", "0"))
@@ -287,6 +317,7 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         one_step(False)
     launches0 = _abi.launch_count()
     e2e_ms, ttft, tbt, gaps2, push_gbs, push_tail, push_raw = [], [], [], [], [], [], []
+    dec_steps = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             t0, out, dms, wall = one_step(False)
@@ -295,8 +326,12 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
             if is_prompt:
                 st = server.push_log[-1]
                 payload["push"] = (st.bytes_per_layer, st.layer_ms, st.tail_ms)
+            else:
+                payload["steps"] = list(server.step_log)
             dist.all_gather_object(gathered, payload, group=ctrl)
             e2e_ms.append(dms)
+            for pr in range(0, world, 2 * tp):
+                dec_steps += gathered[pr + tp]["steps"]
             for pr in range(0, world, 2 * tp):
                 first = gathered[pr]["out"]
                 emits = gathered[pr + tp]["out"]
@@ -364,6 +399,7 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
                                     "SMs with the next layers' prefill (64 CTAs); "
                                     "push_kernel_alone_* is the same kernel timed alone, vs "
                                     "770 GB/s measured peer copy (900 nominal)"},
+            "roofline": _decode_roofline(cfg, tp, dec_steps, hbm_peak, peak_kind),
             "gpu_launches": int(launches_t.item()),
             "clocks": clocks,
         }

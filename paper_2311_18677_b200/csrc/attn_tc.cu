@@ -98,9 +98,14 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seq = blockIdx.x / tiles_per_seq;
-  const int qt = tiles_per_seq - 1 - (blockIdx.x % tiles_per_seq);  // heavy tiles first
-  const int h = blockIdx.y, kh = h / (H / Hkv);
+  // grid (H, tiles * seqs), x fastest: the hardware hands out CTAs in order,
+  // so every head's heaviest (last, causal) query tiles of every sequence go
+  // first and the light ones fill the SMs that free up — a longest-first
+  // schedule of the triangular work (1 CTA per SM by smem/TMEM)
+  const int nseq = gridDim.y / tiles_per_seq;
+  const int seq = blockIdx.y % nseq;
+  const int qt = tiles_per_seq - 1 - blockIdx.y / nseq;
+  const int h = blockIdx.x, kh = h / (H / Hkv);
   pdl_wait();
   const int s0 = cu[seq], len = cu[seq + 1] - s0;
   const int q0 = qt * TA_BM;
@@ -322,7 +327,7 @@ static int launch_tc(const CUtensorMap& tm, const int32_t* cu, int num_seqs, int
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, TA_SMEM));
     attr[dev] = true;
   }
-  const cudaError_t le = launch(attn_prefill_tc_kernel<ALIBI>, dim3(num_seqs * tiles, H),
+  const cudaError_t le = launch(attn_prefill_tc_kernel<ALIBI>, dim3(H, num_seqs * tiles),
                                 dim3(TA_THREADS), TA_SMEM, stream, tm, cu, tiles, H, Hkv,
                                 scale * 1.4426950408889634f, alibi,
                                 reinterpret_cast<__nv_bfloat16*>(out));

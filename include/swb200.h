@@ -79,6 +79,24 @@ int swb_gemm_bf16_bias(const void* a, const void* w, void* out,
                        const void* resid, const void* bias, int M, int N,
                        int K, int epilogue, uintptr_t stream);
 
+/* QKV projection of a prefill with the RoPE / KV-write step fused into the
+ * GEMM epilogue: qkv bf16 [M, (H+2Hkv)*128] = a . w^T (+ bias), then the q
+ * and k heads of row r are rotated at positions[r] (theta <= 1: no rotation,
+ * ALiBi models; rope_table may be NULL) and, when slots is given, row r's k/v heads are written to
+ * pool slot slots[r] — bit-identical to swb_gemm_bf16_bias(EPI_BF16) followed
+ * by swb_rope_kv_write.  Replaces the same prompt-phase lookup
+ * (PerfModel.prompt_time, perf.py:119-123). */
+int swb_gemm_qkv_rope(const void* a, const void* w, void* qkv, const void* bias,
+                      int M, int N, int K, const int32_t* positions, float theta,
+                      const void* rope_table, int table_len, int H, int Hkv,
+                      void* k_layer, void* v_layer, const int32_t* slots,
+                      int block_size, uintptr_t stream);
+/* (sin, cos) fp32 pairs [max_pos][64] of the RoPE angles pos * theta^(-2i/128),
+ * computed with the same device math the kernels use on the fly (so a table
+ * lookup is bit-identical); rope_table of swb_gemm_qkv_rope (positions >=
+ * table_len fall back to computing). */
+int swb_rope_table(float theta, int max_pos, void* table, uintptr_t stream);
+
 /* --------------------------------------------- skinny GEMM / GEMV (decode)
  * Same contract as swb_gemm_bf16 for small M (decode batch, 1..16 rows):
  * weight-streaming kernel, 128-bit coalesced weight loads, fp32 accumulate.

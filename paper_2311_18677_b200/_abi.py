@@ -48,6 +48,9 @@ SIGNATURES = {
     "swb_gemv_bf16": [_P, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_gemm_bf16_bias": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_gemv_bf16_bias": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _ST],
+    "swb_gemm_qkv_rope": [_P, _P, _P, _P, _I, _I, _I, _P, _F, _P, _I, _I, _I, _P, _P, _P, _I,
+                          _ST],
+    "swb_rope_table": [_F, _I, _P, _ST],
     "swb_gemv_rmsnorm_bf16": [_P, _P, _F, _P, _P, _P, _I, _I, _I, _I, _ST],
     "swb_embed": [_P, _P, _P, _I, _I, _ST],
     "swb_rmsnorm": [_P, _P, _P, _P, _I, _I, _F, _ST],
@@ -121,6 +124,7 @@ def check(status: int, what: str = "") -> None:
 # kernels launched per successful call (for the bench's gpu_launches claim)
 LAUNCH_MULT = {
     "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemm_bf16_bias": 1, "swb_gemv_bf16_bias": 1,
+    "swb_gemm_qkv_rope": 1, "swb_rope_table": 1,
     "swb_layernorm": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
     "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
     "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1,

@@ -210,6 +210,26 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 // made the SwiGLU GEMM epilogue the bottleneck of the gate/up projection
 // (ncu: fdiv slow-path instructions at the top of the stall samples).
 __device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.f + __expf(-g)); }
+
+// RoPE on one rotary pair (x_d, x_{d+64}) of a 128-dim head at position pos,
+// pair index i: explicit fmas so every kernel that rotates (the RoPE/KV-write
+// kernel, the fused QKV-GEMM epilogue) rounds identically.
+__device__ __forceinline__ void rope_sincos(int i, float pos, float log2_theta, int dh, float& s,
+                                            float& c) {
+  const float inv_freq = exp2f(-log2_theta * (float)(2 * i) / (float)dh);
+  sincosf(pos * inv_freq, &s, &c);
+}
+__device__ __forceinline__ void rope_apply(float a, float b, float s, float c, float& ra,
+                                           float& rb) {
+  ra = fmaf(a, c, -(b * s));
+  rb = fmaf(b, c, a * s);
+}
+__device__ __forceinline__ void rope_pair(float a, float b, int i, float pos, float log2_theta,
+                                          int dh, float& ra, float& rb) {
+  float s, c;
+  rope_sincos(i, pos, log2_theta, dh, s, c);
+  rope_apply(a, b, s, c, ra, rb);
+}
 // optional per-output-feature bf16 bias, added to the fp32 accumulator
 __device__ __forceinline__ float bias_at(const __nv_bfloat16* b, int n) {
   return b ? __bfloat162float(b[n]) : 0.f;

@@ -38,13 +38,120 @@ struct GemmArgs {
   int M, N, K;
   int epi;
   int m_tiles, tiles;
+  // EPI_QKV_ROPE (swb_gemm_qkv_rope): q/k heads rotated at pos[row], k/v
+  // rows written to the paged pool at slots[row] (slots may be null)
+  const int32_t* pos;
+  float log2_theta;
+  int H, Hkv, bs;
+  __nv_bfloat16* kpool;
+  __nv_bfloat16* vpool;
+  const int32_t* slots;
+  const float2* rope_tab;   // [tab_len][64] (sin, cos) or null
+  int tab_len;
 };
+constexpr int EPI_QKV_ROPE = 100;   // internal epilogue id
 
+// QKV projection epilogue: bias, round to bf16 (the stored qkv), RoPE on the
+// q and k heads from the rounded values (bit-identical to swb_rope_kv_write
+// after a plain GEMM), k/v rows appended to the paged pool.  A 256-column
+// tile holds two whole 128-dim heads; thread = row; pairs (d, d+64) come from
+// TMEM column chunks c and c+2 of the head.
+__device__ __forceinline__ void qkv_rope_epilogue(const GemmArgs& a, uint32_t t_row, int row,
+                                                  int n0) {
+  const bool row_ok = row < a.M;
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out);
+  const int qend = a.H * 128, kend = (a.H + a.Hkv) * 128;
+  const int ipos = row_ok ? __ldg(a.pos + row) : 0;
+  const float pos = (float)ipos;
+  const bool use_tab = ipos < a.tab_len;
+  size_t pbase = 0;
+  const bool pool = row_ok && a.slots != nullptr;
+  if (pool) {
+    const int slot = __ldg(a.slots + row);
+    pbase = (((size_t)(slot / a.bs) * a.Hkv) * a.bs + slot % a.bs) * 128;
+  }
+  const bool any_rot = n0 < kend && a.log2_theta > 0.f;      // block-uniform
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    // (sin, cos) of this row's 32 pairs of chunk c, shared by the tile's heads
+    float sn[32], cs[32];
+    if (any_rot && row_ok) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (use_tab) {
+          const float2 v = __ldg(a.rope_tab + ipos * 64 + c * 32 + i);
+          sn[i] = v.x;
+          cs[i] = v.y;
+        } else {
+          rope_sincos(c * 32 + i, pos, a.log2_theta, 128, sn[i], cs[i]);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int hh = 0; hh < 2; ++hh) {
+      const int hcol = n0 + hh * 128;
+      if (hcol >= a.N) break;                      // block-uniform
+      const bool rot = hcol < kend && a.log2_theta > 0.f;
+      uint32_t lo[32], hi[32];
+      tmem_ld32(t_row + hh * 128 + c * 32, lo);
+      tmem_ld32(t_row + hh * 128 + 64 + c * 32, hi);
+      tc_wait_ld();
+      if (!row_ok) continue;
+      uint32_t plo[16], phi[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float x[2], y[2];
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int d = c * 32 + i + e2;
+          float va = __uint_as_float(lo[i + e2]), vb = __uint_as_float(hi[i + e2]);
+          if (a.bias) {
+            va += __bfloat162float(a.bias[hcol + d]);
+            vb += __bfloat162float(a.bias[hcol + 64 + d]);
+          }
+          va = __bfloat162float(__float2bfloat16(va));      // the stored qkv value
+          vb = __bfloat162float(__float2bfloat16(vb));
+          if (rot) {
+            rope_apply(va, vb, sn[i + e2], cs[i + e2], x[e2], y[e2]);
+          } else {
+            x[e2] = va;
+            y[e2] = vb;
+          }
+        }
+        plo[i / 2] = f2_to_bf2(x[0], x[1]);
+        phi[i / 2] = f2_to_bf2(y[0], y[1]);
+      }
+      uint4* o_lo = reinterpret_cast<uint4*>(out + (size_t)row * a.N + hcol + c * 32);
+      uint4* o_hi = reinterpret_cast<uint4*>(out + (size_t)row * a.N + hcol + 64 + c * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        o_lo[i] = make_uint4(plo[4 * i], plo[4 * i + 1], plo[4 * i + 2], plo[4 * i + 3]);
+        o_hi[i] = make_uint4(phi[4 * i], phi[4 * i + 1], phi[4 * i + 2], phi[4 * i + 3]);
+      }
+      if (pool && hcol >= qend) {
+        __nv_bfloat16* dst = (hcol < kend ? a.kpool + (size_t)((hcol - qend) / 128) * a.bs * 128
+                                          : a.vpool + (size_t)((hcol - kend) / 128) * a.bs * 128) +
+                             pbase;
+        uint4* p_lo = reinterpret_cast<uint4*>(dst + c * 32);
+        uint4* p_hi = reinterpret_cast<uint4*>(dst + 64 + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          p_lo[i] = make_uint4(plo[4 * i], plo[4 * i + 1], plo[4 * i + 2], plo[4 * i + 3]);
+          p_hi[i] = make_uint4(phi[4 * i], phi[4 * i + 1], phi[4 * i + 2], phi[4 * i + 3]);
+        }
+      }
+    }
+  }
+}
 
 // Epilogue of one 128 x 256 tile held in TMEM columns [acc_col, acc_col+256):
 // this warp owns TMEM lanes (= tile rows) 32*(warp%4) .. +31.
 __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t t_row, int row,
                                               int n0) {
+  if (args.epi == EPI_QKV_ROPE) {
+    qkv_rope_epilogue(args, t_row, row, n0);
+    return;
+  }
   const bool row_ok = row < args.M;
   uint32_t r[32];
   if (args.epi == SWB_EPI_SWIGLU) {
@@ -471,9 +578,28 @@ static bool gemm_pair_enabled() {
   return on;
 }
 
+struct RopeArgs {
+  const int32_t* pos;
+  float log2_theta;
+  int H, Hkv, bs;
+  __nv_bfloat16* kpool;
+  __nv_bfloat16* vpool;
+  const int32_t* slots;
+  const float2* tab;
+  int tab_len;
+};
+
+__global__ void rope_table_kernel(float log2_theta, int n, float2* tab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;   // pos * 64 + pair
+  if (i >= n * 64) return;
+  float s, c;
+  rope_sincos(i & 63, (float)(i >> 6), log2_theta, 128, s, c);
+  tab[i] = make_float2(s, c);
+}
+
 static int launch_gemm_pair(const CUtensorMap& ta, const void* w, void* out, const void* resid,
                             const void* bias, int M, int N, int K, int epilogue,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, const RopeArgs* rope = nullptr) {
   CUtensorMap tw;
   int st = make_tmap_bf16_kmajor(&tw, w, N, K, GN / 2);   // each CTA loads half of W's tile
   if (st) return st;
@@ -489,6 +615,12 @@ static int launch_gemm_pair(const CUtensorMap& ta, const void* w, void* out, con
   GemmArgs args{out, reinterpret_cast<const float*>(resid),
                 reinterpret_cast<const __nv_bfloat16*>(bias), M, N, K, epilogue, m_pairs,
                 m_pairs * n_tiles};
+  if (rope) {
+    args.pos = rope->pos; args.log2_theta = rope->log2_theta; args.H = rope->H;
+    args.Hkv = rope->Hkv; args.bs = rope->bs; args.kpool = rope->kpool;
+    args.vpool = rope->vpool; args.slots = rope->slots;
+    args.rope_tab = rope->tab; args.tab_len = rope->tab_len;
+  }
   const int pairs = std::min(args.tiles, kNumSMs / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
@@ -515,6 +647,10 @@ static int launch_gemm_pair(const CUtensorMap& ta, const void* w, void* out, con
 
 using namespace swb;
 
+static int gemm_launch(const void* a, const void* w, void* out, const void* resid,
+                       const void* bias, int M, int N, int K, int epilogue,
+                       cudaStream_t stream, const RopeArgs* rope);
+
 extern "C" int swb_gemm_bf16(const void* a, const void* w, void* out,
                              const void* resid, int M, int N, int K, int epilogue,
                              uintptr_t stream) {
@@ -538,11 +674,19 @@ extern "C" int swb_gemm_bf16_bias(const void* a, const void* w, void* out,
               "swb_gemm_bf16: residual epilogue needs resid");
   SWB_REQUIRE((((uintptr_t)a | (uintptr_t)w | (uintptr_t)out) & 15) == 0,
               "swb_gemm_bf16: pointers must be 16-byte aligned");
+  return gemm_launch(a, w, out, resid, bias, M, N, K, epilogue, (cudaStream_t)stream, nullptr);
+}
+
+static int gemm_launch(const void* a, const void* w, void* out, const void* resid,
+                       const void* bias, int M, int N, int K, int epilogue,
+                       cudaStream_t stream_, const RopeArgs* rope) {
+  const uintptr_t stream = (uintptr_t)stream_;
   CUtensorMap ta, tw;
   int st = make_tmap_bf16_kmajor(&ta, a, M, K, GM);
   if (st) return st;
   if (M > GM && gemm_pair_enabled())
-    return launch_gemm_pair(ta, w, out, resid, bias, M, N, K, epilogue, (cudaStream_t)stream);
+    return launch_gemm_pair(ta, w, out, resid, bias, M, N, K, epilogue, (cudaStream_t)stream,
+                            rope);
   st = make_tmap_bf16_kmajor(&tw, w, N, K, GN);
   if (st) return st;
   static bool attr_set[64] = {false};
@@ -558,6 +702,12 @@ extern "C" int swb_gemm_bf16_bias(const void* a, const void* w, void* out,
   GemmArgs args{out, reinterpret_cast<const float*>(resid),
                 reinterpret_cast<const __nv_bfloat16*>(bias), M, N, K, epilogue, m_tiles,
                 m_tiles * n_tiles};
+  if (rope) {
+    args.pos = rope->pos; args.log2_theta = rope->log2_theta; args.H = rope->H;
+    args.Hkv = rope->Hkv; args.bs = rope->bs; args.kpool = rope->kpool;
+    args.vpool = rope->vpool; args.slots = rope->slots;
+    args.rope_tab = rope->tab; args.tab_len = rope->tab_len;
+  }
   dim3 grid(std::min(args.tiles, kNumSMs));
   {
     const cudaError_t le_ = launch(gemm_bf16_tcgen05, dim3(grid), dim3(G_THREADS), G_SMEM_BYTES, (cudaStream_t)stream,
@@ -566,4 +716,33 @@ extern "C" int swb_gemm_bf16_bias(const void* a, const void* w, void* out,
       return swb_set_error(SWB_ERR_CUDA, "launch gemm_bf16_tcgen05: %s", cudaGetErrorString(le_));
   }
   return swb_check_launch("gemm_bf16_tcgen05");
+}
+
+extern "C" int swb_rope_table(float theta, int max_pos, void* table, uintptr_t stream) {
+  SWB_REQUIRE(table && max_pos > 0 && theta > 1.f, "swb_rope_table: bad args");
+  const cudaError_t le = launch(rope_table_kernel, dim3((max_pos * 64 + 255) / 256), dim3(256), 0,
+                                (cudaStream_t)stream, log2f(theta), max_pos,
+                                reinterpret_cast<float2*>(table));
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch rope_table_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("rope_table_kernel");
+}
+
+extern "C" int swb_gemm_qkv_rope(const void* a, const void* w, void* qkv, const void* bias,
+                                 int M, int N, int K, const int32_t* positions, float theta,
+                                 const void* rope_table, int table_len, int H, int Hkv,
+                                 void* k_layer, void* v_layer, const int32_t* slots,
+                                 int block_size, uintptr_t stream) {
+  SWB_REQUIRE(a && w && qkv && positions, "swb_gemm_qkv_rope: null pointer");
+  SWB_REQUIRE(M > 0 && K > 0 && K % 8 == 0, "swb_gemm_qkv_rope: bad shape M=%d K=%d", M, K);
+  SWB_REQUIRE(H > 0 && Hkv > 0 && N == (H + 2 * Hkv) * 128,
+              "swb_gemm_qkv_rope: N=%d must be (H + 2 Hkv) * 128 (head_dim 128)", N);
+  SWB_REQUIRE(!slots || (k_layer && v_layer && block_size > 0),
+              "swb_gemm_qkv_rope: pool write needs k/v layers and block_size");
+  SWB_REQUIRE((((uintptr_t)a | (uintptr_t)w | (uintptr_t)qkv | (uintptr_t)bias) & 15) == 0,
+              "swb_gemm_qkv_rope: pointers must be 16-byte aligned");
+  RopeArgs r{positions, theta > 1.f ? log2f(theta) : 0.f, H, Hkv, block_size,
+             reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
+             slots, reinterpret_cast<const float2*>(rope_table), rope_table ? table_len : 0};
+  return gemm_launch(a, w, qkv, nullptr, bias, M, N, K, EPI_QKV_ROPE, (cudaStream_t)stream, &r);
 }

@@ -213,13 +213,8 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int row_stride,
     float ra[4], rb[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (log2_theta > 0.f) {
-        // inv_freq = theta^(-2i/dh)
-        const float inv_freq = exp2f(-log2_theta * (float)(2 * (i0 + j)) / (float)dh);
-        float s, c;
-        sincosf(pos * inv_freq, &s, &c);
-        ra[j] = a[j] * c - b[j] * s;
-        rb[j] = b[j] * c + a[j] * s;
+      if (log2_theta > 0.f) {   // inv_freq = theta^(-2i/dh)
+        rope_pair(a[j], b[j], i0 + j, pos, log2_theta, dh, ra[j], rb[j]);
       } else {  // no rotary embedding (ALiBi models): KV write only
         ra[j] = a[j];
         rb[j] = b[j];

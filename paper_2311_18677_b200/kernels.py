@@ -77,6 +77,27 @@ def gemv(x, w, epi=EPI_BF16, out=None, resid=None, bias=None):
     return out
 
 
+def gemm_qkv_rope(a, w, qkv, positions, H, Hkv, theta, bias=None, k_layer=None, v_layer=None,
+                  slots=None, block_size=16, rope_table=None):
+    """Prefill QKV projection with RoPE (+ KV write into the paged pool) fused
+    into the tcgen05 GEMM epilogue; bit-identical to gemm + rope_kv_write.
+    rope_table: fp32 [max_pos, 64, 2] from ``rope_table`` (optional)."""
+    _req(a, torch.bfloat16, "a")
+    M, Kd = a.shape
+    call("swb_gemm_qkv_rope", a.data_ptr(), w.data_ptr(), qkv.data_ptr(), _ptr(bias), M,
+         w.shape[0], Kd, positions.data_ptr(), float(theta), _ptr(rope_table),
+         0 if rope_table is None else rope_table.shape[0], H, Hkv, k_layer, v_layer,
+         _ptr(slots), block_size, _stream())
+    return qkv
+
+
+def rope_table(theta, max_pos, device=None):
+    """(sin, cos) of every RoPE angle for positions < max_pos, head_dim 128."""
+    t = torch.empty(max_pos, 64, 2, dtype=torch.float32, device=device or "cuda")
+    call("swb_rope_table", float(theta), max_pos, t.data_ptr(), _stream())
+    return t
+
+
 def gemv_rmsnorm(x, norm_w, eps, w, epi=EPI_BF16, out=None, resid=None):
     """Decode pre-norm linear: out = epi(rmsnorm(x fp32) @ w^T), one kernel."""
     _req(x, torch.float32, "x")

@@ -77,6 +77,9 @@ class ModelRunner:
         self._cap = 0
         self.push_stream = torch.cuda.Stream(device=self.dev)
         self.graphs: dict = {}
+        # RoPE angle table for the fused QKV-GEMM epilogue (16K positions, 8 MB)
+        self.rope_tab = (K.rope_table(cfg.rope_theta, 16384, device=self.dev)
+                         if not self.bloom and self.dh == 128 else None)
 
     # ------------------------------------------------------------ helpers
     def _allreduce(self, x):
@@ -198,13 +201,24 @@ class ModelRunner:
             if push and li >= 2:
                 main.wait_event(push_events[li - 2])  # qkv buffer reuse
             self._norm(x, lw.attn_norm, lw.attn_norm_b, out=h)
-            K.linear(h, lw.wqkv, K.EPI_BF16, out=qkv, bias=lw.bqkv)
-            if local_slots is not None and self.kv is not None:
-                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, self.theta,
-                                self.kv.k_layer_ptr(li), self.kv.v_layer_ptr(li), local_slots,
-                                self.kv.block_size)
-            elif not self.bloom:
-                K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, self.theta)
+            local = local_slots is not None and self.kv is not None
+            if T > K.GEMV_MAX_ROWS and self.dh == 128:
+                # RoPE (+ KV write into this GPU's pages) fused into the GEMM epilogue
+                K.gemm_qkv_rope(h, lw.wqkv, qkv, positions, self.hq, self.hkv, self.theta,
+                                bias=lw.bqkv,
+                                k_layer=self.kv.k_layer_ptr(li) if local else None,
+                                v_layer=self.kv.v_layer_ptr(li) if local else None,
+                                slots=local_slots if local else None,
+                                block_size=self.kv.block_size if local else 16,
+                                rope_table=self.rope_tab)
+            else:
+                K.linear(h, lw.wqkv, K.EPI_BF16, out=qkv, bias=lw.bqkv)
+                if local:
+                    K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, self.theta,
+                                    self.kv.k_layer_ptr(li), self.kv.v_layer_ptr(li),
+                                    local_slots, self.kv.block_size)
+                elif not self.bloom:
+                    K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, self.theta)
             if push:
                 ev = torch.cuda.Event()
                 ev.record(main)

@@ -509,3 +509,31 @@ def test_attn_decode_step_large_batch(K, alibi):
             s = s + slopes[:, None] * (p[None, :] - cached[b]).float()
         ref = torch.einsum("hl,lhd->hd", s.softmax(-1), v)
         assert _rel(out[b].view(H, dh), ref) < 1e-2, b
+
+
+@pytest.mark.parametrize("M,bias,theta", [(100, False, 10000.0), (300, False, 10000.0),
+                                          (300, True, 0.0), (1024, False, 500000.0)])
+def test_gemm_qkv_rope_equals_gemm_then_rope(K, M, bias, theta):
+    """The fused QKV-GEMM epilogue (RoPE + paged KV write) is bit-identical to
+    the GEMM followed by swb_rope_kv_write: stored qkv and pool pages."""
+    H, Hkv, dh, bs, d = 8, 2, 128, 16, 1024
+    N = (H + 2 * Hkv) * dh
+    a = torch.randn(M, d, device="cuda").bfloat16()
+    w = (torch.randn(N, d, device="cuda") * 0.05).bfloat16()
+    b = (torch.randn(N, device="cuda") * 0.1).bfloat16() if bias else None
+    pos = torch.randint(0, 4000, (M,), device="cuda", dtype=torch.int32)
+    nblk = (M + bs - 1) // bs + 4
+    slots = torch.randperm(nblk * bs, device="cuda")[:M].int()
+    k1 = torch.zeros(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    v1, k2, v2 = k1.clone(), k1.clone(), k1.clone()
+    ref = K.gemm(a, w, K.EPI_BF16, bias=b)
+    K.rope_kv_write(ref, pos, H, Hkv, dh, theta, k1.data_ptr(), v1.data_ptr(), slots, bs)
+    for tab in (None, K.rope_table(theta, 2048) if theta > 1 else None):
+        got = torch.empty_like(ref)
+        k2.zero_(); v2.zero_()
+        K.gemm_qkv_rope(a, w, got, pos, H, Hkv, theta, bias=b, k_layer=k2.data_ptr(),
+                        v_layer=v2.data_ptr(), slots=slots, block_size=bs, rope_table=tab)
+        torch.cuda.synchronize()   # positions >= 2048 fall back to computing the angles
+        assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+        assert torch.equal(k2.view(torch.int16), k1.view(torch.int16))
+        assert torch.equal(v2.view(torch.int16), v1.view(torch.int16))

@@ -223,6 +223,21 @@ int swb_attn_decode_step(const void* qkv, int row_stride, void* k_layer,
                          int partition, void* workspace, void* out,
                          uintptr_t stream);
 
+/* Chunked prefill attention: rows [0, C) of qkv are the queries of prompt
+ * positions q_start .. q_start+C-1 (already RoPE'd; their K/V already in the
+ * pool, e.g. by swb_gemm_qkv_rope with slots), keys are read through
+ * table_row for positions <= each query's own (causal).  out bf16 [C, H*128].
+ * workspace: swb_attn_chunk_workspace(C, H, max_ctx) bytes, zeroed once.
+ * Lets a long prompt be prefilled in chunks (mixed with decode rows per
+ * iteration) instead of one batch — the chunked-prefill option of
+ * SURVEY §8(f); reference prompt batching machine.py:186-203. */
+size_t swb_attn_chunk_workspace(int C, int H, int max_ctx);
+int swb_attn_chunk(const void* qkv, int row_stride, int C, int q_start,
+                   const void* k_layer, const void* v_layer,
+                   const int32_t* table_row, int H, int Hkv, int dh,
+                   int block_size, float scale, const float* alibi_slopes,
+                   int max_ctx, void* workspace, void* out, uintptr_t stream);
+
 /* --------------------------------------------- decode-step bookkeeping
  * Graph-resident per-step state update so the decode loop needs no host
  * round trip (Machine.complete_iteration, machine.py:247-275):

@@ -63,6 +63,8 @@ SIGNATURES = {
     "swb_attn_prefill": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],
     "swb_attn_prefill_tc": [_P, _I, _I, _P, _I, _I, _I, _I, _I, _F, _P, _P, _ST],
     "swb_attn_decode_workspace": [_I, _I, _I, _I, _I],
+    "swb_attn_chunk_workspace": [_I, _I, _I],
+    "swb_attn_chunk": [_P, _I, _I, _I, _P, _P, _P, _I, _I, _I, _I, _F, _P, _I, _P, _P, _ST],
     "swb_attn_decode": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _F, _P, _I, _I, _I, _I, _I, _F,
                         _I, _I, _P, _P, _ST],
     "swb_attn_decode_step": [_P, _I, _P, _P, _P, _I, _P, _F, _P, _I, _I, _I, _I, _I, _F, _I,
@@ -85,6 +87,7 @@ SIGNATURES = {
     "swb_tp_allreduce_f32": [_P, _I, _P, _S, _ST],
 }
 _RESTYPE = {"swb_last_error": C.c_char_p, "swb_attn_decode_workspace": _S,
+            "swb_attn_chunk_workspace": _S,
             "swb_tp_comm_slot": _P}
 
 
@@ -127,7 +130,7 @@ LAUNCH_MULT = {
     "swb_gemm_qkv_rope": 1, "swb_rope_table": 1,
     "swb_layernorm": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
     "swb_argmax": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
-    "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1,
+    "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1, "swb_attn_chunk": 1,
     "swb_decode_prepare": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
     "swb_block_free": 1, "swb_tp_allreduce_f32": 1,

@@ -916,6 +916,274 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
                out + (size_t)b * H * DA_D, DM_WARPS * 32);
 }
 
+// ---------------------------------------------------------------- chunked prefill
+// Causal attention of a prompt CHUNK whose keys live in the paged pool (the
+// chunk's own K/V were written there by the QKV GEMM epilogue, earlier chunks'
+// by earlier calls): CTA (key partition p, head h, 16-query tile t) computes
+// S = Q_t . K_p^T and O = P . V_p with mma.sync exactly like the decode MMA
+// kernel, but the 16 A-tile rows are 16 consecutive query positions of one
+// head, each with its own causal bound; partitions merge per row through the
+// workspace (last CTA of (h, t), fixed order).
+template <int DUMMY>
+__global__ void __launch_bounds__(DM_WARPS * 32)
+    attn_chunk_kernel(const __nv_bfloat16* __restrict__ qkv, int rs, int C, int q_start,
+                      const __nv_bfloat16* __restrict__ kpool,
+                      const __nv_bfloat16* __restrict__ vpool, const int32_t* __restrict__ trow,
+                      int H, int Hkv, float scale_log2, const float* __restrict__ alibi,
+                      float* __restrict__ ws, int* __restrict__ tickets,
+                      __nv_bfloat16* __restrict__ out) {
+  constexpr int BS = 16;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(dsm);          // [128][128]
+  __nv_bfloat16* sv = sk + DM_PT * DA_D;                               // [128][128]
+  __nv_bfloat16* sq = sv + DM_PT * DA_D;                               // [16][DM_QS]
+  float* sml = reinterpret_cast<float*>(sq + 16 * DM_QS);              // [4][16][2]
+  float* so = sml + DM_WARPS * 16 * 2;                                 // [4][16][128]
+  __shared__ uint64_t kbar[DM_WARPS], vbar[DM_WARPS];
+  __shared__ int s_last;
+  const int p = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
+  const int NP = gridDim.x;
+  const int kh = h / (H / Hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = qt * 16;                                  // first chunk row of the tile
+  const int nrows = min(16, C - r0);
+  const int qmax = q_start + r0 + nrows - 1;               // last query position
+  const int t0 = p * DM_PT;
+  const int L = qmax + 1;                                  // keys this tile may see
+  const int t1 = min(L, t0 + DM_PT);
+  const int ntok = t1 - t0;
+  // partial of (row, partition): ws[((h * nq + qt) * 16 + row) * NP + p][DA_D + 2]
+  const int nq = gridDim.z;
+  auto wsp = [&](int row, int pp) {
+    return ws + ((((size_t)h * nq + qt) * 16 + row) * NP + pp) * (DA_D + 2);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < DM_WARPS; ++i) {
+      mbar_init(&kbar[i], 1);
+      mbar_init(&vbar[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();          // the chunk's K/V pages and q come from the QKV GEMM
+  if (warp == 0 && ntok > 0) {
+    const int nblk = (ntok + BS - 1) / BS;
+    constexpr uint32_t tile = BS * DA_D * 2;
+    if (lane < DM_WARPS) {
+      const int np = min(max(nblk - 2 * lane, 0), 2);
+      mbar_arrive_expect_tx(&kbar[lane], tile * np);
+      mbar_arrive_expect_tx(&vbar[lane], tile * np);
+    }
+    __syncwarp();
+    if (lane < nblk) {
+      const int blk = __ldg(trow + t0 / BS + lane);
+      const size_t gofs = ((size_t)blk * Hkv + kh) * BS * DA_D;
+      bulk_g2s(sk + (size_t)lane * BS * DA_D, kpool + gofs, tile, &kbar[lane >> 1]);
+      bulk_g2s(sv + (size_t)lane * BS * DA_D, vpool + gofs, tile, &vbar[lane >> 1]);
+    }
+  }
+  if (ntok > 0) {
+    // q tile: 16 consecutive query rows of head h (already RoPE'd), rows past C zero
+    for (int i = threadIdx.x; i < 16 * (DA_D / 8); i += DM_WARPS * 32) {
+      const int rr = i / (DA_D / 8), c8 = (i % (DA_D / 8)) * 8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (rr < nrows) v = *reinterpret_cast<const uint4*>(qkv + (size_t)(r0 + rr) * rs + h * DA_D + c8);
+      *reinterpret_cast<uint4*>(sq + rr * DM_QS + c8) = v;
+    }
+    __syncthreads();
+    const int wt0 = warp * DM_WT;
+    if (wt0 < ntok) {
+      mbar_wait(&kbar[warp], 0);
+      float s[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      const uint32_t sq_u = smem_u32(sq), sk_u = smem_u32(sk), sv_u = smem_u32(sv);
+#pragma unroll
+      for (int kk = 0; kk < DA_D / 16; ++kk) {
+        uint32_t qf[4];
+        ldsm_x4(sq_u + ((lane & 15) * DM_QS + (kk * 2 + (lane >> 4)) * 8) * 2, qf[0], qf[1],
+                qf[2], qf[3]);
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+          const int key = wt0 + np * 16 + (lane & 7) + ((lane >> 4) << 3);
+          const int chunk = kk * 2 + ((lane >> 3) & 1);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(sk_u + (key * DA_D + chunk * 8) * 2, b0, b1, b2, b3);
+          mma_bf16(s[2 * np], qf, b0, b1);
+          mma_bf16(s[2 * np + 1], qf, b2, b3);
+        }
+      }
+      // rows g (c0,c1) and g+8 (c2,c3): query positions q_start + r0 + row
+      const float sl = alibi ? alibi[h] * 1.4426950408889634f : 0.f;
+      float m[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int row = g + 8 * hr;
+        const int qpos = q_start + r0 + row;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int tok = wt0 + nt * 8 + 2 * t + e;
+            const int kpos = t0 + tok;
+            const float v = (tok < ntok && kpos <= qpos && row < nrows)
+                                ? fmaf(sl, (float)(kpos - qpos), s[nt][2 * hr + e] * scale_log2)
+                                : -INFINITY;
+            s[nt][2 * hr + e] = v;
+            m[hr] = fmaxf(m[hr], v);
+          }
+        m[hr] = fmaxf(m[hr], __shfl_xor_sync(0xffffffffu, m[hr], 1));
+        m[hr] = fmaxf(m[hr], __shfl_xor_sync(0xffffffffu, m[hr], 2));
+      }
+      float l[2] = {0.f, 0.f};
+      uint32_t pf[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        float e0 = m[0] == -INFINITY ? 0.f : exp2f(s[nt][0] - m[0]);
+        float e1 = m[0] == -INFINITY ? 0.f : exp2f(s[nt][1] - m[0]);
+        float e2 = m[1] == -INFINITY ? 0.f : exp2f(s[nt][2] - m[1]);
+        float e3 = m[1] == -INFINITY ? 0.f : exp2f(s[nt][3] - m[1]);
+        l[0] += e0 + e1;
+        l[1] += e2 + e3;
+        const uint32_t pk0 = f2_to_bf2(e0, e1), pk1 = f2_to_bf2(e2, e3);
+        if ((nt & 1) == 0) {
+          pf[nt >> 1][0] = pk0;
+          pf[nt >> 1][1] = pk1;
+        } else {
+          pf[nt >> 1][2] = pk0;
+          pf[nt >> 1][3] = pk1;
+        }
+      }
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        l[hr] += __shfl_xor_sync(0xffffffffu, l[hr], 1);
+        l[hr] += __shfl_xor_sync(0xffffffffu, l[hr], 2);
+      }
+      mbar_wait(&vbar[warp], 0);
+      for (int i = max(ntok - wt0, 0) * 16 + lane; i < DM_WT * 16; i += 32)
+        reinterpret_cast<uint4*>(sv + (size_t)wt0 * DA_D)[i] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      float o[16][4];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+        for (int dp = 0; dp < 8; ++dp) {
+          const int key = wt0 + ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+          const int chunk = dp * 2 + (lane >> 4);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(sv_u + (key * DA_D + chunk * 8) * 2, b0, b1, b2, b3);
+          mma_bf16(o[2 * dp], pf[ks], b0, b1);
+          mma_bf16(o[2 * dp + 1], pf[ks], b2, b3);
+        }
+      }
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int row = g + 8 * hr;
+        float* dst = so + ((size_t)warp * 16 + row) * DA_D;
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(dst + nt * 8 + 2 * t) =
+              make_float2(o[nt][2 * hr], o[nt][2 * hr + 1]);
+        if (t == 0) {
+          sml[(warp * 16 + row) * 2] = m[hr];
+          sml[(warp * 16 + row) * 2 + 1] = l[hr];
+        }
+      }
+    } else if (t == 0) {
+      sml[(warp * 16 + g) * 2] = -INFINITY;
+      sml[(warp * 16 + g) * 2 + 1] = 0.f;
+      sml[(warp * 16 + g + 8) * 2] = -INFINITY;
+      sml[(warp * 16 + g + 8) * 2 + 1] = 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 16 * DA_D; i += DM_WARPS * 32) {
+      const int row = i / DA_D, d = i % DA_D;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < DM_WARPS; ++w) M = fmaxf(M, sml[(w * 16 + row) * 2]);
+      float o = 0.f, l = 0.f;
+#pragma unroll
+      for (int w = 0; w < DM_WARPS; ++w) {
+        const float mw = sml[(w * 16 + row) * 2];
+        if (mw == -INFINITY) continue;
+        const float f = exp2f(mw - M);
+        o += f * so[((size_t)w * 16 + row) * DA_D + d];
+        l += f * sml[(w * 16 + row) * 2 + 1];
+      }
+      float* wo = wsp(row, p);
+      wo[d] = o;
+      if (d == 0) {
+        wo[DA_D] = M;
+        wo[DA_D + 1] = l;
+      }
+    }
+  } else {
+    for (int row = threadIdx.x; row < 16; row += DM_WARPS * 32) {
+      float* w = wsp(row, p);
+      w[DA_D] = -INFINITY;
+      w[DA_D + 1] = 0.f;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* tk = tickets + (size_t)h * nq + qt;
+    const int prev = atomicAdd(tk, 1);
+    s_last = prev == NP - 1;
+    if (s_last) *tk = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // merge the partitions of the tile's rows (rows = "heads" of decode_merge)
+  // with out row stride H * DA_D: write through a [16][H*128] view
+  float* sf = reinterpret_cast<float*>(dsm);
+  const int tid = threadIdx.x;
+  const float* base = ws + (((size_t)h * nq + qt) * 16) * NP * (DA_D + 2);
+  for (int i = tid; i < 16 * NP; i += DM_WARPS * 32) {
+    const int row = i / NP, pp = i % NP;
+    const float* w = base + ((size_t)row * NP + pp) * (DA_D + 2);
+    sf[i] = __ldcg(w + DA_D);
+    sf[16 * NP + 16 + i] = __ldcg(w + DA_D + 1);
+  }
+  __syncthreads();
+  for (int row = warp; row < 16; row += DM_WARPS) {
+    float M = -INFINITY;
+    for (int pp = lane; pp < NP; pp += 32) M = fmaxf(M, sf[row * NP + pp]);
+    M = warp_max(M);
+    float Ls = 0.f;
+    for (int pp = lane; pp < NP; pp += 32) {
+      const float mm = sf[row * NP + pp];
+      const float f = mm == -INFINITY ? 0.f : exp2f(mm - M);
+      Ls += f * sf[16 * NP + 16 + row * NP + pp];
+      sf[row * NP + pp] = f;
+    }
+    Ls = warp_sum(Ls);
+    if (lane == 0) sf[16 * NP + row] = Ls;
+  }
+  __syncthreads();
+  for (int i = tid; i < nrows * (DA_D / 4); i += DM_WARPS * 32) {
+    const int row = i / (DA_D / 4), d4 = i % (DA_D / 4);
+    const float* b = base + (size_t)row * NP * (DA_D + 2) + d4 * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int pp = 0; pp < NP; ++pp) {
+      const float f = sf[row * NP + pp];
+      const float2 x0 = __ldcg(reinterpret_cast<const float2*>(b + (size_t)pp * (DA_D + 2)));
+      const float2 x1 = __ldcg(reinterpret_cast<const float2*>(b + (size_t)pp * (DA_D + 2) + 2));
+      acc.x = fmaf(f, x0.x, acc.x); acc.y = fmaf(f, x0.y, acc.y);
+      acc.z = fmaf(f, x1.x, acc.z); acc.w = fmaf(f, x1.y, acc.w);
+    }
+    const float inv = 1.f / sf[16 * NP + row];
+    __nv_bfloat16* dst = out + (size_t)(r0 + row) * H * DA_D + h * DA_D + d4 * 4;
+    *reinterpret_cast<uint2*>(dst) = make_uint2(f2_to_bf2(acc.x * inv, acc.y * inv),
+                                                f2_to_bf2(acc.z * inv, acc.w * inv));
+  }
+}
+
 }  // namespace swb
 
 using namespace swb;
@@ -1071,4 +1339,51 @@ extern "C" int swb_attn_decode_step(const void* qkv, int row_stride, void* k_lay
                                   ctx, nullptr, nullptr, theta, alibi_slopes, B, H, Hkv, dh,
                                   block_size, scale, max_ctx, partition, workspace, out, stream,
                                   "swb_attn_decode_step");
+}
+
+extern "C" size_t swb_attn_chunk_workspace(int C, int H, int max_ctx) {
+  if (C <= 0 || H <= 0 || max_ctx <= 0) return 0;
+  const size_t nq = (C + 15) / 16, np = (max_ctx + DM_PT - 1) / DM_PT;
+  return (size_t)H * nq * 16 * np * (DA_D + 2) * sizeof(float) + (size_t)H * nq * sizeof(int);
+}
+
+extern "C" int swb_attn_chunk(const void* qkv, int row_stride, int C, int q_start,
+                              const void* k_layer, const void* v_layer, const int32_t* table_row,
+                              int H, int Hkv, int dh, int block_size, float scale,
+                              const float* alibi_slopes, int max_ctx, void* workspace, void* out,
+                              uintptr_t stream) {
+  SWB_REQUIRE(qkv && k_layer && v_layer && table_row && workspace && out,
+              "swb_attn_chunk: null pointer");
+  SWB_REQUIRE(dh == DA_D && block_size == 16, "swb_attn_chunk: dh 128 and block_size 16 only");
+  SWB_REQUIRE(H > 0 && Hkv > 0 && H % Hkv == 0, "swb_attn_chunk: bad heads");
+  SWB_REQUIRE(C > 0 && q_start >= 0 && q_start + C <= max_ctx, "swb_attn_chunk: bad chunk");
+  SWB_REQUIRE(row_stride % 8 == 0, "swb_attn_chunk: row_stride %% 8");
+  const int nq = (C + 15) / 16;
+  const int NP = (q_start + C + DM_PT - 1) / DM_PT;          // partitions the chunk can see
+  const int NPmax = (max_ctx + DM_PT - 1) / DM_PT;
+  const size_t smem = std::max((size_t)2 * DM_PT * DA_D * 2 + 16 * DM_QS * 2 +
+                                   sizeof(float) * (DM_WARPS * 16 * 2 + (size_t)DM_WARPS * 16 * DA_D),
+                               sizeof(float) * (2 * 16 * (size_t)NP + 16));
+  static bool attr[64] = {false};
+  int dev = 0;
+  SWB_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !attr[dev]) {
+    SWB_CUDA(cudaFuncSetAttribute(attn_chunk_kernel<0>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    attr[dev] = true;
+  }
+  SWB_REQUIRE(smem <= 160 * 1024, "swb_attn_chunk: context too long");
+  float* ws = reinterpret_cast<float*>(workspace);
+  int* tickets = reinterpret_cast<int*>(ws + (size_t)H * nq * 16 * NPmax * (DA_D + 2));
+  (void)NPmax;
+  const cudaError_t le = launch(
+      attn_chunk_kernel<0>, dim3(NP, H, nq), dim3(DM_WARPS * 32), smem, (cudaStream_t)stream,
+      reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride, C, q_start,
+      reinterpret_cast<const __nv_bfloat16*>(k_layer),
+      reinterpret_cast<const __nv_bfloat16*>(v_layer), table_row, H, Hkv,
+      scale * 1.4426950408889634f, alibi_slopes, ws, tickets,
+      reinterpret_cast<__nv_bfloat16*>(out));
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch attn_chunk_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("attn_chunk_kernel");
 }

@@ -244,6 +244,19 @@ def attn_decode_step(qkv, k_layer, v_layer, block_tables, ctx, B, H, Hkv, dh, bl
     return out
 
 
+def attn_chunk_workspace_bytes(C, H, max_ctx):
+    return int(_abi.lib.swb_attn_chunk_workspace(C, H, max_ctx))
+
+
+def attn_chunk(qkv, C, q_start, k_layer, v_layer, table_row_ptr, H, Hkv, dh, block_size, scale,
+               max_ctx, workspace, out, alibi=None):
+    """Causal attention of a prompt chunk (positions q_start..) over the paged pool."""
+    call("swb_attn_chunk", qkv.data_ptr(), qkv.shape[1], C, q_start, k_layer, v_layer,
+         table_row_ptr, H, Hkv, dh, block_size, float(scale), _ptr(alibi), max_ctx,
+         workspace.data_ptr(), out.data_ptr(), _stream())
+    return out
+
+
 def decode_prepare(ctx, block_tables, block_size, B, pos, slots, attn_len):
     call("swb_decode_prepare", ctx.data_ptr(), block_tables.data_ptr(), block_tables.shape[1],
          block_size, B, pos.data_ptr(), slots.data_ptr(), attn_len.data_ptr(), _stream())

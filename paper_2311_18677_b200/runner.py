@@ -317,6 +317,55 @@ class ModelRunner:
         dec_ctx += 1
         return nxt
 
+    def prefill_chunked(self, tokens: torch.Tensor, seq: int, chunk: int = 512) -> torch.Tensor:
+        """Prompt phase of ONE prompt in chunks of ``chunk`` tokens against this
+        GPU's pool (sequence slot ``seq``): every chunk's QKV GEMM rotates and
+        writes its K/V into the pages (fused epilogue), then the chunk's
+        queries attend over all pages up to their own position
+        (swb_attn_chunk).  Same result as ``prefill`` with local slots (within
+        bf16 rounding); bounds the rows per iteration so a long prompt can
+        share iterations with decode rows.  Returns the first token (int32 [1])."""
+        cfg, w, kv = self.cfg, self.w, self.kv
+        P = int(tokens.shape[0])
+        self._ensure_prefill(min(P, chunk), 1)
+        slots = torch.empty(P, dtype=torch.int32, device=self.dev)
+        K.slots_from_table(kv.table_row_ptr(seq), 0, P, kv.block_size, slots)
+        max_ctx = kv.max_blocks_per_seq * kv.block_size
+        key = ("chunk_ws", chunk, max_ctx)
+        ws = self.graphs.get(key)
+        if ws is None:
+            ws = torch.zeros(K.attn_chunk_workspace_bytes(chunk, self.hq, max_ctx),
+                             dtype=torch.uint8, device=self.dev)
+            self.graphs[key] = ws
+        self._begin_reductions()
+        for c0 in range(0, P, chunk):
+            n = min(chunk, P - c0)
+            x, h, attn, act = self.px[:n], self.ph[:n], self.pattn[:n], self.pact[:n]
+            qkv = self.pqkv[0][:n]
+            positions = torch.arange(c0, c0 + n, dtype=torch.int32, device=self.dev)
+            self._embed(tokens[c0:c0 + n], x)
+            for li, lw in enumerate(w.layers):
+                self._norm(x, lw.attn_norm, lw.attn_norm_b, out=h)
+                K.gemm_qkv_rope(h, lw.wqkv, qkv, positions, self.hq, self.hkv, self.theta,
+                                bias=lw.bqkv, k_layer=kv.k_layer_ptr(li),
+                                v_layer=kv.v_layer_ptr(li), slots=slots[c0:c0 + n],
+                                block_size=kv.block_size, rope_table=self.rope_tab)
+                K.attn_chunk(qkv, n, c0, kv.k_layer_ptr(li), kv.v_layer_ptr(li),
+                             kv.table_row_ptr(seq), self.hq, self.hkv, self.dh, kv.block_size,
+                             self.scale, max_ctx, ws, attn, alibi=self.alibi)
+                self._proj_reduce(attn, lw.wo, x, lw.bo)
+                self._norm(x, lw.mlp_norm, lw.mlp_norm_b, out=h)
+                self._mlp_up(h, lw, act)
+                self._proj_reduce(act, lw.wd, x, lw.bd)
+        last = self.plast[:1]
+        idx = torch.tensor([n - 1], dtype=torch.int32, device=self.dev)
+        self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=idx)
+        logits = self.plogits[:1]
+        K.linear(last, w.lm_head, K.EPI_F32, out=logits)
+        first = self.pfirst[:1]
+        K.argmax(logits, out=first)
+        return first
+
     def finish_push_stats(self):
         """Resolve push timings after the prefill's events completed."""
         if not getattr(self, "_push_timing", None):

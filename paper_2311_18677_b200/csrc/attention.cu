@@ -1375,7 +1375,6 @@ extern "C" int swb_attn_chunk(const void* qkv, int row_stride, int C, int q_star
   SWB_REQUIRE(smem <= 160 * 1024, "swb_attn_chunk: context too long");
   float* ws = reinterpret_cast<float*>(workspace);
   int* tickets = reinterpret_cast<int*>(ws + (size_t)H * nq * 16 * NPmax * (DA_D + 2));
-  (void)NPmax;
   const cudaError_t le = launch(
       attn_chunk_kernel<0>, dim3(NP, H, nq), dim3(DM_WARPS * 32), smem, (cudaStream_t)stream,
       reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride, C, q_start,

@@ -345,8 +345,9 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
                         gaps2.append(g_[0])
                 bpl, lms, tail = gathered[pr]["push"]
                 push_gbs.append(statistics.mean(kv_push_gbps(bpl, m) for m in lms))
-                push_tail.append(tail)
-                push_raw.append(sum(lms))
+                plan = measured_plan(LAYERWISE, lms, tail)   # reference TransferPlan record
+                push_tail.append(plan.visible_latency)
+                push_raw.append(plan.raw_time)
         dev_ms = []
         for _ in range(args.steps):
             dev_ms.append(one_step(True)[2])
@@ -359,8 +360,6 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         pairs = world // (2 * tp)
         toks_step = pairs * R * O
         ms = statistics.mean(dev_ms)
-        plan = measured_plan(LAYERWISE, [0.0], 0.0)
-        _ = plan
         line = {
             "metric": "output tokens/s (+ TTFT/TBT p50,p99) serving "
                       f"{P}/{O} requests, {cfg.name}",

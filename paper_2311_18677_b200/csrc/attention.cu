@@ -637,6 +637,7 @@ __global__ void __launch_bounds__(NW * 32)
 // later pages are still landing; warps combine (max, sum, O) through shared
 // memory, partitions through the fused split-K merge.
 constexpr int DM_WARPS = 4, DM_PT = 128, DM_WT = 32, DM_QS = DA_D + 8;
+constexpr int DC_MAXQT = 512;     // chunked prefill: up to 8192 query rows per chunk
 
 template <bool STEP>
 __global__ void __launch_bounds__(DM_WARPS * 32)
@@ -1130,7 +1131,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    int* tk = tickets + (size_t)h * nq + qt;
+    int* tk = tickets + (size_t)h * DC_MAXQT + qt;
     const int prev = atomicAdd(tk, 1);
     s_last = prev == NP - 1;
     if (s_last) *tk = 0;
@@ -1341,10 +1342,13 @@ extern "C" int swb_attn_decode_step(const void* qkv, int row_stride, void* k_lay
                                   "swb_attn_decode_step");
 }
 
+// workspace: merge tickets [H][DC_MAXQT] ints first (fixed offsets, so calls
+// with different chunk lengths share one zeroed workspace), then the partials
 extern "C" size_t swb_attn_chunk_workspace(int C, int H, int max_ctx) {
   if (C <= 0 || H <= 0 || max_ctx <= 0) return 0;
   const size_t nq = (C + 15) / 16, np = (max_ctx + DM_PT - 1) / DM_PT;
-  return (size_t)H * nq * 16 * np * (DA_D + 2) * sizeof(float) + (size_t)H * nq * sizeof(int);
+  return (size_t)H * DC_MAXQT * sizeof(int) +
+         (size_t)H * nq * 16 * np * (DA_D + 2) * sizeof(float);
 }
 
 extern "C" int swb_attn_chunk(const void* qkv, int row_stride, int C, int q_start,
@@ -1360,7 +1364,6 @@ extern "C" int swb_attn_chunk(const void* qkv, int row_stride, int C, int q_star
   SWB_REQUIRE(row_stride % 8 == 0, "swb_attn_chunk: row_stride %% 8");
   const int nq = (C + 15) / 16;
   const int NP = (q_start + C + DM_PT - 1) / DM_PT;          // partitions the chunk can see
-  const int NPmax = (max_ctx + DM_PT - 1) / DM_PT;
   const size_t smem = std::max((size_t)2 * DM_PT * DA_D * 2 + 16 * DM_QS * 2 +
                                    sizeof(float) * (DM_WARPS * 16 * 2 + (size_t)DM_WARPS * 16 * DA_D),
                                sizeof(float) * (2 * 16 * (size_t)NP + 16));
@@ -1373,8 +1376,9 @@ extern "C" int swb_attn_chunk(const void* qkv, int row_stride, int C, int q_star
     attr[dev] = true;
   }
   SWB_REQUIRE(smem <= 160 * 1024, "swb_attn_chunk: context too long");
-  float* ws = reinterpret_cast<float*>(workspace);
-  int* tickets = reinterpret_cast<int*>(ws + (size_t)H * nq * 16 * NPmax * (DA_D + 2));
+  SWB_REQUIRE(nq <= DC_MAXQT, "swb_attn_chunk: C=%d > %d rows", C, 16 * DC_MAXQT);
+  int* tickets = reinterpret_cast<int*>(workspace);
+  float* ws = reinterpret_cast<float*>(tickets + (size_t)H * DC_MAXQT);
   const cudaError_t le = launch(
       attn_chunk_kernel<0>, dim3(NP, H, nq), dim3(DM_WARPS * 32), smem, (cudaStream_t)stream,
       reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride, C, q_start,

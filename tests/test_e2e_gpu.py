@@ -231,7 +231,10 @@ def test_chunked_prefill_matches_full_prefill(model, P, chunk):
         p = torch.arange(P, device="cuda")
         res[mode] = (int(first[0]), r.plogits[0].clone(),
                      kv.k_view(cfg.n_layers - 1)[tb[p // 16], :, p % 16].float().clone())
-    assert res["full"][0] == res["chunked"][0]
     lf, lc = res["full"][1], res["chunked"][1]
-    assert (lf - lc).abs().max().item() <= 0.03 + 0.02 * lf.abs().max().item()
+    d = (lf - lc).abs().max().item()
+    assert d <= 0.03 + 0.02 * lf.abs().max().item(), d
+    top2 = lf.topk(2).values
+    if (top2[0] - top2[1]).item() > 2 * d:       # greedy ids must agree unless a near-tie
+        assert res["full"][0] == res["chunked"][0]
     assert (res["full"][2] - res["chunked"][2]).abs().max().item() < 0.1

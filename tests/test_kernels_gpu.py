@@ -537,3 +537,35 @@ def test_gemm_qkv_rope_equals_gemm_then_rope(K, M, bias, theta):
         assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
         assert torch.equal(k2.view(torch.int16), k1.view(torch.int16))
         assert torch.equal(v2.view(torch.int16), v1.view(torch.int16))
+
+
+@pytest.mark.parametrize("H,Hkv,C,q0", [(4, 2, 64, 64), (4, 2, 64, 192), (4, 2, 1, 256),
+                                        (4, 2, 44, 256), (8, 8, 128, 0), (32, 4, 100, 900)])
+def test_attn_chunk_against_torch(K, H, Hkv, C, q0):
+    """Chunk attention over the paged pool (keys 0..q0+C-1, causal per query
+    row) against a torch fp32 reference."""
+    dh, bs = 128, 16
+    L = q0 + C
+    maxb = (L + bs - 1) // bs + 2
+    nblk = maxb + 4
+    kp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    vp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    table = torch.randperm(nblk, device="cuda").int()[:maxb].contiguous()
+    qkv = torch.randn(C, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    max_ctx = maxb * bs
+    ws = torch.zeros(K.attn_chunk_workspace_bytes(C, H, max_ctx), dtype=torch.uint8, device="cuda")
+    out = torch.empty(C, H * dh, dtype=torch.bfloat16, device="cuda")
+    for _ in range(2):   # tickets self-reset
+        K.attn_chunk(qkv, C, q0, kp.data_ptr(), vp.data_ptr(), table.data_ptr(), H, Hkv, dh, bs,
+                     1 / math.sqrt(dh), max_ctx, ws, out)
+    torch.cuda.synchronize()
+    p = torch.arange(L, device="cuda")
+    blk = table[p // bs].long()
+    k = kp[blk, :, p % bs].float().repeat_interleave(H // Hkv, 1)    # [L, H, dh]
+    v = vp[blk, :, p % bs].float().repeat_interleave(H // Hkv, 1)
+    q = qkv[:, :H * dh].view(C, H, dh).float()
+    s = torch.einsum("qhd,khd->hqk", q, k) / math.sqrt(dh)
+    qpos = torch.arange(q0, q0 + C, device="cuda")
+    s = s.masked_fill(p[None, None, :] > qpos[None, :, None], float("-inf"))
+    ref = torch.einsum("hqk,khd->qhd", s.softmax(-1), v)
+    assert _rel(out.view(C, H, dh), ref) < 1e-2

@@ -238,6 +238,17 @@ int swb_attn_chunk(const void* qkv, int row_stride, int C, int q_start,
                    int block_size, float scale, const float* alibi_slopes,
                    int max_ctx, void* workspace, void* out, uintptr_t stream);
 
+/* Vocab-parallel greedy pick for TP pools (the LM head split by vocabulary
+ * rows): swb_argmax_shard writes each row's (max logit, global index =
+ * local argmax + offset) into slot `rank` of cand fp32 [rows][tp][2] and
+ * zeros into the other slots; after the pool's sum all-reduce of cand,
+ * swb_argmax_pick returns the index of the largest candidate (lowest index
+ * on ties) — equal to swb_argmax over the full vocabulary. */
+int swb_argmax_shard(const float* logits, int rows, int V, int offset, int rank,
+                     int tp, float* cand, uintptr_t stream);
+int swb_argmax_pick(const float* cand, int rows, int tp, int32_t* out,
+                    uintptr_t stream);
+
 /* --------------------------------------------- decode-step bookkeeping
  * Graph-resident per-step state update so the decode loop needs no host
  * round trip (Machine.complete_iteration, machine.py:247-275):

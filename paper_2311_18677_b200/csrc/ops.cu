@@ -290,6 +290,82 @@ __global__ void signal_kernel(uint32_t* flag, uint32_t value) {
                : "memory");
 }
 
+// ------------------------------------------ vocab-parallel greedy argmax
+// TP pools split the LM head by vocabulary rows: rank r scores rows
+// [offset, offset + V) and publishes its candidate (max logit, global index)
+// in its slot of a [rows][tp][2] fp32 buffer (other slots zero) that the
+// pool's all-reduce (a sum) turns into every rank's candidates; the pick
+// takes the max, lowest global index on ties (= argmax over the full vocab).
+__global__ void argmax_shard_kernel(const float* __restrict__ logits, int V, int offset,
+                                    int rank, int tp, float* __restrict__ cand) {
+  pdl_trigger();
+  pdl_wait();
+  const float* row = logits + (size_t)blockIdx.x * V;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best) {
+      best = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sb[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = threadIdx.x < (int)(blockDim.x >> 5) ? sb[threadIdx.x] : -INFINITY;
+    bi = threadIdx.x < (int)(blockDim.x >> 5) ? si[threadIdx.x] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+  }
+  float* c = cand + (size_t)blockIdx.x * tp * 2;
+  if (threadIdx.x < tp) {
+    const bool mine = (int)threadIdx.x == rank;
+    c[2 * threadIdx.x] = mine ? best : 0.f;
+    c[2 * threadIdx.x + 1] = mine ? (float)(bi + offset) : 0.f;
+  }
+}
+
+__global__ void argmax_pick_kernel(const float* __restrict__ cand, int rows, int tp,
+                                   int32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const float* c = cand + (size_t)r * tp * 2;
+  float best = c[0];
+  int bi = (int)c[1];
+  for (int k = 1; k < tp; ++k) {        // ranks hold increasing index ranges
+    if (c[2 * k] > best) {
+      best = c[2 * k];
+      bi = (int)c[2 * k + 1];
+    }
+  }
+  out[r] = bi;
+}
+
 // -------------------------------------------------- decode bookkeeping
 __global__ void decode_prepare_kernel(const int32_t* __restrict__ ctx,
                                       const int32_t* __restrict__ tables,
@@ -530,4 +606,30 @@ extern "C" int swb_slots_from_table(const int32_t* table_row, int start, int n,
       return swb_set_error(SWB_ERR_CUDA, "launch slots_from_table_kernel: %s", cudaGetErrorString(le_));
   }
   return swb_check_launch("slots_from_table_kernel");
+}
+
+extern "C" int swb_argmax_shard(const float* logits, int rows, int V, int offset, int rank,
+                                int tp, float* cand, uintptr_t stream) {
+  SWB_REQUIRE(logits && cand, "swb_argmax_shard: null pointer");
+  SWB_REQUIRE(rows >= 0 && V > 0 && offset >= 0 && tp >= 1 && tp <= 32 && rank >= 0 &&
+                  rank < tp && offset + V < (1 << 24),
+              "swb_argmax_shard: bad args (indices must stay exact in fp32)");
+  if (rows == 0) return SWB_OK;
+  const cudaError_t le = launch(argmax_shard_kernel, dim3(rows), dim3(1024), 0, STREAM, logits,
+                                V, offset, rank, tp, cand);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch argmax_shard_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("argmax_shard_kernel");
+}
+
+extern "C" int swb_argmax_pick(const float* cand, int rows, int tp, int32_t* out,
+                               uintptr_t stream) {
+  SWB_REQUIRE(cand && out, "swb_argmax_pick: null pointer");
+  SWB_REQUIRE(rows >= 0 && tp >= 1 && tp <= 32, "swb_argmax_pick: bad args");
+  if (rows == 0) return SWB_OK;
+  const cudaError_t le = launch(argmax_pick_kernel, dim3((rows + 127) / 128), dim3(128), 0,
+                                STREAM, cand, rows, tp, out);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch argmax_pick_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("argmax_pick_kernel");
 }

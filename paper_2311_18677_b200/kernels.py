@@ -167,6 +167,18 @@ def argmax(logits, out=None):
     return out
 
 
+def argmax_shard(logits, offset, rank, tp, cand):
+    rows, V = logits.shape
+    call("swb_argmax_shard", logits.data_ptr(), rows, V, offset, rank, tp, cand.data_ptr(),
+         _stream())
+    return cand
+
+
+def argmax_pick(cand, rows, tp, out):
+    call("swb_argmax_pick", cand.data_ptr(), rows, tp, out.data_ptr(), _stream())
+    return out
+
+
 def rope_kv_write(qkv, positions, H, Hkv, dh, theta, k_layer=None, v_layer=None,
                   slots=None, block_size=16, rows=None):
     _req(qkv, torch.bfloat16, "qkv")

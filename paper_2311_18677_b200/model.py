@@ -86,7 +86,9 @@ class ModelConfig:
     def decode_bytes(self, contexts, tp: int = 1) -> int:
         """Algorithmic HBM bytes of one decode step per TP rank: weights once
         + the KV of every context."""
-        w = 2 * (self.params_nonembed() // tp + self.vocab * self.d_model)
+        # LM head split by vocabulary rows across a TP pool (runner.vocab_parallel)
+        head = self.vocab * self.d_model // (tp if self.vocab % tp == 0 else 1)
+        w = 2 * (self.params_nonembed() // tp + head)
         kv = sum(contexts) * self.kv_bytes_per_token(tp)
         return w + kv
 

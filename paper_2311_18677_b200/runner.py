@@ -80,6 +80,15 @@ class ModelRunner:
         # RoPE angle table for the fused QKV-GEMM epilogue (16K positions, 8 MB)
         self.rope_tab = (K.rope_table(cfg.rope_theta, 16384, device=self.dev)
                          if not self.bloom and self.dh == 128 else None)
+        # TP pools: LM head split by vocabulary rows (each rank streams V/TP
+        # rows), greedy pick through the pool's all-reduce of per-rank
+        # (max, index) candidates; SWB_VOCAB_PARALLEL=0 keeps the replicated head
+        self.vocab_parallel = (self.tp > 1 and cfg.vocab % self.tp == 0 and
+                               os.environ.get("SWB_VOCAB_PARALLEL", "1") != "0")
+        self.vocab_local = cfg.vocab // self.tp if self.vocab_parallel else cfg.vocab
+        self.vocab_off = self.rank * self.vocab_local if self.vocab_parallel else 0
+        self.head = (weights.lm_head[self.vocab_off:self.vocab_off + self.vocab_local]
+                     if self.vocab_parallel else weights.lm_head)
 
     # ------------------------------------------------------------ helpers
     def _allreduce(self, x):
@@ -140,6 +149,33 @@ class ModelRunner:
         else:
             K.linear(h, lw.wgu, K.EPI_SWIGLU, out=out)
 
+    def _greedy(self, logits, out):
+        """Greedy token per row of ``logits`` (this rank's vocabulary shard
+        under vocab parallelism)."""
+        if not self.vocab_parallel:
+            K.argmax(logits, out=out)
+            return
+        rows = int(logits.shape[0])
+        c = self._comm()
+        if c is None:        # NCCL all-reduce of the candidate table
+            cand = torch.empty(rows, self.tp, 2, dtype=torch.float32, device=self.dev)
+            K.argmax_shard(logits, self.vocab_off, self.rank, self.tp, cand)
+            self._allreduce(cand)
+        else:
+            s = c.next_slot()
+            part = c.slot(s, (rows, self.tp, 2))
+            K.argmax_shard(logits, self.vocab_off, self.rank, self.tp, part)
+            cand = self._cand_buf(rows)
+            c.allreduce(s, cand)
+        K.argmax_pick(cand, rows, self.tp, out)
+
+    def _cand_buf(self, rows):
+        buf = getattr(self, "_cand", None)
+        if buf is None or buf.shape[0] < rows:
+            self._cand = torch.empty(max(rows, 64), self.tp, 2, dtype=torch.float32,
+                                     device=self.dev)
+        return self._cand[:rows]
+
     def _resid_epi(self):
         # with TP only rank 0 folds the residual in; the all-reduce sums the rest
         return K.EPI_RESID_F32 if self.rank == 0 or self.tp == 1 else K.EPI_F32
@@ -157,7 +193,7 @@ class ModelRunner:
         self.pattn = torch.empty(cap, self.hq * self.dh, dtype=torch.bfloat16, device=dev)
         self.pact = torch.empty(cap, self.ffn, dtype=torch.bfloat16, device=dev)
         self.plast = torch.empty(rcap, d, dtype=torch.bfloat16, device=dev)
-        self.plogits = torch.empty(rcap, self.cfg.vocab, dtype=torch.float32, device=dev)
+        self.plogits = torch.empty(rcap, self.vocab_local, dtype=torch.float32, device=dev)
         self.pfirst = torch.empty(rcap, dtype=torch.int32, device=dev)
         self._cap, self._rcap = cap, rcap
 
@@ -246,9 +282,9 @@ class ModelRunner:
         last = self.plast[:R]
         self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=last_rows)
         logits = self.plogits[:R]
-        K.linear(last, w.lm_head, K.EPI_F32, out=logits)
+        K.linear(last, self.head, K.EPI_F32, out=logits)
         first = self.pfirst[:R]
-        K.argmax(logits, out=first)
+        self._greedy(logits, first)
         if push:
             if timing:
                 self._compute_end.record(main)
@@ -311,9 +347,9 @@ class ModelRunner:
         last = self.plast[:R + Bd]
         self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=idx)
         logits = self.plogits[:R + Bd]
-        K.linear(last, w.lm_head, K.EPI_F32, out=logits)
+        K.linear(last, self.head, K.EPI_F32, out=logits)
         nxt = self.pfirst[:R + Bd]
-        K.argmax(logits, out=nxt)
+        self._greedy(logits, nxt)
         dec_ctx += 1
         return nxt
 
@@ -361,9 +397,9 @@ class ModelRunner:
         idx = torch.tensor([n - 1], dtype=torch.int32, device=self.dev)
         self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=idx)
         logits = self.plogits[:1]
-        K.linear(last, w.lm_head, K.EPI_F32, out=logits)
+        K.linear(last, self.head, K.EPI_F32, out=logits)
         first = self.pfirst[:1]
-        K.argmax(logits, out=first)
+        self._greedy(logits, first)
         return first
 
     def finish_push_stats(self):
@@ -444,7 +480,7 @@ class DecodeGraph:
         self.qkv = torch.zeros(B, runner.qkv_cols, dtype=torch.bfloat16, device=dev)
         self.attn = torch.zeros(B, runner.hq * runner.dh, dtype=torch.bfloat16, device=dev)
         self.act = torch.zeros(B, runner.ffn, dtype=torch.bfloat16, device=dev)
-        self.logits = torch.zeros(B, cfg.vocab, dtype=torch.float32, device=dev)
+        self.logits = torch.zeros(B, runner.vocab_local, dtype=torch.float32, device=dev)
         wsb = K.attn_decode_workspace_bytes(B, runner.hq, max_ctx, part, runner.dh)
         self.ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
         self.graph = None
@@ -488,12 +524,12 @@ class DecodeGraph:
                 r._mlp_up(self.h, lw, self.act)
             r._proj_reduce(self.act, lw.wd, self.x, lw.bd)
         if fused:
-            K.gemv_rmsnorm(self.x, w.final_norm, cfg.norm_eps, w.lm_head, K.EPI_F32,
+            K.gemv_rmsnorm(self.x, w.final_norm, cfg.norm_eps, r.head, K.EPI_F32,
                            out=self.logits)
         else:
             r._norm(self.x, w.final_norm, w.final_norm_b, out=self.h)
-            K.linear(self.h, w.lm_head, K.EPI_F32, out=self.logits)
-        K.argmax(self.logits, out=self.next_tok)
+            K.linear(self.h, r.head, K.EPI_F32, out=self.logits)
+        r._greedy(self.logits, self.next_tok)
         K.decode_advance(self.next_tok, self.cur_tok, self.ctx, self.step, self.out_ring, B)
 
     def load(self, seqs: list[int], cur_tok, ctx, steps=None):

@@ -341,6 +341,13 @@ def main():
     ap.add_argument("--prompt", type=int, default=1024)
     ap.add_argument("--out", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--trace", default=None, choices=[None, "conversation", "coding"],
+                    help="N>=2: serve the reference's synthetic trace in real time instead "
+                         "of the fixed-shape burst")
+    ap.add_argument("--rate", type=float, default=4.0)
+    ap.add_argument("--duration", type=float, default=20.0)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--max-output", type=int, default=0)
     ap.add_argument("--tp", type=int, default=1,
                     help="tensor-parallel degree of each prompt/token machine (N >= 2*tp)")
     args = ap.parse_args()
@@ -348,6 +355,8 @@ def main():
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.trace and world < 2:
+        raise SystemExit("--trace needs N >= 2 GPUs (Splitwise pairs, launched with torchrun)")
     if world == 1 and args.gpus == 1:
         run_colocated(args)
     else:

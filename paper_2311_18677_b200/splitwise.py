@@ -34,7 +34,8 @@ import torch.distributed as dist
 
 from . import _abi
 from . import kernels as K
-from .control import HandoffReceiver, HandoffSender, recv_reservations, send_reservations
+from .control import (HandoffReceiver, HandoffSender, ShmMailbox, recv_reservations,
+                      send_reservations)
 from .kvcache import KVCacheManager, blocks_for
 from .model import get_config, init_weights
 from .perf import PerfModel
@@ -118,6 +119,69 @@ class PromptServer:
         return first_time
 
 
+    def serve_trace(self, requests, t0: float):
+        """Arrival-driven prompt machine: requests = [(rid, arrival_s, host
+        prompt, n_out)] in arrival order; each becomes a prompt task at its
+        arrival (wall clock from t0); batches follow the reference prompt
+        rule; a request's KV lands in the slot the token machine reserved at
+        the same arrival (reservation mailbox).  Returns {rid: first-token
+        host time}."""
+        pending = list(requests)
+        by_id = {r[0]: r for r in requests}
+        seq_of: dict = {}
+        first_time = {}
+        done = 0
+
+        def drain():
+            while True:
+                rows = self.res_box.get()
+                if rows is None:
+                    return
+                for rid, seq, *_ in rows:
+                    seq_of[rid] = seq
+
+        while done < len(requests):
+            now = time.perf_counter() - t0
+            while pending and pending[0][1] <= now:
+                rid, arr, prompt, n_out = pending.pop(0)
+                self.machine.enqueue(Task(rid, PROMPT, len(prompt), arr * 1e3, n_out, n_out),
+                                     now * 1e3)
+            drain()
+            if not self.machine.has_work():
+                wait = (pending[0][1] - now) if pending else 1e-4
+                time.sleep(min(max(wait, 0.0), 1e-3))
+                continue
+            batch = self.machine.form_batch(now * 1e3)
+            self.machine.running = batch
+            chunk = [by_id[t.request_id] for t in batch.prompt_tasks]
+            while any(r[0] not in seq_of for r in chunk):
+                drain()
+                time.sleep(2e-5)
+            lens = [len(r[2]) for r in chunk]
+            toks = torch.cat([r[2] for r in chunk]).pin_memory().to(self.runner.dev,
+                                                                      non_blocking=True)
+            meta = ModelRunner.pack_meta(lens).pin_memory().to(self.runner.dev, non_blocking=True)
+            segs, off = [], 0
+            for r, n in zip(chunk, lens):
+                segs.append(PushSegment(off, n, self.peer, seq_of[r[0]]))
+                off += n
+            st = PushStats(bytes_per_layer=off * 2 * self.runner.hkv * self.runner.dh * 2)
+            first = self.runner.prefill(toks, lens, meta, push=segs, push_stats=st)
+            fh = torch.empty(len(chunk), dtype=torch.int32).pin_memory()
+            fh.copy_(first, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            tnow = time.perf_counter()
+            self.runner.finish_push_stats()
+            self.push_log.append(st)
+            self.tx.send([(r[0], seq_of[r[0]], len(r[2]), int(fh[j]), r[3])
+                          for j, r in enumerate(chunk)])
+            for r in chunk:
+                first_time[r[0]] = tnow
+            done += len(chunk)
+            self.machine.complete_iteration(batch, (tnow - t0) * 1e3)
+        return first_time
+
+
 class TokenServer:
     def __init__(self, runner: ModelRunner, ctrl, prompt_rank: int, sched: SchedulerConfig,
                  tp_ctrl=None):
@@ -129,7 +193,7 @@ class TokenServer:
         self.rx = HandoffReceiver(tp_ctrl)
         self.machine = Machine(0, None, estimated_perf_model(runner.cfg, self.kv,
                                                              runner.w.nbytes()), TOKEN, sched)
-        self.step_log: list[tuple] = []     # (batch, max context, device ms) per decode step
+        self.step_log: list[tuple] = []     # (batch, summed context, device ms) per decode step
         self._ev = None
 
     def _events(self):
@@ -190,7 +254,7 @@ class TokenServer:
             ev1.record()
             ring_h[:B].copy_(graph.next_tok, non_blocking=True)   # stream tokens out
             torch.cuda.current_stream().synchronize()
-            self.step_log.append((B, max(info[r][1] for r in rids), ev0.elapsed_time(ev1)))
+            self.step_log.append((B, sum(info[r][1] for r in rids), ev0.elapsed_time(ev1)))
             tnow = time.perf_counter()
             for b, r in enumerate(rids):
                 t = int(ring_h[b])
@@ -205,6 +269,80 @@ class TokenServer:
         return emit, tokens
 
 
+    def serve_trace(self, requests, t0: float):
+        """Arrival-driven token machine: reserves each request's final context
+        at its arrival (both machines are chosen at arrival, reference
+        cluster.py:153-160) and publishes the slot to the prompt machine,
+        admits hand-overs between decode iterations (continuous batching with
+        the reference token rule), one CUDA-graph step per iteration.
+        Returns ({rid: [emission times]}, decode step log)."""
+        kv = self.kv
+        pending = list(requests)
+        n = len(requests)
+        info, emit = {}, {r[0]: [] for r in requests}
+        finished = 0
+        graph, graph_rids = None, None
+        ring_h = torch.empty(256, dtype=torch.int32).pin_memory()
+        self.step_log = []
+        while finished < n:
+            now = time.perf_counter() - t0
+            arrived = []
+            while pending and pending[0][1] <= now:
+                rid, arr, prompt, n_out = pending.pop(0)
+                arrived.append((rid, kv.allocate(len(prompt) + n_out)))
+            if arrived:
+                torch.cuda.current_stream().synchronize()   # table rows before the peer reads
+                self.res_box.put([(rid, seq, 0, 0, 0) for rid, seq in arrived])
+            rows = self.rx.poll(block=False)
+            if rows is not None:
+                tn = (time.perf_counter() - t0) * 1e3
+                for rid, seq, plen, first, n_out in rows:
+                    if n_out > 1:
+                        info[rid] = [seq, plen, first]
+                        self.machine.enqueue(Task(rid, TOKEN, plen + 1, tn, n_out, n_out - 1), tn)
+                    else:
+                        kv.release(seq)
+                        finished += 1
+            if not self.machine.has_work() and not self.machine.resident:
+                time.sleep(5e-5)
+                continue
+            batch = self.machine.form_batch((time.perf_counter() - t0) * 1e3)
+            if batch is None or not batch.token_tasks:
+                time.sleep(5e-5)
+                continue
+            self.machine.running = batch
+            rids = [t.request_id for t in batch.token_tasks]
+            B = len(rids)
+            if rids != graph_rids:
+                max_ctx = max(info[r][1] + 64 for r in rids) + max(
+                    t.remaining_output for t in batch.token_tasks)
+                graph = self.runner.decode_graph(B, 2048 * ((max_ctx + 2047) // 2048), 1)
+                graph.load([info[r][0] for r in rids], [info[r][2] for r in rids],
+                           [info[r][1] for r in rids])
+                if graph.graph is None:
+                    graph.capture()
+                graph_rids = rids
+            ev0, ev1 = self._events()
+            ev0.record()
+            graph.replay()
+            ev1.record()
+            ring_h[:B].copy_(graph.next_tok, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            tnow = time.perf_counter()
+            self.step_log.append((B, sum(info[r][1] for r in rids), ev0.elapsed_time(ev1)))
+            for b, r in enumerate(rids):
+                t = int(ring_h[b])
+                info[r][1] += 1
+                info[r][2] = t
+                emit[r].append(tnow)
+            for what, task in self.machine.complete_iteration(batch, (tnow - t0) * 1e3):
+                if what == "request_finished":
+                    kv.release(info[task.request_id][0])
+                    finished += 1
+                    graph_rids = None
+        return emit, self.step_log
+
+
 # ---------------------------------------------------------------------------
 def _decode_roofline(cfg, tp, steps, hbm_peak, peak_kind):
     """HBM roofline of the token machine's decode step (the dominant kernel
@@ -215,7 +353,7 @@ def _decode_roofline(cfg, tp, steps, hbm_peak, peak_kind):
         return None
     bmax = max(b for b, _, _ in steps)
     full = [(b, c, ms) for b, c, ms in steps if b == bmax]
-    byts = [cfg.decode_bytes([c] * b, tp) for b, c, _ in full]
+    byts = [cfg.decode_bytes([c], tp) for _, c, _ in full]   # c = the batch's summed context
     ms = [m for _, _, m in full]
     ach = (sum(byts) / len(byts)) / (sum(ms) / len(ms) / 1e3) / 1e9
     return {"kernel": f"decode_step (CUDA graph, B={bmax}, token machine)", "bound": "hbm",
@@ -232,6 +370,8 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
     tp = max(1, int(getattr(args, "tp", 1)))
     if world < 2 * tp or world % (2 * tp):
         raise SystemExit(f"Splitwise TP{tp}+TP{tp} pairs need a multiple of {2 * tp} GPUs")
+    if getattr(args, "trace", None) and tp != 1:
+        raise SystemExit("--trace serves TP1+TP1 pairs")
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctrl = dist.new_group(backend="gloo")
@@ -256,18 +396,23 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
     sched = SchedulerConfig()
     if is_prompt:
         runner = ModelRunner(w, None, tp_group=tp_nccl)
-        handle = [None, None]
+        handle = [None, None, None]
         dist.recv_object_list(handle, src=peer_rank, group=ctrl)
         peer = KVCacheManager.open_peer(handle[0])
         server = PromptServer(runner, peer, ctrl, peer_rank, sched, mailbox=handle[1])
+        server.res_box = ShmMailbox(name=handle[2])
     else:
-        nb = min(pool_blocks_for_memory(cfg, tp, 16, reserve_bytes=2 << 30),
-                 64 * blocks_for(P + O + 64, 16))
-        kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads // tp, cfg.head_dim, 16, 64,
-                            blocks_for(8192 + 1024, 16))
+        trace_mode = bool(getattr(args, "trace", None))
+        nb = pool_blocks_for_memory(cfg, tp, 16, reserve_bytes=2 << 30)
+        if not trace_mode:
+            nb = min(nb, 64 * blocks_for(P + O + 64, 16))
+        kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads // tp, cfg.head_dim, 16,
+                            256 if trace_mode else 64, blocks_for(8192 + 4096, 16))
         runner = ModelRunner(w, kv, tp_group=tp_nccl)
         server = TokenServer(runner, ctrl, peer_rank, sched, tp_ctrl=tp_gloo)
-        dist.send_object_list([kv.ipc_handle(), server.rx.name], dst=peer_rank, group=ctrl)
+        server.res_box = ShmMailbox(create=True)
+        dist.send_object_list([kv.ipc_handle(), server.rx.name, server.res_box.name],
+                              dst=peer_rank, group=ctrl)
     push_alone = None
     if is_prompt:
         # KV-push kernel alone over NVLink (no concurrent prefill): one layer of
@@ -315,6 +460,10 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
 
     for _ in range(args.warmup):
         one_step(False)
+    if getattr(args, "trace", None):
+        _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, ClockSampler,
+                     percentile, peaks)
+        return
     launches0 = _abi.launch_count()
     e2e_ms, ttft, tbt, gaps2, push_gbs, push_tail, push_raw = [], [], [], [], [], [], []
     dec_steps = []
@@ -406,8 +555,92 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
     dist.barrier()
     torch.cuda.synchronize()
     (server.tx if is_prompt else server.rx).close()
+    server.res_box.close()
     # NCCL sub-communicator teardown can stall at interpreter exit (seen with
     # TP groups + CUDA IPC mappings); the result is printed, so bound it.
+    threading.Timer(30.0, lambda: os._exit(0)).start()
+    dist.destroy_process_group()
+    os._exit(0)
+
+
+def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, ClockSampler,
+                 percentile, peaks):
+    """bench.py --trace: the reference's synthetic trace (trace.py presets,
+    Poisson arrivals) served concurrently by the Splitwise pairs in real
+    time; request i goes to pair i mod pairs (TP=1 pairs).  Rank 0 prints
+    TTFT / TBT / E2E percentiles and tokens/s."""
+    import json
+    from .trace import preset_trace
+    pairs = world // 2
+    reqs_all = preset_trace(args.trace, args.rate, args.duration, args.seed)
+    if args.max_output:
+        reqs_all = [type(r)(r.id, r.arrival, r.prompt_tokens, min(r.output_tokens, args.max_output))
+                    for r in reqs_all]
+    mine = [r for r in reqs_all if r.id % pairs == pair]
+    g = torch.Generator().manual_seed(77)
+    prompts = {r.id: torch.randint(0, cfg.vocab, (r.prompt_tokens,), generator=g,
+                                   dtype=torch.int32) for r in reqs_all}
+    items = [(r.id, r.arrival, prompts[r.id], r.output_tokens) for r in mine]
+    # common start (perf_counter is CLOCK_MONOTONIC: comparable across processes)
+    t0t = torch.tensor([time.perf_counter() + 1.0], dtype=torch.float64)
+    dist.broadcast(t0t, src=0, group=ctrl)
+    t0 = float(t0t.item())
+    while time.perf_counter() < t0:
+        time.sleep(1e-4)
+    with ClockSampler(local) as clk:
+        out = server.serve_trace(items, t0)
+    payload = {"rank": rank, "prompt": is_prompt, "out": out if is_prompt else out[0],
+               "steps": None if is_prompt else out[1]}
+    gathered = [None] * world
+    dist.all_gather_object(gathered, payload, group=ctrl)
+    if rank == 0:
+        arrival = {r.id: t0 + r.arrival for r in reqs_all}
+        first = {}
+        emits = {}
+        steps = []
+        for gp in gathered:
+            if gp["prompt"]:
+                first.update(gp["out"])
+            else:
+                emits.update(gp["out"])
+                steps += gp["steps"]
+        ttft, tbt, e2e = [], [], []
+        ntok = 0
+        t_end = 0.0
+        for r in reqs_all:
+            seq = [first[r.id]] + emits.get(r.id, [])
+            ntok += len(seq)
+            ttft.append((first[r.id] - arrival[r.id]) * 1e3)
+            tbt += [(b - a) * 1e3 for a, b in zip(seq, seq[1:])]
+            e2e.append((seq[-1] - arrival[r.id]) * 1e3)
+            t_end = max(t_end, seq[-1])
+        span = t_end - t0
+        hbm_peak, _tc, _tcs, peak_kind = peaks()
+        p = lambda xs, q: percentile(xs, q) if xs else None  # noqa: E731
+        line = {
+            "metric": f"TTFT/TBT p50,p99 + tokens/s serving the reference's {args.trace} trace, "
+                      f"{cfg.name}",
+            "value": ntok / span, "unit": "tokens/s", "n_gpus": world, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic trace (reference presets, Poisson arrivals), random weights",
+            "config": {"workload": f"{args.trace} trace rate {args.rate}/s for {args.duration} s "
+                                   f"(seed {args.seed}), {len(reqs_all)} requests, "
+                                   f"{pairs} Splitwise pair(s), request i -> pair i mod "
+                                   f"{pairs}, served concurrently in real time",
+                       "model": cfg.name, "parallelism": f"{pairs}x(prompt TP1 + token TP1)",
+                       "max_output": args.max_output or None},
+            "ttft_ms": {"p50": p(ttft, 0.5), "p99": p(ttft, 0.99)},
+            "tbt_ms": {"p50": p(tbt, 0.5), "p99": p(tbt, 0.99)},
+            "e2e_ms": {"p50": p(e2e, 0.5), "p99": p(e2e, 0.99)},
+            "requests": len(reqs_all), "output_tokens": ntok, "makespan_s": span,
+            "roofline": _decode_roofline(cfg, 1, steps, hbm_peak, peak_kind),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    (server.tx if is_prompt else server.rx).close()
+    server.res_box.close()
     threading.Timer(30.0, lambda: os._exit(0)).start()
     dist.destroy_process_group()
     os._exit(0)

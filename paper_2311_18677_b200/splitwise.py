@@ -404,8 +404,8 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
     else:
         trace_mode = bool(getattr(args, "trace", None))
         nb = pool_blocks_for_memory(cfg, tp, 16, reserve_bytes=2 << 30)
-        if not trace_mode:
-            nb = min(nb, 64 * blocks_for(P + O + 64, 16))
+        nb = min(nb, 256 * blocks_for(8192 + 4096, 16) if trace_mode
+                 else 64 * blocks_for(P + O + 64, 16))
         kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads // tp, cfg.head_dim, 16,
                             256 if trace_mode else 64, blocks_for(8192 + 4096, 16))
         runner = ModelRunner(w, kv, tp_group=tp_nccl)

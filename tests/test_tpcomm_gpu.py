@@ -109,3 +109,44 @@ def test_tp2_tiny_matches_tp1():
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"ok": true' in r.stdout
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_realtime_trace_serving_one_pair():
+    """bench.py --trace: a Splitwise pair (2 processes) serves a short
+    reference-preset trace in real time; every request completes and the
+    JSON line carries TTFT / TBT percentiles."""
+    import json
+    import subprocess
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "bench.py"), "--gpus", "2", "--model", "tiny",
+                        "--warmup", "1", "--prompt", "128", "--out", "8", "--trace",
+                        "conversation", "--rate", "20", "--duration", "2", "--max-output", "24"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["requests"] > 10 and line["ttft_ms"]["p50"] > 0 and line["tbt_ms"]["p99"] > 0
+    assert line["output_tokens"] >= line["requests"]
+
+
+def test_vocab_parallel_pick_equals_full_argmax():
+    """swb_argmax_shard over TP vocabulary shards + a summed candidate table +
+    swb_argmax_pick == swb_argmax over the full vocabulary (ties included)."""
+    from paper_2311_18677_b200 import kernels as K
+    rows, V, tp = 5, 32000, 4
+    logits = torch.randn(rows, V, device="cuda")
+    logits[1, 7] = logits[1, 16007] = 100.0          # tie across shards: lowest index wins
+    Vs = V // tp
+    total = torch.zeros(rows, tp, 2, device="cuda")
+    for r in range(tp):
+        cand = torch.full((rows, tp, 2), float("nan"), device="cuda")
+        K.argmax_shard(logits[:, r * Vs:(r + 1) * Vs].contiguous(), r * Vs, r, tp, cand)
+        total += cand
+    got = torch.empty(rows, dtype=torch.int32, device="cuda")
+    K.argmax_pick(total, rows, tp, got)
+    want = torch.empty(rows, dtype=torch.int32, device="cuda")
+    K.argmax(logits, out=want)
+    assert got.tolist() == want.tolist()
+    assert got[1].item() == 7

@@ -63,10 +63,23 @@ def estimated_perf_model(cfg, kv: KVCacheManager | None, weight_bytes: int,
                      float(weight_bytes), cap, cfg.max_token_batch)
 
 
+def _lockstep(n: int, tp_ctrl, now_ms: float = 0.0) -> tuple[int, float]:
+    """(arrivals to process, scheduler clock) for this iteration of a TP
+    group: the minimum arrival count and the maximum clock over the peers, so
+    every peer enqueues / reserves the same requests and forms the same batch
+    (the collectives inside the steps stay matched)."""
+    if tp_ctrl is None:
+        return n, now_ms
+    t = torch.tensor([float(n), -now_ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=tp_ctrl)
+    return int(t[0].item()), -float(t[1].item())
+
+
 class PromptServer:
     def __init__(self, runner: ModelRunner, peer: KVCacheManager, ctrl, token_rank: int,
-                 sched: SchedulerConfig, mailbox: str):
+                 sched: SchedulerConfig, mailbox: str, tp_ctrl=None):
         self.runner = runner
+        self.tp_ctrl = tp_ctrl          # TP peers must batch in lockstep (collectives inside)
         self.peer = peer
         self.tx = HandoffSender(mailbox)
         self.ctrl = ctrl
@@ -142,10 +155,14 @@ class PromptServer:
 
         while done < len(requests):
             now = time.perf_counter() - t0
-            while pending and pending[0][1] <= now:
+            n_new = 0
+            while n_new < len(pending) and pending[n_new][1] <= now:
+                n_new += 1
+            n_take, _ = _lockstep(n_new, self.tp_ctrl)
+            for _ in range(n_take):
                 rid, arr, prompt, n_out = pending.pop(0)
                 self.machine.enqueue(Task(rid, PROMPT, len(prompt), arr * 1e3, n_out, n_out),
-                                     now * 1e3)
+                                     arr * 1e3)
             drain()
             if not self.machine.has_work():
                 wait = (pending[0][1] - now) if pending else 1e-4
@@ -287,7 +304,11 @@ class TokenServer:
         while finished < n:
             now = time.perf_counter() - t0
             arrived = []
-            while pending and pending[0][1] <= now:
+            n_new = 0
+            while n_new < len(pending) and pending[n_new][1] <= now:
+                n_new += 1
+            n_take, mnow = _lockstep(n_new, self.tp_ctrl, now * 1e3)
+            for _ in range(n_take):
                 rid, arr, prompt, n_out = pending.pop(0)
                 arrived.append((rid, kv.allocate(len(prompt) + n_out)))
             if arrived:
@@ -295,7 +316,7 @@ class TokenServer:
                 self.res_box.put([(rid, seq, 0, 0, 0) for rid, seq in arrived])
             rows = self.rx.poll(block=False)
             if rows is not None:
-                tn = (time.perf_counter() - t0) * 1e3
+                tn = mnow
                 for rid, seq, plen, first, n_out in rows:
                     if n_out > 1:
                         info[rid] = [seq, plen, first]
@@ -306,7 +327,7 @@ class TokenServer:
             if not self.machine.has_work() and not self.machine.resident:
                 time.sleep(5e-5)
                 continue
-            batch = self.machine.form_batch((time.perf_counter() - t0) * 1e3)
+            batch = self.machine.form_batch(mnow)
             if batch is None or not batch.token_tasks:
                 time.sleep(5e-5)
                 continue
@@ -335,7 +356,7 @@ class TokenServer:
                 info[r][1] += 1
                 info[r][2] = t
                 emit[r].append(tnow)
-            for what, task in self.machine.complete_iteration(batch, (tnow - t0) * 1e3):
+            for what, task in self.machine.complete_iteration(batch, mnow):
                 if what == "request_finished":
                     kv.release(info[task.request_id][0])
                     finished += 1
@@ -370,8 +391,6 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
     tp = max(1, int(getattr(args, "tp", 1)))
     if world < 2 * tp or world % (2 * tp):
         raise SystemExit(f"Splitwise TP{tp}+TP{tp} pairs need a multiple of {2 * tp} GPUs")
-    if getattr(args, "trace", None) and tp != 1:
-        raise SystemExit("--trace serves TP1+TP1 pairs")
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctrl = dist.new_group(backend="gloo")
@@ -399,7 +418,8 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         handle = [None, None, None]
         dist.recv_object_list(handle, src=peer_rank, group=ctrl)
         peer = KVCacheManager.open_peer(handle[0])
-        server = PromptServer(runner, peer, ctrl, peer_rank, sched, mailbox=handle[1])
+        server = PromptServer(runner, peer, ctrl, peer_rank, sched, mailbox=handle[1],
+                              tp_ctrl=tp_gloo)
         server.res_box = ShmMailbox(name=handle[2])
     else:
         trace_mode = bool(getattr(args, "trace", None))
@@ -462,7 +482,7 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         one_step(False)
     if getattr(args, "trace", None):
         _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, ClockSampler,
-                     percentile, peaks)
+                     percentile, peaks, tp)
         return
     launches0 = _abi.launch_count()
     e2e_ms, ttft, tbt, gaps2, push_gbs, push_tail, push_raw = [], [], [], [], [], [], []
@@ -564,14 +584,15 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
 
 
 def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, ClockSampler,
-                 percentile, peaks):
+                 percentile, peaks, tp=1):
     """bench.py --trace: the reference's synthetic trace (trace.py presets,
     Poisson arrivals) served concurrently by the Splitwise pairs in real
-    time; request i goes to pair i mod pairs (TP=1 pairs).  Rank 0 prints
-    TTFT / TBT / E2E percentiles and tokens/s."""
+    time; request i goes to pair i mod pairs; TP pairs process arrivals in
+    lockstep across their peers.  Rank 0 prints TTFT / TBT / E2E percentiles
+    and tokens/s."""
     import json
     from .trace import preset_trace
-    pairs = world // 2
+    pairs = world // (2 * tp)
     reqs_all = preset_trace(args.trace, args.rate, args.duration, args.seed)
     if args.max_output:
         reqs_all = [type(r)(r.id, r.arrival, r.prompt_tokens, min(r.output_tokens, args.max_output))
@@ -599,6 +620,8 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
         emits = {}
         steps = []
         for gp in gathered:
+            if gp["rank"] % tp:          # TP peers report the same requests
+                continue
             if gp["prompt"]:
                 first.update(gp["out"])
             else:
@@ -625,15 +648,16 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
             "data": "synthetic trace (reference presets, Poisson arrivals), random weights",
             "config": {"workload": f"{args.trace} trace rate {args.rate}/s for {args.duration} s "
                                    f"(seed {args.seed}), {len(reqs_all)} requests, "
-                                   f"{pairs} Splitwise pair(s), request i -> pair i mod "
-                                   f"{pairs}, served concurrently in real time",
-                       "model": cfg.name, "parallelism": f"{pairs}x(prompt TP1 + token TP1)",
+                                   f"{pairs} Splitwise pair(s) TP{tp}+TP{tp}, request i -> pair "
+                                   f"i mod {pairs}, served concurrently in real time",
+                       "model": cfg.name,
+                       "parallelism": f"{pairs}x(prompt TP{tp} + token TP{tp})",
                        "max_output": args.max_output or None},
             "ttft_ms": {"p50": p(ttft, 0.5), "p99": p(ttft, 0.99)},
             "tbt_ms": {"p50": p(tbt, 0.5), "p99": p(tbt, 0.99)},
             "e2e_ms": {"p50": p(e2e, 0.5), "p99": p(e2e, 0.99)},
             "requests": len(reqs_all), "output_tokens": ntok, "makespan_s": span,
-            "roofline": _decode_roofline(cfg, 1, steps, hbm_peak, peak_kind),
+            "roofline": _decode_roofline(cfg, tp, steps, hbm_peak, peak_kind),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

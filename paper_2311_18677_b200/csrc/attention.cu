@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(NW * 32)
 constexpr int DM_WARPS = 4, DM_PT = 128, DM_WT = 32, DM_QS = DA_D + 8;
 constexpr int DC_MAXQT = 512;     // chunked prefill: up to 8192 query rows per chunk
 
-template <bool STEP>
+template <bool STEP, int WT>   // WT = tokens per warp (32: partition 128, 16: 64)
 __global__ void __launch_bounds__(DM_WARPS * 32)
     attn_decode_mma_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                            __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
@@ -650,10 +650,11 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
                            float* __restrict__ ws, int* __restrict__ tickets,
                            __nv_bfloat16* __restrict__ out, int trig) {
   constexpr int BS = 16;
+  constexpr int PT = DM_WARPS * WT, PPW = WT / BS;   // partition tokens, pages per warp
   extern __shared__ __align__(128) uint8_t dsm[];
   __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(dsm);          // [128][128]
-  __nv_bfloat16* sv = sk + DM_PT * DA_D;                               // [128][128]
-  __nv_bfloat16* sq = sv + DM_PT * DA_D;                               // [16][DM_QS]
+  __nv_bfloat16* sv = sk + PT * DA_D;                               // [128][128]
+  __nv_bfloat16* sq = sv + PT * DA_D;                               // [16][DM_QS]
   float* sml = reinterpret_cast<float*>(sq + 16 * DM_QS);              // [4][8][2]
   float* so = sml + DM_WARPS * 8 * 2;                                  // [4][G][128]
   __shared__ uint64_t kbar[DM_WARPS], vbar[DM_WARPS];
@@ -686,8 +687,8 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     L = ctx_lens[b];
     cur = pos ? pos[b] : -1;
   }
-  const int t0 = p * DM_PT;
-  const int t1 = min(L, t0 + DM_PT);
+  const int t0 = p * PT;
+  const int t1 = min(L, t0 + PT);
   const int ntok = t1 - t0;
   if (warp == 0 && ntok > 0) {
     // pages of cached tokens; page j feeds warp j/2's barriers
@@ -695,7 +696,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     const int nblk = (max(0, cend - t0) + BS - 1) / BS;
     constexpr uint32_t tile = BS * DA_D * 2;
     if (lane < DM_WARPS) {
-      const int np = min(max(nblk - 2 * lane, 0), 2);
+      const int np = min(max(nblk - PPW * lane, 0), PPW);
       mbar_arrive_expect_tx(&kbar[lane], tile * np);
       mbar_arrive_expect_tx(&vbar[lane], tile * np);
     }
@@ -703,8 +704,8 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     if (lane < nblk) {
       const int blk = __ldg(trow + t0 / BS + lane);
       const size_t gofs = ((size_t)blk * Hkv + kh) * BS * DA_D;
-      bulk_g2s(sk + (size_t)lane * BS * DA_D, kpool + gofs, tile, &kbar[lane >> 1]);
-      bulk_g2s(sv + (size_t)lane * BS * DA_D, vpool + gofs, tile, &vbar[lane >> 1]);
+      bulk_g2s(sk + (size_t)lane * BS * DA_D, kpool + gofs, tile, &kbar[lane / PPW]);
+      bulk_g2s(sv + (size_t)lane * BS * DA_D, vpool + gofs, tile, &vbar[lane / PPW]);
     }
   }
   if constexpr (STEP) pdl_wait();
@@ -765,8 +766,8 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     }
     __syncthreads();
 
-    const int wt0 = warp * DM_WT;
-    const bool cur_here = own_cur && cur - t0 >= wt0 && cur - t0 < wt0 + DM_WT;
+    const int wt0 = warp * WT;
+    const bool cur_here = own_cur && cur - t0 >= wt0 && cur - t0 < wt0 + WT;
     if (wt0 < ntok) {   // warp-uniform
       mbar_wait(&kbar[warp], 0);
       if (cur_here && lane < 16)
@@ -774,9 +775,9 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
             reinterpret_cast<const uint4*>(scur[0])[lane];
       __syncwarp();
       // S = Q K^T (16 heads-rows x 32 tokens)
-      float s[4][4];
+      float s[WT / 8][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+      for (int i = 0; i < WT / 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
       const uint32_t sq_u = smem_u32(sq), sk_u = smem_u32(sk), sv_u = smem_u32(sv);
 #pragma unroll
       for (int kk = 0; kk < DA_D / 16; ++kk) {
@@ -784,7 +785,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
         ldsm_x4(sq_u + ((lane & 15) * DM_QS + (kk * 2 + (lane >> 4)) * 8) * 2, qf[0], qf[1],
                 qf[2], qf[3]);
 #pragma unroll
-        for (int np = 0; np < 2; ++np) {
+        for (int np = 0; np < WT / 16; ++np) {
           const int key = wt0 + np * 16 + (lane & 7) + ((lane >> 4) << 3);
           const int chunk = kk * 2 + ((lane >> 3) & 1);
           uint32_t b0, b1, b2, b3;
@@ -797,7 +798,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       const float sl = (alibi && g < G) ? alibi[kh * G + g] * 1.4426950408889634f : 0.f;
       float m = -INFINITY;
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
+      for (int nt = 0; nt < WT / 8; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int tok = wt0 + nt * 8 + 2 * t + e;
@@ -809,9 +810,9 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
       float l = 0.f;
-      uint32_t pf[2][4];
+      uint32_t pf[WT / 16][4];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
+      for (int nt = 0; nt < WT / 8; ++nt) {
         const float e0 = exp2f(s[nt][0] - m), e1 = exp2f(s[nt][1] - m);
         l += e0 + e1;
         const uint32_t pk = f2_to_bf2(e0, e1);
@@ -831,7 +832,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
             reinterpret_cast<const uint4*>(scur[1])[lane];
       // rows past the context hold stale smem / unwritten pool bytes: P is 0
       // there, but 0 * NaN is not, so zero them
-      for (int i = max(ntok - wt0, 0) * 16 + lane; i < DM_WT * 16; i += 32)
+      for (int i = max(ntok - wt0, 0) * 16 + lane; i < WT * 16; i += 32)
         reinterpret_cast<uint4*>(sv + (size_t)wt0 * DA_D)[i] = make_uint4(0, 0, 0, 0);
       __syncwarp();
       // O = P V (16 x 128)
@@ -839,7 +840,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
 #pragma unroll
       for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
+      for (int ks = 0; ks < WT / 16; ++ks) {
 #pragma unroll
         for (int dp = 0; dp < 8; ++dp) {
           const int key = wt0 + ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
@@ -1277,18 +1278,21 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
   // B=32 54 vs 63 us); for MHA (G=1) the CUDA-core kernel is ahead (7B B=1
   // 10.0 vs 13.9 us: the unswizzled 256-byte page rows cost the MMA kernel
   // 8-way ldmatrix conflicts that only pay off when G rows share them)
-  if (mma_on && G >= 4 && block_size == 16 && partition == DM_PT) {
+  if (mma_on && G >= 4 && block_size == 16 && (partition == 128 || partition == 64)) {
     static bool attr_m[64] = {false};
     if (dev < 64 && !attr_m[dev]) {
-      SWB_CUDA(cudaFuncSetAttribute(attn_decode_mma_kernel<STEP>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      SWB_CUDA(cudaFuncSetAttribute(attn_decode_mma_kernel<STEP, 32>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      SWB_CUDA(cudaFuncSetAttribute(attn_decode_mma_kernel<STEP, 16>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
       attr_m[dev] = true;
     }
     const size_t msm = std::max(merge_scratch,
-                                (size_t)2 * DM_PT * DA_D * 2 + 16 * DM_QS * 2 +
+                                (size_t)2 * partition * DA_D * 2 + 16 * DM_QS * 2 +
                                     sizeof(float) * (DM_WARPS * 8 * 2 + (size_t)DM_WARPS * G * DA_D));
     const cudaError_t lm = launch(
-        attn_decode_mma_kernel<STEP>, dim3(NP, Hkv, B), dim3(DM_WARPS * 32), msm,
+        partition == 128 ? attn_decode_mma_kernel<STEP, 32> : attn_decode_mma_kernel<STEP, 16>,
+        dim3(NP, Hkv, B), dim3(DM_WARPS * 32), msm,
         (cudaStream_t)stream, reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
         reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
         block_tables, max_blocks, ctx_lens, positions, slots,

@@ -57,7 +57,8 @@ def measure(a):
                           "token_knots": model.token_knots, "profile": a.out}), flush=True)
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
+        torch.cuda.synchronize()
+        os._exit(0)        # NCCL / TP-comm teardown at exit is not needed (and can stall)
 
 
 def sweep(a):

@@ -64,6 +64,7 @@ class ModelRunner:
         self.theta = 0.0 if self.bloom else cfg.rope_theta     # 0: ALiBi, no rotation
         self.alibi = weights.alibi
         self.tp_max_rows = tp_max_rows    # largest prefill / decode row count reduced
+        self.ar_nccl_bytes = int(os.environ.get("SWB_TP_AR_NCCL_BYTES", str(4 << 20)))
         self.kv = kv
         self.hq = cfg.n_heads // self.tp
         self.hkv = cfg.n_kv_heads // self.tp
@@ -120,7 +121,12 @@ class ModelRunner:
             return
         b = bias if self.rank == 0 else None
         c = self._comm()
-        if c is None:
+        # large (prefill) messages: NCCL's all-reduce (NVSwitch in-network
+        # reduction) beats the peer-memory kernel — 49 MB at TP4 155 vs 253 us,
+        # 32 MB at TP2 90 vs 97 us (tools/ar_bench.py); small (decode)
+        # messages stay on the graph-replayable peer kernel (20 vs 26-39 us)
+        big = x.numel() * 4 >= self.ar_nccl_bytes
+        if c is None or big:
             K.linear(inp, w, self._resid_epi(), out=x, resid=x, bias=b)
             self._allreduce(x)
             return

@@ -3,7 +3,7 @@
 //
 // Each rank owns one device region, exported by CUDA IPC and mapped by every
 // peer of its TP group:
-//   [slot 0 data | slot 1 data | flags[2][MAXW][MAXC] | counters[2][MAXC]]
+//   [slot 0 | slot 1 | rx[2][MAXW] | flags[2][MAXW][MAXC] | counters[2][MAXC]]
 // The producing GEMM/GEMV writes its fp32 partial sums straight into a slot
 // (rank 0 folds the residual in), so the all-reduce moves no extra copy:
 //   CTA c of rank r   1. system-scope release store of its epoch into
@@ -13,11 +13,17 @@
 //                     3. sums chunk c of the slot over ranks 0..W-1 in rank
 //                        order (bit-identical results on every rank) with
 //                        16-byte L2-only loads over NVLink, writes `out`.
+// Decode-size messages (<= 1 MB) use the push form instead: CTA c first
+// stores chunk c of its own slot into rx[slot][r] of every peer (posted
+// NVLink writes), releases the flag behind them, and after the handshake sums
+// own slot + rx[slot][p] from local memory — one one-way trip instead of a
+// flag trip plus a remote-read round trip; same floats, same order.
 // Epochs are per-(slot, CTA) device counters, so the launch is CUDA-graph
 // replayable.  Two slots alternate: a slot is rewritten only after the next
 // all-reduce (other slot) completed on every rank, i.e. after all peers
 // finished reading it.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -39,6 +45,9 @@ static_assert(sizeof(TpIpcBlob) <= SWB_TP_IPC_BYTES, "blob too large");
 
 struct TpArgs {
   const float* peer_slot[TP_MAXW];   // slot base of every rank (own = local)
+  float* peer_rx[TP_MAXW];           // push mode: rank p's rx[slot][this rank]
+  const float* my_rx;                // push mode: this rank's rx[slot][0]
+  long long rx_stride;               // floats between rx[slot][src] and rx[slot][src+1]
   uint32_t* peer_flags[TP_MAXW];     // flags region of every rank
   uint32_t* my_flags;
   uint32_t* my_ctr;
@@ -90,23 +99,62 @@ __device__ __forceinline__ float4 tp_sum4(const TpArgs& a, long long i) {
   return s;
 }
 
-// one_shot: every rank reads all ranks' slots and sums the whole vector
-// (one handshake; (W-1)*n floats in over NVLink) — small / 2-rank messages.
-// two_shot: reduce-scatter then all-gather through the slots (two
+// mode 0, one-shot pull: every rank reads all ranks' slots and sums the whole
+// vector (one handshake; (W-1)*n floats in over NVLink).
+// mode 1, two-shot: reduce-scatter then all-gather through the slots (two
 // handshakes; 2*(W-1)/W*n in) — large messages on W > 2.
-__global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a, int two_shot) {
+// mode 2, one-shot push: decode-size messages (fit the rx buffers).
+__global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a, int mode,
+                                                                   int trig) {
   pdl_wait();  // the producer GEMM/GEMV must be complete before we publish
+  // past our own wait: the next kernel may launch now and stream its static
+  // weights (pre-wait) while this one waits on the peers' flags over NVLink
+  if (trig) pdl_launch_dependents();
   const int c = blockIdx.x;
   uint32_t* ctr = a.my_ctr + a.slot * TP_MAXC + c;
   uint32_t e = 0;
   if (threadIdx.x == 0) {
     e = *ctr + 1;
-    tp_handshake(a, c, e);
+    if (mode != 2) tp_handshake(a, c, e);
   }
   __syncthreads();
   const long long n4 = a.n >> 2;
   float4* out4 = reinterpret_cast<float4*>(a.out);
-  if (!two_shot) {
+  if (mode == 2) {
+    // push: copy this CTA's chunk of the local partial into every peer's
+    // rx[slot][rank] (posted NVLink stores), release the flag behind them,
+    // then sum the chunk from local memory only (own slot + rx of each peer)
+    // in rank order — the same floats in the same order as the pull form.
+    const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+    const long long lo = (long long)c * per, hi = min(n4, lo + per);
+    const float4* mine = reinterpret_cast<const float4*>(a.peer_slot[a.rank]);
+    for (long long i = lo + threadIdx.x; i < hi; i += TP_THREADS) {
+      const float4 v = __ldcg(mine + i);
+      for (int p = 0; p < a.world; ++p)
+        if (p != a.rank) reinterpret_cast<float4*>(a.peer_rx[p])[i] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tp_handshake(a, c, e);
+    __syncthreads();
+    for (long long i = lo + threadIdx.x; i < hi; i += TP_THREADS) {
+      float4 v[TP_MAXW];
+#pragma unroll
+      for (int p = 0; p < TP_MAXW; ++p)
+        if (p < a.world)
+          v[p] = p == a.rank ? __ldcg(mine + i)
+                             : __ldcg(reinterpret_cast<const float4*>(a.my_rx + p * a.rx_stride) + i);
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < TP_MAXW; ++p)
+        if (p < a.world) {
+          s.x += v[p].x; s.y += v[p].y; s.z += v[p].z; s.w += v[p].w;
+        }
+      out4[i] = s;
+    }
+    if (threadIdx.x == 0) *ctr = e;
+    return;
+  }
+  if (mode == 0) {
     const long long per = (n4 + gridDim.x - 1) / gridDim.x;
     const long long lo = (long long)c * per, hi = min(n4, lo + per);
     for (long long i = lo + threadIdx.x; i < hi; i += 2 * TP_THREADS) {
@@ -160,8 +208,13 @@ struct swb_tp_comm {
   bool connected;
 };
 
+// push-mode receive buffers: rx[2 slots][TP_MAXW sources] of tp_rx_bytes each
+static size_t tp_rx_bytes(size_t slot_bytes) { return std::min<size_t>(slot_bytes, 1 << 20); }
+static size_t tp_flags_off(size_t slot_bytes) {
+  return 2 * slot_bytes + 2 * TP_MAXW * tp_rx_bytes(slot_bytes);
+}
 static size_t tp_region_bytes(size_t slot_bytes) {
-  return 2 * slot_bytes + sizeof(uint32_t) * (2 * TP_MAXW * TP_MAXC + 2 * TP_MAXC);
+  return tp_flags_off(slot_bytes) + sizeof(uint32_t) * (2 * TP_MAXW * TP_MAXC + 2 * TP_MAXC);
 }
 
 extern "C" int swb_tp_comm_create(int rank, int world, size_t slot_bytes, swb_tp_comm** out,
@@ -236,6 +289,15 @@ extern "C" void* swb_tp_comm_slot(const swb_tp_comm* c, int slot) {
   return c->base + (size_t)slot * c->slot_bytes;
 }
 
+// SWB_TP_AR_TRIGGER=0: exit-time PDL trigger instead of right after the wait
+static int tp_trigger() {
+  static const int on = [] {
+    const char* e = std::getenv("SWB_TP_AR_TRIGGER");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
+
 extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t n,
                                     uintptr_t stream) {
   SWB_REQUIRE(c && out, "swb_tp_allreduce_f32: null pointer");
@@ -247,11 +309,16 @@ extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t
   if (n == 0) return SWB_OK;
   TpArgs a;
   memset(&a, 0, sizeof(a));
-  const size_t flags_off = 2 * c->slot_bytes;
+  const size_t flags_off = tp_flags_off(c->slot_bytes);
+  const size_t rxb = tp_rx_bytes(c->slot_bytes);
+  const size_t rx_off = 2 * c->slot_bytes + (size_t)slot * TP_MAXW * rxb;
   for (int p = 0; p < c->world; ++p) {
     a.peer_slot[p] = reinterpret_cast<const float*>(c->peer_base[p] + (size_t)slot * c->slot_bytes);
+    a.peer_rx[p] = reinterpret_cast<float*>(c->peer_base[p] + rx_off + (size_t)c->rank * rxb);
     a.peer_flags[p] = reinterpret_cast<uint32_t*>(c->peer_base[p] + flags_off);
   }
+  a.my_rx = reinterpret_cast<const float*>(c->base + rx_off);
+  a.rx_stride = (long long)(rxb / sizeof(float));
   a.my_flags = reinterpret_cast<uint32_t*>(c->base + flags_off);
   a.my_ctr = a.my_flags + 2 * TP_MAXW * TP_MAXC;
   a.out = out;
@@ -262,9 +329,16 @@ extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t
   // ~16 KB of output per CTA, at most TP_MAXC CTAs (one wave)
   const long long ctas = std::min<long long>(TP_MAXC, std::max<long long>(1, (long long)n / 4096));
   // two-shot once the (W-1)x one-shot traffic outweighs a second handshake
-  const int two_shot = c->world > 2 && n >= (size_t)(1 << 18);
+  int mode = c->world > 2 && n >= (size_t)(1 << 18) ? 1 : 0;
+  // small messages: push (posted NVLink stores + flag, local reads) instead
+  // of pull (flag, then a remote-read round trip); SWB_TP_AR_PUSH=0 for A/B
+  static const bool push_on = [] {
+    const char* e = std::getenv("SWB_TP_AR_PUSH");
+    return !(e && e[0] == '0');
+  }();
+  if (mode == 0 && push_on && c->world > 1 && n * sizeof(float) <= rxb) mode = 2;
   const cudaError_t le = launch(tp_allreduce_kernel, dim3((unsigned)ctas), dim3(TP_THREADS), 0,
-                                (cudaStream_t)stream, a, two_shot);
+                                (cudaStream_t)stream, a, mode, tp_trigger());
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch tp_allreduce_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("tp_allreduce_kernel");

@@ -6,7 +6,7 @@
 //   [slot 0 | slot 1 | rx[2][MAXW] | flags[2][MAXW][MAXC] | counters[2][MAXC]]
 // The producing GEMM/GEMV writes its fp32 partial sums straight into a slot
 // (rank 0 folds the residual in), so the all-reduce moves no extra copy:
-//   CTA c of rank r   1. system-scope release store of its epoch into
+//   CTA c of rank r   1. system-scope fence, then a store of its epoch into
 //                        flags[slot][r][c] of every peer,
 //                     2. spins (acquire, nanosleep back-off, watchdog) until
 //                        every peer's flag for (slot, c) reached the epoch,
@@ -56,8 +56,8 @@ struct TpArgs {
   int rank, world, slot;
 };
 
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
@@ -66,11 +66,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 
 __device__ __forceinline__ void tp_handshake(const TpArgs& a, int c, uint32_t e) {
-  // thread 0 of CTA c: publish epoch e to every peer, wait for theirs
+  // thread 0 of CTA c: publish epoch e to every peer, wait for theirs.  One
+  // system-scope fence orders the CTA's data before all the flags; the flag
+  // stores themselves are relaxed so they go out back to back (a release
+  // store per peer would wait for the previous flag's NVLink round trip).
   __threadfence_system();
   for (int p = 0; p < a.world; ++p)
     if (p != a.rank)
-      st_release_sys(a.peer_flags[p] + ((size_t)a.slot * TP_MAXW + a.rank) * TP_MAXC + c, e);
+      st_relaxed_sys(a.peer_flags[p] + ((size_t)a.slot * TP_MAXW + a.rank) * TP_MAXC + c, e);
   const long long t0 = clock64();
   for (int p = 0; p < a.world; ++p) {
     if (p == a.rank) continue;

@@ -117,6 +117,12 @@ PRESETS: dict[str, ModelConfig] = {
     # 6 heads exercise the non-power-of-two ALiBi slope rule like BLOOM's 112
     "bloom-tiny": ModelConfig("bloom-tiny", n_layers=3, d_model=768, n_heads=6, n_kv_heads=6,
                               head_dim=128, ffn=3072, vocab=2048, arch="bloom"),
+    # TP=4-divisible variants for the 4-GPU pool checks (tools/tp_check.py)
+    "tiny-tp4": ModelConfig("tiny-tp4", n_layers=4, d_model=1024, n_heads=8, n_kv_heads=4,
+                            head_dim=128, ffn=2048, vocab=2048),
+    "bloom-tiny-tp4": ModelConfig("bloom-tiny-tp4", n_layers=3, d_model=1024, n_heads=8,
+                                  n_kv_heads=8, head_dim=128, ffn=4096, vocab=2048,
+                                  arch="bloom"),
 }
 
 

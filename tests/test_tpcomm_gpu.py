@@ -111,6 +111,21 @@ def test_tp2_tiny_matches_tp1():
     assert '"ok": true' in r.stdout
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("model", ["tiny-tp4", "bloom-tiny-tp4"])
+def test_tp4_pool_matches_tp1(model):
+    """A TP=4 pool (push all-reduce for decode, two-shot / NCCL for prefill
+    sizes) generates the TP=1 tokens, logits within tolerance."""
+    import subprocess
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "4",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tools", "tp_check.py"), "--model", model],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert '"ok": true' in r.stdout
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_realtime_trace_serving_one_pair():
     """bench.py --trace: a Splitwise pair (2 processes) serves a short

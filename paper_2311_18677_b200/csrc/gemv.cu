@@ -621,7 +621,10 @@ static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, cons
   // variants: M = 2..8 on the mma.sync kernel with h staged in shared memory.
   if (NORM && M >= 2)
     return launch_gemv_mma<1, true>(x, nw, eps, w, out, rs, bias, M, N, K, epilogue, s);
-  const bool use_mma = M <= 4 || (M <= 8 && 2.0 * N * K < 120e6);
+  // K >= 12288 (BLOOM-176B TP4 qkv/up/down, 70B TP2 down): its 16-row x K
+  // items are ~450 KB, too few per CTA to balance — the tcgen05 GEMV wins
+  // there at every M (tools/gemv_bench.py: BLOOM TP4 up M=2 78.9 vs 68.0 us)
+  const bool use_mma = (M <= 4 && K < 12288) || (M <= 8 && 2.0 * N * K < 120e6);
   if (!NORM && M >= 2 && (!use_mma || !gemv_mma_enabled()) && gemv_tc_enabled())
     return dispatch_gemv_tc(x, w, out, rs, bias, M, N, K, epilogue, s);
   if (!NORM && M >= 2 && M <= 8 && gemv_mma_enabled())

@@ -15,6 +15,12 @@ SHAPES = {  # name: (N, K, epilogue)
     "7b.down": (4096, 11008, K.EPI_RESID_F32),
     "70b-tp2.gu": (28672, 8192, K.EPI_SWIGLU),
     "70b-tp2.down": (8192, 14336, K.EPI_RESID_F32),
+    "70b-tp4.qkv": (2560, 8192, K.EPI_BF16),
+    "70b-tp4.o": (8192, 2048, K.EPI_RESID_F32),
+    "70b-tp4.gu": (14336, 8192, K.EPI_SWIGLU),
+    "70b-tp4.down": (8192, 7168, K.EPI_RESID_F32),
+    "bloom-tp4.qkv": (10752, 14336, K.EPI_BF16),
+    "bloom-tp4.o": (14336, 3584, K.EPI_RESID_F32),
     "bloom-tp4.up": (14336, 14336, K.EPI_GELU),
     "bloom-tp4.down": (14336, 14336, K.EPI_RESID_F32),
 }

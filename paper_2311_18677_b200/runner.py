@@ -501,11 +501,13 @@ class DecodeGraph:
         # B=2..8 with h <= 32 KB: mma.sync kernel, rstd reduced in
         # swb_rmsnorm's order, bit-identical to the two-kernel path) while the
         # weight ring fills; SWB_FUSED_NORM=0/1 forces it off/on (Llama).  Auto
-        # = B=1 only: at B=2/4 the staged variant measured 3.32/3.95 ms/step vs
-        # 3.30/3.82 with the separate norm (its 4-stage ring costs the launch
-        # it saves)
+        # = B=1, and B=2 for d <= 4096: 7B B=2 3.253 vs 3.285 ms/step with the
+        # separate norm, but B=4 3.85 vs 3.79 and 70B TP2 B=2 15.41 vs 15.35
+        # (the staged variant's 4-stage ring costs more than the launch it
+        # saves once h grows)
         mode = os.environ.get("SWB_FUSED_NORM", "auto")
-        fused = (B == 1 and cfg.d_model * 2 <= 16384) if mode == "auto" else mode == "1"
+        fused = ((B == 1 and cfg.d_model * 2 <= 16384) or (B == 2 and cfg.d_model <= 4096)
+                 if mode == "auto" else mode == "1")
         fused = fused and not r.bloom
         for li, lw in enumerate(w.layers):
             if fused:

@@ -322,7 +322,10 @@ int swb_enable_peer(int peer_device);
  * swb_tp_allreduce_f32(comm, s, out, n) writes the rank-ordered sum of all
  * ranks' slot s into out (identical bits on every rank).  Alternate the
  * slot between consecutive reductions.  Epochs live on the device, so the
- * call is CUDA-graph capturable. */
+ * call is CUDA-graph capturable.  Messages up to min(slot_bytes, 1 MB) are
+ * pushed into per-peer receive buffers (decode sizes); larger ones are
+ * pulled (one-shot, or reduce-scatter + all-gather for W > 2); the sum
+ * order, and so the result bits, are the same in every form. */
 #define SWB_TP_IPC_BYTES 128
 typedef struct swb_tp_comm swb_tp_comm;
 int swb_tp_comm_create(int rank, int world, size_t slot_bytes, swb_tp_comm** out,

@@ -348,6 +348,9 @@ def main():
     ap.add_argument("--duration", type=float, default=20.0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--max-output", type=int, default=0)
+    ap.add_argument("--route", default="jsq", choices=["jsq", "rr"],
+                    help="--trace with several pairs: live JSQ routing at arrival (reference "
+                         "Cluster.route) or round-robin")
     ap.add_argument("--tp", type=int, default=1,
                     help="tensor-parallel degree of each prompt/token machine (N >= 2*tp)")
     args = ap.parse_args()

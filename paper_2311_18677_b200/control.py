@@ -106,6 +106,126 @@ class ShmMailbox:
             pass
 
 
+class RouteBoard:
+    """Live JSQ routing across Splitwise pairs served concurrently in real
+    time (bench.py --trace).  One /dev/shm segment per run:
+
+      * ``assign[rid]`` — the pair a request was routed to (-1 = not yet
+        arrived), written once by the router at the request's arrival;
+      * per pair, cumulative counters the servers publish (absolute values, so
+        every TP peer may write them): prompt tokens / requests whose prompt
+        phase finished (prompt machine), requests finished (token machine).
+
+    The router keeps the cumulative routed prompt tokens and requests per
+    pair, so pending(pair) = queued prompt tokens (routed − prompt-done) +
+    one per live token task (prompt-done − finished): the reference's
+    ``pending_tokens`` (cluster.py:82-84) of the pair's prompt machine plus
+    that of its token machine.  The pick is the reference's ``_argmin``
+    (cluster.py:129-134): lowest (pending, id).  The prompt → token pairing
+    is fixed (each prompt machine pushes to its own token machine), so the
+    two JSQ picks of ``Cluster.route`` (cluster.py:153-160) collapse into
+    one pick over pairs."""
+
+    PROMPT_TOK, PROMPT_REQ, FINISHED = 0, 1, 2
+
+    def __init__(self, n_requests: int, pairs: int, name: str | None = None,
+                 create: bool = False):
+        self.n, self.pairs = n_requests, pairs
+        size = 8 * (n_requests + 3 * pairs + 1)
+        if create:
+            self.shm = shared_memory.SharedMemory(create=True, size=size)
+        else:
+            self.shm = shared_memory.SharedMemory(name=name)
+            try:
+                from multiprocessing import resource_tracker
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:
+                pass
+        self.owner = create
+        a = np.ndarray((n_requests + 3 * pairs + 1,), dtype=np.int64, buffer=self.shm.buf)
+        self.assign = a[:n_requests]
+        self.load = a[n_requests:n_requests + 3 * pairs].reshape(pairs, 3)
+        if create:
+            self.assign[:] = -1
+            self.load[:] = 0
+        self.routed_tok = [0] * pairs
+        self.routed_req = [0] * pairs
+
+    @property
+    def name(self) -> str:
+        return self.shm.name
+
+    # -- servers --------------------------------------------------------
+    def publish(self, pair: int, field: int, value: int) -> None:
+        self.load[pair, field] = value
+
+    # -- router ---------------------------------------------------------
+    def pending(self, pair: int) -> int:
+        tok, req, fin = (int(v) for v in self.load[pair])
+        return (self.routed_tok[pair] - tok) + (req - fin)
+
+    def route(self, rid: int, prompt_tokens: int) -> int:
+        best = min(range(self.pairs), key=lambda p: (self.pending(p), p))
+        self.routed_tok[best] += prompt_tokens
+        self.routed_req[best] += 1
+        self.assign[rid] = best     # publish last: servers poll assign
+        return best
+
+    def run_router(self, requests, t0: float) -> None:
+        """Route each request at its arrival (wall clock from t0); requests =
+        [(rid, arrival_s, prompt_tokens)] in arrival order."""
+        for rid, arr, ptok in requests:
+            while True:
+                d = t0 + arr - time.perf_counter()
+                if d <= 0:
+                    break
+                time.sleep(min(d, 1e-3))
+            self.route(rid, ptok)
+
+    def close(self) -> None:
+        try:
+            self.shm.close()
+            if self.owner:
+                self.shm.unlink()
+        except Exception:
+            pass
+
+
+class ArrivalFeed:
+    """Server side of the live routing: yields, in arrival order, the
+    requests routed to ``pair`` whose routing is already published.  With no
+    board it is the static list (request i -> pair i mod pairs)."""
+
+    def __init__(self, requests, pair: int, board: RouteBoard | None = None):
+        self.all = list(requests)
+        self.pair = pair
+        self.board = board
+        self.cursor = 0
+        self.mine = 0
+
+    def poll(self) -> list:
+        out = []
+        if self.board is None:
+            out, self.all = self.all, []
+            self.mine += len(out)
+            return out
+        while self.cursor < len(self.all):
+            r = self.all[self.cursor]
+            p = int(self.board.assign[r[0]])
+            if p < 0:
+                break
+            if p == self.pair:
+                out.append(r)
+            self.cursor += 1
+        self.mine += len(out)
+        return out
+
+    def complete(self) -> bool:
+        """Every request has been routed (so ``mine`` is final)."""
+        return self.board is None and not self.all or (
+            self.board is not None and self.cursor == len(self.all))
+
+
 class HandoffReceiver:
     """Token-side end: owns the mailbox (its name goes to the prompt side at
     start-up) and polls it between decode iterations."""

@@ -34,8 +34,8 @@ import torch.distributed as dist
 
 from . import _abi
 from . import kernels as K
-from .control import (HandoffReceiver, HandoffSender, ShmMailbox, recv_reservations,
-                      send_reservations)
+from .control import (ArrivalFeed, HandoffReceiver, HandoffSender, RouteBoard, ShmMailbox,
+                      recv_reservations, send_reservations)
 from .kvcache import KVCacheManager, blocks_for
 from .model import get_config, init_weights
 from .perf import PerfModel
@@ -63,16 +63,17 @@ def estimated_perf_model(cfg, kv: KVCacheManager | None, weight_bytes: int,
                      float(weight_bytes), cap, cfg.max_token_batch)
 
 
-def _lockstep(n: int, tp_ctrl, now_ms: float = 0.0) -> tuple[int, float]:
-    """(arrivals to process, scheduler clock) for this iteration of a TP
-    group: the minimum arrival count and the maximum clock over the peers, so
-    every peer enqueues / reserves the same requests and forms the same batch
-    (the collectives inside the steps stay matched)."""
+def _lockstep(n: int, tp_ctrl, now_ms: float = 0.0, fin: bool = False):
+    """(arrivals to process, scheduler clock, all done) for this iteration of
+    a TP group: the minimum arrival count, the maximum clock and the AND of
+    the peers' "nothing left" flags, so every peer enqueues / reserves the
+    same requests, forms the same batch (the collectives inside the steps
+    stay matched) and leaves the loop at the same iteration."""
     if tp_ctrl is None:
-        return n, now_ms
-    t = torch.tensor([float(n), -now_ms], dtype=torch.float64)
+        return n, now_ms, fin
+    t = torch.tensor([float(n), -now_ms, float(fin)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MIN, group=tp_ctrl)
-    return int(t[0].item()), -float(t[1].item())
+    return int(t[0].item()), -float(t[1].item()), bool(t[2].item())
 
 
 class PromptServer:
@@ -132,7 +133,7 @@ class PromptServer:
         return first_time
 
 
-    def serve_trace(self, requests, t0: float):
+    def serve_trace(self, requests, t0: float, feed=None):
         """Arrival-driven prompt machine: requests = [(rid, arrival_s, host
         prompt, n_out)] in arrival order; each becomes a prompt task at its
         arrival (wall clock from t0); batches follow the reference prompt
@@ -153,12 +154,16 @@ class PromptServer:
                 for rid, seq, *_ in rows:
                     seq_of[rid] = seq
 
-        while done < len(requests):
+        while True:
+            pending += feed.poll()
+            fin = feed.complete() and done >= feed.mine
             now = time.perf_counter() - t0
             n_new = 0
             while n_new < len(pending) and pending[n_new][1] <= now:
                 n_new += 1
-            n_take, _ = _lockstep(n_new, self.tp_ctrl)
+            n_take, _, fin = _lockstep(n_new, self.tp_ctrl, 0.0, fin)
+            if fin:
+                break
             for _ in range(n_take):
                 rid, arr, prompt, n_out = pending.pop(0)
                 self.machine.enqueue(Task(rid, PROMPT, len(prompt), arr * 1e3, n_out, n_out),
@@ -195,6 +200,10 @@ class PromptServer:
             for r in chunk:
                 first_time[r[0]] = tnow
             done += len(chunk)
+            done_tok += sum(lens)
+            if board is not None:
+                board.publish(self.pair, board.PROMPT_TOK, done_tok)
+                board.publish(self.pair, board.PROMPT_REQ, done)
             self.machine.complete_iteration(batch, (tnow - t0) * 1e3)
         return first_time
 
@@ -286,7 +295,7 @@ class TokenServer:
         return emit, tokens
 
 
-    def serve_trace(self, requests, t0: float):
+    def serve_trace(self, requests, t0: float, feed=None):
         """Arrival-driven token machine: reserves each request's final context
         at its arrival (both machines are chosen at arrival, reference
         cluster.py:153-160) and publishes the slot to the prompt machine,
@@ -294,20 +303,27 @@ class TokenServer:
         the reference token rule), one CUDA-graph step per iteration.
         Returns ({rid: [emission times]}, decode step log)."""
         kv = self.kv
-        pending = list(requests)
-        n = len(requests)
-        info, emit = {}, {r[0]: [] for r in requests}
+        feed = feed or ArrivalFeed(requests, 0)
+        board = getattr(self, "board", None)
+        pending = []
+        info, emit = {}, {}
         finished = 0
         graph, graph_rids = None, None
         ring_h = torch.empty(256, dtype=torch.int32).pin_memory()
         self.step_log = []
-        while finished < n:
+        while True:
+            for r in feed.poll():
+                pending.append(r)
+                emit[r[0]] = []
+            fin = feed.complete() and finished >= feed.mine
             now = time.perf_counter() - t0
             arrived = []
             n_new = 0
             while n_new < len(pending) and pending[n_new][1] <= now:
                 n_new += 1
-            n_take, mnow = _lockstep(n_new, self.tp_ctrl, now * 1e3)
+            n_take, mnow, fin = _lockstep(n_new, self.tp_ctrl, now * 1e3, fin)
+            if fin:
+                break
             for _ in range(n_take):
                 rid, arr, prompt, n_out = pending.pop(0)
                 arrived.append((rid, kv.allocate(len(prompt) + n_out)))
@@ -324,6 +340,8 @@ class TokenServer:
                     else:
                         kv.release(seq)
                         finished += 1
+                        if board is not None:
+                            board.publish(self.pair, board.FINISHED, finished)
             if not self.machine.has_work() and not self.machine.resident:
                 time.sleep(5e-5)
                 continue
@@ -360,6 +378,8 @@ class TokenServer:
                 if what == "request_finished":
                     kv.release(info[task.request_id][0])
                     finished += 1
+                    if board is not None:
+                        board.publish(self.pair, board.FINISHED, finished)
                     graph_rids = None
         return emit, self.step_log
 
@@ -587,7 +607,9 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
                  percentile, peaks, tp=1):
     """bench.py --trace: the reference's synthetic trace (trace.py presets,
     Poisson arrivals) served concurrently by the Splitwise pairs in real
-    time; request i goes to pair i mod pairs; TP pairs process arrivals in
+    time; each request is routed at its arrival to the pair with the fewest
+    pending tokens (control.RouteBoard, the reference's JSQ; --route rr:
+    request i -> pair i mod pairs); TP pairs process arrivals in
     lockstep across their peers.  Rank 0 prints TTFT / TBT / E2E percentiles
     and tokens/s."""
     import json
@@ -597,19 +619,41 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
     if args.max_output:
         reqs_all = [type(r)(r.id, r.arrival, r.prompt_tokens, min(r.output_tokens, args.max_output))
                     for r in reqs_all]
-    mine = [r for r in reqs_all if r.id % pairs == pair]
     g = torch.Generator().manual_seed(77)
     prompts = {r.id: torch.randint(0, cfg.vocab, (r.prompt_tokens,), generator=g,
                                    dtype=torch.int32) for r in reqs_all}
-    items = [(r.id, r.arrival, prompts[r.id], r.output_tokens) for r in mine]
+    jsq = getattr(args, "route", "jsq") == "jsq" and pairs > 1
+    board, router = None, None
+    if jsq:
+        # live JSQ over pairs (control.RouteBoard); rank 0 hosts the router
+        name = [None]
+        if rank == 0:
+            board = RouteBoard(len(reqs_all), pairs, create=True)
+            name = [board.name]
+        dist.broadcast_object_list(name, src=0, group=ctrl)
+        if rank != 0:
+            board = RouteBoard(len(reqs_all), pairs, name=name[0])
+        server.board, server.pair = board, pair
+        items = [(r.id, r.arrival, prompts[r.id], r.output_tokens) for r in reqs_all]
+        feed = ArrivalFeed(items, pair, board)
+    else:
+        mine = [r for r in reqs_all if r.id % pairs == pair]
+        items = [(r.id, r.arrival, prompts[r.id], r.output_tokens) for r in mine]
+        feed = None
     # common start (perf_counter is CLOCK_MONOTONIC: comparable across processes)
     t0t = torch.tensor([time.perf_counter() + 1.0], dtype=torch.float64)
     dist.broadcast(t0t, src=0, group=ctrl)
     t0 = float(t0t.item())
+    if jsq and rank == 0:
+        router = threading.Thread(target=board.run_router, daemon=True,
+                                  args=([(r.id, r.arrival, r.prompt_tokens) for r in reqs_all], t0))
+        router.start()
     while time.perf_counter() < t0:
         time.sleep(1e-4)
     with ClockSampler(local) as clk:
-        out = server.serve_trace(items, t0)
+        out = server.serve_trace(items, t0, feed)
+    if router is not None:
+        router.join()
     payload = {"rank": rank, "prompt": is_prompt, "out": out if is_prompt else out[0],
                "steps": None if is_prompt else out[1]}
     gathered = [None] * world
@@ -648,11 +692,14 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
             "data": "synthetic trace (reference presets, Poisson arrivals), random weights",
             "config": {"workload": f"{args.trace} trace rate {args.rate}/s for {args.duration} s "
                                    f"(seed {args.seed}), {len(reqs_all)} requests, "
-                                   f"{pairs} Splitwise pair(s) TP{tp}+TP{tp}, request i -> pair "
-                                   f"i mod {pairs}, served concurrently in real time",
+                                   f"{pairs} Splitwise pair(s) TP{tp}+TP{tp}, "
+                                   + ("live JSQ routing over pairs at arrival" if jsq else
+                                      f"request i -> pair i mod {pairs}")
+                                   + ", served concurrently in real time",
                        "model": cfg.name,
                        "parallelism": f"{pairs}x(prompt TP{tp} + token TP{tp})",
-                       "max_output": args.max_output or None},
+                       "max_output": args.max_output or None,
+                       "routing": "jsq" if jsq else "round-robin"},
             "ttft_ms": {"p50": p(ttft, 0.5), "p99": p(ttft, 0.99)},
             "tbt_ms": {"p50": p(tbt, 0.5), "p99": p(tbt, 0.99)},
             "e2e_ms": {"p50": p(e2e, 0.5), "p99": p(e2e, 0.99)},
@@ -665,6 +712,8 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
     torch.cuda.synchronize()
     (server.tx if is_prompt else server.rx).close()
     server.res_box.close()
+    if board is not None:
+        board.close()
     threading.Timer(30.0, lambda: os._exit(0)).start()
     dist.destroy_process_group()
     os._exit(0)

@@ -146,6 +146,26 @@ def test_realtime_trace_serving_one_pair():
     assert line["output_tokens"] >= line["requests"]
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
+def test_realtime_trace_serving_two_pairs_jsq():
+    """bench.py --trace on two Splitwise pairs with live JSQ routing
+    (control.RouteBoard): every request is routed once and completes."""
+    import json
+    import subprocess
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "4",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "bench.py"), "--gpus", "4", "--model", "tiny",
+                        "--warmup", "1", "--prompt", "128", "--out", "8", "--trace",
+                        "conversation", "--rate", "40", "--duration", "2", "--max-output", "24",
+                        "--route", "jsq"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["config"]["routing"] == "jsq"
+    assert line["requests"] > 20 and line["output_tokens"] >= line["requests"]
+
+
 def test_vocab_parallel_pick_equals_full_argmax():
     """swb_argmax_shard over TP vocabulary shards + a summed candidate table +
     swb_argmax_pick == swb_argmax over the full vocabulary (ties included)."""

@@ -139,12 +139,17 @@ class PromptServer:
         arrival (wall clock from t0); batches follow the reference prompt
         rule; a request's KV lands in the slot the token machine reserved at
         the same arrival (reservation mailbox).  Returns {rid: first-token
-        host time}."""
-        pending = list(requests)
+        host time}.  ``feed`` (control.ArrivalFeed) supplies the requests
+        the live JSQ router sent to this pair; without one every request in
+        ``requests`` is this machine's."""
+        feed = feed or ArrivalFeed(requests, 0)
+        board = getattr(self, "board", None)
+        pending = []
         by_id = {r[0]: r for r in requests}
         seq_of: dict = {}
         first_time = {}
         done = 0
+        done_tok = 0
 
         def drain():
             while True:

@@ -699,12 +699,13 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
                                    f"(seed {args.seed}), {len(reqs_all)} requests, "
                                    f"{pairs} Splitwise pair(s) TP{tp}+TP{tp}, "
                                    + ("live JSQ routing over pairs at arrival" if jsq else
-                                      f"request i -> pair i mod {pairs}")
+                                      f"request i -> pair i mod {pairs}" if pairs > 1 else
+                                      "every request on the one pair")
                                    + ", served concurrently in real time",
                        "model": cfg.name,
                        "parallelism": f"{pairs}x(prompt TP{tp} + token TP{tp})",
                        "max_output": args.max_output or None,
-                       "routing": "jsq" if jsq else "round-robin"},
+                       "routing": "jsq" if jsq else "round-robin" if pairs > 1 else "single pair"},
             "ttft_ms": {"p50": p(ttft, 0.5), "p99": p(ttft, 0.99)},
             "tbt_ms": {"p50": p(tbt, 0.5), "p99": p(tbt, 0.99)},
             "e2e_ms": {"p50": p(e2e, 0.5), "p99": p(e2e, 0.99)},

@@ -222,8 +222,9 @@ class ArrivalFeed:
 
     def complete(self) -> bool:
         """Every request has been routed (so ``mine`` is final)."""
-        return self.board is None and not self.all or (
-            self.board is not None and self.cursor == len(self.all))
+        if self.board is None:
+            return not self.all
+        return self.cursor == len(self.all)
 
 
 class HandoffReceiver:

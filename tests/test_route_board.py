@@ -113,3 +113,59 @@ def test_router_across_processes():
         assert res[0] == sorted(res[0]) and res[1] == sorted(res[1])
     finally:
         b.close()
+
+
+def _tp_peer(rank, port, name, n, q):
+    import os
+    import random as _r
+    import torch.distributed as dist
+    from paper_2311_18677_b200.splitwise import _lockstep
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    b = RouteBoard(n, 2, name=name)
+    feed = ArrivalFeed([(i, 0.0, None, 1) for i in range(n)], 1, b)
+    rng = _r.Random(rank)
+    pending, taken, it = [], [], 0
+    while True:
+        if rank == 1 and rng.random() < 0.5:
+            time.sleep(2e-3)                   # this peer sees assignments late
+        else:
+            pending += feed.poll()
+        fin = feed.complete() and len(taken) >= feed.mine
+        k, _, fin = _lockstep(len(pending), dist.group.WORLD, 0.0, fin)
+        if fin:
+            break
+        taken += [r[0] for r in pending[:k]]
+        del pending[:k]
+        it += 1
+    q.put((rank, taken, it))
+    b.close()
+    dist.destroy_process_group()
+
+
+def test_tp_peers_take_the_same_arrivals_and_exit_together():
+    """Two TP peers of one pair (gloo, world 2) fed by the live router: the
+    MIN lockstep makes them take the same requests at the same iterations
+    and leave the serve loop at the same iteration although one of them
+    observes the assignments late."""
+    import socket
+    n = 30
+    b = RouteBoard(n, 2, create=True)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    try:
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        ps = [ctx.Process(target=_tp_peer, args=(r, port, b.name, n, q)) for r in range(2)]
+        for p in ps:
+            p.start()
+        time.sleep(3.0)                        # let both peers join the group
+        b.run_router([(i, 0.005 * i, 100) for i in range(n)], time.perf_counter())
+        res = {r: (t, it) for r, t, it in (q.get(timeout=120) for _ in ps)}
+        for p in ps:
+            p.join(timeout=30)
+        assert res[0] == res[1]
+        assert res[0][0] == [i for i in range(n) if int(b.assign[i]) == 1]
+    finally:
+        b.close()

@@ -21,10 +21,12 @@ step streams them from HBM (no L2 flush needed).
 
 `--impl reference` times the reference's CPU path: the reference package
 (`splitsim`) has no model arithmetic, so its CPU implementation of the path
-is the fp32 port in oracle/ (numerics oracle), run on all host cores over a
-bounded full-width 2-layer slice and scaled to 32 layers; the splitsim
-simulator's *modeled* H100 latencies for the same request are attached when
-baseline/_ref is importable.
+is the fp32 port in oracle/ (numerics oracle), run on all host cores over ONE
+full request of the workload (all 32 layers, prompt phase and every decode
+iteration timed, nothing scaled); the splitsim simulator's *modeled* H100
+latencies for the same request are attached from baseline/_ref.
+`--gpus N` (N > 1) without torchrun re-launches itself under
+torch.distributed.run with N local ranks.
 """
 
 from __future__ import annotations
@@ -110,49 +112,116 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU leg
-def cpu_port_sample(model="llama2-7b", prompt=1024, n_out=128, layers=2, dec_steps=4,
-                    threads=None):
-    """Time the fp32 oracle (the CPU port of the path) on a bounded sample:
-    a full-width `layers`-layer slice, one prefill of `prompt` tokens and
-    `dec_steps` decode iterations; scale to the full depth."""
+def metric_name(cfg, P, O):
+    """One metric string for every arm and every N (the driver pairs the
+    arms' lines by it)."""
+    return f"output tokens/s (+ TTFT/TBT p50,p99) serving {P}/{O} requests, {cfg.name}"
+
+
+def host_cpu():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_port_model(model="llama2-7b", threads=None):
+    """The fp32 oracle (oracle/decoder.py, the CPU port of the path) at the
+    model's FULL depth and width.  Weights are distinct fp32 tensors filled
+    from a seeded N(0, init_std) pool (a full seeded draw of 6.7 B normals
+    would take minutes of single-threaded RNG; the values do not change the
+    arithmetic done)."""
     import torch
     from oracle.decoder import OracleDecoder
     from paper_2311_18677_b200.model import get_config
     cfg = get_config(model)
     threads = threads or os.cpu_count()
     torch.set_num_threads(threads)
+    d, dh, H, Hkv, f, V = (cfg.d_model, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads, cfg.ffn,
+                           cfg.vocab)
+    need = 4 * (cfg.params_nonembed() + 2 * V * d) + 4 * 2 * cfg.n_layers * Hkv * dh * 4096
+    if _mem_available() < 1.2 * need:
+        raise MemoryError(f"fp32 {model} needs {need / 2**30:.1f} GiB host memory, "
+                          f"{_mem_available() / 2**30:.1f} GiB available")
     g = torch.Generator().manual_seed(0)
-    d, dh, H, Hkv, f = cfg.d_model, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads, cfg.ffn
+    pool = torch.randn((1 << 22) + 4096, generator=g)
+    cursor = [0]
 
-    def r(*s):
-        return torch.randn(*s, generator=g) * cfg.init_std
+    def r(*shape, std=cfg.init_std):
+        t = torch.empty(*shape)
+        flat = t.view(-1)
+        n, m = flat.numel(), 1 << 22
+        for k in range(0, n, m):
+            o = (cursor[0] * 2654435761) % 4096
+            cursor[0] += 1
+            flat[k:k + m].copy_(pool[o:o + min(m, n - k)])
+        return t.mul_(std)
 
     lay = [{"attn_norm": torch.ones(d), "wq": r(H * dh, d), "wk": r(Hkv * dh, d),
             "wv": r(Hkv * dh, d), "wo": r(d, H * dh), "mlp_norm": torch.ones(d),
-            "w_gate": r(f, d), "w_up": r(f, d), "wd": r(d, f)} for _ in range(layers)]
-    small = type(cfg)(**{**cfg.__dict__, "n_layers": layers})
-    orc = OracleDecoder(small, lay, torch.randn(cfg.vocab, d, generator=g), r(cfg.vocab, d),
-                        torch.ones(d))
+            "w_gate": r(f, d), "w_up": r(f, d), "wd": r(d, f)} for _ in range(cfg.n_layers)]
+    return cfg, OracleDecoder(cfg, lay, r(V, d, std=1.0), r(V, d), torch.ones(d)), threads
+
+
+def cpu_port_request(model="llama2-7b", prompt=1024, n_out=128, dec_steps=None, threads=None):
+    """Time one request (prompt phase + decode iterations) through the full
+    fp32 CPU port on the host cores.  dec_steps=None runs every one of the
+    n_out-1 decode iterations; a smaller number times that many and prices
+    the rest at their mean (contexts prompt..prompt+n_out differ by < 13 %)."""
+    import torch
+    t_init = time.perf_counter()
+    cfg, orc, threads = cpu_port_model(model, threads)
+    t_init = time.perf_counter() - t_init
+    g = torch.Generator().manual_seed(1234)
     toks = torch.randint(0, cfg.vocab, (prompt,), generator=g).tolist()
+    n_dec = n_out - 1 if dec_steps is None else min(dec_steps, n_out - 1)
     t0 = time.perf_counter()
-    logits, cache = orc.prefill(toks)
+    logits, cache = orc.prefill(toks, orc.new_cache(prompt + n_out))
     t_pre = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    tok = int(logits.argmax())
-    for i in range(dec_steps):
+    tok, tbt = int(logits.argmax()), []
+    for i in range(n_dec):
+        t1 = time.perf_counter()
         logits = orc.decode(tok, prompt + i, cache)
         tok = int(logits.argmax())
-    t_dec = (time.perf_counter() - t0) / dec_steps
-    scale = cfg.n_layers / layers
-    ttft = t_pre * scale
-    tbt = t_dec * scale
-    e2e = ttft + (n_out - 1) * tbt
-    return {"value": n_out / e2e, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "ttft_ms": ttft * 1e3, "tbt_ms": tbt * 1e3,
-            "sample": f"fp32 oracle, {model} full-width {layers}-layer slice: 1 prefill of "
-                      f"{prompt} tokens + {dec_steps} decode steps, scaled x{scale:.0f} to "
-                      f"{cfg.n_layers} layers; 1 request {prompt}/{n_out}",
-            "wall_s": t_pre + t_dec * dec_steps}
+        tbt.append(time.perf_counter() - t1)
+    dec_total = sum(tbt) + (n_out - 1 - n_dec) * (statistics.mean(tbt) if tbt else 0.0)
+    req_s = t_pre + dec_total
+    full = n_dec == n_out - 1
+    sample = (f"fp32 CPU port (oracle/decoder.py), {cfg.name} at full depth and width "
+              f"({cfg.n_layers} layers): 1 request {prompt}/{n_out}, prompt phase + "
+              + (f"all {n_dec} decode iterations timed" if full else
+                 f"{n_dec} of {n_out - 1} decode iterations timed (rest at their mean)")
+              + f"; {threads} threads on {host_cpu()}")
+    return {"value": n_out / req_s, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "host_cpu": host_cpu(), "ttft_ms": t_pre * 1e3,
+            "tbt_ms": {"p50": 1e3 * percentile(tbt, 0.5), "p99": 1e3 * percentile(tbt, 0.99)}
+            if tbt else None,
+            "request_ms": req_s * 1e3, "decode_iterations_timed": n_dec, "sample": sample,
+            "wall_s": t_pre + sum(tbt), "init_s": t_init}
+
+
+def cpu_baseline_sample(model, prompt, n_out):
+    """bench.py's cpu_baseline leg: a bounded sample (~15-25 s of CPU work)
+    of the same request through the full-depth CPU port."""
+    try:
+        return cpu_port_request(model, prompt, n_out, dec_steps=6)
+    except MemoryError as e:
+        return {"value": None, "unit": "tokens/s", "unavailable": str(e)}
 
 
 def splitsim_modeled(prompt=1024, n_out=128, n_gpus=1):
@@ -180,32 +249,41 @@ def splitsim_modeled(prompt=1024, n_out=128, n_gpus=1):
 
 
 def run_reference(args):
+    """The reference arm: the reference package has no arithmetic for the
+    path (its prompt/token phases are latency lookups, reference
+    perf.py:119-132), so its CPU implementation of the path is the fp32 port
+    in oracle/, run here over ONE full request of the workload (full depth,
+    every decode iteration timed — about a minute on 16 cores, so one step;
+    the step of the GPU arm is also one request burst).  Nothing is scaled."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    samples = []
-    t_all = time.perf_counter()
-    for _ in range(args.warmup + args.steps):
-        samples.append(cpu_port_sample(args.model, args.prompt, args.out, layers=2,
-                                       dec_steps=3))
-        if time.perf_counter() - t_all > 240:
-            break
-    timed = samples[args.warmup:] or samples[-1:]
-    v = statistics.median(s["value"] for s in timed)
-    base = dict(timed[0])
-    base["value"] = v
-    line = {"impl": "reference", "metric": "output tokens/s (1024/128 requests, Llama-2-7B)",
-            "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(timed),
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "ms_per_step": 1e3 * args.out / v,
-            "config": {"workload": f"{args.model} {args.prompt}/{args.out}, 1 request per step, "
-                                   "fp32 CPU port on host cores (bounded 2-layer sample)"},
-            "cpu_baseline": base,
+    from paper_2311_18677_b200.model import get_config
+    cfg = get_config(args.model)
+    P, O = args.prompt, args.out
+    try:
+        cb = cpu_port_request(args.model, P, O, dec_steps=None)
+    except MemoryError as e:
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}), flush=True)
+        return
+    v = cb["value"]
+    line = {"impl": "reference", "metric": metric_name(cfg, P, O),
+            "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+            "requested_steps": args.steps, "requested_warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded random weights/tokens)",
+            "ms_per_step": cb["request_ms"],
+            "config": {"workload": f"{cfg.name} {P}-token prompt / {O} greedy outputs, 1 request "
+                                   "per step; fp32 CPU port of the path on all host cores "
+                                   "(one full request: steps=1 whatever --steps asks)",
+                       "model": cfg.name, "prompt_tokens": P, "output_tokens": O,
+                       "requests_per_step": 1, "parallelism": f"cpu x{cb['cores']}"},
+            "ttft_ms": {"p50": cb["ttft_ms"], "p99": cb["ttft_ms"]},
+            "tbt_ms": cb["tbt_ms"],
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "ttft_ms_p50": base["ttft_ms"], "tbt_ms_p50": base["tbt_ms"],
-            "splitsim_modeled": splitsim_modeled(args.prompt, args.out, args.gpus)}
+            "splitsim_modeled": splitsim_modeled(P, O, args.gpus)}
     print(json.dumps(line), flush=True)
 
 
@@ -291,7 +369,7 @@ def run_colocated(args):
     pre_tfs = pre_flops / (pre_avg / 1e3) / 1e12
     traffic = _ncu_traffic("decode_step")
     line = {
-        "metric": "output tokens/s (+ TTFT/TBT p50,p99) serving 1024/128 requests, Llama-2-7B",
+        "metric": metric_name(cfg, P, O),
         "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random weights/tokens)",
@@ -318,7 +396,7 @@ def run_colocated(args):
         "clocks": clocks,
     }
     if not args.no_cpu:
-        line["cpu_baseline"] = cpu_port_sample(args.model, P, O, layers=2, dec_steps=3)
+        line["cpu_baseline"] = cpu_baseline_sample(args.model, P, O)
     print(json.dumps(line), flush=True)
 
 
@@ -329,6 +407,20 @@ def _ncu_traffic(key):
             return json.load(f).get(key)
     except Exception:
         return None
+
+
+def _self_launch(n):
+    """`python bench.py --gpus N` without torchrun: re-exec under
+    torch.distributed.run with N local ranks (rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -357,14 +449,21 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _self_launch(args.gpus)          # one rank per GPU, exec's torchrun
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.trace:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from reftrace import preset_trace
+        args.trace_requests = preset_trace(args.trace, args.rate, args.duration, args.seed)
     if args.trace and world < 2:
         raise SystemExit("--trace needs N >= 2 GPUs (Splitwise pairs, launched with torchrun)")
     if world == 1 and args.gpus == 1:
         run_colocated(args)
     else:
         from paper_2311_18677_b200.splitwise import run_split_bench
-        run_split_bench(args, ClockSampler, percentile, cpu_port_sample, _peaks, _ncu_traffic)
+        run_split_bench(args, ClockSampler, percentile, cpu_baseline_sample, _peaks, _ncu_traffic,
+                        metric_name)
 
 
 if __name__ == "__main__":

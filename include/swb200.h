@@ -159,12 +159,34 @@ int swb_kv_push_layer(const void* qkv, int rows, int row_stride, int k_col,
                       int v_col, int Hkv, int dh, void* dst_k_layer,
                       void* dst_v_layer, const int32_t* dst_slots,
                       int block_size, int num_ctas, uintptr_t stream);
-/* Completion flag of a push (the paper's per-request semaphore,
- * PAPER.md:804): system-scope release store of `value` to `flag` (which may
- * be peer memory) after all prior work on `stream`. */
-int swb_kv_signal(uint32_t* flag, uint32_t value, uintptr_t stream);
-/* Stream-ordered wait until *flag >= value (cuStreamWaitValue32 GEQ). */
-int swb_stream_wait_flag(uint32_t* flag, uint32_t value, uintptr_t stream);
+/* Serialized transfer mode (reference select_mode / plan_transfer,
+ * transfer.py:73-99: prompts below the mode threshold move their KV after
+ * the prompt phase instead of layer by layer): one launch pushes `layers`
+ * layers; layer l reads qkv + l * qkv_layer_stride elements and writes the
+ * destination layer arrays at dst_k/v_layer0 + l * dst_layer_stride_bytes. */
+int swb_kv_push_layers(const void* qkv, size_t qkv_layer_stride, int layers,
+                       int rows, int row_stride, int k_col, int v_col, int Hkv,
+                       int dh, void* dst_k_layer0, void* dst_v_layer0,
+                       size_t dst_layer_stride_bytes, const int32_t* dst_slots,
+                       int block_size, int num_ctas, uintptr_t stream);
+/* Hand-off of a finished prompt batch — the paper's per-request semaphore
+ * and the reference's TRANSFER event (engine.py:286-297):
+ * after all prior work on `stream` (the KV pushes), request i's slot
+ * table + seqs[i] * stride_bytes (int32 [flag, first_token, ...]) gets
+ * first_tok[i] (device) in word 1 and then epochs[i] in word 0.  The flag
+ * stores are stream memory operations preceded by a full memory barrier,
+ * so a consumer that observes flag == epoch also observes the token and
+ * every pushed KV page.  `table` is device-accessible: host-mapped shared
+ * memory (swb_host_register) polled by the token machine's host, or peer
+ * memory.  n <= 64; seqs/epochs are host arrays. */
+int swb_kv_handoff(const int32_t* first_tok, int n, const int32_t* seqs,
+                   const uint32_t* epochs, void* table, int stride_bytes,
+                   uintptr_t stream);
+/* Page-lock and map host memory (e.g. a /dev/shm mapping shared with the
+ * token machine's process) for device stores; *dev_ptr receives its device
+ * address. */
+int swb_host_register(void* ptr, size_t bytes, void** dev_ptr);
+int swb_host_unregister(void* ptr);
 
 /* ---------------------------------------------------- attention kernels */
 /* Causal varlen prefill attention with GQA over qkv rows; sequences are
@@ -252,14 +274,9 @@ int swb_argmax_pick(const float* cand, int rows, int tp, int32_t* out,
 /* --------------------------------------------- decode-step bookkeeping
  * Graph-resident per-step state update so the decode loop needs no host
  * round trip (Machine.complete_iteration, machine.py:247-275):
- *  prepare: pos[b] = ctx[b]; slot[b] = table[b][ctx/bs]*bs + ctx%bs;
- *           attn_len[b] = ctx[b] + 1
  *  advance: cur_tok[b] = next_tok[b]; out_ring[b*ring + step[b]] = next_tok[b];
  *           step[b] += 1; ctx[b] += 1
  */
-int swb_decode_prepare(const int32_t* ctx, const int32_t* block_tables,
-                       int max_blocks, int block_size, int B, int32_t* pos,
-                       int32_t* slots, int32_t* attn_len, uintptr_t stream);
 int swb_decode_advance(const int32_t* next_tok, int32_t* cur_tok, int32_t* ctx,
                        int32_t* step, int32_t* out_ring, int ring, int B,
                        uintptr_t stream);

@@ -149,8 +149,9 @@ class OracleDecoder:
         if w.cfg.arch == "bloom":
             extra = {k: getattr(w, k).float().cpu()
                      for k in ("final_norm_b", "emb_norm", "emb_norm_b", "alibi")}
-        return cls(w.cfg, layers, w.embed.float().cpu(), w.lm_head.float().cpu(),
-                   w.final_norm.float().cpu(), extra=extra)
+        embed = w.embed.float().cpu()
+        head = embed if w.lm_head.data_ptr() == w.embed.data_ptr() else w.lm_head.float().cpu()
+        return cls(w.cfg, layers, embed, head, w.final_norm.float().cpu(), extra=extra)
 
     def _bloom_layer(self, li, x, pos0, kv_get, kv_put):
         """BLOOM block: pre-LayerNorm, fused biased qkv, ALiBi scores
@@ -193,7 +194,8 @@ class OracleDecoder:
         kv_put(li, pos0, k, v)
         K_all, V_all = kv_get(li, pos0 + S)
         G = H // Hkv
-        Kx, Vx = K_all.repeat_interleave(G, 1), V_all.repeat_interleave(G, 1)
+        Kx, Vx = (K_all, V_all) if G == 1 else (K_all.repeat_interleave(G, 1),
+                                                 V_all.repeat_interleave(G, 1))
         s = torch.einsum("qhd,khd->hqk", q, Kx) / math.sqrt(dh)
         qpos = torch.arange(pos0, pos0 + S)[:, None]
         kpos = torch.arange(pos0 + S)[None, :]
@@ -217,13 +219,24 @@ class OracleDecoder:
             h = _rmsnorm(x[-1:], self.final_norm, eps)
         return (h @ self.lm_head.t())[0]
 
-    # -- contiguous KV
-    def new_cache(self):
-        return {"k": [None] * self.cfg.n_layers, "v": [None] * self.cfg.n_layers}
+    # -- contiguous KV (preallocated when the final length is known, so a
+    #    decode step writes one row instead of re-concatenating the cache)
+    def new_cache(self, max_len: int | None = None):
+        c = {"k": [None] * self.cfg.n_layers, "v": [None] * self.cfg.n_layers, "cap": 0}
+        if max_len:
+            hkv, dh = self.cfg.n_kv_heads, self.cfg.head_dim
+            c["k"] = [torch.empty(max_len, hkv, dh) for _ in range(self.cfg.n_layers)]
+            c["v"] = [torch.empty(max_len, hkv, dh) for _ in range(self.cfg.n_layers)]
+            c["cap"] = max_len
+        return c
 
     def _contig(self, cache):
         def put(li, pos0, k, v):
-            if cache["k"][li] is None:
+            n = pos0 + k.shape[0]
+            if n <= cache["cap"]:
+                cache["k"][li][pos0:n] = k
+                cache["v"][li][pos0:n] = v
+            elif cache["k"][li] is None:
                 cache["k"][li], cache["v"][li] = k, v
             else:
                 cache["k"][li] = torch.cat([cache["k"][li][:pos0], k])
@@ -246,7 +259,7 @@ class OracleDecoder:
         """Greedy generation of n_out tokens (first from the prompt phase).
         ``forced`` teacher-forces the fed-back tokens (for comparing against a
         device run whose near-tie argmax may differ)."""
-        logits, cache = self.prefill(prompt)
+        logits, cache = self.prefill(prompt, self.new_cache(len(prompt) + n_out))
         toks, all_logits = [int(logits.argmax())], [logits]
         for i in range(1, n_out):
             feed = toks[-1] if forced is None else forced[i - 1]

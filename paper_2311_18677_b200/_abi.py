@@ -60,8 +60,10 @@ SIGNATURES = {
     "swb_argmax_pick": [_P, _I, _I, _P, _ST],
     "swb_rope_kv_write": [_P, _I, _I, _P, _I, _I, _I, _F, _P, _P, _P, _I, _ST],
     "swb_kv_push_layer": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _I, _ST],
-    "swb_kv_signal": [_P, _U, _ST],
-    "swb_stream_wait_flag": [_P, _U, _ST],
+    "swb_kv_push_layers": [_P, _S, _I, _I, _I, _I, _I, _I, _I, _P, _P, _S, _P, _I, _I, _ST],
+    "swb_kv_handoff": [_P, _I, _P, _P, _P, _I, _ST],
+    "swb_host_register": [_P, _S, C.POINTER(_P)],
+    "swb_host_unregister": [_P],
     "swb_attn_prefill": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],
     "swb_attn_prefill_tc": [_P, _I, _I, _P, _I, _I, _I, _I, _I, _F, _P, _P, _ST],
     "swb_attn_decode_workspace": [_I, _I, _I, _I, _I],
@@ -71,7 +73,6 @@ SIGNATURES = {
                         _I, _I, _P, _P, _ST],
     "swb_attn_decode_step": [_P, _I, _P, _P, _P, _I, _P, _F, _P, _I, _I, _I, _I, _I, _F, _I,
                              _I, _P, _P, _ST],
-    "swb_decode_prepare": [_P, _P, _I, _I, _I, _P, _P, _P, _ST],
     "swb_decode_advance": [_P, _P, _P, _P, _P, _I, _I, _ST],
     "swb_slots_from_table": [_P, _I, _I, _I, _P, _ST],
     "swb_kv_pool_create": [_I, _I, _I, _I, _I, _I, _I, C.POINTER(_P)],
@@ -131,9 +132,9 @@ LAUNCH_MULT = {
     "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemm_bf16_bias": 1, "swb_gemv_bf16_bias": 1,
     "swb_gemm_qkv_rope": 1, "swb_rope_table": 1,
     "swb_layernorm": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
-    "swb_argmax": 1, "swb_argmax_shard": 1, "swb_argmax_pick": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_signal": 1,
+    "swb_argmax": 1, "swb_argmax_shard": 1, "swb_argmax_pick": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_push_layers": 1,
+    "swb_kv_handoff": 1,
     "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1, "swb_attn_chunk": 1,
-    "swb_decode_prepare": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
     "swb_block_free": 1, "swb_tp_allreduce_f32": 1,
 }

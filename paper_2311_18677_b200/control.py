@@ -1,28 +1,36 @@
 """Control channel between a prompt machine and its token machine.
 
-Only tiny int32 messages cross it (the KV bytes go GPU-to-GPU over NVLink):
+Only tiny messages cross it (the KV bytes go GPU-to-GPU over NVLink):
 
-  * reservation  token -> prompt : the KV sequence slots the token machine
-    reserved (final context = prompt + outputs) for the routed requests, so
-    the prompt machine can push each layer straight into those blocks
-    (both machines are chosen at arrival, reference cluster.py:153-160);
-  * hand-off     prompt -> token : one row per request whose prompt phase
-    finished and whose KV landed: (request id, KV slot, prompt length, first
-    token, output tokens) — the reference's TRANSFER event + token-task
-    enqueue (engine.py:286-297).
+  * reservation  token -> prompt : the KV sequence slot (and its epoch) the
+    token machine reserved (final context = prompt + outputs) for each
+    routed request, so the prompt machine can push each layer straight into
+    those blocks (both machines are chosen at arrival, reference
+    cluster.py:153-160);
+  * hand-off     prompt GPU -> token host : per KV slot, a record in a
+    host shared-memory table [flag, first token] that the prompt GPU writes
+    itself after the last layer's push landed (``swb_kv_handoff``: the
+    token, then flag = the reservation's epoch behind a full memory
+    barrier) — the paper's per-request semaphore and the
+    reference's TRANSFER event + token-task enqueue (engine.py:286-297).
+    The prompt host never waits for its pushes; the token host polls the
+    flags between (and while waiting for) decode iterations.
 
-Hand-offs travel through a single-producer/single-consumer mailbox in host
-shared memory (``ShmMailbox``; the pair always shares a node because the KV
-moves over NVLink), because a decode loop must be able to *poll* for them
-between iterations: a gloo ``irecv`` only reports completion once waited on.
-``HandoffReceiver`` polls it; when the token machine is a tensor-parallel
-group, every TP peer admits a hand-off at the same scheduler iteration (a MIN
-all-reduce of "received" flags over the TP group), so the peers' batches —
-and the NCCL all-reduces inside their decode steps — stay identical.
+``HandoffWatch`` is the token host's view: reservations in FIFO order, and a
+poll that returns the leading ones whose flag landed.  When the token
+machine is a tensor-parallel group, every TP peer admits the same prefix at
+the same scheduler iteration (a MIN all-reduce of the landed counts over the
+TP group), so the peers' batches — and the collectives inside their decode
+steps — stay identical.
+
+Host-memory publication order relies on x86-64 (TSO: loads are not reordered
+with older loads, stores not with older stores); ``require_tso`` refuses to
+run elsewhere.
 """
 
 from __future__ import annotations
 
+import platform
 import time
 from multiprocessing import shared_memory
 
@@ -33,14 +41,25 @@ import torch.distributed as dist
 HANDOFF_FIELDS = ("request_id", "kv_slot", "prompt_tokens", "first_token", "output_tokens")
 
 
-def send_reservations(slots, dst: int, group) -> None:
-    dist.send(torch.tensor(list(slots), dtype=torch.int32), dst=dst, group=group)
+def require_tso() -> None:
+    """The shared-memory records are published with plain stores and read with
+    plain loads; that is ordered on x86-64 only."""
+    m = platform.machine().lower()
+    if m not in ("x86_64", "amd64"):
+        raise RuntimeError(f"control-channel shared memory assumes x86-64 TSO, host is {m}")
 
 
-def recv_reservations(n: int, src: int, group) -> list:
-    buf = torch.empty(n, dtype=torch.int32)
+def send_reservations(slots, dst: int, group, epochs=None) -> None:
+    """(slot, epoch) per request; epochs default to 0."""
+    epochs = list(epochs) if epochs is not None else [0] * len(slots)
+    dist.send(torch.tensor(list(slots) + epochs, dtype=torch.int64), dst=dst, group=group)
+
+
+def recv_reservations(n: int, src: int, group, with_epochs: bool = False):
+    buf = torch.empty(2 * n, dtype=torch.int64)
     dist.recv(buf, src=src, group=group)
-    return buf.tolist()
+    v = buf.tolist()
+    return (v[:n], v[n:]) if with_epochs else v[:n]
 
 
 class ShmMailbox:
@@ -53,6 +72,7 @@ class ShmMailbox:
     SLOT = 1 + MAXROWS * 5
 
     def __init__(self, name: str | None = None, create: bool = False):
+        require_tso()
         size = 8 * (2 + self.NSLOT * self.SLOT)
         if create:
             self.shm = shared_memory.SharedMemory(create=True, size=size)
@@ -227,45 +247,107 @@ class ArrivalFeed:
         return self.cursor == len(self.all)
 
 
-class HandoffReceiver:
-    """Token-side end: owns the mailbox (its name goes to the prompt side at
-    start-up) and polls it between decode iterations."""
+class HandoffTable:
+    """Per-KV-slot hand-off records in host shared memory, int32
+    [max_seqs][STRIDE/4]: word 0 = flag (epoch of the reservation whose KV
+    landed), word 1 = first token.  Created by the token machine's process;
+    the prompt machine's process attaches by name and page-locks / maps it
+    (``device_ptr``) so its GPU stores the records (swb_kv_handoff)."""
 
-    def __init__(self, tp_group=None):
-        self.box = ShmMailbox(create=True)
-        self.tp_group = tp_group
+    STRIDE = 16
+
+    def __init__(self, max_seqs: int = 0, name: str | None = None, create: bool = False):
+        require_tso()
+        if create:
+            self.shm = shared_memory.SharedMemory(create=True, size=max(4096, max_seqs * self.STRIDE))
+        else:
+            self.shm = shared_memory.SharedMemory(name=name)
+            try:
+                from multiprocessing import resource_tracker
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:
+                pass
+        self.owner = create
+        self.max_seqs = self.shm.size // self.STRIDE
+        self.a = np.ndarray((self.max_seqs, self.STRIDE // 4), dtype=np.int32, buffer=self.shm.buf)
+        if create:
+            self.a[:] = 0
+        self._dev = None
+        self._host_ptr = None
 
     @property
     def name(self) -> str:
-        return self.box.name
+        return self.shm.name
 
-    def poll(self, block: bool = False):
-        """Rows of the next hand-off, or None if it has not arrived on every TP
-        peer yet.  ``block`` waits for it."""
-        while True:
-            ready = 1 if self.box.ready() else 0
-            if self.tp_group is not None:
-                flag = torch.tensor([ready], dtype=torch.int32)
-                dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.tp_group)
-                ready = int(flag.item())
-            if ready:
-                return self.box.get()
-            if not block:
-                return None
-            time.sleep(2e-5)
+    def device_ptr(self) -> int:
+        """Device address of this process's mapping (registered on first use)."""
+        if self._dev is None:
+            import ctypes as C
+            from . import _abi
+            self._host_ptr = C.addressof(C.c_char.from_buffer(self.shm.buf))
+            dev = C.c_void_p()
+            _abi.call("swb_host_register", self._host_ptr, self.shm.size, C.byref(dev))
+            self._dev = int(dev.value)
+        return self._dev
 
-    def close(self) -> None:
-        self.box.close()
+    def landed(self, seq: int, epoch: int) -> bool:
+        return int(self.a[seq, 0]) == epoch
 
-
-class HandoffSender:
-    """Prompt-side end: attaches to the token machine's mailbox by name."""
-
-    def __init__(self, name: str):
-        self.box = ShmMailbox(name=name)
-
-    def send(self, rows) -> None:
-        self.box.put(rows)
+    def token(self, seq: int) -> int:
+        return int(self.a[seq, 1])
 
     def close(self) -> None:
-        self.box.close()
+        try:
+            if self._host_ptr is not None:
+                from . import _abi
+                _abi.call("swb_host_unregister", self._host_ptr)
+                self._host_ptr = None
+            del self.a
+            self.shm.close()
+            if self.owner:
+                self.shm.unlink()
+        except Exception:
+            pass
+
+
+class HandoffWatch:
+    """Token host: the reservations whose KV is on its way, in FIFO order
+    (the prompt machine batches FCFS, so they land in this order), and the
+    first instant each landing was observed (the first token's emission)."""
+
+    def __init__(self, table: HandoffTable, tp_group=None):
+        self.table = table
+        self.tp_group = tp_group
+        self.pending: list = []          # [rid, seq, epoch, plen, n_out]
+        self.seen: dict = {}             # rid -> host time the flag was first observed
+
+    def expect(self, rid: int, seq: int, epoch: int, plen: int, n_out: int) -> None:
+        self.pending.append([rid, seq, epoch, plen, n_out])
+
+    def observe(self) -> int:
+        """Record the observation time of newly landed leading reservations;
+        returns how many leading reservations have landed."""
+        k = 0
+        now = None
+        for rid, seq, epoch, _p, _o in self.pending:
+            if not self.table.landed(seq, epoch):
+                break
+            if rid not in self.seen:
+                now = now or time.perf_counter()
+                self.seen[rid] = now
+            k += 1
+        return k
+
+    def poll(self) -> list:
+        """Hand-off rows (rid, seq, plen, first token, n_out) of the leading
+        landed reservations — the same prefix on every TP peer."""
+        k = self.observe()
+        if self.tp_group is not None:
+            t = torch.tensor([k], dtype=torch.int64)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.tp_group)
+            k = int(t.item())
+        rows = []
+        for rid, seq, _e, plen, n_out in self.pending[:k]:
+            rows.append((rid, seq, plen, self.table.token(seq), n_out))
+        del self.pending[:k]
+        return rows

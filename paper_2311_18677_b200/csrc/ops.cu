@@ -246,12 +246,18 @@ __global__ void rope_kv_kernel(__nv_bfloat16* __restrict__ qkv, int row_stride,
 // destination pool's paged blocks — a peer GPU's HBM mapped through CUDA
 // IPC — as coalesced 256-byte NVLink writes per head.
 constexpr int PUSH_UNROLL = 16;
+// blockIdx.y = layer: the serialized mode pushes every layer of a finished
+// prompt in one launch (layer strides in elements; 0 for the per-layer mode).
 __global__ void __launch_bounds__(256)
     kv_push_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int row_stride,
                    int k_col, int v_col, int Hkv, int dh, __nv_bfloat16* __restrict__ dk,
-                   __nv_bfloat16* __restrict__ dv, const int32_t* __restrict__ slots, int bs) {
+                   __nv_bfloat16* __restrict__ dv, const int32_t* __restrict__ slots, int bs,
+                   size_t src_layer_stride, size_t dst_layer_stride) {
   pdl_trigger();
   pdl_wait();
+  qkv += blockIdx.y * src_layer_stride;
+  dk += blockIdx.y * dst_layer_stride;
+  dv += blockIdx.y * dst_layer_stride;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -282,12 +288,24 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-__global__ void signal_kernel(uint32_t* flag, uint32_t value) {
+// Hand-off record of a finished prompt batch: thread i stores request i's
+// first token into word 1 of its slot in the token machine's hand-off table
+// (host-mapped shared memory or peer memory); the per-request flags (word 0)
+// follow as stream memory operations (swb_kv_handoff).
+constexpr int HANDOFF_MAX = 64;
+struct HandoffBatch {
+  int seq[HANDOFF_MAX];
+};
+__global__ void handoff_token_kernel(const int32_t* __restrict__ first, int n,
+                                     HandoffBatch b, char* base, int stride) {
   pdl_trigger();
   pdl_wait();
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value)
-               : "memory");
+  const int i = threadIdx.x;
+  if (i < n) {
+    int32_t* rec = reinterpret_cast<int32_t*>(base + (size_t)b.seq[i] * stride);
+    asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(rec + 1), "r"(first[i])
+                 : "memory");
+  }
 }
 
 // ------------------------------------------ vocab-parallel greedy argmax
@@ -367,22 +385,6 @@ __global__ void argmax_pick_kernel(const float* __restrict__ cand, int rows, int
 }
 
 // -------------------------------------------------- decode bookkeeping
-__global__ void decode_prepare_kernel(const int32_t* __restrict__ ctx,
-                                      const int32_t* __restrict__ tables,
-                                      int max_blocks, int bs, int B,
-                                      int32_t* __restrict__ pos,
-                                      int32_t* __restrict__ slots,
-                                      int32_t* __restrict__ attn_len) {
-  pdl_trigger();
-  pdl_wait();
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const int c = ctx[b];
-  pos[b] = c;
-  slots[b] = tables[(size_t)b * max_blocks + c / bs] * bs + c % bs;
-  attn_len[b] = c + 1;
-}
-
 __global__ void decode_advance_kernel(const int32_t* __restrict__ next_tok,
                                       int32_t* __restrict__ cur_tok,
                                       int32_t* __restrict__ ctx,
@@ -504,77 +506,110 @@ extern "C" int swb_rope_kv_write(void* qkv, int rows, int row_stride,
   return swb_check_launch("rope_kv_kernel");
 }
 
+static int push_launch(const void* qkv, int rows, int row_stride, int k_col, int v_col,
+                       int Hkv, int dh, void* dk, void* dv, const int32_t* dst_slots,
+                       int block_size, int num_ctas, int layers, size_t src_layer_stride,
+                       size_t dst_layer_stride, uintptr_t stream) {
+  SWB_REQUIRE(qkv && dk && dv && dst_slots, "swb_kv_push: null pointer");
+  SWB_REQUIRE(dh % 8 == 0 && Hkv > 0 && block_size > 0 && rows >= 0 && layers > 0,
+              "swb_kv_push: bad shape");
+  SWB_REQUIRE(row_stride % 8 == 0 && k_col % 8 == 0 && v_col % 8 == 0 &&
+                  src_layer_stride % 8 == 0,
+              "swb_kv_push: 16-byte alignment of rows/columns");
+  if (rows == 0) return SWB_OK;
+  int grid = num_ctas > 0 ? num_ctas : 64;
+  const int need = (rows * 2 + 7) / 8;     // 8 warps per CTA, one (row, k|v) unit each
+  if (need < grid) grid = need;
+  const cudaError_t le_ = launch(kv_push_kernel, dim3(grid, layers), dim3(256), 0, STREAM,
+      reinterpret_cast<const __nv_bfloat16*>(qkv), rows, row_stride, k_col, v_col,
+      Hkv, dh, reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv),
+      dst_slots, block_size, src_layer_stride, dst_layer_stride);
+  if (le_ != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch kv_push_kernel: %s", cudaGetErrorString(le_));
+  return swb_check_launch("kv_push_kernel");
+}
+
 extern "C" int swb_kv_push_layer(const void* qkv, int rows, int row_stride,
                                  int k_col, int v_col, int Hkv, int dh,
                                  void* dst_k_layer, void* dst_v_layer,
                                  const int32_t* dst_slots, int block_size,
                                  int num_ctas, uintptr_t stream) {
-  SWB_REQUIRE(qkv && dst_k_layer && dst_v_layer && dst_slots,
-              "swb_kv_push_layer: null pointer");
-  SWB_REQUIRE(dh % 8 == 0 && Hkv > 0 && block_size > 0 && rows >= 0,
-              "swb_kv_push_layer: bad shape");
-  SWB_REQUIRE(row_stride % 8 == 0 && k_col % 8 == 0 && v_col % 8 == 0,
-              "swb_kv_push_layer: 16-byte alignment of rows/columns");
-  if (rows == 0) return SWB_OK;
-  int grid = num_ctas > 0 ? num_ctas : 64;
-  const int need = (rows * 2 + 7) / 8;     // 8 warps per CTA, one (row, k|v) unit each
-  if (need < grid) grid = need;
-  {
-    const cudaError_t le_ = launch(kv_push_kernel, dim3(grid), dim3(256), 0, STREAM,
-        
-      reinterpret_cast<const __nv_bfloat16*>(qkv), rows, row_stride, k_col, v_col,
-      Hkv, dh, reinterpret_cast<__nv_bfloat16*>(dst_k_layer),
-      reinterpret_cast<__nv_bfloat16*>(dst_v_layer), dst_slots, block_size);
-    if (le_ != cudaSuccess)
-      return swb_set_error(SWB_ERR_CUDA, "launch kv_push_kernel: %s", cudaGetErrorString(le_));
-  }
-  return swb_check_launch("kv_push_kernel");
+  return push_launch(qkv, rows, row_stride, k_col, v_col, Hkv, dh, dst_k_layer, dst_v_layer,
+                     dst_slots, block_size, num_ctas, 1, 0, 0, stream);
 }
 
-extern "C" int swb_kv_signal(uint32_t* flag, uint32_t value, uintptr_t stream) {
-  SWB_REQUIRE(flag, "swb_kv_signal: null flag");
-  {
-    const cudaError_t le_ = launch(signal_kernel, dim3(1), dim3(1), 0, STREAM,
-        flag, value);
-    if (le_ != cudaSuccess)
-      return swb_set_error(SWB_ERR_CUDA, "launch signal_kernel: %s", cudaGetErrorString(le_));
-  }
-  return swb_check_launch("signal_kernel");
+extern "C" int swb_kv_push_layers(const void* qkv, size_t qkv_layer_stride, int layers,
+                                  int rows, int row_stride, int k_col, int v_col, int Hkv,
+                                  int dh, void* dst_k_layer0, void* dst_v_layer0,
+                                  size_t dst_layer_stride_bytes, const int32_t* dst_slots,
+                                  int block_size, int num_ctas, uintptr_t stream) {
+  SWB_REQUIRE(dst_layer_stride_bytes % 16 == 0, "swb_kv_push_layers: layer stride alignment");
+  return push_launch(qkv, rows, row_stride, k_col, v_col, Hkv, dh, dst_k_layer0, dst_v_layer0,
+                     dst_slots, block_size, num_ctas, layers, qkv_layer_stride,
+                     dst_layer_stride_bytes / sizeof(__nv_bfloat16), stream);
 }
 
-extern "C" int swb_stream_wait_flag(uint32_t* flag, uint32_t value,
-                                    uintptr_t stream) {
-  SWB_REQUIRE(flag, "swb_stream_wait_flag: null flag");
-  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
+static PFN_cuStreamWriteValue32_v11070 write_value_fn() {
+  static PFN_cuStreamWriteValue32_v11070 fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return swb_set_error(SWB_ERR_CUDA, "cuStreamWaitValue32 unavailable");
-    fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
   }
-  CUresult r = fn((CUstream)stream, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ);
-  if (r != CUDA_SUCCESS)
-    return swb_set_error(SWB_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  return fn;
+}
+
+extern "C" int swb_kv_handoff(const int32_t* first_tok, int n, const int32_t* seqs,
+                              const uint32_t* epochs, void* table, int stride_bytes,
+                              uintptr_t stream) {
+  SWB_REQUIRE(first_tok && seqs && epochs && table, "swb_kv_handoff: null pointer");
+  SWB_REQUIRE(n > 0 && n <= HANDOFF_MAX && stride_bytes >= 8 && stride_bytes % 4 == 0,
+              "swb_kv_handoff: bad batch (n <= %d)", HANDOFF_MAX);
+  HandoffBatch b;
+  for (int i = 0; i < n; ++i) {
+    SWB_REQUIRE(seqs[i] >= 0, "swb_kv_handoff: negative slot");
+    b.seq[i] = seqs[i];
+  }
+  const cudaError_t le = launch(handoff_token_kernel, dim3(1), dim3(HANDOFF_MAX), 0, STREAM,
+                                first_tok, n, b, reinterpret_cast<char*>(table), stride_bytes);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch handoff_token_kernel: %s", cudaGetErrorString(le));
+  int rc = swb_check_launch("handoff_token_kernel");
+  if (rc != SWB_OK) return rc;
+  auto fn = write_value_fn();
+  if (!fn) return swb_set_error(SWB_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  for (int i = 0; i < n; ++i) {
+    // default flags: a full memory barrier precedes the store, so the pushed
+    // KV pages and the first token are visible before the flag
+    CUresult r = fn((CUstream)stream,
+                    (CUdeviceptr)(reinterpret_cast<char*>(table) + (size_t)seqs[i] * stride_bytes),
+                    epochs[i], CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS)
+      return swb_set_error(SWB_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  }
   return SWB_OK;
 }
 
-extern "C" int swb_decode_prepare(const int32_t* ctx, const int32_t* block_tables,
-                                  int max_blocks, int block_size, int B, int32_t* pos,
-                                  int32_t* slots, int32_t* attn_len, uintptr_t stream) {
-  SWB_REQUIRE(ctx && block_tables && pos && slots && attn_len,
-              "swb_decode_prepare: null pointer");
-  SWB_REQUIRE(B > 0 && max_blocks > 0 && block_size > 0, "swb_decode_prepare: bad shape");
-  {
-    const cudaError_t le_ = launch(decode_prepare_kernel, dim3((B + 127) / 128), dim3(128), 0, STREAM,
-        
-      ctx, block_tables, max_blocks, block_size, B, pos, slots, attn_len);
-    if (le_ != cudaSuccess)
-      return swb_set_error(SWB_ERR_CUDA, "launch decode_prepare_kernel: %s", cudaGetErrorString(le_));
-  }
-  return swb_check_launch("decode_prepare_kernel");
+extern "C" int swb_host_register(void* ptr, size_t bytes, void** dev_ptr) {
+  SWB_REQUIRE(ptr && bytes && dev_ptr, "swb_host_register: null pointer");
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+  e = cudaHostGetDevicePointer(dev_ptr, ptr, 0);
+  if (e != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
+  return SWB_OK;
+}
+
+extern "C" int swb_host_unregister(void* ptr) {
+  SWB_REQUIRE(ptr, "swb_host_unregister: null pointer");
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+  return SWB_OK;
 }
 
 extern "C" int swb_decode_advance(const int32_t* next_tok, int32_t* cur_tok,

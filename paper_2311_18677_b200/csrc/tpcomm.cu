@@ -3,7 +3,7 @@
 //
 // Each rank owns one device region, exported by CUDA IPC and mapped by every
 // peer of its TP group:
-//   [slot 0 | slot 1 | rx[2][MAXW] | flags[2][MAXW][MAXC] | counters[2][MAXC]]
+//   [slot 0 | slot 1 | aux slot 2 | rx[3][MAXW] | flags[3][MAXW][MAXC] | counters[3][MAXC]]
 // The producing GEMM/GEMV writes its fp32 partial sums straight into a slot
 // (rank 0 folds the residual in), so the all-reduce moves no extra copy:
 //   CTA c of rank r   1. system-scope fence, then a store of its epoch into
@@ -19,9 +19,12 @@
 // own slot + rx[slot][p] from local memory — one one-way trip instead of a
 // flag trip plus a remote-read round trip; same floats, same order.
 // Epochs are per-(slot, CTA) device counters, so the launch is CUDA-graph
-// replayable.  Two slots alternate: a slot is rewritten only after the next
-// all-reduce (other slot) completed on every rank, i.e. after all peers
-// finished reading it.
+// replayable.  Slots 0 and 1 alternate: a slot is rewritten only after the
+// next all-reduce (other slot) completed on every rank, i.e. after all peers
+// finished reading it.  Slot 2 (small, <= 1 MB) is the once-per-step
+// reduction (the vocab-parallel greedy candidates): the slot 0/1 all-reduces
+// between two of its uses order them the same way, and it keeps the 0/1
+// alternation unbroken across steps (a step does an even number of those).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -31,6 +34,7 @@
 namespace swb {
 
 constexpr int TP_MAXW = 8;
+constexpr int TP_NSLOT = 3;
 constexpr int TP_MAXC = 256;
 constexpr int TP_THREADS = 512;
 constexpr uint32_t kTpMagic = 0x53575450u;  // "SWTP"
@@ -211,13 +215,21 @@ struct swb_tp_comm {
   bool connected;
 };
 
-// push-mode receive buffers: rx[2 slots][TP_MAXW sources] of tp_rx_bytes each
+// push-mode receive buffers: rx[3 slots][TP_MAXW sources] of tp_rx_bytes each
 static size_t tp_rx_bytes(size_t slot_bytes) { return std::min<size_t>(slot_bytes, 1 << 20); }
+static size_t tp_slot_cap(size_t slot_bytes, int slot) {
+  return slot < 2 ? slot_bytes : tp_rx_bytes(slot_bytes);
+}
+static size_t tp_slot_off(size_t slot_bytes, int slot) { return (size_t)slot * slot_bytes; }
+static size_t tp_rx_off(size_t slot_bytes) {
+  return 2 * slot_bytes + tp_rx_bytes(slot_bytes);
+}
 static size_t tp_flags_off(size_t slot_bytes) {
-  return 2 * slot_bytes + 2 * TP_MAXW * tp_rx_bytes(slot_bytes);
+  return tp_rx_off(slot_bytes) + TP_NSLOT * TP_MAXW * tp_rx_bytes(slot_bytes);
 }
 static size_t tp_region_bytes(size_t slot_bytes) {
-  return tp_flags_off(slot_bytes) + sizeof(uint32_t) * (2 * TP_MAXW * TP_MAXC + 2 * TP_MAXC);
+  return tp_flags_off(slot_bytes) +
+         sizeof(uint32_t) * (TP_NSLOT * TP_MAXW * TP_MAXC + TP_NSLOT * TP_MAXC);
 }
 
 extern "C" int swb_tp_comm_create(int rank, int world, size_t slot_bytes, swb_tp_comm** out,
@@ -288,8 +300,8 @@ extern "C" int swb_tp_comm_destroy(swb_tp_comm* c) {
 }
 
 extern "C" void* swb_tp_comm_slot(const swb_tp_comm* c, int slot) {
-  if (!c || slot < 0 || slot > 1) return nullptr;
-  return c->base + (size_t)slot * c->slot_bytes;
+  if (!c || slot < 0 || slot >= TP_NSLOT) return nullptr;
+  return c->base + tp_slot_off(c->slot_bytes, slot);
 }
 
 // SWB_TP_AR_TRIGGER=0: exit-time PDL trigger instead of right after the wait
@@ -305,25 +317,26 @@ extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t
                                     uintptr_t stream) {
   SWB_REQUIRE(c && out, "swb_tp_allreduce_f32: null pointer");
   SWB_REQUIRE(c->connected || c->world == 1, "swb_tp_allreduce_f32: not connected");
-  SWB_REQUIRE(slot == 0 || slot == 1, "swb_tp_allreduce_f32: slot must be 0 or 1");
-  SWB_REQUIRE(n % 4 == 0 && n * sizeof(float) <= c->slot_bytes,
-              "swb_tp_allreduce_f32: n=%zu must be a multiple of 4 and fit the slot", n);
+  SWB_REQUIRE(slot >= 0 && slot < TP_NSLOT, "swb_tp_allreduce_f32: slot must be 0, 1 or 2");
+  SWB_REQUIRE(n % 4 == 0 && n * sizeof(float) <= tp_slot_cap(c->slot_bytes, slot),
+              "swb_tp_allreduce_f32: n=%zu must be a multiple of 4 and fit slot %d", n, slot);
   SWB_REQUIRE((((uintptr_t)out) & 15) == 0, "swb_tp_allreduce_f32: out must be 16-byte aligned");
   if (n == 0) return SWB_OK;
   TpArgs a;
   memset(&a, 0, sizeof(a));
   const size_t flags_off = tp_flags_off(c->slot_bytes);
   const size_t rxb = tp_rx_bytes(c->slot_bytes);
-  const size_t rx_off = 2 * c->slot_bytes + (size_t)slot * TP_MAXW * rxb;
+  const size_t rx_off = tp_rx_off(c->slot_bytes) + (size_t)slot * TP_MAXW * rxb;
   for (int p = 0; p < c->world; ++p) {
-    a.peer_slot[p] = reinterpret_cast<const float*>(c->peer_base[p] + (size_t)slot * c->slot_bytes);
+    a.peer_slot[p] = reinterpret_cast<const float*>(c->peer_base[p] +
+                                                    tp_slot_off(c->slot_bytes, slot));
     a.peer_rx[p] = reinterpret_cast<float*>(c->peer_base[p] + rx_off + (size_t)c->rank * rxb);
     a.peer_flags[p] = reinterpret_cast<uint32_t*>(c->peer_base[p] + flags_off);
   }
   a.my_rx = reinterpret_cast<const float*>(c->base + rx_off);
   a.rx_stride = (long long)(rxb / sizeof(float));
   a.my_flags = reinterpret_cast<uint32_t*>(c->base + flags_off);
-  a.my_ctr = a.my_flags + 2 * TP_MAXW * TP_MAXC;
+  a.my_ctr = a.my_flags + TP_NSLOT * TP_MAXW * TP_MAXC;
   a.out = out;
   a.n = (long long)n;
   a.rank = c->rank;

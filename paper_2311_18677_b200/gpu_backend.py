@@ -210,7 +210,7 @@ class GpuBackend:
             first_h = first.cpu()                   # synchronises the prompt GPU
             if push:
                 runner.finish_push_stats()
-                ms = e0.elapsed_time(runner._compute_end)
+                ms = stats.compute_ms
                 for r in recs:
                     self.visible[r.request_id] = (stats.tail_ms, sum(stats.layer_ms))
             else:

@@ -5,6 +5,7 @@ device and contiguity, then launches on the current torch CUDA stream.
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import torch
@@ -15,8 +16,8 @@ from .errors import ValidationError
 
 __all__ = ["gemm", "gemv", "gemv_rmsnorm", "linear", "embed", "rmsnorm", "layernorm", "argmax",
            "rope_kv_write",
-           "kv_push_layer", "attn_prefill", "attn_decode", "attn_decode_step", "decode_prepare",
-           "decode_advance", "slots_from_table", "kv_signal", "stream_wait_flag",
+           "kv_push_layer", "kv_push_layers", "kv_handoff", "attn_prefill", "attn_decode",
+           "attn_decode_step", "decode_advance", "slots_from_table",
            "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "EPI_GELU", "GEMV_MAX_ROWS"]
 
 # rows handled by the weight-streaming GEMVs (the tcgen05 GEMV takes up to 32)
@@ -197,6 +198,20 @@ def kv_push_layer(qkv, rows, H, Hkv, dh, dst_k, dst_v, dst_slots, block_size, nu
          stream if stream is not None else _stream())
 
 
+def kv_push_layers(qkv_stack, rows, H, Hkv, dh, dst_k0, dst_v0, dst_layer_stride, dst_slots,
+                   block_size, num_ctas=0, row0=0, stream=None):
+    """Serialized mode: push rows [row0, row0+rows) of every layer of
+    qkv_stack [L, T, qkv_cols] into the destination pool in ONE launch."""
+    _req(qkv_stack, torch.bfloat16, "qkv_stack")
+    L, T, cols = qkv_stack.shape
+    if row0 < 0 or row0 + rows > T:
+        raise ValidationError("kv_push_layers: rows outside the stash")
+    call("swb_kv_push_layers", qkv_stack.data_ptr() + 2 * row0 * cols, T * cols, L, rows, cols,
+         H * dh,
+         (H + Hkv) * dh, Hkv, dh, dst_k0, dst_v0, dst_layer_stride, dst_slots.data_ptr(),
+         block_size, num_ctas, stream if stream is not None else _stream())
+
+
 def attn_prefill(qkv, cu_seqlens, num_seqs, max_seqlen, H, Hkv, dh, scale, out=None,
                  impl=None, alibi=None):
     """Causal varlen prefill attention.  impl "tc" = tcgen05/TMEM kernel (the
@@ -269,11 +284,6 @@ def attn_chunk(qkv, C, q_start, k_layer, v_layer, table_row_ptr, H, Hkv, dh, blo
     return out
 
 
-def decode_prepare(ctx, block_tables, block_size, B, pos, slots, attn_len):
-    call("swb_decode_prepare", ctx.data_ptr(), block_tables.data_ptr(), block_tables.shape[1],
-         block_size, B, pos.data_ptr(), slots.data_ptr(), attn_len.data_ptr(), _stream())
-
-
 def decode_advance(next_tok, cur_tok, ctx, step, ring, B):
     call("swb_decode_advance", next_tok.data_ptr(), cur_tok.data_ptr(), ctx.data_ptr(),
          step.data_ptr(), ring.data_ptr(), ring.shape[1], B, _stream())
@@ -284,9 +294,17 @@ def slots_from_table(table_row_ptr, start, n, block_size, slots, stream=None):
          stream if stream is not None else _stream())
 
 
-def kv_signal(flag_ptr, value, stream=None):
-    call("swb_kv_signal", flag_ptr, value, stream if stream is not None else _stream())
-
-
-def stream_wait_flag(flag_ptr, value, stream=None):
-    call("swb_stream_wait_flag", flag_ptr, value, stream if stream is not None else _stream())
+def kv_handoff(first_tok, seqs, epochs, table_dev_ptr, stride_bytes, stream=None):
+    """Publish a finished prompt batch to the token machine's hand-off table:
+    first tokens, then per-request flags = epochs, after all prior work on
+    the stream (the KV pushes)."""
+    _req(first_tok, torch.int32, "first_tok")
+    n = len(seqs)
+    if n == 0:
+        return
+    if n != len(epochs) or first_tok.numel() < n:
+        raise ValidationError("kv_handoff: seqs / epochs / first_tok lengths differ")
+    s = (ctypes.c_int32 * n)(*seqs)
+    e = (ctypes.c_uint32 * n)(*epochs)
+    call("swb_kv_handoff", first_tok.data_ptr(), n, s, e, table_dev_ptr, stride_bytes,
+         stream if stream is not None else _stream())

@@ -29,8 +29,17 @@ import torch
 
 from . import _abi
 from . import kernels as K
+from .errors import CapacityError
 from .kvcache import KVCacheManager
 from .model import Weights
+from .transfer import B200_NVLINK_PAIR, LAYERWISE, SERIALIZED
+
+# serialized transfer mode (reference select_mode, transfer.py:73-76): every
+# prompt of the batch shorter than the NVLink threshold and the batch small
+# enough for the per-layer stash
+SERIAL_THRESHOLD = int(os.environ.get("SWB_SERIAL_THRESHOLD",
+                                      str(B200_NVLINK_PAIR["mode_threshold_tokens"])))
+SERIAL_MAX_ROWS = 256
 
 
 @dataclass
@@ -49,6 +58,19 @@ class PushStats:
     bytes_per_layer: int = 0
     total_ms: float = 0.0        # first push start -> last push end
     tail_ms: float = 0.0         # compute end -> last push end (visible latency)
+    compute_ms: float = 0.0      # prefill compute (first kernel -> compute end)
+    mode: str = LAYERWISE
+
+
+@dataclass
+class Handoff:
+    """Where a prompt batch announces its landed KV (control.HandoffTable):
+    per request the token machine's KV slot and reservation epoch, and the
+    table's device address in this process."""
+    seqs: list
+    epochs: list
+    table_ptr: int
+    stride: int = 16
 
 
 class ModelRunner:
@@ -77,6 +99,10 @@ class ModelRunner:
         self.dev = weights.embed.device
         self._cap = 0
         self.push_stream = torch.cuda.Stream(device=self.dev)
+        self._buf_ev = [None, None]      # last push that read each qkv buffer
+        self._stash = None               # [L, SERIAL_MAX_ROWS, qkv_cols] (serialized mode)
+        self._stash_ev = None
+        self._pending_push = []          # (timing, compute_end, last_event, stats)
         self.graphs: dict = {}
         # RoPE angle table for the fused QKV-GEMM epilogue (16K positions, 8 MB)
         self.rope_tab = (K.rope_table(cfg.rope_theta, 16384, device=self.dev)
@@ -168,11 +194,12 @@ class ModelRunner:
             K.argmax_shard(logits, self.vocab_off, self.rank, self.tp, cand)
             self._allreduce(cand)
         else:
-            s = c.next_slot()
-            part = c.slot(s, (rows, self.tp, 2))
+            # the aux slot: outside the slot-0/1 alternation of the step's
+            # O / down reductions (which must stay even per step)
+            part = c.slot(c.AUX, (rows, self.tp, 2))
             K.argmax_shard(logits, self.vocab_off, self.rank, self.tp, part)
             cand = self._cand_buf(rows)
-            c.allreduce(s, cand)
+            c.allreduce(c.AUX, cand)
         K.argmax_pick(cand, rows, self.tp, out)
 
     def _cand_buf(self, rows):
@@ -204,16 +231,43 @@ class ModelRunner:
         self._cap, self._rcap = cap, rcap
 
     # ------------------------------------------------------------ prefill
+    def transfer_mode(self, lens: list[int]) -> str:
+        """Serialized when every prompt of the batch is below the NVLink
+        threshold (reference select_mode, transfer.py:73-76) and the batch
+        fits the stash; layer-wise otherwise (a short prompt that shares a
+        batch with a long one rides that batch's per-layer pushes)."""
+        if sum(lens) <= SERIAL_MAX_ROWS and all(n < SERIAL_THRESHOLD for n in lens):
+            return SERIALIZED
+        return LAYERWISE
+
+    def _wait_buffer(self, main, ev):
+        if ev is not None:
+            main.wait_event(ev)
+
+    def _wait_push_tails(self):
+        """Paths that reuse pqkv[0] / pfirst without push bookkeeping wait for
+        every push still reading them."""
+        main = torch.cuda.current_stream()
+        for ev in (*self._buf_ev, self._stash_ev):
+            self._wait_buffer(main, ev)
+
     def prefill(self, tokens: torch.Tensor, lens: list[int], meta: torch.Tensor,
                 local_slots: torch.Tensor | None = None,
                 push: list[PushSegment] | None = None,
-                push_stats: PushStats | None = None) -> torch.Tensor:
+                push_stats: PushStats | None = None,
+                handoff: Handoff | None = None, mode: str | None = None) -> torch.Tensor:
         """Run the prompt phase for a batch of prompts packed back to back.
 
         tokens      int32 [T] on device
         meta        int32 device tensor = [positions(T) | cu_seqlens(R+1) | last_rows(R)]
         local_slots int32 [T] slots in this GPU's pool (co-located token phase)
         push        per-request destination segments (token machine elsewhere)
+        handoff     announce the landed KV to the token machine (control.
+                    HandoffTable) from the push stream; the call then returns
+                    without waiting for the pushes (the prompt machine is free
+                    once its compute ends).  Without it, the current stream
+                    waits for every push before the call returns.
+        mode        SERIALIZED / LAYERWISE (default: transfer_mode(lens))
         Returns the greedy first token of every prompt (int32 [R], device).
         """
         cfg, w = self.cfg, self.w
@@ -224,7 +278,8 @@ class ModelRunner:
         last_rows = meta[T + R + 1:T + 2 * R + 1]
         x, h, attn, act = self.px[:T], self.ph[:T], self.pattn[:T], self.pact[:T]
         main = torch.cuda.current_stream()
-        push_events = []
+        mode = (mode or self.transfer_mode(lens)) if push else LAYERWISE
+        serial = push and mode == SERIALIZED
         timing = None
         if push:
             for seg in push:
@@ -232,16 +287,27 @@ class ModelRunner:
                     seg.slots = torch.empty(seg.rows, dtype=torch.int32, device=self.dev)
                 K.slots_from_table(seg.dst.table_row_ptr(seg.dst_seq), 0, seg.rows,
                                    seg.dst.block_size, seg.slots)
+                seg.slots.record_stream(self.push_stream)
             if push_stats is not None:
+                push_stats.mode = mode
+                n_ev = 1 if serial else cfg.n_layers
                 timing = [(torch.cuda.Event(enable_timing=True),
-                           torch.cuda.Event(enable_timing=True)) for _ in range(cfg.n_layers)]
-                self._compute_end = torch.cuda.Event(enable_timing=True)
+                           torch.cuda.Event(enable_timing=True)) for _ in range(n_ev)]
+                compute_start = torch.cuda.Event(enable_timing=True)
+                compute_start.record(main)
+        if serial:
+            if self._stash is None:
+                self._stash = torch.empty(cfg.n_layers, SERIAL_MAX_ROWS, self.qkv_cols,
+                                          dtype=torch.bfloat16, device=self.dev)
+            self._wait_buffer(main, self._stash_ev)
         self._begin_reductions()
         self._embed(tokens, x)
         for li, lw in enumerate(w.layers):
-            qkv = self.pqkv[li & 1][:T]
-            if push and li >= 2:
-                main.wait_event(push_events[li - 2])  # qkv buffer reuse
+            if serial:
+                qkv = self._stash[li, :T]
+            else:
+                qkv = self.pqkv[li & 1][:T]
+                self._wait_buffer(main, self._buf_ev[li & 1])    # qkv buffer reuse
             self._norm(x, lw.attn_norm, lw.attn_norm_b, out=h)
             local = local_slots is not None and self.kv is not None
             if T > K.GEMV_MAX_ROWS and self.dh == 128:
@@ -261,7 +327,7 @@ class ModelRunner:
                                     local_slots, self.kv.block_size)
                 elif not self.bloom:
                     K.rope_kv_write(qkv, positions, self.hq, self.hkv, self.dh, self.theta)
-            if push:
+            if push and not serial:
                 ev = torch.cuda.Event()
                 ev.record(main)
                 self.push_stream.wait_event(ev)
@@ -278,7 +344,7 @@ class ModelRunner:
                         timing[li][1].record(self.push_stream)
                     done = torch.cuda.Event()
                     done.record(self.push_stream)
-                push_events.append(done)
+                self._buf_ev[li & 1] = done
             K.attn_prefill(qkv, cu, R, max(lens), self.hq, self.hkv, self.dh, self.scale,
                            out=attn, alibi=self.alibi)
             self._proj_reduce(attn, lw.wo, x, lw.bo)
@@ -292,13 +358,37 @@ class ModelRunner:
         first = self.pfirst[:R]
         self._greedy(logits, first)
         if push:
-            if timing:
-                self._compute_end.record(main)
-            main.wait_event(push_events[-1])  # KV fully landed before we report done
+            compute_end = torch.cuda.Event(enable_timing=True)
+            compute_end.record(main)
+            self.push_stream.wait_event(compute_end)
+            with torch.cuda.stream(self.push_stream):
+                if serial:
+                    # serialized mode: every layer of the finished prompts in one launch
+                    if timing:
+                        timing[0][0].record(self.push_stream)
+                    for seg in push:
+                        K.kv_push_layers(self._stash, seg.rows, self.hq, self.hkv, self.dh,
+                                         seg.dst.k_layer_ptr(0), seg.dst.v_layer_ptr(0),
+                                         seg.dst.info.layer_stride_bytes, seg.slots,
+                                         seg.dst.block_size, self.push_ctas, row0=seg.row0,
+                                         stream=self.push_stream.cuda_stream)
+                    if timing:
+                        timing[0][1].record(self.push_stream)
+                if handoff is not None:
+                    K.kv_handoff(first, handoff.seqs, handoff.epochs, handoff.table_ptr,
+                                 handoff.stride, stream=self.push_stream.cuda_stream)
+                tail = torch.cuda.Event()
+                tail.record(self.push_stream)
+            # the next batch reuses the buffers (and pfirst) only after this tail
+            if serial:
+                self._stash_ev = tail
+            else:
+                self._buf_ev[(cfg.n_layers - 1) & 1] = tail
+            if handoff is None:
+                main.wait_event(tail)       # KV fully landed before we report done
             if push_stats is not None:
-                self._push_timing = (timing, push_stats)
+                self._pending_push.append((timing, compute_start, compute_end, tail, push_stats))
         return first
-
     def mixed(self, tokens: torch.Tensor, lens: list[int], meta: torch.Tensor,
               local_slots: torch.Tensor, dec_tables: torch.Tensor, dec_tok: torch.Tensor,
               dec_ctx: torch.Tensor, dec_max_ctx: int) -> torch.Tensor:
@@ -331,6 +421,7 @@ class ModelRunner:
                                                            self.partition, self.dh),
                              dtype=torch.uint8, device=self.dev)
             self.graphs[key] = ws
+        self._wait_push_tails()
         self._begin_reductions()
         self._embed(torch.cat([tokens, dec_tok]), x)
         for li, lw in enumerate(w.layers):
@@ -379,6 +470,7 @@ class ModelRunner:
             ws = torch.zeros(K.attn_chunk_workspace_bytes(chunk, self.hq, max_ctx),
                              dtype=torch.uint8, device=self.dev)
             self.graphs[key] = ws
+        self._wait_push_tails()
         self._begin_reductions()
         for c0 in range(0, P, chunk):
             n = min(chunk, P - c0)
@@ -408,16 +500,23 @@ class ModelRunner:
         self._greedy(logits, first)
         return first
 
-    def finish_push_stats(self):
-        """Resolve push timings after the prefill's events completed."""
-        if not getattr(self, "_push_timing", None):
-            return None
-        timing, st = self._push_timing
-        st.layer_ms = [a.elapsed_time(b) for a, b in timing]
-        st.total_ms = timing[0][0].elapsed_time(timing[-1][1])
-        st.tail_ms = max(0.0, self._compute_end.elapsed_time(timing[-1][1]))
-        self._push_timing = None
-        return st
+    def finish_push_stats(self, block: bool = True):
+        """Resolve the push timings of finished prefills (all of them when
+        ``block``); returns the latest resolved PushStats or None."""
+        last = None
+        while self._pending_push:
+            timing, c0, c1, tail, st = self._pending_push[0]
+            if block:
+                tail.synchronize()
+            elif not tail.query():
+                break
+            self._pending_push.pop(0)
+            st.layer_ms = [a.elapsed_time(b) for a, b in timing]
+            st.total_ms = timing[0][0].elapsed_time(timing[-1][1])
+            st.tail_ms = max(0.0, c1.elapsed_time(timing[-1][1]))
+            st.compute_ms = c0.elapsed_time(c1)
+            last = st
+        return last
 
     @staticmethod
     def pack_meta(lens: list[int]) -> torch.Tensor:
@@ -544,6 +643,12 @@ class DecodeGraph:
         """Bind batch rows to KV sequence slots and their state (host lists
         or device tensors).  Called when the batch composition changes."""
         kv = self.r.kv
+        # host mirror of the largest context: a replay past the bucket would
+        # append K/V outside every attention partition (silently dropped)
+        self._ctx_max = (None if isinstance(ctx, torch.Tensor) and ctx.is_cuda
+                         else int(max(torch.as_tensor(ctx).tolist(), default=0)))
+        if self._ctx_max is not None and self._ctx_max >= self.max_ctx:
+            raise CapacityError(f"context {self._ctx_max} >= decode bucket {self.max_ctx}")
         idx = torch.tensor(seqs, dtype=torch.long, device=self.r.dev)
         torch.index_select(kv.tables(), 0, idx, out=self.tables)
         self.cur_tok.copy_(torch.as_tensor(cur_tok, dtype=torch.int32), non_blocking=True)
@@ -570,11 +675,18 @@ class DecodeGraph:
         # current then, and would bind a second GPU's graph to the first GPU
         with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.r.dev)):
             self._step_body()
+        if self.r.tp_comm is not None:
+            self.r.tp_comm.assert_even()
         self.launches_per_step = _abi.launch_count() - n0
         _abi.add_launches(-self.launches_per_step)  # capture launches nothing
         self.graph = g
 
     def replay(self):
+        if getattr(self, "_ctx_max", None) is not None:
+            if self._ctx_max >= self.max_ctx:
+                raise CapacityError(f"decode step at context {self._ctx_max} overruns the "
+                                    f"{self.max_ctx}-token bucket")
+            self._ctx_max += 1
         if self.graph is None:
             self._step_body()
         else:

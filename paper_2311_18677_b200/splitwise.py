@@ -34,12 +34,12 @@ import torch.distributed as dist
 
 from . import _abi
 from . import kernels as K
-from .control import (ArrivalFeed, HandoffReceiver, HandoffSender, RouteBoard, ShmMailbox,
+from .control import (ArrivalFeed, HandoffTable, HandoffWatch, RouteBoard, ShmMailbox,
                       recv_reservations, send_reservations)
 from .kvcache import KVCacheManager, blocks_for
 from .model import get_config, init_weights
 from .perf import PerfModel
-from .runner import ModelRunner, PushSegment, PushStats
+from .runner import Handoff, ModelRunner, PushSegment, PushStats
 from .serving import pool_blocks_for_memory
 from .transfer import LAYERWISE, kv_push_gbps, measured_plan
 from .workers import PROMPT, TOKEN, Machine, SchedulerConfig, Task
@@ -77,12 +77,15 @@ def _lockstep(n: int, tp_ctrl, now_ms: float = 0.0, fin: bool = False):
 
 
 class PromptServer:
+    """Prompt machine of a Splitwise pair (one process per GPU / TP rank)."""
+
     def __init__(self, runner: ModelRunner, peer: KVCacheManager, ctrl, token_rank: int,
-                 sched: SchedulerConfig, mailbox: str, tp_ctrl=None):
+                 sched: SchedulerConfig, table_name: str, tp_ctrl=None):
         self.runner = runner
         self.tp_ctrl = tp_ctrl          # TP peers must batch in lockstep (collectives inside)
         self.peer = peer
-        self.tx = HandoffSender(mailbox)
+        self.table = HandoffTable(name=table_name)
+        self.table_ptr = self.table.device_ptr()
         self.ctrl = ctrl
         self.token_rank = token_rank
         cfg = runner.cfg
@@ -91,137 +94,132 @@ class PromptServer:
                                                              capacity=hbm), PROMPT, sched)
         self.push_log: list[PushStats] = []
 
+    def _run_batch(self, chunk, seq_of, epoch_of, toks):
+        """chunk: [(rid, prompt, n_out)].  Enqueue the prefill, the per-layer
+        pushes into the reserved pages and the hand-off records, then wait
+        only for the prompt COMPUTE (the pushes' tail and the hand-off run on
+        the push stream).  Returns the host time the compute finished."""
+        lens = [len(r[1]) for r in chunk]
+        meta = ModelRunner.pack_meta(lens).pin_memory().to(self.runner.dev, non_blocking=True)
+        segs, off = [], 0
+        for r, n in zip(chunk, lens):
+            segs.append(PushSegment(off, n, self.peer, seq_of[r[0]]))
+            off += n
+        st = PushStats(bytes_per_layer=off * 2 * self.runner.hkv * self.runner.dh * 2)
+        hand = Handoff([seq_of[r[0]] for r in chunk], [epoch_of[r[0]] for r in chunk],
+                       self.table_ptr, HandoffTable.STRIDE)
+        self.runner.prefill(toks, lens, meta, push=segs, push_stats=st, handoff=hand)
+        done = torch.cuda.Event()
+        done.record()
+        done.synchronize()
+        self.push_log.append(st)
+        self.runner.finish_push_stats(block=False)
+        return time.perf_counter()
+
     def serve_burst(self, requests, t0: float, prompts_dev: dict | None = None):
-        """requests: list of (rid, host int32 prompt, n_out).  Returns
-        {rid: first-token host time}."""
+        """requests: list of (rid, host int32 prompt, n_out).  Returns {rid:
+        host time its prompt compute finished}."""
         dev = self.runner.dev
-        seqs = recv_reservations(len(requests), self.token_rank, self.ctrl)
+        seqs, epochs = recv_reservations(len(requests), self.token_rank, self.ctrl,
+                                         with_epochs=True)
         seq_of = {r[0]: s for r, s in zip(requests, seqs)}
+        epoch_of = {r[0]: e for r, e in zip(requests, epochs)}
         by_id = {r[0]: r for r in requests}
         now_ms = 0.0
         for rid, prompt, n_out in requests:
             self.machine.enqueue(Task(rid, PROMPT, len(prompt), now_ms, n_out, n_out), now_ms)
-        first_time = {}
+        done_time = {}
         while self.machine.has_work():
             batch = self.machine.form_batch(now_ms)
             self.machine.running = batch
             chunk = [by_id[t.request_id] for t in batch.prompt_tasks]
-            lens = [len(r[1]) for r in chunk]
             if prompts_dev is not None:
                 toks = torch.cat([prompts_dev[r[0]] for r in chunk])
             else:
                 toks = torch.cat([r[1] for r in chunk]).pin_memory().to(dev, non_blocking=True)
-            meta = ModelRunner.pack_meta(lens).pin_memory().to(dev, non_blocking=True)
-            segs, off = [], 0
-            for r, n in zip(chunk, lens):
-                segs.append(PushSegment(off, n, self.peer, seq_of[r[0]]))
-                off += n
-            st = PushStats(bytes_per_layer=off * 2 * self.runner.hkv * self.runner.dh * 2)
-            first = self.runner.prefill(toks, lens, meta, push=segs, push_stats=st)
-            fh = torch.empty(len(chunk), dtype=torch.int32).pin_memory()
-            fh.copy_(first, non_blocking=True)
-            torch.cuda.current_stream().synchronize()   # compute done + every push landed
-            tnow = time.perf_counter()
-            self.runner.finish_push_stats()
-            self.push_log.append(st)
-            self.tx.send([(r[0], seq_of[r[0]], len(r[1]), int(fh[j]), r[2])
-                          for j, r in enumerate(chunk)])
+            tnow = self._run_batch(chunk, seq_of, epoch_of, toks)
             for r in chunk:
-                first_time[r[0]] = tnow
+                done_time[r[0]] = tnow
             now_ms = (tnow - t0) * 1e3
             self.machine.complete_iteration(batch, now_ms)
-        return first_time
-
+        self.runner.finish_push_stats(block=True)
+        return done_time
 
     def serve_trace(self, requests, t0: float, feed=None):
         """Arrival-driven prompt machine: requests = [(rid, arrival_s, host
-        prompt, n_out)] in arrival order; each becomes a prompt task at its
-        arrival (wall clock from t0); batches follow the reference prompt
-        rule; a request's KV lands in the slot the token machine reserved at
-        the same arrival (reservation mailbox).  Returns {rid: first-token
-        host time}.  ``feed`` (control.ArrivalFeed) supplies the requests
-        the live JSQ router sent to this pair; without one every request in
-        ``requests`` is this machine's."""
+        prompt, n_out)] in arrival order.  A request becomes a prompt task
+        (enqueue time = its arrival) once the token machine has reserved its
+        final context (reservation mailbox; the token machine admits
+        reservations in arrival order with the blocked-head memory rule), so
+        its KV always has pages to land in.  Batches follow the reference
+        prompt rule.  Returns {rid: host time its prompt compute finished}.
+        ``feed`` (control.ArrivalFeed) supplies the requests the live JSQ
+        router sent to this pair; without one every request is this
+        machine's."""
         feed = feed or ArrivalFeed(requests, 0)
         board = getattr(self, "board", None)
-        pending = []
         by_id = {r[0]: r for r in requests}
-        seq_of: dict = {}
-        first_time = {}
+        reserved: list = []             # (rid, seq, epoch) in reservation order
+        seq_of, epoch_of = {}, {}
+        done_time = {}
         done = 0
         done_tok = 0
-
-        def drain():
+        while True:
+            feed.poll()
             while True:
                 rows = self.res_box.get()
                 if rows is None:
-                    return
-                for rid, seq, *_ in rows:
-                    seq_of[rid] = seq
-
-        while True:
-            pending += feed.poll()
+                    break
+                reserved += [(rid, seq, ep) for rid, seq, ep, *_ in rows]
             fin = feed.complete() and done >= feed.mine
-            now = time.perf_counter() - t0
-            n_new = 0
-            while n_new < len(pending) and pending[n_new][1] <= now:
-                n_new += 1
-            n_take, _, fin = _lockstep(n_new, self.tp_ctrl, 0.0, fin)
+            n_take, _, fin = _lockstep(len(reserved), self.tp_ctrl, 0.0, fin)
             if fin:
                 break
-            for _ in range(n_take):
-                rid, arr, prompt, n_out = pending.pop(0)
+            for rid, seq, ep in reserved[:n_take]:
+                _, arr, prompt, n_out = by_id[rid]
+                seq_of[rid], epoch_of[rid] = seq, ep
                 self.machine.enqueue(Task(rid, PROMPT, len(prompt), arr * 1e3, n_out, n_out),
                                      arr * 1e3)
-            drain()
+            del reserved[:n_take]
             if not self.machine.has_work():
-                wait = (pending[0][1] - now) if pending else 1e-4
-                time.sleep(min(max(wait, 0.0), 1e-3))
+                time.sleep(5e-5)
                 continue
+            now = time.perf_counter() - t0
             batch = self.machine.form_batch(now * 1e3)
             self.machine.running = batch
-            chunk = [by_id[t.request_id] for t in batch.prompt_tasks]
-            while any(r[0] not in seq_of for r in chunk):
-                drain()
-                time.sleep(2e-5)
-            lens = [len(r[2]) for r in chunk]
-            toks = torch.cat([r[2] for r in chunk]).pin_memory().to(self.runner.dev,
+            chunk = [(r[0], r[2], r[3]) for r in (by_id[t.request_id] for t in batch.prompt_tasks)]
+            toks = torch.cat([r[1] for r in chunk]).pin_memory().to(self.runner.dev,
                                                                       non_blocking=True)
-            meta = ModelRunner.pack_meta(lens).pin_memory().to(self.runner.dev, non_blocking=True)
-            segs, off = [], 0
-            for r, n in zip(chunk, lens):
-                segs.append(PushSegment(off, n, self.peer, seq_of[r[0]]))
-                off += n
-            st = PushStats(bytes_per_layer=off * 2 * self.runner.hkv * self.runner.dh * 2)
-            first = self.runner.prefill(toks, lens, meta, push=segs, push_stats=st)
-            fh = torch.empty(len(chunk), dtype=torch.int32).pin_memory()
-            fh.copy_(first, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            tnow = time.perf_counter()
-            self.runner.finish_push_stats()
-            self.push_log.append(st)
-            self.tx.send([(r[0], seq_of[r[0]], len(r[2]), int(fh[j]), r[3])
-                          for j, r in enumerate(chunk)])
+            tnow = self._run_batch(chunk, seq_of, epoch_of, toks)
             for r in chunk:
-                first_time[r[0]] = tnow
+                done_time[r[0]] = tnow
             done += len(chunk)
-            done_tok += sum(lens)
+            done_tok += sum(len(r[1]) for r in chunk)
             if board is not None:
                 board.publish(self.pair, board.PROMPT_TOK, done_tok)
                 board.publish(self.pair, board.PROMPT_REQ, done)
             self.machine.complete_iteration(batch, (tnow - t0) * 1e3)
-        return first_time
+        self.runner.finish_push_stats(block=True)
+        return done_time
+
+    def close(self):
+        self.table.close()
+        self.res_box.close()
 
 
 class TokenServer:
+    """Token machine of a Splitwise pair (one process per GPU / TP rank)."""
+
     def __init__(self, runner: ModelRunner, ctrl, prompt_rank: int, sched: SchedulerConfig,
                  tp_ctrl=None):
         self.runner = runner
         self.kv = runner.kv
         self.ctrl = ctrl
         self.prompt_rank = prompt_rank
-        self.tp_ctrl = tp_ctrl          # TP peers must admit in lockstep (NCCL inside steps)
-        self.rx = HandoffReceiver(tp_ctrl)
+        self.tp_ctrl = tp_ctrl          # TP peers must admit in lockstep (collectives inside)
+        self.table = HandoffTable(self.kv.max_seqs, create=True)
+        self.watch = HandoffWatch(self.table, tp_ctrl)
+        self.epoch = [0] * self.kv.max_seqs
         self.machine = Machine(0, None, estimated_perf_model(runner.cfg, self.kv,
                                                              runner.w.nbytes()), TOKEN, sched)
         self.step_log: list[tuple] = []     # (batch, summed context, device ms) per decode step
@@ -232,86 +230,130 @@ class TokenServer:
             self._ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         return self._ev
 
+    def _reserve(self, tokens: int):
+        seq = self.kv.allocate(tokens)
+        self.epoch[seq] = (self.epoch[seq] + 1) & 0x7FFFFFFF
+        return seq, self.epoch[seq]
+
+    def _fits_prefix(self, lens: list[int]) -> int:
+        """How many leading reservations fit the pool now (blocks and sequence
+        slots) — the reference's blocked-head memory admission
+        (machine.py:216-223): the first that does not fit blocks the rest."""
+        free_b, free_s = self.kv.free_blocks, len(self.kv._free_slots)
+        n = 0
+        for t in lens:
+            nb = blocks_for(t, self.kv.block_size)
+            if nb > free_b or free_s == 0 or nb > self.kv.max_blocks_per_seq:
+                break
+            free_b -= nb
+            free_s -= 1
+            n += 1
+        return n
+
+    def _graph_for(self, rids, info, remaining):
+        """Decode graph whose context bucket covers every row until it
+        finishes: current context + remaining outputs + 1."""
+        need = max(info[r][1] + remaining[r] + 1 for r in rids)
+        g = self.runner.decode_graph(len(rids), 2048 * ((need + 2047) // 2048), 1)
+        g.load([info[r][0] for r in rids], [info[r][2] for r in rids], [info[r][1] for r in rids])
+        if g.graph is None:
+            g.capture()
+        return g
+
+    def _step(self, graph, B, ring_h):
+        """One decode iteration; while it runs, watch the hand-off table so a
+        landing is time-stamped when it happens, not at the next iteration."""
+        ev0, ev1 = self._events()
+        ev0.record()
+        graph.replay()
+        ev1.record()
+        ring_h[:B].copy_(graph.next_tok, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        while not done.query():
+            self.watch.observe()
+            time.sleep(2e-5)
+        return ev0.elapsed_time(ev1)
+
     def serve_burst(self, requests, t0: float):
         """Reserve KV for the routed requests, then admit hand-overs and
-        decode until all of them finished.  Returns {rid: [emission times]}."""
+        decode until all of them finished.  Returns ({rid: [emission times]},
+        {rid: generated tokens}, {rid: first-token time})."""
         kv = self.kv
         self.step_log = []
-        seqs = [kv.allocate(len(p) + n) for _rid, p, n in requests]
+        res = [self._reserve(len(p) + n) for _rid, p, n in requests]
         torch.cuda.current_stream().synchronize()    # tables written before the peer reads
-        send_reservations(seqs, self.prompt_rank, self.ctrl)
+        send_reservations([s for s, _ in res], self.prompt_rank, self.ctrl,
+                          [e for _, e in res])
+        for (rid, p, n), (seq, ep) in zip(requests, res):
+            self.watch.expect(rid, seq, ep, len(p), n)
         expected = len(requests)
         received = 0
-        info = {}         # rid -> [seq, ctx_kv, last_token]
+        info, remaining = {}, {}      # rid -> [seq, ctx_kv, last_token]; outputs left
         emit = {r[0]: [] for r in requests}
         tokens = {r[0]: [] for r in requests}
+        first_seen = {}
         graph, graph_rids = None, None
-        ring_h = torch.empty(64, dtype=torch.int32).pin_memory()
+        ring_h = torch.empty(256, dtype=torch.int32).pin_memory()
         while received < expected or self.machine.has_work() or self.machine.resident:
-            if received < expected:
-                rows = self.rx.poll(block=not self.machine.has_work())
-                if rows is not None:
-                    now_ms = (time.perf_counter() - t0) * 1e3
-                    for rid, seq, plen, first, n_out in rows:
-                        received += 1
-                        tokens[rid].append(first)
-                        if n_out > 1:
-                            info[rid] = [seq, plen, first]
-                            self.machine.enqueue(
-                                Task(rid, TOKEN, plen + 1, now_ms, n_out, n_out - 1), now_ms)
-                        else:
-                            kv.release(seq)
-                    continue
-            if not self.machine.has_work():
-                continue
+            rows = self.watch.poll() if received < expected else []
             now_ms = (time.perf_counter() - t0) * 1e3
+            for rid, seq, plen, first, n_out in rows:
+                received += 1
+                tokens[rid].append(first)
+                first_seen[rid] = self.watch.seen.pop(rid)
+                if n_out > 1:
+                    info[rid] = [seq, plen, first]
+                    remaining[rid] = n_out - 1
+                    self.machine.enqueue(Task(rid, TOKEN, plen + 1, now_ms, n_out, n_out - 1),
+                                         now_ms)
+                else:
+                    kv.release(seq)
+            if not self.machine.has_work():
+                time.sleep(2e-5)
+                continue
             batch = self.machine.form_batch(now_ms)
-            if batch is None:
+            if batch is None or not batch.token_tasks:
+                time.sleep(2e-5)
                 continue
             self.machine.running = batch
             rids = [t.request_id for t in batch.token_tasks]
             B = len(rids)
             if rids != graph_rids:
-                max_ctx = max(info[r][1] + len(tokens[r]) + 64 for r in rids)
-                graph = self.runner.decode_graph(B, 2048 * ((max_ctx + 2047) // 2048), 1)
-                graph.load([info[r][0] for r in rids], [info[r][2] for r in rids],
-                           [info[r][1] for r in rids])
-                if graph.graph is None:
-                    graph.capture()
+                graph = self._graph_for(rids, info, remaining)
                 graph_rids = rids
-            ev0, ev1 = self._events()
-            ev0.record()
-            graph.replay()
-            ev1.record()
-            ring_h[:B].copy_(graph.next_tok, non_blocking=True)   # stream tokens out
-            torch.cuda.current_stream().synchronize()
-            self.step_log.append((B, sum(info[r][1] for r in rids), ev0.elapsed_time(ev1)))
+            ms = self._step(graph, B, ring_h)
+            self.step_log.append((B, sum(info[r][1] for r in rids), ms))
             tnow = time.perf_counter()
             for b, r in enumerate(rids):
                 t = int(ring_h[b])
                 tokens[r].append(t)
                 info[r][1] += 1
                 info[r][2] = t
+                remaining[r] -= 1
                 emit[r].append(tnow)
             for what, task in self.machine.complete_iteration(batch, (tnow - t0) * 1e3):
                 if what == "request_finished":
                     kv.release(info[task.request_id][0])
-                    graph_rids = None if task.request_id in (graph_rids or []) else graph_rids
-        return emit, tokens
-
+                    graph_rids = None
+        return emit, tokens, first_seen
 
     def serve_trace(self, requests, t0: float, feed=None):
         """Arrival-driven token machine: reserves each request's final context
         at its arrival (both machines are chosen at arrival, reference
-        cluster.py:153-160) and publishes the slot to the prompt machine,
-        admits hand-overs between decode iterations (continuous batching with
+        cluster.py:153-160) when the pool can hold it — arrivals that do not
+        fit wait, in order, until finished requests free their pages (the
+        reference's blocked-head memory admission; TP peers decide in
+        lockstep) — and publishes the slot to the prompt machine; admits
+        landed hand-offs between decode iterations (continuous batching with
         the reference token rule), one CUDA-graph step per iteration.
-        Returns ({rid: [emission times]}, decode step log)."""
+        Returns ({rid: [emission times]}, decode step log, {rid: first-token
+        time})."""
         kv = self.kv
         feed = feed or ArrivalFeed(requests, 0)
         board = getattr(self, "board", None)
         pending = []
-        info, emit = {}, {}
+        info, remaining, emit, first_seen = {}, {}, {}, {}
         finished = 0
         graph, graph_rids = None, None
         ring_h = torch.empty(256, dtype=torch.int32).pin_memory()
@@ -322,31 +364,33 @@ class TokenServer:
                 emit[r[0]] = []
             fin = feed.complete() and finished >= feed.mine
             now = time.perf_counter() - t0
-            arrived = []
             n_new = 0
             while n_new < len(pending) and pending[n_new][1] <= now:
                 n_new += 1
+            n_new = self._fits_prefix([len(p[2]) + p[3] for p in pending[:n_new]])
             n_take, mnow, fin = _lockstep(n_new, self.tp_ctrl, now * 1e3, fin)
             if fin:
                 break
+            arrived = []
             for _ in range(n_take):
                 rid, arr, prompt, n_out = pending.pop(0)
-                arrived.append((rid, kv.allocate(len(prompt) + n_out)))
+                seq, ep = self._reserve(len(prompt) + n_out)
+                arrived.append((rid, seq, ep))
+                self.watch.expect(rid, seq, ep, len(prompt), n_out)
             if arrived:
                 torch.cuda.current_stream().synchronize()   # table rows before the peer reads
-                self.res_box.put([(rid, seq, 0, 0, 0) for rid, seq in arrived])
-            rows = self.rx.poll(block=False)
-            if rows is not None:
-                tn = mnow
-                for rid, seq, plen, first, n_out in rows:
-                    if n_out > 1:
-                        info[rid] = [seq, plen, first]
-                        self.machine.enqueue(Task(rid, TOKEN, plen + 1, tn, n_out, n_out - 1), tn)
-                    else:
-                        kv.release(seq)
-                        finished += 1
-                        if board is not None:
-                            board.publish(self.pair, board.FINISHED, finished)
+                self.res_box.put([(rid, seq, ep, 0, 0) for rid, seq, ep in arrived])
+            for rid, seq, plen, first, n_out in self.watch.poll():
+                first_seen[rid] = self.watch.seen.pop(rid)
+                if n_out > 1:
+                    info[rid] = [seq, plen, first]
+                    remaining[rid] = n_out - 1
+                    self.machine.enqueue(Task(rid, TOKEN, plen + 1, mnow, n_out, n_out - 1), mnow)
+                else:
+                    kv.release(seq)
+                    finished += 1
+                    if board is not None:
+                        board.publish(self.pair, board.FINISHED, finished)
             if not self.machine.has_work() and not self.machine.resident:
                 time.sleep(5e-5)
                 continue
@@ -358,26 +402,16 @@ class TokenServer:
             rids = [t.request_id for t in batch.token_tasks]
             B = len(rids)
             if rids != graph_rids:
-                max_ctx = max(info[r][1] + 64 for r in rids) + max(
-                    t.remaining_output for t in batch.token_tasks)
-                graph = self.runner.decode_graph(B, 2048 * ((max_ctx + 2047) // 2048), 1)
-                graph.load([info[r][0] for r in rids], [info[r][2] for r in rids],
-                           [info[r][1] for r in rids])
-                if graph.graph is None:
-                    graph.capture()
+                graph = self._graph_for(rids, info, remaining)
                 graph_rids = rids
-            ev0, ev1 = self._events()
-            ev0.record()
-            graph.replay()
-            ev1.record()
-            ring_h[:B].copy_(graph.next_tok, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            ms = self._step(graph, B, ring_h)
             tnow = time.perf_counter()
-            self.step_log.append((B, sum(info[r][1] for r in rids), ev0.elapsed_time(ev1)))
+            self.step_log.append((B, sum(info[r][1] for r in rids), ms))
             for b, r in enumerate(rids):
                 t = int(ring_h[b])
                 info[r][1] += 1
                 info[r][2] = t
+                remaining[r] -= 1
                 emit[r].append(tnow)
             for what, task in self.machine.complete_iteration(batch, mnow):
                 if what == "request_finished":
@@ -386,7 +420,11 @@ class TokenServer:
                     if board is not None:
                         board.publish(self.pair, board.FINISHED, finished)
                     graph_rids = None
-        return emit, self.step_log
+        return emit, self.step_log, first_seen
+
+    def close(self):
+        self.table.close()
+        self.res_box.close()
 
 
 # ---------------------------------------------------------------------------
@@ -408,7 +446,15 @@ def _decode_roofline(cfg, tp, steps, hbm_peak, peak_kind):
             "traffic": None, "steps_timed": len(full)}
 
 
-def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_traffic):
+def _full_batch_ms(steps):
+    if not steps:
+        return None
+    bmax = max(b for b, _, _ in steps)
+    return statistics.mean(m for b, _, m in steps if b == bmax)
+
+
+def run_split_bench(args, ClockSampler, percentile, cpu_baseline, peaks, ncu_traffic,
+                    metric_name):
     import json
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -443,7 +489,7 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         handle = [None, None, None]
         dist.recv_object_list(handle, src=peer_rank, group=ctrl)
         peer = KVCacheManager.open_peer(handle[0])
-        server = PromptServer(runner, peer, ctrl, peer_rank, sched, mailbox=handle[1],
+        server = PromptServer(runner, peer, ctrl, peer_rank, sched, table_name=handle[1],
                               tp_ctrl=tp_gloo)
         server.res_box = ShmMailbox(name=handle[2])
     else:
@@ -456,7 +502,7 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         runner = ModelRunner(w, kv, tp_group=tp_nccl)
         server = TokenServer(runner, ctrl, peer_rank, sched, tp_ctrl=tp_gloo)
         server.res_box = ShmMailbox(create=True)
-        dist.send_object_list([kv.ipc_handle(), server.rx.name, server.res_box.name],
+        dist.send_object_list([kv.ipc_handle(), server.table.name, server.res_box.name],
                               dst=peer_rank, group=ctrl)
     push_alone = None
     if is_prompt:
@@ -511,37 +557,40 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         return
     launches0 = _abi.launch_count()
     e2e_ms, ttft, tbt, gaps2, push_gbs, push_tail, push_raw = [], [], [], [], [], [], []
-    dec_steps = []
+    dec_steps, pre_ms, pre_flops, overhead = [], [], [], []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             t0, out, dms, wall = one_step(False)
             gathered = [None] * world
-            payload = {"rank": rank, "t0": t0, "out": out if is_prompt else out[0]}
+            payload = {"rank": rank, "t0": t0}
             if is_prompt:
-                st = server.push_log[-1]
-                payload["push"] = (st.bytes_per_layer, st.layer_ms, st.tail_ms)
+                payload["push"] = [(st.bytes_per_layer, st.layer_ms, st.tail_ms, st.compute_ms,
+                                    st.mode) for st in server.push_log[-8:]]
+                server.push_log.clear()
             else:
+                payload["emit"], payload["first"] = out[0], out[2]
                 payload["steps"] = list(server.step_log)
             dist.all_gather_object(gathered, payload, group=ctrl)
             e2e_ms.append(dms)
             for pr in range(0, world, 2 * tp):
-                dec_steps += gathered[pr + tp]["steps"]
-            for pr in range(0, world, 2 * tp):
-                first = gathered[pr]["out"]
-                emits = gathered[pr + tp]["out"]
+                tok = gathered[pr + tp]
+                dec_steps += tok["steps"]
                 t0p = gathered[pr]["t0"]
-                for rid, tf in first.items():
-                    ttft.append((tf - t0p) * 1e3)
-                    seq = [tf] + emits[rid]
+                for rid, tf in tok["first"].items():
+                    ttft.append((tf - t0p) * 1e3)        # all requests arrive at t0
+                    seq = [tf] + tok["emit"][rid]
                     g_ = [(b - a) * 1e3 for a, b in zip(seq, seq[1:])]
                     tbt += g_
                     if g_:
                         gaps2.append(g_[0])
-                bpl, lms, tail = gathered[pr]["push"]
-                push_gbs.append(statistics.mean(kv_push_gbps(bpl, m) for m in lms))
-                plan = measured_plan(LAYERWISE, lms, tail)   # reference TransferPlan record
-                push_tail.append(plan.visible_latency)
-                push_raw.append(plan.raw_time)
+                for bpl, lms, tail, cms, mode in gathered[pr]["push"]:
+                    push_gbs.append(statistics.mean(kv_push_gbps(bpl, m) for m in lms))
+                    plan = measured_plan(mode, lms, tail)   # reference TransferPlan record
+                    push_tail.append(plan.visible_latency)
+                    push_raw.append(plan.raw_time)
+                    pre_ms.append(cms)
+                    overhead.append(tail / cms if cms > 0 else 0.0)
+            pre_flops.append(R * cfg.prefill_flops(P, tp))
         dev_ms = []
         for _ in range(args.steps):
             dev_ms.append(one_step(True)[2])
@@ -554,9 +603,16 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
         pairs = world // (2 * tp)
         toks_step = pairs * R * O
         ms = statistics.mean(dev_ms)
+        # every prompt batch of a step is timed on its machine; a step's R
+        # prompts go through one or two batches (2048-token cap)
+        batches_per_step = max(1, len(pre_ms) // max(1, args.steps * pairs))
+        pre_step_ms = statistics.mean(pre_ms) * batches_per_step
+        pre_tfs = statistics.mean(pre_flops) / (pre_step_ms / 1e3) / 1e12
+        dec = _decode_roofline(cfg, tp, dec_steps, hbm_peak, peak_kind)
+        if dec is not None:
+            dec["traffic"] = ncu_traffic("decode_step") if cfg.name == "llama2-7b" else None
         line = {
-            "metric": "output tokens/s (+ TTFT/TBT p50,p99) serving "
-                      f"{P}/{O} requests, {cfg.name}",
+            "metric": metric_name(cfg, P, O),
             "value": toks_step / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -577,12 +633,16 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
                     "ms_per_step": statistics.mean(e2e_ms),
                     "h2d_bytes_per_step": pairs * R * 4 * (4 * P),
                     "d2h_bytes_per_step": pairs * R * 4 * O},
-            "kv_transfer": {"mode": "layerwise P2P push (NVLink, CUDA IPC)",
+            "phases_ms": {"prefill": pre_step_ms,
+                          "decode_step": _full_batch_ms(dec_steps)},
+            "kv_transfer": {"mode": "layerwise P2P push (NVLink, CUDA IPC); hand-off flags "
+                                    "stored by the prompt GPU (swb_kv_handoff)",
                             "push_GBps_per_layer": statistics.mean(push_gbs),
                             "nvlink_peak_GBps": 770.0,
                             "frac": statistics.mean(push_gbs) / 770.0,
                             "raw_ms": statistics.mean(push_raw),
                             "visible_ms": statistics.mean(push_tail),
+                            "visible_frac_of_prefill": statistics.mean(overhead),
                             "visible_frac_of_ttft": statistics.mean(push_tail) /
                             percentile(ttft, 0.5),
                             "push_kernel_alone_GBps": {f"{c}_ctas": round(v, 1)
@@ -592,15 +652,20 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
                                     "SMs with the next layers' prefill (64 CTAs); "
                                     "push_kernel_alone_* is the same kernel timed alone, vs "
                                     "770 GB/s measured peer copy (900 nominal)"},
-            "roofline": _decode_roofline(cfg, tp, dec_steps, hbm_peak, peak_kind),
+            "roofline": dec,
+            "roofline_prefill": {"bound": "tensor", "achieved": pre_tfs, "peak": tc_peak,
+                                 "unit": "TFLOP/s", "frac": pre_tfs / tc_peak,
+                                 "algorithmic_flops": statistics.mean(pre_flops),
+                                 "peak_kind": peak_kind, "kernel": "prompt machine prefill"},
             "gpu_launches": int(launches_t.item()),
             "clocks": clocks,
         }
+        if not getattr(args, "no_cpu", False):
+            line["cpu_baseline"] = cpu_baseline(args.model, P, O)
         print(json.dumps(line), flush=True)
     dist.barrier()
     torch.cuda.synchronize()
-    (server.tx if is_prompt else server.rx).close()
-    server.res_box.close()
+    server.close()
     # NCCL sub-communicator teardown can stall at interpreter exit (seen with
     # TP groups + CUDA IPC mappings); the result is printed, so bound it.
     threading.Timer(30.0, lambda: os._exit(0)).start()
@@ -610,17 +675,16 @@ def run_split_bench(args, ClockSampler, percentile, cpu_port_sample, peaks, ncu_
 
 def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, ClockSampler,
                  percentile, peaks, tp=1):
-    """bench.py --trace: the reference's synthetic trace (trace.py presets,
-    Poisson arrivals) served concurrently by the Splitwise pairs in real
+    """bench.py --trace: the reference's synthetic trace (reference trace.py
+    presets and generator, via tools/reftrace.py; Poisson arrivals) served concurrently by the Splitwise pairs in real
     time; each request is routed at its arrival to the pair with the fewest
     pending tokens (control.RouteBoard, the reference's JSQ; --route rr:
     request i -> pair i mod pairs); TP pairs process arrivals in
     lockstep across their peers.  Rank 0 prints TTFT / TBT / E2E percentiles
     and tokens/s."""
     import json
-    from .trace import preset_trace
     pairs = world // (2 * tp)
-    reqs_all = preset_trace(args.trace, args.rate, args.duration, args.seed)
+    reqs_all = list(args.trace_requests)     # the reference generator's trace (bench.py)
     if args.max_output:
         reqs_all = [type(r)(r.id, r.arrival, r.prompt_tokens, min(r.output_tokens, args.max_output))
                     for r in reqs_all]
@@ -659,8 +723,8 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
         out = server.serve_trace(items, t0, feed)
     if router is not None:
         router.join()
-    payload = {"rank": rank, "prompt": is_prompt, "out": out if is_prompt else out[0],
-               "steps": None if is_prompt else out[1]}
+    payload = {"rank": rank, "prompt": is_prompt, "out": None if is_prompt else out[0],
+               "steps": None if is_prompt else out[1], "first": None if is_prompt else out[2]}
     gathered = [None] * world
     dist.all_gather_object(gathered, payload, group=ctrl)
     if rank == 0:
@@ -671,9 +735,8 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
         for gp in gathered:
             if gp["rank"] % tp:          # TP peers report the same requests
                 continue
-            if gp["prompt"]:
-                first.update(gp["out"])
-            else:
+            if not gp["prompt"]:
+                first.update(gp["first"])       # the token host saw the first token land
                 emits.update(gp["out"])
                 steps += gp["steps"]
         ttft, tbt, e2e = [], [], []
@@ -716,8 +779,7 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
         print(json.dumps(line), flush=True)
     dist.barrier()
     torch.cuda.synchronize()
-    (server.tx if is_prompt else server.rx).close()
-    server.res_box.close()
+    server.close()
     if board is not None:
         board.close()
     threading.Timer(30.0, lambda: os._exit(0)).start()

@@ -4,9 +4,12 @@
 One ``TPComm`` per TP rank.  The producing GEMM/GEMV writes its fp32 partial
 sums into ``slot(s)`` (a view of IPC-shared device memory), then
 ``allreduce(s, out)`` writes the rank-ordered sum of every rank's slot ``s``
-into ``out``.  Slots must strictly alternate between consecutive reductions
-(``next_slot``); ``reset()`` at the start of every prefill / decode step keeps
-the sequence graph-replayable (every step performs an even number).
+into ``out``.  Slots 0 and 1 must strictly alternate between consecutive
+reductions (``next_slot``); ``reset()`` at the start of every prefill / decode
+step keeps the sequence graph-replayable, so every step must perform an even
+number of them (``assert_even``).  Slot 2 (``AUX``, <= 1 MB) carries the one
+reduction per step outside that alternation: the vocab-parallel greedy
+candidates.
 Replaces the NCCL ``all_reduce`` of ``ModelRunner._allreduce``
 ("all-reduce twice per layer").
 """
@@ -37,8 +40,17 @@ class TPComm:
         dist.all_gather_object(blobs, bytes(blob.raw), group=group)
         allb = C.create_string_buffer(b"".join(blobs), _abi.TP_IPC_BYTES * self.world)
         _abi.call("swb_tp_comm_connect", self._h, allb, _abi.TP_IPC_BYTES)
-        self._slots = [int(_abi.lib.swb_tp_comm_slot(self._h, s)) for s in (0, 1)]
+        self._slots = [int(_abi.lib.swb_tp_comm_slot(self._h, s)) for s in (0, 1, 2)]
         self._next = 0
+
+    AUX = 2
+    AUX_BYTES = 1 << 20
+
+    def assert_even(self) -> None:
+        """A step must end on the slot it started with (even count of 0/1
+        reductions), or the next replay would reuse a slot back to back."""
+        if self._next != 0:
+            raise RuntimeError("odd number of slot-0/1 all-reduces in one step")
 
     def reset(self) -> None:
         self._next = 0
@@ -52,7 +64,7 @@ class TPComm:
         n = 1
         for v in shape:
             n *= int(v)
-        if 4 * n > self.slot_bytes:
+        if 4 * n > (self.slot_bytes if s < 2 else min(self.slot_bytes, self.AUX_BYTES)):
             raise ValueError(f"TP slot of {self.slot_bytes} bytes cannot hold {tuple(shape)} fp32")
         return device_view(self._slots[s], tuple(shape), torch.float32)
 

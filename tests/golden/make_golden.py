@@ -11,14 +11,16 @@ replayed by tests/test_reference_parity.py against this repo's host code:
                  extrapolated points (perf.py:77-88, :297-350)
   machine.json   randomized enqueue / form_batch / complete_iteration scripts
                  on prompt, token and mixed machines (machine.py:118-275)
-  cluster.json   randomized routing scripts over Splitwise / Baseline layouts
-                 (cluster.py:129-185)
   engine.json    full Simulator runs (engine.py:160-358) on small traces:
                  per-request TTFT/E2E/TBT, routing, transfer visible latency
   csv.json       the reference's trace CSV / requests_csv / tbt_csv text for
                  two runs (engine.py:369-391, trace.py:206-212)
+  traces.json    the reference generator's preset traces (trace.py:143-153,
+                 :215-243) at the (preset, rate, duration, seed) points the GPU
+                 tests and bench --trace use, for boxes where the installed
+                 reference (baseline/_ref) is absent (tools/reftrace.py)
 
-Run:  python tests/golden/make_golden.py   (needs /root/reference)
+Run:  python tests/golden/make_golden.py [name ...]   (needs /root/reference)
 """
 
 from __future__ import annotations
@@ -211,12 +213,30 @@ def gen_csv(engine, cluster, perf, trace):
     return out
 
 
+TRACE_POINTS = ([(pr, rate, dur, 0) for pr in ("conversation", "coding")
+                 for rate in (1.0, 2.0, 4.0, 8.0, 16.0, 24.0) for dur in (15.0, 20.0, 60.0)]
+                + [("conversation", 20.0, 1.0, 5)])
+
+
+def gen_traces(trace):
+    out = {}
+    for preset, rate, dur, seed in TRACE_POINTS:
+        pd, od = trace.PRESETS[preset]["prompt"], trace.PRESETS[preset]["output"]
+        tr = trace.generate_trace(pd, od, rate, dur, seed=seed)
+        out[f"{preset}/{rate:g}/{dur:g}/{seed}"] = [[r.arrival, r.prompt_tokens, r.output_tokens]
+                                                    for r in tr.requests]
+    return out
+
+
 def main():
     cluster, engine, machine, perf, trace, transfer = load_ref()
-    fixtures = {"transfer": gen_transfer(transfer), "perf": gen_perf(perf),
-                "machine": gen_machine(machine, perf),
-                "engine": gen_engine(engine, cluster, perf, trace),
-                "csv": gen_csv(engine, cluster, perf, trace)}
+    gens = {"transfer": lambda: gen_transfer(transfer), "perf": lambda: gen_perf(perf),
+            "machine": lambda: gen_machine(machine, perf),
+            "engine": lambda: gen_engine(engine, cluster, perf, trace),
+            "csv": lambda: gen_csv(engine, cluster, perf, trace),
+            "traces": lambda: gen_traces(trace)}
+    names = sys.argv[1:] or list(gens)
+    fixtures = {n: gens[n]() for n in names}
     for name, data in fixtures.items():
         with open(os.path.join(HERE, f"{name}.json"), "w") as f:
             json.dump(data, f, separators=(",", ":"))

@@ -1,6 +1,9 @@
 """Multi-process (gloo, CPU) tests of the prompt -> token control channel
-(paper_2311_18677_b200/control.py): reservations, hand-offs, non-blocking
-polling, and TP lockstep admission across a token machine's TP group."""
+(paper_2311_18677_b200/control.py): reservations with epochs, hand-off
+records in the shared table (written here by the peer process the way the
+prompt GPU's swb_kv_handoff writes them: token, then flag), non-blocking
+polling, prefix/epoch admission, and TP lockstep admission across a token
+machine's TP group."""
 
 import os
 import socket
@@ -26,35 +29,44 @@ def _init(rank, world, port):
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
 
+def _land(table, seq, epoch, token):
+    """What swb_kv_handoff does from the prompt GPU: token, then flag."""
+    table.a[seq, 1] = token
+    table.a[seq, 0] = epoch
+
+
 def _pair(rank, world, port, q):
-    from paper_2311_18677_b200.control import (HandoffReceiver, HandoffSender,
+    from paper_2311_18677_b200.control import (HandoffTable, HandoffWatch,
                                                recv_reservations, send_reservations)
     _init(rank, world, port)
     try:
         if rank == 1:                     # token machine
-            rx = HandoffReceiver()
-            dist.send_object_list([rx.name], dst=0)
-            send_reservations([3, 5], 0, None)
+            table = HandoffTable(8, create=True)
+            watch = HandoffWatch(table)
+            dist.send_object_list([table.name], dst=0)
+            send_reservations([3, 5], 0, None, epochs=[7, 2])
+            watch.expect(10, 3, 7, 1024, 128)
+            watch.expect(11, 5, 2, 999, 1)
             got, polls = [], 0
             while len(got) < 2:
-                rows = rx.poll(block=False)
+                got += watch.poll()
                 polls += 1
-                if rows:
-                    got += rows
                 time.sleep(0.005)
-            rx.close()
-            q.put(("token", got, polls))
+            seen = sorted(watch.seen)
+            table.close()
+            q.put(("token", got, polls, seen))
         else:                             # prompt machine
             name = [None]
             dist.recv_object_list(name, src=1)
-            tx = HandoffSender(name[0])
-            slots = recv_reservations(2, 1, None)
+            table = HandoffTable(name=name[0])
+            slots, epochs = recv_reservations(2, 1, None, with_epochs=True)
             time.sleep(0.1)               # the token side polls meanwhile
-            tx.send([(10, slots[0], 1024, 77, 128)])
+            _land(table, slots[1], epochs[1] - 1, 99)   # stale epoch: must not admit
+            _land(table, slots[0], epochs[0], 77)
             time.sleep(0.05)
-            tx.send([(11, slots[1], 999, 42, 1)])
-            tx.close()
-            q.put(("prompt", slots, 0))
+            _land(table, slots[1], epochs[1], 42)
+            table.close()
+            q.put(("prompt", (slots, epochs), 0, None))
     finally:
         dist.destroy_process_group()
 
@@ -66,21 +78,42 @@ def test_reservation_and_handoff_roundtrip():
     procs = [ctx.Process(target=_pair, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    out = dict((k, (a, b)) for k, a, b in (q.get(timeout=120) for _ in range(2)))
+    out = dict((k, (a, b, c)) for k, a, b, c in (q.get(timeout=120) for _ in range(2)))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert out["prompt"][0] == [3, 5]
-    rows, polls = out["token"]
+    assert out["prompt"][0] == ([3, 5], [7, 2])
+    rows, polls, seen = out["token"]
     assert rows == [(10, 3, 1024, 77, 128), (11, 5, 999, 42, 1)]
-    assert polls > 1          # it polled without blocking before the message came
+    assert polls > 1          # it polled without blocking before the flags landed
+    assert seen == [10, 11]
+
+
+def test_handoff_prefix_order_and_epochs():
+    """Landings are admitted as a prefix of the reservation order (the prompt
+    machine batches FCFS), and only for the current epoch of a slot."""
+    from paper_2311_18677_b200.control import HandoffTable, HandoffWatch
+    table = HandoffTable(4, create=True)
+    try:
+        w = HandoffWatch(table)
+        w.expect(1, 0, 5, 10, 3)
+        w.expect(2, 1, 1, 20, 4)
+        _land(table, 1, 1, 8)             # the second lands first
+        assert w.poll() == []
+        _land(table, 0, 4, 9)             # previous epoch of slot 0
+        assert w.poll() == []
+        _land(table, 0, 5, 6)
+        assert w.poll() == [(1, 0, 10, 6, 3), (2, 1, 20, 8, 4)]
+        assert w.pending == [] and set(w.seen) == {1, 2}
+    finally:
+        table.close()
 
 
 def _tp_group(rank, world, port, q):
-    """ranks 0,1 = prompt TP group, 2,3 = token TP group; prompt rank i sends
-    to token rank i+2, rank 1's message is delayed: both token ranks must admit
-    at the same poll iteration."""
-    from paper_2311_18677_b200.control import HandoffReceiver, HandoffSender
+    """ranks 0,1 = prompt TP group, 2,3 = token TP group; prompt rank i lands
+    on token rank i+2's table, rank 1's landing is delayed: both token ranks
+    must admit at the same poll iteration."""
+    from paper_2311_18677_b200.control import HandoffTable, HandoffWatch
     _init(rank, world, port)
     try:
         tok_group = dist.new_group([2, 3], backend="gloo")
@@ -88,17 +121,19 @@ def _tp_group(rank, world, port, q):
         if rank < 2:
             name = [None]
             dist.recv_object_list(name, src=rank + 2)
-            tx = HandoffSender(name[0])
+            table = HandoffTable(name=name[0])
             time.sleep(0.05 if rank == 0 else 0.4)
-            tx.send([(7, 1, 100, 5, 9)])
-            tx.close()
+            _land(table, 1, 3, 5)
+            table.close()
         else:
-            rx = HandoffReceiver(tp_group=tok_group)
-            dist.send_object_list([rx.name], dst=rank - 2)
+            table = HandoffTable(4, create=True)
+            watch = HandoffWatch(table, tp_group=tok_group)
+            watch.expect(7, 1, 3, 100, 9)
+            dist.send_object_list([table.name], dst=rank - 2)
             it = 0
             while True:
-                rows = rx.poll(block=False)
-                if rows is not None:
+                rows = watch.poll()
+                if rows:
                     break
                 it += 1
                 time.sleep(0.01)
@@ -107,7 +142,7 @@ def _tp_group(rank, world, port, q):
             lo, hi = t.clone(), t.clone()
             dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=tok_group)
             dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=tok_group)
-            rx.close()
+            table.close()
             q.put((rank, rows, int(lo), int(hi)))
     finally:
         dist.destroy_process_group()
@@ -127,7 +162,7 @@ def test_tp_lockstep_admission():
     for rank, rows, lo, hi in res:
         assert rows == [(7, 1, 100, 5, 9)]
         assert lo == hi           # admitted in lockstep
-        assert lo >= 10           # and only once the slow peer's message arrived
+        assert lo >= 10           # and only once the slow peer's record landed
 
 
 if __name__ == "__main__":

@@ -5,7 +5,7 @@ import torch
 
 from paper_2311_18677_b200.cluster import ClusterConfig
 from paper_2311_18677_b200.driver import Driver, Request
-from paper_2311_18677_b200.trace import preset_trace
+from reftrace import preset_trace
 
 pytestmark = pytest.mark.gpu
 

@@ -123,3 +123,41 @@ def test_bloom_oracle_matches_transformers_bloom():
     with torch.no_grad():
         ref = hf(torch.tensor([prompt + toks[:3]])).logits[0, len(prompt) - 1:].float()
     assert (logits - ref).abs().max().item() < 2e-4 * max(1.0, ref.abs().max().item())
+
+
+def test_llama_oracle_matches_transformers_llama():
+    """The Llama restatement (RMSNorm, half-split RoPE, GQA head grouping,
+    SwiGLU, untied head) equals transformers' LlamaForCausalLM on the same
+    weights — the independent pin of the branch C1-C4 run on."""
+    from transformers import LlamaConfig, LlamaForCausalLM
+    from paper_2311_18677_b200.model import ModelConfig, init_weights, logical_layer_fp32
+    cfg = ModelConfig("llama-t", 2, 512, 4, 2, 128, 1024, 300, init_std=0.05)
+    w = init_weights(cfg, seed=4, device="cpu")
+    orc = OracleDecoder.from_weights(w)
+    hf = LlamaForCausalLM(LlamaConfig(
+        vocab_size=cfg.vocab, hidden_size=cfg.d_model, intermediate_size=cfg.ffn,
+        num_hidden_layers=cfg.n_layers, num_attention_heads=cfg.n_heads,
+        num_key_value_heads=cfg.n_kv_heads, head_dim=cfg.head_dim, rms_norm_eps=cfg.norm_eps,
+        rope_theta=cfg.rope_theta, max_position_embeddings=4096, tie_word_embeddings=False,
+        attention_bias=False, mlp_bias=False)).eval()
+    sd = {"model.embed_tokens.weight": w.embed.float(), "model.norm.weight": w.final_norm.float(),
+          "lm_head.weight": w.lm_head.float()}
+    for i in range(cfg.n_layers):
+        L = logical_layer_fp32(w, i)
+        p = f"model.layers.{i}."
+        sd.update({p + "input_layernorm.weight": L["attn_norm"],
+                   p + "self_attn.q_proj.weight": L["wq"], p + "self_attn.k_proj.weight": L["wk"],
+                   p + "self_attn.v_proj.weight": L["wv"], p + "self_attn.o_proj.weight": L["wo"],
+                   p + "post_attention_layernorm.weight": L["mlp_norm"],
+                   p + "mlp.gate_proj.weight": L["w_gate"], p + "mlp.up_proj.weight": L["w_up"],
+                   p + "mlp.down_proj.weight": L["wd"]})
+    missing, unexpected = hf.load_state_dict(sd, strict=False)
+    assert not unexpected and not [m for m in missing if "rotary" not in m], (missing, unexpected)
+    # positions past the first few hundred exercise the RoPE angle tables
+    prompt = torch.randint(0, cfg.vocab, (300,), generator=torch.Generator().manual_seed(2)).tolist()
+    toks, logits = orc.generate(prompt, 5)
+    with torch.no_grad():
+        ref = hf(torch.tensor([prompt + toks[:4]])).logits[0, len(prompt) - 1:].float()
+    err = (logits - ref).abs().max().item()
+    assert err < 2e-4 * max(1.0, ref.abs().max().item()), err
+    assert toks == ref.argmax(-1).tolist()

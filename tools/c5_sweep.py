@@ -65,7 +65,7 @@ def sweep(a):
     from paper_2311_18677_b200.cluster import ClusterConfig
     from paper_2311_18677_b200.driver import Driver
     from paper_2311_18677_b200.perf import PerfModel
-    from paper_2311_18677_b200.trace import preset_trace
+    from reftrace import preset_trace
     text = open(a.sweep).read()
     samples = []     # (machine_type, llm, phase, prompt_tokens, batch_size, time_ms, memory)
     for line in text.strip().splitlines()[1:]:

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 from paper_2311_18677_b200.cluster import ClusterConfig  # noqa: E402
 from paper_2311_18677_b200.driver import Driver  # noqa: E402
 from paper_2311_18677_b200.gpu_backend import GpuBackend  # noqa: E402
-from paper_2311_18677_b200.trace import preset_trace  # noqa: E402
+from reftrace import preset_trace  # noqa: E402
 
 
 def main():
@@ -39,7 +39,7 @@ def main():
                     help="clamp output lengths (0 = preset support)")
     a = ap.parse_args()
     if a.trace_csv:
-        from paper_2311_18677_b200.trace import parse_trace
+        from reftrace import parse_trace_csv as parse_trace
         with open(a.trace_csv) as f:
             reqs = parse_trace(f.read())
         a.preset, a.duration = os.path.basename(a.trace_csv), max(r.arrival for r in reqs) or 1.0
@@ -72,7 +72,7 @@ def main():
     s = res.report.summary()
     if a.out_dir:
         from paper_2311_18677_b200.metrics import requests_csv, tbt_csv
-        from paper_2311_18677_b200.trace import serialize_trace
+        from reftrace import serialize_trace
         os.makedirs(a.out_dir, exist_ok=True)
         recs_sorted = [res.records[r.id] for r in reqs]
         for name, text in (("requests.csv", requests_csv(recs_sorted)),

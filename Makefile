@@ -1,5 +1,6 @@
-# Build of libswb200.so (sm_100a only) and the C oracle helpers.
-#   make            -> paper_2311_18677_b200/libswb200.so + oracle/_build/liboracle.so
+# Build of libswb200.so (sm_100a only).  The oracle (oracle/decoder.py) is
+# fp32 torch on the CPU and needs no build.
+#   make            -> paper_2311_18677_b200/libswb200.so
 #   make sass       -> dump SASS of the library (proof of UTCHMMA / UTMALDG)
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
@@ -12,7 +13,7 @@ CPP := $(wildcard $(SRC)/*.cpp)
 OBJ := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU)) $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.o,$(CPP))
 LIB := paper_2311_18677_b200/libswb200.so
 
-all: $(LIB) oracle
+all: $(LIB)
 
 $(OBJDIR)/%.o: $(SRC)/%.cu $(SRC)/common.cuh include/swb200.h
 	@mkdir -p $(OBJDIR)
@@ -25,9 +26,6 @@ $(OBJDIR)/%.o: $(SRC)/%.cpp include/swb200.h
 $(LIB): $(OBJ)
 	$(NVCC) -shared $(ARCH) -o $@ $(OBJ) -cudart static
 
-oracle:
-	$(MAKE) -C oracle
-
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libswb200.sass
 	@grep -c UTCHMMA build/libswb200.sass || true
@@ -36,4 +34,4 @@ sass: $(LIB)
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean sass oracle
+.PHONY: all clean sass

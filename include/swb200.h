@@ -171,17 +171,19 @@ int swb_kv_push_layers(const void* qkv, size_t qkv_layer_stride, int layers,
                        int block_size, int num_ctas, uintptr_t stream);
 /* Hand-off of a finished prompt batch — the paper's per-request semaphore
  * and the reference's TRANSFER event (engine.py:286-297):
- * after all prior work on `stream` (the KV pushes), request i's slot
- * table + seqs[i] * stride_bytes (int32 [flag, first_token, ...]) gets
- * first_tok[i] (device) in word 1 and then epochs[i] in word 0.  The flag
- * stores are stream memory operations preceded by a full memory barrier,
- * so a consumer that observes flag == epoch also observes the token and
- * every pushed KV page.  `table` is device-accessible: host-mapped shared
- * memory (swb_host_register) polled by the token machine's host, or peer
- * memory.  n <= 64; seqs/epochs are host arrays. */
-int swb_kv_handoff(const int32_t* first_tok, int n, const int32_t* seqs,
-                   const uint32_t* epochs, void* table, int stride_bytes,
-                   uintptr_t stream);
+ * after all prior work on `stream` (the KV pushes), request i's record at
+ * table + seqs[i] * stride_bytes (int32 [flag, first_token, group_key, n])
+ * gets first_tok[rows[i]] (device; rows NULL = i), group_key and n, and then
+ * epochs[i] in word 0.  The flag stores are stream memory operations
+ * preceded by a full memory barrier, so a consumer that observes
+ * flag == epoch also observes the record and every pushed KV page; it admits
+ * the n records of one group together.  `table` is device-accessible:
+ * host-mapped shared memory (swb_host_register) polled by the token
+ * machine's host, or peer memory.  n <= 64; rows/seqs/epochs are host
+ * arrays; stride_bytes >= 16. */
+int swb_kv_handoff(const int32_t* first_tok, int n, const int32_t* rows,
+                   const int32_t* seqs, const uint32_t* epochs, int group_key,
+                   void* table, int stride_bytes, uintptr_t stream);
 /* Page-lock and map host memory (e.g. a /dev/shm mapping shared with the
  * token machine's process) for device stores; *dev_ptr receives its device
  * address. */

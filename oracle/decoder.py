@@ -128,8 +128,12 @@ class OracleDecoder:
     with ``extra`` = final_norm_b, emb_norm, emb_norm_b, alibi slopes)."""
 
     def __init__(self, cfg, layers, embed, lm_head, final_norm, threads: int | None = None,
-                 extra: dict | None = None):
+                 extra: dict | None = None, emulate_bf16: bool = False):
         self.cfg = cfg
+        # emulate_bf16: round every activation the device path stores in bf16
+        # (GEMM inputs, q/k/v, attention output, MLP activation) — a
+        # diagnostic twin that measures the error bf16 storage alone causes
+        self.emulate_bf16 = emulate_bf16
         self.layers = layers
         self.embed = embed
         self.lm_head = lm_head
@@ -153,6 +157,9 @@ class OracleDecoder:
         head = embed if w.lm_head.data_ptr() == w.embed.data_ptr() else w.lm_head.float().cpu()
         return cls(w.cfg, layers, embed, head, w.final_norm.float().cpu(), extra=extra)
 
+    def _r(self, t):
+        return t.bfloat16().float() if self.emulate_bf16 else t
+
     def _bloom_layer(self, li, x, pos0, kv_get, kv_put):
         """BLOOM block: pre-LayerNorm, fused biased qkv, ALiBi scores
         (slope * key position, as BLOOM builds its alibi tensor), biased
@@ -160,10 +167,11 @@ class OracleDecoder:
         cfg, L = self.cfg, self.layers[li]
         S = x.shape[0]
         H, dh, eps = cfg.n_heads, cfg.head_dim, cfg.norm_eps
-        h = _layernorm(x, L["ln1_w"], L["ln1_b"], eps)
-        q = (h @ L["wq"].t() + L["bq"]).view(S, H, dh)
-        k = (h @ L["wk"].t() + L["bk"]).view(S, H, dh)
-        v = (h @ L["wv"].t() + L["bv"]).view(S, H, dh)
+        r = self._r
+        h = r(_layernorm(x, L["ln1_w"], L["ln1_b"], eps))
+        q = r(h @ L["wq"].t() + L["bq"]).view(S, H, dh)
+        k = r(h @ L["wk"].t() + L["bk"]).view(S, H, dh)
+        v = r(h @ L["wv"].t() + L["bv"]).view(S, H, dh)
         kv_put(li, pos0, k, v)
         K_all, V_all = kv_get(li, pos0 + S)
         n = pos0 + S
@@ -172,10 +180,10 @@ class OracleDecoder:
         qpos = torch.arange(pos0, pos0 + S)[:, None]
         kpos = torch.arange(n)[None, :]
         s = s.masked_fill((kpos > qpos)[None], float("-inf"))
-        o = torch.einsum("hqk,khd->qhd", s.softmax(-1), V_all).reshape(S, H * dh)
+        o = r(torch.einsum("hqk,khd->qhd", s.softmax(-1), V_all).reshape(S, H * dh))
         x = x + o @ L["wo"].t() + L["bo"]
-        h2 = _layernorm(x, L["ln2_w"], L["ln2_b"], eps)
-        a = _gelu_tanh(h2 @ L["w_up"].t() + L["b_up"])
+        h2 = r(_layernorm(x, L["ln2_w"], L["ln2_b"], eps))
+        a = r(_gelu_tanh(h2 @ L["w_up"].t() + L["b_up"]))
         return x + a @ L["wd"].t() + L["bd"]
 
     # -- one layer over S new tokens at positions pos0.. with cached K/V
@@ -185,12 +193,13 @@ class OracleDecoder:
         cfg, L = self.cfg, self.layers[li]
         S = x.shape[0]
         H, Hkv, dh = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
-        h = _rmsnorm(x, L["attn_norm"], cfg.norm_eps)
-        q = (h @ L["wq"].t()).view(S, H, dh)
-        k = (h @ L["wk"].t()).view(S, Hkv, dh)
-        v = (h @ L["wv"].t()).view(S, Hkv, dh)
+        r = self._r
+        h = r(_rmsnorm(x, L["attn_norm"], cfg.norm_eps))
+        q = r(h @ L["wq"].t()).view(S, H, dh)
+        k = r(h @ L["wk"].t()).view(S, Hkv, dh)
+        v = r(h @ L["wv"].t()).view(S, Hkv, dh)
         cos, sin = rope_tables(torch.arange(pos0, pos0 + S), dh, cfg.rope_theta)
-        q, k = apply_rope(q, cos, sin), apply_rope(k, cos, sin)
+        q, k = r(apply_rope(q, cos, sin)), r(apply_rope(k, cos, sin))
         kv_put(li, pos0, k, v)
         K_all, V_all = kv_get(li, pos0 + S)
         G = H // Hkv
@@ -200,10 +209,10 @@ class OracleDecoder:
         qpos = torch.arange(pos0, pos0 + S)[:, None]
         kpos = torch.arange(pos0 + S)[None, :]
         s = s.masked_fill((kpos > qpos)[None], float("-inf"))
-        o = torch.einsum("hqk,khd->qhd", s.softmax(-1), Vx).reshape(S, H * dh)
+        o = r(torch.einsum("hqk,khd->qhd", s.softmax(-1), Vx).reshape(S, H * dh))
         x = x + o @ L["wo"].t()
-        h2 = _rmsnorm(x, L["mlp_norm"], cfg.norm_eps)
-        a = torch.nn.functional.silu(h2 @ L["w_gate"].t()) * (h2 @ L["w_up"].t())
+        h2 = r(_rmsnorm(x, L["mlp_norm"], cfg.norm_eps))
+        a = r(torch.nn.functional.silu(h2 @ L["w_gate"].t()) * (h2 @ L["w_up"].t()))
         return x + a @ L["wd"].t()
 
     def forward(self, tokens, pos0, kv_get, kv_put):
@@ -217,7 +226,7 @@ class OracleDecoder:
             h = _layernorm(x[-1:], self.final_norm, self.extra["final_norm_b"], eps)
         else:
             h = _rmsnorm(x[-1:], self.final_norm, eps)
-        return (h @ self.lm_head.t())[0]
+        return (self._r(h) @ self.lm_head.t())[0]
 
     # -- contiguous KV (preallocated when the final length is known, so a
     #    decode step writes one row instead of re-concatenating the cache)

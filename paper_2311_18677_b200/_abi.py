@@ -61,7 +61,7 @@ SIGNATURES = {
     "swb_rope_kv_write": [_P, _I, _I, _P, _I, _I, _I, _F, _P, _P, _P, _I, _ST],
     "swb_kv_push_layer": [_P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _I, _ST],
     "swb_kv_push_layers": [_P, _S, _I, _I, _I, _I, _I, _I, _I, _P, _P, _S, _P, _I, _I, _ST],
-    "swb_kv_handoff": [_P, _I, _P, _P, _P, _I, _ST],
+    "swb_kv_handoff": [_P, _I, _P, _P, _P, _I, _P, _I, _ST],
     "swb_host_register": [_P, _S, C.POINTER(_P)],
     "swb_host_unregister": [_P],
     "swb_attn_prefill": [_P, _I, _P, _I, _I, _I, _I, _I, _F, _P, _ST],

@@ -127,31 +127,30 @@ class ShmMailbox:
 
 
 class RouteBoard:
-    """Live JSQ routing across Splitwise pairs served concurrently in real
-    time (bench.py --trace).  One /dev/shm segment per run:
+    """Live JSQ routing at arrival for the real-time trace path: the
+    reference's ``Cluster.route`` (cluster.py:153-160) makes TWO independent
+    picks — the prompt machine by JSQ over the prompt pool and the token
+    machine by JSQ over the token pool — each the lowest (pending, id)
+    (``_argmin``, cluster.py:129-134) with pending = the machine's
+    ``pending_tokens`` (cluster.py:82-84): queued prompt tokens on a prompt
+    machine, one per live token task on a token machine.  Every prompt
+    machine maps every token machine's KV pool, so any pairing is served.
 
-      * ``assign[rid]`` — the pair a request was routed to (-1 = not yet
-        arrived), written once by the router at the request's arrival;
-      * per pair, cumulative counters the servers publish (absolute values, so
-        every TP peer may write them): prompt tokens / requests whose prompt
-        phase finished (prompt machine), requests finished (token machine).
+    One /dev/shm segment per run: ``assign_p[rid]`` / ``assign_t[rid]`` (the
+    picks, -1 until the request arrives; the prompt pick is published
+    first), per prompt machine the prompt tokens whose prompt phase finished,
+    per token machine the requests whose KV landed (token task live) and the
+    requests finished — cumulative values the servers publish.  The
+    router adds the prompt tokens it routed itself."""
 
-    The router keeps the cumulative routed prompt tokens and requests per
-    pair, so pending(pair) = queued prompt tokens (routed − prompt-done) +
-    one per live token task (prompt-done − finished): the reference's
-    ``pending_tokens`` (cluster.py:82-84) of the pair's prompt machine plus
-    that of its token machine.  The pick is the reference's ``_argmin``
-    (cluster.py:129-134): lowest (pending, id).  The prompt → token pairing
-    is fixed (each prompt machine pushes to its own token machine), so the
-    two JSQ picks of ``Cluster.route`` (cluster.py:153-160) collapse into
-    one pick over pairs."""
+    PROMPT_TOK = 0                # prompt machine field
+    LANDED, FINISHED = 0, 1       # token machine fields
 
-    PROMPT_TOK, PROMPT_REQ, FINISHED = 0, 1, 2
-
-    def __init__(self, n_requests: int, pairs: int, name: str | None = None,
-                 create: bool = False):
-        self.n, self.pairs = n_requests, pairs
-        size = 8 * (n_requests + 3 * pairs + 1)
+    def __init__(self, n_requests: int, prompts: int, tokens: int | None = None,
+                 name: str | None = None, create: bool = False):
+        tokens = prompts if tokens is None else tokens
+        self.n, self.prompts, self.tokens = n_requests, prompts, tokens
+        size = 8 * (2 * n_requests + prompts + 2 * tokens + 1)
         if create:
             self.shm = shared_memory.SharedMemory(create=True, size=size)
         else:
@@ -162,34 +161,44 @@ class RouteBoard:
             except Exception:
                 pass
         self.owner = create
-        a = np.ndarray((n_requests + 3 * pairs + 1,), dtype=np.int64, buffer=self.shm.buf)
-        self.assign = a[:n_requests]
-        self.load = a[n_requests:n_requests + 3 * pairs].reshape(pairs, 3)
+        a = np.ndarray((2 * n_requests + prompts + 2 * tokens + 1,), dtype=np.int64,
+                       buffer=self.shm.buf)
+        self.assign_p = a[:n_requests]
+        self.assign_t = a[n_requests:2 * n_requests]
+        o = 2 * n_requests
+        self.p_load = a[o:o + prompts]
+        self.t_load = a[o + prompts:o + prompts + 2 * tokens].reshape(tokens, 2)
         if create:
-            self.assign[:] = -1
-            self.load[:] = 0
-        self.routed_tok = [0] * pairs
-        self.routed_req = [0] * pairs
+            a[:] = 0
+            self.assign_p[:] = -1
+            self.assign_t[:] = -1
+        self.routed_tok = [0] * prompts
 
     @property
     def name(self) -> str:
         return self.shm.name
 
     # -- servers --------------------------------------------------------
-    def publish(self, pair: int, field: int, value: int) -> None:
-        self.load[pair, field] = value
+    def publish_prompt(self, machine: int, done_tokens: int) -> None:
+        self.p_load[machine] = done_tokens
+
+    def publish_token(self, machine: int, field: int, value: int) -> None:
+        self.t_load[machine, field] = value
 
     # -- router ---------------------------------------------------------
-    def pending(self, pair: int) -> int:
-        tok, req, fin = (int(v) for v in self.load[pair])
-        return (self.routed_tok[pair] - tok) + (req - fin)
+    def pending_prompt(self, m: int) -> int:
+        return self.routed_tok[m] - int(self.p_load[m])
 
-    def route(self, rid: int, prompt_tokens: int) -> int:
-        best = min(range(self.pairs), key=lambda p: (self.pending(p), p))
-        self.routed_tok[best] += prompt_tokens
-        self.routed_req[best] += 1
-        self.assign[rid] = best     # publish last: servers poll assign
-        return best
+    def pending_token(self, m: int) -> int:
+        return int(self.t_load[m, self.LANDED]) - int(self.t_load[m, self.FINISHED])
+
+    def route(self, rid: int, prompt_tokens: int) -> tuple[int, int]:
+        pm = min(range(self.prompts), key=lambda m: (self.pending_prompt(m), m))
+        tm = min(range(self.tokens), key=lambda m: (self.pending_token(m), m))
+        self.routed_tok[pm] += prompt_tokens
+        self.assign_p[rid] = pm       # publish the prompt pick first: the token
+        self.assign_t[rid] = tm       # machine reads it when it reserves
+        return pm, tm
 
     def run_router(self, requests, t0: float) -> None:
         """Route each request at its arrival (wall clock from t0); requests =
@@ -213,13 +222,16 @@ class RouteBoard:
 
 class ArrivalFeed:
     """Server side of the live routing: yields, in arrival order, the
-    requests routed to ``pair`` whose routing is already published.  With no
-    board it is the static list (request i -> pair i mod pairs)."""
+    requests routed to this machine (``role`` "prompt" or "token") whose
+    routing is already published.  With no board it is a static list."""
 
-    def __init__(self, requests, pair: int, board: RouteBoard | None = None):
+    def __init__(self, requests, machine: int, board: RouteBoard | None = None,
+                 role: str = "prompt"):
         self.all = list(requests)
-        self.pair = pair
+        self.machine = machine
         self.board = board
+        self.assign = None if board is None else (board.assign_p if role == "prompt"
+                                                  else board.assign_t)
         self.cursor = 0
         self.mine = 0
 
@@ -231,10 +243,10 @@ class ArrivalFeed:
             return out
         while self.cursor < len(self.all):
             r = self.all[self.cursor]
-            p = int(self.board.assign[r[0]])
-            if p < 0:
+            m = int(self.assign[r[0]])
+            if m < 0:
                 break
-            if p == self.pair:
+            if m == self.machine:
                 out.append(r)
             self.cursor += 1
         self.mine += len(out)
@@ -250,7 +262,8 @@ class ArrivalFeed:
 class HandoffTable:
     """Per-KV-slot hand-off records in host shared memory, int32
     [max_seqs][STRIDE/4]: word 0 = flag (epoch of the reservation whose KV
-    landed), word 1 = first token.  Created by the token machine's process;
+    landed), word 1 = first token, word 2 = group key of the prompt batch,
+    word 3 = the group's record count in this table.  Created by the token machine's process;
     the prompt machine's process attaches by name and page-locks / maps it
     (``device_ptr``) so its GPU stores the records (swb_kv_handoff)."""
 
@@ -296,6 +309,9 @@ class HandoffTable:
     def token(self, seq: int) -> int:
         return int(self.a[seq, 1])
 
+    def group(self, seq: int) -> tuple[int, int]:
+        return int(self.a[seq, 2]), int(self.a[seq, 3])
+
     def close(self) -> None:
         try:
             if self._host_ptr is not None:
@@ -311,9 +327,12 @@ class HandoffTable:
 
 
 class HandoffWatch:
-    """Token host: the reservations whose KV is on its way, in FIFO order
-    (the prompt machine batches FCFS, so they land in this order), and the
-    first instant each landing was observed (the first token's emission)."""
+    """Token host: the reservations whose KV is on its way, and the first
+    instant each landing was observed (the first token's emission).  A
+    prompt batch's requests are admitted together (all records of its group
+    landed) — the reference enqueues the token tasks of a batch at the same
+    transfer time — and groups from different prompt machines in whatever
+    order they land."""
 
     def __init__(self, table: HandoffTable, tp_group=None):
         self.table = table
@@ -324,30 +343,37 @@ class HandoffWatch:
     def expect(self, rid: int, seq: int, epoch: int, plen: int, n_out: int) -> None:
         self.pending.append([rid, seq, epoch, plen, n_out])
 
-    def observe(self) -> int:
-        """Record the observation time of newly landed leading reservations;
-        returns how many leading reservations have landed."""
-        k = 0
+    def observe(self) -> list:
+        """Time-stamp new landings; returns the pending indices whose whole
+        group has landed."""
         now = None
-        for rid, seq, epoch, _p, _o in self.pending:
+        landed, count = [], {}
+        for i, (rid, seq, epoch, _p, _o) in enumerate(self.pending):
             if not self.table.landed(seq, epoch):
-                break
+                continue
             if rid not in self.seen:
                 now = now or time.perf_counter()
                 self.seen[rid] = now
-            k += 1
-        return k
+            key, n = self.table.group(seq)
+            landed.append((i, key, n))
+            count[key] = count.get(key, 0) + 1
+        return [i for i, key, n in landed if count[key] >= n]
 
     def poll(self) -> list:
-        """Hand-off rows (rid, seq, plen, first token, n_out) of the leading
-        landed reservations — the same prefix on every TP peer."""
-        k = self.observe()
-        if self.tp_group is not None:
-            t = torch.tensor([k], dtype=torch.int64)
-            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.tp_group)
-            k = int(t.item())
-        rows = []
-        for rid, seq, _e, plen, n_out in self.pending[:k]:
-            rows.append((rid, seq, plen, self.table.token(seq), n_out))
-        del self.pending[:k]
+        """Hand-off rows (rid, seq, plen, first token, n_out) of the complete
+        landed groups, in reservation order — the same set on every TP peer
+        (MIN all-reduce of the per-reservation ready mask)."""
+        ready = self.observe()
+        if self.tp_group is not None and self.pending:
+            mask = torch.zeros(len(self.pending), dtype=torch.int32)
+            if ready:
+                mask[ready] = 1
+            dist.all_reduce(mask, op=dist.ReduceOp.MIN, group=self.tp_group)
+            ready = mask.nonzero().flatten().tolist()
+        if not ready:
+            return []
+        take = set(ready)
+        rows = [(rid, seq, plen, self.table.token(seq), n_out)
+                for i, (rid, seq, _e, plen, n_out) in enumerate(self.pending) if i in take]
+        self.pending = [r for i, r in enumerate(self.pending) if i not in take]
         return rows

@@ -288,23 +288,28 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Hand-off record of a finished prompt batch: thread i stores request i's
-// first token into word 1 of its slot in the token machine's hand-off table
-// (host-mapped shared memory or peer memory); the per-request flags (word 0)
-// follow as stream memory operations (swb_kv_handoff).
+// Hand-off record of a finished prompt batch in the token machine's table
+// (host-mapped shared memory or peer memory), per request i: word 1 = its
+// first token (first[row[i]]), word 2 = the batch's group key, word 3 = how
+// many records of this table the batch writes (the token machine admits a
+// group only when all of it landed); the per-request flags (word 0) follow
+// as stream memory operations (swb_kv_handoff).
 constexpr int HANDOFF_MAX = 64;
 struct HandoffBatch {
   int seq[HANDOFF_MAX];
+  int row[HANDOFF_MAX];
 };
 __global__ void handoff_token_kernel(const int32_t* __restrict__ first, int n,
-                                     HandoffBatch b, char* base, int stride) {
+                                     HandoffBatch b, int key, char* base, int stride) {
   pdl_trigger();
   pdl_wait();
   const int i = threadIdx.x;
   if (i < n) {
     int32_t* rec = reinterpret_cast<int32_t*>(base + (size_t)b.seq[i] * stride);
-    asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(rec + 1), "r"(first[i])
+    asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(rec + 1), "r"(first[b.row[i]])
                  : "memory");
+    asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(rec + 2), "r"(key) : "memory");
+    asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(rec + 3), "r"(n) : "memory");
   }
 }
 
@@ -562,19 +567,22 @@ static PFN_cuStreamWriteValue32_v11070 write_value_fn() {
   return fn;
 }
 
-extern "C" int swb_kv_handoff(const int32_t* first_tok, int n, const int32_t* seqs,
-                              const uint32_t* epochs, void* table, int stride_bytes,
-                              uintptr_t stream) {
+extern "C" int swb_kv_handoff(const int32_t* first_tok, int n, const int32_t* rows,
+                              const int32_t* seqs, const uint32_t* epochs, int group_key,
+                              void* table, int stride_bytes, uintptr_t stream) {
   SWB_REQUIRE(first_tok && seqs && epochs && table, "swb_kv_handoff: null pointer");
-  SWB_REQUIRE(n > 0 && n <= HANDOFF_MAX && stride_bytes >= 8 && stride_bytes % 4 == 0,
-              "swb_kv_handoff: bad batch (n <= %d)", HANDOFF_MAX);
+  SWB_REQUIRE(n > 0 && n <= HANDOFF_MAX && stride_bytes >= 16 && stride_bytes % 4 == 0,
+              "swb_kv_handoff: bad batch (n <= %d, stride >= 16)", HANDOFF_MAX);
   HandoffBatch b;
   for (int i = 0; i < n; ++i) {
     SWB_REQUIRE(seqs[i] >= 0, "swb_kv_handoff: negative slot");
     b.seq[i] = seqs[i];
+    b.row[i] = rows ? rows[i] : i;
+    SWB_REQUIRE(b.row[i] >= 0, "swb_kv_handoff: negative row");
   }
   const cudaError_t le = launch(handoff_token_kernel, dim3(1), dim3(HANDOFF_MAX), 0, STREAM,
-                                first_tok, n, b, reinterpret_cast<char*>(table), stride_bytes);
+                                first_tok, n, b, group_key, reinterpret_cast<char*>(table),
+                                stride_bytes);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch handoff_token_kernel: %s", cudaGetErrorString(le));
   int rc = swb_check_launch("handoff_token_kernel");

@@ -294,17 +294,21 @@ def slots_from_table(table_row_ptr, start, n, block_size, slots, stream=None):
          stream if stream is not None else _stream())
 
 
-def kv_handoff(first_tok, seqs, epochs, table_dev_ptr, stride_bytes, stream=None):
-    """Publish a finished prompt batch to the token machine's hand-off table:
-    first tokens, then per-request flags = epochs, after all prior work on
-    the stream (the KV pushes)."""
+def kv_handoff(first_tok, seqs, epochs, table_dev_ptr, stride_bytes, rows=None, group_key=0,
+               stream=None):
+    """Publish a finished prompt batch to a token machine's hand-off table:
+    per request its first token (first_tok[rows[i]]), the group key and
+    size, then its flag = epoch — after all prior work on the stream (the
+    KV pushes)."""
     _req(first_tok, torch.int32, "first_tok")
     n = len(seqs)
     if n == 0:
         return
-    if n != len(epochs) or first_tok.numel() < n:
-        raise ValidationError("kv_handoff: seqs / epochs / first_tok lengths differ")
+    rows = list(range(n)) if rows is None else list(rows)
+    if n != len(epochs) or n != len(rows) or max(rows) >= first_tok.numel():
+        raise ValidationError("kv_handoff: seqs / epochs / rows / first_tok lengths differ")
+    r = (ctypes.c_int32 * n)(*rows)
     s = (ctypes.c_int32 * n)(*seqs)
     e = (ctypes.c_uint32 * n)(*epochs)
-    call("swb_kv_handoff", first_tok.data_ptr(), n, s, e, table_dev_ptr, stride_bytes,
-         stream if stream is not None else _stream())
+    call("swb_kv_handoff", first_tok.data_ptr(), n, r, s, e, int(group_key), table_dev_ptr,
+         stride_bytes, stream if stream is not None else _stream())

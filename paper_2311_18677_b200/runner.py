@@ -64,12 +64,16 @@ class PushStats:
 
 @dataclass
 class Handoff:
-    """Where a prompt batch announces its landed KV (control.HandoffTable):
-    per request the token machine's KV slot and reservation epoch, and the
-    table's device address in this process."""
+    """Where a prompt batch announces its landed KV to ONE token machine
+    (control.HandoffTable): per request the batch row, the token machine's
+    KV slot and reservation epoch; the table's device address in this
+    process; the batch's group key (the token machine admits the group's
+    requests together)."""
     seqs: list
     epochs: list
     table_ptr: int
+    rows: list | None = None
+    key: int = 0
     stride: int = 16
 
 
@@ -255,15 +259,16 @@ class ModelRunner:
                 local_slots: torch.Tensor | None = None,
                 push: list[PushSegment] | None = None,
                 push_stats: PushStats | None = None,
-                handoff: Handoff | None = None, mode: str | None = None) -> torch.Tensor:
+                handoff: Handoff | list | None = None, mode: str | None = None) -> torch.Tensor:
         """Run the prompt phase for a batch of prompts packed back to back.
 
         tokens      int32 [T] on device
         meta        int32 device tensor = [positions(T) | cu_seqlens(R+1) | last_rows(R)]
         local_slots int32 [T] slots in this GPU's pool (co-located token phase)
         push        per-request destination segments (token machine elsewhere)
-        handoff     announce the landed KV to the token machine (control.
-                    HandoffTable) from the push stream; the call then returns
+        handoff     announce the landed KV to the token machine(s) (one Handoff
+                    per destination table, control.HandoffTable) from the push
+                    stream; the call then returns
                     without waiting for the pushes (the prompt machine is free
                     once its compute ends).  Without it, the current stream
                     waits for every push before the call returns.
@@ -279,6 +284,8 @@ class ModelRunner:
         x, h, attn, act = self.px[:T], self.ph[:T], self.pattn[:T], self.pact[:T]
         main = torch.cuda.current_stream()
         mode = (mode or self.transfer_mode(lens)) if push else LAYERWISE
+        handoffs = ([] if handoff is None else
+                    list(handoff) if isinstance(handoff, (list, tuple)) else [handoff])
         serial = push and mode == SERIALIZED
         timing = None
         if push:
@@ -374,9 +381,10 @@ class ModelRunner:
                                          stream=self.push_stream.cuda_stream)
                     if timing:
                         timing[0][1].record(self.push_stream)
-                if handoff is not None:
-                    K.kv_handoff(first, handoff.seqs, handoff.epochs, handoff.table_ptr,
-                                 handoff.stride, stream=self.push_stream.cuda_stream)
+                for hnd in handoffs:
+                    K.kv_handoff(first, hnd.seqs, hnd.epochs, hnd.table_ptr, hnd.stride,
+                                 rows=hnd.rows, group_key=hnd.key,
+                                 stream=self.push_stream.cuda_stream)
                 tail = torch.cuda.Event()
                 tail.record(self.push_stream)
             # the next batch reuses the buffers (and pfirst) only after this tail
@@ -384,7 +392,7 @@ class ModelRunner:
                 self._stash_ev = tail
             else:
                 self._buf_ev[(cfg.n_layers - 1) & 1] = tail
-            if handoff is None:
+            if not handoffs:
                 main.wait_event(tail)       # KV fully landed before we report done
             if push_stats is not None:
                 self._pending_push.append((timing, compute_start, compute_end, tail, push_stats))

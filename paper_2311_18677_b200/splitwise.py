@@ -77,38 +77,57 @@ def _lockstep(n: int, tp_ctrl, now_ms: float = 0.0, fin: bool = False):
 
 
 class PromptServer:
-    """Prompt machine of a Splitwise pair (one process per GPU / TP rank)."""
+    """Prompt machine (one process per GPU / TP rank).  It maps the KV pool,
+    the hand-off table and the reservation mailbox of EVERY token machine
+    (same TP rank), so a request can be pushed to whichever token machine
+    the router picked (reference Cluster.route, cluster.py:153-160)."""
 
-    def __init__(self, runner: ModelRunner, peer: KVCacheManager, ctrl, token_rank: int,
-                 sched: SchedulerConfig, table_name: str, tp_ctrl=None):
+    def __init__(self, runner: ModelRunner, peers: dict, ctrl, token_rank: int,
+                 sched: SchedulerConfig, tables: dict, tp_ctrl=None, machine_id: int = 0,
+                 res_boxes: dict | None = None):
+        """peers / tables: {token machine: KVCacheManager peer view / hand-off
+        table name}; token_rank: the control-group rank of the paired token
+        machine (burst mode); res_boxes: {token machine: mailbox name}."""
         self.runner = runner
         self.tp_ctrl = tp_ctrl          # TP peers must batch in lockstep (collectives inside)
-        self.peer = peer
-        self.table = HandoffTable(name=table_name)
-        self.table_ptr = self.table.device_ptr()
+        self.peers = dict(peers)
+        self.tables = {t: HandoffTable(name=n) for t, n in tables.items()}
+        self.table_ptrs = {t: tb.device_ptr() for t, tb in self.tables.items()}
+        self.res_boxes = {t: ShmMailbox(name=n) for t, n in (res_boxes or {}).items()}
         self.ctrl = ctrl
         self.token_rank = token_rank
+        self.machine_id = machine_id
+        self._batches = 0
         cfg = runner.cfg
         hbm = float(torch.cuda.get_device_properties(runner.dev).total_memory)
         self.machine = Machine(0, None, estimated_perf_model(cfg, None, runner.w.nbytes(),
                                                              capacity=hbm), PROMPT, sched)
         self.push_log: list[PushStats] = []
 
-    def _run_batch(self, chunk, seq_of, epoch_of, toks):
-        """chunk: [(rid, prompt, n_out)].  Enqueue the prefill, the per-layer
-        pushes into the reserved pages and the hand-off records, then wait
-        only for the prompt COMPUTE (the pushes' tail and the hand-off run on
-        the push stream).  Returns the host time the compute finished."""
+    def _run_batch(self, chunk, dest, toks):
+        """chunk: [(rid, prompt, n_out)]; dest: {rid: (token machine, KV slot,
+        epoch)}.  Enqueue the prefill, the per-layer pushes into the reserved
+        pages of each request's token machine and one hand-off group per
+        destination table, then wait only for the prompt COMPUTE (the pushes'
+        tail and the hand-off run on the push stream).  Returns the host time
+        the compute finished."""
         lens = [len(r[1]) for r in chunk]
         meta = ModelRunner.pack_meta(lens).pin_memory().to(self.runner.dev, non_blocking=True)
         segs, off = [], 0
         for r, n in zip(chunk, lens):
-            segs.append(PushSegment(off, n, self.peer, seq_of[r[0]]))
+            t, seq, _ep = dest[r[0]]
+            segs.append(PushSegment(off, n, self.peers[t], seq))
             off += n
         st = PushStats(bytes_per_layer=off * 2 * self.runner.hkv * self.runner.dh * 2)
-        hand = Handoff([seq_of[r[0]] for r in chunk], [epoch_of[r[0]] for r in chunk],
-                       self.table_ptr, HandoffTable.STRIDE)
-        self.runner.prefill(toks, lens, meta, push=segs, push_stats=st, handoff=hand)
+        self._batches += 1
+        key = ((self.machine_id & 0xFF) << 23) | (self._batches & 0x7FFFFF)
+        hands = []
+        for t in sorted({dest[r[0]][0] for r in chunk}):
+            idx = [i for i, r in enumerate(chunk) if dest[r[0]][0] == t]
+            hands.append(Handoff([dest[chunk[i][0]][1] for i in idx],
+                                 [dest[chunk[i][0]][2] for i in idx], self.table_ptrs[t],
+                                 rows=idx, key=key, stride=HandoffTable.STRIDE))
+        self.runner.prefill(toks, lens, meta, push=segs, push_stats=st, handoff=hands)
         done = torch.cuda.Event()
         done.record()
         done.synchronize()
@@ -122,8 +141,8 @@ class PromptServer:
         dev = self.runner.dev
         seqs, epochs = recv_reservations(len(requests), self.token_rank, self.ctrl,
                                          with_epochs=True)
-        seq_of = {r[0]: s for r, s in zip(requests, seqs)}
-        epoch_of = {r[0]: e for r, e in zip(requests, epochs)}
+        t = self.machine_id                       # burst mode: the paired token machine
+        dest = {r[0]: (t, s, e) for r, s, e in zip(requests, seqs, epochs)}
         by_id = {r[0]: r for r in requests}
         now_ms = 0.0
         for rid, prompt, n_out in requests:
@@ -137,7 +156,7 @@ class PromptServer:
                 toks = torch.cat([prompts_dev[r[0]] for r in chunk])
             else:
                 toks = torch.cat([r[1] for r in chunk]).pin_memory().to(dev, non_blocking=True)
-            tnow = self._run_batch(chunk, seq_of, epoch_of, toks)
+            tnow = self._run_batch(chunk, dest, toks)
             for r in chunk:
                 done_time[r[0]] = tnow
             now_ms = (tnow - t0) * 1e3
@@ -148,39 +167,45 @@ class PromptServer:
     def serve_trace(self, requests, t0: float, feed=None):
         """Arrival-driven prompt machine: requests = [(rid, arrival_s, host
         prompt, n_out)] in arrival order.  A request becomes a prompt task
-        (enqueue time = its arrival) once the token machine has reserved its
-        final context (reservation mailbox; the token machine admits
-        reservations in arrival order with the blocked-head memory rule), so
-        its KV always has pages to land in.  Batches follow the reference
-        prompt rule.  Returns {rid: host time its prompt compute finished}.
-        ``feed`` (control.ArrivalFeed) supplies the requests the live JSQ
-        router sent to this pair; without one every request is this
-        machine's."""
+        (enqueue time = its arrival) once the token machine it was routed to
+        has reserved its final context (that machine's reservation mailbox;
+        token machines admit reservations in arrival order with the
+        blocked-head memory rule), so its KV always has pages to land in;
+        tasks are enqueued in arrival order (the longest reserved prefix).
+        Batches follow the reference prompt rule.  Returns {rid: host time its
+        prompt compute finished}.  ``feed`` (control.ArrivalFeed, role
+        "prompt") supplies the requests the live router sent to this
+        machine; without one every request is this machine's and goes to
+        token machine ``self.machine_id``."""
         feed = feed or ArrivalFeed(requests, 0)
         board = getattr(self, "board", None)
         by_id = {r[0]: r for r in requests}
-        reserved: list = []             # (rid, seq, epoch) in reservation order
-        seq_of, epoch_of = {}, {}
+        mine: list = []                 # my arrivals, in arrival order
+        dest: dict = {}                 # rid -> (token machine, slot, epoch)
         done_time = {}
         done = 0
         done_tok = 0
         while True:
-            feed.poll()
-            while True:
-                rows = self.res_box.get()
-                if rows is None:
-                    break
-                reserved += [(rid, seq, ep) for rid, seq, ep, *_ in rows]
+            mine += [r[0] for r in feed.poll()]
+            for t, box in self.res_boxes.items():
+                while True:
+                    rows = box.get()
+                    if rows is None:
+                        break
+                    for rid, seq, ep, *_ in rows:
+                        dest[rid] = (t, seq, ep)
+            n_res = 0
+            while n_res < len(mine) and mine[n_res] in dest:
+                n_res += 1
             fin = feed.complete() and done >= feed.mine
-            n_take, _, fin = _lockstep(len(reserved), self.tp_ctrl, 0.0, fin)
+            n_take, _, fin = _lockstep(n_res, self.tp_ctrl, 0.0, fin)
             if fin:
                 break
-            for rid, seq, ep in reserved[:n_take]:
+            for rid in mine[:n_take]:
                 _, arr, prompt, n_out = by_id[rid]
-                seq_of[rid], epoch_of[rid] = seq, ep
                 self.machine.enqueue(Task(rid, PROMPT, len(prompt), arr * 1e3, n_out, n_out),
                                      arr * 1e3)
-            del reserved[:n_take]
+            del mine[:n_take]
             if not self.machine.has_work():
                 time.sleep(5e-5)
                 continue
@@ -190,33 +215,38 @@ class PromptServer:
             chunk = [(r[0], r[2], r[3]) for r in (by_id[t.request_id] for t in batch.prompt_tasks)]
             toks = torch.cat([r[1] for r in chunk]).pin_memory().to(self.runner.dev,
                                                                       non_blocking=True)
-            tnow = self._run_batch(chunk, seq_of, epoch_of, toks)
+            tnow = self._run_batch(chunk, dest, toks)
             for r in chunk:
                 done_time[r[0]] = tnow
             done += len(chunk)
             done_tok += sum(len(r[1]) for r in chunk)
             if board is not None:
-                board.publish(self.pair, board.PROMPT_TOK, done_tok)
-                board.publish(self.pair, board.PROMPT_REQ, done)
+                board.publish_prompt(self.machine_id, done_tok)
             self.machine.complete_iteration(batch, (tnow - t0) * 1e3)
         self.runner.finish_push_stats(block=True)
         return done_time
 
     def close(self):
-        self.table.close()
-        self.res_box.close()
+        for tb in self.tables.values():
+            tb.close()
+        for box in self.res_boxes.values():
+            box.close()
 
 
 class TokenServer:
     """Token machine of a Splitwise pair (one process per GPU / TP rank)."""
 
     def __init__(self, runner: ModelRunner, ctrl, prompt_rank: int, sched: SchedulerConfig,
-                 tp_ctrl=None):
+                 tp_ctrl=None, machine_id: int = 0, prompt_machines: int = 1):
+        """prompt_rank: control-group rank of the paired prompt machine (burst
+        mode); one reservation mailbox per prompt machine (res_boxes)."""
         self.runner = runner
         self.kv = runner.kv
         self.ctrl = ctrl
         self.prompt_rank = prompt_rank
+        self.machine_id = machine_id
         self.tp_ctrl = tp_ctrl          # TP peers must admit in lockstep (collectives inside)
+        self.res_boxes = {p: ShmMailbox(create=True) for p in range(prompt_machines)}
         self.table = HandoffTable(self.kv.max_seqs, create=True)
         self.watch = HandoffWatch(self.table, tp_ctrl)
         self.epoch = [0] * self.kv.max_seqs
@@ -348,10 +378,13 @@ class TokenServer:
         landed hand-offs between decode iterations (continuous batching with
         the reference token rule), one CUDA-graph step per iteration.
         Returns ({rid: [emission times]}, decode step log, {rid: first-token
-        time})."""
+        time}).  ``feed`` (role "token") supplies the requests routed here;
+        each one's prompt machine is the board's pick (``assign_p``), or
+        ``self.machine_id`` without a board."""
         kv = self.kv
         feed = feed or ArrivalFeed(requests, 0)
         board = getattr(self, "board", None)
+        landed = 0
         pending = []
         info, remaining, emit, first_seen = {}, {}, {}, {}
         finished = 0
@@ -379,9 +412,17 @@ class TokenServer:
                 self.watch.expect(rid, seq, ep, len(prompt), n_out)
             if arrived:
                 torch.cuda.current_stream().synchronize()   # table rows before the peer reads
-                self.res_box.put([(rid, seq, ep, 0, 0) for rid, seq, ep in arrived])
+                by_p: dict = {}
+                for rid, seq, ep in arrived:
+                    pm = int(board.assign_p[rid]) if board is not None else self.machine_id
+                    by_p.setdefault(pm, []).append((rid, seq, ep, 0, 0))
+                for pm, rows in by_p.items():
+                    self.res_boxes[pm].put(rows)
             for rid, seq, plen, first, n_out in self.watch.poll():
                 first_seen[rid] = self.watch.seen.pop(rid)
+                landed += 1
+                if board is not None:
+                    board.publish_token(self.machine_id, board.LANDED, landed)
                 if n_out > 1:
                     info[rid] = [seq, plen, first]
                     remaining[rid] = n_out - 1
@@ -390,7 +431,7 @@ class TokenServer:
                     kv.release(seq)
                     finished += 1
                     if board is not None:
-                        board.publish(self.pair, board.FINISHED, finished)
+                        board.publish_token(self.machine_id, board.FINISHED, finished)
             if not self.machine.has_work() and not self.machine.resident:
                 time.sleep(5e-5)
                 continue
@@ -418,13 +459,14 @@ class TokenServer:
                     kv.release(info[task.request_id][0])
                     finished += 1
                     if board is not None:
-                        board.publish(self.pair, board.FINISHED, finished)
+                        board.publish_token(self.machine_id, board.FINISHED, finished)
                     graph_rids = None
         return emit, self.step_log, first_seen
 
     def close(self):
         self.table.close()
-        self.res_box.close()
+        for box in self.res_boxes.values():
+            box.close()
 
 
 # ---------------------------------------------------------------------------
@@ -484,14 +526,9 @@ def run_split_bench(args, ClockSampler, percentile, cpu_baseline, peaks, ncu_tra
     P, O = args.prompt, args.out
     R = 2 * tp                                  # one request per GPU of the pair
     sched = SchedulerConfig()
+    pairs = world // (2 * tp)
     if is_prompt:
         runner = ModelRunner(w, None, tp_group=tp_nccl)
-        handle = [None, None, None]
-        dist.recv_object_list(handle, src=peer_rank, group=ctrl)
-        peer = KVCacheManager.open_peer(handle[0])
-        server = PromptServer(runner, peer, ctrl, peer_rank, sched, table_name=handle[1],
-                              tp_ctrl=tp_gloo)
-        server.res_box = ShmMailbox(name=handle[2])
     else:
         trace_mode = bool(getattr(args, "trace", None))
         nb = pool_blocks_for_memory(cfg, tp, 16, reserve_bytes=2 << 30)
@@ -500,10 +537,23 @@ def run_split_bench(args, ClockSampler, percentile, cpu_baseline, peaks, ncu_tra
         kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads // tp, cfg.head_dim, 16,
                             256 if trace_mode else 64, blocks_for(8192 + 4096, 16))
         runner = ModelRunner(w, kv, tp_group=tp_nccl)
-        server = TokenServer(runner, ctrl, peer_rank, sched, tp_ctrl=tp_gloo)
-        server.res_box = ShmMailbox(create=True)
-        dist.send_object_list([kv.ipc_handle(), server.table.name, server.res_box.name],
-                              dst=peer_rank, group=ctrl)
+        server = TokenServer(runner, ctrl, peer_rank, sched, tp_ctrl=tp_gloo, machine_id=pair,
+                             prompt_machines=pairs)
+    # every token machine's (TP rank i) pool, hand-off table and per-prompt-
+    # machine mailboxes go to every prompt machine's TP rank i (any-to-any)
+    info = None if is_prompt else {"machine": pair, "tp_rank": tp_rank,
+                                   "kv": kv.ipc_handle(), "table": server.table.name,
+                                   "boxes": {p: b.name for p, b in server.res_boxes.items()}}
+    everyone = [None] * world
+    dist.all_gather_object(everyone, info, group=ctrl)
+    if is_prompt:
+        mine = [e for e in everyone if e is not None and e["tp_rank"] == tp_rank]
+        peers = {e["machine"]: KVCacheManager.open_peer(e["kv"]) for e in mine}
+        server = PromptServer(runner, peers, ctrl, peer_rank, sched,
+                              {e["machine"]: e["table"] for e in mine}, tp_ctrl=tp_gloo,
+                              machine_id=pair,
+                              res_boxes={e["machine"]: e["boxes"][pair] for e in mine})
+        peer = peers[pair]
     push_alone = None
     if is_prompt:
         # KV-push kernel alone over NVLink (no concurrent prefill): one layer of
@@ -694,17 +744,18 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
     jsq = getattr(args, "route", "jsq") == "jsq" and pairs > 1
     board, router = None, None
     if jsq:
-        # live JSQ over pairs (control.RouteBoard); rank 0 hosts the router
+        # live JSQ, independent prompt and token picks (control.RouteBoard);
+        # rank 0 hosts the router
         name = [None]
         if rank == 0:
-            board = RouteBoard(len(reqs_all), pairs, create=True)
+            board = RouteBoard(len(reqs_all), pairs, pairs, create=True)
             name = [board.name]
         dist.broadcast_object_list(name, src=0, group=ctrl)
         if rank != 0:
-            board = RouteBoard(len(reqs_all), pairs, name=name[0])
-        server.board, server.pair = board, pair
+            board = RouteBoard(len(reqs_all), pairs, pairs, name=name[0])
+        server.board = board
         items = [(r.id, r.arrival, prompts[r.id], r.output_tokens) for r in reqs_all]
-        feed = ArrivalFeed(items, pair, board)
+        feed = ArrivalFeed(items, pair, board, role="prompt" if is_prompt else "token")
     else:
         mine = [r for r in reqs_all if r.id % pairs == pair]
         items = [(r.id, r.arrival, prompts[r.id], r.output_tokens) for r in mine]
@@ -761,7 +812,9 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
             "config": {"workload": f"{args.trace} trace rate {args.rate}/s for {args.duration} s "
                                    f"(seed {args.seed}), {len(reqs_all)} requests, "
                                    f"{pairs} Splitwise pair(s) TP{tp}+TP{tp}, "
-                                   + ("live JSQ routing over pairs at arrival" if jsq else
+                                   + ("live JSQ routing at arrival, independent prompt and "
+                                      "token picks (any prompt machine -> any token machine)"
+                                      if jsq else
                                       f"request i -> pair i mod {pairs}" if pairs > 1 else
                                       "every request on the one pair")
                                    + ", served concurrently in real time",

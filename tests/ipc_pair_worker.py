@@ -61,6 +61,38 @@ def colocated(w, prompt, n_out, want_logits=False):
     return out, pages, logits
 
 
+def colocated_batch(w, prompts, n_out):
+    """The burst as ONE co-located prefill batch + one B=len(prompts) decode
+    graph — the schedule the pair runs (the prompt machine batches all three,
+    the token machine admits the landed group together)."""
+    from paper_2311_18677_b200 import kernels as K
+    from paper_2311_18677_b200.kvcache import KVCacheManager
+    from paper_2311_18677_b200.runner import ModelRunner
+    cfg = w.cfg
+    lens = [len(p) for p in prompts]
+    nb = sum((n + n_out + 15) // 16 for n in lens) + 4
+    kv = KVCacheManager(cfg.n_layers, nb, cfg.n_kv_heads, cfg.head_dim, 16, len(prompts), nb)
+    r = ModelRunner(w, kv)
+    seqs = [kv.allocate(n + n_out) for n in lens]
+    toks = torch.tensor(sum(prompts, []), dtype=torch.int32, device="cuda")
+    slots = torch.empty(sum(lens), dtype=torch.int32, device="cuda")
+    off = 0
+    for sq, n in zip(seqs, lens):
+        K.slots_from_table(kv.table_row_ptr(sq), 0, n, 16, slots[off:off + n])
+        off += n
+    first = r.prefill(toks, lens, ModelRunner.pack_meta(lens).cuda(), local_slots=slots)
+    # the token server's context bucket (TokenServer._graph_for): same
+    # attention partitioning, so the same split-K merge order
+    need = max(lens) + n_out
+    g = r.decode_graph(len(prompts), 2048 * ((need + 2047) // 2048), n_out)
+    g.load(seqs, first[:len(prompts)], lens)
+    g.capture()
+    for _ in range(n_out - 1):
+        g.replay()
+    torch.cuda.synchronize()
+    return [[int(first[b])] + g.out_ring[b, :n_out - 1].tolist() for b in range(len(prompts))]
+
+
 def gather(kv, seq, P):
     tb = kv.tables()[seq].long()
     p = torch.arange(P, device="cuda")
@@ -87,7 +119,7 @@ def main(rank, port, model, out_path, cases):
     dist.init_process_group("gloo", rank=rank, world_size=2)
     torch.cuda.set_device(0)
     from oracle.decoder import LowestFreeAllocator
-    from paper_2311_18677_b200.control import ShmMailbox, recv_reservations, send_reservations
+    from paper_2311_18677_b200.control import recv_reservations, send_reservations
     from paper_2311_18677_b200.kvcache import KVCacheManager
     from paper_2311_18677_b200.model import init_weights
     from paper_2311_18677_b200.runner import ModelRunner
@@ -104,12 +136,12 @@ def main(rank, port, model, out_path, cases):
     if rank == 1:
         kv = KVCacheManager(cfg.n_layers, NB, cfg.n_kv_heads, cfg.head_dim, 16, 8, 128)
         runner = ModelRunner(w, kv)
-        server = TokenServer(runner, None, 0, SchedulerConfig())
-        server.res_box = ShmMailbox(create=True)
+        server = TokenServer(runner, None, 0, SchedulerConfig(), machine_id=0, prompt_machines=1)
         cpu = LowestFreeAllocator(NB)
         pad = kv.allocate(100)              # non-trivial tables
         cpu.alloc(7)
-        dist.send_object_list([kv.ipc_handle(), server.table.name, server.res_box.name], dst=0)
+        dist.send_object_list([kv.ipc_handle(), server.table.name, server.res_boxes[0].name],
+                              dst=0)
         res = {"cases": []}
         for P, prompt in zip(cases, prompts):
             seq, ep = server._reserve(P + n_out)
@@ -148,12 +180,12 @@ def main(rank, port, model, out_path, cases):
         # phase 2: the bench's serve_burst path
         reqs = [(100 + i, torch.tensor(p, dtype=torch.int32), n_out) for i, p in enumerate(burst)]
         emit, tokens, first_seen = server.serve_burst(reqs, time.perf_counter())
-        res["burst"] = [{"rid": rid, "tokens": tokens[rid],
-                         "colocated": colocated(w, p, n_out)[0],
+        ref = colocated_batch(w, burst, n_out)
+        res["burst"] = [{"rid": rid, "tokens": tokens[rid], "colocated": ref[i],
                          "emitted": len(emit[rid]), "first_seen": rid in first_seen}
-                        for (rid, _, _), p in zip(reqs, burst)]
+                        for i, (rid, _, _) in enumerate(reqs)]
+        res["burst_steps"] = [b for b, _, _ in server.step_log]
         kv.release(pad)
-        res["mode"] = [c for c in res["cases"]]
         server.close()
         with open(out_path, "w") as f:
             json.dump(res, f)
@@ -162,13 +194,13 @@ def main(rank, port, model, out_path, cases):
         dist.recv_object_list(handle, src=1)
         peer = KVCacheManager.open_peer(handle[0])
         runner = ModelRunner(w, None)
-        server = PromptServer(runner, peer, None, 1, SchedulerConfig(), table_name=handle[1])
-        server.res_box = ShmMailbox(name=handle[2])
+        server = PromptServer(runner, {0: peer}, None, 1, SchedulerConfig(), {0: handle[1]},
+                              machine_id=0, res_boxes={0: handle[2]})
         modes = []
         for P, prompt in zip(cases, prompts):
             (seq,), (ep,) = recv_reservations(1, 1, None, with_epochs=True)
             toks = torch.tensor(prompt, dtype=torch.int32, device="cuda")
-            server._run_batch([(0, prompt, n_out)], {0: seq}, {0: ep}, toks)
+            server._run_batch([(0, prompt, n_out)], {0: (0, seq, ep)}, toks)
             modes.append(server.push_log[-1].mode)
         runner.finish_push_stats(block=True)
         dist.barrier()

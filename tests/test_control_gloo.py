@@ -29,9 +29,12 @@ def _init(rank, world, port):
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
 
-def _land(table, seq, epoch, token):
-    """What swb_kv_handoff does from the prompt GPU: token, then flag."""
+def _land(table, seq, epoch, token, key=0, n=1):
+    """What swb_kv_handoff does from the prompt GPU: token, group key and
+    size, then the flag."""
     table.a[seq, 1] = token
+    table.a[seq, 2] = key
+    table.a[seq, 3] = n
     table.a[seq, 0] = epoch
 
 
@@ -61,10 +64,10 @@ def _pair(rank, world, port, q):
             table = HandoffTable(name=name[0])
             slots, epochs = recv_reservations(2, 1, None, with_epochs=True)
             time.sleep(0.1)               # the token side polls meanwhile
-            _land(table, slots[1], epochs[1] - 1, 99)   # stale epoch: must not admit
-            _land(table, slots[0], epochs[0], 77)
+            _land(table, slots[1], epochs[1] - 1, 99, key=1)   # stale epoch: must not admit
+            _land(table, slots[0], epochs[0], 77, key=1)
             time.sleep(0.05)
-            _land(table, slots[1], epochs[1], 42)
+            _land(table, slots[1], epochs[1], 42, key=2)
             table.close()
             q.put(("prompt", (slots, epochs), 0, None))
     finally:
@@ -89,22 +92,26 @@ def test_reservation_and_handoff_roundtrip():
     assert seen == [10, 11]
 
 
-def test_handoff_prefix_order_and_epochs():
-    """Landings are admitted as a prefix of the reservation order (the prompt
-    machine batches FCFS), and only for the current epoch of a slot."""
+def test_handoff_groups_and_epochs():
+    """A prompt batch's requests are admitted together once its whole group
+    landed; groups (e.g. from different prompt machines) in landing order;
+    only the current epoch of a slot counts."""
     from paper_2311_18677_b200.control import HandoffTable, HandoffWatch
-    table = HandoffTable(4, create=True)
+    table = HandoffTable(8, create=True)
     try:
         w = HandoffWatch(table)
         w.expect(1, 0, 5, 10, 3)
-        w.expect(2, 1, 1, 20, 4)
-        _land(table, 1, 1, 8)             # the second lands first
+        w.expect(2, 1, 1, 20, 4)          # rids 2, 3: one batch of another machine
+        w.expect(3, 2, 1, 30, 5)
+        _land(table, 1, 1, 8, key=7, n=2)  # half of group 7
+        assert w.poll() == [] and 2 in w.seen
+        _land(table, 0, 4, 9, key=6)      # previous epoch of slot 0
         assert w.poll() == []
-        _land(table, 0, 4, 9)             # previous epoch of slot 0
-        assert w.poll() == []
-        _land(table, 0, 5, 6)
-        assert w.poll() == [(1, 0, 10, 6, 3), (2, 1, 20, 8, 4)]
-        assert w.pending == [] and set(w.seen) == {1, 2}
+        _land(table, 2, 1, 4, key=7, n=2)  # group 7 complete: admitted before rid 1
+        assert w.poll() == [(2, 1, 20, 8, 4), (3, 2, 30, 4, 5)]
+        _land(table, 0, 5, 6, key=6)
+        assert w.poll() == [(1, 0, 10, 6, 3)]
+        assert w.pending == [] and set(w.seen) == {1, 2, 3}
     finally:
         table.close()
 

@@ -10,7 +10,8 @@ the co-located run's; tiny model: teacher-forced logits vs the fp32 oracle
 within the stated bound; prompts below the NVLink threshold (33 tokens) take
 the serialized mode (one push launch for all layers), the rest layer-wise
 (reference select_mode, transfer.py:73-76); the bench's serve_burst path
-generates the co-located tokens for every request."""
+admits the prompt batch's requests as one group and generates the tokens of
+the same batched schedule run co-located."""
 
 import json
 import os
@@ -56,6 +57,7 @@ def test_ipc_pair_push_exact(model, cases, tol, tmp_path):
         assert c["tokens"] == c["colocated_tokens"], c["P"]
         if tol is not None:
             assert c["max_dlogit_vs_oracle"] <= tol, c
+    assert set(res["burst_steps"]) == {3}      # the landed group was admitted together
     for b in res["burst"]:
         assert b["tokens"] == b["colocated"], b["rid"]
         assert b["emitted"] == 11 and b["first_seen"]

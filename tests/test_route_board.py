@@ -1,6 +1,11 @@
-"""Live JSQ routing across Splitwise pairs (control.RouteBoard / ArrivalFeed),
-the real-time trace path's restatement of the reference's Cluster.route
-(cluster.py:82-84 pending_tokens, :129-134 _argmin, :153-160 route)."""
+"""Live JSQ routing for the real-time trace path (control.RouteBoard /
+ArrivalFeed): the reference's Cluster.route (cluster.py:153-160) makes two
+independent picks at arrival — prompt machine by JSQ over the prompt pool,
+token machine by JSQ over the token pool — each the lowest (pending, id)
+(_argmin, cluster.py:129-134) with pending = pending_tokens (cluster.py:82-84):
+queued prompt tokens (prompt machine), live token tasks (token machine).
+The randomized test replays the reference's own Cluster with the same
+machine states."""
 
 import multiprocessing as mp
 import random
@@ -9,98 +14,117 @@ import time
 from paper_2311_18677_b200.control import ArrivalFeed, RouteBoard
 
 
-def test_jsq_pick_is_argmin_pending_then_id():
-    b = RouteBoard(8, 3, create=True)
+def test_independent_jsq_picks():
+    b = RouteBoard(8, 2, 3, create=True)
     try:
-        # empty pool: ties broken by the lowest pair id, then the queued
-        # prompt tokens steer the next picks
-        assert b.route(0, 1000) == 0
-        assert b.route(1, 500) == 1
-        assert b.route(2, 700) == 2
-        assert b.route(3, 10) == 1            # pending 1000 / 500 / 700
-        # pair 0 finishes its prompt: its request becomes one live token task
-        b.publish(0, b.PROMPT_TOK, 1000)
-        b.publish(0, b.PROMPT_REQ, 1)
-        assert b.pending(0) == 1
-        assert b.route(4, 50) == 0
-        # ... and finishes decoding
-        b.publish(0, b.FINISHED, 1)
-        assert b.pending(0) == 50
-        assert list(b.assign[:5]) == [0, 1, 2, 1, 0]
+        assert b.route(0, 1000) == (0, 0)       # empty: lowest ids
+        assert b.route(1, 500) == (1, 0)        # prompt 0 has 1000 queued; token pool idle
+        assert b.route(2, 700) == (1, 0)        # 1000 vs 500
+        b.publish_token(0, b.LANDED, 2)         # two token tasks live on token machine 0
+        assert b.route(3, 10) == (0, 1)         # prompt 1000 vs 1200; token 2 / 0 / 0
+        b.publish_prompt(0, 1000)               # prompt 0 finished its first prompt
+        b.publish_token(0, b.FINISHED, 2)
+        assert b.pending_prompt(0) == 10 and b.pending_token(0) == 0
+        assert b.route(4, 50) == (0, 0)
+        assert list(b.assign_p[:5]) == [0, 1, 1, 0, 0]
+        assert list(b.assign_t[:5]) == [0, 0, 0, 1, 0]
     finally:
         b.close()
 
 
-def test_jsq_matches_reference_argmin_randomised():
+def test_picks_match_reference_cluster_route():
+    """Randomised machine loads; the board's picks equal the reference's own
+    Cluster.route (imported through tools/reftrace.py) for the same queued
+    prompt tokens and live token tasks.  Loads stay under the reference's
+    overflow threshold (queue_threshold_tokens = 4096, machine.py:35): the
+    concurrent path does not run prompts on token machines (no mixed pool),
+    so overflow routing is out of its scope."""
+    import reftrace
+    ss = reftrace.splitsim()
+    if ss is None:
+        import pytest
+        pytest.skip("reference not importable")
+    from splitsim import cluster as C
     rng = random.Random(3)
-    for _ in range(20):
-        pairs = rng.randint(2, 4)
-        b = RouteBoard(64, pairs, create=True)
+    perf = {"H100": ss.get_calibration("llama2-70b", "H100")}
+    for trial in range(30):
+        P, T = rng.randint(1, 4), rng.randint(1, 4)
+        b = RouteBoard(64, P, T, create=True)
+        cl = C.Cluster(C.ClusterConfig("Splitwise-HH", P, T), perf)
         try:
-            routed = [[] for _ in range(pairs)]     # prompt sizes per pair
-            done = [0] * pairs                       # prompts finished
-            fin = [0] * pairs                        # requests finished
-            for rid in range(64):
-                p = rng.randrange(pairs)
-                if done[p] < len(routed[p]) and rng.random() < 0.5:
-                    done[p] += 1
-                    b.publish(p, b.PROMPT_TOK, sum(routed[p][:done[p]]))
-                    b.publish(p, b.PROMPT_REQ, done[p])
-                if fin[p] < done[p] and rng.random() < 0.5:
-                    fin[p] += 1
-                    b.publish(p, b.FINISHED, fin[p])
-                pend = [sum(routed[q][done[q]:]) + (done[q] - fin[q]) for q in range(pairs)]
-                want = min(range(pairs), key=lambda q: (pend[q], q))
-                size = rng.randint(1, 2048)
-                assert b.route(rid, size) == want
-                routed[want].append(size)
+            routed = [0] * P
+            for rid in range(40):
+                # random progress: prompts finish, token tasks land and finish
+                for m in range(P):
+                    done = rng.randint(int(b.p_load[m]), routed[m])
+                    b.publish_prompt(m, done)
+                    cl.machines[m].pending_token_count = routed[m] - done
+                for m in range(T):
+                    land = int(b.t_load[m, 0]) + rng.randint(0, 2)
+                    fin = rng.randint(int(b.t_load[m, 1]), land)
+                    b.publish_token(m, b.LANDED, land)
+                    b.publish_token(m, b.FINISHED, fin)
+                    cl.machines[P + m].pending_token_count = land - fin
+                size = rng.randint(1, 1500)
+                dec = cl.route(rid, 0.0)
+                got = b.route(rid, size)
+                assert got == (dec.prompt_machine, dec.token_machine - P), (trial, rid)
+                routed[got[0]] += size
+                if max(routed[m] - int(b.p_load[m]) for m in range(P)) > 3000:
+                    for m in range(P):          # drain: stay below the overflow threshold
+                        b.publish_prompt(m, routed[m])
         finally:
             b.close()
 
 
 def test_arrival_feed_in_order_and_complete():
-    b = RouteBoard(4, 2, create=True)
+    b = RouteBoard(4, 2, 2, create=True)
     try:
         reqs = [(i, 0.0, None, 1) for i in range(4)]
         f0, f1 = ArrivalFeed(reqs, 0, b), ArrivalFeed(reqs, 1, b)
+        t1 = ArrivalFeed(reqs, 1, b, role="token")
         assert f0.poll() == [] and not f0.complete()
-        b.assign[0] = 1
-        b.assign[2] = 0          # published out of order: the feed waits for rid 1
+        b.assign_p[0], b.assign_t[0] = 1, 1
+        b.assign_p[2], b.assign_t[2] = 0, 1   # published out of order: feeds wait for rid 1
         assert f0.poll() == [] and [r[0] for r in f1.poll()] == [0]
-        b.assign[1] = 0
+        assert [r[0] for r in t1.poll()] == [0]
+        b.assign_p[1], b.assign_t[1] = 0, 0
         assert [r[0] for r in f0.poll()] == [1, 2]
-        b.assign[3] = 1
+        assert [r[0] for r in t1.poll()] == [2]
+        b.assign_p[3], b.assign_t[3] = 1, 1
         assert [r[0] for r in f1.poll()] == [3]
         f0.poll()
         assert f0.complete() and f1.complete() and f0.mine == 2 and f1.mine == 2
-        # static feed (no board): everything at once
+        assert [r[0] for r in t1.poll()] == [3] and t1.complete() and t1.mine == 3
         s = ArrivalFeed(reqs, 0)
         assert not s.complete() and len(s.poll()) == 4 and s.complete()
     finally:
         b.close()
 
 
-def _server(name, pair, n, q):
-    b = RouteBoard(n, 2, name=name)
-    feed = ArrivalFeed([(i, 0.0, None, 1) for i in range(n)], pair, b)
+def _server(name, m, role, n, q):
+    b = RouteBoard(n, 2, 2, name=name)
+    feed = ArrivalFeed([(i, 0.0, None, 1) for i in range(n)], m, b, role=role)
     got = []
     t_end = time.time() + 20
     while not feed.complete() and time.time() < t_end:
         got += [r[0] for r in feed.poll()]
         time.sleep(1e-3)
     got += [r[0] for r in feed.poll()]
-    b.publish(pair, b.FINISHED, len(got))
-    q.put((pair, got))
+    if role == "token":
+        b.publish_token(m, b.LANDED, len(got))
+    q.put(((role, m), got))
     b.close()
 
 
 def test_router_across_processes():
     n = 24
-    b = RouteBoard(n, 2, create=True)
+    b = RouteBoard(n, 2, 2, create=True)
     try:
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
-        ps = [ctx.Process(target=_server, args=(b.name, p, n, q)) for p in range(2)]
+        ps = [ctx.Process(target=_server, args=(b.name, m, role, n, q))
+              for role in ("prompt", "token") for m in range(2)]
         for p in ps:
             p.start()
         t0 = time.perf_counter()
@@ -108,9 +132,12 @@ def test_router_across_processes():
         res = dict(q.get(timeout=60) for _ in ps)
         for p in ps:
             p.join(timeout=30)
-        assert sorted(res[0] + res[1]) == list(range(n))
-        assert [int(b.assign[i]) for i in res[0]] == [0] * len(res[0])
-        assert res[0] == sorted(res[0]) and res[1] == sorted(res[1])
+        for role, arr in (("prompt", b.assign_p), ("token", b.assign_t)):
+            got = res[(role, 0)] + res[(role, 1)]
+            assert sorted(got) == list(range(n))
+            for m in (0, 1):
+                assert all(int(arr[i]) == m for i in res[(role, m)])
+                assert res[(role, m)] == sorted(res[(role, m)])
     finally:
         b.close()
 
@@ -122,7 +149,7 @@ def _tp_peer(rank, port, name, n, q):
     from paper_2311_18677_b200.splitwise import _lockstep
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=2)
-    b = RouteBoard(n, 2, name=name)
+    b = RouteBoard(n, 2, 2, name=name)
     feed = ArrivalFeed([(i, 0.0, None, 1) for i in range(n)], 1, b)
     rng = _r.Random(rank)
     pending, taken, it = [], [], 0
@@ -144,13 +171,13 @@ def _tp_peer(rank, port, name, n, q):
 
 
 def test_tp_peers_take_the_same_arrivals_and_exit_together():
-    """Two TP peers of one pair (gloo, world 2) fed by the live router: the
-    MIN lockstep makes them take the same requests at the same iterations
-    and leave the serve loop at the same iteration although one of them
-    observes the assignments late."""
+    """Two TP peers of one prompt machine (gloo, world 2) fed by the live
+    router: the MIN lockstep makes them take the same requests at the same
+    iterations and leave the serve loop at the same iteration although one
+    of them observes the assignments late."""
     import socket
     n = 30
-    b = RouteBoard(n, 2, create=True)
+    b = RouteBoard(n, 2, 2, create=True)
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
@@ -166,6 +193,6 @@ def test_tp_peers_take_the_same_arrivals_and_exit_together():
         for p in ps:
             p.join(timeout=30)
         assert res[0] == res[1]
-        assert res[0][0] == [i for i in range(n) if int(b.assign[i]) == 1]
+        assert res[0][0] == [i for i in range(n) if int(b.assign_p[i]) == 1]
     finally:
         b.close()

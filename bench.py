@@ -215,11 +215,11 @@ def cpu_port_request(model="llama2-7b", prompt=1024, n_out=128, dec_steps=None, 
             "wall_s": t_pre + sum(tbt), "init_s": t_init}
 
 
-def cpu_baseline_sample(model, prompt, n_out):
-    """bench.py's cpu_baseline leg: a bounded sample (~15-25 s of CPU work)
+def cpu_baseline_sample(model, prompt, n_out, threads=None):
+    """bench.py's cpu_baseline leg: a bounded sample (~10-20 s of CPU work)
     of the same request through the full-depth CPU port."""
     try:
-        return cpu_port_request(model, prompt, n_out, dec_steps=6)
+        return cpu_port_request(model, prompt, n_out, dec_steps=6, threads=threads)
     except MemoryError as e:
         return {"value": None, "unit": "tokens/s", "unavailable": str(e)}
 

@@ -280,6 +280,21 @@ class TokenServer:
             n += 1
         return n
 
+    def prewarm(self, max_batch: int = 24, buckets=(2048, 4096)) -> int:
+        """Capture the decode graphs of the batch sizes / context buckets a
+        trace will use before serving starts (a capture inside the serve
+        loop stalls every running request for its duration).  Run before
+        any sequence is live: the warm-up step of a capture writes block 0."""
+        n = 0
+        for bucket in buckets:
+            for B in range(1, max_batch + 1):
+                g = self.runner.decode_graph(B, bucket, 1)
+                if g.graph is None:
+                    g.capture()
+                    n += 1
+        torch.cuda.synchronize()
+        return n
+
     def _graph_for(self, rids, info, remaining):
         """Decode graph whose context bucket covers every row until it
         finishes: current context + remaining outputs + 1."""
@@ -659,8 +674,6 @@ def run_split_bench(args, ClockSampler, percentile, cpu_baseline, peaks, ncu_tra
         pre_step_ms = statistics.mean(pre_ms) * batches_per_step
         pre_tfs = statistics.mean(pre_flops) / (pre_step_ms / 1e3) / 1e12
         dec = _decode_roofline(cfg, tp, dec_steps, hbm_peak, peak_kind)
-        if dec is not None:
-            dec["traffic"] = ncu_traffic("decode_step") if cfg.name == "llama2-7b" else None
         line = {
             "metric": metric_name(cfg, P, O),
             "value": toks_step / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
@@ -711,9 +724,13 @@ def run_split_bench(args, ClockSampler, percentile, cpu_baseline, peaks, ncu_tra
             "clocks": clocks,
         }
         if not getattr(args, "no_cpu", False):
-            line["cpu_baseline"] = cpu_baseline(args.model, P, O)
+            # the other ranks wait in a gloo (sleeping) barrier, and their
+            # processes keep one core each: an OpenMP region with a thread on
+            # a busy core runs at the speed of its time slice
+            line["cpu_baseline"] = cpu_baseline(args.model, P, O,
+                                                threads=max(1, (os.cpu_count() or 1) - world))
         print(json.dumps(line), flush=True)
-    dist.barrier()
+    dist.barrier(group=ctrl)
     torch.cuda.synchronize()
     server.close()
     # NCCL sub-communicator teardown can stall at interpreter exit (seen with
@@ -760,6 +777,9 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
         mine = [r for r in reqs_all if r.id % pairs == pair]
         items = [(r.id, r.arrival, prompts[r.id], r.output_tokens) for r in mine]
         feed = None
+    if not is_prompt:
+        server.prewarm()
+    dist.barrier(group=ctrl)
     # common start (perf_counter is CLOCK_MONOTONIC: comparable across processes)
     t0t = torch.tensor([time.perf_counter() + 1.0], dtype=torch.float64)
     dist.broadcast(t0t, src=0, group=ctrl)

@@ -5,18 +5,22 @@ prompt writing the paged pool, then CUDA-graph decode steps) and through the
 fp32 CPU oracle (oracle/decoder.py) on the same random-init weights.
 
 Checked per config: teacher-forced logits (the oracle is fed the GPU's
-tokens) within the stated bf16-vs-fp32 tolerance, and the greedy horizon —
+tokens) within the stated bf16-vs-fp32 tolerance, and greedy agreement —
 the GPU's token equals the oracle's argmax at every checked step whose
-oracle top-2 margin exceeds twice the tolerance (near-ties are reported, not
-asserted).  Beside the fp32 oracle runs its bf16-storage twin
+oracle top-2 margin exceeds twice that step's observed logit error (such a
+step cannot flip by rounding; closer margins are counted as near-ties and
+reported, not asserted).  ``greedy_horizon`` is the number of leading steps
+on which the tokens agree.  Beside the fp32 oracle runs its bf16-storage twin
 (OracleDecoder(emulate_bf16=True): the same fp32 math with every activation
 the device stores in bf16 rounded there); its distance to the fp32 oracle is
 the error bf16 storage alone explains, reported as ``emul_dlogit``.
 Observed errors are written to gpurun_out/parity_widths.json.
 
-Tolerance: max |logit_gpu - logit_oracle| over all checked steps <=
+Tolerances: max |logit_gpu - logit_oracle| over all checked steps <=
 TOL_REL[model] * max |logit|, TOL_REL = 3x the relative error observed on
-B200 (profiles/r2_parity_widths.json), rounded up.
+B200 (profiles/r2_parity_widths.json: 0.48 % / 2.2 % / 0.69 %), rounded up;
+and <= EMUL_FACTOR x the bf16-storage twin's error (observed ratio 1.04-1.11:
+the kernels add almost nothing on top of storing activations in bf16).
 """
 
 import dataclasses
@@ -35,6 +39,7 @@ sys.path.insert(0, ROOT)
 P, N_OUT = 1024, 16
 # model -> max |dlogit| / max |logit| allowed (3x observed, see module docstring)
 TOL_REL = {"llama2-7b": 0.015, "llama2-70b": 0.07, "bloom-176b": 0.021}
+EMUL_FACTOR = 1.5
 
 
 def _record(name, rec):
@@ -96,7 +101,7 @@ def compare(gpu_toks, gpu_logits, ref_toks, ref_logits, tol_rel, emul_logits=Non
     top2 = ref_logits.topk(2, -1).values
     margin = top2[:, 0] - top2[:, 1]
     agree = [a == b for a, b in zip(gpu_toks, ref_toks)]
-    decisive = (margin > 2 * tol).tolist()
+    decisive = (margin > 2 * diff).tolist()
     horizon = 0
     for a in agree:
         if not a:
@@ -121,4 +126,5 @@ def test_full_width_slice_matches_oracle(model):
     _record(model, rec)
     print(json.dumps(rec))
     assert rec["max_dlogit"] <= rec["tol"], rec
+    assert rec["max_dlogit"] <= EMUL_FACTOR * rec["emul_dlogit"], rec
     assert rec["disagree_decisive"] == 0, rec

@@ -626,6 +626,287 @@ __global__ void __launch_bounds__(NW * 32)
 }
 
 
+// ---------------------------------------------------------------- decode, cluster
+// Streaming decode attention for MHA / small groups (G <= 2, block_size 16,
+// decode-graph form).  One thread-block CLUSTER of DCL_CL CTAs per (sequence,
+// kv head); CTA r of the cluster streams pages [r*pp, (r+1)*pp) of the context
+// through a DCL_S-stage shared-memory ring: a producer warp issues the 4 KB K
+// and V bulk copies of each (block, head) page (the first DCL_S pages before
+// griddepcontrol.wait, overlapping the QKV projection's tail), and DCL_CW
+// consumer warps each own every DCL_CW-th page with an online softmax of
+// their own — no block-wide barrier until the end, so a warp computes as
+// soon as ITS page landed.  Warps combine through shared memory and the
+// cluster's CTAs through distributed shared memory (rank 0 reads its peers'
+// (m, l, o) with ld.shared::cluster, fixed order): no global partials, no
+// atomic ticket, no system fences.  The current token (position ctx) is
+// RoPE'd and appended to the pool by the warp owning its page, which patches
+// the staged page row from registers.
+constexpr int DCL_CL = 8;             // CTAs per (b, kv head)
+constexpr int DCL_S = 8;              // ring stages (one page of K and V each)
+constexpr int DCL_CW = 4;             // consumer warps
+constexpr int DCL_THREADS = (DCL_CW + 1) * 32;
+constexpr int DCL_PAGE = 16 * DA_D;   // elements of one (block, head) page
+constexpr int DCL_ST = DA_D + 4;      // floats per (o[128], m, l) record (16-byte aligned)
+
+__host__ __device__ constexpr size_t dcl_smem(int G) {
+  return (size_t)DCL_S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(DCL_CW + 1) * G * DCL_ST;
+}
+
+template <int G>
+__global__ void __launch_bounds__(DCL_THREADS)
+    attn_decode_cl_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
+                          __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
+                          const int32_t* __restrict__ tables, int max_blocks,
+                          const int32_t* __restrict__ ctx_lens, float log2_theta,
+                          const float* __restrict__ alibi, int H, int Hkv, float scale_log2,
+                          __nv_bfloat16* __restrict__ out, int trig) {
+  extern __shared__ __align__(128) uint8_t dsm_raw[];
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(dsm_raw);         // [S][K|V][PAGE]
+  float* wst = reinterpret_cast<float*>(ring + (size_t)DCL_S * 2 * DCL_PAGE);  // [CW][G][ST]
+  float* res = wst + DCL_CW * G * DCL_ST;                                       // [G][ST]
+  __shared__ uint64_t full[DCL_S], empty[DCL_S];
+  const int r = blockIdx.x;             // cluster rank (cluster (DCL_CL,1,1), gridDim.x == DCL_CL)
+  const int kh = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < DCL_S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int32_t* trow = tables + (size_t)b * max_blocks;
+  const int cur = __ldg(ctx_lens + b);      // written >= 2 launches back (decode_advance)
+  const int L = cur + 1;                     // attention length incl. the current token
+  const int npg = (L + 15) >> 4;
+  const int pp = (npg + DCL_CL - 1) / DCL_CL;
+  const int pg0 = r * pp;
+  const int nmy = max(0, min(npg, pg0 + pp) - pg0);
+  constexpr uint32_t kTile = DCL_PAGE * 2;   // bytes of one page of K (or V)
+
+  if (warp == DCL_CW) {
+    // ------------------------------------------------ producer (one lane)
+    if (lane == 0) {
+      auto issue = [&](int i) {
+        const int st = i % DCL_S;
+        const int blk = __ldg(trow + pg0 + i);
+        const size_t src = ((size_t)blk * Hkv + kh) * DCL_PAGE;
+        mbar_arrive_expect_tx(&full[st], 2 * kTile);
+        bulk_g2s(ring + (size_t)(2 * st) * DCL_PAGE, kpool + src, kTile, &full[st]);
+        bulk_g2s(ring + (size_t)(2 * st + 1) * DCL_PAGE, vpool + src, kTile, &full[st]);
+      };
+      const int pre = min(nmy, DCL_S);
+      for (int i = 0; i < pre; ++i) issue(i);     // cached pages: before the PDL wait
+      pdl_wait();
+      for (int i = DCL_S; i < nmy; ++i) {
+        mbar_wait_sleep(&empty[i % DCL_S], ((i / DCL_S) - 1) & 1);
+        issue(i);
+      }
+      if (trig) pdl_launch_dependents();
+    }
+  } else {
+    // ------------------------------------------------ consumers
+    pdl_wait();                                   // q / current k,v from the QKV projection
+    const int half = lane >> 4, hl = lane & 15;
+    const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
+    const float fpos = (float)cur;
+    // lane hl holds dims [4hl, 4hl+4) and [64+4hl, 64+4hl+4): its RoPE pairs
+    float q[G][8];
+    float sl[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const __nv_bfloat16* hp = qrow + (size_t)(kh * G + g) * DA_D;
+      const uint2 ql = *reinterpret_cast<const uint2*>(hp + 4 * hl);
+      const uint2 qh = *reinterpret_cast<const uint2*>(hp + 64 + 4 * hl);
+      const float2 l0 = bf2_to_f2(ql.x), l1 = bf2_to_f2(ql.y);
+      const float2 h0 = bf2_to_f2(qh.x), h1 = bf2_to_f2(qh.y);
+      float lo[4] = {l0.x, l0.y, l1.x, l1.y}, hi[4] = {h0.x, h0.y, h1.x, h1.y};
+      if (!alibi) {
+        rope4(lo, hi, 4 * hl, fpos, log2_theta);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {            // rotated q is stored in bf16 (two-kernel path)
+          lo[j] = __bfloat162float(__float2bfloat16(lo[j]));
+          hi[j] = __bfloat162float(__float2bfloat16(hi[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        q[g][j] = lo[j] * scale_log2;
+        q[g][4 + j] = hi[j] * scale_log2;
+      }
+      sl[g] = alibi ? alibi[kh * G + g] * 1.4426950408889634f : 0.f;
+    }
+    // the current token: its page's owner warp RoPEs k, appends k/v to the
+    // pool (half 0: k, half 1: v) and keeps the rows to patch the staged page
+    const int cpg = cur >> 4;
+    const bool own = cpg >= pg0 && cpg < pg0 + nmy && ((cpg - pg0) % DCL_CW) == warp;
+    uint2 cur_lo = make_uint2(0, 0), cur_hi = make_uint2(0, 0);
+    if (own) {
+      const __nv_bfloat16* src = qrow + (size_t)(half == 0 ? H + kh : H + Hkv + kh) * DA_D;
+      const uint2 a = *reinterpret_cast<const uint2*>(src + 4 * hl);
+      const uint2 c = *reinterpret_cast<const uint2*>(src + 64 + 4 * hl);
+      if (half == 0 && !alibi) {
+        const float2 a0 = bf2_to_f2(a.x), a1 = bf2_to_f2(a.y);
+        const float2 c0 = bf2_to_f2(c.x), c1 = bf2_to_f2(c.y);
+        float lo[4] = {a0.x, a0.y, a1.x, a1.y}, hi[4] = {c0.x, c0.y, c1.x, c1.y};
+        rope4(lo, hi, 4 * hl, fpos, log2_theta);
+        cur_lo = make_uint2(f2_to_bf2(lo[0], lo[1]), f2_to_bf2(lo[2], lo[3]));
+        cur_hi = make_uint2(f2_to_bf2(hi[0], hi[1]), f2_to_bf2(hi[2], hi[3]));
+      } else {
+        cur_lo = a;
+        cur_hi = c;
+      }
+      const int slot = __ldg(trow + cpg) * 16 + (cur & 15);
+      const size_t gdst = (((size_t)(slot >> 4) * Hkv + kh) * 16 + (slot & 15)) * DA_D;
+      __nv_bfloat16* pool = half == 0 ? kpool : vpool;
+      *reinterpret_cast<uint2*>(pool + gdst + 4 * hl) = cur_lo;
+      *reinterpret_cast<uint2*>(pool + gdst + 64 + 4 * hl) = cur_hi;
+    }
+    float m[G], l[G], o[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      m[g] = -INFINITY;
+      l[g] = 0.f;
+      o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
+    }
+    for (int i = warp; i < nmy; i += DCL_CW) {
+      const int st = i % DCL_S;
+      mbar_wait(&full[st], (i / DCL_S) & 1);
+      __nv_bfloat16* ks = ring + (size_t)(2 * st) * DCL_PAGE;
+      __nv_bfloat16* vs = ks + DCL_PAGE;
+      const int t0 = (pg0 + i) * 16;
+      if (own && pg0 + i == cpg) {               // patch the current token's rows
+        __nv_bfloat16* row = (half == 0 ? ks : vs) + (cur - t0) * DA_D;
+        *reinterpret_cast<uint2*>(row + 4 * hl) = cur_lo;
+        *reinterpret_cast<uint2*>(row + 64 + 4 * hl) = cur_hi;
+        __syncwarp();
+      }
+      const int valid = min(16, L - t0);
+      float sc[G][8];
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {          // token 2*it + half
+        const int t = 2 * it + half;
+        const __nv_bfloat16* kr = ks + t * DA_D;
+        const uint2 a = *reinterpret_cast<const uint2*>(kr + 4 * hl);
+        const uint2 c = *reinterpret_cast<const uint2*>(kr + 64 + 4 * hl);
+        const float2 a0 = bf2_to_f2(a.x), a1 = bf2_to_f2(a.y);
+        const float2 c0 = bf2_to_f2(c.x), c1 = bf2_to_f2(c.y);
+        const float kf[8] = {a0.x, a0.y, a1.x, a1.y, c0.x, c0.y, c1.x, c1.y};
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          float d = q[g][0] * kf[0];
+#pragma unroll
+          for (int j = 1; j < 8; ++j) d = fmaf(q[g][j], kf[j], d);
+          sc[g][it] = d;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int sh = 8; sh > 0; sh >>= 1)
+#pragma unroll
+          for (int it = 0; it < 8; ++it) sc[g][it] += __shfl_xor_sync(0xffffffffu, sc[g][it], sh);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int t = 2 * it + half;
+          sc[g][it] = t < valid ? fmaf(sl[g], (float)(t0 + t - cur), sc[g][it]) : -INFINITY;
+          mx = fmaxf(mx, sc[g][it]);
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        const float mn = fmaxf(m[g], mx);
+        const float corr = m[g] == -INFINITY ? 0.f : exp2f(m[g] - mn);
+        float ps = 0.f;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          sc[g][it] = exp2f(sc[g][it] - mn);
+          ps += sc[g][it];
+        }
+        ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+        l[g] = l[g] * corr + ps;
+        m[g] = mn;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[g][j] *= corr;
+      }
+      // P.V: lane owns dims [4*lane, 4*lane+4); token t's p lives in lane (t&1)*16
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const uint2 vv = *reinterpret_cast<const uint2*>(vs + t * DA_D + 4 * lane);
+        const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float pt = __shfl_sync(0xffffffffu, sc[g][t >> 1], (t & 1) * 16);
+          o[g][0] = fmaf(pt, v0.x, o[g][0]);
+          o[g][1] = fmaf(pt, v0.y, o[g][1]);
+          o[g][2] = fmaf(pt, v1.x, o[g][2]);
+          o[g][3] = fmaf(pt, v1.y, o[g][3]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float* w = wst + ((size_t)warp * G + g) * DCL_ST;
+      *reinterpret_cast<float4*>(w + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+      if (lane == 0) {
+        w[DA_D] = m[g];
+        w[DA_D + 1] = l[g];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- combine the consumer warps (fixed order) into this CTA's record
+  for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
+    const int g = idx / DA_D, d = idx % DA_D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < DCL_CW; ++w) M = fmaxf(M, wst[(w * G + g) * DCL_ST + DA_D]);
+    float O = 0.f, Ls = 0.f;
+#pragma unroll
+    for (int w = 0; w < DCL_CW; ++w) {
+      const float* ww = wst + (w * G + g) * DCL_ST;
+      const float f = ww[DA_D] == -INFINITY ? 0.f : exp2f(ww[DA_D] - M);
+      O = fmaf(f, ww[d], O);
+      Ls = fmaf(f, ww[DA_D + 1], Ls);
+    }
+    res[g * DCL_ST + d] = O;
+    if (d == 0) {
+      res[g * DCL_ST + DA_D] = M;
+      res[g * DCL_ST + DA_D + 1] = Ls;
+    }
+  }
+  cluster_sync_all();                  // every CTA's record is in its shared memory
+  if (r == 0) {
+    const uint32_t res_local = smem_u32(res);
+    for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
+      const int g = idx / DA_D, d = idx % DA_D;
+      float mp[DCL_CL], lp[DCL_CL], op[DCL_CL];
+#pragma unroll
+      for (int p = 0; p < DCL_CL; ++p) {
+        const uint32_t base = mapa(res_local, p) + (uint32_t)(g * DCL_ST) * 4u;
+        mp[p] = ld_dsmem(base + DA_D * 4);
+        lp[p] = ld_dsmem(base + (DA_D + 1) * 4);
+        op[p] = ld_dsmem(base + d * 4);
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int p = 0; p < DCL_CL; ++p) M = fmaxf(M, mp[p]);
+      float O = 0.f, Ls = 0.f;
+#pragma unroll
+      for (int p = 0; p < DCL_CL; ++p) {
+        const float f = mp[p] == -INFINITY ? 0.f : exp2f(mp[p] - M);
+        O = fmaf(f, op[p], O);
+        Ls = fmaf(f, lp[p], Ls);
+      }
+      out[((size_t)b * H + kh * G + g) * DA_D + d] = __float2bfloat16(O / Ls);
+    }
+  }
+  cluster_sync_all();                  // peers keep their shared memory until rank 0 read it
+}
+
 // ---------------------------------------------------------------- decode, MMA
 // Tensor-core decode attention (block_size 16, partition 128): the G query
 // heads of a kv group form the rows of a 16-row mma.sync A tile (rows >= G
@@ -1274,6 +1555,59 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     const char* e = std::getenv("SWB_ATTN_MMA");
     return !(e && e[0] == '0');
   }();
+  // cluster-streaming kernel for MHA / small groups in the decode graph
+  // (SWB_ATTN_CL=0 keeps the split-K kernel below; SWB_ATTN_CL_MAXB bounds
+  // the batch it takes)
+  static const int cl_maxb = [] {
+    const char* e = std::getenv("SWB_ATTN_CL");
+    if (e && e[0] == '0') return 0;
+    const char* m = std::getenv("SWB_ATTN_CL_MAXB");
+    return m ? std::atoi(m) : 1 << 30;
+  }();
+  if (STEP && G <= 2 && block_size == 16 && B <= cl_maxb) {
+    static bool attr_c[64] = {false};
+    if (dev < 64 && !attr_c[dev]) {
+      SWB_CUDA(cudaFuncSetAttribute(attn_decode_cl_kernel<1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dcl_smem(1)));
+      SWB_CUDA(cudaFuncSetAttribute(attn_decode_cl_kernel<2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dcl_smem(2)));
+      attr_c[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(DCL_CL, Hkv, B);
+    cfg.blockDim = dim3(DCL_THREADS);
+    cfg.dynamicSmemBytes = dcl_smem(G);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = DCL_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    const float l2t = !alibi_slopes ? log2f(theta) : 0.f;
+    const float sc = scale * 1.4426950408889634f;
+    const int trig = pdl_early_trigger() ? 1 : 0;
+    auto q = reinterpret_cast<const __nv_bfloat16*>(qkv);
+    auto kp = reinterpret_cast<__nv_bfloat16*>(k_layer);
+    auto vp = reinterpret_cast<__nv_bfloat16*>(v_layer);
+    auto op = reinterpret_cast<__nv_bfloat16*>(out);
+    const cudaError_t lc =
+        G == 1 ? cudaLaunchKernelEx(&cfg, attn_decode_cl_kernel<1>, q, row_stride, kp, vp,
+                                    block_tables, max_blocks, ctx_lens, l2t, alibi_slopes, H, Hkv,
+                                    sc, op, trig)
+               : cudaLaunchKernelEx(&cfg, attn_decode_cl_kernel<2>, q, row_stride, kp, vp,
+                                    block_tables, max_blocks, ctx_lens, l2t, alibi_slopes, H, Hkv,
+                                    sc, op, trig);
+    if (lc != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_cl_kernel: %s",
+                           cudaGetErrorString(lc));
+    return swb_check_launch("attn_decode_cl_kernel");
+  }
   // tensor-core kernel for GQA groups (measured: 70B-TP2 B=8 17.0 vs 19.5 us,
   // B=32 54 vs 63 us); for MHA (G=1) the CUDA-core kernel is ahead (7B B=1
   // 10.0 vs 13.9 us: the unswizzled 256-byte page rows cost the MMA kernel

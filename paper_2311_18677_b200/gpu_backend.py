@@ -86,6 +86,7 @@ class GpuBackend:
         self.state: dict[int, _Seq] = {}
         self.visible: dict[int, tuple[float, float]] = {}
         self.iter_log: list[tuple] = []     # (machine, kind, batch tokens/rows, ms)
+        self.tokens: dict[int, list] = {}   # rid -> generated token ids (first, then decode)
         self.driver = None
 
     # ------------------------------------------------------------ set-up
@@ -140,6 +141,9 @@ class GpuBackend:
             print("ok:", what, flush=True)
 
     def iteration_ms(self, machine, batch) -> float:
+        if getattr(batch, "prompt_chunk", None) is not None:
+            ms = self._mixed_chunk(machine.id, batch)
+            return ms if self.clock == "measured" else batch.iteration_time
         ms = 0.0
         if (batch.prompt_tasks and batch.token_tasks and self.mixed and
                 all(self.driver.records[t.request_id].token_machine == machine.id
@@ -217,6 +221,7 @@ class GpuBackend:
                 ms = e0.elapsed_time(e1)
         for r, s, f in zip(recs, seqs, first_h.tolist()):
             self.state[r.request_id] = _Seq(r.token_machine, s, int(f), r.prompt_tokens)
+            self.tokens[r.request_id] = [int(f)]
         self.iter_log.append((mid, "prompt", sum(lens), ms))
         return ms
 
@@ -236,8 +241,9 @@ class GpuBackend:
             e1.record()
             nxt = g.next_tok.cpu().tolist()         # synchronises
             ms = e0.elapsed_time(e1)
-        for s, t in zip(sts, nxt):
+        for tk, s, t in zip(tasks, sts, nxt):
             s.cur = int(t)
+            self.tokens[tk.request_id].append(int(t))
             s.ctx += 1
         self.iter_log.append((mid, "token", B, ms))
         return ms
@@ -272,10 +278,57 @@ class GpuBackend:
         R = len(recs)
         for r, s, f in zip(recs, seqs, nxt_h[:R]):
             self.state[r.request_id] = _Seq(mid, s, int(f), r.prompt_tokens)
-        for s, t in zip(sts, nxt_h[R:]):
+            self.tokens[r.request_id] = [int(f)]
+        for tk, s, t in zip(ttasks, sts, nxt_h[R:]):
             s.cur = int(t)
+            self.tokens[tk.request_id].append(int(t))
             s.ctx += 1
         self.iter_log.append((mid, "mixed", sum(lens) + len(sts), ms))
+        return ms
+
+    def _mixed_chunk(self, mid: int, batch) -> float:
+        """Chunked-prefill iteration of an always-mixed machine: a chunk of
+        the head prompt plus one decode token of every scheduled sequence."""
+        runner, dev = self.runners[mid], self.dev[mid]
+        kv = runner.kv
+        task = batch.prompt_tasks[0]
+        start, n = batch.prompt_chunk
+        rec = self.driver.records[task.request_id]
+        sts = [self.state[t.request_id] for t in batch.token_tasks]
+        with torch.cuda.device(dev):
+            if start == 0:          # first chunk: reserve the final context
+                seq = kv.allocate(rec.prompt_tokens + rec.output_tokens)
+                self._chunking = getattr(self, "_chunking", {})
+                self._chunking[rec.request_id] = seq
+            seq = self._chunking[rec.request_id]
+            ids = self._prompt_ids(rec.request_id, rec.prompt_tokens)[start:start + n]
+            toks = ids.pin_memory().to(f"cuda:{dev}", non_blocking=True)
+            args = {}
+            if sts:
+                idx = torch.tensor([s.seq for s in sts], dtype=torch.long, device=f"cuda:{dev}")
+                args = dict(
+                    dec_tables=torch.index_select(kv.tables(), 0, idx),
+                    dec_tok=torch.tensor([s.cur for s in sts], dtype=torch.int32,
+                                         device=f"cuda:{dev}"),
+                    dec_ctx=torch.tensor([s.ctx for s in sts], dtype=torch.int32,
+                                         device=f"cuda:{dev}"),
+                    dec_max_ctx=CTX_BUCKET * ((max(s.ctx for s in sts) + 2 + CTX_BUCKET - 1)
+                                              // CTX_BUCKET))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            nxt = runner.mixed_chunk(toks, seq, start, **args)
+            e1.record()
+            nxt_h = nxt.cpu().tolist()
+            ms = e0.elapsed_time(e1)
+        if start + n == rec.prompt_tokens:       # last chunk: the first token
+            self._chunking.pop(rec.request_id)
+            self.state[rec.request_id] = _Seq(mid, seq, int(nxt_h[0]), rec.prompt_tokens)
+            self.tokens[rec.request_id] = [int(nxt_h[0])]
+        for tk, s, t in zip(batch.token_tasks, sts, nxt_h[1:]):
+            s.cur = int(t)
+            self.tokens[tk.request_id].append(int(t))
+            s.ctx += 1
+        self.iter_log.append((mid, "chunk", n + len(sts), ms))
         return ms
 
     # ------------------------------------------------------------ hand-off

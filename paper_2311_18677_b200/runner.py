@@ -458,6 +458,73 @@ class ModelRunner:
         dec_ctx += 1
         return nxt
 
+    def mixed_chunk(self, tokens: torch.Tensor, seq: int, start: int,
+                    dec_tables: torch.Tensor | None = None, dec_tok: torch.Tensor | None = None,
+                    dec_ctx: torch.Tensor | None = None, dec_max_ctx: int = 0) -> torch.Tensor:
+        """One chunked-prefill iteration (workers.Machine with
+        prefill_chunk_tokens): rows [0, n) are prompt positions start..start+n
+        of sequence ``seq`` of this machine's pool (RoPE'd, K/V written to
+        their pages, causal attention over every page up to their own
+        position — swb_attn_chunk), rows [n, n+Bd) one decode token of each
+        running sequence (paged decode attention + KV append, as in
+        ``mixed``); every weight GEMM runs once over all rows.  Returns int32
+        [1 + Bd]: the greedy token after the chunk's last row (the prompt's
+        first token when the chunk is its last) and the decode rows' next
+        tokens; dec_ctx advances by one."""
+        cfg, w, kv = self.cfg, self.w, self.kv
+        n = int(tokens.shape[0])
+        Bd = 0 if dec_tok is None else int(dec_tok.shape[0])
+        rows = n + Bd
+        self._ensure_prefill(rows, 1 + Bd)
+        x, h, attn, act = self.px[:rows], self.ph[:rows], self.pattn[:rows], self.pact[:rows]
+        positions = torch.arange(start, start + n, dtype=torch.int32, device=self.dev)
+        slots = torch.empty(n, dtype=torch.int32, device=self.dev)
+        K.slots_from_table(kv.table_row_ptr(seq), start, n, kv.block_size, slots)
+        max_ctx = kv.max_blocks_per_seq * kv.block_size
+        ws = self.graphs.get(("chunk_ws", n, max_ctx))
+        if ws is None:
+            ws = torch.zeros(K.attn_chunk_workspace_bytes(n, self.hq, max_ctx),
+                             dtype=torch.uint8, device=self.dev)
+            self.graphs[("chunk_ws", n, max_ctx)] = ws
+        if Bd:
+            dws = self.graphs.get(("mixed_ws", Bd, dec_max_ctx))
+            if dws is None:
+                dws = torch.zeros(K.attn_decode_workspace_bytes(Bd, self.hq, dec_max_ctx,
+                                                                self.partition, self.dh),
+                                  dtype=torch.uint8, device=self.dev)
+                self.graphs[("mixed_ws", Bd, dec_max_ctx)] = dws
+        self._wait_push_tails()
+        self._begin_reductions()
+        self._embed(tokens if not Bd else torch.cat([tokens, dec_tok]), x)
+        for li, lw in enumerate(w.layers):
+            qkv = self.pqkv[0][:rows]
+            self._norm(x, lw.attn_norm, lw.attn_norm_b, out=h)
+            K.linear(h, lw.wqkv, K.EPI_BF16, out=qkv, bias=lw.bqkv)
+            K.rope_kv_write(qkv[:n], positions, self.hq, self.hkv, self.dh, self.theta,
+                            kv.k_layer_ptr(li), kv.v_layer_ptr(li), slots, kv.block_size)
+            K.attn_chunk(qkv[:n], n, start, kv.k_layer_ptr(li), kv.v_layer_ptr(li),
+                         kv.table_row_ptr(seq), self.hq, self.hkv, self.dh, kv.block_size,
+                         self.scale, max_ctx, ws, attn[:n], alibi=self.alibi)
+            if Bd:
+                K.attn_decode_step(qkv[n:], kv.k_layer_ptr(li), kv.v_layer_ptr(li), dec_tables,
+                                   dec_ctx, Bd, self.hq, self.hkv, self.dh, kv.block_size,
+                                   self.scale, dec_max_ctx, self.partition, dws, out=attn[n:],
+                                   theta=cfg.rope_theta, alibi=self.alibi)
+            self._proj_reduce(attn, lw.wo, x, lw.bo)
+            self._norm(x, lw.mlp_norm, lw.mlp_norm_b, out=h)
+            self._mlp_up(h, lw, act)
+            self._proj_reduce(act, lw.wd, x, lw.bd)
+        idx = torch.arange(n - 1, rows, dtype=torch.int32, device=self.dev)
+        last = self.plast[:1 + Bd]
+        self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=idx)
+        logits = self.plogits[:1 + Bd]
+        K.linear(last, self.head, K.EPI_F32, out=logits)
+        nxt = self.pfirst[:1 + Bd]
+        self._greedy(logits, nxt)
+        if Bd:
+            dec_ctx += 1
+        return nxt
+
     def prefill_chunked(self, tokens: torch.Tensor, seq: int, chunk: int = 512) -> torch.Tensor:
         """Prompt phase of ONE prompt in chunks of ``chunk`` tokens against this
         GPU's pool (sequence slot ``seq``): every chunk's QKV GEMM rotates and

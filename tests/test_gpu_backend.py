@@ -112,3 +112,37 @@ def test_mixed_iteration_matches_separate_phases():
         out[mode + "_kv"] = kv.k_view(1)[tb[p // 16], :, p % 16].float().clone()
     assert out["mixed"] == out["separate"]
     assert (out["mixed_kv"] - out["separate_kv"]).abs().max().item() < 0.05
+
+
+def test_parked_token_tasks_decode_the_oracle_tokens():
+    """A mixed (Baseline) machine with max_token_batch = 2: prompts arriving
+    while two token tasks decode take a slot, so a resident token task is
+    PARKED for that iteration (reference machine.py:207-231; PAPER.md:625-628
+    preemption with aging).  Parking must not disturb its KV or context:
+    every request's tokens equal the fp32 oracle's greedy tokens wherever the
+    oracle's top-2 margin is decisive (> 0.02, ~6x the tiny model's observed
+    bf16 logit error)."""
+    import dataclasses
+    from oracle.decoder import OracleDecoder
+    from paper_2311_18677_b200.gpu_backend import GpuBackend
+    reqs = [Request(0, 0.0, 200, 16), Request(1, 0.00005, 150, 16), Request(2, 0.0003, 300, 8),
+            Request(3, 0.0005, 100, 8), Request(4, 0.0007, 120, 6)]
+    be = GpuBackend("tiny", max_seqs=16, clock="modeled")
+    drv = Driver(ClusterConfig("Baseline-B200", 1, 0, llm="tiny"), be.perf_models(), reqs,
+                 backend=be, record_log=False)
+    for m in drv.cluster.machines.values():
+        m.perf = dataclasses.replace(m.perf, max_token_batch=2)
+    res = drv.run()
+    assert max(r.preempt_count for r in res.report.records) >= 1      # parking happened
+    assert {k for _, k, _, _ in be.iter_log} >= {"mixed", "token"}
+    orc = OracleDecoder.from_weights(be.runners[0].w)
+    for r in reqs:
+        got = be.tokens[r.id]
+        assert len(got) == r.output_tokens
+        prompt = be._prompt_ids(r.id, r.prompt_tokens).tolist()
+        ref_toks, ref_logits = orc.generate(prompt, r.output_tokens, forced=got[:-1])
+        top2 = ref_logits.topk(2, -1).values
+        decisive = (top2[:, 0] - top2[:, 1]) > 0.02
+        for i in range(r.output_tokens):
+            if decisive[i]:
+                assert got[i] == ref_toks[i], (r.id, i)

@@ -338,8 +338,10 @@ def test_attn_decode_fused_rope_append(K, H, Hkv):
                                               (16, 16, 128, True)])
 def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
     """Decode-graph attention (swb_attn_decode_step: position = ctx, slot from
-    the block table, pages gathered before the PDL wait) is bit-identical to
-    the explicit-position form, output and appended pool rows."""
+    the block table, pages gathered before the PDL wait) equals the
+    explicit-position split-K form: appended pool rows bit-identical; output
+    within bf16 rounding (MHA runs the cluster-streaming kernel, whose online
+    softmax sums in a different order)."""
     dh, bs, B = 128, 16, 4
     cached = [0, 15, 128, 1000]          # tokens already in the pool
     nblk, maxb = 400, 80
@@ -363,9 +365,64 @@ def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
                         1 / math.sqrt(dh), max_ctx, part, mk(), positions=ctx, slots=slots,
                         theta=10000.0, alibi=slopes)
     torch.cuda.synchronize()
-    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+    if H == Hkv:
+        assert _rel(out, ref) < 4e-3
+    else:
+        assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
     assert torch.equal(kp.view(torch.int16), kp2.view(torch.int16))
     assert torch.equal(vp.view(torch.int16), vp2.view(torch.int16))
+
+
+@pytest.mark.parametrize("H,Hkv,alibi,cached", [
+    (32, 32, False, [0, 15, 16, 130, 1000, 2047]), (8, 4, False, [3, 700]),
+    (16, 16, True, [31, 1500]), (32, 32, False, [8190])])
+def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached):
+    """The cluster-streaming decode kernel (MHA / G = 2, decode graph form)
+    against a plain torch fp32 attention over the gathered pages: the current
+    token (position = ctx) is RoPE'd (or ALiBi-biased), appended to its
+    block-table slot, and attends over positions 0..ctx; contexts from 1 token
+    to 8191 (every CTA of the 8-CTA cluster empty, partial or full)."""
+    from oracle.decoder import apply_rope, rope_tables
+    dh, bs, B = 128, 16, len(cached)
+    maxb = (max(cached) + 1 + bs - 1) // bs + 1
+    nblk = B * maxb + 8
+    kp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    vp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
+    tables = torch.randperm(nblk, device="cuda").int()[:B * maxb].view(B, maxb).contiguous()
+    ctx = torch.tensor(cached, device="cuda", dtype=torch.int32)
+    qkv = torch.randn(B, (H + 2 * Hkv) * dh, device="cuda").bfloat16()
+    slopes = (torch.rand(H, device="cuda") * 0.1) if alibi else None
+    max_ctx = 16 * maxb
+    ws = torch.zeros(K.attn_decode_workspace_bytes(B, H, max_ctx, 128, dh), dtype=torch.uint8,
+                     device="cuda")
+    out = torch.empty(B, H * dh, dtype=torch.bfloat16, device="cuda")
+    kp0, vp0 = kp.clone(), vp.clone()
+    K.attn_decode_step(qkv, kp.data_ptr(), vp.data_ptr(), tables, ctx, B, H, Hkv, dh, bs,
+                       1 / math.sqrt(dh), max_ctx, 128, ws, out, theta=10000.0, alibi=slopes)
+    torch.cuda.synchronize()
+    G = H // Hkv
+    for b, c in enumerate(cached):
+        q = qkv[b, :H * dh].float().view(1, H, dh)
+        k = qkv[b, H * dh:(H + Hkv) * dh].float().view(1, Hkv, dh)
+        v = qkv[b, (H + Hkv) * dh:].float().view(1, Hkv, dh)
+        if not alibi:
+            cos, sin = rope_tables(torch.tensor([c]), dh, 10000.0)
+            q = apply_rope(q.cpu(), cos, sin).bfloat16().float().cuda()
+            k = apply_rope(k.cpu(), cos, sin).cuda()
+        k = k.bfloat16()
+        blk = tables[b, c // bs].long()
+        assert _rel(kp[blk, :, c % bs], k[0]) < 1e-2              # RoPE'd k appended
+        assert torch.equal(vp[blk, :, c % bs].view(torch.int16), v[0].bfloat16().view(torch.int16))
+        pos = torch.arange(c + 1, device="cuda")
+        Ks = kp0[tables[b, pos // bs].long(), :, pos % bs].float()
+        Vs = vp0[tables[b, pos // bs].long(), :, pos % bs].float()
+        Ks[c], Vs[c] = k[0].float(), v[0].bfloat16().float()
+        Ks, Vs = Ks.repeat_interleave(G, 1), Vs.repeat_interleave(G, 1)
+        s_ = torch.einsum("hd,thd->ht", q[0], Ks) / math.sqrt(dh)
+        if alibi:
+            s_ = s_ + slopes[:, None] * (pos - c)[None, :].float()
+        ref = torch.einsum("ht,thd->hd", s_.softmax(-1), Vs).reshape(-1)
+        assert _rel(out[b], ref) < 1e-2, (b, c)
 
 
 @pytest.mark.parametrize("M", [1, 5, 300])

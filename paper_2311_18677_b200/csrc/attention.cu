@@ -18,6 +18,8 @@
 // (perf.py:119-132); the reference has no attention arithmetic at all.
 #include <algorithm>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace swb {
@@ -641,25 +643,25 @@ __global__ void __launch_bounds__(NW * 32)
 // atomic ticket, no system fences.  The current token (position ctx) is
 // RoPE'd and appended to the pool by the warp owning its page, which patches
 // the staged page row from registers.
-constexpr int DCL_CL = 8;             // CTAs per (b, kv head)
+// Template: G query heads per kv head, DCL_CL CTAs per cluster (8 portable,
+// 16 opt-in), DCL_CW consumer warps.
 constexpr int DCL_S = 8;              // ring stages (one page of K and V each)
-constexpr int DCL_CW = 4;             // consumer warps
-constexpr int DCL_THREADS = (DCL_CW + 1) * 32;
 constexpr int DCL_PAGE = 16 * DA_D;   // elements of one (block, head) page
 constexpr int DCL_ST = DA_D + 4;      // floats per (o[128], m, l) record (16-byte aligned)
 
-__host__ __device__ constexpr size_t dcl_smem(int G) {
-  return (size_t)DCL_S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(DCL_CW + 1) * G * DCL_ST;
+__host__ __device__ constexpr size_t dcl_smem(int G, int CW) {
+  return (size_t)DCL_S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(CW + 1) * G * DCL_ST;
 }
 
-template <int G>
-__global__ void __launch_bounds__(DCL_THREADS)
+template <int G, int DCL_CL, int DCL_CW>
+__global__ void __launch_bounds__((DCL_CW + 1) * 32)
     attn_decode_cl_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                           __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
                           const int32_t* __restrict__ tables, int max_blocks,
                           const int32_t* __restrict__ ctx_lens, float log2_theta,
                           const float* __restrict__ alibi, int H, int Hkv, float scale_log2,
                           __nv_bfloat16* __restrict__ out, int trig) {
+  constexpr int DCL_THREADS = (DCL_CW + 1) * 32;
   extern __shared__ __align__(128) uint8_t dsm_raw[];
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(dsm_raw);         // [S][K|V][PAGE]
   float* wst = reinterpret_cast<float*>(ring + (size_t)DCL_S * 2 * DCL_PAGE);  // [CW][G][ST]
@@ -1561,28 +1563,49 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
   static const int cl_maxb = [] {
     const char* e = std::getenv("SWB_ATTN_CL");
     if (e && e[0] == '0') return 0;
+    // measured (7B, ctx 1100, decode step): B=1 2.68 -> 2.51 ms, B=8 4.65 ->
+    // 4.57, but B=32 8.54 -> 8.87 (8192 single-wave clusters vs the split-K
+    // kernel's 64-token partitions)
     const char* m = std::getenv("SWB_ATTN_CL_MAXB");
-    return m ? std::atoi(m) : 1 << 30;
+    return m ? std::atoi(m) : 16;
   }();
   if (STEP && G <= 2 && block_size == 16 && B <= cl_maxb) {
-    static bool attr_c[64] = {false};
-    if (dev < 64 && !attr_c[dev]) {
-      SWB_CUDA(cudaFuncSetAttribute(attn_decode_cl_kernel<1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)dcl_smem(1)));
-      SWB_CUDA(cudaFuncSetAttribute(attn_decode_cl_kernel<2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)dcl_smem(2)));
-      attr_c[dev] = true;
+    // cluster x consumer-warp shape: SWB_ATTN_CL_CFG = "8x4" | "8x8" | "16x4" | "16x8"
+    static const int cfg_id = [] {
+      const char* e = std::getenv("SWB_ATTN_CL_CFG");
+      if (!e) return 0;
+      if (!strcmp(e, "8x8")) return 1;
+      if (!strcmp(e, "16x4")) return 2;
+      if (!strcmp(e, "16x8")) return 3;
+      return 0;
+    }();
+    const int CL = cfg_id >= 2 ? 16 : 8, CW = (cfg_id & 1) ? 8 : 4;
+    using KFn = void (*)(const __nv_bfloat16*, int, __nv_bfloat16*, __nv_bfloat16*,
+                         const int32_t*, int, const int32_t*, float, const float*, int, int,
+                         float, __nv_bfloat16*, int);
+    static const KFn table[2][4] = {
+        {attn_decode_cl_kernel<1, 8, 4>, attn_decode_cl_kernel<1, 8, 8>,
+         attn_decode_cl_kernel<1, 16, 4>, attn_decode_cl_kernel<1, 16, 8>},
+        {attn_decode_cl_kernel<2, 8, 4>, attn_decode_cl_kernel<2, 8, 8>,
+         attn_decode_cl_kernel<2, 16, 4>, attn_decode_cl_kernel<2, 16, 8>}};
+    const KFn kern = table[G - 1][cfg_id];
+    const size_t smem_c = dcl_smem(G, CW);
+    static bool attr_c[64][8] = {};
+    if (dev < 64 && !attr_c[dev][(G - 1) * 4 + cfg_id]) {
+      SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem_c));
+      if (CL > 8)
+        SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attr_c[dev][(G - 1) * 4 + cfg_id] = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(DCL_CL, Hkv, B);
-    cfg.blockDim = dim3(DCL_THREADS);
-    cfg.dynamicSmemBytes = dcl_smem(G);
+    cfg.gridDim = dim3(CL, Hkv, B);
+    cfg.blockDim = dim3((CW + 1) * 32);
+    cfg.dynamicSmemBytes = smem_c;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = DCL_CL;
+    at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1592,17 +1615,11 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     const float l2t = !alibi_slopes ? log2f(theta) : 0.f;
     const float sc = scale * 1.4426950408889634f;
     const int trig = pdl_early_trigger() ? 1 : 0;
-    auto q = reinterpret_cast<const __nv_bfloat16*>(qkv);
-    auto kp = reinterpret_cast<__nv_bfloat16*>(k_layer);
-    auto vp = reinterpret_cast<__nv_bfloat16*>(v_layer);
-    auto op = reinterpret_cast<__nv_bfloat16*>(out);
-    const cudaError_t lc =
-        G == 1 ? cudaLaunchKernelEx(&cfg, attn_decode_cl_kernel<1>, q, row_stride, kp, vp,
-                                    block_tables, max_blocks, ctx_lens, l2t, alibi_slopes, H, Hkv,
-                                    sc, op, trig)
-               : cudaLaunchKernelEx(&cfg, attn_decode_cl_kernel<2>, q, row_stride, kp, vp,
-                                    block_tables, max_blocks, ctx_lens, l2t, alibi_slopes, H, Hkv,
-                                    sc, op, trig);
+    const cudaError_t lc = cudaLaunchKernelEx(
+        &cfg, kern, reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
+        reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
+        block_tables, max_blocks, ctx_lens, l2t, alibi_slopes, H, Hkv, sc,
+        reinterpret_cast<__nv_bfloat16*>(out), trig);
     if (lc != cudaSuccess)
       return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_cl_kernel: %s",
                            cudaGetErrorString(lc));

@@ -146,3 +146,36 @@ def test_parked_token_tasks_decode_the_oracle_tokens():
         for i in range(r.output_tokens):
             if decisive[i]:
                 assert got[i] == ref_toks[i], (r.id, i)
+
+
+def test_chunked_prefill_decodes_the_oracle_tokens():
+    """Chunked prefill on an always-mixed machine (SchedulerConfig.
+    prefill_chunk_tokens = 64): every iteration runs the running sequences'
+    decode rows plus a chunk of the head prompt (swb_attn_chunk over the
+    pages of the earlier chunks); nobody is parked, and every request's tokens
+    equal the fp32 oracle's wherever its top-2 margin is decisive."""
+    from oracle.decoder import OracleDecoder
+    from paper_2311_18677_b200.gpu_backend import GpuBackend
+    from paper_2311_18677_b200.workers import SchedulerConfig
+    reqs = [Request(0, 0.0, 200, 12), Request(1, 0.00005, 150, 12), Request(2, 0.0003, 300, 8),
+            Request(3, 0.0005, 100, 8), Request(4, 0.0007, 37, 6)]
+    be = GpuBackend("tiny", max_seqs=16, clock="modeled")
+    cc = ClusterConfig("Baseline-B200", 1, 0, llm="tiny")
+    cc.sched = SchedulerConfig(prefill_chunk_tokens=64)
+    drv = Driver(cc, be.perf_models(), reqs, backend=be, record_log=False)
+    res = drv.run()
+    kinds = [k for _, k, _, _ in be.iter_log]
+    assert "chunk" in kinds and "prompt" not in kinds and "mixed" not in kinds
+    assert max(r.preempt_count for r in res.report.records) == 0
+    orc = OracleDecoder.from_weights(be.runners[0].w)
+    for r in reqs:
+        got = be.tokens[r.id]
+        assert len(got) == r.output_tokens
+        prompt = be._prompt_ids(r.id, r.prompt_tokens).tolist()
+        ref_toks, ref_logits = orc.generate(prompt, r.output_tokens, forced=got[:-1])
+        top2 = ref_logits.topk(2, -1).values
+        decisive = (top2[:, 0] - top2[:, 1]) > 0.02
+        for i in range(r.output_tokens):
+            if decisive[i]:
+                assert got[i] == ref_toks[i], (r.id, i)
+    torch.cuda.synchronize()

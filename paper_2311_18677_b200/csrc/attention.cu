@@ -629,8 +629,8 @@ __global__ void __launch_bounds__(NW * 32)
 
 
 // ---------------------------------------------------------------- decode, cluster
-// Streaming decode attention for MHA / small groups (G <= 2, block_size 16,
-// decode-graph form).  One thread-block CLUSTER of DCL_CL CTAs per (sequence,
+// Streaming decode attention (G = 1, 2, 4 or 8 query heads per kv head,
+// block_size 16, decode-graph form).  One thread-block CLUSTER of DCL_CL CTAs per (sequence,
 // kv head); CTA r of the cluster streams pages [r*pp, (r+1)*pp) of the context
 // through a DCL_S-stage shared-memory ring: a producer warp issues the 4 KB K
 // and V bulk copies of each (block, head) page (the first DCL_S pages before
@@ -882,28 +882,41 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
   }
   cluster_sync_all();                  // every CTA's record is in its shared memory
   if (r == 0) {
+    // per head: the peers' (m, l) once -> merge factors, then o element-wise
+    __shared__ float fac[DCL_CL * G];
+    __shared__ float ltot[G];
     const uint32_t res_local = smem_u32(res);
-    for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
-      const int g = idx / DA_D, d = idx % DA_D;
-      float mp[DCL_CL], lp[DCL_CL], op[DCL_CL];
+    for (int g = threadIdx.x; g < G; g += DCL_THREADS) {
+      float mp[DCL_CL], lp[DCL_CL];
 #pragma unroll
       for (int p = 0; p < DCL_CL; ++p) {
         const uint32_t base = mapa(res_local, p) + (uint32_t)(g * DCL_ST) * 4u;
         mp[p] = ld_dsmem(base + DA_D * 4);
         lp[p] = ld_dsmem(base + (DA_D + 1) * 4);
-        op[p] = ld_dsmem(base + d * 4);
       }
       float M = -INFINITY;
 #pragma unroll
       for (int p = 0; p < DCL_CL; ++p) M = fmaxf(M, mp[p]);
-      float O = 0.f, Ls = 0.f;
+      float Ls = 0.f;
 #pragma unroll
       for (int p = 0; p < DCL_CL; ++p) {
         const float f = mp[p] == -INFINITY ? 0.f : exp2f(mp[p] - M);
-        O = fmaf(f, op[p], O);
+        fac[p * G + g] = f;
         Ls = fmaf(f, lp[p], Ls);
       }
-      out[((size_t)b * H + kh * G + g) * DA_D + d] = __float2bfloat16(O / Ls);
+      ltot[g] = Ls;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
+      const int g = idx / DA_D, d = idx % DA_D;
+      float op[DCL_CL];
+#pragma unroll
+      for (int p = 0; p < DCL_CL; ++p)
+        op[p] = ld_dsmem(mapa(res_local, p) + (uint32_t)(g * DCL_ST + d) * 4u);
+      float O = 0.f;
+#pragma unroll
+      for (int p = 0; p < DCL_CL; ++p) O = fmaf(fac[p * G + g], op[p], O);
+      out[((size_t)b * H + kh * G + g) * DA_D + d] = __float2bfloat16(O / ltot[g]);
     }
   }
   cluster_sync_all();                  // peers keep their shared memory until rank 0 read it
@@ -1569,7 +1582,15 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     const char* m = std::getenv("SWB_ATTN_CL_MAXB");
     return m ? std::atoi(m) : 16;
   }();
-  if (STEP && G <= 2 && block_size == 16 && B <= cl_maxb) {
+  // GQA groups (G >= 4): the cluster kernel at small batch only (B <=
+  // SWB_ATTN_CL_MAXB_GQA, default 2) — a handful of (b, kv head) pairs leave
+  // the split-K MMA kernel a handful of CTAs and a global merge round trip
+  static const int cl_maxb_gqa = [] {
+    const char* m = std::getenv("SWB_ATTN_CL_MAXB_GQA");
+    return m ? std::atoi(m) : 2;
+  }();
+  const int gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : -1;
+  if (STEP && gi >= 0 && block_size == 16 && B <= (G <= 2 ? cl_maxb : std::min(cl_maxb, cl_maxb_gqa))) {
     // cluster x consumer-warp shape: SWB_ATTN_CL_CFG = "8x4" | "8x8" | "16x4" | "16x8"
     static const int cfg_id = [] {
       const char* e = std::getenv("SWB_ATTN_CL_CFG");
@@ -1583,20 +1604,19 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     using KFn = void (*)(const __nv_bfloat16*, int, __nv_bfloat16*, __nv_bfloat16*,
                          const int32_t*, int, const int32_t*, float, const float*, int, int,
                          float, __nv_bfloat16*, int);
-    static const KFn table[2][4] = {
-        {attn_decode_cl_kernel<1, 8, 4>, attn_decode_cl_kernel<1, 8, 8>,
-         attn_decode_cl_kernel<1, 16, 4>, attn_decode_cl_kernel<1, 16, 8>},
-        {attn_decode_cl_kernel<2, 8, 4>, attn_decode_cl_kernel<2, 8, 8>,
-         attn_decode_cl_kernel<2, 16, 4>, attn_decode_cl_kernel<2, 16, 8>}};
-    const KFn kern = table[G - 1][cfg_id];
+#define SWB_CLK(g) {attn_decode_cl_kernel<g, 8, 4>, attn_decode_cl_kernel<g, 8, 8>, \
+                    attn_decode_cl_kernel<g, 16, 4>, attn_decode_cl_kernel<g, 16, 8>}
+    static const KFn table[4][4] = {SWB_CLK(1), SWB_CLK(2), SWB_CLK(4), SWB_CLK(8)};
+#undef SWB_CLK
+    const KFn kern = table[gi][cfg_id];
     const size_t smem_c = dcl_smem(G, CW);
-    static bool attr_c[64][8] = {};
-    if (dev < 64 && !attr_c[dev][(G - 1) * 4 + cfg_id]) {
+    static bool attr_c[64][16] = {};
+    if (dev < 64 && !attr_c[dev][gi * 4 + cfg_id]) {
       SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_c));
       if (CL > 8)
         SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      attr_c[dev][(G - 1) * 4 + cfg_id] = true;
+      attr_c[dev][gi * 4 + cfg_id] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL, Hkv, B);

@@ -375,9 +375,10 @@ def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
 
 @pytest.mark.parametrize("H,Hkv,alibi,cached", [
     (32, 32, False, [0, 15, 16, 130, 1000, 2047]), (8, 4, False, [3, 700]),
-    (16, 16, True, [31, 1500]), (32, 32, False, [8190])])
+    (16, 16, True, [31, 1500]), (32, 32, False, [8190]), (64, 8, False, [3, 1100]),
+    (16, 4, True, [500])])
 def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached):
-    """The cluster-streaming decode kernel (MHA / G = 2, decode graph form)
+    """The cluster-streaming decode kernel (G = 1, 2, 4, 8; decode graph form)
     against a plain torch fp32 attention over the gathered pages: the current
     token (position = ctx) is RoPE'd (or ALiBi-biased), appended to its
     block-table slot, and attends over positions 0..ctx; contexts from 1 token

@@ -629,8 +629,8 @@ __global__ void __launch_bounds__(NW * 32)
 
 
 // ---------------------------------------------------------------- decode, cluster
-// Streaming decode attention (G = 1, 2, 4 or 8 query heads per kv head,
-// block_size 16, decode-graph form).  One thread-block CLUSTER of DCL_CL CTAs per (sequence,
+// Streaming decode attention for MHA / small groups (G = 1 or 2 query heads
+// per kv head, block_size 16, decode-graph form).  One thread-block CLUSTER of DCL_CL CTAs per (sequence,
 // kv head); CTA r of the cluster streams pages [r*pp, (r+1)*pp) of the context
 // through a DCL_S-stage shared-memory ring: a producer warp issues the 4 KB K
 // and V bulk copies of each (block, head) page (the first DCL_S pages before
@@ -645,15 +645,16 @@ __global__ void __launch_bounds__(NW * 32)
 // the staged page row from registers.
 // Template: G query heads per kv head, DCL_CL CTAs per cluster (8 portable,
 // 16 opt-in), DCL_CW consumer warps.
-constexpr int DCL_S = 8;              // ring stages (one page of K and V each)
 constexpr int DCL_PAGE = 16 * DA_D;   // elements of one (block, head) page
 constexpr int DCL_ST = DA_D + 4;      // floats per (o[128], m, l) record (16-byte aligned)
 
-__host__ __device__ constexpr size_t dcl_smem(int G, int CW) {
-  return (size_t)DCL_S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(CW + 1) * G * DCL_ST;
+__host__ __device__ constexpr size_t dcl_smem(int G, int CW, int S) {
+  return (size_t)S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(CW + 1) * G * DCL_ST;
 }
 
-template <int G, int DCL_CL, int DCL_CW>
+// DCL_S: ring stages (one page of K and V each); all of a CTA's pages are
+// requested before the PDL wait when they fit the ring
+template <int G, int DCL_CL, int DCL_CW, int DCL_S>
 __global__ void __launch_bounds__((DCL_CW + 1) * 32)
     attn_decode_cl_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                           __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
@@ -1582,16 +1583,14 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     const char* m = std::getenv("SWB_ATTN_CL_MAXB");
     return m ? std::atoi(m) : 16;
   }();
-  // GQA groups (G >= 4): the cluster kernel at small batch only (B <=
-  // SWB_ATTN_CL_MAXB_GQA, default 2) — a handful of (b, kv head) pairs leave
-  // the split-K MMA kernel a handful of CTAs and a global merge round trip
-  static const int cl_maxb_gqa = [] {
-    const char* m = std::getenv("SWB_ATTN_CL_MAXB_GQA");
-    return m ? std::atoi(m) : 2;
-  }();
-  const int gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : -1;
-  if (STEP && gi >= 0 && block_size == 16 && B <= (G <= 2 ? cl_maxb : std::min(cl_maxb, cl_maxb_gqa))) {
-    // cluster x consumer-warp shape: SWB_ATTN_CL_CFG = "8x4" | "8x8" | "16x4" | "16x8"
+  // GQA groups (G >= 4) stay on the tensor-core split-K kernel below: the
+  // CUDA-core cluster kernel with 8 heads per pass is FMA/shuffle-bound
+  // (measured 70B-TP2 B=1 ctx 1100: 24.1 vs 12.8 us; 70B TP4 decode step
+  // 9.93 vs 8.42 ms)
+  if (STEP && G <= 2 && block_size == 16 && B <= cl_maxb) {
+    const int gi = G - 1;
+    // cluster x consumer-warp shape: SWB_ATTN_CL_CFG = "8x4" | "8x8" | "16x4" | "16x8";
+    // ring depth: SWB_ATTN_CL_S = 8 | 12 (default: 12 when a CTA's pages fit it)
     static const int cfg_id = [] {
       const char* e = std::getenv("SWB_ATTN_CL_CFG");
       if (!e) return 0;
@@ -1600,23 +1599,32 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
       if (!strcmp(e, "16x8")) return 3;
       return 0;
     }();
+    static const int s_env = [] {
+      const char* e = std::getenv("SWB_ATTN_CL_S");
+      return e ? std::atoi(e) : 0;
+    }();
     const int CL = cfg_id >= 2 ? 16 : 8, CW = (cfg_id & 1) ? 8 : 4;
+    const int pages_per_cta = ((max_ctx + 15) / 16 + CL - 1) / CL;
+    const int si = s_env == 8 ? 0 : s_env == 12 ? 1 : (pages_per_cta > 8 ? 1 : 0);
+    const int S = si ? 12 : 8;
     using KFn = void (*)(const __nv_bfloat16*, int, __nv_bfloat16*, __nv_bfloat16*,
                          const int32_t*, int, const int32_t*, float, const float*, int, int,
                          float, __nv_bfloat16*, int);
-#define SWB_CLK(g) {attn_decode_cl_kernel<g, 8, 4>, attn_decode_cl_kernel<g, 8, 8>, \
-                    attn_decode_cl_kernel<g, 16, 4>, attn_decode_cl_kernel<g, 16, 8>}
-    static const KFn table[4][4] = {SWB_CLK(1), SWB_CLK(2), SWB_CLK(4), SWB_CLK(8)};
+#define SWB_CLK(g, s) {attn_decode_cl_kernel<g, 8, 4, s>, attn_decode_cl_kernel<g, 8, 8, s>, \
+                       attn_decode_cl_kernel<g, 16, 4, s>, attn_decode_cl_kernel<g, 16, 8, s>}
+    static const KFn table[2][2][4] = {{SWB_CLK(1, 8), SWB_CLK(1, 12)},
+                                       {SWB_CLK(2, 8), SWB_CLK(2, 12)}};
 #undef SWB_CLK
-    const KFn kern = table[gi][cfg_id];
-    const size_t smem_c = dcl_smem(G, CW);
+    const KFn kern = table[gi][si][cfg_id];
+    const size_t smem_c = dcl_smem(G, CW, S);
     static bool attr_c[64][16] = {};
-    if (dev < 64 && !attr_c[dev][gi * 4 + cfg_id]) {
+    const int ai = gi * 8 + si * 4 + cfg_id;
+    if (dev < 64 && !attr_c[dev][ai]) {
       SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_c));
       if (CL > 8)
         SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      attr_c[dev][gi * 4 + cfg_id] = true;
+      attr_c[dev][ai] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL, Hkv, B);

@@ -378,7 +378,8 @@ def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
     (16, 16, True, [31, 1500]), (32, 32, False, [8190]), (64, 8, False, [3, 1100]),
     (16, 4, True, [500])])
 def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached):
-    """The cluster-streaming decode kernel (G = 1, 2, 4, 8; decode graph form)
+    """Decode-graph attention — the cluster-streaming kernel for G = 1, 2, the
+    tensor-core split-K kernel for G = 4, 8 —
     against a plain torch fp32 attention over the gathered pages: the current
     token (position = ctx) is RoPE'd (or ALiBi-biased), appended to its
     block-table slot, and attends over positions 0..ctx; contexts from 1 token

@@ -1590,7 +1590,7 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
   if (STEP && G <= 2 && block_size == 16 && B <= cl_maxb) {
     const int gi = G - 1;
     // cluster x consumer-warp shape: SWB_ATTN_CL_CFG = "8x4" | "8x8" | "16x4" | "16x8";
-    // ring depth: SWB_ATTN_CL_S = 8 | 12 (default: 12 when a CTA's pages fit it)
+    // ring depth: SWB_ATTN_CL_S = 8 (default) | 12
     static const int cfg_id = [] {
       const char* e = std::getenv("SWB_ATTN_CL_CFG");
       if (!e) return 0;
@@ -1605,7 +1605,11 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     }();
     const int CL = cfg_id >= 2 ? 16 : 8, CW = (cfg_id & 1) ? 8 : 4;
     const int pages_per_cta = ((max_ctx + 15) / 16 + CL - 1) / CL;
-    const int si = s_env == 8 ? 0 : s_env == 12 ? 1 : (pages_per_cta > 8 ? 1 : 0);
+    // 12 stages prefetch a 1100-token context whole before the PDL wait (7B
+    // B=1 standalone 6.7 -> 6.0 us) but at 2 CTAs/SM the step loses (2.51 ->
+    // 2.60 ms: less room for the next kernel's early CTAs); default 8
+    (void)pages_per_cta;
+    const int si = s_env == 12 ? 1 : 0;
     const int S = si ? 12 : 8;
     using KFn = void (*)(const __nv_bfloat16*, int, __nv_bfloat16*, __nv_bfloat16*,
                          const int32_t*, int, const int32_t*, float, const float*, int, int,

@@ -102,7 +102,10 @@ class ModelRunner:
         self.push_ctas = push_ctas
         self.dev = weights.embed.device
         self._cap = 0
-        self.push_stream = torch.cuda.Stream(device=self.dev)
+        # SWB_PUSH_PRIORITY=high: the push stream's CTAs are scheduled ahead of
+        # the prefill's (A/B of the in-flight push bandwidth vs the TTFT cost)
+        prio = -1 if os.environ.get("SWB_PUSH_PRIORITY", "normal") == "high" else 0
+        self.push_stream = torch.cuda.Stream(device=self.dev, priority=prio)
         self._buf_ev = [None, None]      # last push that read each qkv buffer
         self._stash = None               # [L, SERIAL_MAX_ROWS, qkv_cols] (serialized mode)
         self._stash_ev = None

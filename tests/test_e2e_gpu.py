@@ -8,8 +8,9 @@ C1 shape: 512-token prompt, 128 greedy tokens).
   the CPU lowest-free-first allocator's tables.
 
 Tolerance (bf16 activations / fp32 accumulation vs fp32 oracle): teacher-
-forced logits within max|diff| <= 0.03 + 0.02*max|logit|; greedy ids must
-agree wherever the oracle's top-2 margin exceeds that bound.
+forced logits within max|diff| <= TOL_REL * max|logit| (recorded with the
+oracle's bf16-storage twin in gpurun_out/parity_tiny.json); greedy ids must
+agree wherever the oracle's top-2 margin exceeds twice that step's error.
 """
 
 import math
@@ -58,6 +59,25 @@ def _run_colocated(cfg, runner, kv, prompt, n_out, return_logits=True):
     return seq, out, torch.stack(logits).cpu()
 
 
+# max |dlogit| / max |logit| allowed (C1 tiny, BLOOM-architecture tiny)
+TOL_REL = {"tiny": 0.02, "bloom-tiny": 0.02}
+
+
+def _record(name, rec):
+    import json
+    d = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    p = os.path.join(d, "parity_tiny.json")
+    try:
+        with open(p) as f:
+            allr = json.load(f)
+    except Exception:
+        allr = {}
+    allr[name] = rec
+    with open(p, "w") as f:
+        json.dump(allr, f, indent=1)
+
+
 @pytest.mark.parametrize("model", ["tiny", "bloom-tiny"])
 def test_tiny_colocated_vs_oracle(model):
     """C1 (Llama architecture) and the BLOOM architecture of C5 (LayerNorm,
@@ -70,14 +90,20 @@ def test_tiny_colocated_vs_oracle(model):
     orc = OracleDecoder.from_weights(w)
     # teacher-force the oracle on the GPU's tokens so both see the same inputs
     ref_toks, ref_logits = orc.generate(prompt, 128, forced=gpu_toks[:-1])
+    twin = OracleDecoder(orc.cfg, orc.layers, orc.embed, orc.lm_head, orc.final_norm,
+                         extra=orc.extra, emulate_bf16=True)
+    _, emul_logits = twin.generate(prompt, 128, forced=gpu_toks[:-1])
     diff = (gpu_logits - ref_logits).abs().max(-1).values
+    emul = float((emul_logits - ref_logits).abs().max())
     scale = ref_logits.abs().max(-1).values
-    tol = 0.03 + 0.02 * scale
-    print(f"max logit diff {diff.max():.4f}, scale {scale.max():.3f}")
-    assert bool((diff <= tol).all()), (diff.max(), scale.max())
+    tol = TOL_REL[model] * float(scale.max())
+    _record(model, {"max_dlogit": float(diff.max()), "emul_dlogit": emul,
+                    "max_logit": float(scale.max()), "tol": tol})
+    print(f"max logit diff {diff.max():.4f} (bf16 twin {emul:.4f}), scale {scale.max():.3f}")
+    assert float(diff.max()) <= tol, (diff.max(), scale.max())
     top2 = ref_logits.topk(2, -1).values
     margin = top2[:, 0] - top2[:, 1]
-    decisive = margin > tol
+    decisive = margin > 2 * diff            # cannot flip by the observed rounding
     agree = torch.tensor(gpu_toks) == torch.tensor(ref_toks)
     assert bool(agree[decisive].all())
     assert int(decisive.sum()) >= 64  # most steps must be decisive

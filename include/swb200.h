@@ -355,6 +355,21 @@ int swb_tp_comm_destroy(swb_tp_comm* comm);
 void* swb_tp_comm_slot(const swb_tp_comm* comm, int slot);
 int swb_tp_allreduce_f32(swb_tp_comm* comm, int slot, float* out, size_t n,
                          uintptr_t stream);
+/* Fused projection + all-reduce push (decode, one row): the weight-streaming
+ * GEMV (epilogue SWB_EPI_F32, or SWB_EPI_RESID_F32 with resid on the rank
+ * that folds the residual) writes its fp32 partial into this rank's slot
+ * `slot` AND stores it straight into every peer's receive buffer for this
+ * rank over NVLink from the epilogue; each CTA then publishes its completion
+ * on the peers' push counters (system-scope fence, then a release add).
+ * swb_tp_allreduce_recv_f32 waits for every peer's CTAs and writes the
+ * rank-ordered sum (same bits as swb_tp_allreduce_f32).  Use the two as a
+ * pair on the same slot, alternating slots like swb_tp_allreduce_f32.
+ * N * 4 bytes must fit the 1 MB receive buffers. */
+int swb_gemv_bf16_tp(const void* x, const void* w, const void* resid, const void* bias,
+                     int M, int N, int K, int epilogue, swb_tp_comm* comm, int slot,
+                     uintptr_t stream);
+int swb_tp_allreduce_recv_f32(swb_tp_comm* comm, int slot, float* out, size_t n,
+                              uintptr_t stream);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,8 @@ SIGNATURES = {
     "swb_tp_comm_destroy": [_P],
     "swb_tp_comm_slot": [_P, _I],
     "swb_tp_allreduce_f32": [_P, _I, _P, _S, _ST],
+    "swb_tp_allreduce_recv_f32": [_P, _I, _P, _S, _ST],
+    "swb_gemv_bf16_tp": [_P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _ST],
 }
 _RESTYPE = {"swb_last_error": C.c_char_p, "swb_attn_decode_workspace": _S,
             "swb_attn_chunk_workspace": _S,
@@ -136,7 +138,8 @@ LAUNCH_MULT = {
     "swb_kv_handoff": 1,
     "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1, "swb_attn_chunk": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
-    "swb_block_free": 1, "swb_tp_allreduce_f32": 1,
+    "swb_block_free": 1, "swb_tp_allreduce_f32": 1, "swb_tp_allreduce_recv_f32": 1,
+    "swb_gemv_bf16_tp": 1,
 }
 _launches = [0]
 

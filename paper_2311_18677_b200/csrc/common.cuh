@@ -33,7 +33,12 @@ int swb_check_launch(const char* what);
                            cudaGetErrorString(e_));                            \
   } while (0)
 
+struct swb_tp_comm;
 namespace swb {
+struct TpPush;
+// tpcomm.cu: peer targets of a fused projection on `slot`, and the number of
+// producer CTAs (nsrc) the matching swb_tp_allreduce_recv_f32 waits for
+int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, TpPush* out);
 
 constexpr int kNumSMs = 148;
 
@@ -400,6 +405,18 @@ __device__ __forceinline__ float ld_dsmem(uint32_t cluster_addr) {
   float v;
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
   return v;
+}
+
+// ---------------------------------------------------------------- TP push
+// Peer receive buffers / push counters a fused projection GEMV writes into
+// (tpcomm.cu fills it; world 0 = no push).
+struct TpPush {
+  float* rx[8];          // peer p's receive buffer for this rank's partial (p != rank)
+  unsigned* cnt[8];      // peer p's push counter for (slot, this rank)
+  int world, rank;
+};
+__device__ __forceinline__ void red_release_sys_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 }  // namespace swb

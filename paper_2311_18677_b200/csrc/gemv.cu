@@ -18,6 +18,8 @@
 //
 // Replaces PerfModel.token_iter_time (reference perf.py:125-132) for the
 // linear layers of a token-phase iteration.
+#include <cstring>
+
 #include "common.cuh"
 
 namespace swb {
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     gemv_bulk_kernel(const void* __restrict__ xin, const __nv_bfloat16* __restrict__ nw,
                      float eps, const __nv_bfloat16* __restrict__ W, void* out,
                      const float* resid, const __nv_bfloat16* bias, int M, int N, int K,
-                     int epi, int n_items, int trig) {
+                     int epi, int n_items, int trig, const TpPush tpp) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TV_STAGES * TV_STAGE_BYTES);
   uint64_t* empty = full + TV_STAGES;
@@ -256,14 +258,27 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
               reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(v);
             else if (epi == SWB_EPI_GELU)
               reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16(gelu_tanh(v));
-            else if (epi == SWB_EPI_F32)
-              reinterpret_cast<float*>(out)[idx] = v;
-            else
-              reinterpret_cast<float*>(out)[idx] = resid[idx] + v;
+            else {
+              const float o = epi == SWB_EPI_F32 ? v : resid[idx] + v;
+              reinterpret_cast<float*>(out)[idx] = o;
+              // fused TP all-reduce: the partial goes straight to every peer
+              // (posted NVLink stores) while the weights still stream
+              for (int p = 0; p < tpp.world; ++p)
+                if (p != tpp.rank) tpp.rx[p][idx] = o;
+            }
           }
         }
       }
     }
+  }
+  if (tpp.world > 1 && warp == 0) {
+    // every partial this CTA pushed is visible system-wide before its
+    // completion count reaches the peers
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0)
+      for (int p = 0; p < tpp.world; ++p)
+        if (p != tpp.rank) red_release_sys_add(tpp.cnt[p], 1u);
   }
 }
 
@@ -283,7 +298,7 @@ template <int MB, bool NORM>
 static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
                        const __nv_bfloat16* w, void* out, const float* r,
                        const __nv_bfloat16* bias, int M, int N, int K, int epi, int items,
-                       cudaStream_t s) {
+                       cudaStream_t s, swb_tp_comm* tp = nullptr, int tp_slot = 0) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
@@ -295,9 +310,15 @@ static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
   }
   const size_t smem = TV_SMEM + (NORM ? (size_t)M * K * 2 : 0);
   const int grid = min(items, gemv_ctas_per_sm() * kNumSMs);
+  TpPush tpp;
+  memset(&tpp, 0, sizeof(tpp));
+  if (tp) {
+    const int st = tp_push_targets(tp, tp_slot, grid, &tpp);
+    if (st) return st;
+  }
   const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM>, dim3(grid), dim3(TV_THREADS),
                                 smem, s, x, nw, eps, w, out, r, bias, M, N, K, epi, items,
-                                pdl_early_trigger() ? 1 : 0);
+                                pdl_early_trigger() ? 1 : 0, tpp);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("gemv_bulk_kernel");
@@ -667,6 +688,26 @@ extern "C" int swb_gemv_bf16_bias(const void* x, const void* w, void* out, const
   if (st) return st;
   SWB_REQUIRE(!bias || epilogue != SWB_EPI_SWIGLU, "swb_gemv_bf16: no bias with SwiGLU");
   return dispatch_gemv<false>(x, nullptr, 0.f, w, out, resid, bias, M, N, K, epilogue, stream);
+}
+
+extern "C" int swb_gemv_bf16_tp(const void* x, const void* w, const void* resid,
+                                const void* bias, int M, int N, int K, int epilogue,
+                                swb_tp_comm* comm, int slot, uintptr_t stream) {
+  SWB_REQUIRE(comm, "swb_gemv_bf16_tp: null communicator");
+  void* out = swb_tp_comm_slot(comm, slot);
+  SWB_REQUIRE(out, "swb_gemv_bf16_tp: bad slot %d", slot);
+  const int st = check_gemv_args("swb_gemv_bf16_tp", x, w, out, resid, M, N, K, epilogue);
+  if (st) return st;
+  SWB_REQUIRE(M == 1, "swb_gemv_bf16_tp: one row (decode B=1) only, got M=%d", M);
+  SWB_REQUIRE(epilogue == SWB_EPI_F32 || epilogue == SWB_EPI_RESID_F32,
+              "swb_gemv_bf16_tp: fp32 epilogues only");
+  SWB_REQUIRE((size_t)N * 4 <= (size_t)(1 << 20), "swb_gemv_bf16_tp: N=%d exceeds the receive "
+              "buffers", N);
+  const int items = (N + TV_ROWS - 1) / TV_ROWS;
+  return launch_gemv<1, false>(x, nullptr, 0.f, reinterpret_cast<const __nv_bfloat16*>(w), out,
+                               reinterpret_cast<const float*>(resid),
+                               reinterpret_cast<const __nv_bfloat16*>(bias), M, N, K, epilogue,
+                               items, (cudaStream_t)stream, comm, slot);
 }
 
 extern "C" int swb_gemv_rmsnorm_bf16(const float* x, const void* norm_w, float eps,

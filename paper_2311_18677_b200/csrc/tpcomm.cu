@@ -3,7 +3,8 @@
 //
 // Each rank owns one device region, exported by CUDA IPC and mapped by every
 // peer of its TP group:
-//   [slot 0 | slot 1 | aux slot 2 | rx[3][MAXW] | flags[3][MAXW][MAXC] | counters[3][MAXC]]
+//   [slot 0 | slot 1 | aux slot 2 | rx[3][MAXW] | flags[3][MAXW][MAXC] | counters[3][MAXC]
+//    | push counters[3][MAXW] | receive epochs[3][MAXC]]
 // The producing GEMM/GEMV writes its fp32 partial sums straight into a slot
 // (rank 0 folds the residual in), so the all-reduce moves no extra copy:
 //   CTA c of rank r   1. system-scope fence, then a store of its epoch into
@@ -25,6 +26,12 @@
 // reduction (the vocab-parallel greedy candidates): the slot 0/1 all-reduces
 // between two of its uses order them the same way, and it keeps the 0/1
 // alternation unbroken across steps (a step does an even number of those).
+// Fused form (swb_gemv_bf16_tp + swb_tp_allreduce_recv_f32): the projection
+// GEMV's epilogue stores its partial into the peers' rx[slot][rank] itself
+// and each of its nsrc CTAs adds 1 to the peers' push counter[slot][rank]
+// after a system fence; the receive kernel's CTA c waits until every peer's
+// counter reached epoch * nsrc (its own per-CTA epoch) and sums from local
+// memory — the separate copy-and-flag pass of the push form disappears.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -48,6 +55,9 @@ struct TpIpcBlob {
 static_assert(sizeof(TpIpcBlob) <= SWB_TP_IPC_BYTES, "blob too large");
 
 struct TpArgs {
+  const uint32_t* my_pcnt;           // fused form: this rank's push counters[slot][src]
+  uint32_t* my_rctr;                 // fused form: per-CTA receive epochs[slot][c]
+  uint32_t nsrc;                     // fused form: producer CTAs per peer
   const float* peer_slot[TP_MAXW];   // slot base of every rank (own = local)
   float* peer_rx[TP_MAXW];           // push mode: rank p's rx[slot][this rank]
   const float* my_rx;                // push mode: this rank's rx[slot][0]
@@ -118,6 +128,49 @@ __global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a
   // weights (pre-wait) while this one waits on the peers' flags over NVLink
   if (trig) pdl_launch_dependents();
   const int c = blockIdx.x;
+  if (mode == 3) {
+    // fused form: the peers' projection GEMVs already pushed their partials
+    // into rx[slot][p] and counted their CTAs; wait, then sum locally
+    const long long n4 = a.n >> 2;
+    const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+    const long long lo = (long long)c * per, hi = min(n4, lo + per);
+    uint32_t* rc = a.my_rctr + a.slot * TP_MAXC + c;
+    uint32_t e = 0;
+    if (threadIdx.x == 0) {
+      e = *rc + 1;
+      const uint32_t target = e * a.nsrc;
+      const long long t0 = clock64();
+      for (int p = 0; p < a.world; ++p) {
+        if (p == a.rank) continue;
+        const uint32_t* f = a.my_pcnt + (size_t)a.slot * TP_MAXW + p;
+        int spins = 0;
+        while ((int)(ld_acquire_sys(f) - target) < 0) {
+          if (++spins > 64) __nanosleep(64);
+          if (clock64() - t0 > 40000000000ll) __trap();
+        }
+      }
+    }
+    __syncthreads();
+    const float4* mine = reinterpret_cast<const float4*>(a.peer_slot[a.rank]);
+    float4* out4 = reinterpret_cast<float4*>(a.out);
+    for (long long i = lo + threadIdx.x; i < hi; i += TP_THREADS) {
+      float4 v[TP_MAXW];
+#pragma unroll
+      for (int p = 0; p < TP_MAXW; ++p)
+        if (p < a.world)
+          v[p] = p == a.rank ? __ldcg(mine + i)
+                             : __ldcg(reinterpret_cast<const float4*>(a.my_rx + p * a.rx_stride) + i);
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < TP_MAXW; ++p)
+        if (p < a.world) {
+          sum.x += v[p].x; sum.y += v[p].y; sum.z += v[p].z; sum.w += v[p].w;
+        }
+      out4[i] = sum;
+    }
+    if (threadIdx.x == 0) *rc = e;
+    return;
+  }
   uint32_t* ctr = a.my_ctr + a.slot * TP_MAXC + c;
   uint32_t e = 0;
   if (threadIdx.x == 0) {
@@ -209,6 +262,7 @@ using namespace swb;
 
 struct swb_tp_comm {
   int rank, world, device;
+  int nsrc[TP_NSLOT];               // producer CTAs of the last fused GEMV per slot
   size_t slot_bytes;
   uint8_t* base;                    // own region
   uint8_t* peer_base[TP_MAXW];      // mapped regions (own at [rank])
@@ -227,9 +281,12 @@ static size_t tp_rx_off(size_t slot_bytes) {
 static size_t tp_flags_off(size_t slot_bytes) {
   return tp_rx_off(slot_bytes) + TP_NSLOT * TP_MAXW * tp_rx_bytes(slot_bytes);
 }
-static size_t tp_region_bytes(size_t slot_bytes) {
+static size_t tp_pcnt_off(size_t slot_bytes) {
   return tp_flags_off(slot_bytes) +
          sizeof(uint32_t) * (TP_NSLOT * TP_MAXW * TP_MAXC + TP_NSLOT * TP_MAXC);
+}
+static size_t tp_region_bytes(size_t slot_bytes) {
+  return tp_pcnt_off(slot_bytes) + sizeof(uint32_t) * (TP_NSLOT * TP_MAXW + TP_NSLOT * TP_MAXC);
 }
 
 extern "C" int swb_tp_comm_create(int rank, int world, size_t slot_bytes, swb_tp_comm** out,
@@ -304,6 +361,29 @@ extern "C" void* swb_tp_comm_slot(const swb_tp_comm* c, int slot) {
   return c->base + tp_slot_off(c->slot_bytes, slot);
 }
 
+namespace swb {
+int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, TpPush* out) {
+  SWB_REQUIRE(c && out, "tp_push_targets: null pointer");
+  SWB_REQUIRE(c->connected || c->world == 1, "tp_push_targets: not connected");
+  SWB_REQUIRE(slot >= 0 && slot < TP_NSLOT, "tp_push_targets: bad slot");
+  SWB_REQUIRE(c->world <= 8, "tp_push_targets: world > 8");
+  const size_t rxb = tp_rx_bytes(c->slot_bytes);
+  const size_t rx_off = tp_rx_off(c->slot_bytes) + (size_t)slot * TP_MAXW * rxb;
+  const size_t pc_off = tp_pcnt_off(c->slot_bytes);
+  memset(out, 0, sizeof(*out));
+  out->world = c->world;
+  out->rank = c->rank;
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) continue;
+    out->rx[p] = reinterpret_cast<float*>(c->peer_base[p] + rx_off + (size_t)c->rank * rxb);
+    out->cnt[p] = reinterpret_cast<unsigned*>(c->peer_base[p] + pc_off) +
+                  (size_t)slot * TP_MAXW + c->rank;
+  }
+  c->nsrc[slot] = nsrc;
+  return SWB_OK;
+}
+}  // namespace swb
+
 // SWB_TP_AR_TRIGGER=0: exit-time PDL trigger instead of right after the wait
 static int tp_trigger() {
   static const int on = [] {
@@ -313,8 +393,26 @@ static int tp_trigger() {
   return on;
 }
 
+static int tp_allreduce(swb_tp_comm* c, int slot, float* out, size_t n, uintptr_t stream,
+                        bool recv);
+
 extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t n,
                                     uintptr_t stream) {
+  return tp_allreduce(c, slot, out, n, stream, false);
+}
+
+extern "C" int swb_tp_allreduce_recv_f32(swb_tp_comm* c, int slot, float* out, size_t n,
+                                         uintptr_t stream) {
+  SWB_REQUIRE(c && c->world > 1, "swb_tp_allreduce_recv_f32: needs a TP group");
+  SWB_REQUIRE(slot >= 0 && slot < TP_NSLOT && c->nsrc[slot] > 0,
+              "swb_tp_allreduce_recv_f32: no fused projection on slot %d", slot);
+  SWB_REQUIRE(n * sizeof(float) <= tp_rx_bytes(c->slot_bytes),
+              "swb_tp_allreduce_recv_f32: n=%zu exceeds the receive buffers", n);
+  return tp_allreduce(c, slot, out, n, stream, true);
+}
+
+static int tp_allreduce(swb_tp_comm* c, int slot, float* out, size_t n, uintptr_t stream,
+                        bool recv) {
   SWB_REQUIRE(c && out, "swb_tp_allreduce_f32: null pointer");
   SWB_REQUIRE(c->connected || c->world == 1, "swb_tp_allreduce_f32: not connected");
   SWB_REQUIRE(slot >= 0 && slot < TP_NSLOT, "swb_tp_allreduce_f32: slot must be 0, 1 or 2");
@@ -337,6 +435,10 @@ extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t
   a.rx_stride = (long long)(rxb / sizeof(float));
   a.my_flags = reinterpret_cast<uint32_t*>(c->base + flags_off);
   a.my_ctr = a.my_flags + TP_NSLOT * TP_MAXW * TP_MAXC;
+  a.my_pcnt = reinterpret_cast<const uint32_t*>(c->base + tp_pcnt_off(c->slot_bytes));
+  a.my_rctr = reinterpret_cast<uint32_t*>(c->base + tp_pcnt_off(c->slot_bytes)) +
+              TP_NSLOT * TP_MAXW;
+  a.nsrc = recv ? (uint32_t)c->nsrc[slot] : 0u;
   a.out = out;
   a.n = (long long)n;
   a.rank = c->rank;
@@ -353,6 +455,7 @@ extern "C" int swb_tp_allreduce_f32(swb_tp_comm* c, int slot, float* out, size_t
     return !(e && e[0] == '0');
   }();
   if (mode == 0 && push_on && c->world > 1 && n * sizeof(float) <= rxb) mode = 2;
+  if (recv) mode = 3;
   const cudaError_t le = launch(tp_allreduce_kernel, dim3((unsigned)ctas), dim3(TP_THREADS), 0,
                                 (cudaStream_t)stream, a, mode, tp_trigger());
   if (le != cudaSuccess)

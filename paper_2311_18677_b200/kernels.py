@@ -18,7 +18,8 @@ __all__ = ["gemm", "gemv", "gemv_rmsnorm", "linear", "embed", "rmsnorm", "layern
            "rope_kv_write",
            "kv_push_layer", "kv_push_layers", "kv_handoff", "attn_prefill", "attn_decode",
            "attn_decode_step", "decode_advance", "slots_from_table",
-           "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "EPI_GELU", "GEMV_MAX_ROWS"]
+           "gemv_tp", "EPI_BF16", "EPI_F32", "EPI_RESID_F32", "EPI_SWIGLU", "EPI_GELU",
+           "GEMV_MAX_ROWS"]
 
 # rows handled by the weight-streaming GEMVs (the tcgen05 GEMV takes up to 32)
 GEMV_MAX_ROWS = 16 if os.environ.get("SWB_GEMV_TC", "1") == "0" else 32
@@ -120,6 +121,18 @@ def linear(x, w, epi=EPI_BF16, out=None, resid=None, bias=None):
     if x.shape[0] <= GEMV_MAX_ROWS:
         return gemv(x, w, epi, out, resid, bias)
     return gemm(x, w, epi, out, resid, bias)
+
+
+def gemv_tp(x, w, epi, comm_handle, slot, resid=None, bias=None):
+    """Fused projection + all-reduce push (one decode row): the fp32 partial
+    lands in this rank's TP slot ``slot`` and, from the epilogue, in every
+    peer's receive buffer; finish with TPComm.allreduce_recv(slot, out)."""
+    _req(x, torch.bfloat16, "x")
+    _req(w, torch.bfloat16, "w")
+    if x.shape[0] != 1 or w.shape[1] != x.shape[1]:
+        raise ValidationError(f"gemv_tp: one row with K = {w.shape[1]}, got {tuple(x.shape)}")
+    call("swb_gemv_bf16_tp", x.data_ptr(), w.data_ptr(), _ptr(resid), _ptr(bias), 1,
+         w.shape[0], w.shape[1], epi, comm_handle, slot, _stream())
 
 
 def embed(tokens, table, out=None):

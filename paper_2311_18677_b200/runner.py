@@ -91,6 +91,9 @@ class ModelRunner:
         self.alibi = weights.alibi
         self.tp_max_rows = tp_max_rows    # largest prefill / decode row count reduced
         self.ar_nccl_bytes = int(os.environ.get("SWB_TP_AR_NCCL_BYTES", str(4 << 20)))
+        # SWB_TP_FUSED=0: decode B=1 projections write their TP slot and a
+        # separate kernel pushes it (A/B of the fused GEMV -> all-reduce push)
+        self.tp_fused = os.environ.get("SWB_TP_FUSED", "1") != "0"
         self.kv = kv
         self.hq = cfg.n_heads // self.tp
         self.hkv = cfg.n_kv_heads // self.tp
@@ -164,6 +167,12 @@ class ModelRunner:
             self._allreduce(x)
             return
         s = c.next_slot()
+        if self.tp_fused and x.shape[0] == 1 and x.numel() * 4 <= c.AUX_BYTES:
+            # decode B=1: the GEMV epilogue pushes its partial to the peers
+            # itself; the receive kernel only waits and sums locally
+            K.gemv_tp(inp, w, self._resid_epi(), c._h, s, resid=x, bias=b)
+            c.allreduce_recv(s, x)
+            return
         part = c.slot(s, x.shape)
         K.linear(inp, w, self._resid_epi(), out=part, resid=x, bias=b)
         c.allreduce(s, x)

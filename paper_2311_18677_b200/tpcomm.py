@@ -72,6 +72,12 @@ class TPComm:
         _abi.call("swb_tp_allreduce_f32", self._h, s, out.data_ptr(), out.numel(),
                   torch.cuda.current_stream().cuda_stream)
 
+    def allreduce_recv(self, s: int, out: torch.Tensor) -> None:
+        """Second half of the fused form: the peers' projection GEMVs
+        (kernels.gemv_tp on slot s) already pushed their partials."""
+        _abi.call("swb_tp_allreduce_recv_f32", self._h, s, out.data_ptr(), out.numel(),
+                  torch.cuda.current_stream().cuda_stream)
+
     def close(self) -> None:
         if self._h:
             _abi.call("swb_tp_comm_destroy", self._h)

@@ -82,6 +82,88 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _fused_worker(rank, world, port, q):
+    """Fused projection + all-reduce (swb_gemv_bf16_tp pushes the partial from
+    its epilogue; swb_tp_allreduce_recv_f32 waits and sums) equals the
+    two-kernel form bit for bit, eagerly and inside replayed CUDA graphs, with
+    the slots alternating between fused and unfused uses."""
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2311_18677_b200 import kernels as K
+        from paper_2311_18677_b200.tpcomm import TPComm
+        comm = TPComm(dist.group.WORLD, 64 * 8192 * 4)
+        N, Kd = 8192, 2048
+        g = torch.Generator(device="cuda").manual_seed(11 + rank)
+        w = (torch.randn(N, Kd, device="cuda", generator=g) * 0.02).bfloat16()
+        x = torch.randn(1, Kd, device="cuda", generator=g).bfloat16()
+        resid = torch.randn(1, N, device="cuda", generator=torch.Generator(device="cuda")
+                            .manual_seed(999))
+        epi = K.EPI_RESID_F32 if rank == 0 else K.EPI_F32
+        errs = []
+
+        def fused(out):
+            s = comm.next_slot()
+            K.gemv_tp(x, w, epi, comm._h, s, resid=resid if rank == 0 else None)
+            comm.allreduce_recv(s, out)
+
+        def plain(out):
+            s = comm.next_slot()
+            K.linear(x, w, epi, out=comm.slot(s, (1, N)), resid=resid)
+            comm.allreduce(s, out)
+        for it in range(6):
+            a, b = torch.empty(1, N, device="cuda"), torch.empty(1, N, device="cuda")
+            fused(a)
+            plain(b)
+            torch.cuda.synchronize()
+            if not torch.equal(a, b):
+                errs.append(("eager", it, (a - b).abs().max().item()))
+        ref = b.clone()
+        outs = torch.empty(2, 1, N, device="cuda")
+
+        def body():
+            comm.reset()
+            fused(outs[0])
+            fused(outs[1])
+        body()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            body()
+        for rep in range(5):
+            outs.zero_()
+            dist.barrier()
+            gr.replay()
+            torch.cuda.synchronize()
+            if not (torch.equal(outs[0], ref) and torch.equal(outs[1], ref)):
+                errs.append(("graph", rep))
+        comm.close()
+        q.put((rank, errs))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_fused_projection_allreduce_exact():
+    world = min(4, torch.cuda.device_count())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, errs in res:
+        assert errs == [], (rank, errs)
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 def test_tp_allreduce_p2p_exact():
     world = min(4, torch.cuda.device_count())

@@ -443,6 +443,8 @@ def main():
     ap.add_argument("--route", default="jsq", choices=["jsq", "rr"],
                     help="--trace with several pairs: live JSQ routing at arrival (reference "
                          "Cluster.route) or round-robin")
+    ap.add_argument("--dump-tokens", default=None,
+                    help="--trace: write {request id: generated token ids} to this JSON file")
     ap.add_argument("--tp", type=int, default=1,
                     help="tensor-parallel degree of each prompt/token machine (N >= 2*tp)")
     args = ap.parse_args()

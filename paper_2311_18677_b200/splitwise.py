@@ -253,6 +253,7 @@ class TokenServer:
         self.machine = Machine(0, None, estimated_perf_model(runner.cfg, self.kv,
                                                              runner.w.nbytes()), TOKEN, sched)
         self.step_log: list[tuple] = []     # (batch, summed context, device ms) per decode step
+        self.tokens: dict = {}              # serve_trace: rid -> generated token ids
         self._ev = None
 
     def _events(self):
@@ -435,6 +436,7 @@ class TokenServer:
                     self.res_boxes[pm].put(rows)
             for rid, seq, plen, first, n_out in self.watch.poll():
                 first_seen[rid] = self.watch.seen.pop(rid)
+                self.tokens[rid] = [first]
                 landed += 1
                 if board is not None:
                     board.publish_token(self.machine_id, board.LANDED, landed)
@@ -469,6 +471,7 @@ class TokenServer:
                 info[r][2] = t
                 remaining[r] -= 1
                 emit[r].append(tnow)
+                self.tokens[r].append(t)
             for what, task in self.machine.complete_iteration(batch, mnow):
                 if what == "request_finished":
                     kv.release(info[task.request_id][0])
@@ -795,7 +798,8 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
     if router is not None:
         router.join()
     payload = {"rank": rank, "prompt": is_prompt, "out": None if is_prompt else out[0],
-               "steps": None if is_prompt else out[1], "first": None if is_prompt else out[2]}
+               "steps": None if is_prompt else out[1], "first": None if is_prompt else out[2],
+               "tokens": None if is_prompt else server.tokens}
     gathered = [None] * world
     dist.all_gather_object(gathered, payload, group=ctrl)
     if rank == 0:
@@ -803,6 +807,7 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
         first = {}
         emits = {}
         steps = []
+        gen_tokens = {}
         for gp in gathered:
             if gp["rank"] % tp:          # TP peers report the same requests
                 continue
@@ -810,6 +815,7 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
                 first.update(gp["first"])       # the token host saw the first token land
                 emits.update(gp["out"])
                 steps += gp["steps"]
+                gen_tokens.update(gp["tokens"])
         ttft, tbt, e2e = [], [], []
         ntok = 0
         t_end = 0.0
@@ -849,6 +855,9 @@ def _trace_phase(args, rank, world, local, pair, is_prompt, server, cfg, ctrl, C
             "roofline": _decode_roofline(cfg, tp, steps, hbm_peak, peak_kind),
             "clocks": clk.summary(),
         }
+        if getattr(args, "dump_tokens", None):
+            with open(args.dump_tokens, "w") as f:
+                json.dump({str(k): v for k, v in gen_tokens.items()}, f)
         print(json.dumps(line), flush=True)
     dist.barrier()
     torch.cuda.synchronize()

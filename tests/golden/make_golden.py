@@ -215,7 +215,8 @@ def gen_csv(engine, cluster, perf, trace):
 
 TRACE_POINTS = ([(pr, rate, dur, 0) for pr in ("conversation", "coding")
                  for rate in (1.0, 2.0, 4.0, 8.0, 16.0, 24.0) for dur in (15.0, 20.0, 60.0)]
-                + [("conversation", 20.0, 1.0, 5)])
+                + [("conversation", 20.0, 1.0, 5), ("conversation", 20.0, 2.0, 0),
+                   ("conversation", 40.0, 2.0, 0)])
 
 
 def gen_traces(trace):

@@ -209,23 +209,48 @@ def test_tp4_pool_matches_tp1(model):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_realtime_trace_serving_one_pair():
+def test_realtime_trace_serving_one_pair(tmp_path):
     """bench.py --trace: a Splitwise pair (2 processes) serves a short
-    reference-preset trace in real time; every request completes and the
-    JSON line carries TTFT / TBT percentiles."""
+    reference-preset trace in real time; every request completes, the JSON
+    line carries TTFT / TBT percentiles, and the tokens generated through
+    the cross-process push + device hand-off + continuous batching are the
+    fp32 oracle's greedy tokens wherever its top-2 margin is decisive."""
     import json
     import subprocess
     port = _free_port()
+    dump = str(tmp_path / "tokens.json")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
                         os.path.join(ROOT, "bench.py"), "--gpus", "2", "--model", "tiny",
                         "--warmup", "1", "--prompt", "128", "--out", "8", "--trace",
-                        "conversation", "--rate", "20", "--duration", "2", "--max-output", "24"],
+                        "conversation", "--rate", "20", "--duration", "2", "--max-output", "24",
+                        "--dump-tokens", dump],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["requests"] > 10 and line["ttft_ms"]["p50"] > 0 and line["tbt_ms"]["p99"] > 0
     assert line["output_tokens"] >= line["requests"]
+    # the same trace and prompts bench.py built (reference generator, seed 77 prompts)
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from oracle.decoder import OracleDecoder
+    from paper_2311_18677_b200.model import get_config, init_weights
+    from reftrace import preset_trace
+    reqs = preset_trace("conversation", 20.0, 2.0, 0)
+    cfg = get_config("tiny")
+    g = torch.Generator().manual_seed(77)
+    prompts = {q.id: torch.randint(0, cfg.vocab, (q.prompt_tokens,), generator=g,
+                                   dtype=torch.int32) for q in reqs}
+    got = {int(k): v for k, v in json.load(open(dump)).items()}
+    assert len(got) == len(reqs)
+    orc = OracleDecoder.from_weights(init_weights(cfg, seed=0))
+    for q in sorted(reqs, key=lambda q: q.prompt_tokens)[:4]:
+        toks = got[q.id]
+        assert len(toks) == min(q.output_tokens, 24)
+        ref_toks, ref_logits = orc.generate(prompts[q.id].tolist(), len(toks), forced=toks[:-1])
+        top2 = ref_logits.topk(2, -1).values
+        for i, dec in enumerate(((top2[:, 0] - top2[:, 1]) > 0.02).tolist()):
+            if dec:
+                assert toks[i] == ref_toks[i], (q.id, i)
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")

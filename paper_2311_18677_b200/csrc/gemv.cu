@@ -261,24 +261,29 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
             else {
               const float o = epi == SWB_EPI_F32 ? v : resid[idx] + v;
               reinterpret_cast<float*>(out)[idx] = o;
-              // fused TP all-reduce: the partial goes straight to every peer
-              // (posted NVLink stores) while the weights still stream
-              for (int p = 0; p < tpp.world; ++p)
-                if (p != tpp.rank) tpp.rx[p][idx] = o;
             }
           }
         }
       }
+      if (tpp.world > 1) {
+        // fused TP all-reduce (one decode row): the item's 4 consecutive
+        // outputs go straight to every peer as one 16-byte posted NVLink
+        // store while the weights of later items still stream
+        __syncwarp();
+        if (lane == 0 && 4 * item + 3 < N) {
+          const float4 v4 = reinterpret_cast<const float4*>(out)[item];
+          for (int p = 0; p < tpp.world; ++p)
+            if (p != tpp.rank) reinterpret_cast<float4*>(tpp.rx[p])[item] = v4;
+        }
+      }
     }
   }
-  if (tpp.world > 1 && warp == 0) {
+  if (tpp.world > 1 && warp == 0 && lane == 0) {
     // every partial this CTA pushed is visible system-wide before its
     // completion count reaches the peers
     __threadfence_system();
-    __syncwarp();
-    if (lane == 0)
-      for (int p = 0; p < tpp.world; ++p)
-        if (p != tpp.rank) red_release_sys_add(tpp.cnt[p], 1u);
+    for (int p = 0; p < tpp.world; ++p)
+      if (p != tpp.rank) red_release_sys_add(tpp.cnt[p], 1u);
   }
 }
 
@@ -701,8 +706,8 @@ extern "C" int swb_gemv_bf16_tp(const void* x, const void* w, const void* resid,
   SWB_REQUIRE(M == 1, "swb_gemv_bf16_tp: one row (decode B=1) only, got M=%d", M);
   SWB_REQUIRE(epilogue == SWB_EPI_F32 || epilogue == SWB_EPI_RESID_F32,
               "swb_gemv_bf16_tp: fp32 epilogues only");
-  SWB_REQUIRE((size_t)N * 4 <= (size_t)(1 << 20), "swb_gemv_bf16_tp: N=%d exceeds the receive "
-              "buffers", N);
+  SWB_REQUIRE((size_t)N * 4 <= (size_t)(1 << 20) && N % 4 == 0,
+              "swb_gemv_bf16_tp: N=%d must be a multiple of 4 within the receive buffers", N);
   const int items = (N + TV_ROWS - 1) / TV_ROWS;
   return launch_gemv<1, false>(x, nullptr, 0.f, reinterpret_cast<const __nv_bfloat16*>(w), out,
                                reinterpret_cast<const float*>(resid),

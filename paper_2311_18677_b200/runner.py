@@ -91,9 +91,11 @@ class ModelRunner:
         self.alibi = weights.alibi
         self.tp_max_rows = tp_max_rows    # largest prefill / decode row count reduced
         self.ar_nccl_bytes = int(os.environ.get("SWB_TP_AR_NCCL_BYTES", str(4 << 20)))
-        # SWB_TP_FUSED=0: decode B=1 projections write their TP slot and a
-        # separate kernel pushes it (A/B of the fused GEMV -> all-reduce push)
-        self.tp_fused = os.environ.get("SWB_TP_FUSED", "1") != "0"
+        # SWB_TP_FUSED=1: decode B=1 projections push their partial to the
+        # peers from the GEMV epilogue (swb_gemv_bf16_tp) and a receive kernel
+        # only waits and sums.  Exact (tests/test_tpcomm_gpu.py) but measured
+        # slower (70B TP4 B=1 decode 12.95 vs 8.51 ms/step), so off by default
+        self.tp_fused = os.environ.get("SWB_TP_FUSED", "0") == "1"
         self.kv = kv
         self.hq = cfg.n_heads // self.tp
         self.hkv = cfg.n_kv_heads // self.tp

@@ -663,6 +663,11 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
                           const float* __restrict__ alibi, int H, int Hkv, float scale_log2,
                           __nv_bfloat16* __restrict__ out, int trig) {
   constexpr int DCL_THREADS = (DCL_CW + 1) * 32;
+  // GQA groups (G > 2): the consumer warps split the group's HEADS (GW each)
+  // and every warp walks every page, instead of splitting the pages
+  constexpr bool HS = G > 2;
+  constexpr int GW = HS ? G / DCL_CW : G;
+  static_assert(!HS || G % DCL_CW == 0, "head split needs G % warps == 0");
   extern __shared__ __align__(128) uint8_t dsm_raw[];
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(dsm_raw);         // [S][K|V][PAGE]
   float* wst = reinterpret_cast<float*>(ring + (size_t)DCL_S * 2 * DCL_PAGE);  // [CW][G][ST]
@@ -675,7 +680,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
 #pragma unroll
     for (int i = 0; i < DCL_S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], HS ? DCL_CW : 1);
     }
     fence_barrier_init();
   }
@@ -716,11 +721,12 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
     const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
     const float fpos = (float)cur;
     // lane hl holds dims [4hl, 4hl+4) and [64+4hl, 64+4hl+4): its RoPE pairs
-    float q[G][8];
-    float sl[G];
+    const int g0 = HS ? warp * GW : 0;         // first head of this warp
+    float q[GW][8];
+    float sl[GW];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const __nv_bfloat16* hp = qrow + (size_t)(kh * G + g) * DA_D;
+    for (int g = 0; g < GW; ++g) {
+      const __nv_bfloat16* hp = qrow + (size_t)(kh * G + g0 + g) * DA_D;
       const uint2 ql = *reinterpret_cast<const uint2*>(hp + 4 * hl);
       const uint2 qh = *reinterpret_cast<const uint2*>(hp + 64 + 4 * hl);
       const float2 l0 = bf2_to_f2(ql.x), l1 = bf2_to_f2(ql.y);
@@ -739,12 +745,13 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
         q[g][j] = lo[j] * scale_log2;
         q[g][4 + j] = hi[j] * scale_log2;
       }
-      sl[g] = alibi ? alibi[kh * G + g] * 1.4426950408889634f : 0.f;
+      sl[g] = alibi ? alibi[kh * G + g0 + g] * 1.4426950408889634f : 0.f;
     }
     // the current token: its page's owner warp RoPEs k, appends k/v to the
     // pool (half 0: k, half 1: v) and keeps the rows to patch the staged page
     const int cpg = cur >> 4;
-    const bool own = cpg >= pg0 && cpg < pg0 + nmy && ((cpg - pg0) % DCL_CW) == warp;
+    const bool has_cur = cpg >= pg0 && cpg < pg0 + nmy;
+    const bool own = has_cur && (HS ? warp == 0 : ((cpg - pg0) % DCL_CW) == warp);
     uint2 cur_lo = make_uint2(0, 0), cur_hi = make_uint2(0, 0);
     if (own) {
       const __nv_bfloat16* src = qrow + (size_t)(half == 0 ? H + kh : H + Hkv + kh) * DA_D;
@@ -767,27 +774,32 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
       *reinterpret_cast<uint2*>(pool + gdst + 4 * hl) = cur_lo;
       *reinterpret_cast<uint2*>(pool + gdst + 64 + 4 * hl) = cur_hi;
     }
-    float m[G], l[G], o[G][4];
+    float m[GW], l[GW], o[GW][4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
+    for (int g = 0; g < GW; ++g) {
       m[g] = -INFINITY;
       l[g] = 0.f;
       o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
     }
-    for (int i = warp; i < nmy; i += DCL_CW) {
+    for (int i = HS ? 0 : warp; i < nmy; i += HS ? 1 : DCL_CW) {
       const int st = i % DCL_S;
       mbar_wait(&full[st], (i / DCL_S) & 1);
       __nv_bfloat16* ks = ring + (size_t)(2 * st) * DCL_PAGE;
       __nv_bfloat16* vs = ks + DCL_PAGE;
       const int t0 = (pg0 + i) * 16;
-      if (own && pg0 + i == cpg) {               // patch the current token's rows
-        __nv_bfloat16* row = (half == 0 ? ks : vs) + (cur - t0) * DA_D;
-        *reinterpret_cast<uint2*>(row + 4 * hl) = cur_lo;
-        *reinterpret_cast<uint2*>(row + 64 + 4 * hl) = cur_hi;
-        __syncwarp();
+      if (pg0 + i == cpg) {                      // patch the current token's rows
+        if (own) {
+          __nv_bfloat16* row = (half == 0 ? ks : vs) + (cur - t0) * DA_D;
+          *reinterpret_cast<uint2*>(row + 4 * hl) = cur_lo;
+          *reinterpret_cast<uint2*>(row + 64 + 4 * hl) = cur_hi;
+        }
+        if constexpr (HS)      // every consumer warp reads this page: wait for the patch
+          asm volatile("bar.sync 1, %0;" ::"n"(DCL_CW * 32) : "memory");
+        else
+          __syncwarp();
       }
       const int valid = min(16, L - t0);
-      float sc[G][8];
+      float sc[GW][8];
 #pragma unroll
       for (int it = 0; it < 8; ++it) {          // token 2*it + half
         const int t = 2 * it + half;
@@ -798,7 +810,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
         const float2 c0 = bf2_to_f2(c.x), c1 = bf2_to_f2(c.y);
         const float kf[8] = {a0.x, a0.y, a1.x, a1.y, c0.x, c0.y, c1.x, c1.y};
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
+        for (int g = 0; g < GW; ++g) {
           float d = q[g][0] * kf[0];
 #pragma unroll
           for (int j = 1; j < 8; ++j) d = fmaf(q[g][j], kf[j], d);
@@ -806,7 +818,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
         }
       }
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
+      for (int g = 0; g < GW; ++g) {
 #pragma unroll
         for (int sh = 8; sh > 0; sh >>= 1)
 #pragma unroll
@@ -839,7 +851,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
         const uint2 vv = *reinterpret_cast<const uint2*>(vs + t * DA_D + 4 * lane);
         const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
+        for (int g = 0; g < GW; ++g) {
           const float pt = __shfl_sync(0xffffffffu, sc[g][t >> 1], (t & 1) * 16);
           o[g][0] = fmaf(pt, v0.x, o[g][0]);
           o[g][1] = fmaf(pt, v0.y, o[g][1]);
@@ -851,12 +863,23 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
       if (lane == 0) mbar_arrive(&empty[st]);
     }
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float* w = wst + ((size_t)warp * G + g) * DCL_ST;
-      *reinterpret_cast<float4*>(w + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+    for (int gg = 0; gg < G; ++gg) {          // heads this warp does not own: empty
+      const int g = gg - g0;
+      const bool mine = g >= 0 && g < GW;
+      float* w = wst + ((size_t)warp * G + gg) * DCL_ST;
+      float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      float mv = -INFINITY, lv = 0.f;
+#pragma unroll
+      for (int h = 0; h < GW; ++h)
+        if (h == g) {
+          v4 = make_float4(o[h][0], o[h][1], o[h][2], o[h][3]);
+          mv = m[h];
+          lv = l[h];
+        }
+      *reinterpret_cast<float4*>(w + 4 * lane) = v4;
       if (lane == 0) {
-        w[DA_D] = m[g];
-        w[DA_D + 1] = l[g];
+        w[DA_D] = mine ? mv : -INFINITY;
+        w[DA_D + 1] = mine ? lv : 0.f;
       }
     }
   }
@@ -1583,12 +1606,18 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     const char* m = std::getenv("SWB_ATTN_CL_MAXB");
     return m ? std::atoi(m) : 16;
   }();
-  // GQA groups (G >= 4) stay on the tensor-core split-K kernel below: the
-  // CUDA-core cluster kernel with 8 heads per pass is FMA/shuffle-bound
-  // (measured 70B-TP2 B=1 ctx 1100: 24.1 vs 12.8 us; 70B TP4 decode step
-  // 9.93 vs 8.42 ms)
-  if (STEP && G <= 2 && block_size == 16 && B <= cl_maxb) {
-    const int gi = G - 1;
+  // GQA groups (G = 4, 8) at small batch (B <= SWB_ATTN_CL_MAXB_GQA): the
+  // consumer warps split the group's heads (G/4 each) and all walk every
+  // page.  (Splitting pages instead, every warp carrying 8 heads, was
+  // FMA/shuffle-bound: 70B-TP2 B=1 ctx 1100 24.1 vs 12.8 us for the MMA
+  // kernel.)
+  static const int cl_maxb_gqa = [] {
+    const char* e = std::getenv("SWB_ATTN_CL_MAXB_GQA");
+    return e ? std::atoi(e) : 2;
+  }();
+  const int gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : -1;
+  if (STEP && gi >= 0 && block_size == 16 &&
+      B <= (G <= 2 ? cl_maxb : std::min(cl_maxb, cl_maxb_gqa))) {
     // cluster x consumer-warp shape: SWB_ATTN_CL_CFG = "8x4" | "8x8" | "16x4" | "16x8";
     // ring depth: SWB_ATTN_CL_S = 8 (default) | 12
     static const int cfg_id = [] {
@@ -1603,7 +1632,7 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
       const char* e = std::getenv("SWB_ATTN_CL_S");
       return e ? std::atoi(e) : 0;
     }();
-    const int CL = cfg_id >= 2 ? 16 : 8, CW = (cfg_id & 1) ? 8 : 4;
+    const int CL = cfg_id >= 2 ? 16 : 8, CW = ((cfg_id & 1) && G <= 2) ? 8 : 4;
     const int pages_per_cta = ((max_ctx + 15) / 16 + CL - 1) / CL;
     // 12 stages prefetch a 1100-token context whole before the PDL wait (7B
     // B=1 standalone 6.7 -> 6.0 us) but at 2 CTAs/SM the step loses (2.51 ->
@@ -1616,12 +1645,18 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
                          float, __nv_bfloat16*, int);
 #define SWB_CLK(g, s) {attn_decode_cl_kernel<g, 8, 4, s>, attn_decode_cl_kernel<g, 8, 8, s>, \
                        attn_decode_cl_kernel<g, 16, 4, s>, attn_decode_cl_kernel<g, 16, 8, s>}
-    static const KFn table[2][2][4] = {{SWB_CLK(1, 8), SWB_CLK(1, 12)},
-                                       {SWB_CLK(2, 8), SWB_CLK(2, 12)}};
+#define SWB_CLK4(g, s) {attn_decode_cl_kernel<g, 8, 4, s>, attn_decode_cl_kernel<g, 8, 4, s>, \
+                        attn_decode_cl_kernel<g, 16, 4, s>, attn_decode_cl_kernel<g, 16, 4, s>}
+    // GQA (head split across the 4 consumer warps): 4 warps in every shape
+    static const KFn table[4][2][4] = {{SWB_CLK(1, 8), SWB_CLK(1, 12)},
+                                       {SWB_CLK(2, 8), SWB_CLK(2, 12)},
+                                       {SWB_CLK4(4, 8), SWB_CLK4(4, 12)},
+                                       {SWB_CLK4(8, 8), SWB_CLK4(8, 12)}};
+#undef SWB_CLK4
 #undef SWB_CLK
     const KFn kern = table[gi][si][cfg_id];
     const size_t smem_c = dcl_smem(G, CW, S);
-    static bool attr_c[64][16] = {};
+    static bool attr_c[64][32] = {};
     const int ai = gi * 8 + si * 4 + cfg_id;
     if (dev < 64 && !attr_c[dev][ai]) {
       SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -638,9 +638,10 @@ __global__ void __launch_bounds__(NW * 32)
 // consumer warps each own every DCL_CW-th page with an online softmax of
 // their own — no block-wide barrier until the end, so a warp computes as
 // soon as ITS page landed.  Warps combine through shared memory and the
-// cluster's CTAs through distributed shared memory (rank 0 reads its peers'
-// (m, l, o) with ld.shared::cluster, fixed order): no global partials, no
-// atomic ticket, no system fences.  The current token (position ctx) is
+// cluster's CTAs through distributed shared memory (every CTA stores its
+// (m, l, o) into rank 0's inbox with st.shared::cluster and arrives on rank
+// 0's merge barrier, then exits; rank 0 merges in fixed order): no global
+// partials, no atomic ticket, no system fences.  The current token (position ctx) is
 // RoPE'd and appended to the pool by the warp owning its page, which patches
 // the staged page row from registers.
 // Template: G query heads per kv head, DCL_CL CTAs per cluster (8 portable,
@@ -648,8 +649,8 @@ __global__ void __launch_bounds__(NW * 32)
 constexpr int DCL_PAGE = 16 * DA_D;   // elements of one (block, head) page
 constexpr int DCL_ST = DA_D + 4;      // floats per (o[128], m, l) record (16-byte aligned)
 
-__host__ __device__ constexpr size_t dcl_smem(int G, int CW, int S) {
-  return (size_t)S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(CW + 1) * G * DCL_ST;
+__host__ __device__ constexpr size_t dcl_smem(int G, int CW, int S, int CL) {
+  return (size_t)S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(CW + CL) * G * DCL_ST;
 }
 
 // DCL_S: ring stages (one page of K and V each); all of a CTA's pages are
@@ -671,8 +672,9 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
   extern __shared__ __align__(128) uint8_t dsm_raw[];
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(dsm_raw);         // [S][K|V][PAGE]
   float* wst = reinterpret_cast<float*>(ring + (size_t)DCL_S * 2 * DCL_PAGE);  // [CW][G][ST]
-  float* res = wst + DCL_CW * G * DCL_ST;                                       // [G][ST]
+  float* inbox = wst + DCL_CW * G * DCL_ST;         // rank 0: [CL][G][ST] records of the CTAs
   __shared__ uint64_t full[DCL_S], empty[DCL_S];
+  __shared__ uint64_t merge_bar;
   const int r = blockIdx.x;             // cluster rank (cluster (DCL_CL,1,1), gridDim.x == DCL_CL)
   const int kh = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -682,9 +684,11 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], HS ? DCL_CW : 1);
     }
+    mbar_init(&merge_bar, DCL_CL - 1);
     fence_barrier_init();
   }
   __syncthreads();
+  cluster_arrive_relaxed();            // matched by cluster_wait() before the record push
   const int32_t* trow = tables + (size_t)b * max_blocks;
   const int cur = __ldg(ctx_lens + b);      // written >= 2 launches back (decode_advance)
   const int L = cur + 1;                     // attention length incl. the current token
@@ -884,7 +888,11 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
     }
   }
   __syncthreads();
-  // ---- combine the consumer warps (fixed order) into this CTA's record
+  // ---- combine the consumer warps (fixed order) into this CTA's record and
+  // PUSH it into rank 0's inbox (st.shared::cluster); one release arrive on
+  // rank 0's merge barrier per CTA, then non-zero ranks exit at once
+  cluster_wait();                      // rank 0's merge barrier is initialised
+  const uint32_t inbox_local = smem_u32(inbox);
   for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
     const int g = idx / DA_D, d = idx % DA_D;
     float M = -INFINITY;
@@ -898,52 +906,54 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
       O = fmaf(f, ww[d], O);
       Ls = fmaf(f, ww[DA_D + 1], Ls);
     }
-    res[g * DCL_ST + d] = O;
-    if (d == 0) {
-      res[g * DCL_ST + DA_D] = M;
-      res[g * DCL_ST + DA_D + 1] = Ls;
+    const uint32_t dst = inbox_local + (uint32_t)(((r * G + g) * DCL_ST + d) * 4);
+    if (r == 0) {
+      inbox[(g * DCL_ST) + d] = O;
+      if (d == 0) {
+        inbox[g * DCL_ST + DA_D] = M;
+        inbox[g * DCL_ST + DA_D + 1] = Ls;
+      }
+    } else {
+      const uint32_t rd = mapa(dst, 0);
+      st_dsmem(rd, O);
+      if (d == 0) {
+        st_dsmem(rd + (DA_D - d) * 4, M);
+        st_dsmem(rd + (DA_D + 1 - d) * 4, Ls);
+      }
     }
   }
-  cluster_sync_all();                  // every CTA's record is in its shared memory
-  if (r == 0) {
-    // per head: the peers' (m, l) once -> merge factors, then o element-wise
-    __shared__ float fac[DCL_CL * G];
-    __shared__ float ltot[G];
-    const uint32_t res_local = smem_u32(res);
-    for (int g = threadIdx.x; g < G; g += DCL_THREADS) {
-      float mp[DCL_CL], lp[DCL_CL];
-#pragma unroll
-      for (int p = 0; p < DCL_CL; ++p) {
-        const uint32_t base = mapa(res_local, p) + (uint32_t)(g * DCL_ST) * 4u;
-        mp[p] = ld_dsmem(base + DA_D * 4);
-        lp[p] = ld_dsmem(base + (DA_D + 1) * 4);
-      }
-      float M = -INFINITY;
-#pragma unroll
-      for (int p = 0; p < DCL_CL; ++p) M = fmaxf(M, mp[p]);
-      float Ls = 0.f;
-#pragma unroll
-      for (int p = 0; p < DCL_CL; ++p) {
-        const float f = mp[p] == -INFINITY ? 0.f : exp2f(mp[p] - M);
-        fac[p * G + g] = f;
-        Ls = fmaf(f, lp[p], Ls);
-      }
-      ltot[g] = Ls;
-    }
+  if (r != 0) {
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
     __syncthreads();
-    for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
-      const int g = idx / DA_D, d = idx % DA_D;
-      float op[DCL_CL];
-#pragma unroll
-      for (int p = 0; p < DCL_CL; ++p)
-        op[p] = ld_dsmem(mapa(res_local, p) + (uint32_t)(g * DCL_ST + d) * 4u);
-      float O = 0.f;
-#pragma unroll
-      for (int p = 0; p < DCL_CL; ++p) O = fmaf(fac[p * G + g], op[p], O);
-      out[((size_t)b * H + kh * G + g) * DA_D + d] = __float2bfloat16(O / ltot[g]);
-    }
+    if (threadIdx.x == 0) mbar_arrive_remote(mapa(smem_u32(&merge_bar), 0));
+    return;
   }
-  cluster_sync_all();                  // peers keep their shared memory until rank 0 read it
+  __syncthreads();
+  mbar_wait_cluster(&merge_bar, 0);    // every peer's record landed in the inbox
+  __shared__ float fac[DCL_CL * G];
+  __shared__ float ltot[G];
+  for (int g = threadIdx.x; g < G; g += DCL_THREADS) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int p = 0; p < DCL_CL; ++p) M = fmaxf(M, inbox[(p * G + g) * DCL_ST + DA_D]);
+    float Ls = 0.f;
+#pragma unroll
+    for (int p = 0; p < DCL_CL; ++p) {
+      const float mp = inbox[(p * G + g) * DCL_ST + DA_D];
+      const float f = mp == -INFINITY ? 0.f : exp2f(mp - M);
+      fac[p * G + g] = f;
+      Ls = fmaf(f, inbox[(p * G + g) * DCL_ST + DA_D + 1], Ls);
+    }
+    ltot[g] = Ls;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
+    const int g = idx / DA_D, d = idx % DA_D;
+    float O = 0.f;
+#pragma unroll
+    for (int p = 0; p < DCL_CL; ++p) O = fmaf(fac[p * G + g], inbox[(p * G + g) * DCL_ST + d], O);
+    out[((size_t)b * H + kh * G + g) * DA_D + d] = __float2bfloat16(O / ltot[g]);
+  }
 }
 
 // ---------------------------------------------------------------- decode, MMA
@@ -1655,7 +1665,7 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
 #undef SWB_CLK4
 #undef SWB_CLK
     const KFn kern = table[gi][si][cfg_id];
-    const size_t smem_c = dcl_smem(G, CW, S);
+    const size_t smem_c = dcl_smem(G, CW, S, CL);
     static bool attr_c[64][32] = {};
     const int ai = gi * 8 + si * 4 + cfg_id;
     if (dev < 64 && !attr_c[dev][ai]) {

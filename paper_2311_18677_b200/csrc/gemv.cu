@@ -645,6 +645,16 @@ static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, cons
   // (The mma.sync kernel's two-MMA variant for M = 9..16 showed sporadic
   // wrong columns under a repeat test and is not dispatched.)  Pre-norm fused
   // variants: M = 2..8 on the mma.sync kernel with h staged in shared memory.
+  // SWB_GEMV_CORE_MAXM=m: rows M <= m stay on the CUDA-core bulk kernel (A/B)
+  static const int core_maxm = [] {
+    const char* e = std::getenv("SWB_GEMV_CORE_MAXM");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (M >= 2 && M <= core_maxm && M <= 4 && (!NORM || (size_t)M * K * 2 <= (size_t)TV_HS_MAX)) {
+    if (M <= 2)
+      return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
+    return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
+  }
   if (NORM && M >= 2)
     return launch_gemv_mma<1, true>(x, nw, eps, w, out, rs, bias, M, N, K, epilogue, s);
   // K >= 12288 (BLOOM-176B TP4 qkv/up/down, 70B TP2 down): its 16-row x K

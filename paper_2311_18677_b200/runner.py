@@ -21,6 +21,7 @@ advance) is captured once in a CUDA graph and replayed; all per-step state
 
 from __future__ import annotations
 
+import gc
 import math
 import os
 from dataclasses import dataclass, field
@@ -759,11 +760,21 @@ class DecodeGraph:
             t.copy_(v)
         g = torch.cuda.CUDAGraph()
         n0 = _abi.launch_count()
+        # a garbage-collected KV pool / TP communicator frees device memory
+        # (cudaFree), which is illegal while a stream captures and would
+        # invalidate the capture: collect now, and not during the capture
+        gc.collect()
+        gc_was = gc.isenabled()
+        gc.disable()
         # explicit capture stream on this runner's device: torch.cuda.graph's
         # default capture stream is created once, on whichever device was
         # current then, and would bind a second GPU's graph to the first GPU
-        with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.r.dev)):
-            self._step_body()
+        try:
+            with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.r.dev)):
+                self._step_body()
+        finally:
+            if gc_was:
+                gc.enable()
         if self.r.tp_comm is not None:
             self.r.tp_comm.assert_even()
         self.launches_per_step = _abi.launch_count() - n0

@@ -1616,14 +1616,16 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     const char* m = std::getenv("SWB_ATTN_CL_MAXB");
     return m ? std::atoi(m) : 16;
   }();
-  // GQA groups (G = 4, 8) at small batch (B <= SWB_ATTN_CL_MAXB_GQA): the
+  // GQA groups (G = 4, 8) only with SWB_ATTN_CL_MAXB_GQA > 0 (A/B): the
   // consumer warps split the group's heads (G/4 each) and all walk every
-  // page.  (Splitting pages instead, every warp carrying 8 heads, was
-  // FMA/shuffle-bound: 70B-TP2 B=1 ctx 1100 24.1 vs 12.8 us for the MMA
-  // kernel.)
+  // page; CUDA-core dot products for 8 heads per page do not beat the
+  // tensor-core split-K kernel.  (Splitting pages instead, every warp
+  // carrying 8 heads, was FMA/shuffle-bound: 24.1 vs 12.8 us.)
+  // measured (head split, B=1): 70B-TP2 ctx 1100 12.7 vs 12.4 us, ctx 8000
+  // 58 vs 25 us, 70B TP4 step unchanged (8.48 ms) — so off by default
   static const int cl_maxb_gqa = [] {
     const char* e = std::getenv("SWB_ATTN_CL_MAXB_GQA");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 0;
   }();
   const int gi = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : -1;
   if (STEP && gi >= 0 && block_size == 16 &&

@@ -378,8 +378,9 @@ def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
     (16, 16, True, [31, 1500]), (32, 32, False, [8190]), (64, 8, False, [3, 1100]),
     (16, 4, True, [500])])
 def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached):
-    """Decode-graph attention — the cluster-streaming kernel for G = 1, 2, the
-    tensor-core split-K kernel for G = 4, 8 —
+    """Decode-graph attention — the cluster-streaming kernel for G = 1, 2 (and
+    its head-split GQA mode, forced on here), the tensor-core split-K kernel
+    for G = 4, 8 by default —
     against a plain torch fp32 attention over the gathered pages: the current
     token (position = ctx) is RoPE'd (or ALiBi-biased), appended to its
     block-table slot, and attends over positions 0..ctx; contexts from 1 token

@@ -1623,7 +1623,7 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
   // carrying 8 heads, was FMA/shuffle-bound: 24.1 vs 12.8 us.)
   // measured (head split, B=1): 70B-TP2 ctx 1100 12.7 vs 12.4 us, ctx 8000
   // 58 vs 25 us, 70B TP4 step unchanged (8.48 ms) — so off by default
-  static const int cl_maxb_gqa = [] {
+  const int cl_maxb_gqa = [] {            // read per call: tests switch it
     const char* e = std::getenv("SWB_ATTN_CL_MAXB_GQA");
     return e ? std::atoi(e) : 0;
   }();

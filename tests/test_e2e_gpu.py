@@ -59,8 +59,11 @@ def _run_colocated(cfg, runner, kv, prompt, n_out, return_logits=True):
     return seq, out, torch.stack(logits).cpu()
 
 
-# max |dlogit| / max |logit| allowed (C1 tiny, BLOOM-architecture tiny)
-TOL_REL = {"tiny": 0.02, "bloom-tiny": 0.02}
+# max |dlogit| / max |logit| allowed: 3x the B200 observation (tiny 0.19 %,
+# bloom-tiny 0.051 %), and at most 1.5x the bf16-storage twin's error
+# (observed ratio 1.09 / 1.04) — gpurun_out/parity_tiny.json
+TOL_REL = {"tiny": 0.006, "bloom-tiny": 0.0016}
+EMUL_FACTOR = 1.5
 
 
 def _record(name, rec):
@@ -101,6 +104,7 @@ def test_tiny_colocated_vs_oracle(model):
                     "max_logit": float(scale.max()), "tol": tol})
     print(f"max logit diff {diff.max():.4f} (bf16 twin {emul:.4f}), scale {scale.max():.3f}")
     assert float(diff.max()) <= tol, (diff.max(), scale.max())
+    assert float(diff.max()) <= EMUL_FACTOR * emul, (diff.max(), emul)
     top2 = ref_logits.topk(2, -1).values
     margin = top2[:, 0] - top2[:, 1]
     decisive = margin > 2 * diff            # cannot flip by the observed rounding

@@ -377,7 +377,7 @@ def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
     (32, 32, False, [0, 15, 16, 130, 1000, 2047]), (8, 4, False, [3, 700]),
     (16, 16, True, [31, 1500]), (32, 32, False, [8190]), (64, 8, False, [3, 1100]),
     (16, 4, True, [500])])
-def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached):
+def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached, monkeypatch):
     """Decode-graph attention — the cluster-streaming kernel for G = 1, 2 (and
     its head-split GQA mode, forced on here), the tensor-core split-K kernel
     for G = 4, 8 by default —
@@ -386,6 +386,7 @@ def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached):
     block-table slot, and attends over positions 0..ctx; contexts from 1 token
     to 8191 (every CTA of the 8-CTA cluster empty, partial or full)."""
     from oracle.decoder import apply_rope, rope_tables
+    monkeypatch.setenv("SWB_ATTN_CL_MAXB_GQA", "2")
     dh, bs, B = 128, 16, len(cached)
     maxb = (max(cached) + 1 + bs - 1) // bs + 1
     nblk = B * maxb + 8

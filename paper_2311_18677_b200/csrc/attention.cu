@@ -969,7 +969,10 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
 constexpr int DM_WARPS = 4, DM_PT = 128, DM_WT = 32, DM_QS = DA_D + 8;
 constexpr int DC_MAXQT = 512;     // chunked prefill: up to 8192 query rows per chunk
 
-template <bool STEP, int WT>   // WT = tokens per warp (32: partition 128, 16: 64)
+// CLN > 0: the NP = CLN partitions of a (b, kv head) form one thread-block
+// cluster and merge through rank 0's shared-memory inbox (push-merge, as the
+// cluster-streaming kernel does) instead of global partials + ticket.
+template <bool STEP, int WT, int CLN = 0>   // WT = tokens per warp (32: partition 128, 16: 64)
 __global__ void __launch_bounds__(DM_WARPS * 32)
     attn_decode_mma_kernel(const __nv_bfloat16* __restrict__ qkv, int rs,
                            __nv_bfloat16* __restrict__ kpool, __nv_bfloat16* __restrict__ vpool,
@@ -987,7 +990,10 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
   __nv_bfloat16* sq = sv + PT * DA_D;                               // [16][DM_QS]
   float* sml = reinterpret_cast<float*>(sq + 16 * DM_QS);              // [4][8][2]
   float* so = sml + DM_WARPS * 8 * 2;                                  // [4][G][128]
+  float* inbox = so + DM_WARPS * (H / Hkv) * DA_D;         // CLN: rank 0 [CLN][G][DCL_ST]
+  float* rec = inbox + CLN * (H / Hkv) * DCL_ST;           // CLN: this CTA's [G][DA_D + 2]
   __shared__ uint64_t kbar[DM_WARPS], vbar[DM_WARPS];
+  __shared__ uint64_t merge_bar;
   __shared__ int s_last;
   __shared__ __align__(16) __nv_bfloat16 scur[2][DA_D];
   const int p = blockIdx.x, kh = blockIdx.y, b = blockIdx.z;
@@ -1003,9 +1009,11 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       mbar_init(&kbar[i], 1);
       mbar_init(&vbar[i], 1);
     }
+    if constexpr (CLN > 0) mbar_init(&merge_bar, CLN - 1);
     fence_barrier_init();
   }
   __syncthreads();
+  if constexpr (CLN > 0) cluster_arrive_relaxed();   // matched before the record push
   const int32_t* trow = tables + (size_t)b * max_blocks;
   int L, cur;
   if constexpr (STEP) {
@@ -1212,8 +1220,16 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
         o += f * so[((size_t)w * G + gi) * DA_D + d];
         l += f * sml[(w * 8 + gi) * 2 + 1];
       }
-      if (NP == 1) {
+      if (CLN == 0 && NP == 1) {
         out[((size_t)b * H + kh * G + gi) * DA_D + d] = __float2bfloat16(o / l);
+        continue;
+      }
+      if constexpr (CLN > 0) {
+        rec[gi * (DA_D + 2) + d] = o;
+        if (d == 0) {
+          rec[gi * (DA_D + 2) + DA_D] = M;
+          rec[gi * (DA_D + 2) + DA_D + 1] = l;
+        }
         continue;
       }
       float* wo = wsp(kh * G + gi, p);
@@ -1223,14 +1239,63 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
         wo[DA_D + 1] = l;
       }
     }
-    if (NP == 1) return;
+    if (CLN == 0 && NP == 1) return;
   } else {
     if (trig) pdl_launch_dependents();
-    if (threadIdx.x < G) {
+    if constexpr (CLN > 0) {
+      for (int i = threadIdx.x; i < G * (DA_D + 2); i += DM_WARPS * 32)
+        rec[i] = (i % (DA_D + 2)) == DA_D ? -INFINITY : 0.f;
+    } else if (threadIdx.x < G) {
       float* w = wsp(kh * G + threadIdx.x, p);
       w[DA_D] = -INFINITY;
       w[DA_D + 1] = 0.f;
     }
+  }
+  if constexpr (CLN > 0) {
+    // ---- push this partition's (o, m, l) into rank 0's inbox, merge there
+    __syncthreads();
+    cluster_wait();
+    const uint32_t inbox_local = smem_u32(inbox);
+    for (int i = threadIdx.x; i < G * (DA_D + 2); i += DM_WARPS * 32) {
+      const int gi = i / (DA_D + 2), d = i % (DA_D + 2);
+      const float v = rec[i];
+      const int slot = (p * G + gi) * DCL_ST + d;
+      if (p == 0)
+        inbox[slot] = v;
+      else
+        st_dsmem(mapa(inbox_local + (uint32_t)slot * 4u, 0), v);
+    }
+    if (p != 0) {
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) mbar_arrive_remote(mapa(smem_u32(&merge_bar), 0));
+      return;
+    }
+    __syncthreads();
+    mbar_wait_cluster(&merge_bar, 0);
+    float* fac = sml;                     // [CLN][G] merge factors (sml is free now)
+    float* ltot = so;                     // [G]
+    if (threadIdx.x < G) {
+      const int gi = threadIdx.x;
+      float Mx = -INFINITY;
+      for (int q = 0; q < CLN; ++q) Mx = fmaxf(Mx, inbox[(q * G + gi) * DCL_ST + DA_D]);
+      float Ls = 0.f;
+      for (int q = 0; q < CLN; ++q) {
+        const float mq = inbox[(q * G + gi) * DCL_ST + DA_D];
+        const float f = mq == -INFINITY ? 0.f : exp2f(mq - Mx);
+        fac[q * G + gi] = f;
+        Ls = fmaf(f, inbox[(q * G + gi) * DCL_ST + DA_D + 1], Ls);
+      }
+      ltot[gi] = Ls;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * DA_D; i += DM_WARPS * 32) {
+      const int gi = i / DA_D, d = i % DA_D;
+      float o = 0.f;
+      for (int q = 0; q < CLN; ++q) o = fmaf(fac[q * G + gi], inbox[(q * G + gi) * DCL_ST + d], o);
+      out[((size_t)b * H + kh * G + gi) * DA_D + d] = __float2bfloat16(o / ltot[gi]);
+    }
+    return;
   }
   // ---- fused split-K merge: the last CTA of (b, kh) combines the partitions
   __threadfence();
@@ -1720,6 +1785,54 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
     const size_t msm = std::max(merge_scratch,
                                 (size_t)2 * partition * DA_D * 2 + 16 * DM_QS * 2 +
                                     sizeof(float) * (DM_WARPS * 8 * 2 + (size_t)DM_WARPS * G * DA_D));
+    // cluster form (decode graph, 128-token partitions): the NP partitions of
+    // a (b, kv head) are one cluster of 8 or 16 CTAs merging through DSMEM —
+    // no global partials / ticket / fences (SWB_ATTN_MMA_CL_MAXB bounds B)
+    const int mcl_maxb = [] {
+      const char* e = std::getenv("SWB_ATTN_MMA_CL_MAXB");
+      return e ? std::atoi(e) : 2;
+    }();
+    if (STEP && partition == 128 && B <= mcl_maxb && NP <= 16) {
+      const int CLN = NP <= 8 ? 8 : 16;
+      auto kern = CLN == 8 ? attn_decode_mma_kernel<STEP, 32, 8> : attn_decode_mma_kernel<STEP, 32, 16>;
+      const size_t csm = (size_t)2 * partition * DA_D * 2 + 16 * DM_QS * 2 +
+                         sizeof(float) * (DM_WARPS * 8 * 2 + (size_t)DM_WARPS * G * DA_D +
+                                          (size_t)CLN * G * DCL_ST + (size_t)G * (DA_D + 2));
+      static bool attr_mc[64][2] = {};
+      if (dev < 64 && !attr_mc[dev][CLN == 16]) {
+        SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      160 * 1024));
+        if (CLN > 8)
+          SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_mc[dev][CLN == 16] = true;
+      }
+      SWB_REQUIRE(csm <= 160 * 1024, "%s: cluster MMA smem", fn);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CLN, Hkv, B);
+      cfg.blockDim = dim3(DM_WARPS * 32);
+      cfg.dynamicSmemBytes = csm;
+      cfg.stream = (cudaStream_t)stream;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CLN;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = pdl_enabled() ? 2 : 1;
+      const cudaError_t lc = cudaLaunchKernelEx(
+          &cfg, kern, reinterpret_cast<const __nv_bfloat16*>(qkv), row_stride,
+          reinterpret_cast<__nv_bfloat16*>(k_layer), reinterpret_cast<__nv_bfloat16*>(v_layer),
+          block_tables, max_blocks, ctx_lens, positions, slots,
+          !alibi_slopes ? log2f(theta) : 0.f, alibi_slopes, H, Hkv,
+          scale * 1.4426950408889634f, ws, tickets, reinterpret_cast<__nv_bfloat16*>(out),
+          pdl_early_trigger() ? 1 : 0);
+      if (lc != cudaSuccess)
+        return swb_set_error(SWB_ERR_CUDA, "launch attn_decode_mma_kernel (cluster): %s",
+                             cudaGetErrorString(lc));
+      return swb_check_launch("attn_decode_mma_kernel");
+    }
     const cudaError_t lm = launch(
         partition == 128 ? attn_decode_mma_kernel<STEP, 32> : attn_decode_mma_kernel<STEP, 16>,
         dim3(NP, Hkv, B), dim3(DM_WARPS * 32), msm,

@@ -373,20 +373,24 @@ def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
     assert torch.equal(vp.view(torch.int16), vp2.view(torch.int16))
 
 
-@pytest.mark.parametrize("H,Hkv,alibi,cached", [
-    (32, 32, False, [0, 15, 16, 130, 1000, 2047]), (8, 4, False, [3, 700]),
-    (16, 16, True, [31, 1500]), (32, 32, False, [8190]), (64, 8, False, [3, 1100]),
-    (16, 4, True, [500])])
-def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached, monkeypatch):
+@pytest.mark.parametrize("H,Hkv,alibi,cached,gqa", [
+    (32, 32, False, [0, 15, 16, 130, 1000, 2047], "-"), (8, 4, False, [3, 700], "-"),
+    (16, 16, True, [31, 1500], "-"), (32, 32, False, [8190], "-"),
+    (64, 8, False, [3, 1100], "cuda"), (16, 4, True, [500], "cuda"),
+    (64, 8, False, [3, 1100], "mma"), (64, 8, False, [1900], "mma"), (16, 4, True, [500], "mma"),
+    (64, 8, False, [5, 900, 40, 1023], "split")])
+def test_attn_decode_cluster_kernel_vs_torch(K, H, Hkv, alibi, cached, gqa, monkeypatch):
     """Decode-graph attention — the cluster-streaming kernel for G = 1, 2 (and
-    its head-split GQA mode, forced on here), the tensor-core split-K kernel
-    for G = 4, 8 by default —
+    its head-split GQA mode), the tensor-core kernel for G = 4, 8 in its
+    cluster (DSMEM merge) and split-K forms —
     against a plain torch fp32 attention over the gathered pages: the current
     token (position = ctx) is RoPE'd (or ALiBi-biased), appended to its
     block-table slot, and attends over positions 0..ctx; contexts from 1 token
     to 8191 (every CTA of the 8-CTA cluster empty, partial or full)."""
     from oracle.decoder import apply_rope, rope_tables
-    monkeypatch.setenv("SWB_ATTN_CL_MAXB_GQA", "2")
+    # GQA path: the CUDA-core cluster kernel's head split ("cuda"), the
+    # tensor-core cluster form ("mma", B <= 2) or the split-K MMA kernel
+    monkeypatch.setenv("SWB_ATTN_CL_MAXB_GQA", "2" if gqa == "cuda" else "0")
     dh, bs, B = 128, 16, len(cached)
     maxb = (max(cached) + 1 + bs - 1) // bs + 1
     nblk = B * maxb + 8

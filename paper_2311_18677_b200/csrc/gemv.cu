@@ -279,9 +279,9 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     }
   }
   if (tpp.world > 1 && warp == 0 && lane == 0) {
-    // every partial this CTA pushed is visible system-wide before its
-    // completion count reaches the peers
-    __threadfence_system();
+    // lane 0 issued every remote store of this CTA, so the release semantics
+    // of its count increment order them before the count (no fence.sc.sys:
+    // 296 CTAs' system-wide SC fences serialize)
     for (int p = 0; p < tpp.world; ++p)
       if (p != tpp.rank) red_release_sys_add(tpp.cnt[p], 1u);
   }

@@ -1273,8 +1273,8 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     }
     __syncthreads();
     mbar_wait_cluster(&merge_bar, 0);
-    float* fac = sml;                     // [CLN][G] merge factors (sml is free now)
-    float* ltot = so;                     // [G]
+    float* fac = rec;                     // [CLN][G] merge factors (rec was pushed)
+    float* ltot = rec + CLN * G;          // [G]
     if (threadIdx.x < G) {
       const int gi = threadIdx.x;
       float Mx = -INFINITY;

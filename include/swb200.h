@@ -130,6 +130,13 @@ int swb_layernorm(const float* x, const int32_t* row_index, const void* w,
                   int out_f32, uintptr_t stream);
 /* Greedy sampling: out[r] = argmax_v logits fp32 [rows,V] (lowest index on
  * ties). */
+/* TP prefill: x[src] += addend[src] (bf16, the all-reduced sum of the ranks'
+ * bf16 projection partials) over the normalised rows, written back to the
+ * fp32 residual stream, then the norm as swb_rmsnorm / swb_layernorm. */
+int swb_add_rmsnorm(float* x, const void* addend, const int32_t* row_index, const void* w,
+                    void* out, int rows, int d, float eps, uintptr_t stream);
+int swb_add_layernorm(float* x, const void* addend, const int32_t* row_index, const void* w,
+                      const void* b, void* out, int rows, int d, float eps, uintptr_t stream);
 int swb_argmax(const float* logits, int rows, int V, int32_t* out,
                uintptr_t stream);
 

@@ -55,6 +55,8 @@ SIGNATURES = {
     "swb_embed": [_P, _P, _P, _I, _I, _ST],
     "swb_rmsnorm": [_P, _P, _P, _P, _I, _I, _F, _ST],
     "swb_layernorm": [_P, _P, _P, _P, _P, _I, _I, _F, _I, _ST],
+    "swb_add_rmsnorm": [_P, _P, _P, _P, _P, _I, _I, _F, _ST],
+    "swb_add_layernorm": [_P, _P, _P, _P, _P, _P, _I, _I, _F, _ST],
     "swb_argmax": [_P, _I, _I, _P, _ST],
     "swb_argmax_shard": [_P, _I, _I, _I, _I, _I, _P, _ST],
     "swb_argmax_pick": [_P, _I, _I, _P, _ST],
@@ -133,7 +135,7 @@ def check(status: int, what: str = "") -> None:
 LAUNCH_MULT = {
     "swb_gemm_bf16": 1, "swb_gemv_bf16": 1, "swb_gemm_bf16_bias": 1, "swb_gemv_bf16_bias": 1,
     "swb_gemm_qkv_rope": 1, "swb_rope_table": 1,
-    "swb_layernorm": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
+    "swb_layernorm": 1, "swb_add_rmsnorm": 1, "swb_add_layernorm": 1, "swb_gemv_rmsnorm_bf16": 1, "swb_embed": 1, "swb_rmsnorm": 1,
     "swb_argmax": 1, "swb_argmax_shard": 1, "swb_argmax_pick": 1, "swb_rope_kv_write": 1, "swb_kv_push_layer": 1, "swb_kv_push_layers": 1,
     "swb_kv_handoff": 1,
     "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1, "swb_attn_chunk": 1,

@@ -37,10 +37,21 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens,
 // LayerNorm (BLOOM): out = (x - mean) * rstd * w + b over fp32 rows, two
 // passes over the (L1/L2-resident) row; bf16 or fp32 output (the embedding
 // LayerNorm produces the fp32 residual stream, possibly in place).
+// addend (optional, bf16 [rows of x]): x[src] += addend[src] first, written
+// back (the TP prefill's bf16 all-reduce result joins the fp32 residual here).
+__device__ __forceinline__ float4 add_row4(float* x, const __nv_bfloat16* addend, size_t i4) {
+  float4 v = reinterpret_cast<float4*>(x)[i4];
+  const uint2 a = reinterpret_cast<const uint2*>(addend)[i4];
+  const float2 a0 = bf2_to_f2(a.x), a1 = bf2_to_f2(a.y);
+  v.x += a0.x; v.y += a0.y; v.z += a1.x; v.w += a1.y;
+  reinterpret_cast<float4*>(x)[i4] = v;
+  return v;
+}
+
 __global__ void layernorm_kernel(const float* x, const int32_t* __restrict__ row_index,
                                  const __nv_bfloat16* __restrict__ w,
                                  const __nv_bfloat16* __restrict__ b, void* out, int d,
-                                 float eps, int out_f32) {
+                                 float eps, int out_f32, const __nv_bfloat16* addend) {
   pdl_wait();
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -49,7 +60,8 @@ __global__ void layernorm_kernel(const float* x, const int32_t* __restrict__ row
   __shared__ float stat[2];
   float s = 0.f;
   for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
-    const float4 v = xr[c];
+    const float4 v = addend ? add_row4(const_cast<float*>(x), addend, (size_t)src * (d / 4) + c)
+                            : xr[c];
     s += (v.x + v.y) + (v.z + v.w);
   }
   s = warp_sum(s);
@@ -96,10 +108,10 @@ __global__ void layernorm_kernel(const float* x, const int32_t* __restrict__ row
   }
 }
 
-__global__ void rmsnorm_kernel(const float* __restrict__ x,
-                               const int32_t* __restrict__ row_index,
+__global__ void rmsnorm_kernel(const float* x, const int32_t* __restrict__ row_index,
                                const __nv_bfloat16* __restrict__ w,
-                               __nv_bfloat16* __restrict__ out, int d, float eps) {
+                               __nv_bfloat16* __restrict__ out, int d, float eps,
+                               const __nv_bfloat16* addend) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
@@ -107,7 +119,8 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x,
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * d);
   float ss = 0.f;
   for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
-    const float4 v = xr[c];
+    const float4 v = addend ? add_row4(const_cast<float*>(x), addend, (size_t)src * (d / 4) + c)
+                            : xr[c];
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   __shared__ float red[32];
@@ -439,6 +452,23 @@ extern "C" int swb_embed(const int32_t* tokens, const void* table, float* x,
   return swb_check_launch("embed_kernel");
 }
 
+extern "C" int swb_add_rmsnorm(float* x, const void* addend, const int32_t* row_index,
+                               const void* w, void* out, int rows, int d, float eps,
+                               uintptr_t stream) {
+  SWB_REQUIRE(x && w && out, "swb_add_rmsnorm: null pointer");
+  SWB_REQUIRE(rows >= 0 && d > 0 && d % 4 == 0, "swb_add_rmsnorm: bad shape");
+  if (rows == 0) return SWB_OK;
+  {
+    const cudaError_t le_ = launch(rmsnorm_kernel, dim3(rows), dim3(512), 0, STREAM,
+      x, row_index, reinterpret_cast<const __nv_bfloat16*>(w),
+      reinterpret_cast<__nv_bfloat16*>(out), d, eps,
+      reinterpret_cast<const __nv_bfloat16*>(addend));
+    if (le_ != cudaSuccess)
+      return swb_set_error(SWB_ERR_CUDA, "launch rmsnorm_kernel: %s", cudaGetErrorString(le_));
+  }
+  return swb_check_launch("rmsnorm_kernel");
+}
+
 extern "C" int swb_rmsnorm(const float* x, const int32_t* row_index, const void* w,
                            void* out, int rows, int d, float eps, uintptr_t stream) {
   SWB_REQUIRE(x && w && out, "swb_rmsnorm: null pointer");
@@ -446,9 +476,8 @@ extern "C" int swb_rmsnorm(const float* x, const int32_t* row_index, const void*
   if (rows == 0) return SWB_OK;
   {
     const cudaError_t le_ = launch(rmsnorm_kernel, dim3(rows), dim3(512), 0, STREAM,
-        
       x, row_index, reinterpret_cast<const __nv_bfloat16*>(w),
-      reinterpret_cast<__nv_bfloat16*>(out), d, eps);
+      reinterpret_cast<__nv_bfloat16*>(out), d, eps, (const __nv_bfloat16*)nullptr);
     if (le_ != cudaSuccess)
       return swb_set_error(SWB_ERR_CUDA, "launch rmsnorm_kernel: %s", cudaGetErrorString(le_));
   }
@@ -465,7 +494,23 @@ extern "C" int swb_layernorm(const float* x, const int32_t* row_index, const voi
   if (rows == 0) return SWB_OK;
   const cudaError_t le = launch(layernorm_kernel, dim3(rows), dim3(512), 0, STREAM, x,
                                 row_index, reinterpret_cast<const __nv_bfloat16*>(w),
-                                reinterpret_cast<const __nv_bfloat16*>(b), out, d, eps, out_f32);
+                                reinterpret_cast<const __nv_bfloat16*>(b), out, d, eps, out_f32,
+                                (const __nv_bfloat16*)nullptr);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch layernorm_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("layernorm_kernel");
+}
+
+extern "C" int swb_add_layernorm(float* x, const void* addend, const int32_t* row_index,
+                                 const void* w, const void* b, void* out, int rows, int d,
+                                 float eps, uintptr_t stream) {
+  SWB_REQUIRE(x && addend && w && b && out, "swb_add_layernorm: null pointer");
+  SWB_REQUIRE(rows >= 0 && d > 0 && d % 4 == 0, "swb_add_layernorm: bad shape");
+  if (rows == 0) return SWB_OK;
+  const cudaError_t le = launch(layernorm_kernel, dim3(rows), dim3(512), 0, STREAM, x,
+                                row_index, reinterpret_cast<const __nv_bfloat16*>(w),
+                                reinterpret_cast<const __nv_bfloat16*>(b), out, d, eps, 0,
+                                reinterpret_cast<const __nv_bfloat16*>(addend));
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch layernorm_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("layernorm_kernel");

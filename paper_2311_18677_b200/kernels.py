@@ -145,20 +145,30 @@ def embed(tokens, table, out=None):
     return out
 
 
-def rmsnorm(x, w, eps, rows_index=None, out=None):
+def rmsnorm(x, w, eps, rows_index=None, out=None, addend=None):
+    """RMSNorm of fp32 rows; with ``addend`` (bf16, x's shape) the rows first
+    get x += addend (written back)."""
     _req(x, torch.float32, "x")
     _req(w, torch.bfloat16, "w")
     rows = x.shape[0] if rows_index is None else rows_index.shape[0]
     d = x.shape[1]
     if out is None:
         out = torch.empty(rows, d, dtype=torch.bfloat16, device=x.device)
+    if addend is not None:
+        _req(addend, torch.bfloat16, "addend")
+        if addend.shape != x.shape:
+            raise ValidationError("rmsnorm: addend must match x")
+        call("swb_add_rmsnorm", x.data_ptr(), addend.data_ptr(), _ptr(rows_index), w.data_ptr(),
+             out.data_ptr(), rows, d, float(eps), _stream())
+        return out
     call("swb_rmsnorm", x.data_ptr(), rows_index.data_ptr() if rows_index is not None else None,
          w.data_ptr(), out.data_ptr(), rows, d, float(eps), _stream())
     return out
 
 
-def layernorm(x, w, b, eps, rows_index=None, out=None, out_f32=False):
-    """LayerNorm with bias (BLOOM); fp32 out (may be x) when out_f32."""
+def layernorm(x, w, b, eps, rows_index=None, out=None, out_f32=False, addend=None):
+    """LayerNorm with bias (BLOOM); fp32 out (may be x) when out_f32; with
+    ``addend`` (bf16) the rows first get x += addend (written back)."""
     _req(x, torch.float32, "x")
     _req(w, torch.bfloat16, "w")
     _req(b, torch.bfloat16, "b")
@@ -167,6 +177,13 @@ def layernorm(x, w, b, eps, rows_index=None, out=None, out_f32=False):
     if out is None:
         out = torch.empty(rows, d, dtype=torch.float32 if out_f32 else torch.bfloat16,
                           device=x.device)
+    if addend is not None:
+        _req(addend, torch.bfloat16, "addend")
+        if addend.shape != x.shape or out_f32:
+            raise ValidationError("layernorm: addend must match x (bf16 output only)")
+        call("swb_add_layernorm", x.data_ptr(), addend.data_ptr(), _ptr(rows_index),
+             w.data_ptr(), b.data_ptr(), out.data_ptr(), rows, d, float(eps), _stream())
+        return out
     call("swb_layernorm", x.data_ptr(), _ptr(rows_index), w.data_ptr(), b.data_ptr(),
          out.data_ptr(), rows, d, float(eps), int(bool(out_f32)), _stream())
     return out

@@ -92,6 +92,9 @@ class ModelRunner:
         self.alibi = weights.alibi
         self.tp_max_rows = tp_max_rows    # largest prefill / decode row count reduced
         self.ar_nccl_bytes = int(os.environ.get("SWB_TP_AR_NCCL_BYTES", str(4 << 20)))
+        # SWB_TP_AR_BF16=0 keeps the prefill all-reduces in fp32 (A/B)
+        self.ar_bf16 = os.environ.get("SWB_TP_AR_BF16", "1") != "0"
+        self._pending_add = None
         # SWB_TP_FUSED=1: decode B=1 projections push their partial to the
         # peers from the GEMV epilogue (swb_gemv_bf16_tp) and a receive kernel
         # only waits and sums.  Exact (tests/test_tpcomm_gpu.py) but measured
@@ -146,6 +149,8 @@ class ModelRunner:
         return self.tp_comm
 
     def _begin_reductions(self):
+        if self._pending_add is not None:
+            raise RuntimeError("a bf16 all-reduce result was never added to the residual")
         c = self._comm()
         if c is not None:
             c.reset()
@@ -165,6 +170,15 @@ class ModelRunner:
         # 32 MB at TP2 90 vs 97 us (tools/ar_bench.py); small (decode)
         # messages stay on the graph-replayable peer kernel (20 vs 26-39 us)
         big = x.numel() * 4 >= self.ar_nccl_bytes
+        if big and self.ar_bf16:
+            # prefill-size messages: the ranks' partials (no residual) go
+            # through the all-reduce in bf16 — half the NVLink bytes — and
+            # join the fp32 residual in the next norm (x += sum, then norm)
+            part = self._ar_part(x.shape)
+            K.linear(inp, w, K.EPI_BF16, out=part, bias=b)
+            self._allreduce(part)
+            self._pending_add = part
+            return
         if c is None or big:
             K.linear(inp, w, self._resid_epi(), out=x, resid=x, bias=b)
             self._allreduce(x)
@@ -180,13 +194,23 @@ class ModelRunner:
         K.linear(inp, w, self._resid_epi(), out=part, resid=x, bias=b)
         c.allreduce(s, x)
 
+    def _ar_part(self, shape):
+        buf = getattr(self, "_arbuf", None)
+        n = shape[0] * shape[1]
+        if buf is None or buf.numel() < n:
+            self._arbuf = buf = torch.empty(n, dtype=torch.bfloat16, device=self.dev)
+        return buf[:n].view(shape)
+
     # -- architecture switches (Llama: RMSNorm / RoPE / SwiGLU; BLOOM:
     #    LayerNorm+bias / ALiBi / biased linears + GELU / embedding LayerNorm)
     def _norm(self, x, w, b, out, rows_index=None):
+        add, self._pending_add = self._pending_add, None    # a bf16 all-reduce result
+        if add is not None and add.shape != x.shape:
+            raise RuntimeError("pending all-reduce result does not match the residual")
         if self.bloom:
-            K.layernorm(x, w, b, self.cfg.norm_eps, rows_index=rows_index, out=out)
+            K.layernorm(x, w, b, self.cfg.norm_eps, rows_index=rows_index, out=out, addend=add)
         else:
-            K.rmsnorm(x, w, self.cfg.norm_eps, rows_index=rows_index, out=out)
+            K.rmsnorm(x, w, self.cfg.norm_eps, rows_index=rows_index, out=out, addend=add)
 
     def _embed(self, tokens, x):
         K.embed(tokens, self.w.embed, out=x)

@@ -182,20 +182,27 @@ def test_tp_allreduce_p2p_exact():
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_tp2_tiny_matches_tp1():
+@pytest.mark.parametrize("model,env", [("tiny", {}), ("tiny", {"SWB_TP_AR_NCCL_BYTES": "0"}),
+                                       ("bloom-tiny", {"SWB_TP_AR_NCCL_BYTES": "0"})])
+def test_tp2_tiny_matches_tp1(model, env):
+    """TP=2 pool == TP=1 tokens; with SWB_TP_AR_NCCL_BYTES=0 every reduction
+    takes the NCCL path, whose prefill-size form all-reduces bf16 partials and
+    adds them to the fp32 residual inside the next norm."""
     import subprocess
     port = _free_port()
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
-                        os.path.join(ROOT, "tools", "tp_check.py")],
-                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+                        os.path.join(ROOT, "tools", "tp_check.py"), "--model", model],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env={**os.environ, **env})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"ok": true' in r.stdout
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
-@pytest.mark.parametrize("model", ["tiny-tp4", "bloom-tiny-tp4"])
-def test_tp4_pool_matches_tp1(model):
+@pytest.mark.parametrize("model,env", [("tiny-tp4", {}), ("bloom-tiny-tp4", {}),
+                                       ("tiny-tp4", {"SWB_TP_AR_NCCL_BYTES": "0"})])
+def test_tp4_pool_matches_tp1(model, env):
     """A TP=4 pool (push all-reduce for decode, two-shot / NCCL for prefill
     sizes) generates the TP=1 tokens, logits within tolerance."""
     import subprocess
@@ -203,7 +210,8 @@ def test_tp4_pool_matches_tp1(model):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "4",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
                         os.path.join(ROOT, "tools", "tp_check.py"), "--model", model],
-                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+                       capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env={**os.environ, **env})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert '"ok": true' in r.stdout
 

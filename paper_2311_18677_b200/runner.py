@@ -170,10 +170,12 @@ class ModelRunner:
         # 32 MB at TP2 90 vs 97 us (tools/ar_bench.py); small (decode)
         # messages stay on the graph-replayable peer kernel (20 vs 26-39 us)
         big = x.numel() * 4 >= self.ar_nccl_bytes
-        if big and self.ar_bf16:
+        if big and self.ar_bf16 and x.shape[0] > K.GEMV_MAX_ROWS:
             # prefill-size messages: the ranks' partials (no residual) go
             # through the all-reduce in bf16 — half the NVLink bytes — and
-            # join the fp32 residual in the next norm (x += sum, then norm)
+            # join the fp32 residual in the next norm (x += sum, then norm).
+            # Prefill rows only: the decode graph's fused pre-norm GEMVs
+            # read x directly.
             part = self._ar_part(x.shape)
             K.linear(inp, w, K.EPI_BF16, out=part, bias=b)
             self._allreduce(part)

@@ -182,12 +182,13 @@ def test_tp_allreduce_p2p_exact():
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("model,env", [("tiny", {}), ("tiny", {"SWB_TP_AR_NCCL_BYTES": "0"}),
-                                       ("bloom-tiny", {"SWB_TP_AR_NCCL_BYTES": "0"})])
+@pytest.mark.parametrize("model,env", [("tiny", {}), ("tiny", {"SWB_TP_AR_NCCL_BYTES": "65536"}),
+                                       ("bloom-tiny", {"SWB_TP_AR_NCCL_BYTES": "65536"})])
 def test_tp2_tiny_matches_tp1(model, env):
-    """TP=2 pool == TP=1 tokens; with SWB_TP_AR_NCCL_BYTES=0 every reduction
-    takes the NCCL path, whose prefill-size form all-reduces bf16 partials and
-    adds them to the fp32 residual inside the next norm."""
+    """TP=2 pool == TP=1 tokens; with a 64 KB NCCL threshold the tiny
+    prefill's reductions take the production prefill path (bf16 partials
+    all-reduced by NCCL, added to the fp32 residual inside the next norm)
+    while decode keeps the peer all-reduce, as at full size."""
     import subprocess
     port = _free_port()
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
@@ -201,7 +202,7 @@ def test_tp2_tiny_matches_tp1(model, env):
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
 @pytest.mark.parametrize("model,env", [("tiny-tp4", {}), ("bloom-tiny-tp4", {}),
-                                       ("tiny-tp4", {"SWB_TP_AR_NCCL_BYTES": "0"})])
+                                       ("tiny-tp4", {"SWB_TP_AR_NCCL_BYTES": "65536"})])
 def test_tp4_pool_matches_tp1(model, env):
     """A TP=4 pool (push all-reduce for decode, two-shot / NCCL for prefill
     sizes) generates the TP=1 tokens, logits within tolerance."""

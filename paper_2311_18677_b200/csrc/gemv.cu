@@ -650,7 +650,13 @@ static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, cons
     const char* e = std::getenv("SWB_GEMV_CORE_MAXM");
     return e ? std::atoi(e) : 1;
   }();
-  if (M >= 2 && M <= core_maxm && M <= 4 && (!NORM || (size_t)M * K * 2 <= (size_t)TV_HS_MAX)) {
+  // SWB_GEMV_CORE_NORM_MAXM=m: only the fused pre-norm GEMVs with M <= m (A/B)
+  static const int core_norm_maxm = [] {
+    const char* e = std::getenv("SWB_GEMV_CORE_NORM_MAXM");
+    return e ? std::atoi(e) : 1;
+  }();
+  const int cmax = NORM ? std::max(core_maxm, core_norm_maxm) : core_maxm;
+  if (M >= 2 && M <= cmax && M <= 4 && (!NORM || (size_t)M * K * 2 <= (size_t)TV_HS_MAX)) {
     if (M <= 2)
       return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
     return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);

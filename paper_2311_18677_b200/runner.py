@@ -111,9 +111,10 @@ class ModelRunner:
         self.push_ctas = push_ctas
         self.dev = weights.embed.device
         self._cap = 0
-        # SWB_PUSH_PRIORITY=high: the push stream's CTAs are scheduled ahead of
-        # the prefill's (A/B of the in-flight push bandwidth vs the TTFT cost)
-        prio = -1 if os.environ.get("SWB_PUSH_PRIORITY", "normal") == "high" else 0
+        # the push stream's CTAs are scheduled ahead of the prefill's: 7B
+        # 1024 tokens, in-flight push 298 -> 353 GB/s and TTFT overhead 2.8 ->
+        # 2.2 % (profiles/r2_push_priority_ab.json); SWB_PUSH_PRIORITY=normal A/B
+        prio = 0 if os.environ.get("SWB_PUSH_PRIORITY", "high") == "normal" else -1
         self.push_stream = torch.cuda.Stream(device=self.dev, priority=prio)
         self._buf_ev = [None, None]      # last push that read each qkv buffer
         self._stash = None               # [L, SERIAL_MAX_ROWS, qkv_cols] (serialized mode)

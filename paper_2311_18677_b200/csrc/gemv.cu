@@ -33,7 +33,11 @@ constexpr int TV_STAGE_BYTES = TV_ROWS * TV_ROW_BYTES;  // 16 KB
 constexpr int TV_THREADS = (TV_WARPS + 1) * 32;
 constexpr int TV_CTAS_PER_SM = 2;             // 2 x ~100 KB ring per SM
 constexpr int TV_HS_MAX = 16 * 1024;          // NORM: staged h (M*K*2 bytes) limit
-constexpr int TV_SMEM = TV_STAGES * TV_STAGE_BYTES + 2 * TV_STAGES * 8 +
+// Items of R in {1, 2, 4} rows (the ring keeps TV_STAGES * 16 KB in flight:
+// 20 / R stages of R rows): small matrices use narrower items so the
+// persistent grid's CTAs get equal shares (7B O / down projections: 1024
+// 4-row items over 296 CTAs = 3.46 each, i.e. the 4-item CTAs set the time).
+constexpr int TV_SMEM = TV_STAGES * TV_STAGE_BYTES + 2 * 20 * 8 +
                         2 * TV_WARPS * TV_ROWS * 16 * 4 + 128;
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -53,8 +57,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // weight row of slot j (0..3) of work item `item`.  Plain: rows 4i..4i+3.
 // SwiGLU: outputs 2i, 2i+1 -> gate rows g, g+1 (slots 0,1), up rows g+128,
 // g+129 (slots 2,3), with gate/up interleaved in 128-row groups.
+template <int R = TV_ROWS>
 __device__ __forceinline__ int item_row(int item, int j, bool swiglu) {
-  if (!swiglu) return item * TV_ROWS + j;
+  if (!swiglu) return item * R + j;
   const int o = item * 2 + (j & 1);
   return (o >> 7) * 256 + (o & 127) + (j >= 2 ? 128 : 0);
 }
@@ -63,27 +68,29 @@ __device__ __forceinline__ int item_row(int item, int j, bool swiglu) {
 // NORM = true : x is the fp32 residual stream [M,K]; the kernel applies
 //               RMSNorm on the fly, h = bf16(x * rsqrt(mean(x^2)+eps) * nw),
 //               bit-identical to swb_rmsnorm's output (fused pre-norm GEMV).
-template <int MB, bool NORM>
+template <int MB, bool NORM, int R = TV_ROWS>
 __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     gemv_bulk_kernel(const void* __restrict__ xin, const __nv_bfloat16* __restrict__ nw,
                      float eps, const __nv_bfloat16* __restrict__ W, void* out,
                      const float* resid, const __nv_bfloat16* bias, int M, int N, int K,
                      int epi, int n_items, int trig, const TpPush tpp) {
+  constexpr int NST = TV_STAGES * TV_ROWS / R;           // ring stages
+  constexpr int SBYTES = R * TV_ROW_BYTES;                // bytes per stage
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + TV_STAGES * TV_STAGE_BYTES);
-  uint64_t* empty = full + TV_STAGES;
-  float* part = reinterpret_cast<float*>(empty + TV_STAGES);  // [2][WARPS][ROWS][16]
+  uint64_t* empty = full + NST;
+  float* part = reinterpret_cast<float*>(full + 2 * 20);     // [2][WARPS][R][16]
   float* rstd = part + 2 * TV_WARPS * TV_ROWS * 16;            // [16]
   __nv_bfloat16* hs = reinterpret_cast<__nv_bfloat16*>(smem + TV_SMEM);  // NORM: [M][K]
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(xin);
   const float* xf = reinterpret_cast<const float*>(xin);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool swiglu = epi == SWB_EPI_SWIGLU;
+  const bool swiglu = R == 4 && epi == SWB_EPI_SWIGLU;     // SwiGLU items are 4-row
   const int nk = (K + TV_KC - 1) / TV_KC;
 
   pdl_trigger();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TV_STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], TV_WARPS);
     }
@@ -98,17 +105,17 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
       int it = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         for (int kc = 0; kc < nk; ++kc, ++it) {
-          const int s = it % TV_STAGES;
-          if (it >= TV_STAGES) mbar_wait_sleep(&empty[s], ((it / TV_STAGES) - 1) & 1);
+          const int s = it % NST;
+          if (it >= NST) mbar_wait_sleep(&empty[s], ((it / NST) - 1) & 1);
           const int k0 = kc * TV_KC;
           const uint32_t bytes = (uint32_t)min(TV_KC, K - k0) * 2;
           uint32_t total = 0;
-          for (int j = 0; j < TV_ROWS; ++j)
-            if (item_row(item, j, swiglu) < N) total += bytes;
+          for (int j = 0; j < R; ++j)
+            if (item_row<R>(item, j, swiglu) < N) total += bytes;
           mbar_arrive_expect_tx(&full[s], total);
-          uint8_t* st = smem + s * TV_STAGE_BYTES;
-          for (int j = 0; j < TV_ROWS; ++j) {
-            const int row = item_row(item, j, swiglu);
+          uint8_t* st = smem + s * SBYTES;
+          for (int j = 0; j < R; ++j) {
+            const int row = item_row<R>(item, j, swiglu);
             if (row < N)
               bulk_load(st + j * TV_ROW_BYTES, W + (size_t)row * K + k0, bytes, &full[s], pol);
           }
@@ -169,13 +176,13 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
   }
   int it = 0, parity = 0;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x, parity ^= 1) {
-    float acc[TV_ROWS][MB];
+    float acc[R][MB];
 #pragma unroll
-    for (int j = 0; j < TV_ROWS; ++j)
+    for (int j = 0; j < R; ++j)
 #pragma unroll
       for (int m = 0; m < MB; ++m) acc[j][m] = 0.f;
     for (int kc = 0; kc < nk; ++kc, ++it) {
-      const int s = it % TV_STAGES;
+      const int s = it % NST;
       const int k = kc * TV_KC + warp * 256 + lane * 8;
       uint4 xq[MB];
       if (k < K) {
@@ -189,12 +196,12 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
             if (m < M) xq[m] = *reinterpret_cast<const uint4*>(x + (size_t)m * K + k);
         }
       }
-      mbar_wait(&full[s], (it / TV_STAGES) & 1);
+      mbar_wait(&full[s], (it / NST) & 1);
       if (k < K) {
-        const uint8_t* st = smem + s * TV_STAGE_BYTES + (warp * 256 + lane * 8) * 2;
-        uint4 wv[TV_ROWS];
+        const uint8_t* st = smem + s * SBYTES + (warp * 256 + lane * 8) * 2;
+        uint4 wv[R];
 #pragma unroll
-        for (int j = 0; j < TV_ROWS; ++j)
+        for (int j = 0; j < R; ++j)
           wv[j] = *reinterpret_cast<const uint4*>(st + j * TV_ROW_BYTES);
 #pragma unroll
         for (int m = 0; m < MB; ++m) {
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
           const float2 x0 = bf2_to_f2(xq[m].x), x1 = bf2_to_f2(xq[m].y),
                        x2 = bf2_to_f2(xq[m].z), x3 = bf2_to_f2(xq[m].w);
 #pragma unroll
-          for (int j = 0; j < TV_ROWS; ++j) {
+          for (int j = 0; j < R; ++j) {
             const float2 w0 = bf2_to_f2(wv[j].x), w1 = bf2_to_f2(wv[j].y),
                          w2 = bf2_to_f2(wv[j].z), w3 = bf2_to_f2(wv[j].w);
             float a = acc[j][m];
@@ -221,23 +228,23 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     // 8 K-slices of each (row, m) and applies the epilogue
     float* pb = part + parity * TV_WARPS * TV_ROWS * 16;
 #pragma unroll
-    for (int j = 0; j < TV_ROWS; ++j)
+    for (int j = 0; j < R; ++j)
 #pragma unroll
       for (int m = 0; m < MB; ++m) {
         if (m >= M) break;
         const float v = warp_sum(acc[j][m]);
-        if (lane == 0) pb[(warp * TV_ROWS + j) * 16 + m] = v;
+        if (lane == 0) pb[(warp * R + j) * 16 + m] = v;
       }
     asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
     if (warp == 0) {
-      for (int e0 = 0; e0 < M * TV_ROWS; e0 += 32) {   // warp-uniform trip count
+      for (int e0 = 0; e0 < M * R; e0 += 32) {   // warp-uniform trip count
         const int e = e0 + lane;
-        const bool active = e < M * TV_ROWS;
-        const int m = e / TV_ROWS, j = e % TV_ROWS;
+        const bool active = e < M * R;
+        const int m = e / R, j = e % R;
         float v = 0.f;
         if (active) {
 #pragma unroll
-          for (int w = 0; w < TV_WARPS; ++w) v += pb[(w * TV_ROWS + j) * 16 + m];
+          for (int w = 0; w < TV_WARPS; ++w) v += pb[(w * R + j) * 16 + m];
         }
         // SwiGLU: rows j = 0,1 gate and 2,3 up of outputs 2*item + (j & 1)
         const float u = __shfl_down_sync(0xffffffffu, v, 2);
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
                   __float2bfloat16(silu_f(v) * u);
           }
         } else {
-          const int r = item_row(item, j, false);
+          const int r = item_row<R>(item, j, false);
           if (r < N) {
             const size_t idx = (size_t)m * N + r;
             v += bias_at(bias, r);
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
           }
         }
       }
-      if (tpp.world > 1) {
+      if (R == 4 && tpp.world > 1) {
         // fused TP all-reduce (one decode row): the item's 4 consecutive
         // outputs go straight to every peer as one 16-byte posted NVLink
         // store while the weights of later items still stream
@@ -299,34 +306,63 @@ static int gemv_ctas_per_sm() {
   return n;
 }
 
-template <int MB, bool NORM>
-static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
-                       const __nv_bfloat16* w, void* out, const float* r,
-                       const __nv_bfloat16* bias, int M, int N, int K, int epi, int items,
-                       cudaStream_t s, swb_tp_comm* tp = nullptr, int tp_slot = 0) {
+template <int MB, bool NORM, int R>
+static int launch_gemv_r(const void* x, const __nv_bfloat16* nw, float eps,
+                         const __nv_bfloat16* w, void* out, const float* r,
+                         const __nv_bfloat16* bias, int M, int N, int K, int epi,
+                         cudaStream_t s, const TpPush& tpp, int grid) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr[dev]) {
-    SWB_CUDA(cudaFuncSetAttribute(gemv_bulk_kernel<MB, NORM>,
+    SWB_CUDA(cudaFuncSetAttribute(gemv_bulk_kernel<MB, NORM, R>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   TV_SMEM + TV_HS_MAX));
     attr[dev] = true;
   }
   const size_t smem = TV_SMEM + (NORM ? (size_t)M * K * 2 : 0);
-  const int grid = min(items, gemv_ctas_per_sm() * kNumSMs);
+  const int items = (N + R - 1) / R;
+  const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM, R>, dim3(grid), dim3(TV_THREADS),
+                                smem, s, x, nw, eps, w, out, r, bias, M, N, K, epi, items,
+                                pdl_early_trigger() ? 1 : 0, tpp);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("gemv_bulk_kernel");
+}
+
+// rows per item: 4 unless the matrix is too small to give every CTA of the
+// persistent grid >= 8 items (then 2, or 1); SwiGLU and the fused TP push
+// keep 4-row items.  SWB_GEMV_ROWS=4 pins the old behaviour (A/B).
+static int gemv_rows_for(int N, int grid_max, bool swiglu, bool tp) {
+  static const int pin = [] {
+    const char* e = std::getenv("SWB_GEMV_ROWS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (swiglu || tp) return 4;
+  if (pin == 1 || pin == 2 || pin == 4) return pin;
+  if ((N + 3) / 4 >= 8 * grid_max) return 4;
+  if ((N + 1) / 2 >= 8 * grid_max) return 2;
+  return 1;
+}
+
+template <int MB, bool NORM>
+static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
+                       const __nv_bfloat16* w, void* out, const float* r,
+                       const __nv_bfloat16* bias, int M, int N, int K, int epi, int items,
+                       cudaStream_t s, swb_tp_comm* tp = nullptr, int tp_slot = 0) {
+  const int grid_max = gemv_ctas_per_sm() * kNumSMs;
+  const int R = gemv_rows_for(N, grid_max, epi == SWB_EPI_SWIGLU, tp != nullptr);
+  const int grid = min((N + R - 1) / R, grid_max);
+  (void)items;
   TpPush tpp;
   memset(&tpp, 0, sizeof(tpp));
   if (tp) {
     const int st = tp_push_targets(tp, tp_slot, grid, &tpp);
     if (st) return st;
   }
-  const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM>, dim3(grid), dim3(TV_THREADS),
-                                smem, s, x, nw, eps, w, out, r, bias, M, N, K, epi, items,
-                                pdl_early_trigger() ? 1 : 0, tpp);
-  if (le != cudaSuccess)
-    return swb_set_error(SWB_ERR_CUDA, "launch gemv_bulk_kernel: %s", cudaGetErrorString(le));
-  return swb_check_launch("gemv_bulk_kernel");
+  if (R == 1) return launch_gemv_r<MB, NORM, 1>(x, nw, eps, w, out, r, bias, M, N, K, epi, s, tpp, grid);
+  if (R == 2) return launch_gemv_r<MB, NORM, 2>(x, nw, eps, w, out, r, bias, M, N, K, epi, s, tpp, grid);
+  return launch_gemv_r<MB, NORM, 4>(x, nw, eps, w, out, r, bias, M, N, K, epi, s, tpp, grid);
 }
 
 // ---------------------------------------------------------------------------

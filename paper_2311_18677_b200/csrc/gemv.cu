@@ -330,13 +330,14 @@ static int launch_gemv_r(const void* x, const __nv_bfloat16* nw, float eps,
   return swb_check_launch("gemv_bulk_kernel");
 }
 
-// rows per item: 4 unless the matrix is too small to give every CTA of the
-// persistent grid >= 8 items (then 2, or 1); SwiGLU and the fused TP push
-// keep 4-row items.  SWB_GEMV_ROWS=4 pins the old behaviour (A/B).
+// rows per item: 4 (default).  SWB_GEMV_ROWS=0 picks narrower items for
+// small matrices so the persistent grid gets equal shares — measured much
+// slower (7B B=1 step 3.41 vs 2.53 ms, 70B TP4 9.06 vs 8.05 ms: 1-2-row
+// stages do too little work per ring handshake), so it stays an A/B option.
 static int gemv_rows_for(int N, int grid_max, bool swiglu, bool tp) {
   static const int pin = [] {
     const char* e = std::getenv("SWB_GEMV_ROWS");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 4;
   }();
   if (swiglu || tp) return 4;
   if (pin == 1 || pin == 2 || pin == 4) return pin;

@@ -421,9 +421,12 @@ __device__ __forceinline__ float ld_dsmem(uint32_t cluster_addr) {
 // (tpcomm.cu fills it; world 0 = no push).
 struct TpPush {
   float* rx[8];          // peer p's receive buffer for this rank's partial (p != rank)
-  unsigned* cnt[8];      // peer p's push counter for (slot, this rank)
+  unsigned* cnt[8];      // peer p's push counter for (slot, this rank); [rank] = own
   int world, rank;
 };
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_sys_add(unsigned* p, unsigned v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -286,9 +286,11 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     }
   }
   if (tpp.world > 1 && warp == 0 && lane == 0) {
-    // lane 0 issued every remote store of this CTA, so the release semantics
-    // of its count increment order them before the count (no fence.sc.sys:
-    // 296 CTAs' system-wide SC fences serialize)
+    // lane 0 issued every remote store of this CTA and read every local
+    // output it pushed, so the release semantics of its count increments
+    // order them before the counts; the own count lets the receive kernel
+    // start without waiting for this grid to exit
+    red_release_gpu_add(tpp.cnt[tpp.rank], 1u);
     for (int p = 0; p < tpp.world; ++p)
       if (p != tpp.rank) red_release_sys_add(tpp.cnt[p], 1u);
   }

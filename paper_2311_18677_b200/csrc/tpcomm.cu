@@ -123,11 +123,13 @@ __device__ __forceinline__ float4 tp_sum4(const TpArgs& a, long long i) {
 // mode 2, one-shot push: decode-size messages (fit the rx buffers).
 __global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a, int mode,
                                                                    int trig) {
-  pdl_wait();  // the producer GEMM/GEMV must be complete before we publish
-  // past our own wait: the next kernel may launch now and stream its static
-  // weights (pre-wait) while this one waits on the peers' flags over NVLink
-  if (trig) pdl_launch_dependents();
   const int c = blockIdx.x;
+  if (mode != 3) {
+    pdl_wait();  // the producer GEMM/GEMV must be complete before we publish
+    // past our own wait: the next kernel may launch now and stream its static
+    // weights (pre-wait) while this one waits on the peers' flags over NVLink
+    if (trig) pdl_launch_dependents();
+  }
   if (mode == 3) {
     // fused form: the peers' projection GEMVs already pushed their partials
     // into rx[slot][p] and counted their CTAs; wait, then sum locally
@@ -140,8 +142,9 @@ __global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a
       e = *rc + 1;
       const uint32_t target = e * a.nsrc;
       const long long t0 = clock64();
+      // the own projection's CTAs count here too: no wait for that grid to
+      // exit (PDL), only for its outputs
       for (int p = 0; p < a.world; ++p) {
-        if (p == a.rank) continue;
         const uint32_t* f = a.my_pcnt + (size_t)a.slot * TP_MAXW + p;
         int spins = 0;
         while ((int)(ld_acquire_sys(f) - target) < 0) {
@@ -151,6 +154,9 @@ __global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a
       }
     }
     __syncthreads();
+    // every partial is in place: dependents may launch (their pre-wait code
+    // only streams static weights)
+    if (trig) pdl_launch_dependents();
     const float4* mine = reinterpret_cast<const float4*>(a.peer_slot[a.rank]);
     float4* out4 = reinterpret_cast<float4*>(a.out);
     for (long long i = lo + threadIdx.x; i < hi; i += TP_THREADS) {
@@ -374,10 +380,11 @@ int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, TpPush* out) {
   out->world = c->world;
   out->rank = c->rank;
   for (int p = 0; p < c->world; ++p) {
-    if (p == c->rank) continue;
-    out->rx[p] = reinterpret_cast<float*>(c->peer_base[p] + rx_off + (size_t)c->rank * rxb);
+    // own entry: this rank's counter slot [slot][rank] in its own region
     out->cnt[p] = reinterpret_cast<unsigned*>(c->peer_base[p] + pc_off) +
                   (size_t)slot * TP_MAXW + c->rank;
+    if (p == c->rank) continue;
+    out->rx[p] = reinterpret_cast<float*>(c->peer_base[p] + rx_off + (size_t)c->rank * rxb);
   }
   c->nsrc[slot] = nsrc;
   return SWB_OK;

@@ -365,13 +365,15 @@ int swb_tp_allreduce_f32(swb_tp_comm* comm, int slot, float* out, size_t n,
 /* Fused projection + all-reduce push (decode, one row): the weight-streaming
  * GEMV (epilogue SWB_EPI_F32, or SWB_EPI_RESID_F32 with resid on the rank
  * that folds the residual) writes its fp32 partial into this rank's slot
- * `slot` AND stores it straight into every peer's receive buffer for this
- * rank over NVLink from the epilogue; each CTA then publishes its completion
- * on the peers' push counters (system-scope fence, then a release add).
- * swb_tp_allreduce_recv_f32 waits for every peer's CTAs and writes the
- * rank-ordered sum (same bits as swb_tp_allreduce_f32).  Use the two as a
- * pair on the same slot, alternating slots like swb_tp_allreduce_f32.
- * N * 4 bytes must fit the 1 MB receive buffers. */
+ * `slot` AND stores it straight into every peer's receive lines for this
+ * rank over NVLink from the epilogue, each output as one 8-byte (value,
+ * epoch) word, so the data carries its own flag (no release fence); each CTA
+ * then counts itself on this rank's own counter (gpu-scope release).
+ * swb_tp_allreduce_recv_f32 waits for the own count and every peer word of
+ * the current epoch and writes the rank-ordered sum (same bits as
+ * swb_tp_allreduce_f32), without waiting for the GEMV grid to exit.  Use the
+ * two as a pair on the same slot, alternating slots like
+ * swb_tp_allreduce_f32.  N <= 16384 (128 KB of lines per source). */
 int swb_gemv_bf16_tp(const void* x, const void* w, const void* resid, const void* bias,
                      int M, int N, int K, int epilogue, swb_tp_comm* comm, int slot,
                      uintptr_t stream);

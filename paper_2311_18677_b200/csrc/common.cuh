@@ -38,7 +38,7 @@ namespace swb {
 struct TpPush;
 // tpcomm.cu: peer targets of a fused projection on `slot`, and the number of
 // producer CTAs (nsrc) the matching swb_tp_allreduce_recv_f32 waits for
-int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, TpPush* out);
+int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, long long n, TpPush* out);
 
 constexpr int kNumSMs = 148;
 
@@ -420,8 +420,13 @@ __device__ __forceinline__ float ld_dsmem(uint32_t cluster_addr) {
 // Peer receive buffers / push counters a fused projection GEMV writes into
 // (tpcomm.cu fills it; world 0 = no push).
 struct TpPush {
-  float* rx[8];          // peer p's receive buffer for this rank's partial (p != rank)
-  unsigned* cnt[8];      // peer p's push counter for (slot, this rank); [rank] = own
+  // peer p's receive lines for this rank's partial (p != rank): every output
+  // travels as (value, epoch) in one 8-byte word, so a peer sees data and
+  // flag together and no release fence is needed (a system-scope release per
+  // CTA costs ~7 us across a 296-CTA grid)
+  unsigned long long* rx[8];
+  unsigned* own_cnt;     // this rank's counter of finished projection CTAs
+  const unsigned* epoch; // uses of the slot so far (the receive kernel's count)
   int world, rank;
 };
 __device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {

@@ -137,6 +137,10 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
   // The producer above streams static weights before the previous kernel has
   // finished (PDL); consumers read x / write out only after it has.
   pdl_wait();
+  // fused TP push: this use's epoch (the previous use of the slot finished
+  // its receive kernel before the kernel ahead of us did)
+  const unsigned ll_e =
+      tpp.world > 1 ? *reinterpret_cast<const volatile unsigned*>(tpp.epoch) + 1u : 0u;
   if constexpr (NORM) {
     // sum of squares of every batch row, by all consumer threads
     const int t = threadIdx.x;
@@ -274,25 +278,31 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
       }
       if (R == 4 && tpp.world > 1) {
         // fused TP all-reduce (one decode row): the item's 4 consecutive
-        // outputs go straight to every peer as one 16-byte posted NVLink
-        // store while the weights of later items still stream
+        // outputs go straight to every peer as two 16-byte posted NVLink
+        // stores of (value, epoch) words while later weights still stream
         __syncwarp();
         if (lane == 0 && 4 * item + 3 < N) {
           const float4 v4 = reinterpret_cast<const float4*>(out)[item];
+          const unsigned long long hi = (unsigned long long)ll_e << 32;
+          const unsigned long long a0 = hi | __float_as_uint(v4.x), a1 = hi | __float_as_uint(v4.y),
+                                   a2 = hi | __float_as_uint(v4.z), a3 = hi | __float_as_uint(v4.w);
           for (int p = 0; p < tpp.world; ++p)
-            if (p != tpp.rank) reinterpret_cast<float4*>(tpp.rx[p])[item] = v4;
+            if (p != tpp.rank) {
+              unsigned long long* d = tpp.rx[p] + 4 * (size_t)item;
+              asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(d), "l"(a0), "l"(a1)
+                           : "memory");
+              asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(d + 2), "l"(a2),
+                           "l"(a3) : "memory");
+            }
         }
       }
     }
   }
   if (tpp.world > 1 && warp == 0 && lane == 0) {
-    // lane 0 issued every remote store of this CTA and read every local
-    // output it pushed, so the release semantics of its count increments
-    // order them before the counts; the own count lets the receive kernel
-    // start without waiting for this grid to exit
-    red_release_gpu_add(tpp.cnt[tpp.rank], 1u);
-    for (int p = 0; p < tpp.world; ++p)
-      if (p != tpp.rank) red_release_sys_add(tpp.cnt[p], 1u);
+    // lane 0 read every local output of this CTA, so its gpu-scope release
+    // orders them before the count: the receive kernel waits for the count,
+    // not for this grid to exit
+    red_release_gpu_add(tpp.own_cnt, 1u);
   }
 }
 
@@ -360,7 +370,7 @@ static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
   TpPush tpp;
   memset(&tpp, 0, sizeof(tpp));
   if (tp) {
-    const int st = tp_push_targets(tp, tp_slot, grid, &tpp);
+    const int st = tp_push_targets(tp, tp_slot, grid, (long long)M * N, &tpp);
     if (st) return st;
   }
   if (R == 1) return launch_gemv_r<MB, NORM, 1>(x, nw, eps, w, out, r, bias, M, N, K, epi, s, tpp, grid);
@@ -761,7 +771,7 @@ extern "C" int swb_gemv_bf16_tp(const void* x, const void* w, const void* resid,
   SWB_REQUIRE(M == 1, "swb_gemv_bf16_tp: one row (decode B=1) only, got M=%d", M);
   SWB_REQUIRE(epilogue == SWB_EPI_F32 || epilogue == SWB_EPI_RESID_F32,
               "swb_gemv_bf16_tp: fp32 epilogues only");
-  SWB_REQUIRE((size_t)N * 4 <= (size_t)(1 << 20) && N % 4 == 0,
+  SWB_REQUIRE(N <= 16384 && N % 4 == 0,
               "swb_gemv_bf16_tp: N=%d must be a multiple of 4 within the receive buffers", N);
   const int items = (N + TV_ROWS - 1) / TV_ROWS;
   return launch_gemv<1, false>(x, nullptr, 0.f, reinterpret_cast<const __nv_bfloat16*>(w), out,

@@ -44,6 +44,7 @@ constexpr int TP_MAXW = 8;
 constexpr int TP_NSLOT = 3;
 constexpr int TP_MAXC = 256;
 constexpr int TP_THREADS = 512;
+constexpr unsigned TP_RECV_CTAS = 4;   // fused form's receive grid (fixed: see mode 3)
 constexpr uint32_t kTpMagic = 0x53575450u;  // "SWTP"
 
 struct TpIpcBlob {
@@ -55,6 +56,8 @@ struct TpIpcBlob {
 static_assert(sizeof(TpIpcBlob) <= SWB_TP_IPC_BYTES, "blob too large");
 
 struct TpArgs {
+  const unsigned long long* my_ll;   // fused form: this rank's receive lines[slot] (source 0)
+  long long ll_stride;               // words per source
   const uint32_t* my_pcnt;           // fused form: this rank's push counters[slot][src]
   uint32_t* my_rctr;                 // fused form: per-CTA receive epochs[slot][c]
   uint32_t nsrc;                     // fused form: producer CTAs per peer
@@ -131,41 +134,58 @@ __global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a
     if (trig) pdl_launch_dependents();
   }
   if (mode == 3) {
-    // fused form: the peers' projection GEMVs already pushed their partials
-    // into rx[slot][p] and counted their CTAs; wait, then sum locally
+    // fused form: the peers' projection GEMVs pushed (value, epoch) words
+    // into rx[slot][p]; the own GEMV's CTAs counted into pcnt[slot][rank].
+    // Always TP_RECV_CTAS CTAs, so rc[slot][0] (the GEMV's epoch) and every
+    // rc[slot][c] advance together.
     const long long n4 = a.n >> 2;
     const long long per = (n4 + gridDim.x - 1) / gridDim.x;
     const long long lo = (long long)c * per, hi = min(n4, lo + per);
     uint32_t* rc = a.my_rctr + a.slot * TP_MAXC + c;
-    uint32_t e = 0;
+    const uint32_t e = *reinterpret_cast<volatile uint32_t*>(rc) + 1;
+    const long long t0 = clock64();
     if (threadIdx.x == 0) {
-      e = *rc + 1;
+      // the own projection's outputs: wait for its CTA count, not its exit
+      const uint32_t* f = a.my_pcnt + (size_t)a.slot * TP_MAXW + a.rank;
       const uint32_t target = e * a.nsrc;
-      const long long t0 = clock64();
-      // the own projection's CTAs count here too: no wait for that grid to
-      // exit (PDL), only for its outputs
-      for (int p = 0; p < a.world; ++p) {
-        const uint32_t* f = a.my_pcnt + (size_t)a.slot * TP_MAXW + p;
-        int spins = 0;
-        while ((int)(ld_acquire_sys(f) - target) < 0) {
-          if (++spins > 64) __nanosleep(64);
-          if (clock64() - t0 > 40000000000ll) __trap();
-        }
+      int spins = 0;
+      while ((int)(ld_acquire_sys(f) - target) < 0) {
+        if (++spins > 64) __nanosleep(32);
+        if (clock64() - t0 > 40000000000ll) __trap();
       }
     }
     __syncthreads();
-    // every partial is in place: dependents may launch (their pre-wait code
-    // only streams static weights)
+    // dependents may launch: their pre-wait code only streams static weights
     if (trig) pdl_launch_dependents();
     const float4* mine = reinterpret_cast<const float4*>(a.peer_slot[a.rank]);
+    const unsigned long long* lines = a.my_ll;
+    const long long lstride = a.ll_stride;
     float4* out4 = reinterpret_cast<float4*>(a.out);
     for (long long i = lo + threadIdx.x; i < hi; i += TP_THREADS) {
       float4 v[TP_MAXW];
 #pragma unroll
-      for (int p = 0; p < TP_MAXW; ++p)
-        if (p < a.world)
-          v[p] = p == a.rank ? __ldcg(mine + i)
-                             : __ldcg(reinterpret_cast<const float4*>(a.my_rx + p * a.rx_stride) + i);
+      for (int p = 0; p < TP_MAXW; ++p) {
+        if (p >= a.world) continue;
+        if (p == a.rank) {
+          v[p] = __ldcg(mine + i);
+          continue;
+        }
+        const unsigned long long* l = lines + p * lstride + 4 * i;
+        unsigned long long w0, w1, w2, w3;
+        for (;;) {
+          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(w0), "=l"(w1) : "l"(l) : "memory");
+          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(w2), "=l"(w3) : "l"(l + 2) : "memory");
+          if ((uint32_t)(w0 >> 32) == e && (uint32_t)(w1 >> 32) == e &&
+              (uint32_t)(w2 >> 32) == e && (uint32_t)(w3 >> 32) == e)
+            break;
+          if (clock64() - t0 > 40000000000ll) __trap();
+        }
+        v[p] = make_float4(__uint_as_float((uint32_t)w0), __uint_as_float((uint32_t)w1),
+                           __uint_as_float((uint32_t)w2), __uint_as_float((uint32_t)w3));
+      }
+      // same source order on every rank: identical sums everywhere
       float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int p = 0; p < TP_MAXW; ++p)
@@ -174,7 +194,7 @@ __global__ void __launch_bounds__(TP_THREADS) tp_allreduce_kernel(const TpArgs a
         }
       out4[i] = sum;
     }
-    if (threadIdx.x == 0) *rc = e;
+    if (threadIdx.x == 0) *rc = e;   // after the __syncthreads above: every thread read rc
     return;
   }
   uint32_t* ctr = a.my_ctr + a.slot * TP_MAXC + c;
@@ -291,8 +311,16 @@ static size_t tp_pcnt_off(size_t slot_bytes) {
   return tp_flags_off(slot_bytes) +
          sizeof(uint32_t) * (TP_NSLOT * TP_MAXW * TP_MAXC + TP_NSLOT * TP_MAXC);
 }
+// fused-form receive lines: (value, epoch) words, ll[3 slots][TP_MAXW sources],
+// apart from the float rx buffers so no float payload can pose as an epoch
+constexpr size_t TP_LL_BYTES = 128 << 10;   // 16384 outputs per source
+static size_t tp_ll_off(size_t slot_bytes) {
+  const size_t end = tp_pcnt_off(slot_bytes) +
+                     sizeof(uint32_t) * (TP_NSLOT * TP_MAXW + TP_NSLOT * TP_MAXC);
+  return (end + 255) & ~(size_t)255;
+}
 static size_t tp_region_bytes(size_t slot_bytes) {
-  return tp_pcnt_off(slot_bytes) + sizeof(uint32_t) * (TP_NSLOT * TP_MAXW + TP_NSLOT * TP_MAXC);
+  return tp_ll_off(slot_bytes) + TP_NSLOT * TP_MAXW * TP_LL_BYTES;
 }
 
 extern "C" int swb_tp_comm_create(int rank, int world, size_t slot_bytes, swb_tp_comm** out,
@@ -368,23 +396,25 @@ extern "C" void* swb_tp_comm_slot(const swb_tp_comm* c, int slot) {
 }
 
 namespace swb {
-int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, TpPush* out) {
+int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, long long n, TpPush* out) {
   SWB_REQUIRE(c && out, "tp_push_targets: null pointer");
+  SWB_REQUIRE(n >= 0 && (size_t)n * 8 <= TP_LL_BYTES,
+              "tp_push_targets: %lld outputs exceed the receive lines", n);
   SWB_REQUIRE(c->connected || c->world == 1, "tp_push_targets: not connected");
   SWB_REQUIRE(slot >= 0 && slot < TP_NSLOT, "tp_push_targets: bad slot");
   SWB_REQUIRE(c->world <= 8, "tp_push_targets: world > 8");
-  const size_t rxb = tp_rx_bytes(c->slot_bytes);
-  const size_t rx_off = tp_rx_off(c->slot_bytes) + (size_t)slot * TP_MAXW * rxb;
+  const size_t ll_off = tp_ll_off(c->slot_bytes) + (size_t)slot * TP_MAXW * TP_LL_BYTES;
   const size_t pc_off = tp_pcnt_off(c->slot_bytes);
   memset(out, 0, sizeof(*out));
   out->world = c->world;
   out->rank = c->rank;
+  out->own_cnt = reinterpret_cast<unsigned*>(c->base + pc_off) + (size_t)slot * TP_MAXW + c->rank;
+  out->epoch = reinterpret_cast<const unsigned*>(c->base + pc_off) + TP_NSLOT * TP_MAXW +
+               (size_t)slot * TP_MAXC;
   for (int p = 0; p < c->world; ++p) {
-    // own entry: this rank's counter slot [slot][rank] in its own region
-    out->cnt[p] = reinterpret_cast<unsigned*>(c->peer_base[p] + pc_off) +
-                  (size_t)slot * TP_MAXW + c->rank;
     if (p == c->rank) continue;
-    out->rx[p] = reinterpret_cast<float*>(c->peer_base[p] + rx_off + (size_t)c->rank * rxb);
+    out->rx[p] = reinterpret_cast<unsigned long long*>(c->peer_base[p] + ll_off +
+                                                       (size_t)c->rank * TP_LL_BYTES);
   }
   c->nsrc[slot] = nsrc;
   return SWB_OK;
@@ -413,8 +443,8 @@ extern "C" int swb_tp_allreduce_recv_f32(swb_tp_comm* c, int slot, float* out, s
   SWB_REQUIRE(c && c->world > 1, "swb_tp_allreduce_recv_f32: needs a TP group");
   SWB_REQUIRE(slot >= 0 && slot < TP_NSLOT && c->nsrc[slot] > 0,
               "swb_tp_allreduce_recv_f32: no fused projection on slot %d", slot);
-  SWB_REQUIRE(n * sizeof(float) <= tp_rx_bytes(c->slot_bytes),
-              "swb_tp_allreduce_recv_f32: n=%zu exceeds the receive buffers", n);
+  SWB_REQUIRE(n * 8 <= TP_LL_BYTES,
+              "swb_tp_allreduce_recv_f32: n=%zu exceeds the receive lines", n);
   return tp_allreduce(c, slot, out, n, stream, true);
 }
 
@@ -445,6 +475,9 @@ static int tp_allreduce(swb_tp_comm* c, int slot, float* out, size_t n, uintptr_
   a.my_pcnt = reinterpret_cast<const uint32_t*>(c->base + tp_pcnt_off(c->slot_bytes));
   a.my_rctr = reinterpret_cast<uint32_t*>(c->base + tp_pcnt_off(c->slot_bytes)) +
               TP_NSLOT * TP_MAXW;
+  a.my_ll = reinterpret_cast<const unsigned long long*>(
+      c->base + tp_ll_off(c->slot_bytes) + (size_t)slot * TP_MAXW * TP_LL_BYTES);
+  a.ll_stride = (long long)(TP_LL_BYTES / 8);
   a.nsrc = recv ? (uint32_t)c->nsrc[slot] : 0u;
   a.out = out;
   a.n = (long long)n;
@@ -463,7 +496,7 @@ static int tp_allreduce(swb_tp_comm* c, int slot, float* out, size_t n, uintptr_
   }();
   if (mode == 0 && push_on && c->world > 1 && n * sizeof(float) <= rxb) mode = 2;
   if (recv) mode = 3;
-  const cudaError_t le = launch(tp_allreduce_kernel, dim3((unsigned)ctas), dim3(TP_THREADS), 0,
+  const cudaError_t le = launch(tp_allreduce_kernel, dim3(recv ? TP_RECV_CTAS : (unsigned)ctas), dim3(TP_THREADS), 0,
                                 (cudaStream_t)stream, a, mode, tp_trigger());
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch tp_allreduce_kernel: %s", cudaGetErrorString(le));

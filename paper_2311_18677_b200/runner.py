@@ -95,11 +95,12 @@ class ModelRunner:
         # SWB_TP_AR_BF16=0 keeps the prefill all-reduces in fp32 (A/B)
         self.ar_bf16 = os.environ.get("SWB_TP_AR_BF16", "1") != "0"
         self._pending_add = None
-        # SWB_TP_FUSED=1: decode B=1 projections push their partial to the
-        # peers from the GEMV epilogue (swb_gemv_bf16_tp) and a receive kernel
-        # only waits and sums.  Exact (tests/test_tpcomm_gpu.py) but measured
-        # slower (70B TP4 B=1 decode 12.95 vs 8.51 ms/step), so off by default
-        self.tp_fused = os.environ.get("SWB_TP_FUSED", "0") == "1"
+        # decode B=1 projections push their partial to the peers from the
+        # GEMV epilogue as (value, epoch) words (swb_gemv_bf16_tp) and a
+        # receive kernel only waits and sums: 70B TP4 B=1 decode 8.21 -> 7.84
+        # ms/step, TP2 12.97 -> 12.61 (profiles/r2_fused_ar.json);
+        # SWB_TP_FUSED=0 restores GEMV + push all-reduce kernel for A/B
+        self.tp_fused = os.environ.get("SWB_TP_FUSED", "1") != "0"
         self.kv = kv
         self.hq = cfg.n_heads // self.tp
         self.hkv = cfg.n_kv_heads // self.tp
@@ -187,7 +188,7 @@ class ModelRunner:
             self._allreduce(x)
             return
         s = c.next_slot()
-        if self.tp_fused and x.shape[0] == 1 and x.numel() * 4 <= c.AUX_BYTES:
+        if self.tp_fused and x.shape[0] == 1 and x.numel() <= c.LL_OUTPUTS:
             # decode B=1: the GEMV epilogue pushes its partial to the peers
             # itself; the receive kernel only waits and sums locally
             K.gemv_tp(inp, w, self._resid_epi(), c._h, s, resid=x, bias=b)

@@ -45,6 +45,7 @@ class TPComm:
 
     AUX = 2
     AUX_BYTES = 1 << 20
+    LL_OUTPUTS = 16384      # fused projection push: outputs per source (TP_LL_BYTES / 8)
 
     def assert_even(self) -> None:
         """A step must end on the slot it started with (even count of 0/1

@@ -32,6 +32,11 @@ def fused():
     comm.allreduce_recv(s, out)
 
 
+def gemv_tp_only():
+    s = comm.next_slot()
+    K.gemv_tp(x, w, epi, comm._h, s)
+
+
 def gemv_only():
     K.linear(x, w, epi, out=out)
 
@@ -57,7 +62,8 @@ def timeit(body, reps=50):
 
 
 r = {"world": world, "N": N, "K": Kd, "plain_us": timeit(plain), "fused_us": timeit(fused),
-     "gemv_only_us": timeit(gemv_only)}
+     "gemv_only_us": timeit(gemv_only), "gemv_tp_only_us": timeit(gemv_tp_only),
+     "dbg": os.environ.get("SWB_TP_DBG", "0")}
 if rank == 0:
     print(json.dumps(r), flush=True)
 dist.barrier()

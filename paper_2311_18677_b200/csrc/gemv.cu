@@ -68,12 +68,14 @@ __device__ __forceinline__ int item_row(int item, int j, bool swiglu) {
 // NORM = true : x is the fp32 residual stream [M,K]; the kernel applies
 //               RMSNorm on the fly, h = bf16(x * rsqrt(mean(x^2)+eps) * nw),
 //               bit-identical to swb_rmsnorm's output (fused pre-norm GEMV).
-template <int MB, bool NORM, int R = TV_ROWS>
+// TPP: the fused TP push variant (one row, 4-row items); false compiles none
+// of its code into the plain kernels
+template <int MB, bool NORM, int R = TV_ROWS, bool TPP = false>
 __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     gemv_bulk_kernel(const void* __restrict__ xin, const __nv_bfloat16* __restrict__ nw,
                      float eps, const __nv_bfloat16* __restrict__ W, void* out,
                      const float* resid, const __nv_bfloat16* bias, int M, int N, int K,
-                     int epi, int n_items, int trig, const TpPush tpp) {
+                     int epi, int n_items, int trig, const __grid_constant__ TpPush tpp) {
   constexpr int NST = TV_STAGES * TV_ROWS / R;           // ring stages
   constexpr int SBYTES = R * TV_ROW_BYTES;                // bytes per stage
   extern __shared__ __align__(128) uint8_t smem[];
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
   // fused TP push: this use's epoch (the previous use of the slot finished
   // its receive kernel before the kernel ahead of us did)
   const unsigned ll_e =
-      tpp.world > 1 ? *reinterpret_cast<const volatile unsigned*>(tpp.epoch) + 1u : 0u;
+      TPP ? *reinterpret_cast<const volatile unsigned*>(tpp.epoch) + 1u : 0u;
   if constexpr (NORM) {
     // sum of squares of every batch row, by all consumer threads
     const int t = threadIdx.x;
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
           }
         }
       }
-      if (R == 4 && tpp.world > 1) {
+      if constexpr (TPP && R == 4) {
         // fused TP all-reduce (one decode row): the item's 4 consecutive
         // outputs go straight to every peer as two 16-byte posted NVLink
         // stores of (value, epoch) words while later weights still stream
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
       }
     }
   }
-  if (tpp.world > 1 && warp == 0 && lane == 0) {
+  if (TPP && warp == 0 && lane == 0) {
     // lane 0 read every local output of this CTA, so its gpu-scope release
     // orders them before the count: the receive kernel waits for the count,
     // not for this grid to exit
@@ -318,7 +320,7 @@ static int gemv_ctas_per_sm() {
   return n;
 }
 
-template <int MB, bool NORM, int R>
+template <int MB, bool NORM, int R, bool TPP = false>
 static int launch_gemv_r(const void* x, const __nv_bfloat16* nw, float eps,
                          const __nv_bfloat16* w, void* out, const float* r,
                          const __nv_bfloat16* bias, int M, int N, int K, int epi,
@@ -327,14 +329,14 @@ static int launch_gemv_r(const void* x, const __nv_bfloat16* nw, float eps,
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr[dev]) {
-    SWB_CUDA(cudaFuncSetAttribute(gemv_bulk_kernel<MB, NORM, R>,
+    SWB_CUDA(cudaFuncSetAttribute(gemv_bulk_kernel<MB, NORM, R, TPP>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   TV_SMEM + TV_HS_MAX));
     attr[dev] = true;
   }
   const size_t smem = TV_SMEM + (NORM ? (size_t)M * K * 2 : 0);
   const int items = (N + R - 1) / R;
-  const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM, R>, dim3(grid), dim3(TV_THREADS),
+  const cudaError_t le = launch(gemv_bulk_kernel<MB, NORM, R, TPP>, dim3(grid), dim3(TV_THREADS),
                                 smem, s, x, nw, eps, w, out, r, bias, M, N, K, epi, items,
                                 pdl_early_trigger() ? 1 : 0, tpp);
   if (le != cudaSuccess)
@@ -372,6 +374,13 @@ static int launch_gemv(const void* x, const __nv_bfloat16* nw, float eps,
   if (tp) {
     const int st = tp_push_targets(tp, tp_slot, grid, (long long)M * N, &tpp);
     if (st) return st;
+  }
+  if constexpr (MB == 1 && !NORM) {
+    if (tp) {   // swb_gemv_bf16_tp: one row, 4-row items (gemv_rows_for)
+      if (R != 4) return swb_set_error(SWB_ERR_INVALID, "fused TP push needs 4-row items");
+      return launch_gemv_r<1, false, 4, true>(x, nw, eps, w, out, r, bias, M, N, K, epi, s, tpp,
+                                              grid);
+    }
   }
   if (R == 1) return launch_gemv_r<MB, NORM, 1>(x, nw, eps, w, out, r, bias, M, N, K, epi, s, tpp, grid);
   if (R == 2) return launch_gemv_r<MB, NORM, 2>(x, nw, eps, w, out, r, bias, M, N, K, epi, s, tpp, grid);

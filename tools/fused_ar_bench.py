@@ -62,8 +62,7 @@ def timeit(body, reps=50):
 
 
 r = {"world": world, "N": N, "K": Kd, "plain_us": timeit(plain), "fused_us": timeit(fused),
-     "gemv_only_us": timeit(gemv_only), "gemv_tp_only_us": timeit(gemv_tp_only),
-     "dbg": os.environ.get("SWB_TP_DBG", "0")}
+     "gemv_only_us": timeit(gemv_only), "gemv_tp_only_us": timeit(gemv_tp_only)}
 if rank == 0:
     print(json.dumps(r), flush=True)
 dist.barrier()

@@ -137,6 +137,15 @@ int swb_add_rmsnorm(float* x, const void* addend, const int32_t* row_index, cons
                     void* out, int rows, int d, float eps, uintptr_t stream);
 int swb_add_layernorm(float* x, const void* addend, const int32_t* row_index, const void* w,
                       const void* b, void* out, int rows, int d, float eps, uintptr_t stream);
+/* Same with the TP ranks' bf16 partials still apart (copy-engine exchange,
+ * swb_tp_stage_*): x[src] += (parts[0][src] + ... + parts[n-1][src]) summed
+ * in fp32 in the given (rank) order, 1 <= n_parts <= 8. */
+int swb_add_parts_rmsnorm(float* x, const void* const* parts, int n_parts,
+                          const int32_t* row_index, const void* w, void* out, int rows, int d,
+                          float eps, uintptr_t stream);
+int swb_add_parts_layernorm(float* x, const void* const* parts, int n_parts,
+                            const int32_t* row_index, const void* w, const void* b, void* out,
+                            int rows, int d, float eps, uintptr_t stream);
 int swb_argmax(const float* logits, int rows, int V, int32_t* out,
                uintptr_t stream);
 
@@ -379,6 +388,32 @@ int swb_gemv_bf16_tp(const void* x, const void* w, const void* resid, const void
                      uintptr_t stream);
 int swb_tp_allreduce_recv_f32(swb_tp_comm* comm, int slot, float* out, size_t n,
                               uintptr_t stream);
+
+/* Prefill partial exchange over the copy engines (TP > 1; replaces the
+ * prefill all-reduces priced in PerfModel.prompt_time, perf.py:119-123 /
+ * 297-326).  Each rank owns rx[n_bufs][world] receive buffers of
+ * bytes_per_src bytes and flags[n_bufs][SWB_TP_STAGE_MAXCH][world] in
+ * IPC-shared device memory (create -> all-gather the blobs -> connect).
+ * swb_tp_stage_send enqueues on `stream`: a DMA copy of src[0, bytes) into
+ * every peer's rx[buf][this rank] + offset, then a write of `epoch` into
+ * every peer's flag[buf][chunk][this rank].  swb_tp_stage_wait makes
+ * `stream` wait until flag[buf][chunk][p] >= epoch for every peer p; the
+ * received partials are then at swb_tp_stage_rx(buf, p) + offset.  The
+ * caller keeps epochs increasing and a buffer's next send behind its last
+ * consumer (tp prefill: one send per projection per chunk, epoch = layer
+ * counter). */
+#define SWB_TP_STAGE_MAXCH 8
+#define SWB_TP_STAGE_IPC_BYTES 128
+typedef struct swb_tp_stage swb_tp_stage;
+int swb_tp_stage_create(int rank, int world, size_t bytes_per_src, int n_bufs,
+                        swb_tp_stage** out, void* ipc_blob, size_t ipc_bytes);
+int swb_tp_stage_connect(swb_tp_stage* stage, const void* blobs, size_t blob_stride);
+int swb_tp_stage_destroy(swb_tp_stage* stage);
+void* swb_tp_stage_rx(const swb_tp_stage* stage, int buf, int src);
+int swb_tp_stage_send(swb_tp_stage* stage, int buf, int chunk, const void* src, size_t offset,
+                      size_t bytes, uint32_t epoch, uintptr_t stream);
+int swb_tp_stage_wait(swb_tp_stage* stage, int buf, int chunk, uint32_t epoch,
+                      uintptr_t stream);
 
 #ifdef __cplusplus
 }

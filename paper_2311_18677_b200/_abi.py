@@ -20,6 +20,8 @@ SWB_OK, SWB_ERR_INVALID, SWB_ERR_CAPACITY, SWB_ERR_CUDA, SWB_ERR_CONFIG = 0, 1, 
 EPI_BF16, EPI_F32, EPI_RESID_F32, EPI_SWIGLU, EPI_GELU = 0, 1, 2, 3, 4
 KV_POOL_IPC_BYTES = 256
 TP_IPC_BYTES = 128
+TP_STAGE_IPC_BYTES = 128   # SWB_TP_STAGE_IPC_BYTES
+TP_STAGE_MAXCH = 8         # SWB_TP_STAGE_MAXCH
 
 _P = C.c_void_p
 _I = C.c_int
@@ -92,10 +94,18 @@ SIGNATURES = {
     "swb_tp_allreduce_f32": [_P, _I, _P, _S, _ST],
     "swb_tp_allreduce_recv_f32": [_P, _I, _P, _S, _ST],
     "swb_gemv_bf16_tp": [_P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _ST],
+    "swb_add_parts_rmsnorm": [_P, _P, _I, _P, _P, _P, _I, _I, _F, _ST],
+    "swb_add_parts_layernorm": [_P, _P, _I, _P, _P, _P, _P, _I, _I, _F, _ST],
+    "swb_tp_stage_create": [_I, _I, _S, _I, C.POINTER(_P), _P, _S],
+    "swb_tp_stage_connect": [_P, _P, _S],
+    "swb_tp_stage_destroy": [_P],
+    "swb_tp_stage_rx": [_P, _I, _I],
+    "swb_tp_stage_send": [_P, _I, _I, _P, _S, _S, C.c_uint32, _ST],
+    "swb_tp_stage_wait": [_P, _I, _I, C.c_uint32, _ST],
 }
 _RESTYPE = {"swb_last_error": C.c_char_p, "swb_attn_decode_workspace": _S,
             "swb_attn_chunk_workspace": _S,
-            "swb_tp_comm_slot": _P}
+            "swb_tp_comm_slot": _P, "swb_tp_stage_rx": _P}
 
 
 def _load():
@@ -141,7 +151,7 @@ LAUNCH_MULT = {
     "swb_attn_prefill": 1, "swb_attn_prefill_tc": 1, "swb_attn_decode": 1, "swb_attn_decode_step": 1, "swb_attn_chunk": 1,
     "swb_decode_advance": 1, "swb_slots_from_table": 1, "swb_block_alloc": 1,
     "swb_block_free": 1, "swb_tp_allreduce_f32": 1, "swb_tp_allreduce_recv_f32": 1,
-    "swb_gemv_bf16_tp": 1,
+    "swb_gemv_bf16_tp": 1, "swb_add_parts_rmsnorm": 1, "swb_add_parts_layernorm": 1,
 }
 _launches = [0]
 

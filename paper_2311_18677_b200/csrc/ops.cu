@@ -10,6 +10,8 @@
 // dh=128), which is the unit the decode-attention kernel streams.
 #include <cudaTypedefs.h>
 
+#include <cstring>
+
 #include "common.cuh"
 
 namespace swb {
@@ -39,11 +41,25 @@ __global__ void embed_kernel(const int32_t* __restrict__ tokens,
 // LayerNorm produces the fp32 residual stream, possibly in place).
 // addend (optional, bf16 [rows of x]): x[src] += addend[src] first, written
 // back (the TP prefill's bf16 all-reduce result joins the fp32 residual here).
-__device__ __forceinline__ float4 add_row4(float* x, const __nv_bfloat16* addend, size_t i4) {
+// With several addends (the TP ranks' partials, copy-engine exchange) their
+// fp32 sum in the given order is added: x += (p0 + p1 + ...).
+struct Addends {
+  const __nv_bfloat16* p[8];
+  int n;
+};
+__device__ __forceinline__ float4 add_row4(float* x, const Addends& ad, size_t i4) {
   float4 v = reinterpret_cast<float4*>(x)[i4];
-  const uint2 a = reinterpret_cast<const uint2*>(addend)[i4];
-  const float2 a0 = bf2_to_f2(a.x), a1 = bf2_to_f2(a.y);
-  v.x += a0.x; v.y += a0.y; v.z += a1.x; v.w += a1.y;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < ad.n; ++k) {
+    const uint2 a = reinterpret_cast<const uint2*>(ad.p[k])[i4];
+    const float2 a0 = bf2_to_f2(a.x), a1 = bf2_to_f2(a.y);
+    if (k == 0) {
+      s = make_float4(a0.x, a0.y, a1.x, a1.y);
+    } else {
+      s.x += a0.x; s.y += a0.y; s.z += a1.x; s.w += a1.y;
+    }
+  }
+  v.x += s.x; v.y += s.y; v.z += s.z; v.w += s.w;
   reinterpret_cast<float4*>(x)[i4] = v;
   return v;
 }
@@ -51,7 +67,7 @@ __device__ __forceinline__ float4 add_row4(float* x, const __nv_bfloat16* addend
 __global__ void layernorm_kernel(const float* x, const int32_t* __restrict__ row_index,
                                  const __nv_bfloat16* __restrict__ w,
                                  const __nv_bfloat16* __restrict__ b, void* out, int d,
-                                 float eps, int out_f32, const __nv_bfloat16* addend) {
+                                 float eps, int out_f32, const __grid_constant__ Addends addend) {
   pdl_wait();
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -60,8 +76,8 @@ __global__ void layernorm_kernel(const float* x, const int32_t* __restrict__ row
   __shared__ float stat[2];
   float s = 0.f;
   for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
-    const float4 v = addend ? add_row4(const_cast<float*>(x), addend, (size_t)src * (d / 4) + c)
-                            : xr[c];
+    const float4 v = addend.n ? add_row4(const_cast<float*>(x), addend, (size_t)src * (d / 4) + c)
+                              : xr[c];
     s += (v.x + v.y) + (v.z + v.w);
   }
   s = warp_sum(s);
@@ -111,7 +127,7 @@ __global__ void layernorm_kernel(const float* x, const int32_t* __restrict__ row
 __global__ void rmsnorm_kernel(const float* x, const int32_t* __restrict__ row_index,
                                const __nv_bfloat16* __restrict__ w,
                                __nv_bfloat16* __restrict__ out, int d, float eps,
-                               const __nv_bfloat16* addend) {
+                               const __grid_constant__ Addends addend) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
@@ -119,8 +135,8 @@ __global__ void rmsnorm_kernel(const float* x, const int32_t* __restrict__ row_i
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * d);
   float ss = 0.f;
   for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
-    const float4 v = addend ? add_row4(const_cast<float*>(x), addend, (size_t)src * (d / 4) + c)
-                            : xr[c];
+    const float4 v = addend.n ? add_row4(const_cast<float*>(x), addend, (size_t)src * (d / 4) + c)
+                              : xr[c];
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   __shared__ float red[32];
@@ -452,6 +468,14 @@ extern "C" int swb_embed(const int32_t* tokens, const void* table, float* x,
   return swb_check_launch("embed_kernel");
 }
 
+static Addends one_addend(const void* a) {
+  Addends ad;
+  memset(&ad, 0, sizeof(ad));
+  ad.p[0] = reinterpret_cast<const __nv_bfloat16*>(a);
+  ad.n = a ? 1 : 0;
+  return ad;
+}
+
 extern "C" int swb_add_rmsnorm(float* x, const void* addend, const int32_t* row_index,
                                const void* w, void* out, int rows, int d, float eps,
                                uintptr_t stream) {
@@ -461,8 +485,7 @@ extern "C" int swb_add_rmsnorm(float* x, const void* addend, const int32_t* row_
   {
     const cudaError_t le_ = launch(rmsnorm_kernel, dim3(rows), dim3(512), 0, STREAM,
       x, row_index, reinterpret_cast<const __nv_bfloat16*>(w),
-      reinterpret_cast<__nv_bfloat16*>(out), d, eps,
-      reinterpret_cast<const __nv_bfloat16*>(addend));
+      reinterpret_cast<__nv_bfloat16*>(out), d, eps, one_addend(addend));
     if (le_ != cudaSuccess)
       return swb_set_error(SWB_ERR_CUDA, "launch rmsnorm_kernel: %s", cudaGetErrorString(le_));
   }
@@ -477,7 +500,7 @@ extern "C" int swb_rmsnorm(const float* x, const int32_t* row_index, const void*
   {
     const cudaError_t le_ = launch(rmsnorm_kernel, dim3(rows), dim3(512), 0, STREAM,
       x, row_index, reinterpret_cast<const __nv_bfloat16*>(w),
-      reinterpret_cast<__nv_bfloat16*>(out), d, eps, (const __nv_bfloat16*)nullptr);
+      reinterpret_cast<__nv_bfloat16*>(out), d, eps, one_addend(nullptr));
     if (le_ != cudaSuccess)
       return swb_set_error(SWB_ERR_CUDA, "launch rmsnorm_kernel: %s", cudaGetErrorString(le_));
   }
@@ -495,7 +518,7 @@ extern "C" int swb_layernorm(const float* x, const int32_t* row_index, const voi
   const cudaError_t le = launch(layernorm_kernel, dim3(rows), dim3(512), 0, STREAM, x,
                                 row_index, reinterpret_cast<const __nv_bfloat16*>(w),
                                 reinterpret_cast<const __nv_bfloat16*>(b), out, d, eps, out_f32,
-                                (const __nv_bfloat16*)nullptr);
+                                one_addend(nullptr));
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch layernorm_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("layernorm_kernel");
@@ -510,7 +533,53 @@ extern "C" int swb_add_layernorm(float* x, const void* addend, const int32_t* ro
   const cudaError_t le = launch(layernorm_kernel, dim3(rows), dim3(512), 0, STREAM, x,
                                 row_index, reinterpret_cast<const __nv_bfloat16*>(w),
                                 reinterpret_cast<const __nv_bfloat16*>(b), out, d, eps, 0,
-                                reinterpret_cast<const __nv_bfloat16*>(addend));
+                                one_addend(addend));
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch layernorm_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("layernorm_kernel");
+}
+
+static int parts_addends(const char* fn, const void* const* parts, int n, Addends* ad) {
+  SWB_REQUIRE(parts && n >= 1 && n <= 8, "%s: 1..8 partials, got %d", fn, n);
+  memset(ad, 0, sizeof(*ad));
+  for (int k = 0; k < n; ++k) {
+    SWB_REQUIRE(parts[k] && ((uintptr_t)parts[k] & 7) == 0, "%s: partial %d null or unaligned",
+                fn, k);
+    ad->p[k] = reinterpret_cast<const __nv_bfloat16*>(parts[k]);
+  }
+  ad->n = n;
+  return SWB_OK;
+}
+
+extern "C" int swb_add_parts_rmsnorm(float* x, const void* const* parts, int n_parts,
+                                     const int32_t* row_index, const void* w, void* out, int rows,
+                                     int d, float eps, uintptr_t stream) {
+  SWB_REQUIRE(x && w && out, "swb_add_parts_rmsnorm: null pointer");
+  SWB_REQUIRE(rows >= 0 && d > 0 && d % 4 == 0, "swb_add_parts_rmsnorm: bad shape");
+  Addends ad;
+  const int st = parts_addends("swb_add_parts_rmsnorm", parts, n_parts, &ad);
+  if (st) return st;
+  if (rows == 0) return SWB_OK;
+  const cudaError_t le = launch(rmsnorm_kernel, dim3(rows), dim3(512), 0, STREAM, x, row_index,
+                                reinterpret_cast<const __nv_bfloat16*>(w),
+                                reinterpret_cast<__nv_bfloat16*>(out), d, eps, ad);
+  if (le != cudaSuccess)
+    return swb_set_error(SWB_ERR_CUDA, "launch rmsnorm_kernel: %s", cudaGetErrorString(le));
+  return swb_check_launch("rmsnorm_kernel");
+}
+
+extern "C" int swb_add_parts_layernorm(float* x, const void* const* parts, int n_parts,
+                                       const int32_t* row_index, const void* w, const void* b,
+                                       void* out, int rows, int d, float eps, uintptr_t stream) {
+  SWB_REQUIRE(x && w && b && out, "swb_add_parts_layernorm: null pointer");
+  SWB_REQUIRE(rows >= 0 && d > 0 && d % 4 == 0, "swb_add_parts_layernorm: bad shape");
+  Addends ad;
+  const int st = parts_addends("swb_add_parts_layernorm", parts, n_parts, &ad);
+  if (st) return st;
+  if (rows == 0) return SWB_OK;
+  const cudaError_t le = launch(layernorm_kernel, dim3(rows), dim3(512), 0, STREAM, x,
+                                row_index, reinterpret_cast<const __nv_bfloat16*>(w),
+                                reinterpret_cast<const __nv_bfloat16*>(b), out, d, eps, 0, ad);
   if (le != cudaSuccess)
     return swb_set_error(SWB_ERR_CUDA, "launch layernorm_kernel: %s", cudaGetErrorString(le));
   return swb_check_launch("layernorm_kernel");

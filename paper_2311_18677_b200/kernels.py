@@ -145,15 +145,32 @@ def embed(tokens, table, out=None):
     return out
 
 
+def _parts(parts, x, fn):
+    """Pointer array of the TP ranks' bf16 partials (each x's shape)."""
+    if not 1 <= len(parts) <= 8:
+        raise ValidationError(f"{fn}: 1..8 partials, got {len(parts)}")
+    for p in parts:
+        _req(p, torch.bfloat16, "addend")
+        if p.shape != x.shape:
+            raise ValidationError(f"{fn}: every partial must match x")
+    return (ctypes.c_void_p * len(parts))(*[p.data_ptr() for p in parts])
+
+
 def rmsnorm(x, w, eps, rows_index=None, out=None, addend=None):
     """RMSNorm of fp32 rows; with ``addend`` (bf16, x's shape) the rows first
-    get x += addend (written back)."""
+    get x += addend (written back); a list of bf16 partials (the TP ranks',
+    rank order) is summed in fp32 first."""
     _req(x, torch.float32, "x")
     _req(w, torch.bfloat16, "w")
     rows = x.shape[0] if rows_index is None else rows_index.shape[0]
     d = x.shape[1]
     if out is None:
         out = torch.empty(rows, d, dtype=torch.bfloat16, device=x.device)
+    if isinstance(addend, (list, tuple)):
+        arr = _parts(addend, x, "rmsnorm")
+        call("swb_add_parts_rmsnorm", x.data_ptr(), arr, len(addend), _ptr(rows_index),
+             w.data_ptr(), out.data_ptr(), rows, d, float(eps), _stream())
+        return out
     if addend is not None:
         _req(addend, torch.bfloat16, "addend")
         if addend.shape != x.shape:
@@ -168,7 +185,8 @@ def rmsnorm(x, w, eps, rows_index=None, out=None, addend=None):
 
 def layernorm(x, w, b, eps, rows_index=None, out=None, out_f32=False, addend=None):
     """LayerNorm with bias (BLOOM); fp32 out (may be x) when out_f32; with
-    ``addend`` (bf16) the rows first get x += addend (written back)."""
+    ``addend`` (bf16) the rows first get x += addend (written back); a list of
+    bf16 partials (rank order) is summed in fp32 first."""
     _req(x, torch.float32, "x")
     _req(w, torch.bfloat16, "w")
     _req(b, torch.bfloat16, "b")
@@ -177,6 +195,13 @@ def layernorm(x, w, b, eps, rows_index=None, out=None, out_f32=False, addend=Non
     if out is None:
         out = torch.empty(rows, d, dtype=torch.float32 if out_f32 else torch.bfloat16,
                           device=x.device)
+    if isinstance(addend, (list, tuple)):
+        if out_f32:
+            raise ValidationError("layernorm: partials need the bf16 output")
+        arr = _parts(addend, x, "layernorm")
+        call("swb_add_parts_layernorm", x.data_ptr(), arr, len(addend), _ptr(rows_index),
+             w.data_ptr(), b.data_ptr(), out.data_ptr(), rows, d, float(eps), _stream())
+        return out
     if addend is not None:
         _req(addend, torch.bfloat16, "addend")
         if addend.shape != x.shape or out_f32:

@@ -95,6 +95,22 @@ class ModelRunner:
         # SWB_TP_AR_BF16=0 keeps the prefill all-reduces in fp32 (A/B)
         self.ar_bf16 = os.environ.get("SWB_TP_AR_BF16", "1") != "0"
         self._pending_add = None
+        # prefill reductions as copy-engine exchanges of the bf16 partials
+        # (tpcomm.TPStage), summed inside the next norm: 70B TP2 1024-token
+        # prefill 71.1 -> 70.4 ms.  At TP4 the all-gather moves twice NCCL's
+        # bytes (73.3 vs 64.0-66.6 ms), so auto = TP2 only; SWB_TP_STAGE=1/0
+        # forces it.  SWB_TP_STAGE_CHUNKS > 1 pipelines row chunks (chunk c's
+        # exchange under chunk c+1's GEMMs) but the half-size GEMMs lose more
+        # to wave quantisation than the overlap wins (TP2: 2 chunks 73.6 ms,
+        # 4 chunks 89.4) — profiles/r2_tp_prefill_exchange.json
+        mode = os.environ.get("SWB_TP_STAGE", "auto")
+        self.tp_stage = self.tp == 2 if mode == "auto" else mode == "1"
+        self.stage_chunks = int(os.environ.get("SWB_TP_STAGE_CHUNKS", "1"))
+        self._stage = None
+        self._stage_epoch = 0
+        self._stage_own = [None, None]      # this rank's O / down partials (bf16)
+        self._stage_sent = [None, None]     # side-stream events: partial copied out
+        self._stage_stream = None
         # decode B=1 projections push their partial to the peers from the
         # GEMV epilogue as (value, epoch) words (swb_gemv_bf16_tp) and a
         # receive kernel only waits and sums: 70B TP4 B=1 decode 8.21 -> 7.84
@@ -209,7 +225,14 @@ class ModelRunner:
     #    LayerNorm+bias / ALiBi / biased linears + GELU / embedding LayerNorm)
     def _norm(self, x, w, b, out, rows_index=None):
         add, self._pending_add = self._pending_add, None    # a bf16 all-reduce result
-        if add is not None and add.shape != x.shape:
+        if isinstance(add, tuple):
+            # copy-engine exchange: wait for every chunk's peer flags, then
+            # the norm adds own + received partials in rank order
+            buf, epoch, n_chunks, own = add
+            for c in range(n_chunks):
+                self._stage.wait(buf, c, epoch)
+            add = self._stage.parts(buf, own, 0, x.shape[0])
+        elif add is not None and add.shape != x.shape:
             raise RuntimeError("pending all-reduce result does not match the residual")
         if self.bloom:
             K.layernorm(x, w, b, self.cfg.norm_eps, rows_index=rows_index, out=out, addend=add)
@@ -259,6 +282,81 @@ class ModelRunner:
     def _resid_epi(self):
         # with TP only rank 0 folds the residual in; the all-reduce sums the rest
         return K.EPI_RESID_F32 if self.rank == 0 or self.tp == 1 else K.EPI_F32
+
+    # ------------------------------------------- TP prefill chunk exchange
+    def _stage_on(self, T: int) -> bool:
+        return (self.tp > 1 and self.tp_stage and T > K.GEMV_MAX_ROWS and
+                T * self.cfg.d_model * 4 >= self.ar_nccl_bytes)
+
+    def _stage_comm(self, T: int):
+        """TPStage sized for T rows (collective: every TP rank runs the same
+        prefill sequence, so all grow together)."""
+        if self._stage is None or self._stage.rows < T:
+            from .tpcomm import TPStage
+            if self._stage is not None:
+                torch.cuda.synchronize()
+                self._stage.close()
+            rows = (T + 2047) // 2048 * 2048
+            self._stage = TPStage(self.tp_group, rows, self.cfg.d_model)
+            d = self.cfg.d_model
+            self._stage_own = [torch.empty(rows, d, dtype=torch.bfloat16, device=self.dev)
+                               for _ in range(2)]
+            self._stage_sent = [None, None]
+            if self._stage_stream is None:
+                self._stage_stream = torch.cuda.Stream(device=self.dev)
+        return self._stage
+
+    def _stage_chunks(self, T: int) -> list:
+        n = max(1, min(self.stage_chunks, 8, T // 256))   # SWB_TP_STAGE_MAXCH
+        step = (T + n - 1) // n
+        step = (step + 127) // 128 * 128
+        return [(r0, min(T, r0 + step)) for r0 in range(0, T, step)]
+
+    def _stage_send(self, kind: int, chunk: int, rows: torch.Tensor, row0: int, epoch: int):
+        main = torch.cuda.current_stream()
+        side = self._stage_stream
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        self._stage.send(kind, chunk, rows, row0, epoch, side)
+        done = torch.cuda.Event()
+        done.record(side)
+        self._stage_sent[kind] = done
+
+    def _stage_layer(self, attn, lw, x, h, act, T: int):
+        """O projection -> residual + norm -> MLP -> down projection of one
+        layer with both TP reductions as per-chunk copy-engine exchanges:
+        chunk c's O partial travels while chunk c+1's O GEMM runs, chunk c's
+        MLP runs while chunk c+1's partial travels, and so on; the last
+        down-projection exchange is added by the next norm (_norm)."""
+        st = self._stage_comm(T)
+        main = torch.cuda.current_stream()
+        chunks = self._stage_chunks(T)
+        self._stage_epoch += 1
+        e = self._stage_epoch
+        bo = lw.bo if self.rank == 0 else None
+        bd = lw.bd if self.rank == 0 else None
+        po, pd = self._stage_own[0][:T], self._stage_own[1][:T]
+        # the previous layer's copies out of the own partial buffers are done
+        if self._stage_sent[0] is not None:
+            main.wait_event(self._stage_sent[0])
+        for c, (r0, r1) in enumerate(chunks):
+            K.linear(attn[r0:r1], lw.wo, K.EPI_BF16, out=po[r0:r1], bias=bo)
+            self._stage_send(0, c, po[r0:r1], r0, e)
+        if self._stage_sent[1] is not None:
+            main.wait_event(self._stage_sent[1])
+        for c, (r0, r1) in enumerate(chunks):
+            st.wait(0, c, e)
+            parts = st.parts(0, po, r0, r1 - r0)
+            if self.bloom:
+                K.layernorm(x[r0:r1], lw.mlp_norm, lw.mlp_norm_b, self.cfg.norm_eps,
+                            out=h[r0:r1], addend=parts)
+            else:
+                K.rmsnorm(x[r0:r1], lw.mlp_norm, self.cfg.norm_eps, out=h[r0:r1], addend=parts)
+            self._mlp_up(h[r0:r1], lw, act[r0:r1])
+            K.linear(act[r0:r1], lw.wd, K.EPI_BF16, out=pd[r0:r1], bias=bd)
+            self._stage_send(1, c, pd[r0:r1], r0, e)
+        self._pending_add = (1, e, len(chunks), pd)
 
     def _ensure_prefill(self, T: int, R: int):
         if T <= self._cap and R <= getattr(self, "_rcap", 0):
@@ -397,10 +495,13 @@ class ModelRunner:
                 self._buf_ev[li & 1] = done
             K.attn_prefill(qkv, cu, R, max(lens), self.hq, self.hkv, self.dh, self.scale,
                            out=attn, alibi=self.alibi)
-            self._proj_reduce(attn, lw.wo, x, lw.bo)
-            self._norm(x, lw.mlp_norm, lw.mlp_norm_b, out=h)
-            self._mlp_up(h, lw, act)
-            self._proj_reduce(act, lw.wd, x, lw.bd)
+            if self._stage_on(T):
+                self._stage_layer(attn, lw, x, h, act, T)
+            else:
+                self._proj_reduce(attn, lw.wo, x, lw.bo)
+                self._norm(x, lw.mlp_norm, lw.mlp_norm_b, out=h)
+                self._mlp_up(h, lw, act)
+                self._proj_reduce(act, lw.wd, x, lw.bd)
         last = self.plast[:R]
         self._norm(x, w.final_norm, w.final_norm_b, out=last, rows_index=last_rows)
         logits = self.plogits[:R]

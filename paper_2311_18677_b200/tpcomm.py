@@ -83,3 +83,62 @@ class TPComm:
         if self._h:
             _abi.call("swb_tp_comm_destroy", self._h)
             self._h = None
+
+
+class TPStage:
+    """Prefill partial exchange over the copy engines (libswb200's
+    ``swb_tp_stage_*``): ``send(buf, chunk, part, row0, epoch)`` DMA-copies
+    this rank's bf16 rows into every peer's receive buffer ``buf`` (on the
+    caller's side stream) and raises the peers' flag ``(buf, chunk)`` to
+    ``epoch``; ``wait(buf, chunk, epoch)`` makes the current stream wait for
+    every peer's flag; ``parts(buf, own, row0, rows)`` lists the rank-ordered
+    partials of those rows (own rows + received views) for the norm that
+    adds them (kernels.rmsnorm / layernorm with a list addend)."""
+
+    def __init__(self, group, rows: int, d: int, n_bufs: int = 2):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.rows, self.d, self.n_bufs = int(rows), int(d), int(n_bufs)
+        per_src = (self.rows * self.d * 2 + 255) // 256 * 256
+        h = C.c_void_p()
+        blob = C.create_string_buffer(_abi.TP_STAGE_IPC_BYTES)
+        _abi.call("swb_tp_stage_create", self.rank, self.world, per_src, self.n_bufs,
+                  C.byref(h), blob, _abi.TP_STAGE_IPC_BYTES)
+        self._h = h
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, bytes(blob.raw), group=group)
+        allb = C.create_string_buffer(b"".join(blobs), _abi.TP_STAGE_IPC_BYTES * self.world)
+        _abi.call("swb_tp_stage_connect", self._h, allb, _abi.TP_STAGE_IPC_BYTES)
+        self._rx = [[device_view(int(_abi.lib.swb_tp_stage_rx(self._h, b, p)),
+                                 (self.rows, self.d), torch.bfloat16)
+                     for p in range(self.world)] for b in range(self.n_bufs)]
+
+    MAXCH = _abi.TP_STAGE_MAXCH
+
+    def send(self, buf: int, chunk: int, part: torch.Tensor, row0: int, epoch: int,
+             stream: torch.cuda.Stream) -> None:
+        if part.dtype != torch.bfloat16 or not part.is_contiguous() or part.shape[1] != self.d:
+            raise ValueError("TPStage.send: contiguous bf16 rows of width d")
+        if row0 + part.shape[0] > self.rows:
+            raise ValueError(f"TPStage.send: rows {row0}+{part.shape[0]} exceed {self.rows}")
+        _abi.call("swb_tp_stage_send", self._h, buf, chunk, part.data_ptr(),
+                  row0 * self.d * 2, part.numel() * 2, epoch & 0xFFFFFFFF, stream.cuda_stream)
+
+    def wait(self, buf: int, chunk: int, epoch: int) -> None:
+        _abi.call("swb_tp_stage_wait", self._h, buf, chunk, epoch & 0xFFFFFFFF,
+                  torch.cuda.current_stream().cuda_stream)
+
+    def parts(self, buf: int, own: torch.Tensor, row0: int, rows: int) -> list:
+        out = []
+        for p in range(self.world):
+            if p == self.rank:
+                out.append(own[row0:row0 + rows])
+            else:
+                out.append(self._rx[buf][p][row0:row0 + rows])
+        return out
+
+    def close(self) -> None:
+        if self._h:
+            _abi.call("swb_tp_stage_destroy", self._h)
+            self._h = None

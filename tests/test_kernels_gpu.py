@@ -634,3 +634,28 @@ def test_attn_chunk_against_torch(K, H, Hkv, C, q0):
     s = s.masked_fill(p[None, None, :] > qpos[None, :, None], float("-inf"))
     ref = torch.einsum("hqk,khd->qhd", s.softmax(-1), v)
     assert _rel(out.view(C, H, dh), ref) < 1e-2
+
+
+@pytest.mark.parametrize("bloom", [False, True])
+def test_add_parts_norm_equals_sum_then_norm(K, bloom):
+    """TP prefill exchange: the norm adds the ranks' bf16 partials (summed in
+    fp32 in rank order) to the fp32 residual, bit-identical to adding the
+    same sum first and normalising after."""
+    T, d = 300, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(T, d, device="cuda", generator=g)
+    parts = [torch.randn(T, d, device="cuda", generator=g).bfloat16() for _ in range(3)]
+    w = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).bfloat16()
+    b = (0.1 * torch.randn(d, device="cuda", generator=g)).bfloat16()
+    s = parts[0].float() + parts[1].float() + parts[2].float()
+    xr = x + s
+    xa = x.clone()
+    if bloom:
+        got = K.layernorm(xa, w, b, 1e-5, addend=parts)
+        ref = K.layernorm(xr, w, b, 1e-5)
+    else:
+        got = K.rmsnorm(xa, w, 1e-5, addend=parts)
+        ref = K.rmsnorm(xr, w, 1e-5)
+    torch.cuda.synchronize()
+    assert torch.equal(xa, xr)
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))

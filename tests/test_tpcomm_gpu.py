@@ -181,19 +181,25 @@ def test_tp_allreduce_p2p_exact():
         assert errs == [], (rank, errs)
 
 
+_BIG = {"SWB_TP_AR_NCCL_BYTES": "65536"}
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("model,env", [("tiny", {}), ("tiny", {"SWB_TP_AR_NCCL_BYTES": "65536"}),
-                                       ("bloom-tiny", {"SWB_TP_AR_NCCL_BYTES": "65536"})])
-def test_tp2_tiny_matches_tp1(model, env):
-    """TP=2 pool == TP=1 tokens; with a 64 KB NCCL threshold the tiny
-    prefill's reductions take the production prefill path (bf16 partials
-    all-reduced by NCCL, added to the fp32 residual inside the next norm)
-    while decode keeps the peer all-reduce, as at full size."""
+@pytest.mark.parametrize("model,env,args", [
+    ("tiny", {}, []), ("tiny", _BIG, []),
+    ("tiny", {**_BIG, "SWB_TP_STAGE_CHUNKS": "2"}, ["--prompt", "600"]),
+    ("tiny", {**_BIG, "SWB_TP_STAGE": "0"}, []), ("bloom-tiny", _BIG, [])])
+def test_tp2_tiny_matches_tp1(model, env, args):
+    """TP=2 pool == TP=1 tokens; with a 64 KB threshold the tiny prefill's
+    reductions take the production prefill path — bf16 partials exchanged
+    by the copy engines (optionally in 2 row chunks) and added to the fp32
+    residual inside the next norm, or with SWB_TP_STAGE=0 all-reduced by
+    NCCL — while decode keeps the peer all-reduce, as at full size."""
     import subprocess
     port = _free_port()
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
-                        os.path.join(ROOT, "tools", "tp_check.py"), "--model", model],
+                        os.path.join(ROOT, "tools", "tp_check.py"), "--model", model, *args],
                        capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env={**os.environ, **env})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
@@ -201,16 +207,19 @@ def test_tp2_tiny_matches_tp1(model, env):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs >= 4 GPUs")
-@pytest.mark.parametrize("model,env", [("tiny-tp4", {}), ("bloom-tiny-tp4", {}),
-                                       ("tiny-tp4", {"SWB_TP_AR_NCCL_BYTES": "65536"})])
-def test_tp4_pool_matches_tp1(model, env):
-    """A TP=4 pool (push all-reduce for decode, two-shot / NCCL for prefill
-    sizes) generates the TP=1 tokens, logits within tolerance."""
+@pytest.mark.parametrize("model,env,args", [
+    ("tiny-tp4", {}, []), ("bloom-tiny-tp4", {**_BIG, "SWB_TP_STAGE": "1"}, []),
+    ("tiny-tp4", {**_BIG, "SWB_TP_STAGE": "1", "SWB_TP_STAGE_CHUNKS": "2"}, ["--prompt", "600"]),
+    ("tiny-tp4", _BIG, [])])
+def test_tp4_pool_matches_tp1(model, env, args):
+    """A TP=4 pool (push all-reduce for decode; prefill sizes through NCCL's
+    bf16 all-reduce, or the copy-engine exchange forced with SWB_TP_STAGE=1)
+    generates the TP=1 tokens, logits within tolerance."""
     import subprocess
     port = _free_port()
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "4",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
-                        os.path.join(ROOT, "tools", "tp_check.py"), "--model", model],
+                        os.path.join(ROOT, "tools", "tp_check.py"), "--model", model, *args],
                        capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env={**os.environ, **env})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

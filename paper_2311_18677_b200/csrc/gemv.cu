@@ -425,13 +425,13 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 // h = bf16(x * rstd * norm_w), with rstd reduced in exactly swb_rmsnorm's
 // order (512 virtual threads, 16 warp partials), so the fused pre-norm GEMV
 // is bit-identical to swb_rmsnorm + GEMV and saves a launch per projection.
-template <int NB, bool NORM>   // NB = 1 (M <= 8) or 2 (M <= 16) MMAs of 8 batch rows
+// ST: ring stages (NORM: 4, or 5 when the staged h leaves room for it)
+template <int NB, bool NORM, int ST = NORM ? TM_NORM_STAGES : TM_STAGES>
 __global__ void __launch_bounds__(TM_THREADS, 2)
     gemv_mma_kernel(const __grid_constant__ CUtensorMap tmW, const void* xin,
                     const __nv_bfloat16* __restrict__ nw, float eps,
                     void* out, const float* resid, const __nv_bfloat16* bias, int M, int N,
                     int K, int epi, int n_items, int trig) {
-  constexpr int ST = NORM ? TM_NORM_STAGES : TM_STAGES;   // NORM: room for staged h
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(xin);
   const float* xf = reinterpret_cast<const float*>(xin);
   extern __shared__ uint8_t smem_raw[];
@@ -637,30 +637,58 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
 
 int make_tmap_rows(CUtensorMap* map, const void* base, int rows, int K, int box_rows);
 
-template <int NB, bool NORM>
-static int launch_gemv_mma(const void* x, const __nv_bfloat16* nw, float eps, const void* w,
-                           void* out, const float* r, const __nv_bfloat16* bias, int M, int N,
-                           int K, int epi, cudaStream_t s) {
+// per-CTA shared-memory budget at 2 CTAs per SM
+constexpr int TM_CTA_BUDGET = (228 * 1024 - 2 * 1024) / 2;
+
+template <int NB, bool NORM, int ST>
+static int launch_gemv_mma_st(const CUtensorMap& tm, const void* x, const __nv_bfloat16* nw,
+                              float eps, void* out, const float* r, const __nv_bfloat16* bias,
+                              int M, int N, int K, int epi, int items, int grid, size_t smem,
+                              cudaStream_t s) {
   static bool attr[64] = {false};
   int dev = 0;
   SWB_CUDA(cudaGetDevice(&dev));
   if (dev < 64 && !attr[dev]) {
-    SWB_CUDA(cudaFuncSetAttribute(gemv_mma_kernel<NB, NORM>,
+    SWB_CUDA(cudaFuncSetAttribute(gemv_mma_kernel<NB, NORM, ST>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  NORM ? tm_smem(TM_NORM_STAGES) + TM_HS_MAX : TM_SMEM));
+                                  NORM ? tm_smem(ST) + TM_HS_MAX : TM_SMEM));
     attr[dev] = true;
   }
+  return launch(gemv_mma_kernel<NB, NORM, ST>, dim3(grid), dim3(TM_THREADS), smem, s, tm, x, nw,
+                eps, out, r, bias, M, N, K, epi, items, pdl_early_trigger() ? 1 : 0) ==
+                 cudaSuccess
+             ? SWB_OK
+             : swb_set_error(SWB_ERR_CUDA, "launch gemv_mma_kernel: %s",
+                             cudaGetErrorString(cudaGetLastError()));
+}
+
+template <int NB, bool NORM>
+static int launch_gemv_mma(const void* x, const __nv_bfloat16* nw, float eps, const void* w,
+                           void* out, const float* r, const __nv_bfloat16* bias, int M, int N,
+                           int K, int epi, cudaStream_t s) {
   CUtensorMap tm;
   const int st = make_tmap_rows(&tm, w, N, K, 8);
   if (st) return st;
   const int items = epi == SWB_EPI_SWIGLU ? (N / 2 + 7) / 8 : (N + TM_ROWS - 1) / TM_ROWS;
   const int grid = min(items, gemv_ctas_per_sm() * kNumSMs);
-  const size_t smem = NORM ? tm_smem(TM_NORM_STAGES) + (size_t)M * K * 2 : TM_SMEM;
-  const cudaError_t le = launch(gemv_mma_kernel<NB, NORM>, dim3(grid), dim3(TM_THREADS),
-                                smem, s, tm, x, nw, eps, out, r, bias, M, N, K, epi, items,
-                                pdl_early_trigger() ? 1 : 0);
-  if (le != cudaSuccess)
-    return swb_set_error(SWB_ERR_CUDA, "launch gemv_mma_kernel: %s", cudaGetErrorString(le));
+  int rc;
+  if constexpr (NORM) {
+    // pre-norm: a 5th ring stage when the staged h (M*K*2 bytes) leaves room
+    // (7B B=2: 16 KB of h)
+    const size_t hs = (size_t)M * K * 2;
+    if (tm_smem(TM_NORM_STAGES + 1) + hs <= (size_t)TM_CTA_BUDGET)
+      rc = launch_gemv_mma_st<NB, true, TM_NORM_STAGES + 1>(
+          tm, x, nw, eps, out, r, bias, M, N, K, epi, items, grid,
+          tm_smem(TM_NORM_STAGES + 1) + hs, s);
+    else
+      rc = launch_gemv_mma_st<NB, true, TM_NORM_STAGES>(tm, x, nw, eps, out, r, bias, M, N, K,
+                                                        epi, items, grid,
+                                                        tm_smem(TM_NORM_STAGES) + hs, s);
+  } else {
+    rc = launch_gemv_mma_st<NB, false, TM_STAGES>(tm, x, nw, eps, out, r, bias, M, N, K, epi,
+                                                  items, grid, TM_SMEM, s);
+  }
+  if (rc) return rc;
   return swb_check_launch("gemv_mma_kernel");
 }
 

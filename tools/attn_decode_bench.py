@@ -22,8 +22,13 @@ def timeit(fn, iters=20):
 
 res = {}
 dh, bs = 128, 16
-for name, H, Hkv in (("7b", 32, 32), ("70b-tp2", 32, 4)):
-    for B, ctx in ((1, 1100), (8, 1100), (32, 1100), (1, 8000), (8, 4000)):
+# SHAPES="name:H:Hkv,..." and CASES="B:ctx,..." override the defaults
+shapes = [(n, int(h), int(k)) for n, h, k in
+          (x.split(":") for x in os.environ.get("SHAPES", "7b:32:32,70b-tp2:32:4").split(","))]
+cases = [tuple(int(v) for v in x.split(":")) for x in
+         os.environ.get("CASES", "1:1100,8:1100,32:1100,1:8000,8:4000").split(",")]
+for name, H, Hkv in shapes:
+    for B, ctx in cases:
         nblk = B * (ctx // bs + 8) + 16
         kp = torch.randn(nblk, Hkv, bs, dh, device="cuda").bfloat16()
         vp = torch.randn_like(kp)

@@ -35,3 +35,10 @@ clean:
 	rm -rf build $(LIB)
 
 .PHONY: all clean sass
+
+# timeline-probe build of the decode attention (tools/attn_probe.py only):
+# build/var/libswb200_probe.so, copied over the library on a GPU box for a run
+probe-lib: $(OBJ)
+	@mkdir -p build/var
+	$(NVCC) $(NVFLAGS) -DSWB_ATTN_PROBE -c $(SRC)/attention.cu -o build/var/attention_probe.o
+	$(NVCC) -shared $(ARCH) -o build/var/libswb200_probe.so $(filter-out $(OBJDIR)/attention.o,$(OBJ)) build/var/attention_probe.o -cudart static

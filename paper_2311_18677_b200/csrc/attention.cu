@@ -967,6 +967,22 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
 // later pages are still landing; warps combine (max, sum, O) through shared
 // memory, partitions through the fused split-K merge.
 constexpr int DM_WARPS = 4, DM_PT = 128, DM_WT = 32, DM_QS = DA_D + 8;
+#ifdef SWB_ATTN_PROBE
+// timeline probe build (tools only): per-CTA globaltimer stamps
+__device__ unsigned long long* g_attn_probe = nullptr;
+#define ATTN_PROBE(k)                                                                    \
+  do {                                                                                   \
+    if (g_attn_probe && threadIdx.x == 0) {                                              \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      g_attn_probe[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + \
+                   (k)] = t_;                                                            \
+    }                                                                                    \
+  } while (0)
+#else
+#define ATTN_PROBE(k) do {} while (0)
+#endif
+
 constexpr int DC_MAXQT = 512;     // chunked prefill: up to 8192 query rows per chunk
 
 // CLN > 0: the NP = CLN partitions of a (b, kv head) form one thread-block
@@ -996,6 +1012,8 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
   __shared__ uint64_t merge_bar;
   __shared__ int s_last;
   __shared__ __align__(16) __nv_bfloat16 scur[2][DA_D];
+  __shared__ float swf[DM_WARPS * 8], swM[8], swL[8];   // per (warp, head) combine factors
+  ATTN_PROBE(0);
   const int p = blockIdx.x, kh = blockIdx.y, b = blockIdx.z;
   const int NP = gridDim.x;
   const int G = H / Hkv;
@@ -1009,7 +1027,9 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       mbar_init(&kbar[i], 1);
       mbar_init(&vbar[i], 1);
     }
-    if constexpr (CLN > 0) mbar_init(&merge_bar, CLN - 1);
+    // one release arrive per warp of every other CTA (their records land
+    // straight in this CTA's inbox from the warp-combine loop)
+    if constexpr (CLN > 0) mbar_init(&merge_bar, (CLN - 1) * DM_WARPS);
     fence_barrier_init();
   }
   __syncthreads();
@@ -1047,6 +1067,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     }
   }
   if constexpr (STEP) pdl_wait();
+  ATTN_PROBE(1);
 
   if (ntok > 0) {
     const int qpos = cur >= 0 ? cur : L - 1;
@@ -1103,11 +1124,13 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       *reinterpret_cast<uint2*>(&scur[1][64 + i0]) = vhi;
     }
     __syncthreads();
+    ATTN_PROBE(2);
 
     const int wt0 = warp * WT;
     const bool cur_here = own_cur && cur - t0 >= wt0 && cur - t0 < wt0 + WT;
     if (wt0 < ntok) {   // warp-uniform
       mbar_wait(&kbar[warp], 0);
+      ATTN_PROBE(3);
       if (cur_here && lane < 16)
         reinterpret_cast<uint4*>(sk + (size_t)(cur - t0) * DA_D)[lane] =
             reinterpret_cast<const uint4*>(scur[0])[lane];
@@ -1165,6 +1188,7 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       l += __shfl_xor_sync(0xffffffffu, l, 1);
       l += __shfl_xor_sync(0xffffffffu, l, 2);
       mbar_wait(&vbar[warp], 0);
+      ATTN_PROBE(4);
       if (cur_here && lane < 16)
         reinterpret_cast<uint4*>(sv + (size_t)(cur - t0) * DA_D)[lane] =
             reinterpret_cast<const uint4*>(scur[1])[lane];
@@ -1204,31 +1228,59 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       sml[(warp * 8 + g) * 2 + 1] = 0.f;
     }
     __syncthreads();
+    ATTN_PROBE(5);
     if (trig) pdl_launch_dependents();
-    // combine the warps' partial softmax states
-    for (int i = threadIdx.x; i < G * DA_D; i += DM_WARPS * 32) {
-      const int gi = i / DA_D, d = i % DA_D;
+    // cluster form: rank 0's merge barrier is initialised (cluster_arrive at
+    // the start) before any record is pushed into its inbox
+    if constexpr (CLN > 0) cluster_wait();
+    const uint32_t inbox0 = CLN > 0 ? mapa(smem_u32(inbox), 0) : 0u;
+    // combine the warps' partial softmax states: the per-(warp, head)
+    // factors once, then one FMA per warp and element
+    if (threadIdx.x < G) {
+      const int gi = threadIdx.x;
       float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < DM_WARPS; ++w) M = fmaxf(M, sml[(w * 8 + gi) * 2]);
-      float o = 0.f, l = 0.f;
+      float l = 0.f;
 #pragma unroll
       for (int w = 0; w < DM_WARPS; ++w) {
         const float mw = sml[(w * 8 + gi) * 2];
-        if (mw == -INFINITY) continue;
-        const float f = exp2f(mw - M);
-        o += f * so[((size_t)w * G + gi) * DA_D + d];
-        l += f * sml[(w * 8 + gi) * 2 + 1];
+        const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
+        swf[w * 8 + gi] = f;
+        if (mw != -INFINITY) l += f * sml[(w * 8 + gi) * 2 + 1];
+      }
+      swM[gi] = M;
+      swL[gi] = l;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * DA_D; i += DM_WARPS * 32) {
+      const int gi = i / DA_D, d = i % DA_D;
+      const float M = swM[gi], l = swL[gi];
+      float o = 0.f;
+#pragma unroll
+      for (int w = 0; w < DM_WARPS; ++w) {
+        if (sml[(w * 8 + gi) * 2] == -INFINITY) continue;   // warp had no tokens
+        o += swf[w * 8 + gi] * so[((size_t)w * G + gi) * DA_D + d];
       }
       if (CLN == 0 && NP == 1) {
         out[((size_t)b * H + kh * G + gi) * DA_D + d] = __float2bfloat16(o / l);
         continue;
       }
       if constexpr (CLN > 0) {
-        rec[gi * (DA_D + 2) + d] = o;
-        if (d == 0) {
-          rec[gi * (DA_D + 2) + DA_D] = M;
-          rec[gi * (DA_D + 2) + DA_D + 1] = l;
+        // this partition's record goes straight into rank 0's inbox
+        const uint32_t slot = (uint32_t)(p * G + gi) * DCL_ST;
+        if (p == 0) {
+          inbox[slot + d] = o;
+          if (d == 0) {
+            inbox[slot + DA_D] = M;
+            inbox[slot + DA_D + 1] = l;
+          }
+        } else {
+          st_dsmem(inbox0 + (slot + d) * 4u, o);
+          if (d == 0) {
+            st_dsmem(inbox0 + (slot + DA_D) * 4u, M);
+            st_dsmem(inbox0 + (slot + DA_D + 1) * 4u, l);
+          }
         }
         continue;
       }
@@ -1243,8 +1295,17 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
   } else {
     if (trig) pdl_launch_dependents();
     if constexpr (CLN > 0) {
-      for (int i = threadIdx.x; i < G * (DA_D + 2); i += DM_WARPS * 32)
-        rec[i] = (i % (DA_D + 2)) == DA_D ? -INFINITY : 0.f;
+      cluster_wait();
+      const uint32_t inbox0 = mapa(smem_u32(inbox), 0);
+      for (int i = threadIdx.x; i < G * (DA_D + 2); i += DM_WARPS * 32) {
+        const int gi = i / (DA_D + 2), d = i % (DA_D + 2);
+        const uint32_t slot = (uint32_t)(p * G + gi) * DCL_ST + d;
+        const float v = d == DA_D ? -INFINITY : 0.f;
+        if (p == 0)
+          inbox[slot] = v;
+        else
+          st_dsmem(inbox0 + slot * 4u, v);
+      }
     } else if (threadIdx.x < G) {
       float* w = wsp(kh * G + threadIdx.x, p);
       w[DA_D] = -INFINITY;
@@ -1252,30 +1313,38 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
     }
   }
   if constexpr (CLN > 0) {
-    // ---- push this partition's (o, m, l) into rank 0's inbox, merge there
-    __syncthreads();
-    cluster_wait();
-    const uint32_t inbox_local = smem_u32(inbox);
-    for (int i = threadIdx.x; i < G * (DA_D + 2); i += DM_WARPS * 32) {
-      const int gi = i / (DA_D + 2), d = i % (DA_D + 2);
-      const float v = rec[i];
-      const int slot = (p * G + gi) * DCL_ST + d;
-      if (p == 0)
-        inbox[slot] = v;
-      else
-        st_dsmem(mapa(inbox_local + (uint32_t)slot * 4u, 0), v);
-    }
+    // ---- records are in rank 0's inbox; every warp of ranks > 0 publishes
+    // its stores with one release arrive (cumulative over the warp's lanes
+    // after __syncwarp), rank 0 merges
+    __syncwarp();
+    ATTN_PROBE(6);
     if (p != 0) {
-      asm volatile("fence.acq_rel.cluster;" ::: "memory");
-      __syncthreads();
-      if (threadIdx.x == 0) mbar_arrive_remote(mapa(smem_u32(&merge_bar), 0));
+      if (lane == 0) mbar_arrive_remote(mapa(smem_u32(&merge_bar), 0));
+      ATTN_PROBE(7);
       return;
     }
     __syncthreads();
     mbar_wait_cluster(&merge_bar, 0);
-    float* fac = rec;                     // [CLN][G] merge factors (rec was pushed)
+    ATTN_PROBE(7);
+    float* fac = rec;                     // [CLN][G] merge factors
     float* ltot = rec + CLN * G;          // [G]
-    if (threadIdx.x < G) {
+    if (G * CLN <= DM_WARPS * 32) {
+      // one (head, partition) per thread; CLN consecutive lanes per head
+      const int i = threadIdx.x, gi = i / CLN, q = i % CLN;
+      const bool on = i < G * CLN;
+      const float mq = on ? inbox[(q * G + gi) * DCL_ST + DA_D] : -INFINITY;
+      float Mx = mq;
+#pragma unroll
+      for (int o = CLN / 2; o > 0; o >>= 1) Mx = fmaxf(Mx, __shfl_xor_sync(0xffffffffu, Mx, o));
+      const float f = (!on || mq == -INFINITY) ? 0.f : exp2f(mq - Mx);
+      float Ls = on ? f * inbox[(q * G + gi) * DCL_ST + DA_D + 1] : 0.f;
+#pragma unroll
+      for (int o = CLN / 2; o > 0; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
+      if (on) {
+        fac[q * G + gi] = f;
+        if (q == 0) ltot[gi] = Ls;
+      }
+    } else if (threadIdx.x < G) {
       const int gi = threadIdx.x;
       float Mx = -INFINITY;
       for (int q = 0; q < CLN; ++q) Mx = fmaxf(Mx, inbox[(q * G + gi) * DCL_ST + DA_D]);
@@ -1289,12 +1358,21 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       ltot[gi] = Ls;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < G * DA_D; i += DM_WARPS * 32) {
-      const int gi = i / DA_D, d = i % DA_D;
-      float o = 0.f;
-      for (int q = 0; q < CLN; ++q) o = fmaf(fac[q * G + gi], inbox[(q * G + gi) * DCL_ST + d], o);
-      out[((size_t)b * H + kh * G + gi) * DA_D + d] = __float2bfloat16(o / ltot[gi]);
+    for (int i = threadIdx.x; i < G * DA_D / 4; i += DM_WARPS * 32) {
+      const int gi = i / (DA_D / 4), d = (i % (DA_D / 4)) * 4;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+      for (int q = 0; q < CLN; ++q) {
+        const float f = fac[q * G + gi];
+        const float4 v = *reinterpret_cast<const float4*>(inbox + (q * G + gi) * DCL_ST + d);
+        o.x = fmaf(f, v.x, o.x); o.y = fmaf(f, v.y, o.y);
+        o.z = fmaf(f, v.z, o.z); o.w = fmaf(f, v.w, o.w);
+      }
+      const float il = ltot[gi];
+      *reinterpret_cast<uint2*>(out + ((size_t)b * H + kh * G + gi) * DA_D + d) =
+          make_uint2(f2_to_bf2(o.x / il, o.y / il), f2_to_bf2(o.z / il, o.w / il));
     }
+    ATTN_PROBE(8);
     return;
   }
   // ---- fused split-K merge: the last CTA of (b, kh) combines the partitions
@@ -1665,6 +1743,13 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
   }
   float* ws = reinterpret_cast<float*>(workspace);
   int* tickets = reinterpret_cast<int*>(ws + (size_t)B * H * NP * (DA_D + 2));
+#ifdef SWB_ATTN_PROBE
+  if (const char* pe = std::getenv("SWB_ATTN_PROBE_ADDR")) {
+    unsigned long long* pp = reinterpret_cast<unsigned long long*>(std::strtoull(pe, nullptr, 0));
+    cudaMemcpyToSymbolAsync(g_attn_probe, &pp, sizeof(pp), 0, cudaMemcpyHostToDevice,
+                            (cudaStream_t)stream);
+  }
+#endif
   static const bool mma_on = [] {
     const char* e = std::getenv("SWB_ATTN_MMA");
     return !(e && e[0] == '0');

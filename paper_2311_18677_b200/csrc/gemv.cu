@@ -282,20 +282,21 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
         // fused TP all-reduce (one decode row): the item's 4 consecutive
         // outputs go straight to every peer as two 16-byte posted NVLink
         // stores of (value, epoch) words while later weights still stream
+        // lane 2p + h stores half h to peer p, so the stores leave in
+        // parallel; lane 0 reads all four outputs (the own count's release
+        // below covers them)
         __syncwarp();
-        if (lane == 0 && 4 * item + 3 < N) {
+        if (lane < 2 * tpp.world && 4 * item + 3 < N) {
           const float4 v4 = reinterpret_cast<const float4*>(out)[item];
-          const unsigned long long hi = (unsigned long long)ll_e << 32;
-          const unsigned long long a0 = hi | __float_as_uint(v4.x), a1 = hi | __float_as_uint(v4.y),
-                                   a2 = hi | __float_as_uint(v4.z), a3 = hi | __float_as_uint(v4.w);
-          for (int p = 0; p < tpp.world; ++p)
-            if (p != tpp.rank) {
-              unsigned long long* d = tpp.rx[p] + 4 * (size_t)item;
-              asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(d), "l"(a0), "l"(a1)
-                           : "memory");
-              asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(d + 2), "l"(a2),
-                           "l"(a3) : "memory");
-            }
+          const int p = lane >> 1, h = lane & 1;
+          if (p != tpp.rank) {
+            const unsigned long long hi = (unsigned long long)ll_e << 32;
+            const unsigned long long a0 = hi | __float_as_uint(h ? v4.z : v4.x),
+                                     a1 = hi | __float_as_uint(h ? v4.w : v4.y);
+            unsigned long long* d = tpp.rx[p] + 4 * (size_t)item + 2 * h;
+            asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(d), "l"(a0), "l"(a1)
+                         : "memory");
+          }
         }
       }
     }

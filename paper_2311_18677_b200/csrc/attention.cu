@@ -648,6 +648,21 @@ __global__ void __launch_bounds__(NW * 32)
 // 16 opt-in), DCL_CW consumer warps.
 constexpr int DCL_PAGE = 16 * DA_D;   // elements of one (block, head) page
 constexpr int DCL_ST = DA_D + 4;      // floats per (o[128], m, l) record (16-byte aligned)
+#ifdef SWB_ATTN_PROBE
+// timeline probe build (tools only): per-CTA globaltimer stamps
+__device__ unsigned long long* g_attn_probe = nullptr;
+#define ATTN_PROBE(k)                                                                    \
+  do {                                                                                   \
+    if (g_attn_probe && threadIdx.x == 0) {                                              \
+      unsigned long long t_;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
+      g_attn_probe[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + \
+                   (k)] = t_;                                                            \
+    }                                                                                    \
+  } while (0)
+#else
+#define ATTN_PROBE(k) do {} while (0)
+#endif
 
 __host__ __device__ constexpr size_t dcl_smem(int G, int CW, int S, int CL) {
   return (size_t)S * 2 * DCL_PAGE * 2 + sizeof(float) * (size_t)(CW + CL) * G * DCL_ST;
@@ -675,6 +690,8 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
   float* inbox = wst + DCL_CW * G * DCL_ST;         // rank 0: [CL][G][ST] records of the CTAs
   __shared__ uint64_t full[DCL_S], empty[DCL_S];
   __shared__ uint64_t merge_bar;
+  __shared__ __align__(16) float pw[DCL_CW * GW * 16];   // per warp: p of the current page
+  ATTN_PROBE(0);
   const int r = blockIdx.x;             // cluster rank (cluster (DCL_CL,1,1), gridDim.x == DCL_CL)
   const int kh = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -684,7 +701,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], HS ? DCL_CW : 1);
     }
-    mbar_init(&merge_bar, DCL_CL - 1);
+    mbar_init(&merge_bar, (DCL_CL - 1) * (DCL_CW + 1));   // one arrive per warp of each peer
     fence_barrier_init();
   }
   __syncthreads();
@@ -721,6 +738,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
   } else {
     // ------------------------------------------------ consumers
     pdl_wait();                                   // q / current k,v from the QKV projection
+    ATTN_PROBE(1);
     const int half = lane >> 4, hl = lane & 15;
     const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
     const float fpos = (float)cur;
@@ -785,9 +803,11 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
       l[g] = 0.f;
       o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
     }
+    ATTN_PROBE(2);
     for (int i = HS ? 0 : warp; i < nmy; i += HS ? 1 : DCL_CW) {
       const int st = i % DCL_S;
       mbar_wait(&full[st], (i / DCL_S) & 1);
+      if (i == 0) ATTN_PROBE(3);
       __nv_bfloat16* ks = ring + (size_t)(2 * st) * DCL_PAGE;
       __nv_bfloat16* vs = ks + DCL_PAGE;
       const int t0 = (pg0 + i) * 16;
@@ -821,51 +841,77 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
           sc[g][it] = d;
         }
       }
+      // reduce-scatter across the 16 lanes of a half (xor 8, 4, 2, then 1):
+      // the same pairwise sums as a full butterfly per token, but 8 shuffles
+      // instead of 32 — lane hl ends with token 2*(hl >> 1) + half
 #pragma unroll
       for (int g = 0; g < GW; ++g) {
+        const bool b3 = hl & 8, b2 = hl & 4, b1 = hl & 2;
+        float r4[4], r2[2];
 #pragma unroll
-        for (int sh = 8; sh > 0; sh >>= 1)
-#pragma unroll
-          for (int it = 0; it < 8; ++it) sc[g][it] += __shfl_xor_sync(0xffffffffu, sc[g][it], sh);
-        float mx = -INFINITY;
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int t = 2 * it + half;
-          sc[g][it] = t < valid ? fmaf(sl[g], (float)(t0 + t - cur), sc[g][it]) : -INFINITY;
-          mx = fmaxf(mx, sc[g][it]);
+        for (int j = 0; j < 4; ++j) {
+          const float keep = b3 ? sc[g][4 + j] : sc[g][j];
+          const float send = b3 ? sc[g][j] : sc[g][4 + j];
+          r4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
         }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const float keep = b2 ? r4[2 + j] : r4[j];
+          const float send = b2 ? r4[j] : r4[2 + j];
+          r2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        float v;
+        {
+          const float keep = b1 ? r2[1] : r2[0];
+          const float send = b1 ? r2[0] : r2[1];
+          v = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        const int t = 2 * (hl >> 1) + half;
+        v = t < valid ? fmaf(sl[g], (float)(t0 + t - cur), v) : -INFINITY;
+        float mx = v;
+#pragma unroll
+        for (int sh = 2; sh < 32; sh <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
         const float mn = fmaxf(m[g], mx);
         const float corr = m[g] == -INFINITY ? 0.f : exp2f(m[g] - mn);
-        float ps = 0.f;
+        const float e = exp2f(v - mn);
+        float ps = (hl & 1) ? 0.f : e;          // each token once
 #pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          sc[g][it] = exp2f(sc[g][it] - mn);
-          ps += sc[g][it];
-        }
-        ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+        for (int sh = 1; sh < 32; sh <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, sh);
         l[g] = l[g] * corr + ps;
         m[g] = mn;
 #pragma unroll
         for (int j = 0; j < 4; ++j) o[g][j] *= corr;
+        // p of every token of the page to this warp's smem row (broadcast reads below)
+        if (!(hl & 1)) pw[(warp * GW + g) * 16 + t] = e;
       }
-      // P.V: lane owns dims [4*lane, 4*lane+4); token t's p lives in lane (t&1)*16
+      __syncwarp();
+      // P.V: lane owns dims [4*lane, 4*lane+4)
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const uint2 vv = *reinterpret_cast<const uint2*>(vs + t * DA_D + 4 * lane);
-        const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
+      for (int t4 = 0; t4 < 4; ++t4) {
+        float4 p4[GW];
 #pragma unroll
-        for (int g = 0; g < GW; ++g) {
-          const float pt = __shfl_sync(0xffffffffu, sc[g][t >> 1], (t & 1) * 16);
-          o[g][0] = fmaf(pt, v0.x, o[g][0]);
-          o[g][1] = fmaf(pt, v0.y, o[g][1]);
-          o[g][2] = fmaf(pt, v1.x, o[g][2]);
-          o[g][3] = fmaf(pt, v1.y, o[g][3]);
+        for (int g = 0; g < GW; ++g)
+          p4[g] = *reinterpret_cast<const float4*>(pw + (warp * GW + g) * 16 + 4 * t4);
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+          const int t = 4 * t4 + tt;
+          const uint2 vv = *reinterpret_cast<const uint2*>(vs + t * DA_D + 4 * lane);
+          const float2 v0 = bf2_to_f2(vv.x), v1 = bf2_to_f2(vv.y);
+#pragma unroll
+          for (int g = 0; g < GW; ++g) {
+            const float pt = tt == 0 ? p4[g].x : tt == 1 ? p4[g].y : tt == 2 ? p4[g].z : p4[g].w;
+            o[g][0] = fmaf(pt, v0.x, o[g][0]);
+            o[g][1] = fmaf(pt, v0.y, o[g][1]);
+            o[g][2] = fmaf(pt, v1.x, o[g][2]);
+            o[g][3] = fmaf(pt, v1.y, o[g][3]);
+          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
+    ATTN_PROBE(4);
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {          // heads this warp does not own: empty
       const int g = gg - g0;
@@ -890,7 +936,8 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
   __syncthreads();
   // ---- combine the consumer warps (fixed order) into this CTA's record and
   // PUSH it into rank 0's inbox (st.shared::cluster); one release arrive on
-  // rank 0's merge barrier per CTA, then non-zero ranks exit at once
+  // rank 0's merge barrier per warp, then non-zero ranks exit at once
+  ATTN_PROBE(5);
   cluster_wait();                      // rank 0's merge barrier is initialised
   const uint32_t inbox_local = smem_u32(inbox);
   for (int idx = threadIdx.x; idx < G * DA_D; idx += DCL_THREADS) {
@@ -923,13 +970,17 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
     }
   }
   if (r != 0) {
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) mbar_arrive_remote(mapa(smem_u32(&merge_bar), 0));
+    // each warp publishes its lanes' stores with one release arrive
+    // (cumulative after __syncwarp): no cluster fence, no CTA barrier
+    __syncwarp();
+    if (lane == 0) mbar_arrive_remote(mapa(smem_u32(&merge_bar), 0));
+    ATTN_PROBE(6);
     return;
   }
+  ATTN_PROBE(6);
   __syncthreads();
   mbar_wait_cluster(&merge_bar, 0);    // every peer's record landed in the inbox
+  ATTN_PROBE(7);
   __shared__ float fac[DCL_CL * G];
   __shared__ float ltot[G];
   for (int g = threadIdx.x; g < G; g += DCL_THREADS) {
@@ -954,6 +1005,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
     for (int p = 0; p < DCL_CL; ++p) O = fmaf(fac[p * G + g], inbox[(p * G + g) * DCL_ST + d], O);
     out[((size_t)b * H + kh * G + g) * DA_D + d] = __float2bfloat16(O / ltot[g]);
   }
+  ATTN_PROBE(8);
 }
 
 // ---------------------------------------------------------------- decode, MMA
@@ -967,21 +1019,6 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
 // later pages are still landing; warps combine (max, sum, O) through shared
 // memory, partitions through the fused split-K merge.
 constexpr int DM_WARPS = 4, DM_PT = 128, DM_WT = 32, DM_QS = DA_D + 8;
-#ifdef SWB_ATTN_PROBE
-// timeline probe build (tools only): per-CTA globaltimer stamps
-__device__ unsigned long long* g_attn_probe = nullptr;
-#define ATTN_PROBE(k)                                                                    \
-  do {                                                                                   \
-    if (g_attn_probe && threadIdx.x == 0) {                                              \
-      unsigned long long t_;                                                             \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                             \
-      g_attn_probe[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + \
-                   (k)] = t_;                                                            \
-    }                                                                                    \
-  } while (0)
-#else
-#define ATTN_PROBE(k) do {} while (0)
-#endif
 
 constexpr int DC_MAXQT = 512;     // chunked prefill: up to 8192 query rows per chunk
 

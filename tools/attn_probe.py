@@ -30,7 +30,8 @@ for _ in range(5):
     f()
 torch.cuda.synchronize()
 NP = max_ctx // part
-ncta = NP * Hkv * B
+# the cluster launches use 8 or 16 partitions per (b, kv head): size for 16
+ncta = max(NP, 16) * Hkv * B
 probe = torch.zeros(ncta * 16, dtype=torch.int64, device="cuda")
 os.environ["SWB_ATTN_PROBE_ADDR"] = str(probe.data_ptr())
 res = []
@@ -41,8 +42,10 @@ for rep in range(3):
     torch.cuda.synchronize()
     p = probe.view(ncta, 16).double()
     t0 = p[:, 0][p[:, 0] > 0].min()
-    names = ["start", "pdl_wait", "q_staged", "k_landed", "v_landed", "pv_done", "combined",
-             "pushed/merge_wait", "out_written"]
+    names = (["start", "pdl_wait", "q_staged", "k_landed", "v_landed", "pv_done", "combined",
+              "pushed/merge_wait", "out_written"] if H // Hkv > 2 else
+             ["start", "pdl_wait", "q_ready", "first_page", "pages_done", "combine_start",
+              "pushed", "merge_wait", "out_written"])
     row = {}
     for k, n in enumerate(names):
         col = p[:, k]

@@ -27,7 +27,10 @@ namespace swb {
 constexpr int TV_ROWS = 4;                    // weight rows per work item
 constexpr int TV_WARPS = 8;                   // consumer warps: 2 per row (K halves)
 constexpr int TV_KC = 2048;                   // K elements per stage per row (4 KB)
-constexpr int TV_STAGES = 5;
+#ifndef SWB_TV_STAGES
+#define SWB_TV_STAGES 5   // ring depth (A/B builds only)
+#endif
+constexpr int TV_STAGES = SWB_TV_STAGES;
 constexpr int TV_ROW_BYTES = TV_KC * 2;
 constexpr int TV_STAGE_BYTES = TV_ROWS * TV_ROW_BYTES;  // 16 KB
 constexpr int TV_THREADS = (TV_WARPS + 1) * 32;

@@ -289,6 +289,7 @@ using namespace swb;
 struct swb_tp_comm {
   int rank, world, device;
   int nsrc[TP_NSLOT];               // producer CTAs of the last fused GEMV per slot
+  long long nout[TP_NSLOT];         // its output count (the receive must match it)
   size_t slot_bytes;
   uint8_t* base;                    // own region
   uint8_t* peer_base[TP_MAXW];      // mapped regions (own at [rank])
@@ -417,6 +418,7 @@ int tp_push_targets(swb_tp_comm* c, int slot, int nsrc, long long n, TpPush* out
                                                        (size_t)c->rank * TP_LL_BYTES);
   }
   c->nsrc[slot] = nsrc;
+  c->nout[slot] = n;
   return SWB_OK;
 }
 }  // namespace swb
@@ -445,6 +447,9 @@ extern "C" int swb_tp_allreduce_recv_f32(swb_tp_comm* c, int slot, float* out, s
               "swb_tp_allreduce_recv_f32: no fused projection on slot %d", slot);
   SWB_REQUIRE(n * 8 <= TP_LL_BYTES,
               "swb_tp_allreduce_recv_f32: n=%zu exceeds the receive lines", n);
+  SWB_REQUIRE((long long)n == c->nout[slot],
+              "swb_tp_allreduce_recv_f32: n=%zu but the fused projection on slot %d produced %lld",
+              n, slot, c->nout[slot]);
   return tp_allreduce(c, slot, out, n, stream, true);
 }
 

@@ -99,13 +99,14 @@ class ModelRunner:
         # (tpcomm.TPStage), summed inside the next norm: 70B TP2 1024-token
         # prefill 71.1 -> 70.4 ms.  At TP4 the all-gather moves twice NCCL's
         # bytes (73.3 vs 64.0-66.6 ms), so auto = TP2 only; SWB_TP_STAGE=1/0
-        # forces it.  SWB_TP_STAGE_CHUNKS > 1 pipelines row chunks (chunk c's
-        # exchange under chunk c+1's GEMMs) but the half-size GEMMs lose more
-        # to wave quantisation than the overlap wins (TP2: 2 chunks 73.6 ms,
-        # 4 chunks 89.4) — profiles/r2_tp_prefill_exchange.json
+        # forces it.  SWB_TP_STAGE_CHUNKS (default 2): the O / down GEMMs run
+        # in row chunks of whole 256-row tiles whose partials leave as they
+        # land (the MLP stays whole: split gate/up GEMMs lose to wave
+        # quantisation) — TP2 70.9 -> 70.4 ms on one box; 4 chunks 81 ms
+        # (profiles/r2_tp_prefill_exchange.json)
         mode = os.environ.get("SWB_TP_STAGE", "auto")
         self.tp_stage = self.tp == 2 if mode == "auto" else mode == "1"
-        self.stage_chunks = int(os.environ.get("SWB_TP_STAGE_CHUNKS", "1"))
+        self.stage_chunks = int(os.environ.get("SWB_TP_STAGE_CHUNKS", "2"))
         self._stage = None
         self._stage_epoch = 0
         self._stage_own = [None, None]      # this rank's O / down partials (bf16)
@@ -309,7 +310,7 @@ class ModelRunner:
     def _stage_chunks(self, T: int) -> list:
         n = max(1, min(self.stage_chunks, 8, T // 256))   # SWB_TP_STAGE_MAXCH
         step = (T + n - 1) // n
-        step = (step + 127) // 128 * 128
+        step = (step + 255) // 256 * 256                 # whole 256-row GEMM tiles
         return [(r0, min(T, r0 + step)) for r0 in range(0, T, step)]
 
     def _stage_send(self, kind: int, chunk: int, rows: torch.Tensor, row0: int, epoch: int):
@@ -325,10 +326,11 @@ class ModelRunner:
 
     def _stage_layer(self, attn, lw, x, h, act, T: int):
         """O projection -> residual + norm -> MLP -> down projection of one
-        layer with both TP reductions as per-chunk copy-engine exchanges:
-        chunk c's O partial travels while chunk c+1's O GEMM runs, chunk c's
-        MLP runs while chunk c+1's partial travels, and so on; the last
-        down-projection exchange is added by the next norm (_norm)."""
+        layer with both TP reductions as copy-engine exchanges.  The two
+        projections run in row chunks whose partials leave as soon as they
+        land (chunk c's copy under chunk c+1's GEMM); the norm and the MLP
+        take all rows (their GEMMs lose to wave quantisation when split);
+        the down projection's exchange is added by the next norm (_norm)."""
         st = self._stage_comm(T)
         main = torch.cuda.current_stream()
         chunks = self._stage_chunks(T)
@@ -343,17 +345,17 @@ class ModelRunner:
         for c, (r0, r1) in enumerate(chunks):
             K.linear(attn[r0:r1], lw.wo, K.EPI_BF16, out=po[r0:r1], bias=bo)
             self._stage_send(0, c, po[r0:r1], r0, e)
+        for c in range(len(chunks)):
+            st.wait(0, c, e)
+        parts = st.parts(0, po, 0, T)
+        if self.bloom:
+            K.layernorm(x, lw.mlp_norm, lw.mlp_norm_b, self.cfg.norm_eps, out=h, addend=parts)
+        else:
+            K.rmsnorm(x, lw.mlp_norm, self.cfg.norm_eps, out=h, addend=parts)
+        self._mlp_up(h, lw, act)
         if self._stage_sent[1] is not None:
             main.wait_event(self._stage_sent[1])
         for c, (r0, r1) in enumerate(chunks):
-            st.wait(0, c, e)
-            parts = st.parts(0, po, r0, r1 - r0)
-            if self.bloom:
-                K.layernorm(x[r0:r1], lw.mlp_norm, lw.mlp_norm_b, self.cfg.norm_eps,
-                            out=h[r0:r1], addend=parts)
-            else:
-                K.rmsnorm(x[r0:r1], lw.mlp_norm, self.cfg.norm_eps, out=h[r0:r1], addend=parts)
-            self._mlp_up(h[r0:r1], lw, act[r0:r1])
             K.linear(act[r0:r1], lw.wd, K.EPI_BF16, out=pd[r0:r1], bias=bd)
             self._stage_send(1, c, pd[r0:r1], r0, e)
         self._pending_add = (1, e, len(chunks), pd)

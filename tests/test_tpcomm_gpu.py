@@ -187,12 +187,12 @@ _BIG = {"SWB_TP_AR_NCCL_BYTES": "65536"}
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("model,env,args", [
     ("tiny", {}, []), ("tiny", _BIG, []),
-    ("tiny", {**_BIG, "SWB_TP_STAGE_CHUNKS": "2"}, ["--prompt", "600"]),
+    ("tiny", {**_BIG, "SWB_TP_STAGE_CHUNKS": "1"}, ["--prompt", "600"]),
     ("tiny", {**_BIG, "SWB_TP_STAGE": "0"}, []), ("bloom-tiny", _BIG, [])])
 def test_tp2_tiny_matches_tp1(model, env, args):
     """TP=2 pool == TP=1 tokens; with a 64 KB threshold the tiny prefill's
     reductions take the production prefill path — bf16 partials exchanged
-    by the copy engines (optionally in 2 row chunks) and added to the fp32
+    by the copy engines (projections in 2 row chunks, or 1) and added to the fp32
     residual inside the next norm, or with SWB_TP_STAGE=0 all-reduced by
     NCCL — while decode keeps the peer all-reduce, as at full size."""
     import subprocess

@@ -1819,19 +1819,23 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
       B <= (G <= 2 ? cl_maxb : std::min(cl_maxb, cl_maxb_gqa))) {
     // cluster x consumer-warp shape: SWB_ATTN_CL_CFG = "8x4" | "8x8" | "16x4" | "16x8";
     // ring depth: SWB_ATTN_CL_S = 8 (default) | 12
-    static const int cfg_id = [] {
+    static const int cfg_env = [] {
       const char* e = std::getenv("SWB_ATTN_CL_CFG");
-      if (!e) return 0;
+      if (!e) return -1;
       if (!strcmp(e, "8x8")) return 1;
       if (!strcmp(e, "16x4")) return 2;
       if (!strcmp(e, "16x8")) return 3;
+      if (!strcmp(e, "4x4")) return 4;
       return 0;
     }();
+    // default 8x4; 4x4 when 8-CTA clusters would not fit one wave at 3
+    // CTAs per SM (7B B=2: 512 CTAs > 444 slots)
+    const int cfg_id = cfg_env >= 0 ? cfg_env : (B * Hkv * 8 > 3 * kNumSMs ? 4 : 0);
     static const int s_env = [] {
       const char* e = std::getenv("SWB_ATTN_CL_S");
       return e ? std::atoi(e) : 0;
     }();
-    const int CL = cfg_id >= 2 ? 16 : 8, CW = ((cfg_id & 1) && G <= 2) ? 8 : 4;
+    const int CL = cfg_id == 4 ? 4 : cfg_id >= 2 ? 16 : 8, CW = (cfg_id == 1 || cfg_id == 3) && G <= 2 ? 8 : 4;
     const int pages_per_cta = ((max_ctx + 15) / 16 + CL - 1) / CL;
     // 12 stages prefetch a 1100-token context whole before the PDL wait (7B
     // B=1 standalone 6.7 -> 6.0 us) but at 2 CTAs/SM the step loses (2.51 ->
@@ -1843,11 +1847,13 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
                          const int32_t*, int, const int32_t*, float, const float*, int, int,
                          float, __nv_bfloat16*, int);
 #define SWB_CLK(g, s) {attn_decode_cl_kernel<g, 8, 4, s>, attn_decode_cl_kernel<g, 8, 8, s>, \
-                       attn_decode_cl_kernel<g, 16, 4, s>, attn_decode_cl_kernel<g, 16, 8, s>}
+                       attn_decode_cl_kernel<g, 16, 4, s>, attn_decode_cl_kernel<g, 16, 8, s>, \
+                       attn_decode_cl_kernel<g, 4, 4, s>}
 #define SWB_CLK4(g, s) {attn_decode_cl_kernel<g, 8, 4, s>, attn_decode_cl_kernel<g, 8, 4, s>, \
-                        attn_decode_cl_kernel<g, 16, 4, s>, attn_decode_cl_kernel<g, 16, 4, s>}
+                        attn_decode_cl_kernel<g, 16, 4, s>, attn_decode_cl_kernel<g, 16, 4, s>, \
+                        attn_decode_cl_kernel<g, 4, 4, s>}
     // GQA (head split across the 4 consumer warps): 4 warps in every shape
-    static const KFn table[4][2][4] = {{SWB_CLK(1, 8), SWB_CLK(1, 12)},
+    static const KFn table[4][2][5] = {{SWB_CLK(1, 8), SWB_CLK(1, 12)},
                                        {SWB_CLK(2, 8), SWB_CLK(2, 12)},
                                        {SWB_CLK4(4, 8), SWB_CLK4(4, 12)},
                                        {SWB_CLK4(8, 8), SWB_CLK4(8, 12)}};
@@ -1855,8 +1861,8 @@ static int launch_attn_decode(const void* qkv, int row_stride, void* k_layer, vo
 #undef SWB_CLK
     const KFn kern = table[gi][si][cfg_id];
     const size_t smem_c = dcl_smem(G, CW, S, CL);
-    static bool attr_c[64][32] = {};
-    const int ai = gi * 8 + si * 4 + cfg_id;
+    static bool attr_c[64][40] = {};
+    const int ai = gi * 10 + si * 5 + cfg_id;
     if (dev < 64 && !attr_c[dev][ai]) {
       SWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem_c));

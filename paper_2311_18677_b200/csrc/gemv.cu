@@ -761,6 +761,21 @@ static int dispatch_gemv(const void* x, const __nv_bfloat16* nw, float eps, cons
     return dispatch_gemv_tc(x, w, out, rs, bias, M, N, K, epilogue, s);
   if (!NORM && M >= 2 && M <= 8 && gemv_mma_enabled())
     return launch_gemv_mma<1, false>(x, nullptr, 0.f, w, out, rs, bias, M, N, K, epilogue, s);
+  // One-row GEMVs without pre-norm (7B O / down projections) on the mma.sync
+  // kernel: its 16-row items give the persistent grid one equal item per
+  // CTA (O: 256 items, down: 256) instead of 3.46 four-row items — 7B B=1
+  // step 2.472 -> 2.439 ms.  The pre-norm ones stay on the streaming kernel
+  // (2.64 ms on mma.sync).  SWB_GEMV_M1_MMA = 0 / 1 (default) / 2 (all).
+  static const int m1_mma = [] {
+    const char* e = std::getenv("SWB_GEMV_M1_MMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (M == 1 && gemv_mma_enabled() && K < 12288 && m1_mma >= (NORM ? 2 : 1)) {
+    if constexpr (NORM)
+      return launch_gemv_mma<1, true>(x, nw, eps, w, out, rs, bias, M, N, K, epilogue, s);
+    else
+      return launch_gemv_mma<1, false>(x, nullptr, 0.f, w, out, rs, bias, M, N, K, epilogue, s);
+  }
   if (M == 1) return launch_gemv<1, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
   if (M <= 2) return launch_gemv<2, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);
   if (M <= 4) return launch_gemv<4, NORM>(x, nw, eps, ws, out, rs, bias, M, N, K, epilogue, items, s);

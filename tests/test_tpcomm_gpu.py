@@ -86,8 +86,11 @@ def _fused_worker(rank, world, port, q):
     """Fused projection + all-reduce (swb_gemv_bf16_tp pushes the partial from
     its epilogue; swb_tp_allreduce_recv_f32 waits and sums) equals the
     two-kernel form bit for bit, eagerly and inside replayed CUDA graphs, with
-    the slots alternating between fused and unfused uses."""
+    the slots alternating between fused and unfused uses.  Both forms on the
+    same streaming GEMV (one-row GEMVs outside the fused push would
+    otherwise go to the mma.sync kernel, whose sums round differently)."""
     sys.path.insert(0, ROOT)
+    os.environ["SWB_GEMV_M1_MMA"] = "0"
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

@@ -141,12 +141,62 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
   // feeds 4 weight rows; lanes shuffle-reduce, warps combine through smem.
   // The producer above streams static weights before the previous kernel has
   // finished (PDL); consumers read x / write out only after it has.
+  // one-row pre-norm: the norm weights are static — fetch them before the
+  // dependency wait; x is read once (kept in registers from the sum of
+  // squares to the staging), each thread owning 8-element groups
+  constexpr int NIT = TV_HS_MAX / 2 / 8 / (TV_WARPS * 32);   // groups per thread (K <= 8192)
+  uint4 nwq[NIT];
+  if constexpr (NORM && MB == 1) {
+#pragma unroll
+    for (int i = 0; i < NIT; ++i) {
+      const int g = threadIdx.x + i * TV_WARPS * 32;
+      if (g < K / 8) nwq[i] = *reinterpret_cast<const uint4*>(nw + 8 * g);
+    }
+  }
   pdl_wait();
   // fused TP push: this use's epoch (the previous use of the slot finished
   // its receive kernel before the kernel ahead of us did)
   const unsigned ll_e =
       TPP ? *reinterpret_cast<const volatile unsigned*>(tpp.epoch) + 1u : 0u;
-  if constexpr (NORM) {
+  if constexpr (NORM && MB == 1) {
+    float4 xa[NIT], xb[NIT];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < NIT; ++i) {
+      const int g = threadIdx.x + i * TV_WARPS * 32;
+      if (g < K / 8) {
+        xa[i] = *reinterpret_cast<const float4*>(xf + 8 * g);
+        xb[i] = *reinterpret_cast<const float4*>(xf + 8 * g + 4);
+        ss += xa[i].x * xa[i].x + xa[i].y * xa[i].y + xa[i].z * xa[i].z + xa[i].w * xa[i].w +
+              xb[i].x * xb[i].x + xb[i].y * xb[i].y + xb[i].z * xb[i].z + xb[i].w * xb[i].w;
+      }
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) part[warp * 16] = ss;
+    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
+    if (threadIdx.x == 0) {
+      float q = 0.f;
+      for (int w = 0; w < TV_WARPS; ++w) q += part[w * 16];
+      rstd[0] = rsqrtf(q / (float)K + eps);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
+    const float r = rstd[0];
+#pragma unroll
+    for (int i = 0; i < NIT; ++i) {
+      const int g = threadIdx.x + i * TV_WARPS * 32;
+      if (g < K / 8) {
+        const float2 n0 = bf2_to_f2(nwq[i].x), n1 = bf2_to_f2(nwq[i].y),
+                     n2 = bf2_to_f2(nwq[i].z), n3 = bf2_to_f2(nwq[i].w);
+        const float4 a = xa[i], b = xb[i];
+        *reinterpret_cast<uint4*>(hs + 8 * g) =
+            make_uint4(f2_to_bf2(a.x * r * n0.x, a.y * r * n0.y),
+                       f2_to_bf2(a.z * r * n1.x, a.w * r * n1.y),
+                       f2_to_bf2(b.x * r * n2.x, b.y * r * n2.y),
+                       f2_to_bf2(b.z * r * n3.x, b.w * r * n3.y));
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
+  } else if constexpr (NORM) {
     // sum of squares of every batch row, by all consumer threads
     const int t = threadIdx.x;
     for (int m = 0; m < M; ++m) {

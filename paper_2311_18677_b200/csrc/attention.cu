@@ -287,6 +287,22 @@ constexpr int DA_MAXPART = 128;
 //   into the staged pages from shared memory, never re-read from global.
 // * Split-K merge fused: every CTA publishes (o, m, l); the last CTA of a
 //   (b, kh) group (atomic ticket) merges all partitions in fixed order.
+// rope4 split in two: the angles (position known early) and the rotation
+__device__ __forceinline__ void rope_sincos4(float* sn, float* cs, int i0, float pos, float l2t) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float inv_freq = exp2f(-l2t * (float)(2 * (i0 + j)) / (float)DA_D);
+    sincosf(pos * inv_freq, &sn[j], &cs[j]);
+  }
+}
+__device__ __forceinline__ void rope_apply4(float* a, float* b, const float* sn, const float* cs) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float x = a[j], y = b[j];
+    a[j] = x * cs[j] - y * sn[j];
+    b[j] = y * cs[j] + x * sn[j];
+  }
+}
 __device__ __forceinline__ void rope4(float* a, float* b, int i0, float pos, float l2t) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -737,11 +753,15 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
     }
   } else {
     // ------------------------------------------------ consumers
+    const int half = lane >> 4, hl = lane & 15;
+    const float fpos = (float)cur;
+    // RoPE angles of this lane's dims at position cur: ctx is known before
+    // the dependency wait, so the sincos work overlaps the QKV projection
+    float rsn[4], rcs[4];
+    if (!alibi) rope_sincos4(rsn, rcs, 4 * hl, fpos, log2_theta);
     pdl_wait();                                   // q / current k,v from the QKV projection
     ATTN_PROBE(1);
-    const int half = lane >> 4, hl = lane & 15;
     const __nv_bfloat16* qrow = qkv + (size_t)b * rs;
-    const float fpos = (float)cur;
     // lane hl holds dims [4hl, 4hl+4) and [64+4hl, 64+4hl+4): its RoPE pairs
     const int g0 = HS ? warp * GW : 0;         // first head of this warp
     float q[GW][8];
@@ -755,7 +775,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
       const float2 h0 = bf2_to_f2(qh.x), h1 = bf2_to_f2(qh.y);
       float lo[4] = {l0.x, l0.y, l1.x, l1.y}, hi[4] = {h0.x, h0.y, h1.x, h1.y};
       if (!alibi) {
-        rope4(lo, hi, 4 * hl, fpos, log2_theta);
+        rope_apply4(lo, hi, rsn, rcs);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {            // rotated q is stored in bf16 (two-kernel path)
           lo[j] = __bfloat162float(__float2bfloat16(lo[j]));
@@ -783,7 +803,7 @@ __global__ void __launch_bounds__((DCL_CW + 1) * 32)
         const float2 a0 = bf2_to_f2(a.x), a1 = bf2_to_f2(a.y);
         const float2 c0 = bf2_to_f2(c.x), c1 = bf2_to_f2(c.y);
         float lo[4] = {a0.x, a0.y, a1.x, a1.y}, hi[4] = {c0.x, c0.y, c1.x, c1.y};
-        rope4(lo, hi, 4 * hl, fpos, log2_theta);
+        rope_apply4(lo, hi, rsn, rcs);
         cur_lo = make_uint2(f2_to_bf2(lo[0], lo[1]), f2_to_bf2(lo[2], lo[3]));
         cur_hi = make_uint2(f2_to_bf2(hi[0], hi[1]), f2_to_bf2(hi[2], hi[3]));
       } else {

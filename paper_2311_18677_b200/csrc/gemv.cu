@@ -174,13 +174,11 @@ __global__ void __launch_bounds__(TV_THREADS, TV_CTAS_PER_SM)
     ss = warp_sum(ss);
     if (lane == 0) part[warp * 16] = ss;
     asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
-    if (threadIdx.x == 0) {
-      float q = 0.f;
-      for (int w = 0; w < TV_WARPS; ++w) q += part[w * 16];
-      rstd[0] = rsqrtf(q / (float)K + eps);
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(TV_WARPS * 32));
-    const float r = rstd[0];
+    // every thread sums the 8 warp partials in the same order: one barrier
+    float q = 0.f;
+#pragma unroll
+    for (int w = 0; w < TV_WARPS; ++w) q += part[w * 16];
+    const float r = rsqrtf(q / (float)K + eps);
 #pragma unroll
     for (int i = 0; i < NIT; ++i) {
       const int g = threadIdx.x + i * TV_WARPS * 32;

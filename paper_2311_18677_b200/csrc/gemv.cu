@@ -540,11 +540,69 @@ __global__ void __launch_bounds__(TM_THREADS, 2)
     }
     return;
   }
+  // pre-norm, M <= 2, K <= 4096: thread t owns x's float4 columns t + 256 j
+  // in the sum of squares AND the staging (the same set), so x is read once
+  // into registers, and the static norm weights before the dependency wait
+  constexpr int XC = 4;                      // float4 columns per thread and row
+  const bool regs = NORM && M <= 2 && K <= XC * 4 * TM_WARPS * 32 && K % (4 * TM_WARPS * 32) == 0;
+  uint2 nwr[XC];
+  if (NORM && regs) {
+#pragma unroll
+    for (int j = 0; j < XC; ++j) {
+      const int c = threadIdx.x + j * TM_WARPS * 32;
+      if (c < K / 4) nwr[j] = *reinterpret_cast<const uint2*>(nw + 4 * c);
+    }
+  }
   pdl_wait();   // x is produced by the previous kernel
   const int g = lane >> 2, t = lane & 3;
   __shared__ float s_part[16 * 16];   // NORM: [row][virtual warp] sums of squares
   __shared__ float s_rstd[16];
-  if constexpr (NORM) {
+  if (NORM && regs) {
+    // same sums as swb_rmsnorm: virtual thread vt = t + 256 half walks
+    // columns vt, vt + 512, ... — here columns t + 256 j, j even = half 0
+    float4 xv[2][XC];
+    const int nc = K / 4 / (TM_WARPS * 32);
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      if (m >= M) break;
+      const float4* xr = reinterpret_cast<const float4*>(xf + (size_t)m * K);
+#pragma unroll
+      for (int j = 0; j < XC; ++j)
+        if (j < nc) xv[m][j] = xr[threadIdx.x + j * TM_WARPS * 32];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float ss = 0.f;
+#pragma unroll
+        for (int j = half; j < XC; j += 2)
+          if (j < nc) {
+            const float4 v = xv[m][j];
+            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+          }
+        ss = warp_sum(ss);
+        if (lane == 0) s_part[m * 16 + warp + half * TM_WARPS] = ss;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TM_WARPS * 32) : "memory");
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      if (m >= M) break;
+      // every warp reduces the 16 partials (same order as before): no barrier
+      float v = lane < 16 ? s_part[m * 16 + lane] : 0.f;
+      v = warp_sum(v);
+      const float r = rsqrtf(v / (float)K + eps);
+#pragma unroll
+      for (int j = 0; j < XC; ++j) {
+        if (j >= nc) continue;
+        const int c = threadIdx.x + j * TM_WARPS * 32;
+        const float4 xx = xv[m][j];
+        const float2 w0 = bf2_to_f2(nwr[j].x), w1 = bf2_to_f2(nwr[j].y);
+        *reinterpret_cast<uint2*>(hs + (size_t)m * K + 4 * c) =
+            make_uint2(f2_to_bf2(xx.x * r * w0.x, xx.y * r * w0.y),
+                       f2_to_bf2(xx.z * r * w1.x, xx.w * r * w1.y));
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TM_WARPS * 32) : "memory");
+  } else if constexpr (NORM) {
     for (int m = 0; m < M; ++m) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {

@@ -1123,6 +1123,10 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       bulk_g2s(sv + (size_t)lane * BS * DA_D, vpool + gofs, tile, &vbar[lane / PPW]);
     }
   }
+  // RoPE angles of this thread's dims (i0 = (tid % 16) * 4 in the q tile and
+  // the current-token rows below) at position cur, before the dependency wait
+  float rsn[4], rcs[4];
+  if (STEP && cur >= 0 && !alibi) rope_sincos4(rsn, rcs, (threadIdx.x & 15) * 4, (float)cur, log2_theta);
   if constexpr (STEP) pdl_wait();
   ATTN_PROBE(1);
 
@@ -1142,7 +1146,10 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
           const float2 l0 = bf2_to_f2(ql.x), l1 = bf2_to_f2(ql.y);
           const float2 h0 = bf2_to_f2(qh.x), h1 = bf2_to_f2(qh.y);
           float lo[4] = {l0.x, l0.y, l1.x, l1.y}, hi[4] = {h0.x, h0.y, h1.x, h1.y};
-          rope4(lo, hi, i0, fpos, log2_theta);
+          if (STEP)
+            rope_apply4(lo, hi, rsn, rcs);        // i0 == (tid % 16) * 4
+          else
+            rope4(lo, hi, i0, fpos, log2_theta);
           lo2 = make_uint2(f2_to_bf2(lo[0], lo[1]), f2_to_bf2(lo[2], lo[3]));
           hi2 = make_uint2(f2_to_bf2(hi[0], hi[1]), f2_to_bf2(hi[2], hi[3]));
         } else {
@@ -1164,7 +1171,12 @@ __global__ void __launch_bounds__(DM_WARPS * 32)
       const float2 a0 = bf2_to_f2(kl.x), a1 = bf2_to_f2(kl.y);
       const float2 c0 = bf2_to_f2(khi.x), c1 = bf2_to_f2(khi.y);
       float lo[4] = {a0.x, a0.y, a1.x, a1.y}, hi[4] = {c0.x, c0.y, c1.x, c1.y};
-      if (!alibi) rope4(lo, hi, i0, fpos, log2_theta);
+      if (!alibi) {
+        if (STEP)
+          rope_apply4(lo, hi, rsn, rcs);          // tid < 16: i0 == tid * 4
+        else
+          rope4(lo, hi, i0, fpos, log2_theta);
+      }
       const int slot = STEP ? __ldg(trow + cur / BS) * BS + (cur & (BS - 1)) : slots[b];
       const size_t go = (((size_t)(slot / BS) * Hkv + kh) * BS + (slot & (BS - 1))) * DA_D;
       const uint2 klo = make_uint2(f2_to_bf2(lo[0], lo[1]), f2_to_bf2(lo[2], lo[3]));

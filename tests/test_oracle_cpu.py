@@ -33,7 +33,9 @@ def test_paged_equals_contiguous():
     store.reserve(0, len(prompt) + 10)
     toks_p, log_p = orc.paged_generate(prompt, 10, store, 0)
     assert toks_c == toks_p
-    assert torch.equal(log_c, log_p)
+    # same arithmetic on gathered pages; CPU BLAS may block a reduction
+    # differently from run to run (thread count under load), so not bitwise
+    torch.testing.assert_close(log_p, log_c, rtol=1e-6, atol=1e-6)
     assert store.tables[0][0] == 1   # block 0 taken by seq 7
 
 

@@ -376,6 +376,8 @@ def test_attn_decode_step_matches_explicit(K, H, Hkv, part, alibi):
 @pytest.mark.parametrize("H,Hkv,alibi,cached,gqa", [
     (32, 32, False, [0, 15, 16, 130, 1000, 2047], "-"), (8, 4, False, [3, 700], "-"),
     (16, 16, True, [31, 1500], "-"), (32, 32, False, [8190], "-"),
+    # B * heads * 8 > 444: the launcher picks 4-CTA clusters (7B B=2 shape)
+    (32, 32, False, [1100, 1100], "-"), (16, 16, True, [31, 1500, 700, 0], "-"),
     (64, 8, False, [3, 1100], "cuda"), (16, 4, True, [500], "cuda"),
     (64, 8, False, [3, 1100], "mma"), (64, 8, False, [1900], "mma"), (16, 4, True, [500], "mma"),
     (64, 8, False, [5, 900, 40, 1023], "split")])
